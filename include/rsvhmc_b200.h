@@ -1,0 +1,161 @@
+/*
+ * rsvhmc_b200.h -- C ABI of the B200-native HMC volatility update of the
+ * realized stochastic volatility (RSV) model (arXiv 1603.08114).
+ *
+ * This is the drop-in boundary for the reference's hot path.  Each entry
+ * point names the reference interface it replaces (paths relative to the
+ * reference tree, pkg/src/rsvhmc/...).  Plain pointers and sizes only; no
+ * torch types.  All functions return 0 on success and a negative
+ * RSV_E_* code on failure; rsv_last_error() returns the message.
+ *
+ * Pointers flagged `on_device` are CUDA device pointers (e.g. a torch
+ * tensor's data_ptr()); otherwise they are host pointers and the call
+ * copies synchronously.  One host thread per context.
+ */
+#ifndef RSVHMC_B200_H
+#define RSVHMC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSV_OK 0
+#define RSV_E_INVALID -1   /* contract violation -> Python ValueError   */
+#define RSV_E_CUDA -2      /* CUDA runtime failure -> RuntimeError      */
+#define RSV_E_STATE -3     /* call order / missing data -> RuntimeError */
+
+/* Bit generator kinds.  Raw 64-bit words, numpy next_double convention
+ * (word >> 11) * 2^-53 for every kind.
+ *   PHILOX: numpy Philox4x64-10; s[0..1] = key, pos = words drawn.
+ *   MINSTD: std::minstd_rand (a=48271, m=2^31-1); s[0] = x0;
+ *           word n = x_{3n+1}<<33 | x_{3n+2}<<2 | x_{3n+3}>>29.
+ *   PCG32 : pcg_basic pcg32; s[0] = LCG state after seeding, s[1] = inc;
+ *           word n = out_{2n}<<32 | out_{2n+1}.
+ *   SFC64 : numpy SFC64; s[0..3] = a, b, c, w at the current position. */
+#define RSV_PRNG_PHILOX 0
+#define RSV_PRNG_MINSTD 1
+#define RSV_PRNG_PCG32 2
+#define RSV_PRNG_SFC64 3
+
+typedef struct {
+  int32_t kind;
+  int32_t reserved;
+  uint64_t s[4];
+  uint64_t pos; /* raw words drawn since seeding (informational for SFC64) */
+} rsv_prng_state;
+
+/* model.py:78-94 Params */
+typedef struct {
+  double phi, mu, xi, sigma_eta_sq, sigma_u_sq;
+} rsv_params;
+
+/* Outcome of one HMC proposal (sampler.py:144-167). */
+typedef struct {
+  int32_t accept;        /* proposal accepted                                  */
+  int32_t diverged;      /* trajectory flagged (|h|>50 or NaN) or dH rejected  */
+  double delta_h;        /* H_new - H_old, or +inf (sampler.py:31 sentinel)    */
+  double h_old, h_new;   /* hamiltonian() before / after (model.py:178-182)    */
+  uint64_t words_used;   /* raw words consumed: momenta (+1 uniform if drawn)  */
+  double u;              /* the Metropolis uniform (NaN if none drawn)         */
+} rsv_result;
+
+typedef struct rsv_ctx rsv_ctx;
+
+const char *rsv_last_error(const rsv_ctx *ctx);
+const char *rsv_version(void);
+
+/* Context for one chain of length T on one CUDA device.  Owns device
+ * buffers, a stream and cached CUDA graphs.  Replaces the implicit state of
+ * sampler.py:291-358 run_chain (latent path, rng) for the device path. */
+int rsv_create(rsv_ctx **out, int device, int64_t T);
+int rsv_destroy(rsv_ctx *ctx);
+
+/* Dataset (model.py:34-75): returns y_t and log realized variances. */
+int rsv_set_data(rsv_ctx *ctx, const double *y, const double *log_rv, int on_device);
+/* Params (model.py:78-94); validated like Params.__post_init__. */
+int rsv_set_params(rsv_ctx *ctx, const rsv_params *p);
+/* Latent path h (sampler.py:291-314 run_chain's h). */
+int rsv_set_latent(rsv_ctx *ctx, const double *h, int on_device);
+int rsv_get_latent(rsv_ctx *ctx, double *h, int on_device);
+/* Bit-generator state (sampler.py:131-133 make_rng).  SFC64 states are
+ * advanced on the device; the others are counter/jump-ahead based. */
+int rsv_set_prng_state(rsv_ctx *ctx, const rsv_prng_state *st);
+int rsv_get_prng_state(rsv_ctx *ctx, rsv_prng_state *st);
+
+/* sampler.py:136-141 refresh_momenta: T standard normals, bit-exact with
+ * numpy's Generator.standard_normal on the same stream; advances it. */
+int rsv_refresh_momenta(rsv_ctx *ctx, double *p_out, int on_device);
+
+/* sampler.py:144-167 hmc_update_volatility on the context's latent path:
+ * momenta -> H_old -> L leapfrog steps -> H_new -> Metropolis, all on
+ * device.  fuse != 0 selects integrate_trajectory(fuse_half_steps=True). */
+int rsv_hmc_update(rsv_ctx *ctx, double step_size, int n_steps, int fuse, rsv_result *out);
+/* n back-to-back proposals with fixed params, captured in one CUDA graph;
+ * results (n entries) optional.  Used by run_chain's HMC-only mode. */
+int rsv_hmc_update_many(rsv_ctx *ctx, double step_size, int n_steps, int fuse, int n, rsv_result *out);
+
+/* integrator.py:149-179 integrate_trajectory from (h_in, p_in).
+ * h_out/p_out may alias the inputs.  *diverged as the reference's flag. */
+int rsv_integrate(rsv_ctx *ctx, const double *h_in, const double *p_in, double step_size, int n_steps, int fuse,
+                  double *h_out, double *p_out, int32_t *diverged, int on_device);
+/* integrator.py:139-146 elementary_step (K1 -> K2 -> K3 fused into one
+ * streamed kernel), in place on (h, p). */
+int rsv_elementary_step(rsv_ctx *ctx, double *h, double *p, double step_size, int32_t *diverged, int on_device);
+
+/* Paper protocol (bench.py:121-190 time_elementary_step): n_steps streamed
+ * elementary steps on the device-resident state left by the last
+ * rsv_elementary_step call; *ms = device time of the n_steps launches. */
+int rsv_bench_elementary(rsv_ctx *ctx, double step_size, int n_steps, float *ms);
+
+/* Kernel-level plug-in (integrator.py:50-65 backend.run protocol):
+ * _kernels.py:37-41 position_update, :44-54 momentum_update,
+ * :57-67 gradient_fill on the index range [lo, hi) of length-n arrays.
+ * scal[7] is model.py:185-199 scalar_pack order:
+ * (half, phi, mu, xi, 1/sigma_u_sq, 1/sigma_eta_sq, 1 - phi^2). */
+int rsv_position_update(rsv_ctx *ctx, double *h, const double *p, double c, int64_t n, int64_t lo, int64_t hi,
+                        int on_device);
+int rsv_momentum_update(rsv_ctx *ctx, const double *h, double *p, const double *y, const double *lrv, double dt,
+                        const double *scal, int64_t n, int64_t lo, int64_t hi, int32_t *flag, int on_device);
+int rsv_gradient(rsv_ctx *ctx, const double *h, const double *y, const double *lrv, const double *scal,
+                 double *out, int64_t n, int64_t lo, int64_t hi, int32_t *flag, int on_device);
+
+/* model.py:178-182 hamiltonian / :134-163 log_posterior of (h, p) against
+ * the context's data and params. */
+int rsv_hamiltonian(rsv_ctx *ctx, const double *h, const double *p, double *out, int on_device);
+int rsv_log_posterior(rsv_ctx *ctx, const double *h, double *out, int on_device);
+
+/* Sufficient statistics of the context's latent path for the theta full
+ * conditionals (sampler.py:170-272), shifted by (c_mu, c_xi):
+ *   out = {d_0, d_{T-1}, sum d, sum d^2, sum_{t>=1} d_t d_{t-1}, sum e, sum e^2}
+ * with d = h - c_mu, e = log_rv - h - c_xi. */
+int rsv_suff_stats(rsv_ctx *ctx, double c_mu, double c_xi, double out[7]);
+
+/* Last proposal's statistics (computed inside the fused trajectory kernel
+ * for whichever path was kept), shifted by the params' (mu, xi). */
+int rsv_last_stats(rsv_ctx *ctx, double out[7]);
+
+/* Device timing helpers for the benchmark: average duration (ms) of the
+ * trajectory kernel and of the whole proposal over the last
+ * rsv_hmc_update_many call with timing enabled. */
+int rsv_set_timing(rsv_ctx *ctx, int enable);
+int rsv_get_timing(rsv_ctx *ctx, double *traj_ms, double *momenta_ms, double *total_ms);
+/* Kernel launches issued by the context so far (gpu_launches evidence). */
+int64_t rsv_launch_count(const rsv_ctx *ctx);
+
+/* ---- host side of the bit generators (no device needed) ----
+ * Seeding from raw seed material (numpy.SeedSequence words), sequential
+ * draws, and a numpy bitgen_t so numpy.random.Generator continues the same
+ * stream for the scalar theta draws (sampler.py:170-272).  Replaces
+ * sampler.py:131-133 make_rng for the non-Philox kinds. */
+int rsv_stream_seed(rsv_prng_state *st, int kind, const uint64_t *material);
+uint64_t rsv_stream_next_u64(rsv_prng_state *st);
+double rsv_stream_next_double(rsv_prng_state *st);
+int rsv_stream_bitgen(rsv_prng_state *st, void *numpy_bitgen_out);
+void rsv_philox_block(uint64_t block, uint64_t key0, uint64_t key1, uint64_t out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSVHMC_B200_H */

@@ -1,0 +1,792 @@
+// rsv_ctx.cu -- the C ABI (include/rsvhmc_b200.h): device buffers, streams,
+// CUDA-graph launch orchestration of one HMC proposal.
+//
+// One proposal (sampler.py:144-167 hmc_update_volatility) is the launch
+// sequence  [SFC64 words] -> Z1 -> Z2 -> Z3 (momenta) -> trajectory -> accept,
+// entirely device-resident: the stream position, the index of the current
+// path buffer and the proposal outcome live in DevControl, so the sequence is
+// captured once per (prng kind, dt, L, fuse) into a CUDA graph and replayed
+// with no host round trip between proposals.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/rsvhmc_b200.h"
+#include "rsv_internal.h"
+#include "rsv_launch.h"
+
+using namespace rsv;
+
+namespace {
+
+struct GraphKey {
+  int kind, n_steps, fuse, timing;
+  double dt;
+  bool operator<(const GraphKey &o) const {
+    return std::tie(kind, n_steps, fuse, timing, dt) < std::tie(o.kind, o.n_steps, o.fuse, o.timing, o.dt);
+  }
+};
+
+__global__ void prep_data_kernel(const double *y, double *a, int64_t T) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < T) a[i] = __dmul_rn(__dmul_rn(0.5, y[i]), y[i]);  // (half * y) * y, _kernels.py:27
+}
+
+__global__ void ring_store_kernel(DevControl *ctrl, DevResult *ring, int cap, int32_t *count) {
+  if (threadIdx.x || blockIdx.x) return;
+  const int i = *count;
+  if (i < cap) ring[i] = ctrl->res;
+  *count = i + 1;
+}
+
+}  // namespace
+
+struct rsv_ctx {
+  int device = 0;
+  int64_t T = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  bool has_data = false, has_params = false, has_latent = false;
+  int kind = PRNG_PHILOX;
+
+  double *hbuf[2] = {nullptr, nullptr};
+  double *y = nullptr, *a = nullptr, *lrv = nullptr, *normals = nullptr;
+  double *sh = nullptr, *sp = nullptr, *sh2 = nullptr, *sp2 = nullptr;  // scratch T each
+  void *zscratch = nullptr;
+  uint64_t *sfc_words = nullptr, *sfc_snaps = nullptr;
+  TilePart *parts = nullptr;
+  int max_tiles = 0;
+  double *rpart = nullptr;  // reduction partials
+  double *rout = nullptr;   // reduction outputs (8 doubles)
+  int32_t *dflag = nullptr;
+  int32_t *ring_count = nullptr;
+  DevResult *ring = nullptr;
+  int ring_cap = 0;
+  DevControl *ctrl = nullptr;
+  DevParams *prm = nullptr;
+  // pinned host mirrors
+  DevControl *h_ctrl = nullptr;
+  DevParams *h_prm = nullptr;
+  double *h_out = nullptr;  // 8 doubles
+  int32_t *h_flag = nullptr;
+  DevResult *h_ring = nullptr;
+  int h_ring_cap = 0;
+  // plug-in scratch (arbitrary n)
+  double *pl[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t pl_n = 0;
+
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  bool timing = false;
+  std::vector<cudaEvent_t> evpool;
+  std::vector<double> last_traj_ms, last_mom_ms, last_total_ms;
+};
+
+static std::string g_err;
+
+static int fail(rsv_ctx *c, int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  else g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return fail(c, RSV_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define LK(call)                                                                                   \
+  do {                                                                                             \
+    if ((call) != 0)                                                                               \
+      return fail(c, RSV_E_CUDA, "launch %s: %s", #call, cudaGetErrorString(cudaGetLastError())); \
+  } while (0)
+
+extern "C" {
+
+const char *rsv_last_error(const rsv_ctx *c) { return c ? c->err.c_str() : g_err.c_str(); }
+const char *rsv_version(void) { return "paper_1603_08114_b200 0.1.0 (sm_100a)"; }
+int64_t rsv_launch_count(const rsv_ctx *c) { return c ? c->launches : 0; }
+
+int rsv_destroy(rsv_ctx *c) {
+  if (!c) return 0;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto e : c->evpool) cudaEventDestroy(e);
+  void *dev[] = {c->hbuf[0], c->hbuf[1], c->y, c->a, c->lrv, c->normals, c->sh, c->sp, c->sh2, c->sp2,
+                 c->zscratch, c->sfc_words, c->sfc_snaps, c->parts, c->rpart, c->rout, c->dflag, c->ring_count,
+                 c->ring, c->ctrl, c->prm, c->pl[0], c->pl[1], c->pl[2], c->pl[3]};
+  for (void *p : dev)
+    if (p) cudaFree(p);
+  void *host[] = {c->h_ctrl, c->h_prm, c->h_out, c->h_flag, c->h_ring};
+  for (void *p : host)
+    if (p) cudaFreeHost(p);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return 0;
+}
+
+static int create_impl(rsv_ctx *c, int device, int64_t T) {
+  c->device = device;
+  c->T = T;
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(c, RSV_E_CUDA, "built for sm_100a (B200); device is sm_%d%d", prop.major, prop.minor);
+  c->sm_count = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  const size_t tb = sizeof(double) * (size_t)T;
+  for (int i = 0; i < 2; i++) CK(cudaMalloc(&c->hbuf[i], tb));
+  double **bufs[] = {&c->y, &c->a, &c->lrv, &c->normals, &c->sh, &c->sp, &c->sh2, &c->sp2};
+  for (double **b : bufs) CK(cudaMalloc(b, tb));
+  CK(cudaMalloc(&c->zscratch, momenta_scratch_bytes(T)));
+  const int64_t nw = momenta_words(T) + 64;
+  CK(cudaMalloc(&c->sfc_words, sizeof(uint64_t) * nw));
+  CK(cudaMalloc(&c->sfc_snaps, sizeof(uint64_t) * 4 * (nw / SFC_SNAP + 2)));
+  c->max_tiles = (int)(T / (TR_W / 4) + 4 * c->sm_count + 8);
+  CK(cudaMalloc(&c->parts, sizeof(TilePart) * c->max_tiles));
+  CK(cudaMalloc(&c->rpart, sizeof(double) * 8 * (reduce_partials_count(T) + 1)));
+  CK(cudaMalloc(&c->rout, sizeof(double) * 8));
+  CK(cudaMalloc(&c->dflag, sizeof(int32_t)));
+  CK(cudaMalloc(&c->ring_count, sizeof(int32_t)));
+  CK(cudaMalloc(&c->ctrl, sizeof(DevControl)));
+  CK(cudaMalloc(&c->prm, sizeof(DevParams)));
+  CK(cudaMallocHost(&c->h_ctrl, sizeof(DevControl)));
+  CK(cudaMallocHost(&c->h_prm, sizeof(DevParams)));
+  CK(cudaMallocHost(&c->h_out, sizeof(double) * 8));
+  CK(cudaMallocHost(&c->h_flag, sizeof(int32_t)));
+  memset(c->h_ctrl, 0, sizeof(DevControl));
+  c->h_ctrl->stream.kind = PRNG_PHILOX;
+  CK(cudaMemcpy(c->ctrl, c->h_ctrl, sizeof(DevControl), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int rsv_create(rsv_ctx **out, int device, int64_t T) {
+  if (!out) return fail(nullptr, RSV_E_INVALID, "out is null");
+  *out = nullptr;
+  if (T < 2) return fail(nullptr, RSV_E_INVALID, "need at least 2 sites, got %lld", (long long)T);
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, RSV_E_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(nullptr, RSV_E_INVALID, "device %d out of range", device);
+  rsv_ctx *c = new rsv_ctx();
+  const int r = create_impl(c, device, T);
+  if (r) {
+    g_err = c->err;
+    rsv_destroy(c);
+    return r;
+  }
+  *out = c;
+  return 0;
+}
+
+static int copy_in(rsv_ctx *c, double *dst, const double *src, int64_t n, int on_device) {
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     c->stream));
+  return 0;
+}
+static int copy_out(rsv_ctx *c, double *dst, const double *src, int64_t n, int on_device) {
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     c->stream));
+  return 0;
+}
+static int sync(rsv_ctx *c) {
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+static int pull_ctrl(rsv_ctx *c) {
+  CK(cudaMemcpyAsync(c->h_ctrl, c->ctrl, sizeof(DevControl), cudaMemcpyDeviceToHost, c->stream));
+  return sync(c);
+}
+
+int rsv_set_data(rsv_ctx *c, const double *y, const double *log_rv, int on_device) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  if (!y || !log_rv) return fail(c, RSV_E_INVALID, "null data pointer");
+  CK(cudaSetDevice(c->device));
+  int r;
+  if ((r = copy_in(c, c->y, y, c->T, on_device))) return r;
+  if ((r = copy_in(c, c->lrv, log_rv, c->T, on_device))) return r;
+  prep_data_kernel<<<(unsigned)((c->T + 255) / 256), 256, 0, c->stream>>>(c->y, c->a, c->T);
+  c->launches++;
+  CK(cudaGetLastError());
+  c->has_data = true;
+  return sync(c);
+}
+
+static int check_params(rsv_ctx *c, const rsv_params *p) {
+  if (!p) return fail(c, RSV_E_INVALID, "null params");
+  if (!(fabs(p->phi) < 1.0)) return fail(c, RSV_E_INVALID, "|phi| must be < 1 for stationarity, got %g", p->phi);
+  if (!(p->sigma_eta_sq > 0.0)) return fail(c, RSV_E_INVALID, "sigma_eta_sq must be positive, got %g", p->sigma_eta_sq);
+  if (!(p->sigma_u_sq > 0.0)) return fail(c, RSV_E_INVALID, "sigma_u_sq must be positive, got %g", p->sigma_u_sq);
+  return 0;
+}
+
+int rsv_set_params(rsv_ctx *c, const rsv_params *p) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  int r = check_params(c, p);
+  if (r) return r;
+  CK(cudaSetDevice(c->device));
+  // the previous graph replays may still read *prm: order the update on the stream
+  CK(cudaStreamSynchronize(c->stream));
+  c->h_prm->phi = p->phi;
+  c->h_prm->mu = p->mu;
+  c->h_prm->xi = p->xi;
+  c->h_prm->se2 = p->sigma_eta_sq;
+  c->h_prm->su2 = p->sigma_u_sq;
+  CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(DevParams), cudaMemcpyHostToDevice, c->stream));
+  c->has_params = true;
+  return sync(c);
+}
+
+int rsv_set_latent(rsv_ctx *c, const double *h, int on_device) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  if (!h) return fail(c, RSV_E_INVALID, "null latent pointer");
+  CK(cudaSetDevice(c->device));
+  int r;
+  if ((r = copy_in(c, c->hbuf[0], h, c->T, on_device))) return r;
+  CK(cudaMemsetAsync(&c->ctrl->cur, 0, sizeof(int32_t), c->stream));
+  c->has_latent = true;
+  return sync(c);
+}
+
+int rsv_get_latent(rsv_ctx *c, double *h, int on_device) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  if (!c->has_latent) return fail(c, RSV_E_STATE, "latent path not set");
+  CK(cudaSetDevice(c->device));
+  int r;
+  if ((r = pull_ctrl(c))) return r;
+  if ((r = copy_out(c, h, c->hbuf[c->h_ctrl->cur & 1], c->T, on_device))) return r;
+  return sync(c);
+}
+
+int rsv_set_prng_state(rsv_ctx *c, const rsv_prng_state *st) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  if (!st || st->kind < 0 || st->kind > 3) return fail(c, RSV_E_INVALID, "invalid bit generator state");
+  if (st->kind == PRNG_MINSTD && (st->s[0] == 0 || st->s[0] >= MINSTD_M))
+    return fail(c, RSV_E_INVALID, "minstd state must be in [1, 2^31-2]");
+  CK(cudaSetDevice(c->device));
+  StreamState s;
+  s.kind = st->kind;
+  s.reserved = 0;
+  for (int i = 0; i < 4; i++) s.s[i] = st->s[i];
+  s.pos = st->pos;
+  CK(cudaStreamSynchronize(c->stream));
+  c->h_ctrl->stream = s;
+  CK(cudaMemcpyAsync(&c->ctrl->stream, &c->h_ctrl->stream, sizeof(StreamState), cudaMemcpyHostToDevice, c->stream));
+  c->kind = st->kind;
+  return sync(c);
+}
+
+int rsv_get_prng_state(rsv_ctx *c, rsv_prng_state *st) {
+  if (!c || !st) return fail(c, RSV_E_INVALID, "null argument");
+  CK(cudaSetDevice(c->device));
+  int r;
+  if ((r = pull_ctrl(c))) return r;
+  st->kind = c->h_ctrl->stream.kind;
+  st->reserved = 0;
+  for (int i = 0; i < 4; i++) st->s[i] = c->h_ctrl->stream.s[i];
+  st->pos = c->h_ctrl->stream.pos;
+  return 0;
+}
+
+static MomentaBufs mbufs(rsv_ctx *c) {
+  MomentaBufs b;
+  b.ctrl = c->ctrl;
+  b.scratch = c->zscratch;
+  b.sfc_words = c->sfc_words;
+  b.sfc_snaps = c->sfc_snaps;
+  b.normals = c->normals;
+  return b;
+}
+
+static int check_err_bits(rsv_ctx *c) {
+  if (c->h_ctrl->err & 1) return fail(c, RSV_E_CUDA, "momenta word budget exhausted (ziggurat shortfall)");
+  return 0;
+}
+
+int rsv_refresh_momenta(rsv_ctx *c, double *p_out, int on_device) {
+  if (!c || !p_out) return fail(c, RSV_E_INVALID, "null argument");
+  CK(cudaSetDevice(c->device));
+  int l = 0;
+  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
+  if (launch_momenta(mbufs(c), c->kind, c->T, c->stream, &l)) return fail(c, RSV_E_CUDA, "momenta launch failed");
+  if (launch_momenta_advance(mbufs(c), c->stream, &l)) return fail(c, RSV_E_CUDA, "advance launch failed");
+  c->launches += l;
+  int r;
+  if ((r = copy_out(c, p_out, c->normals, c->T, on_device))) return r;
+  if ((r = pull_ctrl(c))) return r;
+  return check_err_bits(c);
+}
+
+static TrajArgs traj_args(rsv_ctx *c, double dt, int n_steps, int fuse, const TrajGeom &g) {
+  TrajArgs a;
+  memset(&a, 0, sizeof(a));
+  a.T = c->T;
+  a.n_steps = n_steps;
+  a.fuse = fuse;
+  a.dt = dt;
+  a.g = g;
+  a.hbuf0 = c->hbuf[0];
+  a.hbuf1 = c->hbuf[1];
+  a.p_in = c->normals;
+  a.a = c->a;
+  a.lrv = c->lrv;
+  a.prm = c->prm;
+  a.ctrl = c->ctrl;
+  a.parts = c->parts;
+  return a;
+}
+
+static int check_md(rsv_ctx *c, double dt, int n_steps) {
+  if (!(dt > 0.0)) return fail(c, RSV_E_INVALID, "step_size must be positive, got %g", dt);
+  if (n_steps < 1) return fail(c, RSV_E_INVALID, "n_steps must be >= 1, got %d", n_steps);
+  return 0;
+}
+
+static int ensure_events(rsv_ctx *c, size_t n) {
+  while (c->evpool.size() < n) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->evpool.push_back(e);
+  }
+  return 0;
+}
+
+// Capture one proposal into a graph.  With timing, 4 event-record nodes
+// (start, trajectory begin, trajectory end, end) are added; their events are
+// re-pointed per launch with cudaGraphExecEventRecordNodeSetEvent.
+static std::map<cudaGraphExec_t, std::vector<cudaGraphNode_t>> g_evnodes;
+
+static int build_graph(rsv_ctx *c, const GraphKey &k, cudaGraphExec_t *out) {
+  const TrajGeom g = traj_geometry(c->T, k.n_steps, c->sm_count);
+  if (!g.ok) return fail(c, RSV_E_INVALID, "n_steps=%d too large for one trajectory tile (max %d)", k.n_steps,
+                         TR_W * 3 / 8 - 1);
+  if (g.n_tiles > c->max_tiles) return fail(c, RSV_E_CUDA, "tile count %d exceeds buffer", g.n_tiles);
+  int r;
+  if ((r = ensure_events(c, 4))) return r;
+  cudaGraph_t graph;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  int l = 0;
+  bool ok = true;
+  if (k.timing) cudaEventRecord(c->evpool[0], c->stream);
+  ok &= launch_momenta(mbufs(c), k.kind, c->T, c->stream, &l) == 0;
+  if (k.timing) cudaEventRecord(c->evpool[1], c->stream);
+  ok &= launch_trajectory(traj_args(c, k.dt, k.n_steps, k.fuse, g), c->stream, &l) == 0;
+  if (k.timing) cudaEventRecord(c->evpool[2], c->stream);
+  AcceptArgs aa;
+  memset(&aa, 0, sizeof(aa));
+  aa.T = c->T;
+  aa.n_tiles = g.n_tiles;
+  aa.parts = c->parts;
+  aa.prm = c->prm;
+  aa.ctrl = c->ctrl;
+  aa.sfc_words = c->sfc_words;
+  aa.sfc_snaps = c->sfc_snaps;
+  ok &= launch_accept(aa, c->stream, &l) == 0;
+  if (k.timing) cudaEventRecord(c->evpool[3], c->stream);
+  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+  if (!ok || e != cudaSuccess) return fail(c, RSV_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  cudaGraphExec_t exec;
+  CK(cudaGraphInstantiate(&exec, graph, 0));
+  if (k.timing) {
+    // locate the event-record nodes in capture order
+    size_t n = 0;
+    CK(cudaGraphGetNodes(graph, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CK(cudaGraphGetNodes(graph, nodes.data(), &n));
+    std::vector<cudaGraphNode_t> evn(4, nullptr);
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      cudaGraphNodeGetType(nd, &t);
+      if (t != cudaGraphNodeTypeEventRecord) continue;
+      cudaEvent_t ev;
+      cudaGraphEventRecordNodeGetEvent(nd, &ev);
+      for (int i = 0; i < 4; i++)
+        if (ev == c->evpool[i]) evn[i] = nd;
+    }
+    g_evnodes[exec] = evn;
+  }
+  cudaGraphDestroy(graph);
+  *out = exec;
+  return 0;
+}
+
+static int get_graph(rsv_ctx *c, double dt, int n_steps, int fuse, cudaGraphExec_t *out, int *kernels) {
+  GraphKey k{c->kind, n_steps, fuse ? 1 : 0, c->timing ? 1 : 0, dt};
+  auto it = c->graphs.find(k);
+  if (it == c->graphs.end()) {
+    cudaGraphExec_t e;
+    int r = build_graph(c, k, &e);
+    if (r) return r;
+    it = c->graphs.emplace(k, e).first;
+  }
+  *out = it->second;
+  *kernels = (c->kind == PRNG_SFC64 ? 4 : 3) + 2;
+  return 0;
+}
+
+static int ready(rsv_ctx *c) {
+  if (!c->has_data) return fail(c, RSV_E_STATE, "data not set (rsv_set_data)");
+  if (!c->has_params) return fail(c, RSV_E_STATE, "params not set (rsv_set_params)");
+  if (!c->has_latent) return fail(c, RSV_E_STATE, "latent path not set (rsv_set_latent)");
+  return 0;
+}
+
+static void to_result(const DevResult &d, rsv_result *o) {
+  o->accept = d.accept;
+  o->diverged = d.diverged;
+  o->delta_h = d.delta_h;
+  o->h_old = d.h_old;
+  o->h_new = d.h_new;
+  o->words_used = d.words_used;
+  o->u = d.u;
+}
+
+int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv_result *out) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  int r;
+  if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
+  if (n < 1) return fail(c, RSV_E_INVALID, "n must be >= 1");
+  CK(cudaSetDevice(c->device));
+  cudaGraphExec_t exec;
+  int kpl = 0;
+  if ((r = get_graph(c, dt, n_steps, fuse, &exec, &kpl))) return r;
+  if (out && n > c->ring_cap) {
+    if (c->ring) cudaFree(c->ring);
+    if (c->h_ring) cudaFreeHost(c->h_ring);
+    c->ring_cap = n;
+    CK(cudaMalloc(&c->ring, sizeof(DevResult) * n));
+    CK(cudaMallocHost(&c->h_ring, sizeof(DevResult) * n));
+  }
+  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
+  CK(cudaMemsetAsync(c->ring_count, 0, sizeof(int32_t), c->stream));
+  std::vector<cudaGraphNode_t> *evn = nullptr;
+  if (c->timing) {
+    evn = &g_evnodes[exec];
+    if ((r = ensure_events(c, 4 * (size_t)n + 4))) return r;
+  }
+  for (int i = 0; i < n; i++) {
+    if (evn) {
+      for (int j = 0; j < 4; j++) CK(cudaGraphExecEventRecordNodeSetEvent(exec, (*evn)[j], c->evpool[4 + 4 * i + j]));
+    }
+    CK(cudaGraphLaunch(exec, c->stream));
+    c->launches += kpl;
+    if (out) {
+      ring_store_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, c->ring, c->ring_cap, c->ring_count);
+      c->launches++;
+    }
+  }
+  if (out) CK(cudaMemcpyAsync(c->h_ring, c->ring, sizeof(DevResult) * n, cudaMemcpyDeviceToHost, c->stream));
+  if ((r = pull_ctrl(c))) return r;
+  if ((r = check_err_bits(c))) return r;
+  if (out)
+    for (int i = 0; i < n; i++) to_result(c->h_ring[i], out + i);
+  if (evn) {
+    c->last_traj_ms.assign(n, 0.0);
+    c->last_mom_ms.assign(n, 0.0);
+    c->last_total_ms.assign(n, 0.0);
+    for (int i = 0; i < n; i++) {
+      float t0 = 0, t1 = 0, t2 = 0;
+      cudaEvent_t *e = &c->evpool[4 + 4 * i];
+      CK(cudaEventElapsedTime(&t0, e[0], e[1]));
+      CK(cudaEventElapsedTime(&t1, e[1], e[2]));
+      CK(cudaEventElapsedTime(&t2, e[0], e[3]));
+      c->last_mom_ms[i] = t0;
+      c->last_traj_ms[i] = t1;
+      c->last_total_ms[i] = t2;
+    }
+  }
+  return 0;
+}
+
+int rsv_hmc_update(rsv_ctx *c, double dt, int n_steps, int fuse, rsv_result *out) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  int r;
+  if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
+  CK(cudaSetDevice(c->device));
+  cudaGraphExec_t exec;
+  int kpl = 0;
+  if ((r = get_graph(c, dt, n_steps, fuse, &exec, &kpl))) return r;
+  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
+  CK(cudaGraphLaunch(exec, c->stream));
+  c->launches += kpl;
+  if ((r = pull_ctrl(c))) return r;
+  if ((r = check_err_bits(c))) return r;
+  if (out) to_result(c->h_ctrl->res, out);
+  return 0;
+}
+
+int rsv_last_stats(rsv_ctx *c, double out[7]) {
+  if (!c || !out) return fail(c, RSV_E_INVALID, "null argument");
+  for (int i = 0; i < 7; i++) out[i] = c->h_ctrl->stats[i];
+  return 0;
+}
+
+// integrate_trajectory from explicit (h, p)
+int rsv_integrate(rsv_ctx *c, const double *h_in, const double *p_in, double dt, int n_steps, int fuse,
+                  double *h_out, double *p_out, int32_t *diverged, int on_device) {
+  if (!c || !h_in || !p_in) return fail(c, RSV_E_INVALID, "null argument");
+  int r;
+  if ((r = check_md(c, dt, n_steps))) return r;
+  if (!c->has_data) return fail(c, RSV_E_STATE, "data not set (rsv_set_data)");
+  if (!c->has_params) return fail(c, RSV_E_STATE, "params not set (rsv_set_params)");
+  CK(cudaSetDevice(c->device));
+  if ((r = copy_in(c, c->sh, h_in, c->T, on_device)) || (r = copy_in(c, c->sp, p_in, c->T, on_device))) return r;
+  const TrajGeom g = traj_geometry(c->T, n_steps, c->sm_count);
+  int l = 0;
+  int32_t div = 0;
+  if (g.ok) {
+    TrajArgs a = traj_args(c, dt, n_steps, fuse, g);
+    a.h_src = c->sh;
+    a.h_dst = c->sh2;
+    a.p_in = c->sp;
+    a.p_out = c->sp2;
+    LK(launch_trajectory(a, c->stream, &l));
+    AcceptArgs aa;
+    memset(&aa, 0, sizeof(aa));
+    aa.T = c->T;
+    aa.n_tiles = g.n_tiles;
+    aa.parts = c->parts;
+    aa.prm = c->prm;
+    aa.ctrl = c->ctrl;
+    aa.integrate_only = 1;
+    LK(launch_accept(aa, c->stream, &l));
+    c->launches += l;
+    if ((r = pull_ctrl(c))) return r;
+    div = c->h_ctrl->res.diverged;
+    if ((r = copy_out(c, h_out, c->sh2, c->T, on_device)) || (r = copy_out(c, p_out, c->sp2, c->T, on_device)))
+      return r;
+  } else {
+    // very long trajectories: one streamed elementary step per launch (unfused grouping)
+    CK(cudaMemsetAsync(c->dflag, 0, sizeof(int32_t), c->stream));
+    double *h0 = c->sh, *p0 = c->sp, *h1 = c->sh2, *p1 = c->sp2;
+    for (int k = 0; k < n_steps; k++) {
+      LK(launch_elementary_step(h0, p0, h1, p1, c->a, c->lrv, c->prm, dt, c->T, c->dflag, c->stream, &l));
+      std::swap(h0, h1);
+      std::swap(p0, p1);
+    }
+    c->launches += l;
+    CK(cudaMemcpyAsync(c->h_flag, c->dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    if ((r = copy_out(c, h_out, h0, c->T, on_device)) || (r = copy_out(c, p_out, p0, c->T, on_device))) return r;
+    if ((r = sync(c))) return r;
+    div = *c->h_flag;
+  }
+  if ((r = sync(c))) return r;
+  if (diverged) *diverged = div;
+  return 0;
+}
+
+int rsv_elementary_step(rsv_ctx *c, double *h, double *p, double dt, int32_t *diverged, int on_device) {
+  if (!c || !h || !p) return fail(c, RSV_E_INVALID, "null argument");
+  int r;
+  if ((r = check_md(c, dt, 1))) return r;
+  if (!c->has_data || !c->has_params) return fail(c, RSV_E_STATE, "data/params not set");
+  CK(cudaSetDevice(c->device));
+  if ((r = copy_in(c, c->sh, h, c->T, on_device)) || (r = copy_in(c, c->sp, p, c->T, on_device))) return r;
+  CK(cudaMemsetAsync(c->dflag, 0, sizeof(int32_t), c->stream));
+  int l = 0;
+  LK(launch_elementary_step(c->sh, c->sp, c->sh2, c->sp2, c->a, c->lrv, c->prm, dt, c->T, c->dflag, c->stream, &l));
+  c->launches += l;
+  CK(cudaMemcpyAsync(c->h_flag, c->dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  if ((r = copy_out(c, h, c->sh2, c->T, on_device)) || (r = copy_out(c, p, c->sp2, c->T, on_device))) return r;
+  if ((r = sync(c))) return r;
+  if (diverged) *diverged = *c->h_flag;
+  return 0;
+}
+
+// Repeated elementary steps on device-resident (h, p) for the paper protocol
+// (bench.py:121-190 time_elementary_step): ping-pongs sh/sp <-> sh2/sp2.
+int rsv_bench_elementary(rsv_ctx *c, double dt, int n_steps, float *ms) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  CK(cudaSetDevice(c->device));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaMemsetAsync(c->dflag, 0, sizeof(int32_t), c->stream));
+  double *h0 = c->sh, *p0 = c->sp, *h1 = c->sh2, *p1 = c->sp2;
+  int l = 0;
+  CK(cudaEventRecord(e0, c->stream));
+  for (int k = 0; k < n_steps; k++) {
+    LK(launch_elementary_step(h0, p0, h1, p1, c->a, c->lrv, c->prm, dt, c->T, c->dflag, c->stream, &l));
+    std::swap(h0, h1);
+    std::swap(p0, p1);
+  }
+  CK(cudaEventRecord(e1, c->stream));
+  c->launches += l;
+  CK(cudaEventSynchronize(e1));
+  CK(cudaEventElapsedTime(ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return 0;
+}
+
+static int ensure_plugin(rsv_ctx *c, int64_t n) {
+  if (n <= c->pl_n) return 0;
+  for (int i = 0; i < 4; i++) {
+    if (c->pl[i]) cudaFree(c->pl[i]);
+    CK(cudaMalloc(&c->pl[i], sizeof(double) * n));
+  }
+  c->pl_n = n;
+  return 0;
+}
+
+static int check_range(rsv_ctx *c, int64_t n, int64_t lo, int64_t hi) {
+  if (n < 0 || lo < 0 || hi > n || lo > hi) return fail(c, RSV_E_INVALID, "bad range [%lld, %lld) of %lld",
+                                                       (long long)lo, (long long)hi, (long long)n);
+  return 0;
+}
+
+int rsv_position_update(rsv_ctx *c, double *h, const double *p, double cc, int64_t n, int64_t lo, int64_t hi,
+                        int on_device) {
+  if (!c || !h || !p) return fail(c, RSV_E_INVALID, "null argument");
+  int r;
+  if ((r = check_range(c, n, lo, hi))) return r;
+  CK(cudaSetDevice(c->device));
+  int l = 0;
+  if (on_device) {
+    LK(launch_position_update(h, p, cc, lo, hi, c->stream, &l));
+  } else {
+    if ((r = ensure_plugin(c, n))) return r;
+    CK(cudaMemcpyAsync(c->pl[0] + lo, h + lo, sizeof(double) * (hi - lo), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->pl[1] + lo, p + lo, sizeof(double) * (hi - lo), cudaMemcpyHostToDevice, c->stream));
+    LK(launch_position_update(c->pl[0], c->pl[1], cc, lo, hi, c->stream, &l));
+    CK(cudaMemcpyAsync(h + lo, c->pl[0] + lo, sizeof(double) * (hi - lo), cudaMemcpyDeviceToHost, c->stream));
+  }
+  c->launches += l;
+  return sync(c);
+}
+
+static int plugin_grad(rsv_ctx *c, const double *h, double *p, const double *y, const double *lrv, double dt,
+                       const double *scal, int64_t n, int64_t lo, int64_t hi, int32_t *flag, int on_device,
+                       int fill) {
+  int r;
+  if ((r = check_range(c, n, lo, hi))) return r;
+  if (!scal) return fail(c, RSV_E_INVALID, "null scalars");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemsetAsync(c->dflag, 0, sizeof(int32_t), c->stream));
+  int l = 0;
+  PackedScal P;
+  for (int i = 0; i < 7; i++) P.v[i] = scal[i];
+  if (on_device) {
+    if (fill) LK(launch_gradient(h, y, lrv, P, p, n, lo, hi, c->dflag, c->stream, &l));
+    else LK(launch_momentum_update(h, p, y, lrv, dt, P, n, lo, hi, c->dflag, c->stream, &l));
+  } else {
+    if ((r = ensure_plugin(c, n))) return r;
+    const int64_t a = lo > 0 ? lo - 1 : 0, b = hi < n ? hi + 1 : n;
+    CK(cudaMemcpyAsync(c->pl[0] + a, h + a, sizeof(double) * (b - a), cudaMemcpyHostToDevice, c->stream));
+    if (!fill)
+      CK(cudaMemcpyAsync(c->pl[1] + lo, p + lo, sizeof(double) * (hi - lo), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->pl[2] + lo, y + lo, sizeof(double) * (hi - lo), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->pl[3] + lo, lrv + lo, sizeof(double) * (hi - lo), cudaMemcpyHostToDevice, c->stream));
+    if (fill) LK(launch_gradient(c->pl[0], c->pl[2], c->pl[3], P, c->pl[1], n, lo, hi, c->dflag, c->stream, &l));
+    else LK(launch_momentum_update(c->pl[0], c->pl[1], c->pl[2], c->pl[3], dt, P, n, lo, hi, c->dflag, c->stream, &l));
+    CK(cudaMemcpyAsync(p + lo, c->pl[1] + lo, sizeof(double) * (hi - lo), cudaMemcpyDeviceToHost, c->stream));
+  }
+  c->launches += l;
+  CK(cudaMemcpyAsync(c->h_flag, c->dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  if ((r = sync(c))) return r;
+  if (flag) *flag = *c->h_flag;
+  return 0;
+}
+
+int rsv_momentum_update(rsv_ctx *c, const double *h, double *p, const double *y, const double *lrv, double dt,
+                        const double *scal, int64_t n, int64_t lo, int64_t hi, int32_t *flag, int on_device) {
+  if (!c || !h || !p || !y || !lrv) return fail(c, RSV_E_INVALID, "null argument");
+  return plugin_grad(c, h, p, y, lrv, dt, scal, n, lo, hi, flag, on_device, 0);
+}
+
+int rsv_gradient(rsv_ctx *c, const double *h, const double *y, const double *lrv, const double *scal,
+                 double *out, int64_t n, int64_t lo, int64_t hi, int32_t *flag, int on_device) {
+  if (!c || !h || !out || !y || !lrv) return fail(c, RSV_E_INVALID, "null argument");
+  return plugin_grad(c, h, out, y, lrv, 0.0, scal, n, lo, hi, flag, on_device, 1);
+}
+
+static int energy(rsv_ctx *c, const double *h, const double *p, int on_device, double *kin, double *logf) {
+  if (!c->has_data || !c->has_params) return fail(c, RSV_E_STATE, "data/params not set");
+  CK(cudaSetDevice(c->device));
+  int r;
+  if ((r = copy_in(c, c->sh, h, c->T, on_device))) return r;
+  if (p) {
+    if ((r = copy_in(c, c->sp, p, c->T, on_device))) return r;
+  } else {
+    CK(cudaMemsetAsync(c->sp, 0, sizeof(double) * c->T, c->stream));
+  }
+  int l = 0;
+  LK(launch_energy(c->sh, c->sp, c->y, c->lrv, c->prm, c->T, c->rpart, c->rout, c->stream, &l));
+  c->launches += l;
+  CK(cudaMemcpyAsync(c->h_out, c->rout, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
+  if ((r = sync(c))) return r;
+  *kin = c->h_out[0];
+  *logf = c->h_out[1];
+  return 0;
+}
+
+int rsv_hamiltonian(rsv_ctx *c, const double *h, const double *p, double *out, int on_device) {
+  if (!c || !h || !p || !out) return fail(c, RSV_E_INVALID, "null argument");
+  double k, lf;
+  int r = energy(c, h, p, on_device, &k, &lf);
+  if (r) return r;
+  *out = k - lf;
+  return 0;
+}
+
+int rsv_log_posterior(rsv_ctx *c, const double *h, double *out, int on_device) {
+  if (!c || !h || !out) return fail(c, RSV_E_INVALID, "null argument");
+  double k, lf;
+  int r = energy(c, h, nullptr, on_device, &k, &lf);
+  if (r) return r;
+  *out = lf;
+  return 0;
+}
+
+int rsv_suff_stats(rsv_ctx *c, double c_mu, double c_xi, double out[7]) {
+  if (!c || !out) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->has_data || !c->has_latent) return fail(c, RSV_E_STATE, "data/latent not set");
+  CK(cudaSetDevice(c->device));
+  int r;
+  if ((r = pull_ctrl(c))) return r;
+  int l = 0;
+  LK(launch_suff_stats(c->hbuf[c->h_ctrl->cur & 1], c->lrv, c->T, c_mu, c_xi, c->rpart, c->rout, c->stream, &l));
+  c->launches += l;
+  CK(cudaMemcpyAsync(c->h_out, c->rout, sizeof(double) * 7, cudaMemcpyDeviceToHost, c->stream));
+  if ((r = sync(c))) return r;
+  for (int i = 0; i < 7; i++) out[i] = c->h_out[i];
+  return 0;
+}
+
+int rsv_set_timing(rsv_ctx *c, int enable) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  c->timing = enable != 0;
+  return 0;
+}
+
+int rsv_get_timing(rsv_ctx *c, double *traj_ms, double *momenta_ms, double *total_ms) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  auto avg = [](const std::vector<double> &v) {
+    double s = 0;
+    for (double x : v) s += x;
+    return v.empty() ? 0.0 : s / v.size();
+  };
+  if (traj_ms) *traj_ms = avg(c->last_traj_ms);
+  if (momenta_ms) *momenta_ms = avg(c->last_mom_ms);
+  if (total_ms) *total_ms = avg(c->last_total_ms);
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// rsv_internal.h -- device data layout shared by the kernels and the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "prng.cuh"
+
+namespace rsv {
+
+// ---- momenta (numpy ziggurat parse) geometry -------------------------------
+constexpr int ZW = 8;            // raw words per thread
+constexpr int ZT = 256;          // threads per block
+constexpr int ZB = ZW * ZT;      // words per block
+constexpr int ZS = 16;           // parse states: words still owed to the running attempt
+constexpr int ZMMAX = 7;         // tail loops resolvable in the parallel parse (len <= 15)
+constexpr int Z2T = 256;         // threads of the block-scan kernel
+constexpr int SFC_SNAP = 64;     // sfc64 state snapshot stride (words)
+
+// ---- trajectory tile geometry ----------------------------------------------
+constexpr int TR_NT = 256;       // threads per tile
+constexpr int TR_R = 8;          // consecutive sites per thread (registers)
+constexpr int TR_W = TR_NT * TR_R;
+constexpr int TR_NW = TR_NT / 32;
+constexpr int TR_NV = 14;        // reduced values per tile (see TilePart)
+
+// ---- streamed (one step per pass) kernel ------------------------------------
+constexpr int ES_NT = 256;
+constexpr int ES_R = 4;
+
+struct DevParams {
+  double phi, mu, xi, se2, su2;
+};
+
+struct TilePart {  // per-tile partial sums over the tile's core sites
+  double dh;       // sum of per-thread (H_new - H_old) variable parts
+  double hold, hnew;
+  double so[5];    // old path: sum d, sum d^2, sum d_t d_{t-1}, sum e, sum e^2
+  double sn[5];    // proposal: same
+  double flag;     // > 0 if any core site left [-50, 50] (or NaN) at a kick
+};
+
+struct DevResult {  // mirrors rsv_result
+  int32_t accept, diverged;
+  double delta_h, h_old, h_new;
+  uint64_t words_used;
+  double u;
+};
+
+struct DevControl {
+  StreamState stream;   // stream position / state for the next draw
+  int32_t cur;          // index of the h buffer holding the current path
+  int32_t err;          // bit 0: momenta shortfall, bit 1: parse overflow (serial fallback ran)
+  uint64_t zig_used;    // raw words consumed by the last momenta draw
+  uint64_t zig_avail;   // normals the parallel parse produced
+  int32_t zig_overflow; // an attempt needed > ZMMAX tail loops
+  int32_t pad;
+  double ends_old[2], ends_new[2];  // d_0, d_{T-1} (shifted by mu)
+  double stats[7];      // statistics of the kept path (shift mu, xi of the params used)
+  DevResult res;
+};
+
+}  // namespace rsv

@@ -1,0 +1,89 @@
+// rsv_launch.h -- host-side launch wrappers of the kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rsv_internal.h"
+
+namespace rsv {
+
+struct MomentaBufs {
+  DevControl *ctrl;
+  void *scratch;        // momenta_scratch_bytes(T)
+  uint64_t *sfc_words;  // SFC64 only: momenta_words(T) + 64 words
+  uint64_t *sfc_snaps;  // SFC64 only: 4 * ((momenta_words(T) + 64) / SFC_SNAP + 1) words
+  double *normals;      // T doubles
+};
+
+int64_t momenta_words(int64_t T);
+size_t momenta_scratch_bytes(int64_t T);
+int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, int *launches);
+int launch_momenta_advance(const MomentaBufs &b, cudaStream_t s, int *launches);
+
+// Tile geometry of the fused trajectory kernel for (T, n_steps).
+struct TrajGeom {
+  int64_t core;   // core sites per tile
+  int halo;       // n_steps + 1
+  int n_tiles;
+  int ok;         // 0 if n_steps is too large for one tile (falls back to per-step passes)
+};
+TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count);
+
+struct TrajArgs {
+  int64_t T;
+  int n_steps;
+  int fuse;
+  double dt;
+  TrajGeom g;
+  const double *h_src;  // if null: h buffers selected by ctrl->cur
+  double *h_dst;
+  double *hbuf0, *hbuf1;
+  const double *p_in;
+  double *p_out;        // optional
+  const double *a;      // 0.5 y^2
+  const double *lrv;
+  const DevParams *prm;
+  DevControl *ctrl;
+  TilePart *parts;
+};
+int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches);
+
+struct AcceptArgs {
+  int64_t T;
+  int n_tiles;
+  const TilePart *parts;
+  const DevParams *prm;
+  DevControl *ctrl;
+  const uint64_t *sfc_words;
+  const uint64_t *sfc_snaps;
+  DevResult *res_out;   // optional per-call result slot
+  int integrate_only;   // 1: just reduce (rsv_integrate), no Metropolis / stream update
+};
+int launch_accept(const AcceptArgs &a, cudaStream_t s, int *launches);
+
+// one streamed leapfrog step over all sites (integrator.py:139-146)
+int launch_elementary_step(const double *h, const double *p, double *ho, double *po, const double *a,
+                           const double *lrv, const DevParams *prm, double dt, int64_t T, int32_t *flag,
+                           cudaStream_t s, int *launches);
+
+// kernel-level plug-in (the reference's backend.run protocol)
+int launch_position_update(double *h, const double *p, double c, int64_t lo, int64_t hi, cudaStream_t s,
+                           int *launches);
+struct PackedScal {  // model.py:185-199 scalar_pack
+  double v[7];
+};
+int launch_momentum_update(const double *h, double *p, const double *y, const double *lrv, double dt,
+                           PackedScal sc, int64_t n, int64_t lo, int64_t hi, int32_t *flag, cudaStream_t s,
+                           int *launches);
+int launch_gradient(const double *h, const double *y, const double *lrv, PackedScal sc, double *out, int64_t n,
+                    int64_t lo, int64_t hi, int32_t *flag, cudaStream_t s, int *launches);
+
+// deterministic reductions for hamiltonian / log_posterior / suff_stats
+// out[0..7): see rsv_suff_stats; out for energy: {kinetic, -log f}
+int launch_energy(const double *h, const double *p, const double *y, const double *lrv, const DevParams *prm,
+                  int64_t T, double *partials, double *out, cudaStream_t s, int *launches);
+int launch_suff_stats(const double *h, const double *lrv, int64_t T, double c_mu, double c_xi, double *partials,
+                      double *out, cudaStream_t s, int *launches);
+int reduce_partials_count(int64_t T);
+
+}  // namespace rsv

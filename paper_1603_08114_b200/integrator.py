@@ -1,0 +1,347 @@
+"""Leapfrog integrator on the B200 (mirror of the reference's ``integrator.py``).
+
+The reference advances the phase state with three barrier-separated range
+kernels per step (``integrator.py:111-146``) run by a pluggable backend
+(``integrator.py:50-105``).  Here:
+
+* :class:`CudaBackend` is a drop-in ``backend=`` object.  Its ``run(kernel,
+  n, args)`` implements the reference's backend protocol for the
+  reference's own kernels (``_kernels.position_update`` /
+  ``momentum_update`` / ``gradient_fill``) on the GPU, so the unmodified
+  reference can run on it; the package's functions below use its fused
+  paths instead.
+* :func:`elementary_step` runs K1->K2->K3 as one streamed kernel.
+* :func:`integrate_trajectory` runs the whole trajectory as one launch of the
+  tiled, register-resident trajectory kernel (csrc/leapfrog.cu).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .model import Dataset, Params, PhaseState, _f64, scalar_pack
+
+DEFAULT_CHUNK = 512
+DH_DIVERGENCE_THRESHOLD = 1000.0  # integrator.py:29; applied on device
+
+
+@dataclass(frozen=True)
+class MDConfig:
+    """Step size and step count of one trajectory (integrator.py:32-47)."""
+
+    step_size: float
+    n_steps: int
+
+    def __post_init__(self):
+        if not self.step_size > 0.0:
+            raise ValueError(f"step_size must be positive, got {self.step_size}")
+        if self.n_steps < 1:
+            raise ValueError(f"n_steps must be >= 1, got {self.n_steps}")
+
+    @property
+    def trajectory_length(self) -> float:
+        return self.n_steps * self.step_size
+
+
+class DeviceChain:
+    """One ``rsv_ctx``: a length-T chain resident on one GPU."""
+
+    def __init__(self, T: int, device: int = 0):
+        self.T = int(T)
+        self.device = device
+        self._lib = N.lib()
+        h = ctypes.c_void_p()
+        N.check(self._lib.rsv_create(ctypes.byref(h), int(device), self.T))
+        self.ctx = h.value
+        self._data_key = None
+        self._params_key = None
+
+    # -- lifecycle --
+    def close(self):
+        if self.ctx:
+            self._lib.rsv_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, code):
+        N.check(code, self.ctx)
+
+    # -- state --
+    def set_data(self, data: Dataset, force: bool = False):
+        key = (id(data), id(data.returns), id(data.log_rv), data.returns.ctypes.data, data.log_rv.ctypes.data)
+        if force or key != self._data_key:
+            if data.length != self.T:
+                raise ValueError(f"dataset length {data.length} does not match chain length {self.T}")
+            y = np.ascontiguousarray(data.returns, dtype=np.float64)
+            lrv = np.ascontiguousarray(data.log_rv, dtype=np.float64)
+            self._ck(self._lib.rsv_set_data(self.ctx, y.ctypes.data, lrv.ctypes.data, 0))
+            self._data_key = key
+            self._data_ref = data  # keep ids alive
+
+    def set_params(self, params: Params):
+        key = (params.phi, params.mu, params.xi, params.sigma_eta_sq, params.sigma_u_sq)
+        if key != self._params_key:
+            self._ck(self._lib.rsv_set_params(self.ctx, ctypes.byref(N.to_params(params))))
+            self._params_key = key
+
+    def set_latent(self, h: np.ndarray):
+        h = _f64(h)
+        if h.shape != (self.T,):
+            raise ValueError(f"latent path length {h.shape[0]} does not match chain length {self.T}")
+        self._ck(self._lib.rsv_set_latent(self.ctx, h.ctypes.data, 0))
+
+    def get_latent(self, out: np.ndarray | None = None) -> np.ndarray:
+        out = np.empty(self.T) if out is None else out
+        self._ck(self._lib.rsv_get_latent(self.ctx, N.ptr(out), 0))
+        return out
+
+    def set_stream(self, st: N.PrngState):
+        self._ck(self._lib.rsv_set_prng_state(self.ctx, ctypes.byref(st)))
+
+    def get_stream(self) -> N.PrngState:
+        st = N.PrngState()
+        self._ck(self._lib.rsv_get_prng_state(self.ctx, ctypes.byref(st)))
+        return st
+
+    # -- hot path --
+    def hmc_update(self, step_size: float, n_steps: int, fuse: bool = False) -> N.Result:
+        r = N.Result()
+        self._ck(self._lib.rsv_hmc_update(self.ctx, float(step_size), int(n_steps), int(bool(fuse)),
+                                          ctypes.byref(r)))
+        return r
+
+    def hmc_update_many(self, step_size: float, n_steps: int, n: int, fuse: bool = False,
+                        results: bool = True):
+        out = (N.Result * n)() if results else None
+        self._ck(self._lib.rsv_hmc_update_many(self.ctx, float(step_size), int(n_steps), int(bool(fuse)), int(n),
+                                               out))
+        return out
+
+    def integrate(self, h, p, step_size, n_steps, fuse=False):
+        h = _f64(h)
+        p = _f64(p, "p")
+        ho, po = np.empty_like(h), np.empty_like(p)
+        div = ctypes.c_int32(0)
+        self._ck(self._lib.rsv_integrate(self.ctx, h.ctypes.data, p.ctypes.data, float(step_size), int(n_steps),
+                                         int(bool(fuse)), ho.ctypes.data, po.ctypes.data, ctypes.byref(div), 0))
+        return ho, po, bool(div.value)
+
+    def elementary_step_inplace(self, h: np.ndarray, p: np.ndarray, step_size: float) -> bool:
+        div = ctypes.c_int32(0)
+        self._ck(self._lib.rsv_elementary_step(self.ctx, N.ptr(h), N.ptr(p), float(step_size),
+                                               ctypes.byref(div), 0))
+        return bool(div.value)
+
+    def refresh_momenta(self) -> np.ndarray:
+        out = np.empty(self.T)
+        self._ck(self._lib.rsv_refresh_momenta(self.ctx, out.ctypes.data, 0))
+        return out
+
+    def hamiltonian(self, h, p) -> float:
+        v = ctypes.c_double()
+        self._ck(self._lib.rsv_hamiltonian(self.ctx, N.ptr(h), N.ptr(p), ctypes.byref(v), 0))
+        return float(v.value)
+
+    def log_posterior(self, h) -> float:
+        v = ctypes.c_double()
+        self._ck(self._lib.rsv_log_posterior(self.ctx, N.ptr(h), ctypes.byref(v), 0))
+        return float(v.value)
+
+    def suff_stats(self, c_mu: float, c_xi: float) -> np.ndarray:
+        out = np.empty(7)
+        self._ck(self._lib.rsv_suff_stats(self.ctx, float(c_mu), float(c_xi),
+                                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def last_stats(self) -> np.ndarray:
+        out = np.empty(7)
+        self._ck(self._lib.rsv_last_stats(self.ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def set_timing(self, on: bool):
+        self._ck(self._lib.rsv_set_timing(self.ctx, int(bool(on))))
+
+    def timing(self):
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        self._ck(self._lib.rsv_get_timing(self.ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def launch_count(self) -> int:
+        return int(self._lib.rsv_launch_count(self.ctx))
+
+
+class CudaBackend:
+    """Drop-in ``backend=`` for the reference API (integrator.py:50-105).
+
+    Holds one :class:`DeviceChain` per series length.  ``run`` speaks the
+    reference's kernel-level protocol; ``workers`` is 1 because a single GPU
+    executes every kernel (results never depend on it)."""
+
+    workers = 1
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        self._chains: dict[int, DeviceChain] = {}
+        self._aux: DeviceChain | None = None
+
+    def chain(self, data: Dataset | None = None, params: Params | None = None, T: int | None = None) -> DeviceChain:
+        T = data.length if data is not None else int(T)
+        ch = self._chains.get(T)
+        if ch is None:
+            ch = self._chains[T] = DeviceChain(T, self.device)
+        if data is not None:
+            ch.set_data(data)
+        if params is not None:
+            ch.set_params(params)
+        return ch
+
+    def _any_chain(self) -> DeviceChain:
+        if self._chains:
+            return next(iter(self._chains.values()))
+        if self._aux is None:
+            self._aux = DeviceChain(2, self.device)
+        return self._aux
+
+    # -- the reference's backend protocol: run(kernel, n, args) -> int --
+    def run(self, kernel, n: int, args: tuple) -> int:
+        name = getattr(kernel, "__name__", getattr(getattr(kernel, "py_func", None), "__name__", ""))
+        ch = self._any_chain()
+        lib = ch._lib
+        if name == "position_update":
+            h, p, c = args
+            self._f64_arrays(h, p)
+            ch._ck(lib.rsv_position_update(ch.ctx, h.ctypes.data, p.ctypes.data, float(c), int(n), 0, int(n), 0))
+            return 0
+        if name == "momentum_update":
+            h, p, y, lrv, dt = args[:5]
+            self._f64_arrays(h, p, y, lrv)
+            scal = np.array([float(v) for v in args[5:12]], dtype=np.float64)
+            flag = ctypes.c_int32(0)
+            ch._ck(lib.rsv_momentum_update(ch.ctx, h.ctypes.data, p.ctypes.data, y.ctypes.data, lrv.ctypes.data,
+                                           float(dt), scal.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                           int(n), 0, int(n), ctypes.byref(flag), 0))
+            return int(flag.value)
+        if name == "gradient_fill":
+            h, y, lrv, out = args[:4]
+            self._f64_arrays(h, y, lrv, out)
+            scal = np.array([float(v) for v in args[4:11]], dtype=np.float64)
+            flag = ctypes.c_int32(0)
+            ch._ck(lib.rsv_gradient(ch.ctx, h.ctypes.data, y.ctypes.data, lrv.ctypes.data,
+                                    scal.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), out.ctypes.data,
+                                    int(n), 0, int(n), ctypes.byref(flag), 0))
+            return int(flag.value)
+        raise NotImplementedError(f"CudaBackend cannot run kernel {name!r}")
+
+    @staticmethod
+    def _f64_arrays(*arrs):
+        for a in arrs:
+            if a.dtype == np.float32:
+                raise NotImplementedError("the B200 path computes in float64 only")
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError("CudaBackend.run needs C-contiguous float64 arrays")
+
+    def gradient(self, h: np.ndarray, params: Params, data: Dataset) -> np.ndarray:
+        out = np.empty_like(h)
+        scal = np.array(scalar_pack(params, np.float64), dtype=np.float64)
+        y = np.ascontiguousarray(data.returns, dtype=np.float64)
+        lrv = np.ascontiguousarray(data.log_rv, dtype=np.float64)
+        ch = self._any_chain()
+        flag = ctypes.c_int32(0)
+        ch._ck(ch._lib.rsv_gradient(ch.ctx, h.ctypes.data, y.ctypes.data, lrv.ctypes.data,
+                                    scal.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), out.ctypes.data,
+                                    h.size, 0, h.size, ctypes.byref(flag), 0))
+        return out
+
+    def close(self):
+        for ch in self._chains.values():
+            ch.close()
+        self._chains.clear()
+        if self._aux is not None:
+            self._aux.close()
+            self._aux = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+_DEFAULT: CudaBackend | None = None
+
+
+def default_backend() -> CudaBackend:
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = CudaBackend(0)
+    return _DEFAULT
+
+
+def _resolve(backend) -> CudaBackend:
+    if backend is None:
+        return default_backend()
+    if not isinstance(backend, CudaBackend):
+        raise TypeError("this package runs on the GPU: pass a CudaBackend (or None for the default)")
+    return backend
+
+
+def kernel1_half_position(state: PhaseState, dt: float, backend=None) -> PhaseState:
+    """integrator.py:111-116: h += (dt/2) p in place (exact reference arithmetic)."""
+    b = _resolve(backend)
+    t = state.h.dtype.type
+    b.run(_named("position_update"), state.size, (state.h, state.p, t(0.5) * t(dt)))
+    return state
+
+
+def kernel2_momentum(state: PhaseState, dt: float, params: Params, data: Dataset,
+                     backend=None) -> tuple[PhaseState, bool]:
+    """integrator.py:119-131: p -= dt * grad, divergence flag."""
+    b = _resolve(backend)
+    dtype = state.h.dtype
+    args = (state.h, state.p, np.ascontiguousarray(data.returns, dtype=dtype),
+            np.ascontiguousarray(data.log_rv, dtype=dtype), dtype.type(dt)) + scalar_pack(params, dtype)
+    flag = b.run(_named("momentum_update"), state.size, args)
+    return state, bool(flag)
+
+
+def kernel3_half_position(state: PhaseState, dt: float, backend=None) -> PhaseState:
+    """integrator.py:134-136."""
+    return kernel1_half_position(state, dt, backend)
+
+
+def elementary_step(state: PhaseState, config: MDConfig, params: Params, data: Dataset,
+                    backend=None) -> tuple[PhaseState, bool]:
+    """integrator.py:139-146: K1 -> K2 -> K3 in place, one streamed kernel."""
+    b = _resolve(backend)
+    if state.h.dtype != np.float64:
+        raise NotImplementedError("the B200 path computes in float64 only")
+    ch = b.chain(data, params)
+    diverged = ch.elementary_step_inplace(state.h, state.p, config.step_size)
+    return state, diverged
+
+
+def integrate_trajectory(state: PhaseState, config: MDConfig, params: Params, data: Dataset, backend=None,
+                         fuse_half_steps: bool = False) -> tuple[PhaseState, bool]:
+    """integrator.py:149-179: n_steps leapfrog steps on a copy of ``state``,
+    as one launch of the fused trajectory kernel."""
+    b = _resolve(backend)
+    if state.h.dtype != np.float64:
+        raise NotImplementedError("the B200 path computes in float64 only")
+    ch = b.chain(data, params)
+    h, p, diverged = ch.integrate(state.h, state.p, config.step_size, config.n_steps, fuse_half_steps)
+    return PhaseState(h, p), diverged
+
+
+class _named:
+    """Stand-in carrying a reference kernel name for CudaBackend.run."""
+
+    def __init__(self, name):
+        self.__name__ = name

@@ -1,0 +1,153 @@
+"""Generate the golden fixtures from the REFERENCE itself (build container only).
+
+Runs the unmodified reference package (pkg/src/rsvhmc under /root/reference)
+with numpy Generators over the oracle's bit generators (oracle/oracle.py
+Stream, a duck-typed numpy BitGenerator), and writes small .npz fixtures
+that travel to the GPU box.  Re-run with:
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Nothing on the GPU box imports the reference; tests only read these files.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import oracle as O  # noqa: E402
+import rsvhmc  # noqa: E402
+import rsvhmc.sampler as RS  # noqa: E402
+
+TRUE = rsvhmc.Params(phi=0.97, mu=-9.0, xi=-0.3, sigma_eta_sq=0.05, sigma_u_sq=0.1)
+KINDS = ("philox", "minstd", "pcg32", "sfc64")
+
+
+def gen(kind, seed):
+    st = O.Stream(kind, seed)
+    return st, st.generator()
+
+
+def prng():
+    out = {}
+    for kind in KINDS:
+        for seed in (0, 1, 12345):
+            st = O.Stream(kind, seed)
+            out[f"raw_{kind}_{seed}"] = st.raw(64)
+            out[f"mat_{kind}_{seed}"] = O.seed_material(kind, seed)
+            _, g = gen(kind, seed)
+            out[f"normal_{kind}_{seed}"] = g.standard_normal(4096)  # numpy's own ziggurat
+    # numpy's own generators, no oracle involved
+    out["np_philox_raw_7"] = np.random.Philox(7).random_raw(64)
+    out["np_sfc64_raw_7"] = np.random.SFC64(7).random_raw(64)
+    out["np_philox_normal_7"] = np.random.Generator(np.random.Philox(7)).standard_normal(8192)
+    out["np_sfc64_normal_7"] = np.random.Generator(np.random.SFC64(7)).standard_normal(8192)
+    # a window with exponential-tail draws (idx == 0 attempts): find words
+    st = O.Stream("philox", 2024)
+    w = st.raw(62000)
+    tail = np.nonzero(((w & 0xFF) == 0) & (((w >> 9) & ((1 << 52) - 1)) >= 0xEF33D8025EF6A))[0]
+    out["tail_word_idx_philox_2024"] = tail[:64]
+    _, g = gen("philox", 2024)
+    out["normal_philox_2024"] = g.standard_normal(60000)
+    np.savez_compressed(os.path.join(HERE, "prng.npz"), **out)
+
+
+def model():
+    out = {}
+    truth = rsvhmc.simulate_rsv(TRUE, 2000, seed=0)
+    out["y"], out["lrv"], out["h_true"] = truth.dataset.returns, truth.dataset.log_rv, truth.latent
+    out["theta"] = np.array([TRUE.phi, TRUE.mu, TRUE.xi, TRUE.sigma_eta_sq, TRUE.sigma_u_sq])
+    data = truth.dataset
+    h = truth.latent
+    out["log_post"] = rsvhmc.log_posterior(h, TRUE, data)
+    out["grad"] = rsvhmc.grad_neg_log_posterior(h, TRUE, data)
+    _, g = gen("minstd", 1)
+    p = RS.refresh_momenta(g, 2000)
+    out["p0"] = p
+    out["ham"] = rsvhmc.hamiltonian(rsvhmc.PhaseState(h.copy(), p.copy()), TRUE, data)
+    for fuse in (False, True):
+        fin, div = rsvhmc.integrate_trajectory(rsvhmc.PhaseState(h.copy(), p.copy()),
+                                               rsvhmc.MDConfig(0.02, 20), TRUE, data, fuse_half_steps=fuse)
+        out[f"traj_h_fuse{int(fuse)}"] = fin.h
+        out[f"traj_p_fuse{int(fuse)}"] = fin.p
+        out[f"traj_div_fuse{int(fuse)}"] = div
+        out[f"traj_ham_fuse{int(fuse)}"] = rsvhmc.hamiltonian(fin, TRUE, data)
+    st = rsvhmc.PhaseState(h.copy(), p.copy())
+    rsvhmc.elementary_step(st, rsvhmc.MDConfig(0.02, 1), TRUE, data)
+    out["estep_h"], out["estep_p"] = st.h, st.p
+    # divergent trajectory (integrator test analogue: huge momenta)
+    _, div = rsvhmc.integrate_trajectory(rsvhmc.PhaseState(h.copy(), np.full(2000, 1e4)),
+                                         rsvhmc.MDConfig(0.5, 20), TRUE, data)
+    out["div_flag"] = div
+    np.savez_compressed(os.path.join(HERE, "model_T2000.npz"), **out)
+
+
+def hmc_sequence(kind="minstd", seed=1, n=40):
+    """Config 1: T=2000, L=20, dt=0.02, minstd; 40 proposals at fixed theta."""
+    truth = rsvhmc.simulate_rsv(TRUE, 2000, seed=0)
+    data = truth.dataset
+    _, h0 = RS.default_init(data)
+    # start from the truth-shifted init so proposals are mostly accepted
+    h = truth.latent.copy()
+    st, g = gen(kind, seed)
+    md = rsvhmc.MDConfig(0.02, 20)
+    acc, dhs, pos, hs = [], [], [], []
+    for i in range(n):
+        h, a, dh = rsvhmc.hmc_update_volatility(h, TRUE, data, md, g)
+        acc.append(a)
+        dhs.append(dh)
+        pos.append(st.pos)
+        if i in (0, 1, n - 1):
+            hs.append(h.copy())
+    np.savez_compressed(os.path.join(HERE, f"hmc_{kind}.npz"), accept=np.array(acc), delta_h=np.array(dhs),
+                        pos=np.array(pos, dtype=np.uint64), h_first=hs[0], h_second=hs[1], h_last=hs[2],
+                        h_start=truth.latent, seed=seed)
+
+
+def hmc_divergent():
+    truth = rsvhmc.simulate_rsv(TRUE, 512, seed=3)
+    st, g = gen("pcg32", 9)
+    md = rsvhmc.MDConfig(0.9, 30)
+    res = [rsvhmc.hmc_update_volatility(truth.latent.copy(), TRUE, truth.dataset, md, g) for _ in range(3)]
+    np.savez_compressed(os.path.join(HERE, "hmc_divergent.npz"), accept=np.array([r[1] for r in res]),
+                        delta_h=np.array([r[2] for r in res]), pos=np.uint64(st.pos), y=truth.dataset.returns,
+                        lrv=truth.dataset.log_rv, h=truth.latent)
+
+
+def chain(kind="pcg32", seed=3, T=200, n=60):
+    truth = rsvhmc.simulate_rsv(rsvhmc.Params(0.95, -1.0, -0.3, 0.05, 0.1), T, seed=24)
+    keep = {}
+
+    def mk(s):
+        st, g = gen(kind, s)
+        keep["st"] = st
+        return g
+
+    old = RS.make_rng
+    RS.make_rng = mk
+    try:
+        cfg = rsvhmc.SamplerConfig(seed=seed, md=rsvhmc.MDConfig(0.05, 10), n_burnin=0, n_samples=n, thin=1,
+                                   store_latent=True)
+        ch = rsvhmc.run_chain(truth.dataset, cfg)
+    finally:
+        RS.make_rng = old
+    np.savez_compressed(os.path.join(HERE, f"chain_{kind}.npz"), y=truth.dataset.returns, lrv=truth.dataset.log_rv,
+                        phi=ch.phi, mu=ch.mu, xi=ch.xi, sigma_eta_sq=ch.sigma_eta_sq, sigma_u_sq=ch.sigma_u_sq,
+                        accept=ch.accept, delta_h=ch.delta_h, latent_last=ch.latent[-1], seed=seed,
+                        pos=np.uint64(keep["st"].pos))
+
+
+if __name__ == "__main__":
+    prng()
+    model()
+    hmc_sequence("minstd", 1)
+    hmc_sequence("philox", 11)
+    hmc_divergent()
+    chain("pcg32", 3)
+    chain("philox", 5)
+    for f in sorted(os.listdir(HERE)):
+        print(f, os.path.getsize(os.path.join(HERE, f)))

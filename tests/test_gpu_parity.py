@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C ABI) against the golden fixtures
+produced by the reference itself and against the CPU oracle.
+
+Tolerances: PRNG words and normals bit-exact; trajectories
+<= 1e-12 relative; H and dH <= 1e-13 |H| absolute (the reference's own dH
+error is ~3e-16 |H|, so no exact implementation can beat this bound);
+accept sequences identical."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1603_08114_b200 as P
+from conftest import TRUE, golden
+
+pytestmark = pytest.mark.gpu
+
+THETA = P.Params(**TRUE)
+
+
+def _data_T2000():
+    z = golden("model_T2000.npz")
+    return z, P.Dataset.from_log_rv(z["y"], z["lrv"])
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+# ---------------------------------------------------------------- momenta
+@pytest.mark.parametrize("kind", ["philox", "minstd", "pcg32", "sfc64"])
+@pytest.mark.parametrize("seed", [0, 1, 12345])
+def test_momenta_bit_exact_vs_numpy(backend, kind, seed):
+    z = golden("prng.npz")
+    want = z[f"normal_{kind}_{seed}"]
+    rng = P.make_rng(seed, kind)
+    got = P.refresh_momenta(rng, want.size, backend=backend)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    # the generator continues where numpy's would be after standard_normal(n)
+    st = O.Stream(kind, seed)
+    st.normals(want.size)
+    assert P.stream_state(rng).pos == st.pos
+
+
+def test_momenta_numpy_philox_object_is_continued(backend):
+    z = golden("prng.npz")
+    rng = np.random.Generator(np.random.Philox(7))
+    got = P.refresh_momenta(rng, 8192, backend=backend)
+    assert np.array_equal(got, z["np_philox_normal_7"])
+    ref = np.random.Generator(np.random.Philox(7))
+    ref.standard_normal(8192)
+    assert rng.random() == ref.random()          # stream state written back exactly
+
+
+def test_momenta_with_tail_draws(backend):
+    z = golden("prng.npz")
+    want = z["normal_philox_2024"]
+    assert len(z["tail_word_idx_philox_2024"]) >= 10   # exponential-tail attempts inside
+    got = P.refresh_momenta(P.make_rng(2024), want.size, backend=backend)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("T", [2, 3, 7, 2047, 2048, 2049, 100003, 1 << 20])
+def test_momenta_sizes_vs_oracle(backend, T):
+    for kind in ("pcg32", "sfc64"):
+        st = O.Stream(kind, T)
+        want = st.normals(T)
+        rng = P.make_rng(T, kind)
+        got = P.refresh_momenta(rng, T, backend=backend)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), kind
+        assert P.stream_state(rng).pos == st.pos
+
+
+# ---------------------------------------------------------------- model
+def test_log_posterior_and_hamiltonian(backend):
+    z, data = _data_T2000()
+    h, p = z["h_true"], z["p0"]
+    lp = P.log_posterior(h, THETA, data, backend=backend)
+    assert abs(lp - float(z["log_post"])) <= 1e-13 * abs(float(z["log_post"]))
+    H = P.hamiltonian(P.PhaseState(h, p), THETA, data, backend=backend)
+    assert abs(H - float(z["ham"])) <= 1e-13 * abs(float(z["ham"]))
+
+
+def test_gradient(backend):
+    z, data = _data_T2000()
+    g = P.grad_neg_log_posterior(z["h_true"], THETA, data, backend=backend)
+    assert _rel(g, z["grad"]) <= 1e-14
+
+
+# ---------------------------------------------------------------- integrator
+@pytest.mark.parametrize("fuse", [False, True])
+def test_trajectory_vs_reference(backend, fuse):
+    z, data = _data_T2000()
+    st = P.PhaseState(z["h_true"].copy(), z["p0"].copy())
+    fin, div = P.integrate_trajectory(st, P.MDConfig(0.02, 20), THETA, data, backend=backend,
+                                      fuse_half_steps=fuse)
+    assert not div
+    assert _rel(fin.h, z[f"traj_h_fuse{int(fuse)}"]) <= 1e-12
+    assert _rel(fin.p, z[f"traj_p_fuse{int(fuse)}"]) <= 1e-12
+    assert np.array_equal(st.h, z["h_true"])  # input untouched (integrator.py:160 copy)
+
+
+def test_elementary_step_vs_reference(backend):
+    z, data = _data_T2000()
+    st = P.PhaseState(z["h_true"].copy(), z["p0"].copy())
+    _, div = P.elementary_step(st, P.MDConfig(0.02, 1), THETA, data, backend=backend)
+    assert not div
+    assert _rel(st.h, z["estep_h"]) <= 1e-14
+    assert _rel(st.p, z["estep_p"]) <= 1e-14
+
+
+def test_divergence_flag(backend):
+    z, data = _data_T2000()
+    st = P.PhaseState(z["h_true"].copy(), np.full(2000, 1e4))
+    _, div = P.integrate_trajectory(st, P.MDConfig(0.5, 20), THETA, data, backend=backend)
+    assert div == bool(z["div_flag"]) and div
+
+
+# ---------------------------------------------------------------- HMC proposals
+@pytest.mark.parametrize("kind,seed", [("minstd", 1), ("philox", 11)])
+def test_hmc_sequence_vs_reference(backend, kind, seed):
+    z, data = _data_T2000()
+    g = golden(f"hmc_{kind}.npz")
+    rng = P.make_rng(seed, kind)
+    h = g["h_start"].copy()
+    H = abs(float(z["ham"]))
+    for i in range(len(g["accept"])):
+        h, acc, dh = P.hmc_update_volatility(h, THETA, data, P.MDConfig(0.02, 20), rng, backend=backend)
+        want = float(g["delta_h"][i])
+        assert abs(dh - want) <= 1e-13 * H, (i, dh, want)
+        assert acc == bool(g["accept"][i]), i
+        assert P.stream_state(rng).pos == int(g["pos"][i]), i
+        if i == 0:
+            assert _rel(h, g["h_first"]) <= 1e-10
+    assert _rel(h, g["h_last"]) <= 1e-10
+
+
+def test_hmc_divergent_sentinel(backend):
+    g = golden("hmc_divergent.npz")
+    data = P.Dataset.from_log_rv(g["y"], g["lrv"])
+    rng = P.make_rng(9, "pcg32")
+    for i in range(3):
+        h, acc, dh = P.hmc_update_volatility(g["h"].copy(), THETA, data, P.MDConfig(0.9, 30), rng, backend=backend)
+        assert not acc and math.isinf(dh)
+    assert P.stream_state(rng).pos == int(g["pos"])   # no uniform drawn on divergence
+
+
+# ---------------------------------------------------------------- chains
+@pytest.mark.parametrize("kind,seed", [("pcg32", 3), ("philox", 5)])
+def test_run_chain_vs_reference(backend, kind, seed):
+    g = golden(f"chain_{kind}.npz")
+    data = P.Dataset.from_log_rv(g["y"], g["lrv"])
+    cfg = P.SamplerConfig(seed=seed, md=P.MDConfig(0.05, 10), n_burnin=0, n_samples=len(g["accept"]), thin=1,
+                          store_latent=True, prng=kind)
+    ch = P.run_chain(data, cfg, backend=backend)
+    assert np.array_equal(ch.accept, g["accept"])
+    for name in ("phi", "mu", "xi", "sigma_eta_sq", "sigma_u_sq"):
+        assert np.allclose(getattr(ch, name), g[name], rtol=1e-9, atol=1e-12), name
+    assert _rel(ch.latent[-1], g["latent_last"]) <= 1e-9
+
+
+# ---------------------------------------------------------------- large-T properties
+def test_large_T_reversibility_and_determinism(backend):
+    T = 1 << 20
+    truth = P.simulate_rsv(THETA, T, seed=5)
+    data = truth.dataset
+    p = P.refresh_momenta(P.make_rng(6, "pcg32"), T, backend=backend)
+    md = P.MDConfig(0.02, 20)
+    fwd, div = P.integrate_trajectory(P.PhaseState(truth.latent, p), md, THETA, data, backend=backend)
+    assert not div
+    fwd2, _ = P.integrate_trajectory(P.PhaseState(truth.latent, p), md, THETA, data, backend=backend)
+    assert np.array_equal(fwd.h, fwd2.h) and np.array_equal(fwd.p, fwd2.p)
+    back, _ = P.integrate_trajectory(P.PhaseState(fwd.h, -fwd.p), md, THETA, data, backend=backend)
+    assert np.max(np.abs(back.h - truth.latent)) <= 1e-9
+    assert np.max(np.abs(-back.p - p)) <= 1e-9
+    # a window of the large trajectory against the oracle (sites far from edges
+    # only depend on a 2L+1 neighbourhood, so a slice with margins suffices)
+    lo, hi = 300000, 300000 + 4096
+    m = 64
+    hh, pp, _ = O.integrate(truth.latent[lo - m:hi + m], p[lo - m:hi + m], THETA, data.returns[lo - m:hi + m],
+                            data.log_rv[lo - m:hi + m], 0.02, 20)
+    assert _rel(fwd.h[lo:hi], hh[m:-m]) <= 1e-12
+    assert _rel(fwd.p[lo:hi], pp[m:-m]) <= 1e-12
+
+
+@pytest.mark.parametrize("T", [2, 3, 5, 41, 42, 43, 2006, 2007, 4096, 65537])
+@pytest.mark.parametrize("L", [1, 3, 20])
+def test_trajectory_edge_sizes_vs_oracle(backend, T, L):
+    truth = P.simulate_rsv(THETA, T, seed=T)
+    data = truth.dataset
+    p = O.Stream("pcg32", T + L).normals(T)
+    fin, div = P.integrate_trajectory(P.PhaseState(truth.latent, p), P.MDConfig(0.02, L), THETA, data,
+                                      backend=backend)
+    hh, pp, dd = O.integrate(truth.latent, p, THETA, data.returns, data.log_rv, 0.02, L)
+    assert div == dd
+    assert _rel(fin.h, hh) <= 1e-12 and _rel(fin.p, pp) <= 1e-12
+
+
+def test_long_trajectory_streamed_fallback(backend):
+    # n_steps beyond one tile's halo budget runs one streamed step per launch
+    T = 3000
+    truth = P.simulate_rsv(THETA, T, seed=1)
+    p = O.Stream("philox", 3).normals(T)
+    fin, div = P.integrate_trajectory(P.PhaseState(truth.latent, p), P.MDConfig(0.002, 900), THETA,
+                                      truth.dataset, backend=backend)
+    hh, pp, dd = O.integrate(truth.latent, p, THETA, truth.dataset.returns, truth.dataset.log_rv, 0.002, 900)
+    assert div == dd
+    assert _rel(fin.h, hh) <= 1e-11
+
+
+# ---------------------------------------------------------------- kernel-level plug-in
+def test_backend_run_protocol_matches_reference_kernels(backend):
+    z, data = _data_T2000()
+    h, p = z["h_true"].copy(), z["p0"].copy()
+    c = np.float64(0.5) * np.float64(0.02)
+    h_ref = h + c * p
+    P.kernel1_half_position(P.PhaseState(h, p), 0.02, backend=backend)
+    assert np.array_equal(h, h_ref)                       # exact reference arithmetic
+    g, _ = O.gradient(h, THETA, data.returns, data.log_rv)
+    st = P.PhaseState(h.copy(), p.copy())
+    _, div = P.kernel2_momentum(st, 0.02, THETA, data, backend=backend)
+    assert not div
+    assert _rel(st.p, p - 0.02 * g) <= 1e-14
+
+
+def test_suff_stats_vs_oracle(backend):
+    z, data = _data_T2000()
+    ch = backend.chain(data, THETA)
+    ch.set_latent(z["h_true"])
+    got = ch.suff_stats(-9.0, -0.3)
+    want = O.suff_stats(z["h_true"], data.log_rv, -9.0, -0.3)
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-9)
