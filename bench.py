@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""bench.py -- HMC site-updates/s of the RSV volatility update on B200.
+
+Metric (BASELINE.json): HMC site-updates/sec (T x leapfrog steps / s) and
+trajectories/s.  One "step" is one full HMC proposal of the reference's
+hmc_update_volatility (sampler.py:144-167): numpy-exact momenta, H_old, an
+L-step leapfrog trajectory, H_new, dH and the Metropolis test -- on one
+synthetic series of T sites (config 3 of BASELINE.json at N=1: a single long
+chain, T=2^20, L=20, dt=0.02, pcg32).  With N>1 (torchrun) every rank runs an
+independent replica chain (weak scaling; the time-sharded single chain is
+not implemented yet).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HMC site-updates/sec (T x leapfrog steps/s)"
+UNIT = "site-updates/s"
+THETA = dict(phi=0.97, mu=-9.0, xi=-0.3, sigma_eta_sq=0.05, sigma_u_sq=0.1)
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+# algorithmic FP64 work of one site-update in the trajectory kernel
+# (DESIGN.md "Roofline"): 2 drifts (2 FMA), kick (3 FMA + 2 ADD),
+# exp(-d) (8 FMA + 1 ADD + 1 MUL)  ->  13 FMA + 4 other = 30 flops.
+FLOPS_PER_SITE_UPDATE = 30
+HBM_BYTES_PER_SITE = 48  # streamed elementary step: r h,p,(y/2)y,lnRV; w h,p
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--T", type=int, default=1 << 20)
+    ap.add_argument("--L", type=int, default=20)
+    ap.add_argument("--dt", type=float, default=0.02)
+    ap.add_argument("--prng", default="pcg32")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples if len(s) >= 6 for i in range(4)
+                          if s[2 + i].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(T, L, dt, kind, seconds, data, h0):
+    """The reference algorithm restated in C (oracle/, kind 'port'), all host
+    threads for the leapfrog kernels, on a bounded sample of trajectories."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    import paper_1603_08114_b200 as P
+    nth = O.max_threads()
+    theta = P.Params(**THETA)
+    st = O.Stream(kind, 1)
+    h = h0.copy()
+    O.hmc_update(h, theta, data.returns, data.log_rv, dt, L, st, nthreads=nth)  # warm the pool
+    n, t0 = 0, time.perf_counter()
+    while True:
+        h, _, _ = O.hmc_update(h, theta, data.returns, data.log_rv, dt, L, st, nthreads=nth)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= 200:
+            break
+    O.lib().orc_pool_shutdown()
+    return {"value": T * L * n / el, "unit": UNIT, "cores": nth, "kind": "port",
+            "sample": f"{n} HMC proposals (momenta+2H+{L}-step trajectory+Metropolis) at T={T}, {el:.1f} s",
+            "trajectories_per_s": n / el}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    import paper_1603_08114_b200 as P
+    theta = P.Params(**THETA)
+    truth = P.simulate_rsv(theta, args.T, seed=0)
+    data = truth.dataset
+    nth = O.max_threads()
+    st = O.Stream(args.prng, 1)
+    h = truth.latent.copy()
+    for _ in range(args.warmup):
+        h, _, _ = O.hmc_update(h, theta, data.returns, data.log_rv, args.dt, args.L, st, nthreads=nth)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        h, _, _ = O.hmc_update(h, theta, data.returns, data.log_rv, args.dt, args.L, st, nthreads=nth)
+        times.append(time.perf_counter() - t0)
+    O.lib().orc_pool_shutdown()
+    tot = sum(times)
+    value = args.T * args.L * args.steps / tot
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (simulate_rsv, seed 0)",
+            "impl": "reference",
+            "config": {"workload": f"single chain T={args.T}, L={args.L}, dt={args.dt}, {args.prng}: one full HMC "
+                                   "proposal per step (reference CPU algorithm, oracle port)",
+                       "T": args.T, "L": args.L, "prng": args.prng},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "port",
+                             "sample": f"{args.steps} HMC proposals at T={args.T}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "trajectories_per_s": args.steps / tot}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    import torch
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    import paper_1603_08114_b200 as P
+
+    theta = P.Params(**THETA)
+    T, L, dt = args.T, args.L, args.dt
+    truth = P.simulate_rsv(theta, T, seed=0)
+    data = truth.dataset
+    be = P.CudaBackend(local)
+    ch = be.chain(data, theta)
+    ch.set_latent(truth.latent)
+    ch.set_stream(P.stream_state(P.make_rng(1 + rank, args.prng)))
+    # warm-up (graph capture + clocks)
+    ch.hmc_update_many(dt, L, max(3, args.warmup), results=False)
+
+    # ---------------- timed region: K proposals, device-timed per step
+    ch.set_l2_flush(L2_FLUSH_BYTES)
+    ch.set_timing(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(local)
+    n0 = ch.launch_count()
+    t_wall = time.perf_counter()
+    res = ch.hmc_update_many(dt, L, args.steps, results=True)
+    bracket_s = time.perf_counter() - t_wall
+    torch.cuda.synchronize(local)
+    launches = ch.launch_count() - n0
+    clk = clocks.stop()
+    traj_ms, mom_ms, step_ms = ch.timing()
+    ch.set_timing(False)
+    ch.set_l2_flush(0)
+    accept_rate = float(np.mean([r.accept for r in res]))
+    step_s = step_ms * 1e-3
+    if dist:
+        t = torch.tensor([step_s, traj_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_s, traj_ms = float(t[0]), float(t[1])
+    value = ws * T * L / step_s
+
+    # ---------------- roofline of the dominant kernel (trajectory, FP64-bound)
+    fp64_peak = ch.fp64_peak_tflops()
+    achieved = FLOPS_PER_SITE_UPDATE * T * L / (traj_ms * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traj_dram_bytes.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(str(T))
+        except Exception:
+            traffic = None
+
+    # ---------------- e2e through the public API (host buffers, copies timed)
+    rng = P.make_rng(7 + rank, args.prng)
+    md = P.MDConfig(dt, L)
+    h_host = torch.empty(T, dtype=torch.float64, pin_memory=True).numpy()
+    h_host[:] = truth.latent
+    h = h_host
+    P.hmc_update_volatility(h, theta, data, md, rng, backend=be)  # warm
+    e2e_steps = max(3, min(args.steps, 20))
+    n_acc = 0
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        h, acc, _ = P.hmc_update_volatility(h, theta, data, md, rng, backend=be)
+        n_acc += int(acc)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    state_bytes = 48 + 40  # stream state + params structs
+    e2e = {"value": ws * T * L / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * T + state_bytes,
+           "d2h_bytes_per_step": int(8 * T * n_acc / e2e_steps) + 48 + 56,
+           "path": "paper_1603_08114_b200.hmc_update_volatility(h numpy[pinned], params, data, md, rng) -> C ABI"}
+
+    extra = {}
+    if rank == 0:
+        # ---------------- HBM roofline of the streamed one-step kernel (T >> L2)
+        Ts = 1 << 24
+        tr2 = P.simulate_rsv(theta, Ts, seed=3)
+        ch2 = be.chain(tr2.dataset, theta)
+        hh = tr2.latent.copy()
+        pp = np.random.default_rng(0).standard_normal(Ts)
+        ch2.elementary_step_inplace(hh, pp, dt)
+        import ctypes
+        ms = ctypes.c_float()
+        ch2._ck(ch2._lib.rsv_bench_elementary(ch2.ctx, dt, 50, ctypes.byref(ms)))
+        per = ms.value / 50 * 1e-3
+        peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
+        hbm_peak = peaks.get("hbm_gbs", 6650.0)
+        gbs = HBM_BYTES_PER_SITE * Ts / per / 1e9
+        extra["roofline_hbm"] = {"kernel": "estep_kernel (one streamed leapfrog step, integrator.py:139-146)",
+                                 "bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                                 "frac": gbs / hbm_peak, "traffic": HBM_BYTES_PER_SITE * Ts,
+                                 "site_updates_per_s": Ts / per, "T": Ts,
+                                 "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback 6.65 TB/s"}
+        be._chains.pop(Ts, None)
+        ch2.close()
+        # ---------------- paper-style sweep (config 2): trajectories/s vs T
+        if not args.no_sweep:
+            sweep = []
+            for Tq in (1 << 10, 1 << 14, 1 << 18):
+                trq = P.simulate_rsv(theta, Tq, seed=4)
+                cq = be.chain(trq.dataset, theta)
+                cq.set_latent(trq.latent)
+                cq.set_stream(P.stream_state(P.make_rng(2, args.prng)))
+                cq.hmc_update_many(dt, L, 5, results=False)
+                cq.set_timing(True)
+                cq.hmc_update_many(dt, L, 50, results=False)
+                tq, mq, sq = cq.timing()
+                cq.set_timing(False)
+                sweep.append({"T": Tq, "ms_per_proposal": sq, "traj_kernel_ms": tq,
+                              "trajectories_per_s": 1e3 / sq, "site_updates_per_s": Tq * L / (sq * 1e-3)})
+                be._chains.pop(Tq, None)
+                cq.close()
+            extra["sweep"] = sweep
+        if not args.no_cpu:
+            extra["cpu_baseline"] = cpu_baseline(T, L, dt, args.prng, args.cpu_seconds, data, truth.latent)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (simulate_rsv, theta of SURVEY §8d, seed 0)",
+            "config": {"workload": f"config 3 at N=1 per GPU: single chain T={T}, L={L}, dt={dt}, {args.prng}; "
+                                   "one step = one full HMC proposal (momenta + H_old + trajectory + H_new + "
+                                   "Metropolis), device-resident, CUDA graph",
+                       "T": T, "L": L, "dt": dt, "prng": args.prng,
+                       "parallelism": "single" if ws == 1 else f"replicas x{ws}",
+                       "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB memset, not timed)"},
+            "trajectories_per_s": ws / step_s, "accept_rate": accept_rate,
+            "breakdown_ms": {"momenta": mom_ms, "trajectory": traj_ms, "proposal": step_s * 1e3},
+            "bracket_ms_per_step_incl_flush": bracket_s * 1e3 / args.steps,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "roofline": {"kernel": "traj_kernel (fused L-step trajectory)", "bound": "fp64", "achieved": achieved,
+                         "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
+                         "flops_per_site_update": FLOPS_PER_SITE_UPDATE,
+                         "peak_source": "measured live: DFMA microbenchmark (rsv_measure_fp64_peak)"},
+            "clocks": clk,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    be.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,13 @@ int rsv_last_stats(rsv_ctx *ctx, double out[7]);
  * rsv_hmc_update_many call with timing enabled. */
 int rsv_set_timing(rsv_ctx *ctx, int enable);
 int rsv_get_timing(rsv_ctx *ctx, double *traj_ms, double *momenta_ms, double *total_ms);
+/* Benchmark hygiene: with bytes > 0, rsv_hmc_update_many writes a
+ * scratch buffer of that size between proposals (outside the timed events)
+ * so each proposal starts with a cold L2. */
+int rsv_set_l2_flush(rsv_ctx *ctx, int64_t bytes);
+/* Measured FP64 FMA throughput of this device (DFMA microbenchmark),
+ * in TFLOP/s (2 flops per FMA); *sm_mhz_est = implied average SM clock. */
+int rsv_measure_fp64_peak(rsv_ctx *ctx, double *tflops);
 /* Kernel launches issued by the context so far (gpu_launches evidence). */
 int64_t rsv_launch_count(const rsv_ctx *ctx);
 

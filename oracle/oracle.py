@@ -31,7 +31,9 @@ def build(force: bool = False) -> str:
 
 class _Stream(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("pad", ctypes.c_int32),
-                ("s", ctypes.c_uint64 * 4), ("pos", ctypes.c_uint64)]
+                ("s", ctypes.c_uint64 * 4), ("pos", ctypes.c_uint64),
+                ("cache_pos", ctypes.c_uint64), ("cache_state", ctypes.c_uint64),
+                ("cache_ok", ctypes.c_int32), ("pad2", ctypes.c_int32)]
 
 
 class _Bitgen(ctypes.Structure):

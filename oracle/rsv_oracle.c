@@ -36,6 +36,10 @@ typedef struct {
   int32_t pad;
   uint64_t s[4];
   uint64_t pos;
+  /* sequential-access cache (not part of the stream's identity): the LCG
+   * state in front of word cache_pos, so consecutive draws cost O(1) */
+  uint64_t cache_pos, cache_state;
+  int32_t cache_ok, pad2;
 } orc_stream;
 
 static inline uint64_t mulhilo64(uint64_t a, uint64_t b, uint64_t *hi) {
@@ -103,13 +107,18 @@ uint64_t orc_next_u64(orc_stream *st) {
       return out[n % 4];
     }
     case 1: {
-      uint64_t xa = minstd_out(st->s[0], 3 * n), xb = minstd_out(st->s[0], 3 * n + 1),
-               xc = minstd_out(st->s[0], 3 * n + 2);
+      /* x_{3n} then three steps */
+      uint64_t x = (st->cache_ok && st->cache_pos == n) ? st->cache_state
+                                                        : (powmod31(MINSTD_A, 3 * n) * st->s[0]) % MINSTD_M;
+      uint64_t xa = (x * MINSTD_A) % MINSTD_M, xb = (xa * MINSTD_A) % MINSTD_M, xc = (xb * MINSTD_A) % MINSTD_M;
+      st->cache_ok = 1; st->cache_pos = n + 1; st->cache_state = xc;
       return (xa << 33) | (xb << 2) | (xc >> 29);
     }
     case 2: {
-      uint64_t s0 = pcg_advance(st->s[0], 2 * n, PCG_MULT, st->s[1]);
+      uint64_t s0 = (st->cache_ok && st->cache_pos == n) ? st->cache_state
+                                                         : pcg_advance(st->s[0], 2 * n, PCG_MULT, st->s[1]);
       uint64_t s1 = s0 * PCG_MULT + st->s[1];
+      st->cache_ok = 1; st->cache_pos = n + 1; st->cache_state = s1 * PCG_MULT + st->s[1];
       return ((uint64_t)pcg_output(s0) << 32) | pcg_output(s1);
     }
     default:

@@ -85,6 +85,8 @@ _SIGS = {
     "rsv_set_timing": (ctypes.c_int, [_CTX, ctypes.c_int]),
     "rsv_get_timing": (ctypes.c_int, [_CTX, _D, _D, _D]),
     "rsv_launch_count": (ctypes.c_int64, [_CTX]),
+    "rsv_set_l2_flush": (ctypes.c_int, [_CTX, ctypes.c_int64]),
+    "rsv_measure_fp64_peak": (ctypes.c_int, [_CTX, _D]),
     "rsv_stream_seed": (ctypes.c_int, [ctypes.POINTER(PrngState), ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
     "rsv_stream_next_u64": (ctypes.c_uint64, [ctypes.POINTER(PrngState)]),
     "rsv_stream_next_double": (ctypes.c_double, [ctypes.POINTER(PrngState)]),

@@ -39,6 +39,21 @@ __global__ void prep_data_kernel(const double *y, double *a, int64_t T) {
   if (i < T) a[i] = __dmul_rn(__dmul_rn(0.5, y[i]), y[i]);  // (half * y) * y, _kernels.py:27
 }
 
+// FP64 peak probe: 8 independent DFMA chains per thread, grid = 8 CTAs/SM.
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double *out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) x[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = fma(x[k], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) s += x[k];
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void ring_store_kernel(DevControl *ctrl, DevResult *ring, int cap, int32_t *count) {
   if (threadIdx.x || blockIdx.x) return;
   const int i = *count;
@@ -84,7 +99,10 @@ struct rsv_ctx {
   double *pl[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t pl_n = 0;
 
+  void *flush_buf = nullptr;
+  int64_t flush_bytes = 0;
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::vector<cudaGraph_t> timed_graphs;
   bool timing = false;
   std::vector<cudaEvent_t> evpool;
   std::vector<double> last_traj_ms, last_mom_ms, last_total_ms;
@@ -126,6 +144,8 @@ int rsv_destroy(rsv_ctx *c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto g : c->timed_graphs) cudaGraphDestroy(g);
+  if (c->flush_buf) cudaFree(c->flush_buf);
   for (auto e : c->evpool) cudaEventDestroy(e);
   void *dev[] = {c->hbuf[0], c->hbuf[1], c->y, c->a, c->lrv, c->normals, c->sh, c->sp, c->sh2, c->sp2,
                  c->zscratch, c->sfc_words, c->sfc_snaps, c->parts, c->rpart, c->rout, c->dflag, c->ring_count,
@@ -384,11 +404,11 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, cudaGraphExec_t *out) {
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   int l = 0;
   bool ok = true;
-  if (k.timing) cudaEventRecord(c->evpool[0], c->stream);
+  if (k.timing) cudaEventRecordWithFlags(c->evpool[0], c->stream, cudaEventRecordExternal);
   ok &= launch_momenta(mbufs(c), k.kind, c->T, c->stream, &l) == 0;
-  if (k.timing) cudaEventRecord(c->evpool[1], c->stream);
+  if (k.timing) cudaEventRecordWithFlags(c->evpool[1], c->stream, cudaEventRecordExternal);
   ok &= launch_trajectory(traj_args(c, k.dt, k.n_steps, k.fuse, g), c->stream, &l) == 0;
-  if (k.timing) cudaEventRecord(c->evpool[2], c->stream);
+  if (k.timing) cudaEventRecordWithFlags(c->evpool[2], c->stream, cudaEventRecordExternal);
   AcceptArgs aa;
   memset(&aa, 0, sizeof(aa));
   aa.T = c->T;
@@ -399,7 +419,7 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, cudaGraphExec_t *out) {
   aa.sfc_words = c->sfc_words;
   aa.sfc_snaps = c->sfc_snaps;
   ok &= launch_accept(aa, c->stream, &l) == 0;
-  if (k.timing) cudaEventRecord(c->evpool[3], c->stream);
+  if (k.timing) cudaEventRecordWithFlags(c->evpool[3], c->stream, cudaEventRecordExternal);
   cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
   if (!ok || e != cudaSuccess) return fail(c, RSV_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
   cudaGraphExec_t exec;
@@ -420,9 +440,13 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, cudaGraphExec_t *out) {
       for (int i = 0; i < 4; i++)
         if (ev == c->evpool[i]) evn[i] = nd;
     }
+    for (int i = 0; i < 4; i++)
+      if (!evn[i]) return fail(c, RSV_E_CUDA, "timing graph: event node %d not found", i);
     g_evnodes[exec] = evn;
+    c->timed_graphs.push_back(graph);  // node handles stay valid while the graph lives
+  } else {
+    cudaGraphDestroy(graph);
   }
-  cudaGraphDestroy(graph);
   *out = exec;
   return 0;
 }
@@ -485,6 +509,7 @@ int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv
     if (evn) {
       for (int j = 0; j < 4; j++) CK(cudaGraphExecEventRecordNodeSetEvent(exec, (*evn)[j], c->evpool[4 + 4 * i + j]));
     }
+    if (c->flush_bytes > 0) CK(cudaMemsetAsync(c->flush_buf, i & 0xff, (size_t)c->flush_bytes, c->stream));
     CK(cudaGraphLaunch(exec, c->stream));
     c->launches += kpl;
     if (out) {
@@ -767,6 +792,43 @@ int rsv_suff_stats(rsv_ctx *c, double c_mu, double c_xi, double out[7]) {
   CK(cudaMemcpyAsync(c->h_out, c->rout, sizeof(double) * 7, cudaMemcpyDeviceToHost, c->stream));
   if ((r = sync(c))) return r;
   for (int i = 0; i < 7; i++) out[i] = c->h_out[i];
+  return 0;
+}
+
+int rsv_set_l2_flush(rsv_ctx *c, int64_t bytes) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  CK(cudaSetDevice(c->device));
+  if (c->flush_buf) {
+    CK(cudaFree(c->flush_buf));
+    c->flush_buf = nullptr;
+  }
+  c->flush_bytes = bytes > 0 ? bytes : 0;
+  if (c->flush_bytes) CK(cudaMalloc(&c->flush_buf, (size_t)c->flush_bytes));
+  return 0;
+}
+
+int rsv_measure_fp64_peak(rsv_ctx *c, double *tflops) {
+  if (!c || !tflops) return fail(c, RSV_E_INVALID, "null argument");
+  CK(cudaSetDevice(c->device));
+  const int blocks = c->sm_count * 8, threads = 256, iters = 4096;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  double best = 0;
+  for (int rep = 0; rep < 5; rep++) {
+    CK(cudaEventRecord(e0, c->stream));
+    dfma_peak_kernel<<<blocks, threads, 0, c->stream>>>(c->rout, iters, 0.999999, 1e-7);
+    CK(cudaEventRecord(e1, c->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    const double fl = 2.0 * 8.0 * iters * (double)blocks * threads;
+    if (rep > 0 && fl / (ms * 1e-3) / 1e12 > best) best = fl / (ms * 1e-3) / 1e12;
+  }
+  c->launches += 5;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *tflops = best;
   return 0;
 }
 

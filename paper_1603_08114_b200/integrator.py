@@ -174,6 +174,14 @@ class DeviceChain:
         self._ck(self._lib.rsv_get_timing(self.ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
         return a.value, b.value, c.value
 
+    def set_l2_flush(self, nbytes: int):
+        self._ck(self._lib.rsv_set_l2_flush(self.ctx, int(nbytes)))
+
+    def fp64_peak_tflops(self) -> float:
+        v = ctypes.c_double()
+        self._ck(self._lib.rsv_measure_fp64_peak(self.ctx, ctypes.byref(v)))
+        return float(v.value)
+
     def launch_count(self) -> int:
         return int(self._lib.rsv_launch_count(self.ctx))
 
