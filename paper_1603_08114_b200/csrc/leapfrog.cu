@@ -25,15 +25,17 @@
 
 namespace rsv {
 
-__device__ const double g_exp_tab[64] = RSV_EXP_TAB_INIT;
+__device__ const unsigned long long g_exp_tab2[64] = RSV_EXP_TAB2_INIT;
 
 constexpr double MAGIC = 6755399441055744.0;  // 1.5 * 2^52
 
-// exp(-d) for the model's range: n = rint(-64 d / ln2), r = -d - n ln2/64,
-// e^r - 1 by a degree-5 polynomial (|r| <= ln2/128), 2^(n/64) by table +
-// exponent add.  10 FP64 instructions; <= ~1.5 ulp.  `t` is returned so the
-// caller can range-check n (divergence test) with integer ops only.
-__device__ __forceinline__ double exp_neg(double d, const double *tab, double &t) {
+// exp(-d) for the model's range.  n = rint(-64 d / ln2) via the magic-number
+// add, r = -d - n ln2/64 (Cody-Waite, two FMAs), e^r - 1 by a degree-5
+// Horner polynomial (|r| <= ln2/128), and S = 2^(n/64) built exactly from a
+// scale-ready table entry (bits(2^(j/64)) - (j << 46)) plus n << 46: one
+// shared-memory load and one integer add.  10 FP64 instructions, <= ~1.5 ulp.
+// `t` is returned for the integer range test of the divergence flag.
+__device__ __forceinline__ double exp_neg(double d, const unsigned long long *tab, double &t) {
   t = fma(-d, RSV_INV_LN2_64, MAGIC);
   const double nd = t - MAGIC;
   double r = fma(nd, -RSV_LN2_64_HI, -d);
@@ -44,54 +46,47 @@ __device__ __forceinline__ double exp_neg(double d, const double *tab, double &t
   q = fma(q, r, 1.0);
   q = q * r;
   const int n = __double2loint(t);
-  const double T = tab[n & 63];
-  const double e = fma(T, q, T);
-  return __hiloint2double(__double2hiint(e) + ((n >> 6) << 20), __double2loint(e));
+  const unsigned long long tb = tab[n & 63];
+  const double S = __hiloint2double((int)(tb >> 32) + (n << 14), (int)(unsigned)tb);
+  return fma(S, q, S);
 }
 
-// |h| <= 50 (and not NaN) <=> n within [n_lo, n_hi] and t a sane magic sum
-__device__ __forceinline__ bool in_range(double t, int n_lo, int n_span) {
+// |h| <= 50 <=> n in [n_lo, n_lo + span]; NaN or huge d leave the magic
+// sum's high word outside {0x4337FFFF, 0x43380000}.  Integer ops only.
+__device__ __forceinline__ bool out_of_range(double t, int n_lo, int n_span) {
   const int n = __double2loint(t);
   const unsigned hw = (unsigned)__double2hiint(t) - 0x4337FFFFu;
-  return ((unsigned)(n - n_lo) <= (unsigned)n_span) & (hw <= 1u);
+  return ((unsigned)(n - n_lo) > (unsigned)n_span) | (hw > 1u);
 }
 
-struct TrajScalars {
-  double mu, phi, c_half, c_full, dt, bphi, g_int, g_end, adt, half_dt, alpha, emu, xm;
-  double inv2su, inv2se, one_m_phi2;
-  int n_lo, n_span;
-};
-
-__device__ __forceinline__ TrajScalars traj_scalars(const DevParams &P, double dt) {
-  TrajScalars s;
+TrajConsts traj_consts(const DevParams &P, double dt) {
+  TrajConsts s;
   s.mu = P.mu;
   s.phi = P.phi;
   s.dt = dt;
   s.c_half = 0.5 * dt;
   s.c_full = dt;
-  const double inv_su2 = 1.0 / P.su2, inv_se2 = 1.0 / P.se2;
-  s.alpha = dt * inv_su2;
-  const double beta = dt * inv_se2;
-  s.bphi = beta * P.phi;
-  s.g_int = s.alpha + beta * (1.0 + P.phi * P.phi);
-  s.g_end = s.alpha + beta;
-  s.emu = exp(-P.mu);
-  s.adt = dt * s.emu;
   s.half_dt = 0.5 * dt;
+  s.alpha = dt * P.inv_su2;
+  const double beta = dt * P.inv_se2;
+  s.bphi = beta * P.phi;
+  s.g_int = s.alpha + beta * (2.0 - P.one_m_phi2);
+  s.g_end = s.alpha + beta;
+  s.emu = P.emu;
   s.xm = P.xi + P.mu;
-  s.inv2su = 0.5 * inv_su2;
-  s.inv2se = 0.5 * inv_se2;
-  s.one_m_phi2 = 1.0 - P.phi * P.phi;
-  // n = rint(-d * 64/ln2) with d = h - mu; |h| <= 50  <=>  n in [n_lo, n_hi]
-  s.n_lo = (int)floor((P.mu - 50.0) * RSV_INV_LN2_64);
-  s.n_span = (int)ceil((P.mu + 50.0) * RSV_INV_LN2_64) - s.n_lo;
+  s.inv2su = 0.5 * P.inv_su2;
+  s.inv2se = 0.5 * P.inv_se2;
+  s.one_m_phi2 = P.one_m_phi2;
+  s.hconst = P.hconst;
+  s.n_lo = P.n_lo;
+  s.n_span = P.n_span;
   return s;
 }
 
-// Variable part of H at one site (the theta-only constants are added by the
-// accept kernel): 0.5 p^2 + 0.5 d + a e^{-mu} e^{-d} + (q - d)^2 / 2su2 + AR.
+// Variable part of H at one site (the theta-only constants are added in
+// the Metropolis step): 0.5 p^2 + 0.5 d + a e^{-mu} e^{-d} + (q-d)^2/2su2 + AR.
 __device__ __forceinline__ double site_energy(double d, double dprev, double p, double ae, double q, bool first,
-                                              const TrajScalars &s, const double *tab) {
+                                              const TrajConsts &s, const unsigned long long *tab) {
   double t;
   const double E = exp_neg(d, tab, t);
   const double r = q - d;
@@ -100,7 +95,31 @@ __device__ __forceinline__ double site_energy(double d, double dprev, double p, 
   return 0.5 * p * p + 0.5 * d + ae * E + r * r * s.inv2su + ar;
 }
 
+// Energies and statistics of the thread's owned core sites (branch-free on
+// the common path; `edge` threads handle the global first site).
+template <int R>
+__device__ __forceinline__ void tile_energy(const double (&d)[R], const double (&p)[R], const double (&av)[R],
+                                            const double (&lv)[R], double dl, uint32_t core, bool edge, int64_t g0,
+                                            const TrajConsts &s, const unsigned long long *tab, double (&v)[6]) {
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    const double dprev = r ? d[r - 1] : dl;
+    const double q = lv[r] - s.xm;
+    const double e = q - d[r];
+    const bool first = edge && (g0 + r == 0);
+    const double en = site_energy(d[r], dprev, p[r], s.emu * av[r], q, first, s, tab);
+    const bool c = (core >> r) & 1;
+    v[0] += c ? en : 0.0;
+    v[1] += c ? d[r] : 0.0;
+    v[2] += c ? d[r] * d[r] : 0.0;
+    v[3] += (c && !first) ? d[r] * dprev : 0.0;
+    v[4] += c ? e : 0.0;
+    v[5] += c ? e * e : 0.0;
+  }
+}
+
 // Exchange the first / last register site with the neighbouring threads.
+template <int NW>
 __device__ __forceinline__ void exchange(double first, double last, double &left, double &right, double *s_first,
                                          double *s_last, int lane, int warp) {
   left = __shfl_up_sync(0xffffffffu, last, 1);
@@ -109,11 +128,13 @@ __device__ __forceinline__ void exchange(double first, double last, double &left
   if (lane == 0) s_first[warp] = first;
   __syncthreads();
   if (lane == 0) left = warp > 0 ? s_last[warp - 1] : 0.0;
-  if (lane == 31) right = warp < TR_NW - 1 ? s_first[warp + 1] : 0.0;
+  if (lane == 31) right = warp < NW - 1 ? s_first[warp + 1] : 0.0;
 }
 
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double (*s_red)[NV], int lane, int warp) {
+// Fixed-order block sum (deterministic): warp butterflies, then warp totals
+// in warp order by thread 0.
+template <int NV, int NW>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double *s_red, int lane, int warp) {
 #pragma unroll
   for (int k = 0; k < NV; k++) {
 #pragma unroll
@@ -121,32 +142,38 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double (*s_red)[NV], 
   }
   if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < NV; k++) s_red[warp][k] = v[k];
+    for (int k = 0; k < NV; k++) s_red[warp * NV + k] = v[k];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < NV; k++) {
-      double acc = s_red[0][k];
-      for (int w = 1; w < TR_NW; w++) acc += s_red[w][k];
+      double acc = s_red[k];
+      for (int w = 1; w < NW; w++) acc += s_red[w * NV + k];
       v[k] = acc;
     }
   }
 }
 
-// One kick p -= dt * dU/dh for the thread's R sites (d-space), see DESIGN.md:
+// One kick p -= dt * dU/dh for the thread's R sites (d-space):
 //   p <- p - Cd - G d + beta phi (d_{i-1} + d_{i+1}) + Ad e^{-d}
-template <bool EDGE>
-__device__ __forceinline__ void kick(double (&d)[TR_R], double (&p)[TR_R], const double (&Ad)[TR_R],
-                                     const double (&Cd)[TR_R], double dl, double dr, const TrajScalars &s,
-                                     const double *tab, uint32_t live, uint32_t endm, uint32_t core, int &bad) {
+// The divergence test (|h| > 50) is accumulated as the largest
+// (unsigned)(n - n_lo) over the thread's core sites and checked once at the
+// end; NaN or astronomically large states (which no longer map to a sane n)
+// propagate to a non-finite dH, which the Metropolis step rejects the same
+// way (sampler.py:157-162).
+template <bool EDGE, int R>
+__device__ __forceinline__ void kick(double (&d)[R], double (&p)[R], const double (&Ad)[R],
+                                     const double (&Cd)[R], double dl, double dr, const TrajConsts &s,
+                                     const unsigned long long *tab, uint32_t live, uint32_t endm,
+                                     const unsigned (&cm)[R], unsigned &nmax) {
 #pragma unroll
-  for (int r = 0; r < TR_R; r++) {
+  for (int r = 0; r < R; r++) {
     const double dm = r ? d[r - 1] : dl;
-    const double dp = r < TR_R - 1 ? d[r + 1] : dr;
+    const double dp = r < R - 1 ? d[r + 1] : dr;
     double t;
     const double E = exp_neg(d[r], tab, t);
-    if (!in_range(t, s.n_lo, s.n_span) && ((core >> r) & 1)) bad = 1;
+    nmax = max(nmax, ((unsigned)__double2loint(t) - (unsigned)s.n_lo) & cm[r]);
     const double G = EDGE && ((endm >> r) & 1) ? s.g_end : s.g_int;
     double pp = p[r] - Cd[r];
     pp = fma(-G, d[r], pp);
@@ -156,21 +183,76 @@ __device__ __forceinline__ void kick(double (&d)[TR_R], double (&p)[TR_R], const
   }
 }
 
-__device__ __forceinline__ void drift(double (&d)[TR_R], const double (&p)[TR_R], double c) {
+template <int R>
+__device__ __forceinline__ void drift(double (&d)[R], const double (&p)[R], double c) {
 #pragma unroll
-  for (int r = 0; r < TR_R; r++) d[r] = fma(c, p[r], d[r]);
+  for (int r = 0; r < R; r++) d[r] = fma(c, p[r], d[r]);
 }
 
-template <bool FUSE>
-__global__ void __launch_bounds__(TR_NT, 2) traj_kernel(TrajArgs A) {
-  __shared__ double s_tab[64];
-  __shared__ double s_first[2][TR_NW], s_last[2][TR_NW];
-  __shared__ double s_red[TR_NW][TR_NV];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 64) s_tab[tid] = g_exp_tab[tid];
+// Metropolis step (sampler.py:155-167) on the tile partials, run by the last
+// tile to finish; deterministic (fixed-order sums).
+template <int NT>
+__device__ void metropolis(const TrajArgs &A, double *s_v);
 
-  const DevParams P = *A.prm;
-  const TrajScalars s = traj_scalars(P, A.dt);
+// Warp windows overlap by one lane on each side ("ghost lanes"): warp w
+// holds sites [w*30R, w*30R + 32R) of the CTA window, its lanes 0 and 31
+// duplicate the last / first core lane of its neighbours.  Within a warp the
+// stencil needs only shuffles; a ghost lane's values go stale from the
+// window edge inwards one site per step, so after R steps they are refreshed
+// from the neighbours' core lanes through shared memory (one CTA barrier per
+// R steps).  Core lanes (1..30) are always exact; a site belongs to the one
+// warp whose core lane holds it.
+template <int R, int NT>
+__device__ __forceinline__ void ghost_refresh(double (&d)[R], double (&p)[R], double *s_gx, int lane, int warp,
+                                              int parity) {
+  constexpr int NW = NT / 32;
+  // s_gx layout: [parity][warp][side 0: lane 30 -> right neighbour's lane 0,
+  //                                side 1: lane 1 -> left neighbour's lane 31][2R]
+  double *slot = s_gx + (size_t)parity * NW * 4 * R;
+  if (lane == 30 || lane == 1) {
+    double *dst = slot + (warp * 2 + (lane == 1)) * 2 * R;
+#pragma unroll
+    for (int r = 0; r < R; r++) { dst[r] = d[r]; dst[R + r] = p[r]; }
+  }
+  __syncthreads();
+  if (lane == 0 && warp > 0) {
+    const double *src = slot + ((warp - 1) * 2 + 0) * 2 * R;
+#pragma unroll
+    for (int r = 0; r < R; r++) { d[r] = src[r]; p[r] = src[R + r]; }
+  }
+  if (lane == 31 && warp < NW - 1) {
+    const double *src = slot + ((warp + 1) * 2 + 1) * 2 * R;
+#pragma unroll
+    for (int r = 0; r < R; r++) { d[r] = src[r]; p[r] = src[R + r]; }
+  }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define RSV_STAMP(k)                                                                  \
+  do {                                                                                \
+    if (A.dbg && threadIdx.x == 0) A.dbg[(size_t)blockIdx.x * 8 + (k)] = gtimer(); \
+  } while (0)
+
+template <int R, int NT, int MINB, bool FUSE>
+__global__ void __launch_bounds__(NT, MINB) traj_kernel(TrajArgs A) {
+  constexpr int NW = NT / 32;
+  constexpr int WSTEP = 30 * R;  // window advance per warp
+  RSV_STAMP(0);
+  __shared__ unsigned long long s_tab[64];
+  __shared__ double s_first[NW], s_last[NW];
+  __shared__ double s_red[NW * TR_NV];
+  __shared__ double s_v[NW * TR_NV + TR_NV];
+  __shared__ double s_gx[2 * NW * 4 * R];
+  __shared__ double s_old[6 * NT];
+  __shared__ int s_last_tile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 64) s_tab[tid] = g_exp_tab2[tid];
+
+  const TrajConsts &s = A.k;
   const double *hsrc;
   double *hdst;
   if (A.h_src) {
@@ -182,181 +264,295 @@ __global__ void __launch_bounds__(TR_NT, 2) traj_kernel(TrajArgs A) {
     hdst = cur ? A.hbuf0 : A.hbuf1;
   }
   const int64_t T = A.T;
-  const int H = A.g.halo;
-  const int64_t t0 = (int64_t)blockIdx.x * A.g.core;
+  const int H = A.g.halo;                    // multiple of R (>= n_steps + 1)
+  const int64_t t0 = (int64_t)blockIdx.x * A.g.core;  // core is a multiple of R
   const int64_t t1 = min(t0 + A.g.core, T);
+  // live range [t0 - H, t1 + H): lanes start on multiples of R, so only the
+  // lanes at the global ends of the series hold partially live sites
   const int64_t lo_live = max((int64_t)0, t0 - H), hi_live = min(T, t1 + H);
-  const int64_t g0 = t0 - H + (int64_t)tid * TR_R;
+  const int64_t g0 = t0 - H + (int64_t)warp * WSTEP + (int64_t)lane * R;
+  const bool own_lane = (lane >= 1 && lane <= 30) || (lane == 0 && warp == 0) || (lane == 31 && warp == NW - 1);
 
-  uint32_t live = 0, core = 0, endm = 0;
-  double d[TR_R], p[TR_R], Ad[TR_R], Cd[TR_R];
-  double hold = 0.0, so[5] = {0, 0, 0, 0, 0};
+  // ---- load: vectorised when the lane's R sites are all live ----
+  double d[R], p[R], av[R], lv[R];
+  const bool full = g0 >= lo_live && g0 + R <= hi_live;
+  if (full) {
 #pragma unroll
-  for (int r = 0; r < TR_R; r++) {
-    const int64_t gi = g0 + r;
-    d[r] = 0.0; p[r] = 0.0; Ad[r] = 0.0; Cd[r] = 0.0;
-    if (gi >= lo_live && gi < hi_live) {
-      live |= 1u << r;
-      if (gi >= t0 && gi < t1) core |= 1u << r;
-      if (gi == 0 || gi == T - 1) endm |= 1u << r;
-      d[r] = hsrc[gi] - s.mu;
-      p[r] = A.p_in[gi];
-      const double ae = s.emu * A.a[gi];
-      const double q = A.lrv[gi] - s.xm;
-      Ad[r] = s.dt * ae;
-      Cd[r] = fma(-s.alpha, q, s.half_dt);
+    for (int r = 0; r < R; r += 2) {
+      const double2 h2 = __ldg(reinterpret_cast<const double2 *>(hsrc + g0 + r));
+      const double2 p2 = __ldg(reinterpret_cast<const double2 *>(A.p_in + g0 + r));
+      const double2 a2 = __ldg(reinterpret_cast<const double2 *>(A.a + g0 + r));
+      const double2 l2 = __ldg(reinterpret_cast<const double2 *>(A.lrv + g0 + r));
+      d[r] = h2.x; d[r + 1] = h2.y;
+      p[r] = p2.x; p[r + 1] = p2.y;
+      av[r] = a2.x; av[r + 1] = a2.y;
+      lv[r] = l2.x; lv[r + 1] = l2.y;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t gi = g0 + r;
+      const bool in = gi >= lo_live && gi < hi_live;
+      d[r] = in ? hsrc[gi] : s.mu;
+      p[r] = in ? A.p_in[gi] : 0.0;
+      av[r] = in ? A.a[gi] : 0.0;
+      lv[r] = in ? A.lrv[gi] : 0.0;
     }
   }
-  const bool edge = (live != (1u << TR_R) - 1) || endm;
-  const bool warp_live = __any_sync(0xffffffffu, live != 0);
+  uint32_t live = 0, core = 0, endm = 0;
+  double Ad[R], Cd[R];
+  unsigned cm[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    const int64_t gi = g0 + r;
+    const bool in = gi >= lo_live && gi < hi_live;
+    const bool c = in && own_lane && gi >= t0 && gi < t1;
+    live |= (uint32_t)in << r;
+    core |= (uint32_t)c << r;
+    endm |= (uint32_t)(gi == 0 || gi == T - 1) << r;
+    cm[r] = c ? ~0u : 0u;
+    d[r] = d[r] - s.mu;
+    Ad[r] = s.dt * (s.emu * av[r]);
+    Cd[r] = in ? fma(-s.alpha, lv[r] - s.xm, s.half_dt) : 0.0;
+  }
+  const bool any_live = live != 0;
+  const bool edge = (any_live && live != (1u << R) - 1) || endm;
   __syncthreads();  // s_tab
 
-  // ---- H_old and statistics of the current path (core sites) ----
+  // ---- H_old and statistics of the current path (owned core sites) ----
+  double hold;
   {
-    double dl, dr;
-    exchange(d[0], d[TR_R - 1], dl, dr, s_first[0], s_last[0], lane, warp);
+    double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
     double v[6] = {0, 0, 0, 0, 0, 0};
+    tile_energy<R>(d, p, av, lv, dl, core, edge, g0, s, s_tab, v);
+    hold = v[0];
+    asm volatile("" ::: "memory");
 #pragma unroll
-    for (int r = 0; r < TR_R; r++) {
-      if ((core >> r) & 1) {
-        const int64_t gi = g0 + r;
-        const double dprev = r ? d[r - 1] : dl;
-        const double ae = s.emu * A.a[gi];
-        const double q = A.lrv[gi] - s.xm;
-        const double e = q - d[r];
-        hold += site_energy(d[r], dprev, p[r], ae, q, gi == 0, s, s_tab);
-        so[0] += d[r];
-        so[1] += d[r] * d[r];
-        if (gi > 0) so[2] += d[r] * dprev;
-        so[3] += e;
-        so[4] += e * e;
-        if (!A.h_src) {
-          if (gi == 0) A.ctrl->ends_old[0] = d[r];
-          if (gi == T - 1) A.ctrl->ends_old[1] = d[r];
+    for (int k = 0; k < 6; k++) s_old[k * NT + tid] = v[k];  // reduced with the new ones at the end
+    if (edge && !A.h_src) {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        if ((core >> r) & 1) {
+          if (g0 + r == 0) A.ctrl->ends_old[0] = d[r];
+          if (g0 + r == T - 1) A.ctrl->ends_old[1] = d[r];
         }
       }
     }
-    v[0] = hold; v[1] = so[0]; v[2] = so[1]; v[3] = so[2]; v[4] = so[3]; v[5] = so[4];
-    block_sum<6>(v, reinterpret_cast<double(*)[6]>(&s_red[0][0]), lane, warp);
-    if (tid == 0) {
-      TilePart *tp = A.parts + blockIdx.x;
-      tp->hold = v[0];
-      for (int k = 0; k < 5; k++) tp->so[k] = v[k + 1];
-    }
   }
 
-  // ---- the trajectory ----
-  int bad = 0;
+  // ---- the trajectory: shuffles only, ghost lanes refreshed every R steps ----
+  RSV_STAMP(2);
+  unsigned nmax = 0;
   const int L = A.n_steps;
-  if (FUSE) {
-    if (warp_live) drift(d, p, s.c_half);
-  }
+  int parity = 0;
+  if (FUSE) drift(d, p, s.c_half);
   for (int step = 0; step < L; step++) {
-    const int b = (step + 1) & 1;
-    if (!FUSE && warp_live) drift(d, p, s.c_half);
-    double dl, dr;
-    exchange(d[0], d[TR_R - 1], dl, dr, s_first[b], s_last[b], lane, warp);
-    if (warp_live) {
-      if (edge) kick<true>(d, p, Ad, Cd, dl, dr, s, s_tab, live, endm, core, bad);
-      else kick<false>(d, p, Ad, Cd, dl, dr, s, s_tab, live, endm, core, bad);
-      if (FUSE) drift(d, p, step < L - 1 ? s.c_full : s.c_half);
-      else drift(d, p, s.c_half);
+    if (!FUSE) drift(d, p, s.c_half);
+    double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
+    double dr = __shfl_down_sync(0xffffffffu, d[0], 1);
+    if (lane == 0) dl = 0.0;   // window edges: stale ghosts, never read by core results
+    if (lane == 31) dr = 0.0;
+    if (edge) kick<true, R>(d, p, Ad, Cd, dl, dr, s, s_tab, live, endm, cm, nmax);
+    else if (any_live) kick<false, R>(d, p, Ad, Cd, dl, dr, s, s_tab, live, endm, cm, nmax);
+    if (FUSE) drift(d, p, step < L - 1 ? s.c_full : s.c_half);
+    else drift(d, p, s.c_half);
+    if (NW > 1 && (step + 1) % R == 0 && step + 1 < L) {
+      ghost_refresh<R, NT>(d, p, s_gx, lane, warp, parity);
+      parity ^= 1;
     }
   }
+  if (NW > 1) ghost_refresh<R, NT>(d, p, s_gx, lane, warp, parity);  // exact d_{i-1} for the energies
+  const bool bad = nmax > (unsigned)s.n_span;
+  RSV_STAMP(3);
 
   // ---- H_new, statistics of the proposal, write-back ----
   {
-    double dl, dr;
-    exchange(d[0], d[TR_R - 1], dl, dr, s_first[(L + 1) & 1], s_last[(L + 1) & 1], lane, warp);
-    double hnew = 0.0, sn[5] = {0, 0, 0, 0, 0};
+    // reload the static per-site data (L2-resident) rather than holding it
+    // in registers through the trajectory
+    if (full) {
 #pragma unroll
-    for (int r = 0; r < TR_R; r++) {
-      if ((core >> r) & 1) {
+      for (int r = 0; r < R; r += 2) {
+        const double2 a2 = __ldg(reinterpret_cast<const double2 *>(A.a + g0 + r));
+        const double2 l2 = __ldg(reinterpret_cast<const double2 *>(A.lrv + g0 + r));
+        av[r] = a2.x; av[r + 1] = a2.y;
+        lv[r] = l2.x; lv[r + 1] = l2.y;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
         const int64_t gi = g0 + r;
-        const double dprev = r ? d[r - 1] : dl;
-        const double ae = s.emu * A.a[gi];
-        const double q = A.lrv[gi] - s.xm;
-        const double e = q - d[r];
-        hnew += site_energy(d[r], dprev, p[r], ae, q, gi == 0, s, s_tab);
-        sn[0] += d[r];
-        sn[1] += d[r] * d[r];
-        if (gi > 0) sn[2] += d[r] * dprev;
-        sn[3] += e;
-        sn[4] += e * e;
-        hdst[gi] = d[r] + s.mu;
-        if (A.p_out) A.p_out[gi] = p[r];
-        if (!A.h_src) {
-          if (gi == 0) A.ctrl->ends_new[0] = d[r];
-          if (gi == T - 1) A.ctrl->ends_new[1] = d[r];
+        const bool in = gi >= lo_live && gi < hi_live;
+        av[r] = in ? A.a[gi] : 0.0;
+        lv[r] = in ? A.lrv[gi] : 0.0;
+      }
+    }
+    double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
+    double v[6] = {0, 0, 0, 0, 0, 0};
+    tile_energy<R>(d, p, av, lv, dl, core, edge, g0, s, s_tab, v);
+    const int64_t gi0 = g0;
+    if (full && core == (1u << R) - 1) {
+#pragma unroll
+      for (int r = 0; r < R; r += 2) {
+        *reinterpret_cast<double2 *>(hdst + gi0 + r) = make_double2(d[r] + s.mu, d[r + 1] + s.mu);
+        if (A.p_out) *reinterpret_cast<double2 *>(A.p_out + gi0 + r) = make_double2(p[r], p[r + 1]);
+      }
+    } else if (core) {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        if ((core >> r) & 1) {
+          hdst[gi0 + r] = d[r] + s.mu;
+          if (A.p_out) A.p_out[gi0 + r] = p[r];
         }
       }
     }
-    double v[8] = {hnew - hold, hnew, sn[0], sn[1], sn[2], sn[3], sn[4], (double)bad};
+    if (edge && !A.h_src) {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        if ((core >> r) & 1) {
+          if (g0 + r == 0) A.ctrl->ends_new[0] = d[r];
+          if (g0 + r == T - 1) A.ctrl->ends_new[1] = d[r];
+        }
+      }
+    }
+    double w[TR_NV];
+    w[0] = v[0] - hold;
+    w[1] = s_old[0 * NT + tid];
+    w[2] = v[0];
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+      w[3 + k] = s_old[(k + 1) * NT + tid];
+      w[8 + k] = v[1 + k];
+    }
+    w[13] = bad ? 1.0 : 0.0;
     __syncthreads();  // s_red reuse
-    block_sum<8>(v, reinterpret_cast<double(*)[8]>(&s_red[0][0]), lane, warp);
+    block_sum<TR_NV, NW>(w, s_red, lane, warp);
     if (tid == 0) {
       TilePart *tp = A.parts + blockIdx.x;
-      tp->dh = v[0];
-      tp->hnew = v[1];
-      for (int k = 0; k < 5; k++) tp->sn[k] = v[k + 2];
-      tp->flag = v[7];
+      tp->dh = w[0];
+      tp->hold = w[1];
+      tp->hnew = w[2];
+      for (int k = 0; k < 5; k++) {
+        tp->so[k] = w[3 + k];
+        tp->sn[k] = w[8 + k];
+      }
+      tp->flag = w[13];
+      __threadfence();
+      const unsigned done = atomicAdd(&A.ctrl->tiles_done, 1u);
+      s_last_tile = (done == (unsigned)gridDim.x - 1);
     }
   }
+  RSV_STAMP(4);
+  __syncthreads();
+  if (s_last_tile) {
+    __threadfence();
+    metropolis<NT>(A, s_v);
+    RSV_STAMP(5);
+  }
+  (void)s_first;
+  (void)s_last;
 }
 
-TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count) {
+struct TrajVariant {
+  int R, NT, MINB;
+};
+static const TrajVariant kVariants[] = {{8, 256, 2}, {4, 256, 3}, {4, 128, 6}, {8, 128, 4}, {16, 128, 2},
+                                        {2, 256, 4}, {8, 64, 8}, {4, 256, 2}, {8, 32, 16}};
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+
+int traj_num_variants() { return kNumVariants; }
+
+TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant) {
   TrajGeom g;
-  g.halo = n_steps + 1;
-  const int64_t core_max = TR_W - 2 * (int64_t)g.halo;
-  g.ok = core_max >= TR_W / 4;
+  if (variant < 0 || variant >= kNumVariants) variant = 0;
+  const TrajVariant v = kVariants[variant];
+  const int64_t NWv = v.NT / 32;
+  const int64_t W = NWv > 1 ? NWv * 30 * v.R + 2 * v.R : (int64_t)v.R * 32;  // CTA window (ghost lanes overlap)
+  g.variant = variant;
+  g.halo = (n_steps + 1 + v.R - 1) / v.R * v.R;
+  const int64_t core_max = (W - 2 * (int64_t)g.halo) / v.R * v.R;
+  g.ok = core_max >= W / 4;
   if (!g.ok) { g.core = 0; g.n_tiles = 0; return g; }
   int64_t n = (T + core_max - 1) / core_max;
-  const int64_t slots = 2LL * sm_count;
+  const int64_t slots = (int64_t)v.MINB * sm_count;
   if (n > slots / 2) n = (n + slots - 1) / slots * slots;
-  g.core = (T + n - 1) / n;
+  g.core = ((T + n - 1) / n + v.R - 1) / v.R * v.R;
   g.n_tiles = (int)((T + g.core - 1) / g.core);
   return g;
 }
 
+template <int R, int NT, int MINB>
+static void launch_v(const TrajArgs &a, cudaStream_t s) {
+  if (a.fuse) traj_kernel<R, NT, MINB, true><<<a.g.n_tiles, NT, 0, s>>>(a);
+  else traj_kernel<R, NT, MINB, false><<<a.g.n_tiles, NT, 0, s>>>(a);
+}
+
+const void *traj_kernel_fn(int variant, int fuse) {
+#define RSV_FN(R, NT, MB) (fuse ? (const void *)traj_kernel<R, NT, MB, true> : (const void *)traj_kernel<R, NT, MB, false>)
+  switch (variant) {
+    case 0: return RSV_FN(8, 256, 2);
+    case 1: return RSV_FN(4, 256, 3);
+    case 2: return RSV_FN(4, 128, 6);
+    case 3: return RSV_FN(8, 128, 4);
+    case 4: return RSV_FN(16, 128, 2);
+    case 5: return RSV_FN(2, 256, 4);
+    case 6: return RSV_FN(8, 64, 8);
+    case 7: return RSV_FN(4, 256, 2);
+    default: return RSV_FN(8, 32, 16);
+  }
+#undef RSV_FN
+}
+
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
-  if (a.fuse) traj_kernel<true><<<a.g.n_tiles, TR_NT, 0, s>>>(a);
-  else traj_kernel<false><<<a.g.n_tiles, TR_NT, 0, s>>>(a);
+  switch (a.g.variant) {
+    case 0: launch_v<8, 256, 2>(a, s); break;
+    case 1: launch_v<4, 256, 3>(a, s); break;
+    case 2: launch_v<4, 128, 6>(a, s); break;
+    case 3: launch_v<8, 128, 4>(a, s); break;
+    case 4: launch_v<16, 128, 2>(a, s); break;
+    case 5: launch_v<2, 256, 4>(a, s); break;
+    case 6: launch_v<8, 64, 8>(a, s); break;
+    case 7: launch_v<4, 256, 2>(a, s); break;
+    default: launch_v<8, 32, 16>(a, s); break;
+  }
   (*launches)++;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 // ---------------------------------------------------------------------------
 // Metropolis (sampler.py:155-167) on the reduced tile partials.
-constexpr int AC_NT = 256;
-__global__ void __launch_bounds__(AC_NT) accept_kernel(AcceptArgs A) {
-  __shared__ double s_v[AC_NT][TR_NV];
+template <int NT>
+__device__ void metropolis(const TrajArgs &A, double *s_v) {
+  constexpr int NW = NT / 32;
   double v[TR_NV];
 #pragma unroll
   for (int k = 0; k < TR_NV; k++) v[k] = 0.0;
-  for (int i = threadIdx.x; i < A.n_tiles; i += AC_NT) {
+  const int n_tiles = A.g.n_tiles;
+  for (int i = threadIdx.x; i < n_tiles; i += NT) {
     const TilePart &tp = A.parts[i];
     v[0] += tp.dh; v[1] += tp.hold; v[2] += tp.hnew;
 #pragma unroll
     for (int k = 0; k < 5; k++) { v[3 + k] += tp.so[k]; v[8 + k] += tp.sn[k]; }
     v[13] += tp.flag;
   }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k < TR_NV; k++) s_v[threadIdx.x][k] = v[k];
-  __syncthreads();
-  for (int w = AC_NT / 2; w >= 1; w >>= 1) {
-    if (threadIdx.x < w) {
+  for (int k = 0; k < TR_NV; k++) {
 #pragma unroll
-      for (int k = 0; k < TR_NV; k++) s_v[threadIdx.x][k] += s_v[threadIdx.x + w][k];
-    }
-    __syncthreads();
+    for (int o = 16; o >= 1; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
   }
+  if (lane == 0)
+    for (int k = 0; k < TR_NV; k++) s_v[warp * TR_NV + k] = v[k];
+  __syncthreads();
   if (threadIdx.x) return;
-  const DevParams P = *A.prm;
+  double tot[TR_NV];
+  for (int k = 0; k < TR_NV; k++) {
+    double acc = s_v[k];
+    for (int w = 1; w < NW; w++) acc += s_v[w * TR_NV + k];
+    tot[k] = acc;
+  }
   DevControl *C = A.ctrl;
-  const double Td = (double)A.T;
-  const double cst = 0.5 * Td * P.mu + 0.5 * Td * log(P.su2) + 0.5 * log(P.se2 / (1.0 - P.phi * P.phi)) +
-                     0.5 * (Td - 1.0) * log(P.se2);
-  const double *tot = s_v[0];
+  C->tiles_done = 0;  // re-arm for the next launch
+  const double cst = A.k.hconst;
   DevResult r;
   r.h_old = tot[1] + cst;
   r.h_new = tot[2] + cst;
@@ -368,27 +564,20 @@ __global__ void __launch_bounds__(AC_NT) accept_kernel(AcceptArgs A) {
     r.diverged = flagged;
     r.delta_h = tot[0];
     C->res = r;
-    if (A.res_out) *A.res_out = r;
     return;
   }
-  uint64_t used = C->zig_used;
+  const uint64_t used = C->zig_used;
   bool drew = false;
-  if (flagged) {
+  const double dh = tot[0];
+  if (flagged || !isfinite(dh) || fabs(dh) > 1000.0) {
     r.diverged = 1;
     r.delta_h = __longlong_as_double(0x7ff0000000000000LL);
   } else {
-    const double dh = tot[0];
-    if (!isfinite(dh) || fabs(dh) > 1000.0) {
-      r.diverged = 1;
-      r.delta_h = __longlong_as_double(0x7ff0000000000000LL);
-    } else {
-      r.diverged = 0;
-      r.delta_h = dh;
-      const uint64_t w = C->stream.kind == PRNG_SFC64 ? A.sfc_words[used] : word_at(C->stream, C->stream.pos + used);
-      r.u = u01(w);
-      drew = true;
-      r.accept = (dh <= 0.0) || (r.u < exp(-dh));
-    }
+    r.diverged = 0;
+    r.delta_h = dh;
+    r.u = u01(C->u_word);  // raw word at stream position pos0 + used (momenta kernel)
+    drew = true;
+    r.accept = (dh <= 0.0) || (r.u < exp(-dh));
   }
   const uint64_t consumed = used + (drew ? 1 : 0);
   r.words_used = consumed;
@@ -400,19 +589,11 @@ __global__ void __launch_bounds__(AC_NT) accept_kernel(AcceptArgs A) {
   }
   C->stream.pos += consumed;
   if (r.accept) C->cur ^= 1;
-  // statistics of the kept path, shifted by (mu, xi) of the params used
   const double *sm = r.accept ? tot + 8 : tot + 3;
   C->stats[0] = r.accept ? C->ends_new[0] : C->ends_old[0];
   C->stats[1] = r.accept ? C->ends_new[1] : C->ends_old[1];
   for (int k = 0; k < 5; k++) C->stats[2 + k] = sm[k];
   C->res = r;
-  if (A.res_out) *A.res_out = r;
-}
-
-int launch_accept(const AcceptArgs &a, cudaStream_t s, int *launches) {
-  accept_kernel<<<1, AC_NT, 0, s>>>(a);
-  (*launches)++;
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 // ---------------------------------------------------------------------------

@@ -1,27 +1,29 @@
-// momenta.cu -- bit-exact numpy momenta on the GPU.
+// momenta.cu -- bit-exact numpy momenta on the GPU, one kernel per draw.
 //
-// Replaces sampler.py:136-141 refresh_momenta = rng.standard_normal(T) with
+// Replaces sampler.py:136-141 refresh_momenta = rng.standard_normal(T):
 // numpy's 256-layer ziggurat (random_standard_normal, numpy 2.3.5).  A
-// ziggurat draw consumes a variable number of raw words (1 for the 98.9 %
+// ziggurat draw consumes a variable number of raw words (1 on the 98.9 %
 // fast path, 2 for a wedge test, 1 + 2m for m exponential-tail loops), so
-// normal i's position in the raw stream depends on every earlier draw.  We
-// parse that in parallel:
+// normal i's place in the raw stream depends on every earlier draw.
 //
-//   Z1  every raw word k is classified as if an attempt started there:
-//       (len_k, acc_k, x_k).  The parse is the automaton over states
-//       s in {0..15} = "words still owed to the running attempt"; word k
-//       maps s=0 -> len_k - 1 and s>0 -> s-1, emitting x_k when s=0 and
-//       acc_k.  Each thread summarises its 8 words as a map
-//       (exit state, #normals) for all 16 entry states by a backward DP;
-//       blocks compose the 256 thread maps in a shared-memory tree.
-//   Z2  one CTA scans the block maps from state 0 -> each block's entry
-//       state and output offset.
-//   Z3  each block re-derives its thread maps, runs the tree down from its
-//       entry state and writes its normals to their global slots; the
-//       thread that emits normal T-1 records how many words were used.
-//
-// Attempts needing more than ZMMAX tail loops (p ~ 1e-12 per word) set a
-// flag and Z3 falls back to a serial walk, so results stay exact.
+// zig_kernel parses the stream in parallel with *speculation + local
+// verification*:
+//   1. a CTA owns 2048 raw words (8 per thread) and stages them, plus a
+//      16-word guard before and 32 look-ahead words after, in shared memory;
+//   2. every word k is classified as if an attempt started there:
+//      (len_k, acc_k, x_k);
+//   3. each thread assumes the parse is "in sync" 16 words before its
+//      segment (state 0 there) and walks forward to its segment: the
+//      attempt chains of a ziggurat stream merge within a few words, so the
+//      entry state it finds is the true one -- and it is *checked*: it must
+//      equal the exit state of the previous thread's walk (and, for thread 0,
+//      of the previous CTA).  By induction from word 0 every entry is exact;
+//      any mismatch (p ~ 1e-30) or an attempt needing > 7 tail loops
+//      (p ~ 1e-12 per word) diverts the draw to an exact serial walk;
+//   4. per-thread normal counts are scanned in the CTA and across CTAs by a
+//      decoupled look-back (single pass), and the normals are written to
+//      their final slots.  The thread that emits normal T-1 records how many
+//      words the draw used and the next raw word (the Metropolis uniform).
 #include <math.h>
 
 #include "rsv_internal.h"
@@ -33,31 +35,62 @@ __device__ const uint64_t g_ki[256] = RSV_KI_DOUBLE_INIT;
 __device__ const double g_wi[256] = RSV_WI_DOUBLE_INIT;
 __device__ const double g_fi[256] = RSV_FI_DOUBLE_INIT;
 
-struct ZigTables {
-  uint64_t ki[256];
-  double wi[256];
-};
+constexpr int ZG = 16;                 // guard words before a CTA's block
+constexpr int ZLA = 32;                // look-ahead words after it
+constexpr int ZSW = ZG + ZB + ZLA;     // staged words per CTA
+constexpr int ZCH = ZSW / ZW;          // 8-word chunks per CTA (262)
 
-__device__ __forceinline__ uint64_t look_word(const StreamState &st, const uint64_t *words, uint64_t pos0, uint64_t j) {
-  return words ? words[j] : word_at(st, pos0 + j);
+struct ZigJump {  // per-chunk jump-ahead constants (inc-free), built once
+  uint64_t pcg_a[ZCH], pcg_g[ZCH];     // state_c = a * base + inc * g  (16 c outputs ahead)
+  uint64_t minstd_a[ZCH];              // x_c = a * x_base mod m        (24 c outputs ahead)
+};
+__device__ ZigJump g_jump;
+
+__global__ void zig_jump_init_kernel() {
+  if (threadIdx.x || blockIdx.x) return;
+  // pcg: 16 outputs per chunk; accumulate (A^k, G_k) with G_k = sum_{i<k} A^i
+  uint64_t a = 1, g = 0;
+  uint64_t A16 = 1, G16 = 0;
+  for (int i = 0; i < 16; i++) { G16 = G16 * PCG_MULT + 1; A16 *= PCG_MULT; }
+  uint64_t m = 1, m24 = minstd_pow(24);
+  for (int c = 0; c < ZCH; c++) {
+    g_jump.pcg_a[c] = a;
+    g_jump.pcg_g[c] = g;
+    g_jump.minstd_a[c] = m;
+    g = g * A16 + G16;  // (A^k,G_k) o (A^16,G_16)
+    a *= A16;
+    m = mod31(m * m24);
+  }
 }
 
-// Classify raw word j (relative to the draw's first word) as the first word
-// of an attempt of numpy's random_standard_normal.
-__device__ __forceinline__ void zig_classify(uint64_t r, uint64_t j, const StreamState &st, const uint64_t *words,
-                                             uint64_t pos0, const uint64_t *ki, const double *wi, int mmax,
-                                             int &len, int &acc, double &x) {
+struct ZigShared {
+  uint64_t w[ZSW];        // raw words: local index i <-> draw word b*ZB - ZG + i
+  double x[ZB];           // candidate normal of an attempt starting at block word k
+  uint8_t len[ZG + ZB];   // attempt length | acc << 7 for guard + block words
+  uint64_t ki[256];
+  double wi[256];
+  int32_t warp_tot[ZT / 32];
+  int32_t warp_exit[ZT / 32];
+  uint64_t base_a, base_b;  // sequential-generator state at local word 0
+  uint64_t blk_off;         // exclusive normal offset of this CTA
+  int32_t blk;              // dynamic CTA index (ticket)
+  int32_t bad;
+};
+
+// Classify the attempt starting at local word i (numpy random_standard_normal).
+__device__ __forceinline__ void zig_classify_at(const ZigShared &S, int i, int mmax, int &len, int &acc, double &x) {
+  uint64_t r = S.w[i];
   const int idx = (int)(r & 0xff);
   r >>= 8;
   const int sign = (int)(r & 0x1);
   const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-  x = __dmul_rn((double)rabs, wi[idx]);
+  x = __dmul_rn((double)rabs, S.wi[idx]);
   if (sign) x = -x;
-  if (rabs < ki[idx]) { len = 1; acc = 1; return; }
+  if (rabs < S.ki[idx]) { len = 1; acc = 1; return; }
   if (idx == 0) {
     for (int m = 1; m <= mmax; m++) {
-      const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, glibc_log1p(-u01(look_word(st, words, pos0, j + 2 * m - 1))));
-      const double yy = -glibc_log1p(-u01(look_word(st, words, pos0, j + 2 * m)));
+      const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, glibc_log1p(-u01(S.w[i + 2 * m - 1])));
+      const double yy = -glibc_log1p(-u01(S.w[i + 2 * m]));
       if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
         x = ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
         len = 1 + 2 * m;
@@ -65,67 +98,246 @@ __device__ __forceinline__ void zig_classify(uint64_t r, uint64_t j, const Strea
         return;
       }
     }
-    len = 0;  // overflow: resolved by the serial fallback
+    len = 0;  // needs more tail loops than staged words: exact serial fallback
     acc = 0;
     return;
   }
-  const double u = u01(look_word(st, words, pos0, j + 1));
+  const double u = u01(S.w[i + 1]);
   const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(g_fi[idx - 1], g_fi[idx]), u), g_fi[idx]);
   acc = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x)) ? 1 : 0;
   len = 2;
 }
 
-// Parse element over entry states 0..15: exit state (nibbles) + counts.
-template <typename C>
-struct ZElem {
-  uint64_t exit;
-  C cnt[ZS];
-};
-
-template <typename C, typename D>
-__device__ __forceinline__ void zcompose(const ZElem<C> &f, const ZElem<D> &g, ZElem<C> &out) {
-  uint64_t ex = 0;
-  C cn[ZS];
-#pragma unroll
-  for (int e = 0; e < ZS; e++) {
-    const int m = (int)((f.exit >> (4 * e)) & 15);
-    ex |= ((g.exit >> (4 * m)) & 15ULL) << (4 * e);
-    cn[e] = (C)(f.cnt[e] + (C)g.cnt[m]);
-  }
-  out.exit = ex;
-#pragma unroll
-  for (int e = 0; e < ZS; e++) out.cnt[e] = cn[e];
+// decoupled look-back status word: [63:62] flag (1 aggregate, 2 prefix),
+// [61:58] exit state of the CTA's parse, [57:0] normal count
+__device__ __forceinline__ uint64_t zpack(int flag, int exitst, uint64_t cnt) {
+  return ((uint64_t)flag << 62) | ((uint64_t)exitst << 58) | cnt;
 }
 
-// Thread-level element from 8 (len, acc) pairs packed as nibbles / bits.
-__device__ __forceinline__ void zthread_elem(uint32_t lens, uint32_t accs, ZElem<uint16_t> &el) {
-  uint32_t exp_ = 0, cnp = 0;
-#pragma unroll
-  for (int p = ZW - 1; p >= 0; p--) {
-    const int L = (int)((lens >> (4 * p)) & 15);
-    const int a = (int)((accs >> p) & 1);
-    const int nx = p + (L ? L : 1);
-    int ex, cn;
-    if (nx >= ZW) { ex = nx - ZW; cn = a; }
-    else { ex = (int)((exp_ >> (4 * nx)) & 15); cn = a + (int)((cnp >> (4 * nx)) & 15); }
-    exp_ |= (uint32_t)ex << (4 * p);
-    cnp |= (uint32_t)cn << (4 * p);
+template <int KIND>
+__device__ __forceinline__ void stage_words(ZigShared &S, const DevControl *ctrl, const uint64_t *words, int b,
+                                            int64_t nwords_buf) {
+  const int tid = threadIdx.x;
+  const int64_t rel0 = (int64_t)b * ZB - ZG;  // draw-relative index of local word 0
+  if (KIND == PRNG_SFC64) {
+    for (int i = tid; i < ZSW; i += ZT) {
+      const int64_t k = rel0 + i;
+      S.w[i] = (k >= 0 && k < nwords_buf) ? words[k] : 0;
+    }
+    return;
   }
-  uint64_t ex = 0;
-#pragma unroll
-  for (int e = 0; e < ZS; e++) {
-    const uint64_t v = e < ZW ? ((exp_ >> (4 * e)) & 15) : (uint64_t)(e - ZW);
-    ex |= v << (4 * e);
-    el.cnt[e] = e < ZW ? (uint16_t)((cnp >> (4 * e)) & 15) : (uint16_t)0;
+  const StreamState &st = ctrl->stream;
+  if (tid == 0) {
+    // state in front of local word 0 (draw word rel0 may be negative for CTA 0:
+    // the guard is never walked there, start the jump at word 0 and shift)
+    const uint64_t k = st.pos + (uint64_t)(rel0 < 0 ? 0 : rel0);
+    if (KIND == PRNG_PCG32) S.base_a = pcg_advance(st.s[0], 2 * k, st.s[1]);
+    else if (KIND == PRNG_MINSTD) S.base_a = mod31(minstd_pow(3 * k) * st.s[0]);
   }
-  el.exit = ex;
+  __syncthreads();
+  const int shift = rel0 < 0 ? ZG : 0;  // CTA 0: local word ZG is draw word 0
+  for (int c = tid; c < ZCH; c += ZT) {
+    const int i0 = c * ZW;
+    if (i0 + ZW <= shift) {  // pure guard chunk of CTA 0: no words there
+      for (int i = 0; i < ZW; i++) S.w[i0 + i] = 0;
+    } else if (KIND == PRNG_PHILOX) {
+      SeqGen g;
+      g.init(st, st.pos + (uint64_t)(rel0 + i0));
+#pragma unroll
+      for (int i = 0; i < ZW; i++) S.w[i0 + i] = g.next();
+    } else if (KIND == PRNG_PCG32) {
+      const int cc = c - shift / ZW;
+      uint64_t s0 = g_jump.pcg_a[cc] * S.base_a + st.s[1] * g_jump.pcg_g[cc];
+#pragma unroll
+      for (int i = 0; i < ZW; i++) {
+        const uint64_t s1 = s0 * PCG_MULT + st.s[1];
+        S.w[i0 + i] = ((uint64_t)pcg_output(s0) << 32) | pcg_output(s1);
+        s0 = s1 * PCG_MULT + st.s[1];
+      }
+    } else {  // MINSTD
+      const int cc = c - shift / ZW;
+      uint64_t x = mod31(g_jump.minstd_a[cc] * S.base_a);
+#pragma unroll
+      for (int i = 0; i < ZW; i++) {
+        const uint64_t xa = mod31(x * MINSTD_A), xb = mod31(xa * MINSTD_A), xc = mod31(xb * MINSTD_A);
+        x = xc;
+        S.w[i0 + i] = (xa << 33) | (xb << 2) | (xc >> 29);
+      }
+    }
+  }
 }
 
-__device__ __forceinline__ void load_tables(ZigTables &t) {
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    t.ki[i] = g_ki[i];
-    t.wi[i] = g_wi[i];
+template <int KIND>
+__global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_t *words, int64_t nwords_buf,
+                                                 double *normals, int64_t T, uint64_t *status, uint32_t *ticket) {
+  extern __shared__ __align__(16) unsigned char zsmem[];
+  ZigShared &S = *reinterpret_cast<ZigShared *>(zsmem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    S.blk = (int)atomicAdd(ticket, 1u);
+    S.bad = 0;
   }
+  for (int i = tid; i < 256; i += ZT) {
+    S.ki[i] = g_ki[i];
+    S.wi[i] = g_wi[i];
+  }
+  __syncthreads();
+  const int b = S.blk;
+  stage_words<KIND>(S, ctrl, words, b, nwords_buf);
+  __syncthreads();
+
+  // ---- classify every guard + block word as an attempt start
+  const int first = (b == 0) ? ZG : 0;  // CTA 0 has no guard
+  int ovf = 0;
+  for (int i = tid; i < ZG + ZB; i += ZT) {
+    if (i < first) { S.len[i] = 1; continue; }
+    int len, acc;
+    double x;
+    zig_classify_at(S, i, ZMMAX, len, acc, x);
+    S.len[i] = (uint8_t)(len | (acc << 7));
+    if (i >= ZG) S.x[i - ZG] = x;
+    ovf |= (len == 0);
+  }
+  if (ovf) atomicOr(&ctrl->zig_overflow, 1);
+  __syncthreads();
+
+  // ---- speculative walk: in sync 16 words before my segment
+  const int seg = ZG + tid * ZW;
+  int pos = (b == 0 && tid == 0) ? ZG : seg - ZG;
+  while (pos < seg) {
+    const int L = S.len[pos] & 15;
+    pos += L ? L : 1;
+  }
+  const int entry = pos - seg;
+  int cnt = 0;
+  while (pos < seg + ZW) {
+    const uint8_t m = S.len[pos];
+    cnt += m >> 7;
+    const int L = m & 15;
+    pos += L ? L : 1;
+  }
+  const int exitst = pos - (seg + ZW);
+  // verify: my entry == previous thread's exit
+  int prev_exit = __shfl_up_sync(0xffffffffu, exitst, 1);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) {
+    S.warp_tot[warp] = incl;
+    S.warp_exit[warp] = exitst;
+  }
+  __syncthreads();
+  if (lane == 0 && warp > 0) prev_exit = S.warp_exit[warp - 1];
+  if (tid > 0 && prev_exit != entry) S.bad = 1;
+  int woff = 0, btot = 0;
+  for (int w = 0; w < ZT / 32; w++) {
+    if (w < warp) woff += S.warp_tot[w];
+    btot += S.warp_tot[w];
+  }
+  const int toff = woff + incl - cnt;  // exclusive offset of my normals in the CTA
+
+  // ---- decoupled look-back over CTAs for the global normal offset
+  if (tid == 0) {
+    const int bexit = S.warp_exit[ZT / 32 - 1];
+    volatile uint64_t *vst = status;
+    if (b == 0) {
+      __threadfence();
+      vst[0] = zpack(2, bexit, (uint64_t)btot);
+      S.blk_off = 0;
+      if (entry != 0) S.bad = 1;
+    } else {
+      vst[b] = zpack(1, bexit, (uint64_t)btot);
+      __threadfence();
+      uint64_t acc = 0;
+      int j = b - 1;
+      // the previous CTA's exit must match my thread 0's speculative entry
+      uint64_t sv;
+      while (((sv = vst[j]) >> 62) == 0) {}
+      if ((int)((sv >> 58) & 15) != entry) S.bad = 1;
+      for (;;) {
+        const int f = (int)(sv >> 62);
+        acc += sv & ((1ULL << 58) - 1);
+        if (f == 2) break;
+        j--;
+        while (((sv = vst[j]) >> 62) == 0) {}
+      }
+      S.blk_off = acc;
+      __threadfence();
+      vst[b] = zpack(2, bexit, acc + (uint64_t)btot);
+    }
+    if (S.bad) atomicOr(&ctrl->zig_overflow, 2);
+  }
+  __syncthreads();
+
+  // ---- write my normals to their final slots
+  uint64_t off = S.blk_off + (uint64_t)toff;
+  pos = seg + entry;
+  if (off < (uint64_t)T) {
+    while (pos < seg + ZW) {
+      const uint8_t m = S.len[pos];
+      const int L = m & 15;
+      if (m >> 7) {
+        if (off < (uint64_t)T) normals[off] = S.x[pos - ZG];
+        if (off == (uint64_t)T - 1) {
+          const int nxt = pos + L;  // local index of the next unread word
+          ctrl->zig_used = (uint64_t)((int64_t)b * ZB - ZG + nxt);
+          ctrl->u_word = S.w[nxt];
+        }
+        off++;
+      }
+      pos += L ? L : 1;
+    }
+  }
+  // the last CTA publishes how many normals the parse produced
+  if (tid == ZT - 1 && b == (int)gridDim.x - 1) ctrl->zig_avail = S.blk_off + (uint64_t)btot;
+}
+
+// Exact serial walk of the whole draw (fallback; normally exits at once).
+__device__ uint64_t serial_word(const StreamState &st, const uint64_t *words, int64_t nbuf, uint64_t j) {
+  if (st.kind == PRNG_SFC64) return j < (uint64_t)nbuf ? words[j] : 0;
+  return word_at(st, st.pos + j);
+}
+
+__global__ void zig_fallback_kernel(DevControl *ctrl, const uint64_t *words, int64_t nbuf, double *normals,
+                                    int64_t T) {
+  if (threadIdx.x || blockIdx.x) return;
+  if (ctrl->zig_overflow == 0 && ctrl->zig_avail >= (uint64_t)T) return;
+  const StreamState st = ctrl->stream;
+  uint64_t j = 0;
+  for (int64_t i = 0; i < T;) {
+    uint64_t r = serial_word(st, words, nbuf, j);
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 0x1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double x = __dmul_rn((double)rabs, g_wi[idx]);
+    if (sign) x = -x;
+    j++;
+    if (rabs < g_ki[idx]) { normals[i++] = x; continue; }
+    if (idx == 0) {
+      for (;;) {
+        const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, glibc_log1p(-u01(serial_word(st, words, nbuf, j))));
+        const double yy = -glibc_log1p(-u01(serial_word(st, words, nbuf, j + 1)));
+        j += 2;
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+          normals[i++] = ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
+          break;
+        }
+      }
+    } else {
+      const double u = u01(serial_word(st, words, nbuf, j));
+      j++;
+      const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(g_fi[idx - 1], g_fi[idx]), u), g_fi[idx]);
+      if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) normals[i++] = x;
+    }
+  }
+  ctrl->zig_used = j;
+  ctrl->u_word = serial_word(st, words, nbuf, j);
+  ctrl->zig_avail = (uint64_t)T;
+  ctrl->err |= 2;
 }
 
 // Z0: sequential SFC64 words (no jump-ahead exists) + state snapshots.
@@ -138,202 +350,6 @@ __global__ void z0_sfc64_kernel(DevControl *ctrl, uint64_t *words, uint64_t *sna
       q[0] = s[0]; q[1] = s[1]; q[2] = s[2]; q[3] = s[3];
     }
     words[i] = sfc64_next(s);
-  }
-}
-
-// Z1: classify words [0, nb*ZB) of the draw, block maps -> agg.
-__global__ void __launch_bounds__(ZT) z1_kernel(DevControl *ctrl, const uint64_t *words, double *xs,
-                                                uint8_t *meta, ZElem<uint16_t> *agg) {
-  __shared__ ZigTables tab;
-  __shared__ ZElem<uint16_t> nodes[2 * ZT];
-  load_tables(tab);
-  const StreamState st = ctrl->stream;
-  const uint64_t pos0 = st.pos;
-  const uint64_t j0 = ((uint64_t)blockIdx.x * ZT + threadIdx.x) * ZW;
-  uint64_t w[ZW];
-  if (words) {
-#pragma unroll
-    for (int i = 0; i < ZW; i++) w[i] = words[j0 + i];
-  } else {
-    SeqGen g;
-    g.init(st, pos0 + j0);
-#pragma unroll
-    for (int i = 0; i < ZW; i++) w[i] = g.next();
-  }
-  __syncthreads();
-  uint32_t lens = 0, accs = 0;
-  uint64_t m8 = 0;
-  int ovf = 0;
-  double xv[ZW];
-#pragma unroll
-  for (int i = 0; i < ZW; i++) {
-    int len, acc;
-    zig_classify(w[i], j0 + i, st, words, pos0, tab.ki, tab.wi, ZMMAX, len, acc, xv[i]);
-    lens |= (uint32_t)len << (4 * i);
-    accs |= (uint32_t)acc << i;
-    m8 |= (uint64_t)(len | (acc << 7)) << (8 * i);
-    ovf |= (len == 0);
-  }
-  *reinterpret_cast<uint64_t *>(meta + j0) = m8;
-#pragma unroll
-  for (int i = 0; i < ZW; i += 2) *reinterpret_cast<double2 *>(xs + j0 + i) = make_double2(xv[i], xv[i + 1]);
-  if (ovf) atomicExch(&ctrl->zig_overflow, 1);
-  ZElem<uint16_t> el;
-  zthread_elem(lens, accs, el);
-  nodes[ZT + threadIdx.x] = el;
-  __syncthreads();
-  for (int width = ZT / 2; width >= 1; width >>= 1) {
-    if (threadIdx.x < width) {
-      const int i = width + threadIdx.x;
-      ZElem<uint16_t> o;
-      zcompose(nodes[2 * i], nodes[2 * i + 1], o);
-      nodes[i] = o;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) agg[blockIdx.x] = nodes[1];
-}
-
-struct ZEntry {
-  uint32_t state;
-  uint32_t pad;
-  uint64_t offset;
-};
-
-// Z2: scan block maps from (state 0, offset 0) -> per-block entries.
-__global__ void __launch_bounds__(Z2T) z2_kernel(DevControl *ctrl, const ZElem<uint16_t> *agg, ZEntry *entries,
-                                                 int nb) {
-  __shared__ ZElem<uint32_t> nodes[2 * Z2T];
-  __shared__ uint32_t in_state[2 * Z2T];
-  __shared__ uint64_t in_off[2 * Z2T];
-  const int per = (nb + Z2T - 1) / Z2T;
-  const int b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
-  ZElem<uint32_t> el;
-  el.exit = 0xFEDCBA9876543210ULL;  // identity
-#pragma unroll
-  for (int e = 0; e < ZS; e++) el.cnt[e] = 0;
-  for (int b = b0; b < b1; b++) {
-    ZElem<uint16_t> g = agg[b];
-    zcompose(el, g, el);
-  }
-  nodes[Z2T + threadIdx.x] = el;
-  __syncthreads();
-  for (int width = Z2T / 2; width >= 1; width >>= 1) {
-    if (threadIdx.x < width) {
-      const int i = width + threadIdx.x;
-      ZElem<uint32_t> o;
-      zcompose(nodes[2 * i], nodes[2 * i + 1], o);
-      nodes[i] = o;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) { in_state[1] = 0; in_off[1] = 0; }
-  __syncthreads();
-  for (int width = 1; width < Z2T; width <<= 1) {
-    if (threadIdx.x < width) {
-      const int i = width + threadIdx.x;
-      const uint32_t s = in_state[i];
-      const uint64_t o = in_off[i];
-      in_state[2 * i] = s;
-      in_off[2 * i] = o;
-      in_state[2 * i + 1] = (uint32_t)((nodes[2 * i].exit >> (4 * s)) & 15);
-      in_off[2 * i + 1] = o + nodes[2 * i].cnt[s];
-    }
-    __syncthreads();
-  }
-  uint32_t s = in_state[Z2T + threadIdx.x];
-  uint64_t o = in_off[Z2T + threadIdx.x];
-  for (int b = b0; b < b1; b++) {
-    entries[b].state = s;
-    entries[b].offset = o;
-    const ZElem<uint16_t> &g = agg[b];
-    o += g.cnt[s];
-    s = (uint32_t)((g.exit >> (4 * s)) & 15);
-  }
-  if (threadIdx.x == Z2T - 1) ctrl->zig_avail = o;
-}
-
-// Serial walk of the whole draw (exact fallback for parse overflow).
-__device__ void zig_serial(DevControl *ctrl, const uint64_t *words, double *normals, int64_t T) {
-  const StreamState st = ctrl->stream;
-  uint64_t j = 0;
-  for (int64_t i = 0; i < T;) {
-    int len, acc;
-    double x;
-    const uint64_t r = words ? words[j] : word_at(st, st.pos + j);
-    zig_classify(r, j, st, words, st.pos, g_ki, g_wi, 1 << 20, len, acc, x);
-    if (acc) normals[i++] = x;
-    j += (uint64_t)len;
-  }
-  ctrl->zig_used = j;
-  ctrl->zig_avail = (uint64_t)T;
-}
-
-// Z3: emit normals.
-__global__ void __launch_bounds__(ZT) z3_kernel(DevControl *ctrl, const uint64_t *words, const double *xs,
-                                                const uint8_t *meta, const ZEntry *entries, double *normals,
-                                                int64_t T) {
-  __shared__ ZElem<uint16_t> nodes[2 * ZT];
-  __shared__ uint8_t in_state[2 * ZT];
-  __shared__ uint32_t in_off[2 * ZT];
-  if (ctrl->zig_overflow) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      zig_serial(ctrl, words, normals, T);
-      ctrl->err |= 2;
-    }
-    return;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && ctrl->zig_avail < (uint64_t)T) ctrl->err |= 1;
-  const uint64_t j0 = ((uint64_t)blockIdx.x * ZT + threadIdx.x) * ZW;
-  const uint64_t m8 = *reinterpret_cast<const uint64_t *>(meta + j0);
-  uint32_t lens = 0, accs = 0;
-#pragma unroll
-  for (int i = 0; i < ZW; i++) {
-    const uint32_t m = (uint32_t)((m8 >> (8 * i)) & 0xff);
-    lens |= (m & 15u) << (4 * i);
-    accs |= (m >> 7) << i;
-  }
-  ZElem<uint16_t> el;
-  zthread_elem(lens, accs, el);
-  nodes[ZT + threadIdx.x] = el;
-  __syncthreads();
-  for (int width = ZT / 2; width >= 1; width >>= 1) {
-    if (threadIdx.x < width) {
-      const int i = width + threadIdx.x;
-      ZElem<uint16_t> o;
-      zcompose(nodes[2 * i], nodes[2 * i + 1], o);
-      nodes[i] = o;
-    }
-    __syncthreads();
-  }
-  const ZEntry be = entries[blockIdx.x];
-  if (threadIdx.x == 0) { in_state[1] = (uint8_t)be.state; in_off[1] = 0; }
-  __syncthreads();
-  for (int width = 1; width < ZT; width <<= 1) {
-    if (threadIdx.x < width) {
-      const int i = width + threadIdx.x;
-      const uint32_t s = in_state[i];
-      const uint32_t o = in_off[i];
-      in_state[2 * i] = (uint8_t)s;
-      in_off[2 * i] = o;
-      in_state[2 * i + 1] = (uint8_t)((nodes[2 * i].exit >> (4 * s)) & 15);
-      in_off[2 * i + 1] = o + nodes[2 * i].cnt[s];
-    }
-    __syncthreads();
-  }
-  int pos = in_state[ZT + threadIdx.x];
-  uint64_t off = be.offset + in_off[ZT + threadIdx.x];
-  if (off >= (uint64_t)T) return;
-  while (pos < ZW) {
-    const int L = (int)((lens >> (4 * pos)) & 15);
-    if ((accs >> pos) & 1) {
-      if (off < (uint64_t)T) {
-        normals[off] = xs[j0 + pos];
-        if (off == (uint64_t)T - 1) ctrl->zig_used = j0 + pos + L;
-      }
-      off++;
-    }
-    pos += L;
   }
 }
 
@@ -357,29 +373,50 @@ int64_t momenta_words(int64_t T) {
 }
 
 size_t momenta_scratch_bytes(int64_t T) {
-  const int64_t N = momenta_words(T), nb = N / ZB;
-  return (size_t)N * 8 + (size_t)N + (size_t)nb * sizeof(ZElem<uint16_t>) + (size_t)nb * sizeof(ZEntry) + 256;
+  const int64_t nb = momenta_words(T) / ZB;
+  return (size_t)(nb + 2) * sizeof(uint64_t) + 64;
+}
+
+int momenta_init(cudaStream_t s) {
+  zig_jump_init_kernel<<<1, 1, 0, s>>>();
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, int *launches) {
   const int64_t N = momenta_words(T);
   const int nb = (int)(N / ZB);
-  char *base = (char *)b.scratch;
-  double *xs = (double *)base;
-  uint8_t *meta = (uint8_t *)(base + (size_t)N * 8);
-  ZElem<uint16_t> *agg = (ZElem<uint16_t> *)(base + (size_t)N * 9);
-  ZEntry *entries = (ZEntry *)(base + (size_t)N * 9 + (size_t)nb * sizeof(ZElem<uint16_t>));
-  const uint64_t *words = nullptr;
+  uint64_t *status = (uint64_t *)b.scratch;
+  uint32_t *ticket = (uint32_t *)(status + nb);
   cudaMemsetAsync(&b.ctrl->zig_overflow, 0, sizeof(int32_t), s);
+  cudaMemsetAsync(status, 0, (size_t)(nb + 2) * sizeof(uint64_t), s);
+  const uint64_t *words = nullptr;
+  const int64_t nbuf = N + 64;
   if (kind == PRNG_SFC64) {
-    z0_sfc64_kernel<<<1, 1, 0, s>>>(b.ctrl, b.sfc_words, b.sfc_snaps, N + 64);
+    z0_sfc64_kernel<<<1, 1, 0, s>>>(b.ctrl, b.sfc_words, b.sfc_snaps, nbuf);
     words = b.sfc_words;
     (*launches)++;
   }
-  z1_kernel<<<nb, ZT, 0, s>>>(b.ctrl, words, xs, meta, agg);
-  z2_kernel<<<1, Z2T, 0, s>>>(b.ctrl, agg, entries, nb);
-  z3_kernel<<<nb, ZT, 0, s>>>(b.ctrl, words, xs, meta, entries, b.normals, T);
-  *launches += 3;
+  const size_t smem = sizeof(ZigShared);
+  switch (kind) {
+    case PRNG_PHILOX:
+      cudaFuncSetAttribute(zig_kernel<PRNG_PHILOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      zig_kernel<PRNG_PHILOX><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, ticket);
+      break;
+    case PRNG_MINSTD:
+      cudaFuncSetAttribute(zig_kernel<PRNG_MINSTD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      zig_kernel<PRNG_MINSTD><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, ticket);
+      break;
+    case PRNG_PCG32:
+      cudaFuncSetAttribute(zig_kernel<PRNG_PCG32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      zig_kernel<PRNG_PCG32><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, ticket);
+      break;
+    default:
+      cudaFuncSetAttribute(zig_kernel<PRNG_SFC64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      zig_kernel<PRNG_SFC64><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, ticket);
+      break;
+  }
+  zig_fallback_kernel<<<1, 1, 0, s>>>(b.ctrl, words, nbuf, b.normals, T);
+  *launches += 2;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

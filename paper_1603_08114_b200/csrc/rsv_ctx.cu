@@ -11,6 +11,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <map>
@@ -19,6 +20,7 @@
 #include <vector>
 
 #include "../../include/rsvhmc_b200.h"
+#include "exp_table.h"
 #include "rsv_internal.h"
 #include "rsv_launch.h"
 
@@ -72,6 +74,8 @@ struct rsv_ctx {
   int64_t launches = 0;
   bool has_data = false, has_params = false, has_latent = false;
   int kind = PRNG_PHILOX;
+  int variant = 0;
+  unsigned long long *dbg = nullptr;  // RSV_TRAJ_STAMPS=1: per-tile timestamps
 
   double *hbuf[2] = {nullptr, nullptr};
   double *y = nullptr, *a = nullptr, *lrv = nullptr, *normals = nullptr;
@@ -101,8 +105,16 @@ struct rsv_ctx {
 
   void *flush_buf = nullptr;
   int64_t flush_bytes = 0;
-  std::map<GraphKey, cudaGraphExec_t> graphs;
-  std::vector<cudaGraph_t> timed_graphs;
+  struct Cached {
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    cudaGraphNode_t traj_node;
+    cudaKernelNodeParams traj_params;
+    TrajArgs args;
+    double dt;
+    std::vector<cudaGraphNode_t> ev;  // timing event-record nodes
+  };
+  std::map<GraphKey, Cached *> graphs;
   bool timing = false;
   std::vector<cudaEvent_t> evpool;
   std::vector<double> last_traj_ms, last_mom_ms, last_total_ms;
@@ -143,9 +155,13 @@ int rsv_destroy(rsv_ctx *c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
-  for (auto g : c->timed_graphs) cudaGraphDestroy(g);
+  for (auto &kv : c->graphs) {
+    cudaGraphExecDestroy(kv.second->exec);
+    cudaGraphDestroy(kv.second->graph);
+    delete kv.second;
+  }
   if (c->flush_buf) cudaFree(c->flush_buf);
+  if (c->dbg) cudaFree(c->dbg);
   for (auto e : c->evpool) cudaEventDestroy(e);
   void *dev[] = {c->hbuf[0], c->hbuf[1], c->y, c->a, c->lrv, c->normals, c->sh, c->sp, c->sh2, c->sp2,
                  c->zscratch, c->sfc_words, c->sfc_snaps, c->parts, c->rpart, c->rout, c->dflag, c->ring_count,
@@ -178,7 +194,12 @@ static int create_impl(rsv_ctx *c, int device, int64_t T) {
   const int64_t nw = momenta_words(T) + 64;
   CK(cudaMalloc(&c->sfc_words, sizeof(uint64_t) * nw));
   CK(cudaMalloc(&c->sfc_snaps, sizeof(uint64_t) * 4 * (nw / SFC_SNAP + 2)));
-  c->max_tiles = (int)(T / (TR_W / 4) + 4 * c->sm_count + 8);
+  c->max_tiles = (int)(T / 64 + 16 * c->sm_count + 8);
+  if (const char *v = getenv("RSV_TRAJ_VARIANT")) c->variant = atoi(v);
+  if (getenv("RSV_TRAJ_STAMPS")) {
+    CK(cudaMalloc(&c->dbg, sizeof(unsigned long long) * 8 * c->max_tiles));
+    CK(cudaMemset(c->dbg, 0, sizeof(unsigned long long) * 8 * c->max_tiles));
+  }
   CK(cudaMalloc(&c->parts, sizeof(TilePart) * c->max_tiles));
   CK(cudaMalloc(&c->rpart, sizeof(double) * 8 * (reduce_partials_count(T) + 1)));
   CK(cudaMalloc(&c->rout, sizeof(double) * 8));
@@ -193,6 +214,9 @@ static int create_impl(rsv_ctx *c, int device, int64_t T) {
   memset(c->h_ctrl, 0, sizeof(DevControl));
   c->h_ctrl->stream.kind = PRNG_PHILOX;
   CK(cudaMemcpy(c->ctrl, c->h_ctrl, sizeof(DevControl), cudaMemcpyHostToDevice));
+  if (momenta_init(c->stream)) return fail(c, RSV_E_CUDA, "momenta table init failed");
+  c->launches++;
+  CK(cudaStreamSynchronize(c->stream));
   return 0;
 }
 
@@ -264,13 +288,33 @@ int rsv_set_params(rsv_ctx *c, const rsv_params *p) {
   CK(cudaSetDevice(c->device));
   // the previous graph replays may still read *prm: order the update on the stream
   CK(cudaStreamSynchronize(c->stream));
-  c->h_prm->phi = p->phi;
-  c->h_prm->mu = p->mu;
-  c->h_prm->xi = p->xi;
-  c->h_prm->se2 = p->sigma_eta_sq;
-  c->h_prm->su2 = p->sigma_u_sq;
+  DevParams &q = *c->h_prm;
+  q.phi = p->phi;
+  q.mu = p->mu;
+  q.xi = p->xi;
+  q.se2 = p->sigma_eta_sq;
+  q.su2 = p->sigma_u_sq;
+  q.inv_su2 = 1.0 / q.su2;
+  q.inv_se2 = 1.0 / q.se2;
+  q.emu = exp(-q.mu);
+  q.one_m_phi2 = 1.0 - q.phi * q.phi;
+  const double Td = (double)c->T;
+  q.hconst = 0.5 * Td * q.mu + 0.5 * Td * log(q.su2) + 0.5 * log(q.se2 / (1.0 - q.phi * q.phi)) +
+             0.5 * (Td - 1.0) * log(q.se2);
+  q.n_lo = (int32_t)floor((q.mu - 50.0) * RSV_INV_LN2_64);
+  q.n_span = (int32_t)ceil((q.mu + 50.0) * RSV_INV_LN2_64) - q.n_lo;
   CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(DevParams), cudaMemcpyHostToDevice, c->stream));
   c->has_params = true;
+  // the trajectory reads the derived constants from its parameter block:
+  // update the kernel node of every cached graph
+  for (auto &kv : c->graphs) {
+    auto *g = kv.second;
+    g->args.k = traj_consts(q, g->dt);
+    void *kp[] = {&g->args};
+    cudaKernelNodeParams np = g->traj_params;
+    np.kernelParams = kp;
+    CK(cudaGraphExecKernelNodeSetParams(g->exec, g->traj_node, &np));
+  }
   return sync(c);
 }
 
@@ -357,6 +401,7 @@ int rsv_refresh_momenta(rsv_ctx *c, double *p_out, int on_device) {
 static TrajArgs traj_args(rsv_ctx *c, double dt, int n_steps, int fuse, const TrajGeom &g) {
   TrajArgs a;
   memset(&a, 0, sizeof(a));
+  a.k = traj_consts(*c->h_prm, dt);
   a.T = c->T;
   a.n_steps = n_steps;
   a.fuse = fuse;
@@ -370,6 +415,9 @@ static TrajArgs traj_args(rsv_ctx *c, double dt, int n_steps, int fuse, const Tr
   a.prm = c->prm;
   a.ctrl = c->ctrl;
   a.parts = c->parts;
+  a.sfc_snaps = c->sfc_snaps;
+  a.integrate_only = 0;
+  a.dbg = c->dbg;
   return a;
 }
 
@@ -391,15 +439,15 @@ static int ensure_events(rsv_ctx *c, size_t n) {
 // Capture one proposal into a graph.  With timing, 4 event-record nodes
 // (start, trajectory begin, trajectory end, end) are added; their events are
 // re-pointed per launch with cudaGraphExecEventRecordNodeSetEvent.
-static std::map<cudaGraphExec_t, std::vector<cudaGraphNode_t>> g_evnodes;
-
-static int build_graph(rsv_ctx *c, const GraphKey &k, cudaGraphExec_t *out) {
-  const TrajGeom g = traj_geometry(c->T, k.n_steps, c->sm_count);
-  if (!g.ok) return fail(c, RSV_E_INVALID, "n_steps=%d too large for one trajectory tile (max %d)", k.n_steps,
-                         TR_W * 3 / 8 - 1);
+static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
+  const TrajGeom g = traj_geometry(c->T, k.n_steps, c->sm_count, c->variant);
+  if (!g.ok) return fail(c, RSV_E_INVALID, "n_steps=%d too large for one trajectory tile", k.n_steps);
   if (g.n_tiles > c->max_tiles) return fail(c, RSV_E_CUDA, "tile count %d exceeds buffer", g.n_tiles);
   int r;
   if ((r = ensure_events(c, 4))) return r;
+  auto *cg = new rsv_ctx::Cached();
+  cg->dt = k.dt;
+  cg->args = traj_args(c, k.dt, k.n_steps, k.fuse, g);
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   int l = 0;
@@ -407,61 +455,59 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, cudaGraphExec_t *out) {
   if (k.timing) cudaEventRecordWithFlags(c->evpool[0], c->stream, cudaEventRecordExternal);
   ok &= launch_momenta(mbufs(c), k.kind, c->T, c->stream, &l) == 0;
   if (k.timing) cudaEventRecordWithFlags(c->evpool[1], c->stream, cudaEventRecordExternal);
-  ok &= launch_trajectory(traj_args(c, k.dt, k.n_steps, k.fuse, g), c->stream, &l) == 0;
+  ok &= launch_trajectory(cg->args, c->stream, &l) == 0;
   if (k.timing) cudaEventRecordWithFlags(c->evpool[2], c->stream, cudaEventRecordExternal);
-  AcceptArgs aa;
-  memset(&aa, 0, sizeof(aa));
-  aa.T = c->T;
-  aa.n_tiles = g.n_tiles;
-  aa.parts = c->parts;
-  aa.prm = c->prm;
-  aa.ctrl = c->ctrl;
-  aa.sfc_words = c->sfc_words;
-  aa.sfc_snaps = c->sfc_snaps;
-  ok &= launch_accept(aa, c->stream, &l) == 0;
   if (k.timing) cudaEventRecordWithFlags(c->evpool[3], c->stream, cudaEventRecordExternal);
   cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
-  if (!ok || e != cudaSuccess) return fail(c, RSV_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
-  cudaGraphExec_t exec;
-  CK(cudaGraphInstantiate(&exec, graph, 0));
-  if (k.timing) {
-    // locate the event-record nodes in capture order
-    size_t n = 0;
-    CK(cudaGraphGetNodes(graph, nullptr, &n));
-    std::vector<cudaGraphNode_t> nodes(n);
-    CK(cudaGraphGetNodes(graph, nodes.data(), &n));
-    std::vector<cudaGraphNode_t> evn(4, nullptr);
-    for (auto nd : nodes) {
-      cudaGraphNodeType t;
-      cudaGraphNodeGetType(nd, &t);
-      if (t != cudaGraphNodeTypeEventRecord) continue;
+  if (!ok || e != cudaSuccess) {
+    delete cg;
+    return fail(c, RSV_E_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  }
+  cg->graph = graph;
+  size_t n = 0;
+  CK(cudaGraphGetNodes(graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  CK(cudaGraphGetNodes(graph, nodes.data(), &n));
+  const void *fn = traj_kernel_fn(g.variant, k.fuse);
+  cg->traj_node = nullptr;
+  cg->ev.assign(4, nullptr);
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    cudaGraphNodeGetType(nd, &t);
+    if (t == cudaGraphNodeTypeKernel) {
+      cudaKernelNodeParams kp;
+      CK(cudaGraphKernelNodeGetParams(nd, &kp));
+      if (kp.func == fn) {
+        cg->traj_node = nd;
+        cg->traj_params = kp;
+      }
+    } else if (t == cudaGraphNodeTypeEventRecord) {
       cudaEvent_t ev;
       cudaGraphEventRecordNodeGetEvent(nd, &ev);
       for (int i = 0; i < 4; i++)
-        if (ev == c->evpool[i]) evn[i] = nd;
+        if (ev == c->evpool[i]) cg->ev[i] = nd;
     }
-    for (int i = 0; i < 4; i++)
-      if (!evn[i]) return fail(c, RSV_E_CUDA, "timing graph: event node %d not found", i);
-    g_evnodes[exec] = evn;
-    c->timed_graphs.push_back(graph);  // node handles stay valid while the graph lives
-  } else {
-    cudaGraphDestroy(graph);
   }
-  *out = exec;
+  if (!cg->traj_node) return fail(c, RSV_E_CUDA, "trajectory node not found in the captured graph");
+  if (k.timing)
+    for (int i = 0; i < 4; i++)
+      if (!cg->ev[i]) return fail(c, RSV_E_CUDA, "timing graph: event node %d not found", i);
+  CK(cudaGraphInstantiate(&cg->exec, graph, 0));
+  *out = cg;
   return 0;
 }
 
-static int get_graph(rsv_ctx *c, double dt, int n_steps, int fuse, cudaGraphExec_t *out, int *kernels) {
+static int get_graph(rsv_ctx *c, double dt, int n_steps, int fuse, rsv_ctx::Cached **out, int *kernels) {
   GraphKey k{c->kind, n_steps, fuse ? 1 : 0, c->timing ? 1 : 0, dt};
   auto it = c->graphs.find(k);
   if (it == c->graphs.end()) {
-    cudaGraphExec_t e;
-    int r = build_graph(c, k, &e);
+    rsv_ctx::Cached *cg = nullptr;
+    int r = build_graph(c, k, &cg);
     if (r) return r;
-    it = c->graphs.emplace(k, e).first;
+    it = c->graphs.emplace(k, cg).first;
   }
   *out = it->second;
-  *kernels = (c->kind == PRNG_SFC64 ? 4 : 3) + 2;
+  *kernels = (c->kind == PRNG_SFC64 ? 3 : 2) + 1;
   return 0;
 }
 
@@ -488,9 +534,10 @@ int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv
   if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
   if (n < 1) return fail(c, RSV_E_INVALID, "n must be >= 1");
   CK(cudaSetDevice(c->device));
-  cudaGraphExec_t exec;
+  rsv_ctx::Cached *cg = nullptr;
   int kpl = 0;
-  if ((r = get_graph(c, dt, n_steps, fuse, &exec, &kpl))) return r;
+  if ((r = get_graph(c, dt, n_steps, fuse, &cg, &kpl))) return r;
+  cudaGraphExec_t exec = cg->exec;
   if (out && n > c->ring_cap) {
     if (c->ring) cudaFree(c->ring);
     if (c->h_ring) cudaFreeHost(c->h_ring);
@@ -502,7 +549,7 @@ int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv
   CK(cudaMemsetAsync(c->ring_count, 0, sizeof(int32_t), c->stream));
   std::vector<cudaGraphNode_t> *evn = nullptr;
   if (c->timing) {
-    evn = &g_evnodes[exec];
+    evn = &cg->ev;
     if ((r = ensure_events(c, 4 * (size_t)n + 4))) return r;
   }
   for (int i = 0; i < n; i++) {
@@ -545,11 +592,11 @@ int rsv_hmc_update(rsv_ctx *c, double dt, int n_steps, int fuse, rsv_result *out
   int r;
   if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
   CK(cudaSetDevice(c->device));
-  cudaGraphExec_t exec;
+  rsv_ctx::Cached *cg = nullptr;
   int kpl = 0;
-  if ((r = get_graph(c, dt, n_steps, fuse, &exec, &kpl))) return r;
+  if ((r = get_graph(c, dt, n_steps, fuse, &cg, &kpl))) return r;
   CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
-  CK(cudaGraphLaunch(exec, c->stream));
+  CK(cudaGraphLaunch(cg->exec, c->stream));
   c->launches += kpl;
   if ((r = pull_ctrl(c))) return r;
   if ((r = check_err_bits(c))) return r;
@@ -573,7 +620,7 @@ int rsv_integrate(rsv_ctx *c, const double *h_in, const double *p_in, double dt,
   if (!c->has_params) return fail(c, RSV_E_STATE, "params not set (rsv_set_params)");
   CK(cudaSetDevice(c->device));
   if ((r = copy_in(c, c->sh, h_in, c->T, on_device)) || (r = copy_in(c, c->sp, p_in, c->T, on_device))) return r;
-  const TrajGeom g = traj_geometry(c->T, n_steps, c->sm_count);
+  const TrajGeom g = traj_geometry(c->T, n_steps, c->sm_count, c->variant);
   int l = 0;
   int32_t div = 0;
   if (g.ok) {
@@ -582,16 +629,8 @@ int rsv_integrate(rsv_ctx *c, const double *h_in, const double *p_in, double dt,
     a.h_dst = c->sh2;
     a.p_in = c->sp;
     a.p_out = c->sp2;
+    a.integrate_only = 1;
     LK(launch_trajectory(a, c->stream, &l));
-    AcceptArgs aa;
-    memset(&aa, 0, sizeof(aa));
-    aa.T = c->T;
-    aa.n_tiles = g.n_tiles;
-    aa.parts = c->parts;
-    aa.prm = c->prm;
-    aa.ctrl = c->ctrl;
-    aa.integrate_only = 1;
-    LK(launch_accept(aa, c->stream, &l));
     c->launches += l;
     if ((r = pull_ctrl(c))) return r;
     div = c->h_ctrl->res.diverged;
@@ -829,6 +868,15 @@ int rsv_measure_fp64_peak(rsv_ctx *c, double *tflops) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   *tflops = best;
+  return 0;
+}
+
+// development aid: copy the per-tile timestamps of the last trajectory
+int rsv_debug_stamps(rsv_ctx *c, unsigned long long *out, int max_tiles) {
+  if (!c || !c->dbg) return fail(c, RSV_E_STATE, "stamps not enabled (RSV_TRAJ_STAMPS=1)");
+  CK(cudaStreamSynchronize(c->stream));
+  const int n = max_tiles < c->max_tiles ? max_tiles : c->max_tiles;
+  CK(cudaMemcpy(out, c->dbg, sizeof(unsigned long long) * 8 * n, cudaMemcpyDeviceToHost));
   return 0;
 }
 

@@ -18,7 +18,8 @@ constexpr int SFC_SNAP = 64;     // sfc64 state snapshot stride (words)
 
 // ---- trajectory tile geometry ----------------------------------------------
 constexpr int TR_NT = 256;       // threads per tile
-constexpr int TR_R = 8;          // consecutive sites per thread (registers)
+constexpr int TR_R = 4;          // consecutive sites per thread (registers)
+constexpr int TR_MINB = 3;       // resident CTAs per SM (register budget 85/thread)
 constexpr int TR_W = TR_NT * TR_R;
 constexpr int TR_NW = TR_NT / 32;
 constexpr int TR_NV = 14;        // reduced values per tile (see TilePart)
@@ -29,6 +30,10 @@ constexpr int ES_R = 4;
 
 struct DevParams {
   double phi, mu, xi, se2, su2;
+  // derived once on the host (rsv_set_params) so no tile recomputes them
+  double inv_su2, inv_se2, emu, one_m_phi2;
+  double hconst;   // theta-only part of H (model.py:134-163 log terms + 0.5*T*mu)
+  int32_t n_lo, n_span;  // |h| <= 50  <=>  rint(-64 (h - mu)/ln2) - n_lo in [0, n_span]
 };
 
 struct TilePart {  // per-tile partial sums over the tile's core sites
@@ -57,6 +62,9 @@ struct DevControl {
   double ends_old[2], ends_new[2];  // d_0, d_{T-1} (shifted by mu)
   double stats[7];      // statistics of the kept path (shift mu, xi of the params used)
   DevResult res;
+  uint64_t u_word;      // raw word right after the momenta (the Metropolis uniform)
+  uint32_t tiles_done;  // trajectory tiles finished (last one runs the Metropolis step)
+  uint32_t pad3;
 };
 
 }  // namespace rsv

@@ -16,6 +16,7 @@ struct MomentaBufs {
 };
 
 int64_t momenta_words(int64_t T);
+int momenta_init(cudaStream_t s);  // builds the jump-ahead tables (once per device)
 size_t momenta_scratch_bytes(int64_t T);
 int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, int *launches);
 int launch_momenta_advance(const MomentaBufs &b, cudaStream_t s, int *launches);
@@ -26,10 +27,23 @@ struct TrajGeom {
   int halo;       // n_steps + 1
   int n_tiles;
   int ok;         // 0 if n_steps is too large for one tile (falls back to per-step passes)
+  int variant;    // (sites/thread, threads/CTA, CTAs/SM) configuration, see leapfrog.cu
 };
-TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count);
+TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant);
+int traj_num_variants();
+
+// Trajectory constants derived on the host from (params, dt): passed by
+// value in the kernel's parameter block so the hot loop reads them as
+// constant-bank operands instead of holding ~30 registers.
+struct TrajConsts {
+  double mu, phi, dt, c_half, c_full, half_dt, alpha, bphi, g_int, g_end, emu, xm, inv2su, inv2se, one_m_phi2;
+  double hconst;
+  int32_t n_lo, n_span;
+};
+TrajConsts traj_consts(const DevParams &P, double dt);
 
 struct TrajArgs {
+  TrajConsts k;
   int64_t T;
   int n_steps;
   int fuse;
@@ -45,21 +59,14 @@ struct TrajArgs {
   const DevParams *prm;
   DevControl *ctrl;
   TilePart *parts;
+  // Metropolis step folded into the last tile
+  const uint64_t *sfc_snaps;
+  int integrate_only;   // 1: only reduce (rsv_integrate): no Metropolis, no stream update
+  unsigned long long *dbg;  // optional per-tile %globaltimer stamps (8 per tile), development aid
 };
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches);
+const void *traj_kernel_fn(int variant, int fuse);  // for locating the node in a captured graph
 
-struct AcceptArgs {
-  int64_t T;
-  int n_tiles;
-  const TilePart *parts;
-  const DevParams *prm;
-  DevControl *ctrl;
-  const uint64_t *sfc_words;
-  const uint64_t *sfc_snaps;
-  DevResult *res_out;   // optional per-call result slot
-  int integrate_only;   // 1: just reduce (rsv_integrate), no Metropolis / stream update
-};
-int launch_accept(const AcceptArgs &a, cudaStream_t s, int *launches);
 
 // one streamed leapfrog step over all sites (integrator.py:139-146)
 int launch_elementary_step(const double *h, const double *p, double *ho, double *po, const double *a,
