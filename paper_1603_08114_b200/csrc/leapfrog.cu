@@ -51,6 +51,25 @@ __device__ __forceinline__ double exp_neg(double d, const unsigned long long *ta
   return fma(S, q, S);
 }
 
+// Same evaluation, constants taken from the kernel's parameter block so the
+// hot loop uses constant-bank operands (no per-iteration immediates).
+template <typename K>
+__device__ __forceinline__ double exp_neg_k(double d, const unsigned long long *tab, double &t, const K &k) {
+  t = fma(-d, k.e_k, MAGIC);
+  const double nd = t - MAGIC;
+  double r = fma(nd, -k.e_hi, -d);
+  r = fma(nd, -k.e_lo, r);
+  double q = fma(r, k.e_c5, k.e_c4);
+  q = fma(q, r, k.e_c3);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = q * r;
+  const int n = __double2loint(t);
+  const unsigned long long tb = tab[n & 63];
+  const double S = __hiloint2double((int)(tb >> 32) + (n << 14), (int)(unsigned)tb);
+  return fma(S, q, S);
+}
+
 // |h| <= 50 <=> n in [n_lo, n_lo + span]; NaN or huge d leave the magic
 // sum's high word outside {0x4337FFFF, 0x43380000}.  Integer ops only.
 __device__ __forceinline__ bool out_of_range(double t, int n_lo, int n_span) {
@@ -78,6 +97,12 @@ TrajConsts traj_consts(const DevParams &P, double dt) {
   s.inv2se = 0.5 * P.inv_se2;
   s.one_m_phi2 = P.one_m_phi2;
   s.hconst = P.hconst;
+  s.e_k = RSV_INV_LN2_64;
+  s.e_hi = RSV_LN2_64_HI;
+  s.e_lo = RSV_LN2_64_LO;
+  s.e_c5 = 1.0 / 120.0;
+  s.e_c4 = 1.0 / 24.0;
+  s.e_c3 = 1.0 / 6.0;
   s.n_lo = P.n_lo;
   s.n_span = P.n_span;
   return s;
@@ -172,7 +197,7 @@ __device__ __forceinline__ void kick(double (&d)[R], double (&p)[R], const doubl
     const double dm = r ? d[r - 1] : dl;
     const double dp = r < R - 1 ? d[r + 1] : dr;
     double t;
-    const double E = exp_neg(d[r], tab, t);
+    const double E = exp_neg_k(d[r], tab, t, s);
     nmax = max(nmax, ((unsigned)__double2loint(t) - (unsigned)s.n_lo) & cm[r]);
     const double G = EDGE && ((endm >> r) & 1) ? s.g_end : s.g_int;
     double pp = p[r] - Cd[r];
@@ -192,7 +217,11 @@ __device__ __forceinline__ void drift(double (&d)[R], const double (&p)[R], doub
 // Metropolis step (sampler.py:155-167) on the tile partials, run by the last
 // tile to finish; deterministic (fixed-order sums).
 template <int NT>
-__device__ void metropolis(const TrajArgs &A, double *s_v);
+__device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts);
+template <int NT>
+__device__ __forceinline__ void metropolis(const TrajArgs &A, double *s_v) {
+  metropolis_n<NT>(A, s_v, A.g.n_tiles);
+}
 
 // Warp windows overlap by one lane on each side ("ghost lanes"): warp w
 // holds sites [w*30R, w*30R + 32R) of the CTA window, its lanes 0 and 31
@@ -452,11 +481,286 @@ __global__ void __launch_bounds__(NT, MINB) traj_kernel(TrajArgs A) {
   (void)s_last;
 }
 
+// ---------------------------------------------------------------------------
+// Persistent, TMA-staged trajectory kernel.  The grid is MINB CTAs per SM;
+// CTA c runs tiles c, c + G, c + 2G, ...  While a tile's trajectory runs in
+// registers, the next tile's h, p, (y/2)y and lnRV windows stream from HBM
+// into shared memory with 1-D bulk-tensor copies (cp.async.bulk, completion
+// on an mbarrier), so the HBM latency of a tile is hidden behind the
+// previous tile's FP64 work.  Per-thread energy / statistics partials are
+// accumulated in shared memory across tiles and reduced once per CTA.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Issue the window [t0 - H, t0 - H + W) of the four arrays into stage[4][W]
+// (clamped to [0, Tpad); arrays are padded to a multiple of 8 doubles).
+template <int W>
+__device__ __forceinline__ void stage_tile(const TrajArgs &A, const double *hsrc, int tile, double *stage,
+                                           uint64_t *bar) {
+  const int64_t g = (int64_t)tile * A.g.core - A.g.halo;
+  const int64_t lo = g < 0 ? 0 : g, hi = min(g + W, A.Tpad);
+  const uint32_t bytes = (uint32_t)((hi - lo) * 8);
+  const int off = (int)(lo - g);
+  mbar_expect_tx(bar, 4 * bytes);
+  tma_load_1d(stage + 0 * W + off, hsrc + lo, bytes, bar);
+  tma_load_1d(stage + 1 * W + off, A.p_in + lo, bytes, bar);
+  tma_load_1d(stage + 2 * W + off, A.a + lo, bytes, bar);
+  tma_load_1d(stage + 3 * W + off, A.lrv + lo, bytes, bar);
+}
+
+template <int R, int NT>
+struct PersistSmem {
+  static constexpr int NW = NT / 32;
+  static constexpr int W = NW > 1 ? NW * 30 * R + 2 * R : 32 * R;
+  double stage[4 * W];
+  double acc[TR_NV * NT];       // per-thread partials across tiles
+  double gx[2 * NW * 4 * R];    // ghost-lane refresh slots
+  double red[NW * TR_NV];
+  double v[NW * TR_NV + TR_NV];
+  unsigned long long tab[64];
+  uint64_t bar;
+  int last;
+};
+
+template <int R, int NT, int MINB, bool FUSE>
+__global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
+  using SM = PersistSmem<R, NT>;
+  constexpr int NW = SM::NW, W = SM::W;
+  constexpr int WSTEP = 30 * R;
+  extern __shared__ __align__(128) unsigned char psmem[];
+  SM &S = *reinterpret_cast<SM *>(psmem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const TrajConsts &s = A.k;
+  const double *hsrc;
+  double *hdst;
+  if (A.h_src) {
+    hsrc = A.h_src;
+    hdst = A.h_dst;
+  } else {
+    const int cur = A.ctrl->cur;
+    hsrc = cur ? A.hbuf1 : A.hbuf0;
+    hdst = cur ? A.hbuf0 : A.hbuf1;
+  }
+  if (tid < 64) S.tab[tid] = g_exp_tab2[tid];
+  for (int k = 0; k < TR_NV; k++) S.acc[k * NT + tid] = 0.0;
+  const int n_tiles = A.g.n_tiles;
+  int tile = blockIdx.x;
+  if (tid == 0) {
+    mbar_init(&S.bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tile < n_tiles) stage_tile<W>(A, hsrc, tile, S.stage, &S.bar);
+  }
+  __syncthreads();
+  const int64_t T = A.T;
+  const int H = A.g.halo;
+  const bool own_lane = (lane >= 1 && lane <= 30) || (lane == 0 && warp == 0) || (lane == 31 && warp == NW - 1);
+  const int lw = warp * WSTEP + lane * R;  // my first site inside the window
+  uint32_t parity = 0;
+  long long cyc_wait = 0, cyc_pre = 0, cyc_loop = 0, cyc_post = 0, c0, c1;
+  for (; tile < n_tiles; tile += gridDim.x) {
+    c0 = clock64();
+    const int64_t t0 = (int64_t)tile * A.g.core;
+    const int64_t t1 = min(t0 + A.g.core, T);
+    const int64_t lo_live = max((int64_t)0, t0 - H), hi_live = min(T, t1 + H);
+    const int64_t g0 = t0 - H + lw;
+
+    // ---- tile data from the staging buffer ----
+    mbar_wait(&S.bar, parity);
+    parity ^= 1;
+    c1 = clock64(); cyc_wait += c1 - c0; c0 = c1;
+    double d[R], p[R], Ad[R], Cd[R], av[R], lv[R];
+    uint32_t live = 0, core = 0, endm = 0;
+    unsigned cm[R];
+#pragma unroll
+    for (int r = 0; r < R; r += 2) {
+      const double2 h2 = *reinterpret_cast<const double2 *>(S.stage + 0 * W + lw + r);
+      const double2 p2 = *reinterpret_cast<const double2 *>(S.stage + 1 * W + lw + r);
+      const double2 a2 = *reinterpret_cast<const double2 *>(S.stage + 2 * W + lw + r);
+      const double2 l2 = *reinterpret_cast<const double2 *>(S.stage + 3 * W + lw + r);
+      d[r] = h2.x; d[r + 1] = h2.y;
+      p[r] = p2.x; p[r + 1] = p2.y;
+      av[r] = a2.x; av[r + 1] = a2.y;
+      lv[r] = l2.x; lv[r + 1] = l2.y;
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t gi = g0 + r;
+      const bool in = gi >= lo_live && gi < hi_live;
+      const bool c = in && own_lane && gi >= t0 && gi < t1;
+      live |= (uint32_t)in << r;
+      core |= (uint32_t)c << r;
+      endm |= (uint32_t)(gi == 0 || gi == T - 1) << r;
+      cm[r] = c ? ~0u : 0u;
+      d[r] = in ? d[r] - s.mu : 0.0;
+      p[r] = in ? p[r] : 0.0;
+      Ad[r] = in ? s.dt * (s.emu * av[r]) : 0.0;
+      Cd[r] = in ? fma(-s.alpha, lv[r] - s.xm, s.half_dt) : 0.0;
+    }
+    const bool any_live = live != 0;
+    const bool edge = (any_live && live != (1u << R) - 1) || endm;
+    // warp-uniform kick path: the masked (edge) kick handles partially or
+    // non-live lanes and the global end sites; all other warps run the lean one
+    const bool warp_edge = __any_sync(0xffffffffu, edge || !any_live);
+    // H_old of the owned core sites while a / lnRV are at hand
+    double vold[6] = {0, 0, 0, 0, 0, 0};
+    {
+      const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
+      tile_energy<R>(d, p, av, lv, dl, core, edge, g0, s, S.tab, vold);
+    }
+    if (edge && !A.h_src) {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        if ((core >> r) & 1) {
+          if (g0 + r == 0) A.ctrl->ends_old[0] = d[r];
+          if (g0 + r == T - 1) A.ctrl->ends_old[1] = d[r];
+        }
+      }
+    }
+    // everyone has read the staging buffer: stream the next tile into it
+    __syncthreads();
+    if (tid == 0 && tile + (int)gridDim.x < n_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      stage_tile<W>(A, hsrc, tile + gridDim.x, S.stage, &S.bar);
+    }
+    const double hold = vold[0];
+#pragma unroll
+    for (int k = 0; k < 6; k++) S.acc[(k == 0 ? 1 : 2 + k) * NT + tid] += vold[k];  // slots 1, 3..7
+
+    // ---- the trajectory ----
+    c1 = clock64(); cyc_pre += c1 - c0; c0 = c1;
+    unsigned nmax = 0;
+    const int L = A.n_steps;
+    int gpar = 0;
+    if (FUSE) drift(d, p, s.c_half);
+    for (int step = 0; step < L; step++) {
+      if (!FUSE) drift(d, p, s.c_half);
+      // lanes 0 / 31 get their own value back: those are ghost lanes (or the
+      // CTA window edges, inside the halo) whose stale values never reach a
+      // core site; next to a global end the neighbour lane is non-live (d = 0)
+      const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
+      const double dr = __shfl_down_sync(0xffffffffu, d[0], 1);
+      if (warp_edge) kick<true, R>(d, p, Ad, Cd, dl, dr, s, S.tab, live, endm, cm, nmax);
+      else kick<false, R>(d, p, Ad, Cd, dl, dr, s, S.tab, live, endm, cm, nmax);
+      if (FUSE) drift(d, p, step < L - 1 ? s.c_full : s.c_half);
+      else drift(d, p, s.c_half);
+      if (NW > 1 && (step + 1) % R == 0 && step + 1 < L) {
+        ghost_refresh<R, NT>(d, p, S.gx, lane, warp, gpar);
+        gpar ^= 1;
+      }
+    }
+    if (NW > 1) ghost_refresh<R, NT>(d, p, S.gx, lane, warp, gpar);
+    __syncthreads();  // refresh slots reused by the next tile
+    c1 = clock64(); cyc_loop += c1 - c0; c0 = c1;
+
+    // ---- H_new, statistics, write-back ----
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t gi = g0 + r;
+      const bool in = gi >= lo_live && gi < hi_live;
+      av[r] = in ? __ldg(A.a + gi) : 0.0;
+      lv[r] = in ? __ldg(A.lrv + gi) : 0.0;
+    }
+    double vnew[6] = {0, 0, 0, 0, 0, 0};
+    {
+      const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
+      tile_energy<R>(d, p, av, lv, dl, core, edge, g0, s, S.tab, vnew);
+    }
+    if (core == (1u << R) - 1) {
+#pragma unroll
+      for (int r = 0; r < R; r += 2) {
+        *reinterpret_cast<double2 *>(hdst + g0 + r) = make_double2(d[r] + s.mu, d[r + 1] + s.mu);
+        if (A.p_out) *reinterpret_cast<double2 *>(A.p_out + g0 + r) = make_double2(p[r], p[r + 1]);
+      }
+    } else if (core) {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        if ((core >> r) & 1) {
+          hdst[g0 + r] = d[r] + s.mu;
+          if (A.p_out) A.p_out[g0 + r] = p[r];
+        }
+      }
+    }
+    if (edge && !A.h_src) {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        if ((core >> r) & 1) {
+          if (g0 + r == 0) A.ctrl->ends_new[0] = d[r];
+          if (g0 + r == T - 1) A.ctrl->ends_new[1] = d[r];
+        }
+      }
+    }
+    S.acc[0 * NT + tid] += vnew[0] - hold;
+    S.acc[2 * NT + tid] += vnew[0];
+#pragma unroll
+    for (int k = 0; k < 5; k++) S.acc[(8 + k) * NT + tid] += vnew[1 + k];
+    if (nmax > (unsigned)s.n_span) S.acc[13 * NT + tid] = 1.0;
+    c1 = clock64(); cyc_post += c1 - c0;
+  }
+  if (A.dbg && tid == 0) {
+    A.dbg[(size_t)blockIdx.x * 8 + 0] = cyc_wait;
+    A.dbg[(size_t)blockIdx.x * 8 + 1] = cyc_pre;
+    A.dbg[(size_t)blockIdx.x * 8 + 2] = cyc_loop;
+    A.dbg[(size_t)blockIdx.x * 8 + 3] = cyc_post;
+    A.dbg[(size_t)blockIdx.x * 8 + 4] = clock64();
+  }
+
+  // ---- one reduction per CTA ----
+  double w[TR_NV];
+#pragma unroll
+  for (int k = 0; k < TR_NV; k++) w[k] = S.acc[k * NT + tid];
+  block_sum<TR_NV, NW>(w, S.red, lane, warp);
+  if (tid == 0) {
+    TilePart *tp = A.parts + blockIdx.x;
+    tp->dh = w[0];
+    tp->hold = w[1];
+    tp->hnew = w[2];
+    for (int k = 0; k < 5; k++) {
+      tp->so[k] = w[3 + k];
+      tp->sn[k] = w[8 + k];
+    }
+    tp->flag = w[13];
+    __threadfence();
+    const unsigned done = atomicAdd(&A.ctrl->tiles_done, 1u);
+    S.last = (done == (unsigned)gridDim.x - 1);
+  }
+  __syncthreads();
+  if (S.last) {
+    __threadfence();
+    metropolis_n<NT>(A, S.v, gridDim.x);
+  }
+}
+
 struct TrajVariant {
   int R, NT, MINB;
 };
 static const TrajVariant kVariants[] = {{8, 256, 2}, {4, 256, 3}, {4, 128, 6}, {8, 128, 4}, {16, 128, 2},
-                                        {2, 256, 4}, {8, 64, 8}, {4, 256, 2}, {8, 32, 16}};
+                                        {2, 256, 4}, {8, 64, 8}, {4, 256, 2}, {8, 32, 16},
+                                        // persistent + TMA-staged (9..11)
+                                        {8, 256, 2}, {4, 256, 3}, {4, 256, 2}};
+static bool variant_persistent(int v) { return v >= 9; }
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 int traj_num_variants() { return kNumVariants; }
@@ -477,6 +781,7 @@ TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant) {
   if (n > slots / 2) n = (n + slots - 1) / slots * slots;
   g.core = ((T + n - 1) / n + v.R - 1) / v.R * v.R;
   g.n_tiles = (int)((T + g.core - 1) / g.core);
+  g.grid = variant_persistent(variant) ? (int)((int64_t)g.n_tiles < slots ? (int64_t)g.n_tiles : slots) : g.n_tiles;
   return g;
 }
 
@@ -484,6 +789,20 @@ template <int R, int NT, int MINB>
 static void launch_v(const TrajArgs &a, cudaStream_t s) {
   if (a.fuse) traj_kernel<R, NT, MINB, true><<<a.g.n_tiles, NT, 0, s>>>(a);
   else traj_kernel<R, NT, MINB, false><<<a.g.n_tiles, NT, 0, s>>>(a);
+}
+
+template <int R, int NT, int MINB>
+static void launch_p(const TrajArgs &a, cudaStream_t s) {
+  const size_t smem = sizeof(PersistSmem<R, NT>);
+  if (a.fuse) {
+    cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    traj_persistent_kernel<R, NT, MINB, true><<<a.g.grid, NT, smem, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    traj_persistent_kernel<R, NT, MINB, false><<<a.g.grid, NT, smem, s>>>(a);
+  }
 }
 
 const void *traj_kernel_fn(int variant, int fuse) {
@@ -497,7 +816,13 @@ const void *traj_kernel_fn(int variant, int fuse) {
     case 5: return RSV_FN(2, 256, 4);
     case 6: return RSV_FN(8, 64, 8);
     case 7: return RSV_FN(4, 256, 2);
-    default: return RSV_FN(8, 32, 16);
+    case 8: return RSV_FN(8, 32, 16);
+#undef RSV_FN
+#define RSV_FN(R, NT, MB) \
+  (fuse ? (const void *)traj_persistent_kernel<R, NT, MB, true> : (const void *)traj_persistent_kernel<R, NT, MB, false>)
+    case 9: return RSV_FN(8, 256, 2);
+    case 10: return RSV_FN(4, 256, 3);
+    default: return RSV_FN(4, 256, 2);
   }
 #undef RSV_FN
 }
@@ -512,7 +837,10 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
     case 5: launch_v<2, 256, 4>(a, s); break;
     case 6: launch_v<8, 64, 8>(a, s); break;
     case 7: launch_v<4, 256, 2>(a, s); break;
-    default: launch_v<8, 32, 16>(a, s); break;
+    case 8: launch_v<8, 32, 16>(a, s); break;
+    case 9: launch_p<8, 256, 2>(a, s); break;
+    case 10: launch_p<4, 256, 3>(a, s); break;
+    default: launch_p<4, 256, 2>(a, s); break;
   }
   (*launches)++;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
@@ -521,13 +849,12 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
 // ---------------------------------------------------------------------------
 // Metropolis (sampler.py:155-167) on the reduced tile partials.
 template <int NT>
-__device__ void metropolis(const TrajArgs &A, double *s_v) {
+__device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   constexpr int NW = NT / 32;
   double v[TR_NV];
 #pragma unroll
   for (int k = 0; k < TR_NV; k++) v[k] = 0.0;
-  const int n_tiles = A.g.n_tiles;
-  for (int i = threadIdx.x; i < n_tiles; i += NT) {
+  for (int i = threadIdx.x; i < n_parts; i += NT) {
     const TilePart &tp = A.parts[i];
     v[0] += tp.dh; v[1] += tp.hold; v[2] += tp.hnew;
 #pragma unroll
@@ -588,6 +915,15 @@ __device__ void metropolis(const TrajArgs &A, double *s_v) {
     for (int i = 0; i < 4; i++) C->stream.s[i] = st[i];
   }
   C->stream.pos += consumed;
+  if (C->stream.kind == PRNG_PCG32) {
+    uint64_t q = C->seq_next;
+    if (drew) { q = q * PCG_MULT + C->stream.s[1]; q = q * PCG_MULT + C->stream.s[1]; }
+    C->seq_state = q;
+  } else if (C->stream.kind == PRNG_MINSTD) {
+    uint64_t q = C->seq_next;
+    if (drew) q = mod31(mod31(mod31(q * MINSTD_A) * MINSTD_A) * MINSTD_A);
+    C->seq_state = q;
+  }
   if (r.accept) C->cur ^= 1;
   const double *sm = r.accept ? tot + 8 : tot + 3;
   C->stats[0] = r.accept ? C->ends_new[0] : C->ends_old[0];

@@ -74,14 +74,14 @@ struct rsv_ctx {
   int64_t launches = 0;
   bool has_data = false, has_params = false, has_latent = false;
   int kind = PRNG_PHILOX;
-  int variant = 0;
+  int variant = 11;  // persistent, TMA-staged, 4 sites x 256 threads, 2 CTAs/SM (see leapfrog.cu)
   unsigned long long *dbg = nullptr;  // RSV_TRAJ_STAMPS=1: per-tile timestamps
 
   double *hbuf[2] = {nullptr, nullptr};
   double *y = nullptr, *a = nullptr, *lrv = nullptr, *normals = nullptr;
   double *sh = nullptr, *sp = nullptr, *sh2 = nullptr, *sp2 = nullptr;  // scratch T each
   void *zscratch = nullptr;
-  uint64_t *sfc_words = nullptr, *sfc_snaps = nullptr;
+  uint64_t *sfc_words = nullptr, *sfc_snaps = nullptr, *bjump = nullptr;
   TilePart *parts = nullptr;
   int max_tiles = 0;
   double *rpart = nullptr;  // reduction partials
@@ -165,7 +165,7 @@ int rsv_destroy(rsv_ctx *c) {
   for (auto e : c->evpool) cudaEventDestroy(e);
   void *dev[] = {c->hbuf[0], c->hbuf[1], c->y, c->a, c->lrv, c->normals, c->sh, c->sp, c->sh2, c->sp2,
                  c->zscratch, c->sfc_words, c->sfc_snaps, c->parts, c->rpart, c->rout, c->dflag, c->ring_count,
-                 c->ring, c->ctrl, c->prm, c->pl[0], c->pl[1], c->pl[2], c->pl[3]};
+                 c->ring, c->ctrl, c->prm, c->pl[0], c->pl[1], c->pl[2], c->pl[3], c->bjump};
   for (void *p : dev)
     if (p) cudaFree(p);
   void *host[] = {c->h_ctrl, c->h_prm, c->h_out, c->h_flag, c->h_ring};
@@ -186,11 +186,19 @@ static int create_impl(rsv_ctx *c, int device, int64_t T) {
     return fail(c, RSV_E_CUDA, "built for sm_100a (B200); device is sm_%d%d", prop.major, prop.minor);
   c->sm_count = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-  const size_t tb = sizeof(double) * (size_t)T;
-  for (int i = 0; i < 2; i++) CK(cudaMalloc(&c->hbuf[i], tb));
+  // zero-padded to a multiple of 8 doubles so tiles can be bulk-copied in 64 B units
+  const size_t tb = sizeof(double) * (size_t)((T + 7) / 8 * 8);
+  for (int i = 0; i < 2; i++) {
+    CK(cudaMalloc(&c->hbuf[i], tb));
+    CK(cudaMemset(c->hbuf[i], 0, tb));
+  }
   double **bufs[] = {&c->y, &c->a, &c->lrv, &c->normals, &c->sh, &c->sp, &c->sh2, &c->sp2};
-  for (double **b : bufs) CK(cudaMalloc(b, tb));
+  for (double **b : bufs) {
+    CK(cudaMalloc(b, tb));
+    CK(cudaMemset(*b, 0, tb));
+  }
   CK(cudaMalloc(&c->zscratch, momenta_scratch_bytes(T)));
+  CK(cudaMemset(c->zscratch, 0, momenta_scratch_bytes(T)));  // look-back status words (epoch-tagged)
   const int64_t nw = momenta_words(T) + 64;
   CK(cudaMalloc(&c->sfc_words, sizeof(uint64_t) * nw));
   CK(cudaMalloc(&c->sfc_snaps, sizeof(uint64_t) * 4 * (nw / SFC_SNAP + 2)));
@@ -214,8 +222,9 @@ static int create_impl(rsv_ctx *c, int device, int64_t T) {
   memset(c->h_ctrl, 0, sizeof(DevControl));
   c->h_ctrl->stream.kind = PRNG_PHILOX;
   CK(cudaMemcpy(c->ctrl, c->h_ctrl, sizeof(DevControl), cudaMemcpyHostToDevice));
-  if (momenta_init(c->stream)) return fail(c, RSV_E_CUDA, "momenta table init failed");
-  c->launches++;
+  CK(cudaMalloc(&c->bjump, momenta_jump_bytes(T)));
+  if (momenta_init(c->stream, c->bjump, T)) return fail(c, RSV_E_CUDA, "momenta table init failed");
+  c->launches += 2;
   CK(cudaStreamSynchronize(c->stream));
   return 0;
 }
@@ -353,6 +362,12 @@ int rsv_set_prng_state(rsv_ctx *c, const rsv_prng_state *st) {
   CK(cudaStreamSynchronize(c->stream));
   c->h_ctrl->stream = s;
   CK(cudaMemcpyAsync(&c->ctrl->stream, &c->h_ctrl->stream, sizeof(StreamState), cudaMemcpyHostToDevice, c->stream));
+  uint64_t seq = 0;
+  if (s.kind == PRNG_PCG32) seq = pcg_advance(s.s[0], 2 * s.pos, s.s[1]);
+  else if (s.kind == PRNG_MINSTD) seq = mod31(minstd_pow(3 * s.pos) * s.s[0]);
+  c->h_ctrl->seq_state = seq;
+  CK(cudaMemcpyAsync(&c->ctrl->seq_state, &c->h_ctrl->seq_state, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                     c->stream));
   c->kind = st->kind;
   return sync(c);
 }
@@ -376,6 +391,7 @@ static MomentaBufs mbufs(rsv_ctx *c) {
   b.sfc_words = c->sfc_words;
   b.sfc_snaps = c->sfc_snaps;
   b.normals = c->normals;
+  b.bjump = c->bjump;
   return b;
 }
 
@@ -403,6 +419,7 @@ static TrajArgs traj_args(rsv_ctx *c, double dt, int n_steps, int fuse, const Tr
   memset(&a, 0, sizeof(a));
   a.k = traj_consts(*c->h_prm, dt);
   a.T = c->T;
+  a.Tpad = (c->T + 7) / 8 * 8;
   a.n_steps = n_steps;
   a.fuse = fuse;
   a.dt = dt;

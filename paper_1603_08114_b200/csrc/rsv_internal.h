@@ -65,6 +65,11 @@ struct DevControl {
   uint64_t u_word;      // raw word right after the momenta (the Metropolis uniform)
   uint32_t tiles_done;  // trajectory tiles finished (last one runs the Metropolis step)
   uint32_t pad3;
+  // sequential state of jump-ahead generators at the stream position (pcg32:
+  // LCG state before output 2*pos; minstd: x_{3*pos}); seq_next = at pos + used
+  uint64_t seq_state, seq_next;
+  // momenta kernel bookkeeping (reset by its last CTA: no memsets per draw)
+  uint32_t zig_ticket, zig_done, zig_epoch, pad4;
 };
 
 }  // namespace rsv

@@ -13,10 +13,12 @@ struct MomentaBufs {
   uint64_t *sfc_words;  // SFC64 only: momenta_words(T) + 64 words
   uint64_t *sfc_snaps;  // SFC64 only: 4 * ((momenta_words(T) + 64) / SFC_SNAP + 1) words
   double *normals;      // T doubles
+  const uint64_t *bjump;  // momenta_jump_bytes(T): per-CTA jump-ahead constants
 };
 
 int64_t momenta_words(int64_t T);
-int momenta_init(cudaStream_t s);  // builds the jump-ahead tables (once per device)
+int momenta_init(cudaStream_t s, uint64_t *bjump, int64_t T);  // builds the jump-ahead tables
+size_t momenta_jump_bytes(int64_t T);
 size_t momenta_scratch_bytes(int64_t T);
 int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, int *launches);
 int launch_momenta_advance(const MomentaBufs &b, cudaStream_t s, int *launches);
@@ -28,6 +30,7 @@ struct TrajGeom {
   int n_tiles;
   int ok;         // 0 if n_steps is too large for one tile (falls back to per-step passes)
   int variant;    // (sites/thread, threads/CTA, CTAs/SM) configuration, see leapfrog.cu
+  int grid;       // CTAs launched (== n_tiles, or the persistent grid)
 };
 TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant);
 int traj_num_variants();
@@ -38,6 +41,8 @@ int traj_num_variants();
 struct TrajConsts {
   double mu, phi, dt, c_half, c_full, half_dt, alpha, bphi, g_int, g_end, emu, xm, inv2su, inv2se, one_m_phi2;
   double hconst;
+  // exp(-d) constants: constant-bank operands of the FP64 instructions
+  double e_k, e_hi, e_lo, e_c5, e_c4, e_c3;
   int32_t n_lo, n_span;
 };
 TrajConsts traj_consts(const DevParams &P, double dt);
@@ -45,6 +50,7 @@ TrajConsts traj_consts(const DevParams &P, double dt);
 struct TrajArgs {
   TrajConsts k;
   int64_t T;
+  int64_t Tpad;         // arrays are allocated (and zero padded) to Tpad = roundup(T, 8)
   int n_steps;
   int fuse;
   double dt;

@@ -1,0 +1,22 @@
+import ctypes, os, sys
+import numpy as np
+sys.path.insert(0, ".")
+os.environ["RSV_TRAJ_STAMPS"] = "1"
+import paper_1603_08114_b200 as P
+from paper_1603_08114_b200 import _native as N
+L = N.lib()
+L.rsv_debug_stamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+theta = P.Params(0.97, -9.0, -0.3, 0.05, 0.1)
+for T in [1 << 20, 1 << 22]:
+    tr = P.simulate_rsv(theta, T, seed=1)
+    be = P.CudaBackend(0)
+    ch = be.chain(tr.dataset, theta)
+    ch.set_latent(tr.latent)
+    ch.set_stream(P.stream_state(P.make_rng(1, "pcg32")))
+    ch.hmc_update_many(0.02, 20, 3, results=False)
+    st = np.zeros((400, 8), dtype=np.int64)
+    N.check(L.rsv_debug_stamps(ch.ctx, st.ctypes.data, 400), ch.ctx)
+    st = st[st[:, 2] > 0]
+    tot = st[:, :4].sum(axis=1)
+    print(f"T={T} CTAs={len(st)} mean cycles: wait {st[:,0].mean():.0f} pre {st[:,1].mean():.0f} loop {st[:,2].mean():.0f} post {st[:,3].mean():.0f}  total {tot.mean():.0f} (max {tot.max()})")
+    be.close()

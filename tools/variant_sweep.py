@@ -23,7 +23,8 @@ for T in [1 << 14, 1 << 18, 1 << 20, 1 << 22]:
     be.close()
 print(" | ".join(out))
 '''
-for v in range(int(sys.argv[1]) if len(sys.argv) > 1 else 6):
+if __name__ == "__main__":
+  for v in range(int(sys.argv[1]) if len(sys.argv) > 1 else 6):
     env = dict(os.environ, RSV_TRAJ_VARIANT=str(v))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     print(f"variant {v}:", r.stdout.strip() or r.stderr[-500:], flush=True)
