@@ -92,8 +92,10 @@ int rsv_refresh_momenta(rsv_ctx *ctx, double *p_out, int on_device);
  * momenta -> H_old -> L leapfrog steps -> H_new -> Metropolis, all on
  * device.  fuse != 0 selects integrate_trajectory(fuse_half_steps=True). */
 int rsv_hmc_update(rsv_ctx *ctx, double step_size, int n_steps, int fuse, rsv_result *out);
-/* n back-to-back proposals with fixed params, captured in one CUDA graph;
- * results (n entries) optional.  Used by run_chain's HMC-only mode. */
+/* n back-to-back proposals with fixed params (one CUDA graph per proposal,
+ * no host round trip in between); results (n entries) optional.  Like the
+ * reference's hmc_update_volatility these proposals do not evaluate the theta
+ * statistics (rsv_last_stats is only valid after rsv_hmc_update). */
 int rsv_hmc_update_many(rsv_ctx *ctx, double step_size, int n_steps, int fuse, int n, rsv_result *out);
 
 /* integrator.py:149-179 integrate_trajectory from (h_in, p_in).

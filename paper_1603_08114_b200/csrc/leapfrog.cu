@@ -122,7 +122,7 @@ __device__ __forceinline__ double site_energy(double d, double dprev, double p, 
 
 // Energies and statistics of the thread's owned core sites (branch-free on
 // the common path; `edge` threads handle the global first site).
-template <int R>
+template <int R, bool STATS = true>
 __device__ __forceinline__ void tile_energy(const double (&d)[R], const double (&p)[R], const double (&av)[R],
                                             const double (&lv)[R], double dl, uint32_t core, bool edge, int64_t g0,
                                             const TrajConsts &s, const unsigned long long *tab, double (&v)[6]) {
@@ -130,16 +130,18 @@ __device__ __forceinline__ void tile_energy(const double (&d)[R], const double (
   for (int r = 0; r < R; r++) {
     const double dprev = r ? d[r - 1] : dl;
     const double q = lv[r] - s.xm;
-    const double e = q - d[r];
     const bool first = edge && (g0 + r == 0);
     const double en = site_energy(d[r], dprev, p[r], s.emu * av[r], q, first, s, tab);
     const bool c = (core >> r) & 1;
     v[0] += c ? en : 0.0;
-    v[1] += c ? d[r] : 0.0;
-    v[2] += c ? d[r] * d[r] : 0.0;
-    v[3] += (c && !first) ? d[r] * dprev : 0.0;
-    v[4] += c ? e : 0.0;
-    v[5] += c ? e * e : 0.0;
+    if (STATS) {
+      const double e = q - d[r];
+      v[1] += c ? d[r] : 0.0;
+      v[2] += c ? d[r] * d[r] : 0.0;
+      v[3] += (c && !first) ? d[r] * dprev : 0.0;
+      v[4] += c ? e : 0.0;
+      v[5] += c ? e * e : 0.0;
+    }
   }
 }
 
@@ -535,17 +537,17 @@ template <int R, int NT>
 struct PersistSmem {
   static constexpr int NW = NT / 32;
   static constexpr int W = NW > 1 ? NW * 30 * R + 2 * R : 32 * R;
-  double stage[4 * W];
+  double stage[2][4 * W];       // double-buffered tile windows
   double acc[TR_NV * NT];       // per-thread partials across tiles
   double gx[2 * NW * 4 * R];    // ghost-lane refresh slots
   double red[NW * TR_NV];
   double v[NW * TR_NV + TR_NV];
   unsigned long long tab[64];
-  uint64_t bar;
+  uint64_t bar[2];
   int last;
 };
 
-template <int R, int NT, int MINB, bool FUSE>
+template <int R, int NT, int MINB, bool FUSE, bool STATS>
 __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   using SM = PersistSmem<R, NT>;
   constexpr int NW = SM::NW, W = SM::W;
@@ -569,37 +571,46 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   const int n_tiles = A.g.n_tiles;
   int tile = blockIdx.x;
   if (tid == 0) {
-    mbar_init(&S.bar, 1);
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (tile < n_tiles) stage_tile<W>(A, hsrc, tile, S.stage, &S.bar);
+    if (tile < n_tiles) stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0]);
   }
   __syncthreads();
   const int64_t T = A.T;
   const int H = A.g.halo;
   const bool own_lane = (lane >= 1 && lane <= 30) || (lane == 0 && warp == 0) || (lane == 31 && warp == NW - 1);
   const int lw = warp * WSTEP + lane * R;  // my first site inside the window
-  uint32_t parity = 0;
+  uint32_t parity[2] = {0, 0};
+  int buf = 0;
   long long cyc_wait = 0, cyc_pre = 0, cyc_loop = 0, cyc_post = 0, c0, c1;
-  for (; tile < n_tiles; tile += gridDim.x) {
+  for (; tile < n_tiles; tile += gridDim.x, buf ^= 1) {
     c0 = clock64();
+    // the other buffer was released at the end of the previous tile: stream
+    // the next tile into it while this one runs
+    if (tid == 0 && tile + (int)gridDim.x < n_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      stage_tile<W>(A, hsrc, tile + gridDim.x, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
+    }
+    const double *stg = S.stage[buf];
     const int64_t t0 = (int64_t)tile * A.g.core;
     const int64_t t1 = min(t0 + A.g.core, T);
     const int64_t lo_live = max((int64_t)0, t0 - H), hi_live = min(T, t1 + H);
     const int64_t g0 = t0 - H + lw;
 
     // ---- tile data from the staging buffer ----
-    mbar_wait(&S.bar, parity);
-    parity ^= 1;
+    mbar_wait(&S.bar[buf], parity[buf]);
+    parity[buf] ^= 1;
     c1 = clock64(); cyc_wait += c1 - c0; c0 = c1;
     double d[R], p[R], Ad[R], Cd[R], av[R], lv[R];
     uint32_t live = 0, core = 0, endm = 0;
     unsigned cm[R];
 #pragma unroll
     for (int r = 0; r < R; r += 2) {
-      const double2 h2 = *reinterpret_cast<const double2 *>(S.stage + 0 * W + lw + r);
-      const double2 p2 = *reinterpret_cast<const double2 *>(S.stage + 1 * W + lw + r);
-      const double2 a2 = *reinterpret_cast<const double2 *>(S.stage + 2 * W + lw + r);
-      const double2 l2 = *reinterpret_cast<const double2 *>(S.stage + 3 * W + lw + r);
+      const double2 h2 = *reinterpret_cast<const double2 *>(stg + 0 * W + lw + r);
+      const double2 p2 = *reinterpret_cast<const double2 *>(stg + 1 * W + lw + r);
+      const double2 a2 = *reinterpret_cast<const double2 *>(stg + 2 * W + lw + r);
+      const double2 l2 = *reinterpret_cast<const double2 *>(stg + 3 * W + lw + r);
       d[r] = h2.x; d[r + 1] = h2.y;
       p[r] = p2.x; p[r + 1] = p2.y;
       av[r] = a2.x; av[r + 1] = a2.y;
@@ -628,7 +639,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     double vold[6] = {0, 0, 0, 0, 0, 0};
     {
       const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      tile_energy<R>(d, p, av, lv, dl, core, edge, g0, s, S.tab, vold);
+      tile_energy<R, STATS>(d, p, av, lv, dl, core, edge, g0, s, S.tab, vold);
     }
     if (edge && !A.h_src) {
 #pragma unroll
@@ -638,12 +649,6 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
           if (g0 + r == T - 1) A.ctrl->ends_old[1] = d[r];
         }
       }
-    }
-    // everyone has read the staging buffer: stream the next tile into it
-    __syncthreads();
-    if (tid == 0 && tile + (int)gridDim.x < n_tiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      stage_tile<W>(A, hsrc, tile + gridDim.x, S.stage, &S.bar);
     }
     const double hold = vold[0];
 #pragma unroll
@@ -677,16 +682,16 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
 
     // ---- H_new, statistics, write-back ----
 #pragma unroll
-    for (int r = 0; r < R; r++) {
-      const int64_t gi = g0 + r;
-      const bool in = gi >= lo_live && gi < hi_live;
-      av[r] = in ? __ldg(A.a + gi) : 0.0;
-      lv[r] = in ? __ldg(A.lrv + gi) : 0.0;
+    for (int r = 0; r < R; r += 2) {
+      const double2 a2 = *reinterpret_cast<const double2 *>(stg + 2 * W + lw + r);
+      const double2 l2 = *reinterpret_cast<const double2 *>(stg + 3 * W + lw + r);
+      av[r] = a2.x; av[r + 1] = a2.y;
+      lv[r] = l2.x; lv[r + 1] = l2.y;
     }
     double vnew[6] = {0, 0, 0, 0, 0, 0};
     {
       const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      tile_energy<R>(d, p, av, lv, dl, core, edge, g0, s, S.tab, vnew);
+      tile_energy<R, STATS>(d, p, av, lv, dl, core, edge, g0, s, S.tab, vnew);
     }
     if (core == (1u << R) - 1) {
 #pragma unroll
@@ -717,6 +722,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
 #pragma unroll
     for (int k = 0; k < 5; k++) S.acc[(8 + k) * NT + tid] += vnew[1 + k];
     if (nmax > (unsigned)s.n_span) S.acc[13 * NT + tid] = 1.0;
+    __syncthreads();  // all reads of this tile's buffer done before it is refilled
     c1 = clock64(); cyc_post += c1 - c0;
   }
   if (A.dbg && tid == 0) {
@@ -791,21 +797,25 @@ static void launch_v(const TrajArgs &a, cudaStream_t s) {
   else traj_kernel<R, NT, MINB, false><<<a.g.n_tiles, NT, 0, s>>>(a);
 }
 
+template <int R, int NT, int MINB, bool FUSE, bool STATS>
+static void launch_p2(const TrajArgs &a, cudaStream_t s) {
+  const size_t smem = sizeof(PersistSmem<R, NT>);
+  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  traj_persistent_kernel<R, NT, MINB, FUSE, STATS><<<a.g.grid, NT, smem, s>>>(a);
+}
 template <int R, int NT, int MINB>
 static void launch_p(const TrajArgs &a, cudaStream_t s) {
-  const size_t smem = sizeof(PersistSmem<R, NT>);
   if (a.fuse) {
-    cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    traj_persistent_kernel<R, NT, MINB, true><<<a.g.grid, NT, smem, s>>>(a);
+    if (a.stats) launch_p2<R, NT, MINB, true, true>(a, s);
+    else launch_p2<R, NT, MINB, true, false>(a, s);
   } else {
-    cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    traj_persistent_kernel<R, NT, MINB, false><<<a.g.grid, NT, smem, s>>>(a);
+    if (a.stats) launch_p2<R, NT, MINB, false, true>(a, s);
+    else launch_p2<R, NT, MINB, false, false>(a, s);
   }
 }
 
-const void *traj_kernel_fn(int variant, int fuse) {
+const void *traj_kernel_fn(int variant, int fuse, int stats) {
 #define RSV_FN(R, NT, MB) (fuse ? (const void *)traj_kernel<R, NT, MB, true> : (const void *)traj_kernel<R, NT, MB, false>)
   switch (variant) {
     case 0: return RSV_FN(8, 256, 2);
@@ -818,8 +828,11 @@ const void *traj_kernel_fn(int variant, int fuse) {
     case 7: return RSV_FN(4, 256, 2);
     case 8: return RSV_FN(8, 32, 16);
 #undef RSV_FN
-#define RSV_FN(R, NT, MB) \
-  (fuse ? (const void *)traj_persistent_kernel<R, NT, MB, true> : (const void *)traj_persistent_kernel<R, NT, MB, false>)
+#define RSV_FN(R, NT, MB)                                                                                   \
+  (fuse ? (stats ? (const void *)traj_persistent_kernel<R, NT, MB, true, true>                             \
+                 : (const void *)traj_persistent_kernel<R, NT, MB, true, false>)                           \
+        : (stats ? (const void *)traj_persistent_kernel<R, NT, MB, false, true>                            \
+                 : (const void *)traj_persistent_kernel<R, NT, MB, false, false>))
     case 9: return RSV_FN(8, 256, 2);
     case 10: return RSV_FN(4, 256, 3);
     default: return RSV_FN(4, 256, 2);

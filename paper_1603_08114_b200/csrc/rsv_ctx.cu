@@ -29,10 +29,11 @@ using namespace rsv;
 namespace {
 
 struct GraphKey {
-  int kind, n_steps, fuse, timing;
+  int kind, n_steps, fuse, timing, stats;
   double dt;
   bool operator<(const GraphKey &o) const {
-    return std::tie(kind, n_steps, fuse, timing, dt) < std::tie(o.kind, o.n_steps, o.fuse, o.timing, o.dt);
+    return std::tie(kind, n_steps, fuse, timing, stats, dt) <
+           std::tie(o.kind, o.n_steps, o.fuse, o.timing, o.stats, o.dt);
   }
 };
 
@@ -465,6 +466,7 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   auto *cg = new rsv_ctx::Cached();
   cg->dt = k.dt;
   cg->args = traj_args(c, k.dt, k.n_steps, k.fuse, g);
+  cg->args.stats = k.stats;
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   int l = 0;
@@ -485,7 +487,7 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   CK(cudaGraphGetNodes(graph, nullptr, &n));
   std::vector<cudaGraphNode_t> nodes(n);
   CK(cudaGraphGetNodes(graph, nodes.data(), &n));
-  const void *fn = traj_kernel_fn(g.variant, k.fuse);
+  const void *fn = traj_kernel_fn(g.variant, k.fuse, k.stats);
   cg->traj_node = nullptr;
   cg->ev.assign(4, nullptr);
   for (auto nd : nodes) {
@@ -514,8 +516,9 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   return 0;
 }
 
-static int get_graph(rsv_ctx *c, double dt, int n_steps, int fuse, rsv_ctx::Cached **out, int *kernels) {
-  GraphKey k{c->kind, n_steps, fuse ? 1 : 0, c->timing ? 1 : 0, dt};
+static int get_graph(rsv_ctx *c, double dt, int n_steps, int fuse, int stats, rsv_ctx::Cached **out,
+                     int *kernels) {
+  GraphKey k{c->kind, n_steps, fuse ? 1 : 0, c->timing ? 1 : 0, stats ? 1 : 0, dt};
   auto it = c->graphs.find(k);
   if (it == c->graphs.end()) {
     rsv_ctx::Cached *cg = nullptr;
@@ -553,7 +556,8 @@ int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv
   CK(cudaSetDevice(c->device));
   rsv_ctx::Cached *cg = nullptr;
   int kpl = 0;
-  if ((r = get_graph(c, dt, n_steps, fuse, &cg, &kpl))) return r;
+  // HMC-only proposals (the reference's hmc_update_volatility): no theta statistics
+  if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl))) return r;
   cudaGraphExec_t exec = cg->exec;
   if (out && n > c->ring_cap) {
     if (c->ring) cudaFree(c->ring);
@@ -611,7 +615,7 @@ int rsv_hmc_update(rsv_ctx *c, double dt, int n_steps, int fuse, rsv_result *out
   CK(cudaSetDevice(c->device));
   rsv_ctx::Cached *cg = nullptr;
   int kpl = 0;
-  if ((r = get_graph(c, dt, n_steps, fuse, &cg, &kpl))) return r;
+  if ((r = get_graph(c, dt, n_steps, fuse, 1, &cg, &kpl))) return r;
   CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
   CK(cudaGraphLaunch(cg->exec, c->stream));
   c->launches += kpl;
@@ -647,6 +651,7 @@ int rsv_integrate(rsv_ctx *c, const double *h_in, const double *p_in, double dt,
     a.p_in = c->sp;
     a.p_out = c->sp2;
     a.integrate_only = 1;
+    a.stats = 1;
     LK(launch_trajectory(a, c->stream, &l));
     c->launches += l;
     if ((r = pull_ctrl(c))) return r;

@@ -68,10 +68,11 @@ struct TrajArgs {
   // Metropolis step folded into the last tile
   const uint64_t *sfc_snaps;
   int integrate_only;   // 1: only reduce (rsv_integrate): no Metropolis, no stream update
+  int stats;            // compute the theta statistics of both paths (persistent kernel)
   unsigned long long *dbg;  // optional per-tile %globaltimer stamps (8 per tile), development aid
 };
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches);
-const void *traj_kernel_fn(int variant, int fuse);  // for locating the node in a captured graph
+const void *traj_kernel_fn(int variant, int fuse, int stats);  // for locating the node in a captured graph
 
 
 // one streamed leapfrog step over all sites (integrator.py:139-146)
