@@ -39,6 +39,7 @@ constexpr int ZG = 16;                 // guard words before a CTA's block
 constexpr int ZLA = 32;                // look-ahead words after it
 constexpr int ZSW = ZG + ZB + ZLA;     // staged words per CTA
 constexpr int ZCH = ZSW / ZW;          // 8-word chunks per CTA (262)
+constexpr int ZDIRECT = 4096;          // up to this many CTAs: direct predecessor sums
 
 struct ZigJump {  // per-chunk jump-ahead constants (inc-free), built once
   uint64_t pcg_a[ZCH], pcg_g[ZCH];     // state_c = a * base + inc * g  (16 c outputs ahead)
@@ -179,9 +180,19 @@ __device__ __forceinline__ void stage_words(ZigShared &S, const DevControl *ctrl
 
 __device__ void zig_serial(DevControl *ctrl, const uint64_t *words, int64_t nbuf, double *normals, int64_t T);
 
+__device__ __forceinline__ unsigned long long zgt() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_t *words, int64_t nwords_buf,
-                                                 double *normals, int64_t T, uint64_t *status, const uint64_t *bjump) {
+                                                 double *normals, int64_t T, uint64_t *status, const uint64_t *bjump,
+                                                 unsigned long long *dbg) {
+#define ZSTAMP(k) \
+  do { if (dbg && threadIdx.x == 0) dbg[(size_t)blockIdx.x * 8 + (k)] = zgt(); } while (0)
+  ZSTAMP(0);
   extern __shared__ __align__(16) unsigned char zsmem[];
   ZigShared &S = *reinterpret_cast<ZigShared *>(zsmem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -196,8 +207,10 @@ __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_
   }
   __syncthreads();
   const int b = S.blk;
+  ZSTAMP(1);
   stage_words<KIND>(S, ctrl, words, b, nwords_buf, bjump);
   __syncthreads();
+  ZSTAMP(2);
 
   // ---- classify every guard + block word as an attempt start
   const int first = (b == 0) ? ZG : 0;  // CTA 0 has no guard
@@ -213,6 +226,7 @@ __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_
   }
   if (ovf) atomicOr(&ctrl->zig_overflow, 1);
   __syncthreads();
+  ZSTAMP(3);
 
   // ---- speculative walk: in sync 16 words before my segment
   const int seg = ZG + tid * ZW;
@@ -253,6 +267,7 @@ __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_
   }
   const int toff = woff + incl - cnt;  // exclusive offset of my normals in the CTA
 
+  ZSTAMP(4);
   // ---- decoupled look-back over CTAs for the global normal offset
   // (warp 0 inspects 32 predecessors per round)
   if (warp == 0) {
@@ -266,19 +281,49 @@ __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_
       }
     } else {
       if (lane == 0) vst[b] = zpack(1, bexit, S.epoch, (uint64_t)btot);
-      // look back 256 predecessors per round (8 independent loads per lane)
       uint64_t acc = 0;
+      if (gridDim.x <= ZDIRECT) {
+        // small grids: every CTA sums all its predecessors' aggregates in one
+        // round of independent loads (no chain of published prefixes)
+        for (;;) {
+          uint64_t part = 0;
+          bool ok = true;
+          for (int j = lane; j < b; j += 32) {
+            const uint64_t v = vst[j];
+            ok &= zready(v, S.epoch);
+            part += v & ZCNT;
+          }
+          if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            acc = part;
+            break;
+          }
+          __nanosleep(100);
+        }
+        if (lane == 0) {
+          const uint64_t prev = vst[b - 1];
+          if ((int)((prev >> 58) & 15) != S.warp0_entry) S.bad = 1;
+        }
+      } else {
+      // look back 256 predecessors per round (8 independent loads per lane)
       int hi = b - 1;
       bool checked = false;
       for (;;) {
+        // 8 independent loads per lane, re-issued until every predecessor in
+        // the window has published (no serial chain of dependent loads)
         uint64_t sv[8];
+        for (;;) {
+          bool ok = true;
 #pragma unroll
-        for (int w = 0; w < 8; w++) {
-          const int j = hi - lane - 32 * w;
-          sv[w] = 2ULL << 62;  // before CTA 0: an empty prefix
-          if (j >= 0) {
-            do { sv[w] = vst[j]; } while (!zready(sv[w], S.epoch));
+          for (int w = 0; w < 8; w++) {
+            const int j = hi - lane - 32 * w;
+            sv[w] = j >= 0 ? vst[j] : (uint64_t)S.epoch << 34 | 2ULL << 62;  // before CTA 0: empty prefix
           }
+#pragma unroll
+          for (int w = 0; w < 8; w++) ok &= zready(sv[w], S.epoch);
+          if (__all_sync(0xffffffffu, ok)) break;
+          __nanosleep(200);  // back off: hundreds of CTAs poll the same lines
         }
         if (!checked) {  // the previous CTA's exit must equal my thread 0's entry
           const uint64_t prev = __shfl_sync(0xffffffffu, sv[0], 0);
@@ -302,16 +347,22 @@ __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_
         if (done) break;
         hi -= 256;
       }
+      }
       if (lane == 0) {
         S.blk_off = acc;
-        __threadfence();
-        vst[b] = zpack(2, bexit, S.epoch, acc + (uint64_t)btot);
+        // prefixes are only consumed by the chained look-back of large grids
+        // (the direct sums need every CTA's own count to stay in place)
+        if (gridDim.x > ZDIRECT) {
+          __threadfence();
+          vst[b] = zpack(2, bexit, S.epoch, acc + (uint64_t)btot);
+        }
       }
     }
     if (lane == 0 && S.bad) atomicOr(&ctrl->zig_overflow, 2);
   }
   __syncthreads();
 
+  ZSTAMP(5);
   // ---- write my normals to their final slots
   uint64_t off = S.blk_off + (uint64_t)toff;
   pos = seg + entry;
@@ -336,6 +387,7 @@ __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_
   }
   // the last CTA publishes how many normals the parse produced
   if (tid == ZT - 1 && b == (int)gridDim.x - 1) ctrl->zig_avail = S.blk_off + (uint64_t)btot;
+  ZSTAMP(6);
   // the CTA that finishes last re-arms the bookkeeping and, if the parallel
   // parse could not be trusted (p ~ 1e-12 per word), redoes it serially
   __syncthreads();
@@ -479,19 +531,19 @@ int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, in
   switch (kind) {
     case PRNG_PHILOX:
       cudaFuncSetAttribute(zig_kernel<PRNG_PHILOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      zig_kernel<PRNG_PHILOX><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj);
+      zig_kernel<PRNG_PHILOX><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, b.dbg);
       break;
     case PRNG_MINSTD:
       cudaFuncSetAttribute(zig_kernel<PRNG_MINSTD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      zig_kernel<PRNG_MINSTD><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj);
+      zig_kernel<PRNG_MINSTD><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, b.dbg);
       break;
     case PRNG_PCG32:
       cudaFuncSetAttribute(zig_kernel<PRNG_PCG32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      zig_kernel<PRNG_PCG32><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj);
+      zig_kernel<PRNG_PCG32><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, b.dbg);
       break;
     default:
       cudaFuncSetAttribute(zig_kernel<PRNG_SFC64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      zig_kernel<PRNG_SFC64><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj);
+      zig_kernel<PRNG_SFC64><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, b.dbg);
       break;
   }
   (*launches)++;

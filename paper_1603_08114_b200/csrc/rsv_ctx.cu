@@ -204,8 +204,9 @@ static int create_impl(rsv_ctx *c, int device, int64_t T) {
   CK(cudaMalloc(&c->sfc_words, sizeof(uint64_t) * nw));
   CK(cudaMalloc(&c->sfc_snaps, sizeof(uint64_t) * 4 * (nw / SFC_SNAP + 2)));
   c->max_tiles = (int)(T / 64 + 16 * c->sm_count + 8);
+  if (c->max_tiles < (int)(momenta_words(T) / ZB) + 8) c->max_tiles = (int)(momenta_words(T) / ZB) + 8;
   if (const char *v = getenv("RSV_TRAJ_VARIANT")) c->variant = atoi(v);
-  if (getenv("RSV_TRAJ_STAMPS")) {
+  if (getenv("RSV_TRAJ_STAMPS") || getenv("RSV_ZIG_STAMPS")) {
     CK(cudaMalloc(&c->dbg, sizeof(unsigned long long) * 8 * c->max_tiles));
     CK(cudaMemset(c->dbg, 0, sizeof(unsigned long long) * 8 * c->max_tiles));
   }
@@ -393,6 +394,7 @@ static MomentaBufs mbufs(rsv_ctx *c) {
   b.sfc_snaps = c->sfc_snaps;
   b.normals = c->normals;
   b.bjump = c->bjump;
+  b.dbg = getenv("RSV_ZIG_STAMPS") ? c->dbg : nullptr;
   return b;
 }
 
@@ -435,7 +437,7 @@ static TrajArgs traj_args(rsv_ctx *c, double dt, int n_steps, int fuse, const Tr
   a.parts = c->parts;
   a.sfc_snaps = c->sfc_snaps;
   a.integrate_only = 0;
-  a.dbg = c->dbg;
+  a.dbg = getenv("RSV_TRAJ_STAMPS") ? c->dbg : nullptr;
   return a;
 }
 

@@ -14,6 +14,7 @@ struct MomentaBufs {
   uint64_t *sfc_snaps;  // SFC64 only: 4 * ((momenta_words(T) + 64) / SFC_SNAP + 1) words
   double *normals;      // T doubles
   const uint64_t *bjump;  // momenta_jump_bytes(T): per-CTA jump-ahead constants
+  unsigned long long *dbg;  // optional per-CTA %globaltimer stamps (development aid)
 };
 
 int64_t momenta_words(int64_t T);
