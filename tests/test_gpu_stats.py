@@ -1,0 +1,133 @@
+"""Statistical and physical properties of the GPU sampler (the reference's
+acceptance criteria c1-c5 and sampler tests, re-targeted at the CUDA path)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1603_08114_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+TRUE = P.Params(phi=0.97, mu=-1.0, xi=-0.3, sigma_eta_sq=0.05, sigma_u_sq=0.1)
+
+
+def _random_instance(seed, T):
+    rng = np.random.default_rng(seed)
+    params = P.Params(phi=float(rng.uniform(-0.9, 0.98)), mu=float(rng.normal()), xi=float(rng.normal(0, 0.5)),
+                      sigma_eta_sq=float(rng.uniform(0.02, 0.5)), sigma_u_sq=float(rng.uniform(0.05, 0.5)))
+    h = params.mu + rng.normal(0.0, 1.0, T)
+    y = np.exp(0.5 * h) * rng.standard_normal(T)
+    lrv = params.xi + h + math.sqrt(params.sigma_u_sq) * rng.standard_normal(T)
+    return h, params, P.Dataset.from_log_rv(y, lrv)
+
+
+def test_c1_gradient_matches_finite_differences(backend):
+    worst = 0.0
+    for seed in range(20):
+        h, params, data = _random_instance(1000 + seed, 64)
+        g = P.grad_neg_log_posterior(h, params, data, backend=backend)
+        fd = np.empty_like(h)
+        for i in range(h.size):
+            hp, hm = h.copy(), h.copy()
+            hp[i] += 1e-5
+            hm[i] -= 1e-5
+            fd[i] = -(O.log_posterior(hp, params, data.returns, data.log_rv) -
+                      O.log_posterior(hm, params, data.returns, data.log_rv)) / 2e-5
+        worst = max(worst, float(np.max(np.abs(fd - g)) / max(1.0, np.max(np.abs(g)))))
+    assert worst <= 1e-6
+
+
+def test_c2_reversibility(backend):
+    md = P.MDConfig(0.02, 50)
+    for seed in range(10):
+        h, params, data = _random_instance(2000 + seed, 256)
+        p = P.make_rng(seed).standard_normal(256)
+        fwd, div = P.integrate_trajectory(P.PhaseState(h, p), md, params, data, backend=backend)
+        assert not div
+        back, _ = P.integrate_trajectory(P.PhaseState(fwd.h, -fwd.p), md, params, data, backend=backend)
+        assert max(np.max(np.abs(back.h - h)), np.max(np.abs(-back.p - p))) <= 1e-9
+
+
+def test_c3_energy_error_is_second_order(backend):
+    truth = P.simulate_rsv(TRUE, 256, seed=30)
+    data, h0 = truth.dataset, truth.latent
+    rng = P.make_rng(31)
+    sums = {0.02: 0.0, 0.04: 0.0}
+    for _ in range(100):
+        p = rng.standard_normal(256)
+        for dt, k in ((0.02, 50), (0.04, 25)):
+            fin, div = P.integrate_trajectory(P.PhaseState(h0, p), P.MDConfig(dt, k), TRUE, data, backend=backend)
+            assert not div
+            dh = P.hamiltonian(fin, TRUE, data, backend=backend) - P.hamiltonian(P.PhaseState(h0, p), TRUE, data,
+                                                                                backend=backend)
+            sums[dt] += dh * dh
+    ratio = math.sqrt(sums[0.04]) / math.sqrt(sums[0.02])
+    assert 3.4 <= ratio <= 4.6
+
+
+def test_c4_exp_neg_dh_identity(backend):
+    data = P.simulate_rsv(TRUE, 500, seed=40).dataset
+    cfg = P.SamplerConfig(seed=41, md=P.MDConfig(0.03, 33), n_burnin=300, n_samples=2000, thin=1)
+    ch = P.run_chain(data, cfg, backend=backend)
+    x = np.exp(-ch.delta_h[np.isfinite(ch.delta_h)])
+    # batch-means standard error (autocorrelated series)
+    b = x[: len(x) // 20 * 20].reshape(20, -1).mean(axis=1)
+    se = b.std(ddof=1) / math.sqrt(len(b))
+    assert abs(x.mean() - 1.0) <= 4 * se + 1e-3
+
+
+def test_c5_two_site_marginals_match_quadrature(backend):
+    params = P.Params(phi=0.95, mu=-1.0, xi=-0.3, sigma_eta_sq=0.05, sigma_u_sq=0.1)
+    data = P.Dataset.from_log_rv(np.array([0.3, -0.2]), np.array([-1.1, -0.8]))
+    grid = np.linspace(-4.0, 2.0, 801)
+    h1, h2 = np.meshgrid(grid, grid, indexing="ij")
+    y1, y2 = data.returns
+    l1, l2 = data.log_rv
+    ld = (-0.5 * h1 - 0.5 * y1 * y1 * np.exp(-h1) - 0.5 * h2 - 0.5 * y2 * y2 * np.exp(-h2)
+          - (l1 - params.xi - h1) ** 2 / (2 * params.sigma_u_sq) - (l2 - params.xi - h2) ** 2 / (2 * params.sigma_u_sq)
+          - (1 - params.phi ** 2) * (h1 - params.mu) ** 2 / (2 * params.sigma_eta_sq)
+          - (h2 - params.mu - params.phi * (h1 - params.mu)) ** 2 / (2 * params.sigma_eta_sq))
+    w = np.exp(ld - ld.max())
+    w /= w.sum()
+    want = ((h1 * w).sum(), (h2 * w).sum())
+    ch = backend.chain(data, params)
+    ch.set_stream(P.stream_state(P.make_rng(6)))
+    ch.set_latent(data.log_rv.copy())
+    dense = np.empty((4000, 2))
+    for i in range(4000):
+        ch.hmc_update(0.05, 20)
+        dense[i] = ch.get_latent()
+    for j in range(2):
+        s = dense[:, j]
+        b = s[: len(s) // 20 * 20].reshape(20, -1).mean(axis=1)
+        se = b.std(ddof=1) / math.sqrt(len(b))
+        assert abs(s.mean() - want[j]) <= 4 * se + 1e-3, (j, s.mean(), want[j], se)
+
+
+def test_acceptance_monotone_in_step_size(backend):
+    h, params, data = _random_instance(4, 64)
+    rates = []
+    for dt, k in ((0.05, 12), (0.1, 6), (0.2, 3), (0.3, 2)):
+        ch = backend.chain(data, params)
+        ch.set_latent(h)
+        ch.set_stream(P.stream_state(P.make_rng(5)))
+        res = ch.hmc_update_many(dt, k, 400)
+        rates.append(np.mean([r.accept for r in res]))
+    for lo, hi in zip(rates[1:], rates[:-1]):
+        se = math.sqrt((lo * (1 - lo) + hi * (1 - hi)) / 400 + 1e-9)
+        assert lo <= hi + 3 * se
+
+
+def test_run_chain_bitwise_reproducible_and_storm(backend):
+    data = P.simulate_rsv(P.Params(0.95, -1.0, -0.3, 0.05, 0.1), 100, seed=24).dataset
+    cfg = P.SamplerConfig(seed=77, md=P.MDConfig(0.03, 20), n_burnin=20, n_samples=50, thin=2, store_latent=True)
+    a = P.run_chain(data, cfg, backend=backend)
+    b = P.run_chain(data, cfg, backend=backend)
+    for name in ("phi", "mu", "xi", "sigma_eta_sq", "sigma_u_sq", "delta_h"):
+        assert np.array_equal(getattr(a, name), getattr(b, name))
+    assert np.array_equal(a.latent, b.latent)
+    assert list(a.iters[:3]) == [20, 22, 24]
+    with pytest.raises(P.DivergenceStormError):
+        P.run_chain(data, P.SamplerConfig(seed=1, md=P.MDConfig(50.0, 5), n_burnin=0, n_samples=500), backend=backend)
