@@ -153,6 +153,30 @@ int rsv_measure_fp64_peak(rsv_ctx *ctx, double *tflops);
 /* Kernel launches issued by the context so far (gpu_launches evidence). */
 int64_t rsv_launch_count(const rsv_ctx *ctx);
 
+/* ---- time sharding: one chain split over several contexts / GPUs ----
+ * (SURVEY §8e).  A shard context holds the global sites [local_start,
+ * local_start + local_len) = the owned sites [lo, hi) plus a margin of at
+ * least n_steps + 1 sites on each side (clamped at the series ends); the
+ * margins are refreshed from the neighbours' owned sites before each
+ * proposal.  rsv_set_data / rsv_set_latent take the local slices.  Every
+ * shard draws the momenta of the whole series (same stream, same normals),
+ * runs the trajectory on its local range and publishes its totals; the host
+ * combines the shards' totals in rank order (bitwise independent of the
+ * shard count's scheduling), decides (same u on every shard) and applies. */
+typedef struct {
+  double part[14];     /* dH, H_old, H_new (variable parts), 5 old stats, 5 new stats, divergence flag */
+  double ends[4];      /* d_0 old, d_{T-1} old, d_0 new, d_{T-1} new (0 unless owned) */
+  uint64_t u_word;     /* raw word after the momenta: the Metropolis uniform */
+  uint64_t words_used; /* raw words consumed by the momenta */
+} rsv_shard_totals;
+int rsv_create_shard(rsv_ctx **out, int device, int64_t T_global, int64_t lo, int64_t hi, int64_t margin,
+                     int64_t *local_start, int64_t *local_len);
+int rsv_shard_propose(rsv_ctx *ctx, double step_size, int n_steps, int fuse, int stats, rsv_shard_totals *out);
+int rsv_shard_apply(rsv_ctx *ctx, int accept, int drew_uniform);
+/* copy [offset, offset + n) of the current local path to (to_ctx = 0) or
+ * from (to_ctx = 1) buf -- the halo exchange of a sharded chain */
+int rsv_latent_slice(rsv_ctx *ctx, int64_t offset, int64_t n, double *buf, int to_ctx, int on_device);
+
 /* ---- host side of the bit generators (no device needed) ----
  * Seeding from raw seed material (numpy.SeedSequence words), sequential
  * draws, and a numpy bitgen_t so numpy.random.Generator continues the same

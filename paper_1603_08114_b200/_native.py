@@ -38,6 +38,11 @@ class Result(ctypes.Structure):
                 ("u", ctypes.c_double)]
 
 
+class ShardTotals(ctypes.Structure):
+    _fields_ = [("part", ctypes.c_double * 14), ("ends", ctypes.c_double * 4), ("u_word", ctypes.c_uint64),
+                ("words_used", ctypes.c_uint64)]
+
+
 class Bitgen(ctypes.Structure):  # numpy/random/bitgen.h
     _fields_ = [("state", ctypes.c_void_p), ("next_uint64", ctypes.c_void_p),
                 ("next_uint32", ctypes.c_void_p), ("next_double", ctypes.c_void_p),
@@ -87,6 +92,14 @@ _SIGS = {
     "rsv_launch_count": (ctypes.c_int64, [_CTX]),
     "rsv_set_l2_flush": (ctypes.c_int, [_CTX, ctypes.c_int64]),
     "rsv_measure_fp64_peak": (ctypes.c_int, [_CTX, _D]),
+    "rsv_create_shard": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                                        ctypes.POINTER(ctypes.c_int64)]),
+    "rsv_shard_propose": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(ShardTotals)]),
+    "rsv_shard_apply": (ctypes.c_int, [_CTX, ctypes.c_int, ctypes.c_int]),
+    "rsv_latent_slice": (ctypes.c_int, [_CTX, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.c_int]),
     "rsv_stream_seed": (ctypes.c_int, [ctypes.POINTER(PrngState), ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
     "rsv_stream_next_u64": (ctypes.c_uint64, [ctypes.POINTER(PrngState)]),
     "rsv_stream_next_double": (ctypes.c_double, [ctypes.POINTER(PrngState)]),

@@ -577,7 +577,9 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     if (tile < n_tiles) stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0]);
   }
   __syncthreads();
-  const int64_t T = A.T;
+  const int64_t T = A.T;       // local series length (a shard's extended range, or the chain)
+  const int64_t goff = A.goff; // global index of local site 0
+  const int64_t Tg = A.Tg;     // global series length
   const int H = A.g.halo;
   const bool own_lane = (lane >= 1 && lane <= 30) || (lane == 0 && warp == 0) || (lane == 31 && warp == NW - 1);
   const int lw = warp * WSTEP + lane * R;  // my first site inside the window
@@ -620,10 +622,10 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     for (int r = 0; r < R; r++) {
       const int64_t gi = g0 + r;
       const bool in = gi >= lo_live && gi < hi_live;
-      const bool c = in && own_lane && gi >= t0 && gi < t1;
+      const bool c = in && own_lane && gi >= t0 && gi < t1 && gi >= A.own_lo && gi < A.own_hi;
       live |= (uint32_t)in << r;
       core |= (uint32_t)c << r;
-      endm |= (uint32_t)(gi == 0 || gi == T - 1) << r;
+      endm |= (uint32_t)(gi + goff == 0 || gi + goff == Tg - 1) << r;
       cm[r] = c ? ~0u : 0u;
       d[r] = in ? d[r] - s.mu : 0.0;
       p[r] = in ? p[r] : 0.0;
@@ -639,14 +641,14 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     double vold[6] = {0, 0, 0, 0, 0, 0};
     {
       const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      tile_energy<R, STATS>(d, p, av, lv, dl, core, edge, g0, s, S.tab, vold);
+      tile_energy<R, STATS>(d, p, av, lv, dl, core, edge, g0 + goff, s, S.tab, vold);
     }
     if (edge && !A.h_src) {
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if ((core >> r) & 1) {
-          if (g0 + r == 0) A.ctrl->ends_old[0] = d[r];
-          if (g0 + r == T - 1) A.ctrl->ends_old[1] = d[r];
+          if (g0 + r + goff == 0) A.ctrl->ends_old[0] = d[r];
+          if (g0 + r + goff == Tg - 1) A.ctrl->ends_old[1] = d[r];
         }
       }
     }
@@ -691,7 +693,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     double vnew[6] = {0, 0, 0, 0, 0, 0};
     {
       const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      tile_energy<R, STATS>(d, p, av, lv, dl, core, edge, g0, s, S.tab, vnew);
+      tile_energy<R, STATS>(d, p, av, lv, dl, core, edge, g0 + goff, s, S.tab, vnew);
     }
     if (core == (1u << R) - 1) {
 #pragma unroll
@@ -712,8 +714,8 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if ((core >> r) & 1) {
-          if (g0 + r == 0) A.ctrl->ends_new[0] = d[r];
-          if (g0 + r == T - 1) A.ctrl->ends_new[1] = d[r];
+          if (g0 + r + goff == 0) A.ctrl->ends_new[0] = d[r];
+          if (g0 + r + goff == Tg - 1) A.ctrl->ends_new[1] = d[r];
         }
       }
     }
@@ -892,6 +894,10 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   }
   DevControl *C = A.ctrl;
   C->tiles_done = 0;  // re-arm for the next launch
+  if (A.shard) {  // time-sharded chain: the host combines the shards' totals
+    for (int k = 0; k < TR_NV; k++) C->shard_parts[k] = tot[k];
+    return;
+  }
   const double cst = A.k.hconst;
   DevResult r;
   r.h_old = tot[1] + cst;

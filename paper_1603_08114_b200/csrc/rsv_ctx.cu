@@ -75,6 +75,10 @@ struct rsv_ctx {
   int64_t launches = 0;
   bool has_data = false, has_params = false, has_latent = false;
   int kind = PRNG_PHILOX;
+  // time sharding: this context holds global sites [goff, goff + T) of a
+  // series of Tg sites and owns [goff + own_lo, goff + own_hi)
+  int64_t Tg = 0, goff = 0, own_lo = 0, own_hi = 0;
+  bool shard = false;
   int variant = 11;  // persistent, TMA-staged, 4 sites x 256 threads, 2 CTAs/SM (see leapfrog.cu)
   unsigned long long *dbg = nullptr;  // RSV_TRAJ_STAMPS=1: per-tile timestamps
 
@@ -177,9 +181,12 @@ int rsv_destroy(rsv_ctx *c) {
   return 0;
 }
 
-static int create_impl(rsv_ctx *c, int device, int64_t T) {
+// T: local series length; Tg: global length (== T unless time-sharded: the
+// momenta are drawn for the whole series so every shard sees the same stream)
+static int create_impl(rsv_ctx *c, int device, int64_t T, int64_t Tg) {
   c->device = device;
   c->T = T;
+  c->Tg = Tg;
   CK(cudaSetDevice(device));
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
@@ -193,18 +200,21 @@ static int create_impl(rsv_ctx *c, int device, int64_t T) {
     CK(cudaMalloc(&c->hbuf[i], tb));
     CK(cudaMemset(c->hbuf[i], 0, tb));
   }
-  double **bufs[] = {&c->y, &c->a, &c->lrv, &c->normals, &c->sh, &c->sp, &c->sh2, &c->sp2};
+  double **bufs[] = {&c->y, &c->a, &c->lrv, &c->sh, &c->sp, &c->sh2, &c->sp2};
   for (double **b : bufs) {
     CK(cudaMalloc(b, tb));
     CK(cudaMemset(*b, 0, tb));
   }
-  CK(cudaMalloc(&c->zscratch, momenta_scratch_bytes(T)));
-  CK(cudaMemset(c->zscratch, 0, momenta_scratch_bytes(T)));  // look-back status words (epoch-tagged)
-  const int64_t nw = momenta_words(T) + 64;
+  const size_t tbg = sizeof(double) * (size_t)((Tg + 7) / 8 * 8);
+  CK(cudaMalloc(&c->normals, tbg));
+  CK(cudaMemset(c->normals, 0, tbg));
+  CK(cudaMalloc(&c->zscratch, momenta_scratch_bytes(Tg)));
+  CK(cudaMemset(c->zscratch, 0, momenta_scratch_bytes(Tg)));  // look-back status words (epoch-tagged)
+  const int64_t nw = momenta_words(Tg) + 64;
   CK(cudaMalloc(&c->sfc_words, sizeof(uint64_t) * nw));
   CK(cudaMalloc(&c->sfc_snaps, sizeof(uint64_t) * 4 * (nw / SFC_SNAP + 2)));
   c->max_tiles = (int)(T / 64 + 16 * c->sm_count + 8);
-  if (c->max_tiles < (int)(momenta_words(T) / ZB) + 8) c->max_tiles = (int)(momenta_words(T) / ZB) + 8;
+  if (c->max_tiles < (int)(momenta_words(Tg) / ZB) + 8) c->max_tiles = (int)(momenta_words(Tg) / ZB) + 8;
   if (const char *v = getenv("RSV_TRAJ_VARIANT")) c->variant = atoi(v);
   if (getenv("RSV_TRAJ_STAMPS") || getenv("RSV_ZIG_STAMPS")) {
     CK(cudaMalloc(&c->dbg, sizeof(unsigned long long) * 8 * c->max_tiles));
@@ -224,8 +234,8 @@ static int create_impl(rsv_ctx *c, int device, int64_t T) {
   memset(c->h_ctrl, 0, sizeof(DevControl));
   c->h_ctrl->stream.kind = PRNG_PHILOX;
   CK(cudaMemcpy(c->ctrl, c->h_ctrl, sizeof(DevControl), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&c->bjump, momenta_jump_bytes(T)));
-  if (momenta_init(c->stream, c->bjump, T)) return fail(c, RSV_E_CUDA, "momenta table init failed");
+  CK(cudaMalloc(&c->bjump, momenta_jump_bytes(Tg)));
+  if (momenta_init(c->stream, c->bjump, Tg)) return fail(c, RSV_E_CUDA, "momenta table init failed");
   c->launches += 2;
   CK(cudaStreamSynchronize(c->stream));
   return 0;
@@ -241,7 +251,9 @@ int rsv_create(rsv_ctx **out, int device, int64_t T) {
     return fail(nullptr, RSV_E_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
   if (device < 0 || device >= ndev) return fail(nullptr, RSV_E_INVALID, "device %d out of range", device);
   rsv_ctx *c = new rsv_ctx();
-  const int r = create_impl(c, device, T);
+  c->own_lo = 0;
+  c->own_hi = T;
+  const int r = create_impl(c, device, T, T);
   if (r) {
     g_err = c->err;
     rsv_destroy(c);
@@ -408,11 +420,11 @@ int rsv_refresh_momenta(rsv_ctx *c, double *p_out, int on_device) {
   CK(cudaSetDevice(c->device));
   int l = 0;
   CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
-  if (launch_momenta(mbufs(c), c->kind, c->T, c->stream, &l)) return fail(c, RSV_E_CUDA, "momenta launch failed");
+  if (launch_momenta(mbufs(c), c->kind, c->Tg, c->stream, &l)) return fail(c, RSV_E_CUDA, "momenta launch failed");
   if (launch_momenta_advance(mbufs(c), c->stream, &l)) return fail(c, RSV_E_CUDA, "advance launch failed");
   c->launches += l;
   int r;
-  if ((r = copy_out(c, p_out, c->normals, c->T, on_device))) return r;
+  if ((r = copy_out(c, p_out, c->normals, c->Tg, on_device))) return r;
   if ((r = pull_ctrl(c))) return r;
   return check_err_bits(c);
 }
@@ -429,7 +441,12 @@ static TrajArgs traj_args(rsv_ctx *c, double dt, int n_steps, int fuse, const Tr
   a.g = g;
   a.hbuf0 = c->hbuf[0];
   a.hbuf1 = c->hbuf[1];
-  a.p_in = c->normals;
+  a.p_in = c->normals + c->goff;
+  a.goff = c->goff;
+  a.Tg = c->Tg;
+  a.own_lo = c->own_lo;
+  a.own_hi = c->own_hi;
+  a.shard = c->shard ? 1 : 0;
   a.a = c->a;
   a.lrv = c->lrv;
   a.prm = c->prm;
@@ -474,7 +491,7 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   int l = 0;
   bool ok = true;
   if (k.timing) cudaEventRecordWithFlags(c->evpool[0], c->stream, cudaEventRecordExternal);
-  ok &= launch_momenta(mbufs(c), k.kind, c->T, c->stream, &l) == 0;
+  ok &= launch_momenta(mbufs(c), k.kind, c->Tg, c->stream, &l) == 0;
   if (k.timing) cudaEventRecordWithFlags(c->evpool[1], c->stream, cudaEventRecordExternal);
   ok &= launch_trajectory(cg->args, c->stream, &l) == 0;
   if (k.timing) cudaEventRecordWithFlags(c->evpool[2], c->stream, cudaEventRecordExternal);
@@ -902,6 +919,112 @@ int rsv_debug_stamps(rsv_ctx *c, unsigned long long *out, int max_tiles) {
   const int n = max_tiles < c->max_tiles ? max_tiles : c->max_tiles;
   CK(cudaMemcpy(out, c->dbg, sizeof(unsigned long long) * 8 * n, cudaMemcpyDeviceToHost));
   return 0;
+}
+
+// ---- time sharding (one chain split over several contexts / GPUs) ----------
+__global__ void shard_apply_kernel(DevControl *C, int accept, int drew) {
+  if (threadIdx.x || blockIdx.x) return;
+  const uint64_t consumed = C->zig_used + (drew ? 1 : 0);
+  if (C->stream.kind == PRNG_PCG32) {
+    uint64_t q = C->seq_next;
+    if (drew) { q = q * PCG_MULT + C->stream.s[1]; q = q * PCG_MULT + C->stream.s[1]; }
+    C->seq_state = q;
+  } else if (C->stream.kind == PRNG_MINSTD) {
+    uint64_t q = C->seq_next;
+    if (drew) q = mod31(mod31(mod31(q * MINSTD_A) * MINSTD_A) * MINSTD_A);
+    C->seq_state = q;
+  }
+  C->stream.pos += consumed;
+  if (accept) C->cur ^= 1;
+}
+
+int rsv_create_shard(rsv_ctx **out, int device, int64_t Tg, int64_t lo, int64_t hi, int64_t margin,
+                     int64_t *local_start, int64_t *local_len) {
+  if (!out) return fail(nullptr, RSV_E_INVALID, "out is null");
+  *out = nullptr;
+  if (Tg < 2 || lo < 0 || hi > Tg || lo >= hi || margin < 0)
+    return fail(nullptr, RSV_E_INVALID, "bad shard [%lld, %lld) of %lld", (long long)lo, (long long)hi, (long long)Tg);
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, RSV_E_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(nullptr, RSV_E_INVALID, "device %d out of range", device);
+  // local range: the owned sites plus `margin` on each side, starting on a
+  // multiple of 8 sites so tiles stay 64 B aligned in the global momenta
+  int64_t ls = lo - margin;
+  ls = ls < 0 ? 0 : ls / 8 * 8;
+  int64_t le = hi + margin;
+  le = le > Tg ? Tg : le;
+  rsv_ctx *c = new rsv_ctx();
+  c->shard = true;
+  c->goff = ls;
+  c->own_lo = lo - ls;
+  c->own_hi = hi - ls;
+  const int r = create_impl(c, device, le - ls, Tg);
+  if (r) {
+    g_err = c->err;
+    rsv_destroy(c);
+    return r;
+  }
+  if (c->variant < 9) c->variant = 11;  // the persistent kernel carries the shard indexing
+  if (local_start) *local_start = ls;
+  if (local_len) *local_len = le - ls;
+  *out = c;
+  return 0;
+}
+
+int rsv_shard_propose(rsv_ctx *c, double dt, int n_steps, int fuse, int stats, rsv_shard_totals *out) {
+  if (!c || !out) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->shard) return fail(c, RSV_E_STATE, "not a shard context (rsv_create_shard)");
+  int r;
+  if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
+  CK(cudaSetDevice(c->device));
+  rsv_ctx::Cached *cg = nullptr;
+  int kpl = 0;
+  if ((r = get_graph(c, dt, n_steps, fuse, stats, &cg, &kpl))) return r;
+  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
+  CK(cudaGraphLaunch(cg->exec, c->stream));
+  c->launches += kpl;
+  if ((r = pull_ctrl(c))) return r;
+  if ((r = check_err_bits(c))) return r;
+  const DevControl &C = *c->h_ctrl;
+  for (int k = 0; k < TR_NV; k++) out->part[k] = C.shard_parts[k];
+  const bool own_first = c->goff + c->own_lo == 0, own_last = c->goff + c->own_hi == c->Tg;
+  out->ends[0] = own_first ? C.ends_old[0] : 0.0;
+  out->ends[1] = own_last ? C.ends_old[1] : 0.0;
+  out->ends[2] = own_first ? C.ends_new[0] : 0.0;
+  out->ends[3] = own_last ? C.ends_new[1] : 0.0;
+  out->u_word = C.u_word;
+  out->words_used = C.zig_used;
+  return 0;
+}
+
+int rsv_shard_apply(rsv_ctx *c, int accept, int drew) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  CK(cudaSetDevice(c->device));
+  shard_apply_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, accept, drew);
+  c->launches++;
+  CK(cudaGetLastError());
+  return sync(c);
+}
+
+int rsv_latent_slice(rsv_ctx *c, int64_t offset, int64_t n, double *buf, int to_ctx, int on_device) {
+  if (!c || (!buf && n > 0)) return fail(c, RSV_E_INVALID, "null argument");
+  if (offset < 0 || n < 0 || offset + n > c->T) return fail(c, RSV_E_INVALID, "slice out of range");
+  if (!c->has_latent) return fail(c, RSV_E_STATE, "latent path not set");
+  CK(cudaSetDevice(c->device));
+  int r;
+  if ((r = pull_ctrl(c))) return r;
+  double *h = c->hbuf[c->h_ctrl->cur & 1] + offset;
+  if (n == 0) return 0;
+  if (to_ctx) {
+    CK(cudaMemcpyAsync(h, buf, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       c->stream));
+  } else {
+    CK(cudaMemcpyAsync(buf, h, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       c->stream));
+  }
+  return sync(c);
 }
 
 int rsv_set_timing(rsv_ctx *c, int enable) {

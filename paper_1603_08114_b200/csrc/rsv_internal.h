@@ -70,6 +70,7 @@ struct DevControl {
   uint64_t seq_state, seq_next;
   // momenta kernel bookkeeping (reset by its last CTA: no memsets per draw)
   uint32_t zig_ticket, zig_done, zig_epoch, pad4;
+  double shard_parts[TR_NV];  // time-sharded chains: this shard's totals (TilePart order)
 };
 
 }  // namespace rsv

@@ -50,8 +50,11 @@ TrajConsts traj_consts(const DevParams &P, double dt);
 
 struct TrajArgs {
   TrajConsts k;
-  int64_t T;
+  int64_t T;            // local series length
   int64_t Tpad;         // arrays are allocated (and zero padded) to Tpad = roundup(T, 8)
+  int64_t goff, Tg;     // global index of local site 0, global length (time sharding)
+  int64_t own_lo, own_hi;  // local sites this context owns (reductions, write-back)
+  int shard;            // 1: publish totals to ctrl->shard_parts instead of the Metropolis step
   int n_steps;
   int fuse;
   double dt;

@@ -1,0 +1,304 @@
+"""One long chain split over several GPUs along the time axis.
+
+The reference runs one chain on one CPU (`sampler.py:144-167`, `run_chain`
+`sampler.py:291-358`); for long series (configs 3 and 5 of BASELINE.json) the
+time axis is partitioned across the ranks of a process group:
+
+* rank r owns the contiguous sites [lo_r, hi_r) and keeps a local copy of
+  [lo_r - M, hi_r + M) with a margin M >= n_steps + 1 (clamped at the ends);
+* before a proposal the margins are refreshed from the neighbours' owned sites
+  (one halo exchange of M doubles per neighbour per *trajectory*: the
+  trajectory kernel's tiles already carry an (L+1)-site halo, so the owned
+  sites come out exactly as a per-step exchange would give them);
+* every rank draws the momenta of the whole series from the same stream, runs
+  the trajectory on its local range and publishes its partial sums of
+  dH, H_old, H_new and the theta statistics;
+* the partials are all-gathered and combined with an exactly rounded sum
+  (math.fsum), so every rank takes the same Metropolis decision with the same
+  uniform and the result does not depend on the number of ranks' reduction
+  order; every rank then applies it (flip current path / advance stream).
+
+`ShardedChain` is the per-rank object.  `hmc_update_distributed` drives it
+over a `torch.distributed` process group (NCCL on GPUs, gloo on CPUs);
+`hmc_update_local` drives several shards held by one process (tests, or a
+single GPU emulating a sharded layout).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .integrator import DH_DIVERGENCE_THRESHOLD
+from .model import Dataset, Params
+
+TOTALS = 14 + 4 + 2  # part[14], ends[4], u_word, words_used (as float64 bit patterns)
+
+
+def shard_bounds(T: int, world: int, align: int = 8) -> list[tuple[int, int]]:
+    """Contiguous owned ranges [lo, hi) of nearly equal size (boundaries on
+    multiples of `align` sites except the last)."""
+    if world < 1 or T < 2 * world:
+        raise ValueError(f"cannot split {T} sites over {world} ranks")
+    edges = [0]
+    for r in range(1, world):
+        e = (T * r // world) // align * align
+        edges.append(max(e, edges[-1] + 1))
+    edges.append(T)
+    return [(edges[r], edges[r + 1]) for r in range(world)]
+
+
+def local_range(T: int, lo: int, hi: int, margin: int) -> tuple[int, int]:
+    """Same rule as rsv_create_shard: start rounded down to a multiple of 8."""
+    ls = lo - margin
+    ls = 0 if ls < 0 else ls // 8 * 8
+    return ls, min(T, hi + margin)
+
+
+class CudaShard:
+    """Shard context on a GPU (rsv_create_shard / rsv_shard_* of the C ABI)."""
+
+    def __init__(self, T: int, lo: int, hi: int, margin: int, device: int = 0):
+        self._lib = N.lib()
+        h = ctypes.c_void_p()
+        ls, ln = ctypes.c_int64(), ctypes.c_int64()
+        N.check(self._lib.rsv_create_shard(ctypes.byref(h), int(device), int(T), int(lo), int(hi), int(margin),
+                                           ctypes.byref(ls), ctypes.byref(ln)))
+        self.ctx = h.value
+        self.local_start, self.local_len = int(ls.value), int(ln.value)
+
+    def _ck(self, code):
+        N.check(code, self.ctx)
+
+    def close(self):
+        if self.ctx:
+            self._lib.rsv_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_data(self, y, lrv):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        lrv = np.ascontiguousarray(lrv, dtype=np.float64)
+        self._ck(self._lib.rsv_set_data(self.ctx, y.ctypes.data, lrv.ctypes.data, 0))
+
+    def set_params(self, params: Params):
+        self._ck(self._lib.rsv_set_params(self.ctx, ctypes.byref(N.to_params(params))))
+
+    def set_latent(self, h):
+        h = np.ascontiguousarray(h, dtype=np.float64)
+        self._ck(self._lib.rsv_set_latent(self.ctx, h.ctypes.data, 0))
+
+    def get_latent(self) -> np.ndarray:
+        out = np.empty(self.local_len)
+        self._ck(self._lib.rsv_get_latent(self.ctx, out.ctypes.data, 0))
+        return out
+
+    def set_stream(self, st):
+        self._ck(self._lib.rsv_set_prng_state(self.ctx, ctypes.byref(st)))
+
+    def get_stream(self):
+        st = N.PrngState()
+        self._ck(self._lib.rsv_get_prng_state(self.ctx, ctypes.byref(st)))
+        return st
+
+    def slice_out(self, offset: int, n: int) -> np.ndarray:
+        out = np.empty(n)
+        if n:
+            self._ck(self._lib.rsv_latent_slice(self.ctx, int(offset), int(n), out.ctypes.data, 0, 0))
+        return out
+
+    def slice_in(self, offset: int, buf: np.ndarray):
+        buf = np.ascontiguousarray(buf, dtype=np.float64)
+        if buf.size:
+            self._ck(self._lib.rsv_latent_slice(self.ctx, int(offset), int(buf.size), buf.ctypes.data, 1, 0))
+
+    def propose(self, step_size: float, n_steps: int, fuse: bool, stats: bool) -> np.ndarray:
+        t = N.ShardTotals()
+        self._ck(self._lib.rsv_shard_propose(self.ctx, float(step_size), int(n_steps), int(bool(fuse)),
+                                             int(bool(stats)), ctypes.byref(t)))
+        v = np.empty(TOTALS)
+        v[:14] = list(t.part)
+        v[14:18] = list(t.ends)
+        v[18:20] = np.array([t.u_word, t.words_used], dtype=np.uint64).view(np.float64)
+        return v
+
+    def apply(self, accept: bool, drew: bool):
+        self._ck(self._lib.rsv_shard_apply(self.ctx, int(bool(accept)), int(bool(drew))))
+
+
+@dataclass
+class Decision:
+    accept: bool
+    diverged: bool
+    delta_h: float
+    h_old: float
+    h_new: float
+    drew: bool
+    u: float
+    stats_kept: np.ndarray  # 7 moments of the kept path (layout of rsv_suff_stats)
+
+
+def h_constant(params: Params, T: int) -> float:
+    """theta-only part of H (model.py:134-163 log terms and 0.5*T*mu)."""
+    phi, se2, su2 = params.phi, params.sigma_eta_sq, params.sigma_u_sq
+    return (0.5 * T * params.mu + 0.5 * T * math.log(su2) + 0.5 * math.log(se2 / (1.0 - phi * phi))
+            + 0.5 * (T - 1) * math.log(se2))
+
+
+def combine(totals: list[np.ndarray], params: Params, T: int) -> Decision:
+    """Metropolis step of sampler.py:155-167 on the shards' partial sums.
+    math.fsum is exactly rounded, so the result is independent of the order
+    and grouping of the shards."""
+    tot = np.array(totals)
+    s = [math.fsum(tot[:, k]) for k in range(18)]
+    u_word = int(tot[0, 18:19].view(np.uint64)[0])
+    if any(int(t[18:19].view(np.uint64)[0]) != u_word for t in tot):
+        raise RuntimeError("shards drew different momenta streams")
+    c = h_constant(params, T)
+    dh = s[0]
+    flagged = s[13] > 0.0
+    drew = False
+    u = float("nan")
+    accept = False
+    if flagged or not math.isfinite(dh) or abs(dh) > DH_DIVERGENCE_THRESHOLD:
+        diverged, delta_h = True, math.inf
+    else:
+        diverged, delta_h = False, dh
+        u = float(u_word >> 11) * (1.0 / 9007199254740992.0)
+        drew = True
+        accept = dh <= 0.0 or u < math.exp(-dh)
+    ends_old, ends_new = (s[14], s[15]), (s[16], s[17])
+    kept = np.array([*(ends_new if accept else ends_old), *(s[8:13] if accept else s[3:8])])
+    return Decision(accept, diverged, delta_h, s[1] + c, s[2] + c, drew, u, kept)
+
+
+class ShardedChain:
+    """Rank-local part of a time-sharded chain."""
+
+    def __init__(self, data: Dataset, params: Params, rank: int, world: int, margin: int = 64, device: int = 0,
+                 shard_factory=None):
+        self.T = data.length
+        self.rank, self.world = rank, world
+        self.bounds = shard_bounds(self.T, world)
+        self.lo, self.hi = self.bounds[rank]
+        self.margin = margin
+        factory = shard_factory or (lambda T, lo, hi, m: CudaShard(T, lo, hi, m, device))
+        self.shard = factory(self.T, self.lo, self.hi, margin)
+        self.ls = self.shard.local_start
+        self.le = self.ls + self.shard.local_len
+        self.shard.set_data(data.returns[self.ls:self.le], data.log_rv[self.ls:self.le])
+        self.params = params
+        self.shard.set_params(params)
+        self.halo_valid = False
+
+    # -- state --
+    def set_params(self, params: Params):
+        self.params = params
+        self.shard.set_params(params)
+
+    def set_latent_global(self, h: np.ndarray):
+        self.shard.set_latent(np.asarray(h, dtype=np.float64)[self.ls:self.le])
+        self.halo_valid = True
+
+    def owned_latent(self) -> np.ndarray:
+        return self.shard.get_latent()[self.lo - self.ls:self.hi - self.ls]
+
+    def set_stream(self, st):
+        self.shard.set_stream(st)
+
+    def get_stream(self):
+        return self.shard.get_stream()
+
+    # -- halo exchange --
+    def halo_sizes(self, r: int) -> tuple[int, int]:
+        lo, hi = self.bounds[r]
+        ls, le = local_range(self.T, lo, hi, self.margin)
+        return lo - ls, le - hi
+
+    def halo_out(self) -> tuple[np.ndarray, np.ndarray]:
+        """(to the left neighbour, to the right neighbour): my owned sites
+        that fall in their margins."""
+        left = right = np.empty(0)
+        if self.rank > 0:
+            n = self.halo_sizes(self.rank - 1)[1]
+            left = self.shard.slice_out(self.lo - self.ls, n)
+        if self.rank < self.world - 1:
+            n = self.halo_sizes(self.rank + 1)[0]
+            right = self.shard.slice_out(self.hi - self.ls - n, n)
+        return left, right
+
+    def halo_in(self, from_left: np.ndarray, from_right: np.ndarray):
+        if self.rank > 0:
+            self.shard.slice_in(0, from_left)
+        if self.rank < self.world - 1:
+            self.shard.slice_in(self.hi - self.ls, from_right)
+        self.halo_valid = True
+
+    # -- proposal phases --
+    def propose(self, step_size: float, n_steps: int, fuse: bool = False, stats: bool = True) -> np.ndarray:
+        if n_steps + 1 > self.margin:
+            raise ValueError(f"n_steps={n_steps} needs a margin of at least {n_steps + 1} (have {self.margin})")
+        return self.shard.propose(step_size, n_steps, fuse, stats)
+
+    def apply(self, d: Decision):
+        self.shard.apply(d.accept, d.drew)
+        if d.accept:
+            self.halo_valid = False
+
+
+def hmc_update_local(chains: list[ShardedChain], step_size: float, n_steps: int, fuse: bool = False,
+                     stats: bool = True) -> Decision:
+    """One proposal of a sharded chain whose shards live in this process."""
+    if not all(c.halo_valid for c in chains):
+        outs = [c.halo_out() for c in chains]
+        for r, c in enumerate(chains):
+            c.halo_in(outs[r - 1][1] if r > 0 else np.empty(0),
+                      outs[r + 1][0] if r < len(chains) - 1 else np.empty(0))
+    totals = [c.propose(step_size, n_steps, fuse, stats) for c in chains]
+    d = combine(totals, chains[0].params, chains[0].T)
+    for c in chains:
+        c.apply(d)
+    return d
+
+
+def hmc_update_distributed(chain: ShardedChain, step_size: float, n_steps: int, fuse: bool = False,
+                           stats: bool = True, group=None, device=None) -> Decision:
+    """One proposal of a sharded chain over a torch.distributed process group.
+    Halo: point-to-point send/recv with the neighbours; totals: all_gather."""
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cpu") if device is None else torch.device(device)
+    r, w = chain.rank, chain.world
+    flag = torch.tensor([0 if chain.halo_valid else 1], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if int(flag.item()):
+        left, right = chain.halo_out()
+        reqs = []
+        recv_l = recv_r = None
+        if r > 0:
+            reqs.append(dist.isend(torch.from_numpy(left).to(dev), r - 1, group=group))
+            recv_l = torch.empty(chain.halo_sizes(r)[0], dtype=torch.float64, device=dev)
+            reqs.append(dist.irecv(recv_l, r - 1, group=group))
+        if r < w - 1:
+            reqs.append(dist.isend(torch.from_numpy(right).to(dev), r + 1, group=group))
+            recv_r = torch.empty(chain.halo_sizes(r)[1], dtype=torch.float64, device=dev)
+            reqs.append(dist.irecv(recv_r, r + 1, group=group))
+        for q in reqs:
+            q.wait()
+        chain.halo_in(recv_l.cpu().numpy() if recv_l is not None else np.empty(0),
+                      recv_r.cpu().numpy() if recv_r is not None else np.empty(0))
+    mine = torch.from_numpy(chain.propose(step_size, n_steps, fuse, stats)).to(dev)
+    allt = [torch.empty_like(mine) for _ in range(w)]
+    dist.all_gather(allt, mine, group=group)
+    d = combine([t.cpu().numpy() for t in allt], chain.params, chain.T)
+    chain.apply(d)
+    return d

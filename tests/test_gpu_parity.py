@@ -240,3 +240,32 @@ def test_suff_stats_vs_oracle(backend):
     got = ch.suff_stats(-9.0, -0.3)
     want = O.suff_stats(z["h_true"], data.log_rv, -9.0, -0.3)
     assert np.allclose(got, want, rtol=1e-12, atol=1e-9)
+
+
+# ---------------------------------------------------------------- time sharding
+@pytest.mark.parametrize("world,T", [(2, 5000), (3, 70001), (4, 1 << 18)])
+def test_sharded_chain_on_one_gpu_matches_single_context(backend, world, T):
+    truth = P.simulate_rsv(THETA, T, seed=9)
+    data = truth.dataset
+    shards = [P.ShardedChain(data, THETA, r, world, margin=32) for r in range(world)]
+    st0 = P.stream_state(P.make_rng(21, "pcg32"))
+    for c in shards:
+        c.set_latent_global(truth.latent)
+        c.set_stream(st0)
+    single = backend.chain(data, THETA)
+    single.set_latent(truth.latent)
+    single.set_stream(st0)
+    H = abs(P.hamiltonian(P.PhaseState(truth.latent, np.zeros(T)), THETA, data, backend=backend))
+    for i in range(8):
+        d = P.hmc_update_local(shards, 0.01, 20)
+        r = single.hmc_update(0.01, 20)
+        assert d.accept == bool(r.accept), i
+        if r.diverged:
+            assert math.isinf(d.delta_h)
+        else:
+            assert abs(d.delta_h - r.delta_h) <= 1e-13 * H, (i, d.delta_h, r.delta_h)
+    h = np.concatenate([c.owned_latent() for c in shards])
+    assert _rel(h, single.get_latent()) <= 1e-12
+    assert all(int(c.get_stream().pos) == int(single.get_stream().pos) for c in shards)
+    for c in shards:
+        c.shard.close()
