@@ -6,9 +6,11 @@ trajectories/s.  One "step" is one full HMC proposal of the reference's
 hmc_update_volatility (sampler.py:144-167): numpy-exact momenta, H_old, an
 L-step leapfrog trajectory, H_new, dH and the Metropolis test -- on one
 synthetic series of T sites (config 3 of BASELINE.json at N=1: a single long
-chain, T=2^20, L=20, dt=0.02, pcg32).  With N>1 (torchrun) every rank runs an
-independent replica chain (weak scaling; the time-sharded single chain is
-not implemented yet).
+chain, T=2^20, L=20, dt=0.02, pcg32).  With N>1 (torchrun) the SAME chain is
+time-sharded over the N GPUs (strong scaling): per proposal one
+margin-halo exchange after an accepted move (NCCL send/recv), local momenta +
+trajectory per GPU, an all_gather of the shards' energy totals and the same
+Metropolis decision on every rank (sharded.py).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -56,6 +58,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the time-sharded path even at N=1 (exercises the N>1 code on one GPU)")
     return ap.parse_args()
 
 
@@ -172,10 +176,15 @@ def main():
         return
     import torch
     dist = None
-    if ws > 1:
+    if ws > 1 or args.sharded:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            dist.init_process_group("nccl", rank=0, world_size=1)
+        else:
+            dist.init_process_group("nccl")
     import paper_1603_08114_b200 as P
 
     theta = P.Params(**THETA)
@@ -183,6 +192,11 @@ def main():
     truth = P.simulate_rsv(theta, T, seed=0)
     data = truth.dataset
     be = P.CudaBackend(local)
+    if dist is not None:
+        sharded_run(args, P, theta, truth, rank, ws, local, dist, torch)
+        be.close()
+        dist.destroy_process_group()
+        return
     ch = be.chain(data, theta)
     ch.set_latent(truth.latent)
     ch.set_stream(P.stream_state(P.make_rng(1 + rank, args.prng)))
@@ -199,8 +213,6 @@ def main():
     while time.perf_counter() - t_load < 0.4:
         ch.hmc_update_many(dt, L, 20, results=False)
     ch.set_timing(True)
-    if dist:
-        dist.barrier()
     torch.cuda.synchronize(local)
     n0 = ch.launch_count()
     t_wall = time.perf_counter()
@@ -215,11 +227,7 @@ def main():
     ch.set_l2_flush(0)
     accept_rate = float(np.mean([r.accept for r in res]))
     step_s = step_ms * 1e-3
-    if dist:
-        t = torch.tensor([step_s, traj_ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_s, traj_ms = float(t[0]), float(t[1])
-    value = ws * T * L / step_s
+    value = T * L / step_s
 
     # ---------------- roofline of the dominant kernel (trajectory, FP64-bound)
     fp64_peak = ch.fp64_peak_tflops()
@@ -241,19 +249,13 @@ def main():
     P.hmc_update_volatility(h, theta, data, md, rng, backend=be)  # warm
     e2e_steps = max(3, min(args.steps, 20))
     n_acc = 0
-    if dist:
-        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         h, acc, _ = P.hmc_update_volatility(h, theta, data, md, rng, backend=be)
         n_acc += int(acc)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if dist:
-        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
     state_bytes = 48 + 40  # stream state + params structs
-    e2e = {"value": ws * T * L / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * T + state_bytes,
+    e2e = {"value": T * L / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * T + state_bytes,
            "d2h_bytes_per_step": int(8 * T * n_acc / e2e_steps) + 48 + 56,
            "path": "paper_1603_08114_b200.hmc_update_volatility(h numpy[pinned], params, data, md, rng) -> C ABI"}
 
@@ -304,15 +306,15 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (simulate_rsv, theta of SURVEY §8d, seed 0)",
             "config": {"workload": f"config 3 at N=1 per GPU: single chain T={T}, L={L}, dt={dt}, {args.prng}; "
                                    "one step = one full HMC proposal (momenta + H_old + trajectory + H_new + "
                                    "Metropolis), device-resident, CUDA graph",
                        "T": T, "L": L, "dt": dt, "prng": args.prng,
-                       "parallelism": "single" if ws == 1 else f"replicas x{ws}",
+                       "parallelism": "single chain, 1 GPU",
                        "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB memset, not timed)"},
-            "trajectories_per_s": ws / step_s, "accept_rate": accept_rate,
+            "trajectories_per_s": 1.0 / step_s, "accept_rate": accept_rate,
             "breakdown_ms": {"momenta": mom_ms, "trajectory": traj_ms, "proposal": step_s * 1e3},
             "bracket_ms_per_step_incl_flush": bracket_s * 1e3 / args.steps,
             "e2e": e2e,
@@ -326,8 +328,65 @@ def main():
         line.update(extra)
         print(json.dumps(line), flush=True)
     be.close()
-    if dist:
-        dist.destroy_process_group()
+
+
+def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
+    """N > 1 (config 3): ONE chain of T sites time-sharded over the N GPUs
+    (strong scaling).  Per proposal: halo exchange of the margins after an
+    accepted move (NCCL send/recv), local momenta + trajectory on each GPU,
+    an all_gather of the shards' totals (NCCL) and the same Metropolis
+    decision on every rank.  Device-timed with CUDA events on the current
+    stream between barrier+synchronize brackets; max over ranks."""
+    T, L, dt = args.T, args.L, args.dt
+    dev = f"cuda:{local}"
+    margin = max(64, (L + 1 + 7) // 8 * 8)
+    chain = P.ShardedChain(truth.dataset, theta, rank, ws, margin=margin, device=local)
+    chain.set_latent_global(truth.latent)
+    chain.set_stream(P.stream_state(P.make_rng(1, args.prng)))
+    for _ in range(max(3, args.warmup)):
+        P.hmc_update_distributed(chain, dt, L, stats=False, device=dev)
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    t_load = time.perf_counter()
+    n_load = 0
+    while n_load < 5 or time.perf_counter() - t_load < 0.4:
+        P.hmc_update_distributed(chain, dt, L, stats=False, device=dev)
+        n_load += 1
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = chain.shard.launch_count()
+    e0.record()
+    acc = 0
+    for _ in range(args.steps):
+        d = P.hmc_update_distributed(chain, dt, L, stats=False, device=dev)
+        acc += int(d.accept)
+    e1.record()
+    torch.cuda.synchronize(local)
+    launches = chain.shard.launch_count() - n0
+    dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    clk = clocks.stop() if clocks else None
+    if rank == 0:
+        v = T * L / (ms * 1e-3)
+        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (simulate_rsv, theta of SURVEY §8d, seed 0)",
+                "config": {"workload": f"config 3: one chain T={T}, L={L}, dt={dt}, {args.prng}, time-sharded over "
+                                       f"{ws} GPUs; one step = one full HMC proposal",
+                           "T": T, "L": L, "dt": dt, "prng": args.prng,
+                           "parallelism": f"time-sharded x{ws} (margin {margin} sites, NCCL halo send/recv + "
+                                          "all_gather of shard totals)",
+                           "l2": "per-GPU working set below L2, not flushed (multi-GPU path)"},
+                "trajectories_per_s": 1e3 / ms, "accept_rate": acc / args.steps, "clocks": clk,
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 8 * 14 * ws, "d2h_bytes_per_step": 8 * 14 * ws,
+                        "path": "ShardedChain + hmc_update_distributed: shard totals to host, decision on host"},
+                "gpu_launches": int(launches)}
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -84,6 +84,9 @@ class CudaShard:
         except Exception:
             pass
 
+    def launch_count(self) -> int:
+        return int(self._lib.rsv_launch_count(self.ctx))
+
     def set_data(self, y, lrv):
         y = np.ascontiguousarray(y, dtype=np.float64)
         lrv = np.ascontiguousarray(lrv, dtype=np.float64)
