@@ -139,10 +139,17 @@ int rsv_suff_stats(rsv_ctx *ctx, double c_mu, double c_xi, double out[7]);
 int rsv_last_stats(rsv_ctx *ctx, double out[7]);
 
 /* Device timing helpers for the benchmark: average duration (ms) of the
- * trajectory kernel and of the whole proposal over the last
- * rsv_hmc_update_many call with timing enabled. */
-int rsv_set_timing(rsv_ctx *ctx, int enable);
+ * whole proposal (level 1: one CUDA event pair per proposal on the context's
+ * stream around the proposal) and, at level 2, of its momenta and trajectory
+ * parts (event nodes inside the proposal graph, which add their own latency)
+ * over the last rsv_hmc_update_many call.  Level 0 disables timing. */
+int rsv_set_timing(rsv_ctx *ctx, int level);
 int rsv_get_timing(rsv_ctx *ctx, double *traj_ms, double *momenta_ms, double *total_ms);
+/* %globaltimer stamps (ns) of the last proposal, taken inside the kernels:
+ * [0] momenta kernel entry (first CTA), [1] its exit (last CTA), [2]
+ * trajectory kernel entry (CTA 0), [3] its exit (Metropolis step), [4] the
+ * previous proposal's trajectory exit.  No events, no added latency. */
+int rsv_kernel_stamps(rsv_ctx *ctx, uint64_t out[5]);
 /* Benchmark hygiene: with bytes > 0, rsv_hmc_update_many writes a
  * scratch buffer of that size between proposals (outside the timed events)
  * so each proposal starts with a cold L2. */

@@ -25,29 +25,29 @@
 
 namespace rsv {
 
-__device__ const unsigned long long g_exp_tab2[64] = RSV_EXP_TAB2_INIT;
+__device__ __align__(128) const unsigned long long g_exp_tab2[RSV_EXP_TAB_N] = RSV_EXP_TAB2_INIT;
 
 constexpr double MAGIC = 6755399441055744.0;  // 1.5 * 2^52
+constexpr int EXP_HI_SHIFT = 20 - RSV_EXP_TAB_BITS;
 
-// exp(-d) for the model's range.  n = rint(-64 d / ln2) via the magic-number
-// add, r = -d - n ln2/64 (Cody-Waite, two FMAs), e^r - 1 by a degree-5
-// Horner polynomial (|r| <= ln2/128), and S = 2^(n/64) built exactly from a
-// scale-ready table entry (bits(2^(j/64)) - (j << 46)) plus n << 46: one
-// shared-memory load and one integer add.  10 FP64 instructions, <= ~1.5 ulp.
+// exp(-d) for the model's range.  n = rint(-2048 d / ln2) via the magic-number
+// add, r = -d - n ln2/2048 (Cody-Waite, two FMAs), e^r - 1 by a degree-3
+// Horner polynomial (|r| <= ln2/4096, truncation ~3e-17), and S = 2^(n/2048)
+// built exactly from a scale-ready table entry (bits(2^(j/2048)) - (j << 41))
+// plus n << 41: one shared-memory load and one integer add.  8 FP64
+// instructions, <= 1.3 ulp (tools/gen_exp_table.py).
 // `t` is returned for the integer range test of the divergence flag.
 __device__ __forceinline__ double exp_neg(double d, const unsigned long long *tab, double &t) {
-  t = fma(-d, RSV_INV_LN2_64, MAGIC);
+  t = fma(-d, RSV_INV_LN2_N, MAGIC);
   const double nd = t - MAGIC;
-  double r = fma(nd, -RSV_LN2_64_HI, -d);
-  r = fma(nd, -RSV_LN2_64_LO, r);
-  double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  q = fma(q, r, 1.0 / 6.0);
-  q = fma(q, r, 0.5);
+  double r = fma(nd, -RSV_LN2_N_HI, -d);
+  r = fma(nd, -RSV_LN2_N_LO, r);
+  double q = fma(r, 1.0 / 6.0, 0.5);
   q = fma(q, r, 1.0);
   q = q * r;
   const int n = __double2loint(t);
-  const unsigned long long tb = tab[n & 63];
-  const double S = __hiloint2double((int)(tb >> 32) + (n << 14), (int)(unsigned)tb);
+  const unsigned long long tb = tab[n & (RSV_EXP_TAB_N - 1)];
+  const double S = __hiloint2double((int)(tb >> 32) + (n << EXP_HI_SHIFT), (int)(unsigned)tb);
   return fma(S, q, S);
 }
 
@@ -59,14 +59,12 @@ __device__ __forceinline__ double exp_neg_k(double d, const unsigned long long *
   const double nd = t - MAGIC;
   double r = fma(nd, -k.e_hi, -d);
   r = fma(nd, -k.e_lo, r);
-  double q = fma(r, k.e_c5, k.e_c4);
-  q = fma(q, r, k.e_c3);
-  q = fma(q, r, 0.5);
+  double q = fma(r, k.e_c3, 0.5);
   q = fma(q, r, 1.0);
   q = q * r;
   const int n = __double2loint(t);
-  const unsigned long long tb = tab[n & 63];
-  const double S = __hiloint2double((int)(tb >> 32) + (n << 14), (int)(unsigned)tb);
+  const unsigned long long tb = tab[n & (RSV_EXP_TAB_N - 1)];
+  const double S = __hiloint2double((int)(tb >> 32) + (n << EXP_HI_SHIFT), (int)(unsigned)tb);
   return fma(S, q, S);
 }
 
@@ -97,11 +95,11 @@ TrajConsts traj_consts(const DevParams &P, double dt) {
   s.inv2se = 0.5 * P.inv_se2;
   s.one_m_phi2 = P.one_m_phi2;
   s.hconst = P.hconst;
-  s.e_k = RSV_INV_LN2_64;
-  s.e_hi = RSV_LN2_64_HI;
-  s.e_lo = RSV_LN2_64_LO;
-  s.e_c5 = 1.0 / 120.0;
-  s.e_c4 = 1.0 / 24.0;
+  s.e_k = RSV_INV_LN2_N;
+  s.e_hi = RSV_LN2_N_HI;
+  s.e_lo = RSV_LN2_N_LO;
+  s.e_c5 = 0.0;  // unused (degree-3 polynomial)
+  s.e_c4 = 0.0;
   s.e_c3 = 1.0 / 6.0;
   s.n_lo = P.n_lo;
   s.n_span = P.n_span;
@@ -273,7 +271,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_kernel(TrajArgs A) {
   constexpr int NW = NT / 32;
   constexpr int WSTEP = 30 * R;  // window advance per warp
   RSV_STAMP(0);
-  __shared__ unsigned long long s_tab[64];
+  __shared__ unsigned long long s_tab[RSV_EXP_TAB_N];
   __shared__ double s_first[NW], s_last[NW];
   __shared__ double s_red[NW * TR_NV];
   __shared__ double s_v[NW * TR_NV + TR_NV];
@@ -281,7 +279,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_kernel(TrajArgs A) {
   __shared__ double s_old[6 * NT];
   __shared__ int s_last_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 64) s_tab[tid] = g_exp_tab2[tid];
+  for (int i = tid; i < RSV_EXP_TAB_N; i += NT) s_tab[i] = g_exp_tab2[i];
 
   const TrajConsts &s = A.k;
   const double *hsrc;
@@ -542,8 +540,8 @@ struct PersistSmem {
   double gx[2 * NW * 4 * R];    // ghost-lane refresh slots
   double red[NW * TR_NV];
   double v[NW * TR_NV + TR_NV];
-  unsigned long long tab[64];
-  uint64_t bar[2];
+  alignas(16) unsigned long long tab[RSV_EXP_TAB_N];
+  uint64_t bar[3];  // two staging buffers, the exp table
   int last;
 };
 
@@ -566,17 +564,22 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     hsrc = cur ? A.hbuf1 : A.hbuf0;
     hdst = cur ? A.hbuf0 : A.hbuf1;
   }
-  if (tid < 64) S.tab[tid] = g_exp_tab2[tid];
+  if (tid == 0 && blockIdx.x == 0) A.ctrl->t_stamp[2] = gtimer();
   for (int k = 0; k < TR_NV; k++) S.acc[k * NT + tid] = 0.0;
   const int n_tiles = A.g.n_tiles;
   int tile = blockIdx.x;
   if (tid == 0) {
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
+    mbar_init(&S.bar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the exp table (16 KB) arrives by one bulk copy alongside the first tile
+    mbar_expect_tx(&S.bar[2], (uint32_t)sizeof(S.tab));
+    tma_load_1d(S.tab, g_exp_tab2, (uint32_t)sizeof(S.tab), &S.bar[2]);
     if (tile < n_tiles) stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0]);
   }
   __syncthreads();
+  mbar_wait(&S.bar[2], 0);
   const int64_t T = A.T;       // local series length (a shard's extended range, or the chain)
   const int64_t goff = A.goff; // global index of local site 0
   const int64_t Tg = A.Tg;     // global series length
@@ -766,14 +769,16 @@ struct TrajVariant {
 };
 static const TrajVariant kVariants[] = {{8, 256, 2}, {4, 256, 3}, {4, 128, 6}, {8, 128, 4}, {16, 128, 2},
                                         {2, 256, 4}, {8, 64, 8}, {4, 256, 2}, {8, 32, 16},
-                                        // persistent + TMA-staged (9..11)
-                                        {8, 256, 2}, {4, 256, 3}, {4, 256, 2}};
+                                        // persistent + TMA-staged (9..14); 12..14 are the
+                                        // small-window shapes for short series
+                                        {8, 256, 2}, {4, 256, 3}, {4, 256, 2}, {4, 128, 3}, {4, 64, 5},
+                                        {4, 32, 8}};
 static bool variant_persistent(int v) { return v >= 9; }
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 int traj_num_variants() { return kNumVariants; }
 
-TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant) {
+static TrajGeom traj_geometry_v(int64_t T, int n_steps, int sm_count, int variant) {
   TrajGeom g;
   if (variant < 0 || variant >= kNumVariants) variant = 0;
   const TrajVariant v = kVariants[variant];
@@ -793,6 +798,26 @@ TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant) {
   return g;
 }
 
+// variant < 0: automatic shape.  Long series use the 256-thread persistent
+// kernel (11); when that leaves SMs idle, the CTA window shrinks (128 / 64 /
+// 32 threads) so a short series still spreads over the whole GPU -- at small
+// T the trajectory is latency-bound per step, and more, smaller tiles
+// shorten it even though the halo share grows.
+TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant) {
+  if (variant >= 0) return traj_geometry_v(T, n_steps, sm_count, variant);
+  static const int kAuto[] = {11, 12, 13, 14};
+  TrajGeom best{};
+  bool have = false;
+  for (int v : kAuto) {
+    const TrajGeom g = traj_geometry_v(T, n_steps, sm_count, v);
+    if (!g.ok) continue;
+    best = g;
+    have = true;
+    if (g.n_tiles >= sm_count) break;
+  }
+  return have ? best : traj_geometry_v(T, n_steps, sm_count, 11);
+}
+
 template <int R, int NT, int MINB>
 static void launch_v(const TrajArgs &a, cudaStream_t s) {
   if (a.fuse) traj_kernel<R, NT, MINB, true><<<a.g.n_tiles, NT, 0, s>>>(a);
@@ -804,6 +829,10 @@ static void launch_p2(const TrajArgs &a, cudaStream_t s) {
   const size_t smem = sizeof(PersistSmem<R, NT>);
   cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
+  // same (maximal) shared-memory carveout as the momenta kernel: no L1/shared
+  // reconfiguration of the SMs between the two kernels of a proposal
+  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   traj_persistent_kernel<R, NT, MINB, FUSE, STATS><<<a.g.grid, NT, smem, s>>>(a);
 }
 template <int R, int NT, int MINB>
@@ -837,6 +866,9 @@ const void *traj_kernel_fn(int variant, int fuse, int stats) {
                  : (const void *)traj_persistent_kernel<R, NT, MB, false, false>))
     case 9: return RSV_FN(8, 256, 2);
     case 10: return RSV_FN(4, 256, 3);
+    case 12: return RSV_FN(4, 128, 3);
+    case 13: return RSV_FN(4, 64, 5);
+    case 14: return RSV_FN(4, 32, 8);
     default: return RSV_FN(4, 256, 2);
   }
 #undef RSV_FN
@@ -855,6 +887,9 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
     case 8: launch_v<8, 32, 16>(a, s); break;
     case 9: launch_p<8, 256, 2>(a, s); break;
     case 10: launch_p<4, 256, 3>(a, s); break;
+    case 12: launch_p<4, 128, 3>(a, s); break;
+    case 13: launch_p<4, 64, 5>(a, s); break;
+    case 14: launch_p<4, 32, 8>(a, s); break;
     default: launch_p<4, 256, 2>(a, s); break;
   }
   (*launches)++;
@@ -894,6 +929,7 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   }
   DevControl *C = A.ctrl;
   C->tiles_done = 0;  // re-arm for the next launch
+  C->t_stamp[3] = gtimer();
   if (A.shard) {  // time-sharded chain: the host combines the shards' totals
     for (int k = 0; k < TR_NV; k++) C->shard_parts[k] = tot[k];
     return;

@@ -35,11 +35,10 @@ __device__ const uint64_t g_ki[256] = RSV_KI_DOUBLE_INIT;
 __device__ const double g_wi[256] = RSV_WI_DOUBLE_INIT;
 __device__ const double g_fi[256] = RSV_FI_DOUBLE_INIT;
 
-constexpr int ZG = 16;                 // guard words before a CTA's block
-constexpr int ZLA = 32;                // look-ahead words after it
-constexpr int ZSW = ZG + ZB + ZLA;     // staged words per CTA
-constexpr int ZCH = ZSW / ZW;          // 8-word chunks per CTA (262)
+constexpr int ZG = 2 * ZW;             // guard words before a CTA's block (threads 0, 1)
+constexpr int ZCH = ZT;                // 8-word chunks staged per CTA: guard, block, look-ahead
 constexpr int ZDIRECT = 4096;          // up to this many CTAs: direct predecessor sums
+static_assert(ZB == (ZT - 4) * ZW, "block = threads 2..ZT-3");
 
 struct ZigJump {  // per-chunk jump-ahead constants (inc-free), built once
   uint64_t pcg_a[ZCH], pcg_g[ZCH];     // state_c = a * base + inc * g  (16 c outputs ahead)
@@ -64,54 +63,33 @@ __global__ void zig_jump_init_kernel() {
   }
 }
 
+constexpr int ZQ = 512;  // queue of non-fast-path words per CTA (expected ~23)
+// shared-memory skews: thread t touches words / normals ~8 apart, so pad two
+// (words) / one (normals) doubles per 16 to spread a warp over all banks
+#define ZWS(j) ((j) + 2 * ((j) >> 4))
+#define ZXS(j) ((j) + ((j) >> 4))
+
 struct ZigShared {
-  uint64_t w[ZSW];        // raw words: local index i <-> draw word b*ZB - ZG + i
-  double x[ZB];           // candidate normal of an attempt starting at block word k
-  uint8_t len[ZG + ZB];   // attempt length | acc << 7 for guard + block words
+  uint64_t w[ZWS(ZCH * ZW)];  // raw words: local index i <-> draw word b*ZB - ZG + i, at ZWS(i)
   uint64_t ki[256];
   double wi[256];
+  double fi[256];
+  double xout[ZXS(ZB)];   // the CTA's normals in block order (copy-out staging), at ZXS(j)
+  double qx[ZQ];          // queued attempts: normal, (len | acc << 4), word index
+  uint8_t qres[ZQ];
+  uint16_t qent[ZQ];
+  int32_t nq;
+  uint32_t edge_lens[ZT / 32][2];  // lanes 30, 31 of each warp: packed attempt lengths
+  uint32_t edge_nu[ZT / 32][2];    // and their non-unit-length start masks
   int32_t warp_tot[ZT / 32];
   int32_t warp_exit[ZT / 32];
-  uint64_t base_a, base_b;  // sequential-generator state at local word 0
   uint64_t blk_off;         // exclusive normal offset of this CTA
   int32_t blk;              // dynamic CTA index (ticket)
   int32_t bad;
-  int32_t warp0_entry;      // thread 0's speculative entry state
+  int32_t blk_entry;        // entry state of the block's first chunk (thread 2)
+  int32_t blk_exit;         // exit state of its last chunk (thread ZT - 3)
   uint32_t epoch;           // this draw's tag in the look-back status words
 };
-
-// Classify the attempt starting at local word i (numpy random_standard_normal).
-__device__ __forceinline__ void zig_classify_at(const ZigShared &S, int i, int mmax, int &len, int &acc, double &x) {
-  uint64_t r = S.w[i];
-  const int idx = (int)(r & 0xff);
-  r >>= 8;
-  const int sign = (int)(r & 0x1);
-  const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-  // rabs < 2^52: (2^52 | rabs) - 2^52 is exactly (double)rabs
-  const double fr = __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | rabs)), 4503599627370496.0);
-  x = __dmul_rn(fr, S.wi[idx]);
-  if (sign) x = -x;
-  if (rabs < S.ki[idx]) { len = 1; acc = 1; return; }
-  if (idx == 0) {
-    for (int m = 1; m <= mmax; m++) {
-      const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, glibc_log1p(-u01(S.w[i + 2 * m - 1])));
-      const double yy = -glibc_log1p(-u01(S.w[i + 2 * m]));
-      if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
-        x = ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
-        len = 1 + 2 * m;
-        acc = 1;
-        return;
-      }
-    }
-    len = 0;  // needs more tail loops than staged words: exact serial fallback
-    acc = 0;
-    return;
-  }
-  const double u = u01(S.w[i + 1]);
-  const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(g_fi[idx - 1], g_fi[idx]), u), g_fi[idx]);
-  acc = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x)) ? 1 : 0;
-  len = 2;
-}
 
 // decoupled look-back status word: [63:62] flag (1 aggregate, 2 prefix),
 // [61:58] exit state of the CTA's parse, [57:34] draw epoch (words from an
@@ -124,60 +102,6 @@ __device__ __forceinline__ bool zready(uint64_t v, uint32_t epoch) {
   return (v >> 62) != 0 && (uint32_t)((v >> 34) & 0xffffffu) == epoch;
 }
 
-template <int KIND>
-__device__ __forceinline__ void stage_words(ZigShared &S, const DevControl *ctrl, const uint64_t *words, int b,
-                                            int64_t nwords_buf, const uint64_t *bjump) {
-  const int tid = threadIdx.x;
-  const int64_t rel0 = (int64_t)b * ZB - ZG;  // draw-relative index of local word 0
-  if (KIND == PRNG_SFC64) {
-    for (int i = tid; i < ZSW; i += ZT) {
-      const int64_t k = rel0 + i;
-      S.w[i] = (k >= 0 && k < nwords_buf) ? words[k] : 0;
-    }
-    return;
-  }
-  const StreamState &st = ctrl->stream;
-  if (tid == 0) {
-    // state in front of local word 0 (draw word rel0 may be negative for CTA 0:
-    // the guard is never walked there, start at word 0 and shift): the
-    // generator state at the stream position, jumped by this CTA's offset
-    // with a precomputed per-CTA constant (bjump, built once per context)
-    if (KIND == PRNG_PCG32) S.base_a = bjump[2 * b] * ctrl->seq_state + st.s[1] * bjump[2 * b + 1];
-    else if (KIND == PRNG_MINSTD) S.base_a = mod31(bjump[b] * ctrl->seq_state);
-  }
-  __syncthreads();
-  const int shift = rel0 < 0 ? ZG : 0;  // CTA 0: local word ZG is draw word 0
-  for (int c = tid; c < ZCH; c += ZT) {
-    const int i0 = c * ZW;
-    if (i0 + ZW <= shift) {  // pure guard chunk of CTA 0: no words there
-      for (int i = 0; i < ZW; i++) S.w[i0 + i] = 0;
-    } else if (KIND == PRNG_PHILOX) {
-      SeqGen g;
-      g.init(st, st.pos + (uint64_t)(rel0 + i0));
-#pragma unroll
-      for (int i = 0; i < ZW; i++) S.w[i0 + i] = g.next();
-    } else if (KIND == PRNG_PCG32) {
-      const int cc = c - shift / ZW;
-      uint64_t s0 = g_jump.pcg_a[cc] * S.base_a + st.s[1] * g_jump.pcg_g[cc];
-#pragma unroll
-      for (int i = 0; i < ZW; i++) {
-        const uint64_t s1 = s0 * PCG_MULT + st.s[1];
-        S.w[i0 + i] = ((uint64_t)pcg_output(s0) << 32) | pcg_output(s1);
-        s0 = s1 * PCG_MULT + st.s[1];
-      }
-    } else {  // MINSTD
-      const int cc = c - shift / ZW;
-      uint64_t x = mod31(g_jump.minstd_a[cc] * S.base_a);
-#pragma unroll
-      for (int i = 0; i < ZW; i++) {
-        const uint64_t xa = mod31(x * MINSTD_A), xb = mod31(xa * MINSTD_A), xc = mod31(xb * MINSTD_A);
-        x = xc;
-        S.w[i0 + i] = (xa << 33) | (xb << 2) | (xc >> 29);
-      }
-    }
-  }
-}
-
 __device__ void zig_serial(DevControl *ctrl, const uint64_t *words, int64_t nbuf, double *normals, int64_t T);
 
 __device__ __forceinline__ unsigned long long zgt() {
@@ -186,10 +110,15 @@ __device__ __forceinline__ unsigned long long zgt() {
   return t;
 }
 
+// zig_kernel: thread t owns the 8 raw words of chunk t of the CTA's window
+// (chunks 0, 1: guard = the last 16 words of the previous block; 2..ZT-3:
+// the block; ZT-2, ZT-1: look-ahead for attempts that run past the block).
+// Words, attempt lengths and candidate normals live in registers; shared
+// memory only holds a copy of the words for the rare multi-word attempts.
 template <int KIND>
-__global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_t *words, int64_t nwords_buf,
+__global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint64_t *words, int64_t nwords_buf,
                                                  double *normals, int64_t T, uint64_t *status, const uint64_t *bjump,
-                                                 unsigned long long *dbg) {
+                                                 int coresident, unsigned long long *dbg) {
 #define ZSTAMP(k) \
   do { if (dbg && threadIdx.x == 0) dbg[(size_t)blockIdx.x * 8 + (k)] = zgt(); } while (0)
   ZSTAMP(0);
@@ -200,52 +129,210 @@ __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_
     S.blk = (int)atomicAdd(&ctrl->zig_ticket, 1u);
     S.epoch = ctrl->zig_epoch & 0xffffffu;
     S.bad = 0;
+    S.nq = 0;
+    if (S.blk == 0) {
+      ctrl->t_stamp[4] = ctrl->t_stamp[3];
+      ctrl->t_stamp[0] = zgt();
+    }
   }
+  // tables (independent of the ticket; overlap its latency)
   for (int i = tid; i < 256; i += ZT) {
     S.ki[i] = g_ki[i];
     S.wi[i] = g_wi[i];
+    S.fi[i] = g_fi[i];
   }
+  const StreamState &st = ctrl->stream;
+  uint64_t jA = 0, jG = 0;
+  const uint64_t inc = st.s[1];
+  if (KIND == PRNG_PCG32) { jA = g_jump.pcg_a[tid]; jG = g_jump.pcg_g[tid]; }
+  if (KIND == PRNG_MINSTD) jA = g_jump.minstd_a[tid];
+  const uint64_t seq = ctrl->seq_state;
   __syncthreads();
   const int b = S.blk;
   ZSTAMP(1);
-  stage_words<KIND>(S, ctrl, words, b, nwords_buf, bjump);
+
+  // ---- my 8 raw words, generated into registers
+  const int64_t k_t = (int64_t)b * ZB - ZG + (int64_t)tid * ZW;  // draw word of my chunk's first word
+  const bool valid = k_t >= 0;                                    // CTA 0 has no guard words
+  uint64_t w[ZW];
+  uint64_t base = 0;  // pcg: LCG state before output 2*k_t; minstd: x_{3 k_t}
+  if (!valid) {
+#pragma unroll
+    for (int i = 0; i < ZW; i++) w[i] = 0;
+  } else if (KIND == PRNG_SFC64) {
+#pragma unroll
+    for (int i = 0; i < ZW; i += 2) {
+      const int64_t k = k_t + i;
+      const ulonglong2 v = k + 2 <= nwords_buf ? *reinterpret_cast<const ulonglong2 *>(words + k) : make_ulonglong2(0, 0);
+      w[i] = v.x;
+      w[i + 1] = v.y;
+    }
+  } else if (KIND == PRNG_PHILOX) {
+    SeqGen g;
+    g.init(st, st.pos + (uint64_t)k_t);
+#pragma unroll
+    for (int i = 0; i < ZW; i++) w[i] = g.next();
+  } else {
+    // per-CTA jump (bjump, built once per context) composed with the
+    // per-chunk jump: CTA b's base word is max(0, b*ZB - ZG)
+    const int cc = b == 0 ? tid - ZG / ZW : tid;
+    if (KIND == PRNG_PCG32) {
+      const uint64_t bA = bjump[2 * b], bG = bjump[2 * b + 1];
+      const uint64_t cA = b == 0 ? g_jump.pcg_a[cc] : jA, cG = b == 0 ? g_jump.pcg_g[cc] : jG;
+      uint64_t s0 = cA * (bA * seq + bG * inc) + cG * inc;
+      base = s0;
+#pragma unroll
+      for (int i = 0; i < ZW; i++) {
+        const uint64_t s1 = s0 * PCG_MULT + inc;
+        w[i] = ((uint64_t)pcg_output(s0) << 32) | pcg_output(s1);
+        s0 = s1 * PCG_MULT + inc;
+      }
+    } else {  // MINSTD
+      const uint64_t cA = b == 0 ? g_jump.minstd_a[cc] : jA;
+      uint64_t x = mod31(cA * mod31(bjump[b] * seq));
+      base = x;
+#pragma unroll
+      for (int i = 0; i < ZW; i++) {
+        const uint64_t xa = mod31(x * MINSTD_A), xb = mod31(xa * MINSTD_A), xc = mod31(xb * MINSTD_A);
+        x = xc;
+        w[i] = (xa << 33) | (xb << 2) | (xc >> 29);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < ZW; i += 2)
+    *reinterpret_cast<ulonglong2 *>(&S.w[ZWS(tid * ZW + i)]) = make_ulonglong2(w[i], w[i + 1]);
   __syncthreads();
   ZSTAMP(2);
 
-  // ---- classify every guard + block word as an attempt start
-  const int first = (b == 0) ? ZG : 0;  // CTA 0 has no guard
-  int ovf = 0;
-  for (int i = tid; i < ZG + ZB; i += ZT) {
-    if (i < first) { S.len[i] = 1; continue; }
-    int len, acc;
-    double x;
-    zig_classify_at(S, i, ZMMAX, len, acc, x);
-    S.len[i] = (uint8_t)(len | (acc << 7));
-    if (i >= ZG) S.x[i - ZG] = x;
-    ovf |= (len == 0);
+  // ---- classify each word as an attempt start (numpy random_standard_normal).
+  // Fast path (98.9 % of words) in registers: one table compare.  The rest
+  // (wedge: one more word; tail: pairs of words) are queued and evaluated by
+  // the whole CTA at once, so the exp / log1p work is not serialised by
+  // divergence inside every warp.
+  const bool classify = valid && tid < ZT - 2;  // look-ahead chunks are words only
+  uint32_t slow = 0;
+  if (classify) {
+#pragma unroll
+    for (int i = 0; i < ZW; i++) {
+      const int idx = (int)(w[i] & 0xff);
+      const uint64_t rabs = (w[i] >> 9) & 0x000fffffffffffffULL;
+      if (!(rabs < S.ki[idx])) slow |= 1u << i;
+    }
   }
-  if (ovf) atomicOr(&ctrl->zig_overflow, 1);
+  const int nslow = __popc(slow);
+  int qbase = 0;
+  if (nslow) qbase = atomicAdd(&S.nq, nslow);
+  {
+    uint32_t m = slow;
+    int k = 0;
+    while (m) {
+      const int i = __ffs(m) - 1;
+      m &= m - 1;
+      if (qbase + k < ZQ) S.qent[qbase + k] = (uint16_t)(tid * ZW + i);
+      k++;
+    }
+  }
   __syncthreads();
+  const int nq = S.nq;
+  for (int q = tid; q < nq && q < ZQ; q += ZT) {
+    const int j0 = S.qent[q];
+    uint64_t r = S.w[ZWS(j0)];
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    const double fr = __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | rabs)), 4503599627370496.0);
+    double x = __dmul_rn(fr, S.wi[idx]);
+    if (r & 1) x = -x;
+    int len = 2, a = 0;
+    if (idx == 0) {  // exponential tail: pairs of words until accepted
+      len = 0;
+      for (int m = 1; m <= ZMMAX; m++) {
+        const int j = j0 + 2 * m;
+        const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, glibc_log1p(-u01(S.w[ZWS(j - 1)])));
+        const double yy = -glibc_log1p(-u01(S.w[ZWS(j)]));
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+          x = ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
+          len = 1 + 2 * m;
+          a = 1;
+          break;
+        }
+      }
+    } else {  // wedge: one more word
+      const double u = u01(S.w[ZWS(j0 + 1)]);
+      const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(S.fi[idx - 1], S.fi[idx]), u), S.fi[idx]);
+      a = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x)) ? 1 : 0;
+    }
+    S.qres[q] = (uint8_t)(len | (a << 4));
+    S.qx[q] = x;
+  }
+  if (tid == 0 && nq > ZQ) atomicOr(&ctrl->zig_overflow, 1);  // never in practice: exact fallback
+  __syncthreads();
+  // attempt lengths (nibbles), accepts, non-unit-length starts
+  uint32_t lens = 0x11111111u, acc = classify ? (~slow & 0xffu) : 0u, nu = 0;
+  {
+    uint32_t m = slow;
+    int k = 0;
+    while (m) {
+      const int i = __ffs(m) - 1;
+      m &= m - 1;
+      const int q = qbase + k < ZQ ? qbase + k : ZQ - 1;
+      const uint32_t res = S.qres[q];
+      lens = (lens & ~(15u << (4 * i))) | ((res & 15u) << (4 * i));
+      acc |= ((res >> 4) & 1u) << i;
+      nu |= 1u << i;
+      k++;
+    }
+  }
   ZSTAMP(3);
 
-  // ---- speculative walk: in sync 16 words before my segment
-  const int seg = ZG + tid * ZW;
-  int pos = (b == 0 && tid == 0) ? ZG : seg - ZG;
-  while (pos < seg) {
-    const int L = S.len[pos] & 15;
-    pos += L ? L : 1;
+  // ---- speculative walk: in sync 16 words (two chunks) before my chunk.
+  // Unit-length attempts are implicit; only the non-unit starts are visited
+  // (usually none in the 24-word window), marking the words they cover.
+  if (lane >= 30) {
+    S.edge_lens[warp][lane - 30] = lens;
+    S.edge_nu[warp][lane - 30] = nu;
   }
-  const int entry = pos - seg;
-  if (tid == 0) S.warp0_entry = entry;
-  int cnt = 0;
-  while (pos < seg + ZW) {
-    const uint8_t m = S.len[pos];
-    cnt += m >> 7;
-    const int L = m & 15;
-    pos += L ? L : 1;
+  uint32_t lm1 = __shfl_up_sync(0xffffffffu, lens, 1);
+  uint32_t lm2 = __shfl_up_sync(0xffffffffu, lens, 2);
+  uint32_t nm1 = __shfl_up_sync(0xffffffffu, nu, 1);
+  uint32_t nm2 = __shfl_up_sync(0xffffffffu, nu, 2);
+  __syncthreads();
+  if (warp > 0) {
+    if (lane == 0) {
+      lm1 = S.edge_lens[warp - 1][1]; lm2 = S.edge_lens[warp - 1][0];
+      nm1 = S.edge_nu[warp - 1][1]; nm2 = S.edge_nu[warp - 1][0];
+    }
+    if (lane == 1) { lm2 = S.edge_lens[warp - 1][1]; nm2 = S.edge_nu[warp - 1][1]; }
   }
-  const int exitst = pos - (seg + ZW);
-  // verify: my entry == previous thread's exit
+  const bool counting = tid >= 2 && tid < ZT - 2;
+  int entry = 0, exitst = 0, cnt = 0;
+  uint32_t vis = 0;
+  int ovf = 0;
+  if (counting) {
+    uint64_t cov = 0;  // window words inside an attempt that started earlier
+    uint32_t m = nm2 | (nm1 << 8) | (nu << 16);
+    while (m) {
+      const int q = __ffs(m) - 1;
+      m &= m - 1;
+      if ((cov >> q) & 1) continue;
+      const uint32_t src = q < 8 ? lm2 : q < 16 ? lm1 : lens;
+      const int L = (int)((src >> (4 * (q & 7))) & 15u);
+      if (L == 0) {
+        if (q >= 16) ovf = 1;
+        continue;
+      }
+      cov |= ((1ull << (L - 1)) - 1) << (q + 1);
+    }
+    const uint32_t free_mine = ~(uint32_t)(cov >> 16);
+    entry = __ffs(free_mine) - 1;  // <= 14 (an attempt covers at most 14 more words)
+    vis = free_mine & 0xffu & (0xffu << entry);
+    cnt = __popc(vis & acc);
+    vis &= acc;
+    exitst = __ffs(~(uint32_t)(cov >> 24)) - 1;
+  }
+  if (ovf) atomicOr(&ctrl->zig_overflow, 1);
+  // verify: my entry == previous chunk's exit; block scan of the counts
   int prev_exit = __shfl_up_sync(0xffffffffu, exitst, 1);
   int incl = cnt;
 #pragma unroll
@@ -257,34 +344,101 @@ __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_
     S.warp_tot[warp] = incl;
     S.warp_exit[warp] = exitst;
   }
+  if (tid == 2) S.blk_entry = entry;
+  if (tid == ZT - 3) S.blk_exit = exitst;
   __syncthreads();
   if (lane == 0 && warp > 0) prev_exit = S.warp_exit[warp - 1];
-  if (tid > 0 && prev_exit != entry) S.bad = 1;
+  if (tid > 2 && counting && prev_exit != entry) S.bad = 1;
   int woff = 0, btot = 0;
-  for (int w = 0; w < ZT / 32; w++) {
-    if (w < warp) woff += S.warp_tot[w];
-    btot += S.warp_tot[w];
+#pragma unroll
+  for (int q = 0; q < ZT / 32; q++) {
+    if (q < warp) woff += S.warp_tot[q];
+    btot += S.warp_tot[q];
   }
   const int toff = woff + incl - cnt;  // exclusive offset of my normals in the CTA
 
-  ZSTAMP(4);
-  // ---- decoupled look-back over CTAs for the global normal offset
-  // (warp 0 inspects 32 predecessors per round)
-  if (warp == 0) {
-    const int bexit = S.warp_exit[ZT / 32 - 1];
-    volatile uint64_t *vst = status;
-    if (b == 0) {
-      if (lane == 0) {
-        vst[0] = zpack(2, bexit, S.epoch, (uint64_t)btot);
-        S.blk_off = 0;
-        if (entry != 0) S.bad = 1;
+  // ---- my normals into the CTA's output staging (block order); the global
+  // offset only shifts the coalesced copy-out after the look-back
+  if (vis) {
+    int o = toff;
+#pragma unroll
+    for (int i = 0; i < ZW; i++) {
+      if ((vis >> i) & 1) {
+        double x;
+        if ((slow >> i) & 1) {
+          const int q = qbase + __popc(slow & ((1u << i) - 1));
+          x = S.qx[q < ZQ ? q : ZQ - 1];
+        } else {
+          uint64_t r = S.w[ZWS(tid * ZW + i)];
+          const int idx = (int)(r & 0xff);
+          r >>= 8;
+          const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+          const double fr =
+              __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | rabs)), 4503599627370496.0);
+          x = __dmul_rn(fr, S.wi[idx]);
+          if (r & 1) x = -x;
+        }
+        S.xout[ZXS(o)] = x;
+        o++;
       }
-    } else {
-      if (lane == 0) vst[b] = zpack(1, bexit, S.epoch, (uint64_t)btot);
-      uint64_t acc = 0;
+    }
+  }
+
+  ZSTAMP(4);
+  // ---- global normal offset of this CTA.  Every CTA publishes its count;
+  // when the grid is co-resident, the CTA that publishes last scans all
+  // counts once and raises a flag (one cheap poll per waiting CTA instead of
+  // hundreds of CTAs re-reading every predecessor).  Otherwise -- or if the
+  // flag is late -- a decoupled look-back over the predecessors' counts,
+  // which only depends on CTAs with smaller tickets (already running).
+  if (warp == 0) {
+    const int bexit = S.blk_exit;
+    volatile uint64_t *vst = status;
+    bool have = false;
+    uint64_t accum = 0;
+    if (lane == 0) vst[b] = zpack(b == 0 ? 2 : 1, bexit, S.epoch, (uint64_t)btot);
+    if (coresident) {
+      // the CTA that publishes last raises the draw's flag; after it, every
+      // count is in place and one round of independent loads sums the
+      // predecessors (no re-polling of hundreds of status words)
+      const unsigned tag = 0x80000000u | S.epoch;
+      unsigned pub = 0;
+      if (lane == 0) {
+        __threadfence();
+        pub = atomicAdd(&ctrl->zig_pub, 1u);
+        if (pub == gridDim.x - 1) {
+          __threadfence();
+          atomicExch(&ctrl->zig_flag, tag);
+        }
+      }
+      bool flag = false;
+      for (int it = 0; it < 4096 && !flag; it++) {
+        const unsigned f = lane == 0 ? *(volatile unsigned *)&ctrl->zig_flag : 0u;
+        flag = __shfl_sync(0xffffffffu, f, 0) == tag;
+        if (!flag) __nanosleep(32);
+      }
+      if (flag) {
+        __threadfence();
+        uint64_t part = 0;
+        bool ok = true;
+        for (int j = lane; j < b; j += 32) {
+          const uint64_t v = __ldcg(reinterpret_cast<const unsigned long long *>(status) + j);
+          ok &= zready(v, S.epoch);
+          part += v & ZCNT;
+        }
+        if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+          accum = part;
+          have = true;
+        }
+      }
+    }
+    if (!have && b == 0) have = true;
+    if (!have) {
       if (gridDim.x <= ZDIRECT) {
-        // small grids: every CTA sums all its predecessors' aggregates in one
-        // round of independent loads (no chain of published prefixes)
+        // every CTA sums all its predecessors' aggregates in one round of
+        // independent loads (no chain of published prefixes)
         for (;;) {
           uint64_t part = 0;
           bool ok = true;
@@ -296,94 +450,85 @@ __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_
           if (__all_sync(0xffffffffu, ok)) {
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-            acc = part;
+            accum = part;
             break;
           }
-          __nanosleep(100);
-        }
-        if (lane == 0) {
-          const uint64_t prev = vst[b - 1];
-          if ((int)((prev >> 58) & 15) != S.warp0_entry) S.bad = 1;
+          __nanosleep(64);
         }
       } else {
-      // look back 256 predecessors per round (8 independent loads per lane)
-      int hi = b - 1;
-      bool checked = false;
-      for (;;) {
-        // 8 independent loads per lane, re-issued until every predecessor in
-        // the window has published (no serial chain of dependent loads)
-        uint64_t sv[8];
+        // look back 256 predecessors per round (8 independent loads per lane)
+        int hi = b - 1;
         for (;;) {
-          bool ok = true;
+          uint64_t sv[8];
+          for (;;) {
+            bool ok = true;
 #pragma unroll
-          for (int w = 0; w < 8; w++) {
-            const int j = hi - lane - 32 * w;
-            sv[w] = j >= 0 ? vst[j] : (uint64_t)S.epoch << 34 | 2ULL << 62;  // before CTA 0: empty prefix
+            for (int q = 0; q < 8; q++) {
+              const int j = hi - lane - 32 * q;
+              sv[q] = j >= 0 ? vst[j] : (uint64_t)S.epoch << 34 | 2ULL << 62;  // before CTA 0: empty prefix
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) ok &= zready(sv[q], S.epoch);
+            if (__all_sync(0xffffffffu, ok)) break;
+            __nanosleep(200);  // back off: hundreds of CTAs poll the same lines
+          }
+          bool done = false;
+          uint64_t mine = 0;
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            if (!done) {
+              const unsigned pref = __ballot_sync(0xffffffffu, (sv[q] >> 62) == 2);
+              const int stop = pref ? __ffs(pref) - 1 : 32;  // nearest predecessor holding a prefix
+              if (lane <= stop) mine += sv[q] & ZCNT;
+              done = pref != 0;
+            }
           }
 #pragma unroll
-          for (int w = 0; w < 8; w++) ok &= zready(sv[w], S.epoch);
-          if (__all_sync(0xffffffffu, ok)) break;
-          __nanosleep(200);  // back off: hundreds of CTAs poll the same lines
+          for (int o = 16; o >= 1; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+          accum += mine;
+          if (done) break;
+          hi -= 256;
         }
-        if (!checked) {  // the previous CTA's exit must equal my thread 0's entry
-          const uint64_t prev = __shfl_sync(0xffffffffu, sv[0], 0);
-          if (lane == 0 && (int)((prev >> 58) & 15) != S.warp0_entry) S.bad = 1;
-          checked = true;
-        }
-        bool done = false;
-        uint64_t mine = 0;
-#pragma unroll
-        for (int w = 0; w < 8; w++) {
-          if (!done) {
-            const unsigned pref = __ballot_sync(0xffffffffu, (sv[w] >> 62) == 2);
-            const int stop = pref ? __ffs(pref) - 1 : 32;  // nearest predecessor holding a prefix
-            if (lane <= stop) mine += sv[w] & ZCNT;
-            done = pref != 0;
-          }
-        }
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-        acc += mine;
-        if (done) break;
-        hi -= 256;
-      }
-      }
-      if (lane == 0) {
-        S.blk_off = acc;
         // prefixes are only consumed by the chained look-back of large grids
         // (the direct sums need every CTA's own count to stay in place)
-        if (gridDim.x > ZDIRECT) {
+        if (lane == 0) {
           __threadfence();
-          vst[b] = zpack(2, bexit, S.epoch, acc + (uint64_t)btot);
+          vst[b] = zpack(2, bexit, S.epoch, accum + (uint64_t)btot);
         }
       }
     }
-    if (lane == 0 && S.bad) atomicOr(&ctrl->zig_overflow, 2);
+    if (lane == 0) {
+      S.blk_off = accum;
+      if (b == 0) {
+        if (S.blk_entry != 0) S.bad = 1;
+      } else {  // the previous CTA's exit must equal my block's entry (it has published)
+        uint64_t prev;
+        do { prev = vst[b - 1]; } while (!zready(prev, S.epoch));
+        if ((int)((prev >> 58) & 15) != S.blk_entry) S.bad = 1;
+      }
+      if (S.bad) atomicOr(&ctrl->zig_overflow, 2);
+    }
   }
   __syncthreads();
 
   ZSTAMP(5);
-  // ---- write my normals to their final slots
-  uint64_t off = S.blk_off + (uint64_t)toff;
-  pos = seg + entry;
-  if (off < (uint64_t)T) {
-    while (pos < seg + ZW) {
-      const uint8_t m = S.len[pos];
-      const int L = m & 15;
-      if (m >> 7) {
-        if (off < (uint64_t)T) normals[off] = S.x[pos - ZG];
-        if (off == (uint64_t)T - 1) {
-          const int nxt = pos + L;  // local index of the next unread word
-          ctrl->zig_used = (uint64_t)((int64_t)b * ZB - ZG + nxt);
-          ctrl->u_word = S.w[nxt];
-          const int shift = b == 0 ? ZG : 0;  // local word of the CTA's base state
-          if (KIND == PRNG_PCG32) ctrl->seq_next = pcg_advance(S.base_a, 2 * (uint64_t)(nxt - shift), ctrl->stream.s[1]);
-          else if (KIND == PRNG_MINSTD) ctrl->seq_next = mod31(minstd_pow(3 * (uint64_t)(nxt - shift)) * S.base_a);
-        }
-        off++;
-      }
-      pos += L ? L : 1;
-    }
+  // ---- coalesced copy-out of the CTA's normals; the thread whose normal is
+  // the draw's last (index T-1) records where the draw ended in the stream
+  const uint64_t boff = S.blk_off;
+  for (int j = tid; j < btot; j += ZT) {
+    if (boff + (uint64_t)j < (uint64_t)T) normals[boff + j] = S.xout[ZXS(j)];
+  }
+  if (vis && boff + (uint64_t)toff <= (uint64_t)T - 1 && (uint64_t)T - 1 < boff + (uint64_t)toff + (uint64_t)cnt) {
+    const int rank = (int)((uint64_t)T - 1 - boff - (uint64_t)toff);  // which of my normals
+    uint32_t m = vis;
+    for (int k = 0; k < rank; k++) m &= m - 1;
+    const int i = __ffs(m) - 1;
+    const int L = (int)((lens >> (4 * i)) & 15u);
+    const int nxt = tid * ZW + i + L;  // local index of the next unread word
+    ctrl->zig_used = (uint64_t)((int64_t)b * ZB - ZG + nxt);
+    ctrl->u_word = S.w[ZWS(nxt)];
+    if (KIND == PRNG_PCG32) ctrl->seq_next = pcg_advance(base, 2 * (uint64_t)(i + L), inc);
+    else if (KIND == PRNG_MINSTD) ctrl->seq_next = mod31(minstd_pow(3 * (uint64_t)(i + L)) * base);
   }
   // the last CTA publishes how many normals the parse produced
   if (tid == ZT - 1 && b == (int)gridDim.x - 1) ctrl->zig_avail = S.blk_off + (uint64_t)btot;
@@ -400,7 +545,9 @@ __global__ void __launch_bounds__(ZT) zig_kernel(DevControl *ctrl, const uint64_
       ctrl->zig_overflow = 0;
       ctrl->zig_ticket = 0;
       ctrl->zig_done = 0;
+      ctrl->zig_pub = 0;
       ctrl->zig_epoch = ctrl->zig_epoch + 1;
+      ctrl->t_stamp[1] = zgt();
     }
   }
 }
@@ -483,9 +630,9 @@ int64_t momenta_words(int64_t T) {
   return (n + ZB - 1) / ZB * ZB;
 }
 
-size_t momenta_scratch_bytes(int64_t T) {
+size_t momenta_scratch_bytes(int64_t T) {  // status words + CTA prefixes
   const int64_t nb = momenta_words(T) / ZB;
-  return (size_t)(nb + 2) * sizeof(uint64_t) + 64;
+  return (size_t)2 * (nb + 2) * sizeof(uint64_t) + 64;
 }
 
 // per-CTA jump constants: CTA b's local word 0 is draw word max(0, b*ZB - ZG)
@@ -515,6 +662,21 @@ int momenta_init(cudaStream_t s, uint64_t *bjump, int64_t T) {
 
 size_t momenta_jump_bytes(int64_t T) { return (size_t)3 * (momenta_words(T) / ZB) * sizeof(uint64_t); }
 
+template <int KIND>
+static void launch_zig(const MomentaBufs &b, const uint64_t *words, int64_t nbuf, int64_t T, uint64_t *status,
+                       const uint64_t *bj, int nb, size_t smem, cudaStream_t s) {
+  cudaFuncSetAttribute(zig_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(zig_kernel<KIND>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  // can every CTA of the draw be resident at once?  (flag-mode prefixes)
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zig_kernel<KIND>, ZT, smem);
+  // (small grids poll their few predecessors directly: cheaper than the flag)
+  const int coresident = nb >= 64 && nb <= per_sm * sms ? 1 : 0;
+  zig_kernel<KIND><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, coresident, b.dbg);
+}
+
 int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, int *launches) {
   const int64_t N = momenta_words(T);
   const int nb = (int)(N / ZB);
@@ -529,22 +691,10 @@ int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, in
   const uint64_t *bj = kind == PRNG_MINSTD ? b.bjump + 2 * nb : b.bjump;
   const size_t smem = sizeof(ZigShared);
   switch (kind) {
-    case PRNG_PHILOX:
-      cudaFuncSetAttribute(zig_kernel<PRNG_PHILOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      zig_kernel<PRNG_PHILOX><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, b.dbg);
-      break;
-    case PRNG_MINSTD:
-      cudaFuncSetAttribute(zig_kernel<PRNG_MINSTD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      zig_kernel<PRNG_MINSTD><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, b.dbg);
-      break;
-    case PRNG_PCG32:
-      cudaFuncSetAttribute(zig_kernel<PRNG_PCG32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      zig_kernel<PRNG_PCG32><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, b.dbg);
-      break;
-    default:
-      cudaFuncSetAttribute(zig_kernel<PRNG_SFC64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      zig_kernel<PRNG_SFC64><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, b.dbg);
-      break;
+    case PRNG_PHILOX: launch_zig<PRNG_PHILOX>(b, words, nbuf, T, status, bj, nb, smem, s); break;
+    case PRNG_MINSTD: launch_zig<PRNG_MINSTD>(b, words, nbuf, T, status, bj, nb, smem, s); break;
+    case PRNG_PCG32: launch_zig<PRNG_PCG32>(b, words, nbuf, T, status, bj, nb, smem, s); break;
+    default: launch_zig<PRNG_SFC64>(b, words, nbuf, T, status, bj, nb, smem, s); break;
   }
   (*launches)++;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;

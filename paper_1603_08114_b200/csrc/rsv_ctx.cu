@@ -79,7 +79,7 @@ struct rsv_ctx {
   // series of Tg sites and owns [goff + own_lo, goff + own_hi)
   int64_t Tg = 0, goff = 0, own_lo = 0, own_hi = 0;
   bool shard = false;
-  int variant = 11;  // persistent, TMA-staged, 4 sites x 256 threads, 2 CTAs/SM (see leapfrog.cu)
+  int variant = -1;  // automatic: persistent, TMA-staged, window size by T (traj_geometry in leapfrog.cu)
   unsigned long long *dbg = nullptr;  // RSV_TRAJ_STAMPS=1: per-tile timestamps
 
   double *hbuf[2] = {nullptr, nullptr};
@@ -120,7 +120,7 @@ struct rsv_ctx {
     std::vector<cudaGraphNode_t> ev;  // timing event-record nodes
   };
   std::map<GraphKey, Cached *> graphs;
-  bool timing = false;
+  int timing = 0;  // 0 off, 1 per-proposal total, 2 with momenta / trajectory breakdown
   std::vector<cudaEvent_t> evpool;
   std::vector<double> last_traj_ms, last_mom_ms, last_total_ms;
 };
@@ -324,8 +324,8 @@ int rsv_set_params(rsv_ctx *c, const rsv_params *p) {
   const double Td = (double)c->T;
   q.hconst = 0.5 * Td * q.mu + 0.5 * Td * log(q.su2) + 0.5 * log(q.se2 / (1.0 - q.phi * q.phi)) +
              0.5 * (Td - 1.0) * log(q.se2);
-  q.n_lo = (int32_t)floor((q.mu - 50.0) * RSV_INV_LN2_64);
-  q.n_span = (int32_t)ceil((q.mu + 50.0) * RSV_INV_LN2_64) - q.n_lo;
+  q.n_lo = (int32_t)floor((q.mu - 50.0) * RSV_INV_LN2_N);
+  q.n_span = (int32_t)ceil((q.mu + 50.0) * RSV_INV_LN2_N) - q.n_lo;
   CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(DevParams), cudaMemcpyHostToDevice, c->stream));
   c->has_params = true;
   // the trajectory reads the derived constants from its parameter block:
@@ -537,7 +537,7 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
 
 static int get_graph(rsv_ctx *c, double dt, int n_steps, int fuse, int stats, rsv_ctx::Cached **out,
                      int *kernels) {
-  GraphKey k{c->kind, n_steps, fuse ? 1 : 0, c->timing ? 1 : 0, stats ? 1 : 0, dt};
+  GraphKey k{c->kind, n_steps, fuse ? 1 : 0, c->timing == 2 ? 1 : 0, stats ? 1 : 0, dt};
   auto it = c->graphs.find(k);
   if (it == c->graphs.end()) {
     rsv_ctx::Cached *cg = nullptr;
@@ -587,9 +587,12 @@ int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv
   }
   CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
   CK(cudaMemsetAsync(c->ring_count, 0, sizeof(int32_t), c->stream));
+  // timing 1: one event pair per proposal on the stream around the graph
+  // launch (the L2 flush stays outside); timing 2: the graph's own four
+  // event-record nodes give the momenta / trajectory breakdown as well
   std::vector<cudaGraphNode_t> *evn = nullptr;
   if (c->timing) {
-    evn = &cg->ev;
+    if (c->timing == 2) evn = &cg->ev;
     if ((r = ensure_events(c, 4 * (size_t)n + 4))) return r;
   }
   for (int i = 0; i < n; i++) {
@@ -597,7 +600,9 @@ int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv
       for (int j = 0; j < 4; j++) CK(cudaGraphExecEventRecordNodeSetEvent(exec, (*evn)[j], c->evpool[4 + 4 * i + j]));
     }
     if (c->flush_bytes > 0) CK(cudaMemsetAsync(c->flush_buf, i & 0xff, (size_t)c->flush_bytes, c->stream));
+    if (c->timing == 1) CK(cudaEventRecord(c->evpool[4 + 4 * i], c->stream));
     CK(cudaGraphLaunch(exec, c->stream));
+    if (c->timing == 1) CK(cudaEventRecord(c->evpool[4 + 4 * i + 3], c->stream));
     c->launches += kpl;
     if (out) {
       ring_store_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, c->ring, c->ring_cap, c->ring_count);
@@ -609,15 +614,17 @@ int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv
   if ((r = check_err_bits(c))) return r;
   if (out)
     for (int i = 0; i < n; i++) to_result(c->h_ring[i], out + i);
-  if (evn) {
+  if (c->timing) {
     c->last_traj_ms.assign(n, 0.0);
     c->last_mom_ms.assign(n, 0.0);
     c->last_total_ms.assign(n, 0.0);
     for (int i = 0; i < n; i++) {
       float t0 = 0, t1 = 0, t2 = 0;
       cudaEvent_t *e = &c->evpool[4 + 4 * i];
-      CK(cudaEventElapsedTime(&t0, e[0], e[1]));
-      CK(cudaEventElapsedTime(&t1, e[1], e[2]));
+      if (evn) {
+        CK(cudaEventElapsedTime(&t0, e[0], e[1]));
+        CK(cudaEventElapsedTime(&t1, e[1], e[2]));
+      }
       CK(cudaEventElapsedTime(&t2, e[0], e[3]));
       c->last_mom_ms[i] = t0;
       c->last_traj_ms[i] = t1;
@@ -966,7 +973,7 @@ int rsv_create_shard(rsv_ctx **out, int device, int64_t Tg, int64_t lo, int64_t 
     rsv_destroy(c);
     return r;
   }
-  if (c->variant < 9) c->variant = 11;  // the persistent kernel carries the shard indexing
+  if (c->variant >= 0 && c->variant < 9) c->variant = -1;  // the persistent kernel carries the shard indexing
   if (local_start) *local_start = ls;
   if (local_len) *local_len = le - ls;
   *out = c;
@@ -1027,9 +1034,18 @@ int rsv_latent_slice(rsv_ctx *c, int64_t offset, int64_t n, double *buf, int to_
   return sync(c);
 }
 
+int rsv_kernel_stamps(rsv_ctx *c, uint64_t out[5]) {
+  if (!c || !out) return fail(c, RSV_E_INVALID, "null argument");
+  CK(cudaSetDevice(c->device));
+  int r;
+  if ((r = pull_ctrl(c))) return r;
+  for (int i = 0; i < 5; i++) out[i] = c->h_ctrl->t_stamp[i];
+  return 0;
+}
+
 int rsv_set_timing(rsv_ctx *c, int enable) {
   if (!c) return fail(c, RSV_E_INVALID, "null context");
-  c->timing = enable != 0;
+  c->timing = enable < 0 ? 0 : enable > 2 ? 2 : enable;
   return 0;
 }
 

@@ -10,7 +10,7 @@ namespace rsv {
 // ---- momenta (numpy ziggurat parse) geometry -------------------------------
 constexpr int ZW = 8;            // raw words per thread
 constexpr int ZT = 256;          // threads per block
-constexpr int ZB = ZW * ZT;      // words per block
+constexpr int ZB = ZW * (ZT - 4); // words per block (threads 0,1: guard; ZT-2, ZT-1: look-ahead)
 constexpr int ZS = 16;           // parse states: words still owed to the running attempt
 constexpr int ZMMAX = 7;         // tail loops resolvable in the parallel parse (len <= 15)
 constexpr int Z2T = 256;         // threads of the block-scan kernel
@@ -33,7 +33,7 @@ struct DevParams {
   // derived once on the host (rsv_set_params) so no tile recomputes them
   double inv_su2, inv_se2, emu, one_m_phi2;
   double hconst;   // theta-only part of H (model.py:134-163 log terms + 0.5*T*mu)
-  int32_t n_lo, n_span;  // |h| <= 50  <=>  rint(-64 (h - mu)/ln2) - n_lo in [0, n_span]
+  int32_t n_lo, n_span;  // |h| <= 50  <=>  rint(-2048 (h - mu)/ln2) - n_lo in [0, n_span]
 };
 
 struct TilePart {  // per-tile partial sums over the tile's core sites
@@ -69,8 +69,13 @@ struct DevControl {
   // LCG state before output 2*pos; minstd: x_{3*pos}); seq_next = at pos + used
   uint64_t seq_state, seq_next;
   // momenta kernel bookkeeping (reset by its last CTA: no memsets per draw)
-  uint32_t zig_ticket, zig_done, zig_epoch, pad4;
+  uint32_t zig_ticket, zig_done, zig_epoch, zig_pub;
+  uint32_t zig_flag, pad5;  // epoch of the last draw whose CTA prefixes are published
   double shard_parts[TR_NV];  // time-sharded chains: this shard's totals (TilePart order)
+  // %globaltimer stamps (ns) of the last proposal: momenta kernel first-CTA
+  // entry / last-CTA exit, trajectory kernel CTA-0 entry / last-CTA exit,
+  // and the previous proposal's trajectory exit
+  unsigned long long t_stamp[5];
 };
 
 }  // namespace rsv

@@ -166,8 +166,20 @@ class DeviceChain:
         self._ck(self._lib.rsv_last_stats(self.ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
 
-    def set_timing(self, on: bool):
-        self._ck(self._lib.rsv_set_timing(self.ctx, int(bool(on))))
+    def set_timing(self, level):
+        """0/False off, 1/True per-proposal total, 2 with the momenta /
+        trajectory breakdown (graph event nodes, slightly slower)."""
+        self._ck(self._lib.rsv_set_timing(self.ctx, int(level)))
+
+    def kernel_stamps(self) -> dict:
+        """In-kernel %globaltimer split of the last proposal (microseconds):
+        momenta kernel, gap, trajectory kernel, and the gap since the
+        previous proposal's trajectory ended."""
+        st = (ctypes.c_uint64 * 5)()
+        self._ck(self._lib.rsv_kernel_stamps(self.ctx, st))
+        t = [int(x) for x in st]
+        return {"momenta_us": (t[1] - t[0]) / 1e3, "gap_us": (t[2] - t[1]) / 1e3,
+                "trajectory_us": (t[3] - t[2]) / 1e3, "since_prev_us": (t[0] - t[4]) / 1e3 if t[4] else None}
 
     def timing(self):
         a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()

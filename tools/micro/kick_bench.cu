@@ -10,10 +10,10 @@ constexpr double MAGIC = 6755399441055744.0;
 
 template <int MODE>
 __device__ __forceinline__ double expn(double d, const unsigned long long *tab) {
-  const double t = fma(-d, RSV_INV_LN2_64, MAGIC);
+  const double t = fma(-d, RSV_INV_LN2_N, MAGIC);
   const double nd = t - MAGIC;
-  double r = fma(nd, -RSV_LN2_64_HI, -d);
-  r = fma(nd, -RSV_LN2_64_LO, r);
+  double r = fma(nd, -RSV_LN2_N_HI, -d);
+  r = fma(nd, -RSV_LN2_N_LO, r);
   double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
   q = fma(q, r, 1.0 / 6.0);
   q = fma(q, r, 0.5);

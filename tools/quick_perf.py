@@ -15,7 +15,7 @@ for T in [2000, 1 << 14, 1 << 18, 1 << 20, 1 << 22]:
     ch.set_latent(truth.latent)
     ch.set_stream(P.stream_state(P.make_rng(1, "pcg32")))
     ch.hmc_update_many(0.02, 20, 5)
-    ch.set_timing(True)
+    ch.set_timing(2)
     n = 50
     res = ch.hmc_update_many(0.02, 20, n)
     tr, mo, tot = ch.timing()

@@ -7,7 +7,7 @@ from paper_1603_08114_b200 import _native as N
 L = N.lib()
 L.rsv_debug_stamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
 theta = P.Params(0.97, -9.0, -0.3, 0.05, 0.1)
-for T in [2000, 1 << 20]:
+for T in [int(a) for a in sys.argv[1:]] or [2000, 1 << 20]:
     tr = P.simulate_rsv(theta, T, seed=1)
     be = P.CudaBackend(0)
     ch = be.chain(tr.dataset, theta)

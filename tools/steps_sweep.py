@@ -10,7 +10,7 @@ for T in [1 << 14, 1 << 20]:
     ch.set_stream(P.stream_state(P.make_rng(1, "pcg32")))
     for L in [1, 2, 5, 10, 20, 40]:
         ch.hmc_update_many(0.02, L, 3, results=False)
-        ch.set_timing(True)
+        ch.set_timing(2)
         ch.hmc_update_many(0.02, L, 20, results=False)
         t, m, tot = ch.timing()
         ch.set_timing(False)

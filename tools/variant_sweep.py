@@ -9,14 +9,14 @@ sys.path.insert(0, ".")
 import paper_1603_08114_b200 as P
 theta = P.Params(0.97, -9.0, -0.3, 0.05, 0.1)
 out = []
-for T in [1 << 14, 1 << 18, 1 << 20, 1 << 22]:
+for T in [2000, 1 << 12, 1 << 14, 1 << 16, 1 << 18, 1 << 20]:
     tr = P.simulate_rsv(theta, T, seed=1)
     be = P.CudaBackend(0)
     ch = be.chain(tr.dataset, theta)
     ch.set_latent(tr.latent)
     ch.set_stream(P.stream_state(P.make_rng(1, "pcg32")))
     ch.hmc_update_many(0.02, 20, 5, results=False)
-    ch.set_timing(True)
+    ch.set_timing(2)
     ch.hmc_update_many(0.02, 20, 30, results=False)
     t, m, tot = ch.timing()
     out.append(f"T=2^{T.bit_length()-1}: traj {t*1e3:8.2f}us ({T*20/(t*1e-3):.3e}/s) tot {tot*1e3:8.2f}us")
