@@ -145,6 +145,28 @@ int rsv_last_stats(rsv_ctx *ctx, double out[7]);
  * over the last rsv_hmc_update_many call.  Level 0 disables timing. */
 int rsv_set_timing(rsv_ctx *ctx, int level);
 int rsv_get_timing(rsv_ctx *ctx, double *traj_ms, double *momenta_ms, double *total_ms);
+/* ---- ensemble of independent chains (BASELINE config 4) ----
+ * n_chains chains of T_chain sites each (chain-major arrays of
+ * n_chains * T_chain doubles for rsv_set_data / rsv_set_latent /
+ * rsv_get_latent), one shared parameter set, one numpy SFC64 stream per chain
+ * (state words a, b, c, counter: chain c of the benchmark uses
+ * SFC64(SeedSequence([seed, c]))).  One round = one hmc_update_volatility
+ * (sampler.py:144-167) of every chain: momenta from the chain's own stream,
+ * trajectory, per-chain dH and Metropolis test with the chain's own uniform.
+ * The reference has no ensemble driver (SURVEY §2 K-ens); per chain the
+ * result is exactly the reference's single-chain update. */
+int rsv_ens_create(rsv_ctx **out, int device, int n_chains, int64_t T_chain);
+int rsv_ens_set_streams(rsv_ctx *ctx, const uint64_t *states /* n_chains x 4 */);
+int rsv_ens_get_streams(rsv_ctx *ctx, uint64_t *states /* n_chains x 4 */);
+/* one momenta draw per chain (sampler.py:136-141); normals may be null */
+int rsv_ens_refresh_momenta(rsv_ctx *ctx, double *normals /* n_chains x T_chain, host */);
+/* n_rounds proposals of every chain; accept / delta_h (+inf: diverged) of
+ * the last round per chain, either may be null */
+int rsv_ens_hmc_update(rsv_ctx *ctx, double step_size, int n_steps, int fuse, int n_rounds, int32_t *accept,
+                       double *delta_h);
+/* accepted / diverged proposals per chain since rsv_ens_set_streams */
+int rsv_ens_counts(rsv_ctx *ctx, int32_t *n_accept, int32_t *n_diverged);
+
 /* %globaltimer stamps (ns) of the last proposal, taken inside the kernels:
  * [0] momenta kernel entry (first CTA), [1] its exit (last CTA), [2]
  * trajectory kernel entry (CTA 0), [3] its exit (Metropolis step), [4] the

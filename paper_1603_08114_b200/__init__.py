@@ -14,6 +14,7 @@ from .integrator import (DH_DIVERGENCE_THRESHOLD, CudaBackend, DeviceChain, MDCo
                          kernel3_half_position)
 from .model import (PARAM_NAMES, Dataset, Params, PhaseState, grad_neg_log_posterior, hamiltonian,
                     log_posterior, scalar_pack)
+from .ensemble import Ensemble, sfc64_states
 from .sharded import ShardedChain, hmc_update_distributed, hmc_update_local, shard_bounds
 from .rng import RsvBitGenerator, make_rng, seed_material, store_stream_state, stream_state
 from .sampler import (Chain, ChainSample, DivergenceStormError, PriorSpec, SamplerConfig, default_init,
@@ -23,7 +24,7 @@ from .sampler import (Chain, ChainSample, DivergenceStormError, PriorSpec, Sampl
 __version__ = "0.1.0"
 
 __all__ = [
-    "Chain", "ChainSample", "CudaBackend", "DH_DIVERGENCE_THRESHOLD", "Dataset", "DeviceChain",
+    "Chain", "ChainSample", "CudaBackend", "Ensemble", "sfc64_states", "DH_DIVERGENCE_THRESHOLD", "Dataset", "DeviceChain",
     "DivergenceStormError", "MDConfig", "PARAM_NAMES", "Params", "PhaseState", "PriorSpec", "RsvBitGenerator",
     "SamplerConfig", "ShardedChain", "SyntheticTruth", "hmc_update_distributed", "hmc_update_local", "shard_bounds", "ar1_path", "default_backend", "default_init", "elementary_step",
     "grad_neg_log_posterior", "hamiltonian", "hmc_update_volatility", "integrate_trajectory",

@@ -91,6 +91,13 @@ _SIGS = {
     "rsv_get_timing": (ctypes.c_int, [_CTX, _D, _D, _D]),
     "rsv_launch_count": (ctypes.c_int64, [_CTX]),
     "rsv_kernel_stamps": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
+    "rsv_ens_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
+    "rsv_ens_set_streams": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
+    "rsv_ens_get_streams": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
+    "rsv_ens_refresh_momenta": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
+    "rsv_ens_hmc_update": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_void_p, ctypes.c_void_p]),
+    "rsv_ens_counts": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p]),
     "rsv_set_l2_flush": (ctypes.c_int, [_CTX, ctypes.c_int64]),
     "rsv_measure_fp64_peak": (ctypes.c_int, [_CTX, _D]),
     "rsv_create_shard": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int64, ctypes.c_int64,

@@ -120,15 +120,17 @@ __device__ __forceinline__ double site_energy(double d, double dprev, double p, 
 
 // Energies and statistics of the thread's owned core sites (branch-free on
 // the common path; `edge` threads handle the global first site).
+// firstm bit r: site r is the first of its series (stationary AR prior, no
+// predecessor term).
 template <int R, bool STATS = true>
 __device__ __forceinline__ void tile_energy(const double (&d)[R], const double (&p)[R], const double (&av)[R],
-                                            const double (&lv)[R], double dl, uint32_t core, bool edge, int64_t g0,
+                                            const double (&lv)[R], double dl, uint32_t core, uint32_t firstm,
                                             const TrajConsts &s, const unsigned long long *tab, double (&v)[6]) {
 #pragma unroll
   for (int r = 0; r < R; r++) {
     const double dprev = r ? d[r - 1] : dl;
     const double q = lv[r] - s.xm;
-    const bool first = edge && (g0 + r == 0);
+    const bool first = (firstm >> r) & 1;
     const double en = site_energy(d[r], dprev, p[r], s.emu * av[r], q, first, s, tab);
     const bool c = (core >> r) & 1;
     v[0] += c ? en : 0.0;
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_kernel(TrajArgs A) {
   {
     double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
     double v[6] = {0, 0, 0, 0, 0, 0};
-    tile_energy<R>(d, p, av, lv, dl, core, edge, g0, s, s_tab, v);
+    tile_energy<R>(d, p, av, lv, dl, core, (edge && g0 <= 0 && g0 + R > 0) ? 1u << (int)(-g0) : 0u, s, s_tab, v);
     hold = v[0];
     asm volatile("" ::: "memory");
 #pragma unroll
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_kernel(TrajArgs A) {
     }
     double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
     double v[6] = {0, 0, 0, 0, 0, 0};
-    tile_energy<R>(d, p, av, lv, dl, core, edge, g0, s, s_tab, v);
+    tile_energy<R>(d, p, av, lv, dl, core, (edge && g0 <= 0 && g0 + R > 0) ? 1u << (int)(-g0) : 0u, s, s_tab, v);
     const int64_t gi0 = g0;
     if (full && core == (1u << R) - 1) {
 #pragma unroll
@@ -531,6 +533,28 @@ __device__ __forceinline__ void stage_tile(const TrajArgs &A, const double *hsrc
   tma_load_1d(stage + 3 * W + off, A.lrv + lo, bytes, bar);
 }
 
+// Ensemble: the h window is split at chain boundaries, each piece read from
+// its chain's current buffer (boundaries sit on multiples of Tc, a multiple of
+// 8 sites, so every piece stays 16-byte aligned).
+template <int W>
+__device__ __forceinline__ void stage_tile_ens(const TrajArgs &A, int tile, double *stage, uint64_t *bar) {
+  const int64_t g = (int64_t)tile * A.g.core - A.g.halo;
+  const int64_t lo = g < 0 ? 0 : g, hi = min(g + W, A.Tpad);
+  const uint32_t bytes = (uint32_t)((hi - lo) * 8);
+  const int off = (int)(lo - g);
+  mbar_expect_tx(bar, 4 * bytes);
+  for (int64_t x = lo; x < hi;) {
+    const int64_t c = x / A.Tc;
+    const int64_t e = min(hi, (c + 1) * A.Tc);
+    const double *src = (A.ens_cur[c] ? A.hbuf1 : A.hbuf0) + x;
+    tma_load_1d(stage + 0 * W + (x - g), src, (uint32_t)((e - x) * 8), bar);
+    x = e;
+  }
+  tma_load_1d(stage + 1 * W + off, A.p_in + lo, bytes, bar);
+  tma_load_1d(stage + 2 * W + off, A.a + lo, bytes, bar);
+  tma_load_1d(stage + 3 * W + off, A.lrv + lo, bytes, bar);
+}
+
 template <int R, int NT>
 struct PersistSmem {
   static constexpr int NW = NT / 32;
@@ -541,11 +565,12 @@ struct PersistSmem {
   double red[NW * TR_NV];
   double v[NW * TR_NV + TR_NV];
   alignas(16) unsigned long long tab[RSV_EXP_TAB_N];
+  double epart[2][NW][8];  // ensemble: per-warp chain partials of a tile (by staging buffer)
   uint64_t bar[3];  // two staging buffers, the exp table
   int last;
 };
 
-template <int R, int NT, int MINB, bool FUSE, bool STATS>
+template <int R, int NT, int MINB, bool FUSE, bool STATS, bool ENS = false>
 __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   using SM = PersistSmem<R, NT>;
   constexpr int NW = SM::NW, W = SM::W;
@@ -576,7 +601,10 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     // the exp table (16 KB) arrives by one bulk copy alongside the first tile
     mbar_expect_tx(&S.bar[2], (uint32_t)sizeof(S.tab));
     tma_load_1d(S.tab, g_exp_tab2, (uint32_t)sizeof(S.tab), &S.bar[2]);
-    if (tile < n_tiles) stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0]);
+    if (tile < n_tiles) {
+      if (ENS) stage_tile_ens<W>(A, tile, S.stage[0], &S.bar[0]);
+      else stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0]);
+    }
   }
   __syncthreads();
   mbar_wait(&S.bar[2], 0);
@@ -595,7 +623,8 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     // the next tile into it while this one runs
     if (tid == 0 && tile + (int)gridDim.x < n_tiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      stage_tile<W>(A, hsrc, tile + gridDim.x, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
+      if (ENS) stage_tile_ens<W>(A, tile + gridDim.x, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
+      else stage_tile<W>(A, hsrc, tile + gridDim.x, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
     }
     const double *stg = S.stage[buf];
     const int64_t t0 = (int64_t)tile * A.g.core;
@@ -621,6 +650,18 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
       av[r] = a2.x; av[r + 1] = a2.y;
       lv[r] = l2.x; lv[r + 1] = l2.y;
     }
+    // ensemble: a thread's R sites never straddle a chain boundary (Tc and
+    // the window offsets are multiples of R); cf / cl: my first / last site
+    // is the first / last of its chain, so the neighbour across is cut off
+    bool cf = false, cl = false;
+    int64_t chain = 0;
+    if (ENS) {
+      const int64_t m = ((g0 % A.Tc) + A.Tc) % A.Tc;
+      cf = m == 0;
+      cl = m + R == A.Tc;
+      chain = g0 >= 0 ? g0 / A.Tc : -1;
+    }
+    uint32_t firstm = 0;
 #pragma unroll
     for (int r = 0; r < R; r++) {
       const int64_t gi = g0 + r;
@@ -628,7 +669,13 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
       const bool c = in && own_lane && gi >= t0 && gi < t1 && gi >= A.own_lo && gi < A.own_hi;
       live |= (uint32_t)in << r;
       core |= (uint32_t)c << r;
-      endm |= (uint32_t)(gi + goff == 0 || gi + goff == Tg - 1) << r;
+      if (ENS) {
+        endm |= (uint32_t)((cf && r == 0) || (cl && r == R - 1)) << r;
+        firstm |= (uint32_t)(cf && r == 0) << r;
+      } else {
+        endm |= (uint32_t)(gi + goff == 0 || gi + goff == Tg - 1) << r;
+        firstm |= (uint32_t)(gi + goff == 0) << r;
+      }
       cm[r] = c ? ~0u : 0u;
       d[r] = in ? d[r] - s.mu : 0.0;
       p[r] = in ? p[r] : 0.0;
@@ -644,9 +691,9 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     double vold[6] = {0, 0, 0, 0, 0, 0};
     {
       const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      tile_energy<R, STATS>(d, p, av, lv, dl, core, edge, g0 + goff, s, S.tab, vold);
+      tile_energy<R, STATS>(d, p, av, lv, dl, core, firstm, s, S.tab, vold);
     }
-    if (edge && !A.h_src) {
+    if (!ENS && edge && !A.h_src) {
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if ((core >> r) & 1) {
@@ -670,8 +717,12 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
       // lanes 0 / 31 get their own value back: those are ghost lanes (or the
       // CTA window edges, inside the halo) whose stale values never reach a
       // core site; next to a global end the neighbour lane is non-live (d = 0)
-      const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      const double dr = __shfl_down_sync(0xffffffffu, d[0], 1);
+      double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
+      double dr = __shfl_down_sync(0xffffffffu, d[0], 1);
+      if (ENS) {  // no coupling across chain boundaries
+        dl = cf ? 0.0 : dl;
+        dr = cl ? 0.0 : dr;
+      }
       if (warp_edge) kick<true, R>(d, p, Ad, Cd, dl, dr, s, S.tab, live, endm, cm, nmax);
       else kick<false, R>(d, p, Ad, Cd, dl, dr, s, S.tab, live, endm, cm, nmax);
       if (FUSE) drift(d, p, step < L - 1 ? s.c_full : s.c_half);
@@ -696,24 +747,26 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     double vnew[6] = {0, 0, 0, 0, 0, 0};
     {
       const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      tile_energy<R, STATS>(d, p, av, lv, dl, core, edge, g0 + goff, s, S.tab, vnew);
+      tile_energy<R, STATS>(d, p, av, lv, dl, core, firstm, s, S.tab, vnew);
     }
+    double *hd = hdst;
+    if (ENS && core) hd = A.ens_cur[chain] ? A.hbuf0 : A.hbuf1;
     if (core == (1u << R) - 1) {
 #pragma unroll
       for (int r = 0; r < R; r += 2) {
-        *reinterpret_cast<double2 *>(hdst + g0 + r) = make_double2(d[r] + s.mu, d[r + 1] + s.mu);
+        *reinterpret_cast<double2 *>(hd + g0 + r) = make_double2(d[r] + s.mu, d[r + 1] + s.mu);
         if (A.p_out) *reinterpret_cast<double2 *>(A.p_out + g0 + r) = make_double2(p[r], p[r + 1]);
       }
     } else if (core) {
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if ((core >> r) & 1) {
-          hdst[g0 + r] = d[r] + s.mu;
+          hd[g0 + r] = d[r] + s.mu;
           if (A.p_out) A.p_out[g0 + r] = p[r];
         }
       }
     }
-    if (edge && !A.h_src) {
+    if (!ENS && edge && !A.h_src) {
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if ((core >> r) & 1) {
@@ -722,12 +775,40 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
         }
       }
     }
-    S.acc[0 * NT + tid] += vnew[0] - hold;
-    S.acc[2 * NT + tid] += vnew[0];
+    if (ENS) {
+      // per-tile partials of the (<= 2) chains the core touches, in a fixed
+      // order: the Metropolis step of each chain sums its tiles in tile order
+      const bool right = g0 >= (t0 / A.Tc + 1) * A.Tc;
+      const double fl = nmax > (unsigned)s.n_span ? 1.0 : 0.0;
+      const double dhv = vnew[0] - hold;
+      double w8[8] = {right ? 0.0 : dhv, right ? 0.0 : hold, right ? 0.0 : vnew[0], right ? 0.0 : fl,
+                      right ? dhv : 0.0, right ? hold : 0.0, right ? vnew[0] : 0.0, right ? fl : 0.0};
+      // warp butterflies only (no CTA barrier, no serial thread-0 sum): the
+      // Metropolis step adds the NW warp partials of each tile in warp order
 #pragma unroll
-    for (int k = 0; k < 5; k++) S.acc[(8 + k) * NT + tid] += vnew[1 + k];
-    if (nmax > (unsigned)s.n_span) S.acc[13 * NT + tid] = 1.0;
+      for (int k = 0; k < 8; k++) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) w8[k] += __shfl_xor_sync(0xffffffffu, w8[k], o);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) S.epart[buf][warp][k] = w8[k];
+      }
+    } else {
+      S.acc[0 * NT + tid] += vnew[0] - hold;
+      S.acc[2 * NT + tid] += vnew[0];
+#pragma unroll
+      for (int k = 0; k < 5; k++) S.acc[(8 + k) * NT + tid] += vnew[1 + k];
+      if (nmax > (unsigned)s.n_span) S.acc[13 * NT + tid] = 1.0;
+    }
     __syncthreads();  // all reads of this tile's buffer done before it is refilled
+    if (ENS && warp == 0 && lane < 8) {  // the tile's two chain records, warps summed in order
+      double v = S.epart[buf][0][lane];
+#pragma unroll
+      for (int w = 1; w < NW; w++) v += S.epart[buf][w][lane];
+      double *q = reinterpret_cast<double *>(A.ens_parts + 2 * (size_t)tile);
+      q[lane] = v;  // EnsPart {dh, hold, hnew, flag} x 2
+    }
     c1 = clock64(); cyc_post += c1 - c0;
   }
   if (A.dbg && tid == 0) {
@@ -738,6 +819,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     A.dbg[(size_t)blockIdx.x * 8 + 4] = clock64();
   }
 
+  if (ENS) return;  // every chain's decision: ens_decide_kernel
   // ---- one reduction per CTA ----
   double w[TR_NV];
 #pragma unroll
@@ -824,16 +906,16 @@ static void launch_v(const TrajArgs &a, cudaStream_t s) {
   else traj_kernel<R, NT, MINB, false><<<a.g.n_tiles, NT, 0, s>>>(a);
 }
 
-template <int R, int NT, int MINB, bool FUSE, bool STATS>
+template <int R, int NT, int MINB, bool FUSE, bool STATS, bool ENS = false>
 static void launch_p2(const TrajArgs &a, cudaStream_t s) {
   const size_t smem = sizeof(PersistSmem<R, NT>);
-  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // same (maximal) shared-memory carveout as the momenta kernel: no L1/shared
   // reconfiguration of the SMs between the two kernels of a proposal
-  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS>,
+  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  traj_persistent_kernel<R, NT, MINB, FUSE, STATS><<<a.g.grid, NT, smem, s>>>(a);
+  traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS><<<a.g.grid, NT, smem, s>>>(a);
 }
 template <int R, int NT, int MINB>
 static void launch_p(const TrajArgs &a, cudaStream_t s) {
@@ -874,7 +956,33 @@ const void *traj_kernel_fn(int variant, int fuse, int stats) {
 #undef RSV_FN
 }
 
+// ensemble geometry: the 256-thread persistent shape with the tile core
+// capped at the chain length (a core then touches at most two chains)
+TrajGeom traj_geometry_ens(int64_t T, int64_t Tc, int n_steps, int sm_count) {
+  TrajGeom g = traj_geometry_v(T, n_steps, sm_count, 11);
+  if (!g.ok || g.core <= Tc) return g;
+  g.core = Tc;
+  g.n_tiles = (int)((T + g.core - 1) / g.core);
+  const int slots = kVariants[11].MINB * sm_count;
+  g.grid = g.n_tiles < slots ? g.n_tiles : slots;
+  return g;
+}
+
+const void *traj_kernel_fn_ens(int fuse) {
+  return fuse ? (const void *)traj_persistent_kernel<4, 256, 2, true, false, true>
+              : (const void *)traj_persistent_kernel<4, 256, 2, false, false, true>;
+}
+
+__global__ void ens_decide_kernel(TrajArgs A);
+
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
+  if (a.Tc > 0) {
+    if (a.fuse) launch_p2<4, 256, 2, true, false, true>(a, s);
+    else launch_p2<4, 256, 2, false, false, true>(a, s);
+    ens_decide_kernel<<<(a.n_chains + 127) / 128, 128, 0, s>>>(a);
+    (*launches) += 2;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   switch (a.g.variant) {
     case 0: launch_v<8, 256, 2>(a, s); break;
     case 1: launch_v<4, 256, 3>(a, s); break;
@@ -985,6 +1093,45 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   C->stats[1] = r.accept ? C->ends_new[1] : C->ends_old[1];
   for (int k = 0; k < 5; k++) C->stats[2 + k] = sm[k];
   C->res = r;
+}
+
+// Metropolis step of every chain of an ensemble (sampler.py:155-167 per
+// chain), one thread per chain: sum the chain's tile records in tile order,
+// decide with the chain's own uniform, keep the matching stream state, flip
+// its buffer.
+__global__ void ens_decide_kernel(TrajArgs A) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c == 0) A.ctrl->t_stamp[3] = gtimer();
+  if (c >= A.n_chains) return;
+  const int64_t Tc = A.Tc, core = A.g.core;
+  const int64_t s0 = (int64_t)c * Tc, s1 = s0 + Tc - 1;
+  const int ta = (int)(s0 / core), tb = (int)(s1 / core);
+  double dh = 0.0, fl = 0.0;
+  for (int t = ta; t <= tb; t++) {
+    const int slot = ((int64_t)t * core) / Tc == c ? 0 : 1;
+    const EnsPart &q = A.ens_parts[2 * (size_t)t + slot];
+    dh += q.dh;
+    fl += q.flag;
+  }
+  EnsChain &e = A.ens[c];
+  bool accept = false, drew = false;
+  if (e.overflow) atomicOr(&A.ctrl->err, 4);  // a tail draw beyond the parse window (never in practice)
+  if (fl > 0.0 || e.overflow || !isfinite(dh) || fabs(dh) > 1000.0) {
+    e.last_dh = __longlong_as_double(0x7ff0000000000000LL);
+    e.n_diverged++;
+  } else {
+    e.last_dh = dh;
+    const double u = u01(e.u_word);
+    drew = true;
+    accept = (dh <= 0.0) || (u < exp(-dh));
+  }
+  const uint64_t *st = drew ? e.st_used1 : e.st_used;
+  for (int k = 0; k < 4; k++) e.st[k] = st[k];
+  e.last_accept = accept;
+  if (accept) {
+    e.n_accept++;
+    A.ens_cur[c] ^= 1;
+  }
 }
 
 // ---------------------------------------------------------------------------

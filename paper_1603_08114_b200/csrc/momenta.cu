@@ -597,6 +597,205 @@ __device__ void zig_serial(DevControl *ctrl, const uint64_t *words, int64_t nbuf
   if (st.kind == PRNG_SFC64 && j + 1 > (uint64_t)nbuf) ctrl->err |= 1;  // ran past the generated words
 }
 
+// ---- ensemble: one numpy SFC64 stream per chain ------------------------------
+// SFC64 has no jump-ahead, so a chain's raw words are inherently sequential.
+// A CTA serves 31 chains: warp 0 generates (lane j runs chain j's SFC64 two
+// 64-word chunks ahead into a shared-memory ring), warp j+1 parses chain j's
+// chunks (lanes = words: one table compare per word, a ballot walk over the
+// few multi-word attempts, coalesced stores of the normals).  A round costs
+// one chunk's generation (~15 cycles per word, the sequential floor) since
+// every parse warp has a single chain.
+// The draw is numpy's random_standard_normal on SFC64(SeedSequence([seed,
+// c])) exactly; the stream states after the draw's words and after the
+// Metropolis uniform are both kept for the trajectory kernel's decision.
+constexpr int ZE_G = 31;      // chains per CTA (one parse warp each)
+constexpr int ZE_CH = 64;     // words per chunk
+constexpr int ZE_RING = 256;  // ring words per chain (4 chunks)
+constexpr int ZE_RS = ZE_RING + 1;  // padded row: generator lanes hit distinct banks
+constexpr int ZE_NT = 32 * (ZE_G + 1);
+constexpr int ZE_MMAX = 30;   // tail loops resolvable inside the ring window
+
+struct ZEnsShared {
+  uint64_t ring[ZE_G * ZE_RS];
+  uint64_t snap[ZE_G][4][4];   // generator state before each chunk (by chunk & 3)
+  uint64_t ki[256];
+  double wi[256], fi[256];
+  int32_t n0[ZE_G], carry[ZE_G], done[ZE_G];
+  int32_t ndone;
+};
+
+__global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *normals, int64_t Tc, int C,
+                                                         unsigned long long *dbg) {
+  extern __shared__ __align__(16) unsigned char zesmem[];
+  ZEnsShared &S = *reinterpret_cast<ZEnsShared *>(zesmem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c0 = blockIdx.x * ZE_G;
+  const int nch = min(ZE_G, C - c0);
+  for (int i = tid; i < 256; i += ZE_NT) {
+    S.ki[i] = g_ki[i];
+    S.wi[i] = g_wi[i];
+    S.fi[i] = g_fi[i];
+  }
+  if (tid < ZE_G) {
+    S.n0[tid] = 0;
+    S.carry[tid] = 0;
+    S.done[tid] = tid >= nch;
+  }
+  if (tid == 0) S.ndone = ZE_G - nch;
+  // generator state (warp 0, lane j = chain c0 + j)
+  uint64_t g[4] = {0, 0, 0, 0};
+  const bool gen = warp == 0 && lane < nch;
+  if (gen)
+    for (int k = 0; k < 4; k++) g[k] = E[c0 + lane].st[k];
+  auto gen_chunk = [&](int m) {
+    uint64_t *row = S.ring + lane * ZE_RS;
+    for (int k = 0; k < 4; k++) S.snap[lane][m & 3][k] = g[k];
+    const int o = (m * ZE_CH) & (ZE_RING - 1);
+#pragma unroll 8
+    for (int k = 0; k < ZE_CH; k++) row[o + k] = sfc64_next(g);
+  };
+  if (gen) {
+    gen_chunk(0);
+    gen_chunk(1);
+  }
+  __syncthreads();
+  long long cy_work = 0, cy_wait = 0, t_a = 0;
+  int rounds = 0;
+  for (int r = 0;; r++) {
+    if (S.ndone >= ZE_G) break;
+    rounds++;
+    if (dbg) t_a = clock64();
+    if (warp == 0) {
+      if (gen) gen_chunk(r + 2);
+    } else {
+      for (int j = warp - 1; j < nch; j += ZE_NT / 32 - 1) {
+        if (S.done[j]) continue;
+        const uint64_t *row = S.ring + j * ZE_RS;
+        const int64_t base = (int64_t)r * ZE_CH;
+        int len[2], acc[2];
+        double x[2];
+#pragma unroll
+        for (int hf = 0; hf < 2; hf++) {
+          const int q = hf * 32 + lane;
+          const int k = (int)((base + q) & (ZE_RING - 1));
+          uint64_t w = row[k];
+          const int idx = (int)(w & 0xff);
+          w >>= 8;
+          const uint64_t rabs = (w >> 1) & 0x000fffffffffffffULL;
+          const double fr =
+              __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | rabs)), 4503599627370496.0);
+          x[hf] = __dmul_rn(fr, S.wi[idx]);
+          if (w & 1) x[hf] = -x[hf];
+          len[hf] = 1;
+          acc[hf] = 1;
+          if (!(rabs < S.ki[idx])) {
+            if (idx == 0) {  // exponential tail
+              len[hf] = 0;
+              acc[hf] = 0;
+              for (int m = 1; m <= ZE_MMAX; m++) {
+                const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R,
+                                            glibc_log1p(-u01(row[(k + 2 * m - 1) & (ZE_RING - 1)])));
+                const double yy = -glibc_log1p(-u01(row[(k + 2 * m) & (ZE_RING - 1)]));
+                if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+                  x[hf] = ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
+                  len[hf] = 1 + 2 * m;
+                  acc[hf] = 1;
+                  break;
+                }
+              }
+            } else {  // wedge
+              const double u = u01(row[(k + 1) & (ZE_RING - 1)]);
+              const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(S.fi[idx - 1], S.fi[idx]), u), S.fi[idx]);
+              acc[hf] = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x[hf]), x[hf])) ? 1 : 0;
+              len[hf] = 2;
+            }
+          }
+        }
+        const uint64_t nu = (uint64_t)__ballot_sync(0xffffffffu, len[0] != 1) |
+                            ((uint64_t)__ballot_sync(0xffffffffu, len[1] != 1) << 32);
+        const uint64_t am = (uint64_t)__ballot_sync(0xffffffffu, acc[0]) |
+                            ((uint64_t)__ballot_sync(0xffffffffu, acc[1]) << 32);
+        // walk: positions covered by attempts that started earlier
+        const int e = S.carry[j];
+        uint64_t cov_lo = e ? ((1ull << e) - 1) : 0, cov_hi = 0;
+        bool ovf = false;
+        uint64_t m = nu;
+        while (m) {
+          const int q = __ffsll((long long)m) - 1;
+          m &= m - 1;
+          if ((cov_lo >> q) & 1) continue;
+          const int L = __shfl_sync(0xffffffffu, q < 32 ? len[0] : len[1], q & 31);
+          if (L == 0) { ovf = true; continue; }
+          for (int t = q + 1; t < q + L; t++) {  // at most 60 positions
+            if (t < 64) cov_lo |= 1ull << t;
+            else cov_hi |= 1ull << (t - 64);
+          }
+        }
+        const uint64_t vis = ~cov_lo & am;
+        const int cnt = __popcll(vis);
+        const int64_t n0 = S.n0[j];
+        double *out = normals + (int64_t)(c0 + j) * Tc;
+#pragma unroll
+        for (int hf = 0; hf < 2; hf++) {
+          const int q = hf * 32 + lane;
+          if ((vis >> q) & 1) {
+            const int64_t o = n0 + __popcll(vis & ((1ull << q) - 1));
+            if (o < Tc) out[o] = x[hf];
+          }
+        }
+        if (n0 + cnt >= Tc) {  // the draw ends in this chunk
+          uint64_t v = vis;
+          for (int64_t t = n0; t < Tc - 1; t++) v &= v - 1;
+          const int q = __ffsll((long long)v) - 1;
+          const int L = __shfl_sync(0xffffffffu, q < 32 ? len[0] : len[1], q & 31);
+          if (lane == 0) {
+            EnsChain &ec = E[c0 + j];
+            const int64_t used = base + q + L;
+            const int mc = (int)(used / ZE_CH);
+            uint64_t st[4];
+            for (int k = 0; k < 4; k++) st[k] = S.snap[j][mc & 3][k];
+            for (int64_t t = (int64_t)mc * ZE_CH; t < used; t++) sfc64_next(st);
+            for (int k = 0; k < 4; k++) ec.st_used[k] = st[k];
+            ec.used = (uint64_t)used;
+            ec.u_word = sfc64_next(st);
+            for (int k = 0; k < 4; k++) ec.st_used1[k] = st[k];
+            ec.overflow = ovf ? 1 : 0;
+            S.done[j] = 1;
+            atomicAdd(&S.ndone, 1);
+          }
+        } else if (lane == 0) {
+          S.n0[j] = (int32_t)(n0 + cnt);
+          S.carry[j] = __ffsll((long long)~cov_hi) - 1;
+          if (ovf) E[c0 + j].overflow = 1;
+        }
+        __syncwarp();
+      }
+    }
+    if (dbg) {
+      const long long t_b = clock64();
+      cy_work += t_b - t_a;
+      __syncthreads();
+      cy_wait += clock64() - t_b;
+    } else {
+      __syncthreads();
+    }
+  }
+  if (dbg && lane == 0 && warp < 2) {
+    dbg[(size_t)blockIdx.x * 8 + warp * 2] = cy_work;
+    dbg[(size_t)blockIdx.x * 8 + warp * 2 + 1] = cy_wait;
+    if (warp == 0) dbg[(size_t)blockIdx.x * 8 + 4] = rounds;
+  }
+}
+
+int launch_momenta_ens(EnsChain *ens, double *normals, int64_t Tc, int n_chains, cudaStream_t s, int *launches,
+                       unsigned long long *dbg) {
+  const size_t smem = sizeof(ZEnsShared);
+  cudaFuncSetAttribute(zig_ens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  zig_ens_kernel<<<(n_chains + ZE_G - 1) / ZE_G, ZE_NT, smem, s>>>(ens, normals, Tc, n_chains, dbg);
+  (*launches)++;
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 // Z0: sequential SFC64 words (no jump-ahead exists) + state snapshots.
 __global__ void z0_sfc64_kernel(DevControl *ctrl, uint64_t *words, uint64_t *snaps, int64_t n) {
   if (threadIdx.x || blockIdx.x) return;

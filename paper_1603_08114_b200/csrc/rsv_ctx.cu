@@ -64,6 +64,18 @@ __global__ void ring_store_kernel(DevControl *ctrl, DevResult *ring, int cap, in
   *count = i + 1;
 }
 
+__global__ void ens_gather_kernel(const double *h0, const double *h1, const int8_t *cur, int64_t Tc, int64_t T,
+                                  double *out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < T) out[i] = cur[i / Tc] ? h1[i] : h0[i];
+}
+
+__global__ void ens_advance_kernel(EnsChain *E, int C) {  // refresh_momenta alone: no uniform drawn
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C)
+    for (int k = 0; k < 4; k++) E[c].st[k] = E[c].st_used[k];
+}
+
 }  // namespace
 
 struct rsv_ctx {
@@ -123,6 +135,14 @@ struct rsv_ctx {
   int timing = 0;  // 0 off, 1 per-proposal total, 2 with momenta / trajectory breakdown
   std::vector<cudaEvent_t> evpool;
   std::vector<double> last_traj_ms, last_mom_ms, last_total_ms;
+  // ensemble of independent chains (rsv_ens_create): T = ens_C * ens_Tc
+  int ens_C = 0;
+  int64_t ens_Tc = 0;
+  bool ens_streams = false;
+  int8_t *ens_cur = nullptr;
+  EnsPart *ens_parts = nullptr;
+  EnsChain *ens = nullptr, *h_ens = nullptr;
+  std::map<GraphKey, Cached *> ens_graphs;
 };
 
 static std::string g_err;
@@ -160,11 +180,17 @@ int rsv_destroy(rsv_ctx *c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (auto &kv : c->graphs) {
-    cudaGraphExecDestroy(kv.second->exec);
-    cudaGraphDestroy(kv.second->graph);
-    delete kv.second;
+  for (auto *m : {&c->graphs, &c->ens_graphs}) {
+    for (auto &kv : *m) {
+      cudaGraphExecDestroy(kv.second->exec);
+      cudaGraphDestroy(kv.second->graph);
+      delete kv.second;
+    }
   }
+  if (c->ens_cur) cudaFree(c->ens_cur);
+  if (c->ens_parts) cudaFree(c->ens_parts);
+  if (c->ens) cudaFree(c->ens);
+  if (c->h_ens) cudaFreeHost(c->h_ens);
   if (c->flush_buf) cudaFree(c->flush_buf);
   if (c->dbg) cudaFree(c->dbg);
   for (auto e : c->evpool) cudaEventDestroy(e);
@@ -216,7 +242,7 @@ static int create_impl(rsv_ctx *c, int device, int64_t T, int64_t Tg) {
   c->max_tiles = (int)(T / 64 + 16 * c->sm_count + 8);
   if (c->max_tiles < (int)(momenta_words(Tg) / ZB) + 8) c->max_tiles = (int)(momenta_words(Tg) / ZB) + 8;
   if (const char *v = getenv("RSV_TRAJ_VARIANT")) c->variant = atoi(v);
-  if (getenv("RSV_TRAJ_STAMPS") || getenv("RSV_ZIG_STAMPS")) {
+  if (getenv("RSV_TRAJ_STAMPS") || getenv("RSV_ZIG_STAMPS") || getenv("RSV_ENS_STAMPS")) {
     CK(cudaMalloc(&c->dbg, sizeof(unsigned long long) * 8 * c->max_tiles));
     CK(cudaMemset(c->dbg, 0, sizeof(unsigned long long) * 8 * c->max_tiles));
   }
@@ -348,6 +374,7 @@ int rsv_set_latent(rsv_ctx *c, const double *h, int on_device) {
   int r;
   if ((r = copy_in(c, c->hbuf[0], h, c->T, on_device))) return r;
   CK(cudaMemsetAsync(&c->ctrl->cur, 0, sizeof(int32_t), c->stream));
+  if (c->ens_cur) CK(cudaMemsetAsync(c->ens_cur, 0, (size_t)c->ens_C, c->stream));
   c->has_latent = true;
   return sync(c);
 }
@@ -357,6 +384,16 @@ int rsv_get_latent(rsv_ctx *c, double *h, int on_device) {
   if (!c->has_latent) return fail(c, RSV_E_STATE, "latent path not set");
   CK(cudaSetDevice(c->device));
   int r;
+  if (c->ens_C) {  // ensemble: every chain's current buffer
+    double *dst = h;
+    if (!on_device) dst = c->sh;
+    ens_gather_kernel<<<(unsigned)((c->T + 255) / 256), 256, 0, c->stream>>>(c->hbuf[0], c->hbuf[1], c->ens_cur,
+                                                                           c->ens_Tc, c->T, dst);
+    c->launches++;
+    CK(cudaGetLastError());
+    if (!on_device && (r = copy_out(c, h, c->sh, c->T, 0))) return r;
+    return sync(c);
+  }
   if ((r = pull_ctrl(c))) return r;
   if ((r = copy_out(c, h, c->hbuf[c->h_ctrl->cur & 1], c->T, on_device))) return r;
   return sync(c);
@@ -412,6 +449,7 @@ static MomentaBufs mbufs(rsv_ctx *c) {
 
 static int check_err_bits(rsv_ctx *c) {
   if (c->h_ctrl->err & 1) return fail(c, RSV_E_CUDA, "momenta word budget exhausted (ziggurat shortfall)");
+  if (c->h_ctrl->err & 4) return fail(c, RSV_E_CUDA, "ensemble momenta: a tail draw needed > 30 loops");
   return 0;
 }
 
@@ -1032,6 +1070,201 @@ int rsv_latent_slice(rsv_ctx *c, int64_t offset, int64_t n, double *buf, int to_
                        c->stream));
   }
   return sync(c);
+}
+
+// ---- ensemble of independent chains (config 4) -----------------------------
+int rsv_ens_create(rsv_ctx **out, int device, int n_chains, int64_t T_chain) {
+  if (!out) return fail(nullptr, RSV_E_INVALID, "out is null");
+  *out = nullptr;
+  if (n_chains < 1) return fail(nullptr, RSV_E_INVALID, "need at least one chain, got %d", n_chains);
+  if (T_chain < 64 || T_chain % 8)
+    return fail(nullptr, RSV_E_INVALID, "chain length must be a multiple of 8 and >= 64, got %lld",
+                (long long)T_chain);
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, RSV_E_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(nullptr, RSV_E_INVALID, "device %d out of range", device);
+  rsv_ctx *c = new rsv_ctx();
+  const int64_t T = (int64_t)n_chains * T_chain;
+  c->own_lo = 0;
+  c->own_hi = T;
+  c->ens_C = n_chains;
+  c->ens_Tc = T_chain;
+  c->kind = PRNG_SFC64;
+  int r = create_impl(c, device, T, T);
+  if (!r) {
+    const int64_t tiles = (T + T_chain - 1) / T_chain + (T + 63) / 64 + 16;  // >= tiles of any ensemble geometry
+    if (cudaMalloc(&c->ens_cur, (size_t)n_chains) != cudaSuccess ||
+        cudaMemset(c->ens_cur, 0, (size_t)n_chains) != cudaSuccess ||
+        cudaMalloc(&c->ens_parts, sizeof(EnsPart) * 2 * 8 * (size_t)tiles) != cudaSuccess ||
+        cudaMalloc(&c->ens, sizeof(EnsChain) * (size_t)n_chains) != cudaSuccess ||
+        cudaMemset(c->ens, 0, sizeof(EnsChain) * (size_t)n_chains) != cudaSuccess ||
+        cudaMallocHost(&c->h_ens, sizeof(EnsChain) * (size_t)n_chains) != cudaSuccess)
+      r = fail(c, RSV_E_CUDA, "ensemble buffers: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  if (r) {
+    g_err = c->err;
+    rsv_destroy(c);
+    return r;
+  }
+  *out = c;
+  return 0;
+}
+
+static int ens_check(rsv_ctx *c) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  if (!c->ens_C) return fail(c, RSV_E_STATE, "not an ensemble context (rsv_ens_create)");
+  return 0;
+}
+
+int rsv_ens_set_streams(rsv_ctx *c, const uint64_t *states) {
+  int r;
+  if ((r = ens_check(c))) return r;
+  if (!states) return fail(c, RSV_E_INVALID, "null states");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  memset(c->h_ens, 0, sizeof(EnsChain) * (size_t)c->ens_C);
+  for (int i = 0; i < c->ens_C; i++)
+    for (int k = 0; k < 4; k++) c->h_ens[i].st[k] = states[4 * (size_t)i + k];
+  CK(cudaMemcpyAsync(c->ens, c->h_ens, sizeof(EnsChain) * (size_t)c->ens_C, cudaMemcpyHostToDevice, c->stream));
+  c->ens_streams = true;
+  return sync(c);
+}
+
+static int ens_pull(rsv_ctx *c) {
+  CK(cudaMemcpyAsync(c->h_ens, c->ens, sizeof(EnsChain) * (size_t)c->ens_C, cudaMemcpyDeviceToHost, c->stream));
+  return sync(c);
+}
+
+int rsv_ens_get_streams(rsv_ctx *c, uint64_t *states) {
+  int r;
+  if ((r = ens_check(c))) return r;
+  if (!states) return fail(c, RSV_E_INVALID, "null states");
+  CK(cudaSetDevice(c->device));
+  if ((r = ens_pull(c))) return r;
+  for (int i = 0; i < c->ens_C; i++)
+    for (int k = 0; k < 4; k++) states[4 * (size_t)i + k] = c->h_ens[i].st[k];
+  return 0;
+}
+
+int rsv_ens_refresh_momenta(rsv_ctx *c, double *normals) {
+  int r;
+  if ((r = ens_check(c))) return r;
+  if (!c->ens_streams) return fail(c, RSV_E_STATE, "streams not set (rsv_ens_set_streams)");
+  CK(cudaSetDevice(c->device));
+  int l = 0;
+  if (launch_momenta_ens(c->ens, c->normals, c->ens_Tc, c->ens_C, c->stream, &l,
+                         getenv("RSV_ENS_STAMPS") ? c->dbg : nullptr))
+    return fail(c, RSV_E_CUDA, "ensemble momenta launch failed");
+  ens_advance_kernel<<<(c->ens_C + 127) / 128, 128, 0, c->stream>>>(c->ens, c->ens_C);
+  c->launches += l + 1;
+  CK(cudaGetLastError());
+  if (normals && (r = copy_out(c, normals, c->normals, c->T, 0))) return r;
+  return sync(c);
+}
+
+static int ens_graph(rsv_ctx *c, double dt, int n_steps, int fuse, rsv_ctx::Cached **out) {
+  GraphKey k{-1, n_steps, fuse ? 1 : 0, 0, 0, dt};
+  auto it = c->ens_graphs.find(k);
+  if (it != c->ens_graphs.end()) {
+    *out = it->second;
+    return 0;
+  }
+  const TrajGeom g = traj_geometry_ens(c->T, c->ens_Tc, n_steps, c->sm_count);
+  if (!g.ok) return fail(c, RSV_E_INVALID, "n_steps=%d too large for one trajectory tile", n_steps);
+  auto *cg = new rsv_ctx::Cached();
+  cg->dt = dt;
+  cg->args = traj_args(c, dt, n_steps, fuse, g);
+  cg->args.Tc = c->ens_Tc;
+  cg->args.n_chains = c->ens_C;
+  cg->args.ens_cur = c->ens_cur;
+  cg->args.ens_parts = c->ens_parts;
+  cg->args.ens = c->ens;
+  cudaGraph_t graph;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  int l = 0;
+  bool ok = launch_momenta_ens(c->ens, c->normals, c->ens_Tc, c->ens_C, c->stream, &l) == 0;
+  ok &= launch_trajectory(cg->args, c->stream, &l) == 0;
+  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+  if (!ok || e != cudaSuccess) {
+    delete cg;
+    return fail(c, RSV_E_CUDA, "ensemble graph capture failed: %s", cudaGetErrorString(e));
+  }
+  cg->graph = graph;
+  size_t n = 0;
+  CK(cudaGraphGetNodes(graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  CK(cudaGraphGetNodes(graph, nodes.data(), &n));
+  const void *fn = traj_kernel_fn_ens(fuse);
+  cg->traj_node = nullptr;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    cudaGraphNodeGetType(nd, &t);
+    if (t == cudaGraphNodeTypeKernel) {
+      cudaKernelNodeParams kp;
+      CK(cudaGraphKernelNodeGetParams(nd, &kp));
+      if (kp.func == fn) {
+        cg->traj_node = nd;
+        cg->traj_params = kp;
+      }
+    }
+  }
+  if (!cg->traj_node) return fail(c, RSV_E_CUDA, "ensemble trajectory node not found");
+  CK(cudaGraphInstantiate(&cg->exec, graph, 0));
+  c->ens_graphs.emplace(k, cg);
+  *out = cg;
+  return 0;
+}
+
+int rsv_ens_hmc_update(rsv_ctx *c, double dt, int n_steps, int fuse, int n_rounds, int32_t *accept,
+                       double *delta_h) {
+  int r;
+  if ((r = ens_check(c))) return r;
+  if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
+  if (!c->ens_streams) return fail(c, RSV_E_STATE, "streams not set (rsv_ens_set_streams)");
+  if (n_rounds < 1) return fail(c, RSV_E_INVALID, "n_rounds must be >= 1");
+  CK(cudaSetDevice(c->device));
+  rsv_ctx::Cached *cg = nullptr;
+  if ((r = ens_graph(c, dt, n_steps, fuse, &cg))) return r;
+  if (c->timing && (r = ensure_events(c, 4 * (size_t)n_rounds + 4))) return r;
+  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
+  for (int i = 0; i < n_rounds; i++) {
+    if (c->flush_bytes > 0) CK(cudaMemsetAsync(c->flush_buf, i & 0xff, (size_t)c->flush_bytes, c->stream));
+    if (c->timing) CK(cudaEventRecord(c->evpool[4 + 4 * i], c->stream));
+    CK(cudaGraphLaunch(cg->exec, c->stream));
+    if (c->timing) CK(cudaEventRecord(c->evpool[4 + 4 * i + 3], c->stream));
+    c->launches += 3;
+  }
+  if ((r = ens_pull(c))) return r;
+  if ((r = pull_ctrl(c)) || (r = check_err_bits(c))) return r;
+  for (int i = 0; i < c->ens_C; i++) {
+    if (accept) accept[i] = c->h_ens[i].last_accept;
+    if (delta_h) delta_h[i] = c->h_ens[i].last_dh;
+  }
+  if (c->timing) {
+    c->last_traj_ms.assign(n_rounds, 0.0);
+    c->last_mom_ms.assign(n_rounds, 0.0);
+    c->last_total_ms.assign(n_rounds, 0.0);
+    for (int i = 0; i < n_rounds; i++) {
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, c->evpool[4 + 4 * i], c->evpool[4 + 4 * i + 3]));
+      c->last_total_ms[i] = t;
+    }
+  }
+  return 0;
+}
+
+int rsv_ens_counts(rsv_ctx *c, int32_t *n_accept, int32_t *n_diverged) {
+  int r;
+  if ((r = ens_check(c))) return r;
+  CK(cudaSetDevice(c->device));
+  if ((r = ens_pull(c))) return r;
+  for (int i = 0; i < c->ens_C; i++) {
+    if (n_accept) n_accept[i] = c->h_ens[i].n_accept;
+    if (n_diverged) n_diverged[i] = c->h_ens[i].n_diverged;
+  }
+  return 0;
 }
 
 int rsv_kernel_stamps(rsv_ctx *c, uint64_t out[5]) {

@@ -44,6 +44,19 @@ struct TilePart {  // per-tile partial sums over the tile's core sites
   double flag;     // > 0 if any core site left [-50, 50] (or NaN) at a kick
 };
 
+// ---- ensemble of independent chains (rsv_ens_*) ------------------------------
+struct EnsPart {  // per trajectory tile: partials of the (<= 2) chains its core touches
+  double dh, hold, hnew, flag;
+};
+struct EnsChain {  // per chain: sfc64 stream and the last proposal's bookkeeping
+  uint64_t st[4];        // stream state for the next draw (a, b, c, counter)
+  uint64_t st_used[4];   // state after the momenta's words (no uniform drawn)
+  uint64_t st_used1[4];  // ... and after the Metropolis uniform
+  uint64_t u_word, used;
+  double last_dh;        // +inf when the proposal diverged
+  int32_t last_accept, n_accept, n_diverged, overflow;
+};
+
 struct DevResult {  // mirrors rsv_result
   int32_t accept, diverged;
   double delta_h, h_old, h_new;

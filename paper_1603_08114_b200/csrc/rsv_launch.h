@@ -34,6 +34,8 @@ struct TrajGeom {
   int grid;       // CTAs launched (== n_tiles, or the persistent grid)
 };
 TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant);
+TrajGeom traj_geometry_ens(int64_t T, int64_t Tc, int n_steps, int sm_count);
+const void *traj_kernel_fn_ens(int fuse);
 int traj_num_variants();
 
 // Trajectory constants derived on the host from (params, dt): passed by
@@ -74,8 +76,18 @@ struct TrajArgs {
   int integrate_only;   // 1: only reduce (rsv_integrate): no Metropolis, no stream update
   int stats;            // compute the theta statistics of both paths (persistent kernel)
   unsigned long long *dbg;  // optional per-tile %globaltimer stamps (8 per tile), development aid
+  // ensemble of independent chains: T = n_chains * Tc sites, chain-major;
+  // Tc == 0 for a single chain
+  int64_t Tc;
+  int n_chains;
+  int8_t *ens_cur;      // per chain: which h buffer holds its current path
+  EnsPart *ens_parts;   // per tile: [2] partials
+  EnsChain *ens;        // per chain bookkeeping
 };
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches);
+// ensemble: per-chain sfc64 momenta (numpy SFC64 + ziggurat, one thread per chain)
+int launch_momenta_ens(EnsChain *ens, double *normals, int64_t Tc, int n_chains, cudaStream_t s, int *launches,
+                       unsigned long long *dbg = nullptr);
 const void *traj_kernel_fn(int variant, int fuse, int stats);  // for locating the node in a captured graph
 
 

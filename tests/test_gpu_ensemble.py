@@ -1,0 +1,108 @@
+"""GPU parity of the chain ensemble (BASELINE config 4): every chain of an
+``Ensemble`` must do exactly what the reference's single-chain
+hmc_update_volatility (sampler.py:144-167) does with that chain's own
+``Generator(SFC64(SeedSequence([seed, c])))`` -- bit-exact momenta and
+stream positions, the same accept sequence, h and dH to the tolerances of
+test_gpu_parity.py."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1603_08114_b200 as P
+from conftest import TRUE
+
+pytestmark = pytest.mark.gpu
+
+THETA = P.Params(**TRUE)
+
+
+def _sims(C, Tc, base=100):
+    sims = [P.simulate_rsv(THETA, Tc, seed=base + c) for c in range(C)]
+    y = np.stack([s.dataset.returns for s in sims])
+    lrv = np.stack([s.dataset.log_rv for s in sims])
+    h = np.stack([s.latent for s in sims])
+    return y, lrv, h
+
+
+def test_ensemble_momenta_bit_exact_per_chain():
+    C, Tc, seed = 5, 200, 7
+    gens = [np.random.Generator(np.random.SFC64(np.random.SeedSequence([seed, c]))) for c in range(C)]
+    with P.Ensemble(C, Tc) as ens:
+        ens.seed(seed)
+        for _ in range(2):  # two draws: the streams continue exactly
+            got = ens.refresh_momenta()
+            st = ens.streams()
+            for c in range(C):
+                want = gens[c].standard_normal(Tc)
+                assert np.array_equal(got[c].view(np.uint64), want.view(np.uint64)), c
+                assert [int(x) for x in st[c]] == [int(x) for x in gens[c].bit_generator.state["state"]["state"]]
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+def test_ensemble_matches_single_chain_oracle(fuse):
+    C, Tc, L, dt, seed = 6, 256, 12, 0.03, 11
+    y, lrv, h0 = _sims(C, Tc)
+    streams = [O.Stream("sfc64", np.random.SeedSequence([seed, c])) for c in range(C)]
+    h = h0.copy()
+    with P.Ensemble(C, Tc) as ens:
+        ens.set_data(y, lrv)
+        ens.set_params(THETA)
+        ens.set_latent(h0)
+        ens.seed(seed)
+        n_acc = np.zeros(C, dtype=int)
+        for _ in range(4):
+            acc, dh = ens.hmc_update(dt, L, fuse=fuse)
+            for c in range(C):
+                if fuse:  # the oracle's trajectory is unfused: compare dH loosely, decisions exactly
+                    hc, a, d = O.hmc_update(h[c], THETA, y[c], lrv[c], dt, L, streams[c])
+                    assert abs(dh[c] - d) <= 1e-6
+                else:
+                    hc, a, d = O.hmc_update(h[c], THETA, y[c], lrv[c], dt, L, streams[c])
+                    assert abs(dh[c] - d) <= 1e-9 * max(1.0, abs(d)), (c, dh[c], d)
+                assert bool(acc[c]) == a, c
+                h[c] = hc
+                n_acc[c] += int(a)
+        got = ens.latent()
+        tol = 1e-6 if fuse else 1e-10
+        assert np.max(np.abs(got - h)) <= tol * max(1.0, float(np.max(np.abs(h))))
+        st = ens.streams()
+        for c in range(C):
+            assert [int(x) for x in st[c]] == streams[c].state_words()[0]
+        a, d = ens.counts()
+        assert np.array_equal(a, n_acc) and not d.any()
+
+
+def test_ensemble_divergent_chain_rejects_without_uniform():
+    # chain 1 gets a step size so large that it diverges; the other chains
+    # are unaffected and its stream must not consume the Metropolis uniform
+    C, Tc, L, seed = 3, 128, 8, 5
+    y, lrv, h0 = _sims(C, Tc, base=300)
+    h0[1, 40] = 49.9  # next to the |h| <= 50 boundary: the first kick leaves it
+    streams = [O.Stream("sfc64", np.random.SeedSequence([seed, c])) for c in range(C)]
+    with P.Ensemble(C, Tc) as ens:
+        ens.set_data(y, lrv)
+        ens.set_params(THETA)
+        ens.set_latent(h0)
+        ens.seed(seed)
+        acc, dh = ens.hmc_update(0.5, L)
+        for c in range(C):
+            hc, a, d = O.hmc_update(h0[c], THETA, y[c], lrv[c], 0.5, L, streams[c])
+            assert bool(acc[c]) == a
+            if np.isinf(d):
+                assert np.isinf(dh[c])
+            else:
+                assert abs(dh[c] - d) <= 1e-9 * max(1.0, abs(d))
+        st = ens.streams()
+        for c in range(C):
+            assert [int(x) for x in st[c]] == streams[c].state_words()[0]
+        assert np.isinf(dh[1])
+
+
+def test_ensemble_rejects_bad_shapes():
+    with pytest.raises(ValueError):
+        P.Ensemble(2, 100)  # chain length must be a multiple of 8
+    with P.Ensemble(2, 64) as ens:
+        with pytest.raises(ValueError):
+            ens.set_latent(np.zeros((3, 64)))
+        with pytest.raises(RuntimeError):
+            ens.hmc_update(0.02, 5)  # nothing set yet

@@ -156,3 +156,10 @@ def test_prior_and_config_defaults_mirror_reference():
     assert (pr.mu_var, pr.var_shape, pr.var_scale, pr.phi_a, pr.phi_b) == (100.0, 2.5, 0.025, 20.0, 1.5)
     cfg = P.SamplerConfig()
     assert cfg.md.step_size == 0.02 and cfg.md.n_steps == 50
+
+
+def test_ensemble_seeding_is_numpy_seedsequence():
+    st = P.sfc64_states(5, 3)
+    for c in range(3):
+        want = np.random.SFC64(np.random.SeedSequence([5, c])).state["state"]["state"]
+        assert [int(x) for x in st[c]] == [int(x) for x in want]
