@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-ensemble", action="store_true")
+    ap.add_argument("--ens-chains", type=int, default=4096)
+    ap.add_argument("--ens-T", type=int, default=4096)
     ap.add_argument("--sharded", action="store_true",
                     help="use the time-sharded path even at N=1 (exercises the N>1 code on one GPU)")
     return ap.parse_args()
@@ -106,6 +109,35 @@ class ClockSampler:
                           if s[2 + i].strip().lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
+
+
+def ensemble_run(P, theta, dt, L, C, Tc, steps):
+    """Config 4: C independent chains x Tc sites, one numpy SFC64 stream per
+    chain (SeedSequence([seed, c])); one round = one HMC proposal of every
+    chain.  Device-timed per round (event pair); the working set (>= 6 x 8 B
+    x C x Tc = 768 MiB at 4096 x 4096) exceeds L2, so no flush is needed."""
+    tr = P.simulate_rsv(theta, Tc, seed=5)
+    ens = P.Ensemble(C, Tc)
+    ens.set_data(tr.dataset.returns, tr.dataset.log_rv)
+    ens.set_params(theta)
+    ens.set_latent(tr.latent)
+    ens.seed(1)
+    ens.hmc_update(dt, L, rounds=3)
+    ens.set_timing(1)
+    n0 = ens.launch_count()
+    ens.hmc_update(dt, L, rounds=steps)
+    launches = ens.launch_count() - n0
+    ms = ens.timing_ms()
+    ens.set_timing(0)
+    acc, _ = ens.counts()
+    out = {"workload": f"config 4: {C} chains x T={Tc}, L={L}, dt={dt}, sfc64 per chain (SeedSequence([1, c]))",
+           "metric": METRIC, "value": C * Tc * L / (ms * 1e-3), "unit": UNIT, "ms_per_round": ms,
+           "chain_trajectories_per_s": C / (ms * 1e-3), "accept_rate": float(acc.sum()) / ((steps + 3) * C),
+           "rounds": steps, "gpu_launches": int(launches),
+           "data": "one simulate_rsv series (seed 5) shared by every chain; latent starts at the true path",
+           "l2": "working set > L2 (768 MiB): not flushed"}
+    ens.close()
+    return out
 
 
 def cpu_baseline(T, L, dt, kind, seconds, data, h0):
@@ -230,6 +262,8 @@ def main():
     traj_ms, mom_ms, bd_total_ms = ch.timing()
     ch.set_timing(0)
     ch.set_l2_flush(0)
+    ch.hmc_update_many(dt, L, 4, results=False)
+    stamps = ch.kernel_stamps()  # in-kernel %globaltimer split (no events, no flush)
     accept_rate = float(np.mean([r.accept for r in res]))
     step_s = step_ms * 1e-3
     value = T * L / step_s
@@ -251,7 +285,8 @@ def main():
     h_host = torch.empty(T, dtype=torch.float64, pin_memory=True).numpy()
     h_host[:] = truth.latent
     h = h_host
-    P.hmc_update_volatility(h, theta, data, md, rng, backend=be)  # warm
+    for _ in range(max(3, args.warmup)):  # warm: graph, pinned result buffers
+        h, _, _ = P.hmc_update_volatility(h, theta, data, md, rng, backend=be)
     e2e_steps = max(3, min(args.steps, 20))
     n_acc = 0
     t0 = time.perf_counter()
@@ -308,6 +343,8 @@ def main():
                 be._chains.pop(Tq, None)
                 cq.close()
             extra["sweep"] = sweep
+        if not args.no_ensemble:
+            extra["ensemble"] = ensemble_run(P, theta, dt, L, args.ens_chains, args.ens_T, args.steps)
         if not args.no_cpu:
             extra["cpu_baseline"] = cpu_baseline(T, L, dt, args.prng, args.cpu_seconds, data, truth.latent)
 
@@ -324,6 +361,7 @@ def main():
                        "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB memset, not timed)"},
             "trajectories_per_s": 1.0 / step_s, "accept_rate": accept_rate,
             "breakdown_ms": {"momenta": mom_ms, "trajectory": traj_ms, "proposal_with_event_nodes": bd_total_ms},
+            "in_kernel_us": stamps,
             "bracket_ms_per_step_incl_flush": bracket_s * 1e3 / args.steps,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -17,6 +17,7 @@ kernels per step (``integrator.py:111-146``) run by a pluggable backend
 from __future__ import annotations
 
 import ctypes
+import sys
 from dataclasses import dataclass
 
 import numpy as np
@@ -98,8 +99,28 @@ class DeviceChain:
             raise ValueError(f"latent path length {h.shape[0]} does not match chain length {self.T}")
         self._ck(self._lib.rsv_set_latent(self.ctx, h.ctypes.data, 0))
 
+    def _pinned_out(self) -> np.ndarray:
+        """A page-locked host array for a returned path.  Pool entries are
+        handed out again only once no caller references them any more (the
+        pool's list slot, the loop name and getrefcount's argument are the
+        only references), so a returned path is never overwritten."""
+        pool = self.__dict__.setdefault("_pool", [])
+        for arr in pool:
+            if sys.getrefcount(arr) <= 3:
+                return arr
+        if not pool:  # allocate the pool at once (page-locking is slow)
+            try:
+                import torch
+                ts = [torch.empty(self.T, dtype=torch.float64, pin_memory=True) for _ in range(3)]
+                self.__dict__["_pool_t"] = ts
+                pool.extend(t.numpy() for t in ts)
+                return pool[0]
+            except Exception:
+                pass
+        return np.empty(self.T)
+
     def get_latent(self, out: np.ndarray | None = None) -> np.ndarray:
-        out = np.empty(self.T) if out is None else out
+        out = self._pinned_out() if out is None else out
         self._ck(self._lib.rsv_get_latent(self.ctx, N.ptr(out), 0))
         return out
 
@@ -112,7 +133,11 @@ class DeviceChain:
         return st
 
     # -- hot path --
-    def hmc_update(self, step_size: float, n_steps: int, fuse: bool = False) -> N.Result:
+    def hmc_update(self, step_size: float, n_steps: int, fuse: bool = False, stats: bool = True) -> N.Result:
+        """One proposal; with stats=False the theta statistics of the kept
+        path are not evaluated (the reference's hmc_update_volatility)."""
+        if not stats:
+            return self.hmc_update_many(step_size, n_steps, 1, fuse)[0]
         r = N.Result()
         self._ck(self._lib.rsv_hmc_update(self.ctx, float(step_size), int(n_steps), int(bool(fuse)),
                                           ctypes.byref(r)))

@@ -144,7 +144,7 @@ def hmc_update_volatility(h: np.ndarray, params: Params, data: Dataset, md: MDCo
     h64 = np.ascontiguousarray(h, dtype=np.float64)
     ch.set_latent(h64)
     ch.set_stream(stream_state(rng))
-    r = ch.hmc_update(md.step_size, md.n_steps, fuse_half_steps)
+    r = ch.hmc_update(md.step_size, md.n_steps, fuse_half_steps, stats=False)
     store_stream_state(rng, ch.get_stream())
     if r.diverged:
         return h, False, DIVERGENT_DELTA_H
