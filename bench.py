@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-ensemble", action="store_true")
+    ap.add_argument("--no-protocol", action="store_true")
     ap.add_argument("--ens-chains", type=int, default=4096)
     ap.add_argument("--ens-T", type=int, default=4096)
     ap.add_argument("--sharded", action="store_true",
@@ -109,6 +110,45 @@ class ClockSampler:
                           if s[2 + i].strip().lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
+
+
+def paper_protocol(no_cpu):
+    """Config 2 as the paper measures it (reference bench.py:121-267): the
+    elementary step at T = 512*B, B = 2..512, 10^4 reps in segments of 100,
+    5 repeats, fit A + C*B; beside it the CPU port with one thread (the
+    reference's SerialBackend role) on fewer reps, and the gain curve."""
+    from paper_1603_08114_b200 import bench_protocol as BP
+    cfg = BP.BenchConfig()
+    study = BP.run_scaling_study(cfg)
+    pts = study.timings["cuda"]
+    fit = study.fits["cuda"]
+    out = {"protocol": "reference bench.py:121-267 (device time of the step launches; state device-resident)",
+           "params": "BENCH_PARAMS (phi .97, mu -1, xi -.3, se2 .05, su2 .1), dt 0.01, seed 0",
+           "points": [{"B": p.b, "T": 512 * p.b, "mean_s": p.mean_seconds, "se_s": p.se_seconds,
+                       "site_updates_per_s": 512 * p.b / p.mean_seconds} for p in pts],
+           "fit_cuda": {"A_s": fit.intercept_a, "C_s_per_B": fit.slope_c, "r2": fit.r_squared}}
+    if not no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        import paper_1603_08114_b200 as P
+        cpu = []
+        for b in cfg.b_values:
+            data = P.simulate_rsv(BP.BENCH_PARAMS, 512 * b, seed=b).dataset
+            h = data.log_rv - BP.BENCH_PARAMS.xi
+            pm = np.random.default_rng(0).standard_normal(h.size)
+            reps = max(20, int(2e6 // (512 * b)))
+            O.integrate(h, pm, BP.BENCH_PARAMS, data.returns, data.log_rv, 0.01, 5, nthreads=1)
+            t0 = time.perf_counter()
+            O.integrate(h, pm, BP.BENCH_PARAMS, data.returns, data.log_rv, 0.01, reps, nthreads=1)
+            cpu.append((b, (time.perf_counter() - t0) / reps))
+        cfit = BP.fit_linear(cpu)
+        out["cpu_port_serial"] = {"points": [{"B": b, "mean_s": t} for b, t in cpu],
+                                  "fit": {"A_s": cfit.intercept_a, "C_s_per_B": cfit.slope_c, "r2": cfit.r_squared},
+                                  "cores": 1}
+        cpu_t = dict(cpu)
+        out["gain_measured"] = [{"B": p.b, "gain": cpu_t[p.b] / p.mean_seconds} for p in pts]
+        out["asymptotic_gain_fit"] = BP.asymptotic_gain(cfit, fit)
+    return out
 
 
 def ensemble_run(P, theta, dt, L, C, Tc, steps):
@@ -310,7 +350,7 @@ def main():
         ch2.elementary_step_inplace(hh, pp, dt)
         import ctypes
         ms = ctypes.c_float()
-        ch2._ck(ch2._lib.rsv_bench_elementary(ch2.ctx, dt, 50, ctypes.byref(ms)))
+        ch2._ck(ch2._lib.rsv_bench_elementary(ch2.ctx, dt, 50, ctypes.byref(ms), None))
         per = ms.value / 50 * 1e-3
         peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
         hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -345,6 +385,8 @@ def main():
             extra["sweep"] = sweep
         if not args.no_ensemble:
             extra["ensemble"] = ensemble_run(P, theta, dt, L, args.ens_chains, args.ens_T, args.steps)
+        if not args.no_protocol:
+            extra["paper_protocol"] = paper_protocol(args.no_cpu)
         if not args.no_cpu:
             extra["cpu_baseline"] = cpu_baseline(T, L, dt, args.prng, args.cpu_seconds, data, truth.latent)
 

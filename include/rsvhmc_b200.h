@@ -107,9 +107,12 @@ int rsv_integrate(rsv_ctx *ctx, const double *h_in, const double *p_in, double s
 int rsv_elementary_step(rsv_ctx *ctx, double *h, double *p, double step_size, int32_t *diverged, int on_device);
 
 /* Paper protocol (bench.py:121-190 time_elementary_step): n_steps streamed
- * elementary steps on the device-resident state left by the last
- * rsv_elementary_step call; *ms = device time of the n_steps launches. */
-int rsv_bench_elementary(rsv_ctx *ctx, double step_size, int n_steps, float *ms);
+ * elementary steps on a device-resident state (set by rsv_bench_state from
+ * host arrays -- null keeps that half -- or left by the previous call /
+ * rsv_elementary_step); *ms = device time of the n_steps launches,
+ * *diverged = any step flagged |h| > 50 (may be null). */
+int rsv_bench_state(rsv_ctx *ctx, const double *h, const double *p);
+int rsv_bench_elementary(rsv_ctx *ctx, double step_size, int n_steps, float *ms, int32_t *diverged);
 
 /* Kernel-level plug-in (integrator.py:50-65 backend.run protocol):
  * _kernels.py:37-41 position_update, :44-54 momentum_update,

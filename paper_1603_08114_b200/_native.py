@@ -74,7 +74,9 @@ _SIGS = {
                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, _I32P, ctypes.c_int]),
     "rsv_elementary_step": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, _I32P,
                                            ctypes.c_int]),
-    "rsv_bench_elementary": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]),
+    "rsv_bench_elementary": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_float),
+                                            ctypes.c_void_p]),
+    "rsv_bench_state": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p]),
     "rsv_position_update": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_int64,
                                            ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
     "rsv_momentum_update": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,

@@ -761,26 +761,70 @@ int rsv_elementary_step(rsv_ctx *c, double *h, double *p, double dt, int32_t *di
 }
 
 // Repeated elementary steps on device-resident (h, p) for the paper protocol
-// (bench.py:121-190 time_elementary_step): ping-pongs sh/sp <-> sh2/sp2.
-int rsv_bench_elementary(rsv_ctx *c, double dt, int n_steps, float *ms) {
+// (bench.py:121-190 time_elementary_step).  The state lives in (sh2, sp2):
+// set by rsv_bench_state or left by rsv_elementary_step; the steps ping-pong
+// with (sh, sp) and the result is moved back to (sh2, sp2) outside the timed
+// events.
+int rsv_bench_state(rsv_ctx *c, const double *h, const double *p) {
   if (!c) return fail(c, RSV_E_INVALID, "null context");
   CK(cudaSetDevice(c->device));
+  int r;
+  if (h && (r = copy_in(c, c->sh2, h, c->T, 0))) return r;
+  if (p && (r = copy_in(c, c->sp2, p, c->T, 0))) return r;
+  return sync(c);
+}
+
+int rsv_bench_elementary(rsv_ctx *c, double dt, int n_steps, float *ms, int32_t *diverged) {
+  if (!c || !ms) return fail(c, RSV_E_INVALID, "null argument");
+  int r;
+  if ((r = check_md(c, dt, n_steps))) return r;
+  if (!c->has_data || !c->has_params) return fail(c, RSV_E_STATE, "data/params not set");
+  CK(cudaSetDevice(c->device));
+  // the n steps are one CUDA graph (cached per (n, dt)): kernel nodes run
+  // back to back without per-launch host submission
+  GraphKey k{-2, n_steps, 0, 0, 0, dt};
+  auto it = c->graphs.find(k);
+  if (it == c->graphs.end()) {
+    auto *cg = new rsv_ctx::Cached();
+    memset(&cg->args, 0, sizeof(cg->args));
+    cg->dt = dt;
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    double *h0 = c->sh2, *p0 = c->sp2, *h1 = c->sh, *p1 = c->sp;
+    int l = 0;
+    bool ok = true;
+    for (int i = 0; i < n_steps; i++) {
+      ok &= launch_elementary_step(h0, p0, h1, p1, c->a, c->lrv, c->prm, dt, c->T, c->dflag, c->stream, &l) == 0;
+      std::swap(h0, h1);
+      std::swap(p0, p1);
+    }
+    if (h0 != c->sh2) {  // result back into the state buffers
+      cudaMemcpyAsync(c->sh2, h0, sizeof(double) * c->T, cudaMemcpyDeviceToDevice, c->stream);
+      cudaMemcpyAsync(c->sp2, p0, sizeof(double) * c->T, cudaMemcpyDeviceToDevice, c->stream);
+    }
+    cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+    if (!ok || e != cudaSuccess) {
+      delete cg;
+      return fail(c, RSV_E_CUDA, "protocol graph capture failed: %s", cudaGetErrorString(e));
+    }
+    cg->graph = graph;
+    cg->traj_node = nullptr;
+    CK(cudaGraphInstantiate(&cg->exec, graph, 0));
+    it = c->graphs.emplace(k, cg).first;
+  }
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaMemsetAsync(c->dflag, 0, sizeof(int32_t), c->stream));
-  double *h0 = c->sh, *p0 = c->sp, *h1 = c->sh2, *p1 = c->sp2;
-  int l = 0;
   CK(cudaEventRecord(e0, c->stream));
-  for (int k = 0; k < n_steps; k++) {
-    LK(launch_elementary_step(h0, p0, h1, p1, c->a, c->lrv, c->prm, dt, c->T, c->dflag, c->stream, &l));
-    std::swap(h0, h1);
-    std::swap(p0, p1);
-  }
+  CK(cudaGraphLaunch(it->second->exec, c->stream));
   CK(cudaEventRecord(e1, c->stream));
-  c->launches += l;
+  c->launches += n_steps;
+  CK(cudaMemcpyAsync(c->h_flag, c->dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaEventSynchronize(e1));
   CK(cudaEventElapsedTime(ms, e0, e1));
+  CK(cudaStreamSynchronize(c->stream));
+  if (diverged) *diverged = *c->h_flag;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return 0;

@@ -106,3 +106,12 @@ def test_ensemble_rejects_bad_shapes():
             ens.set_latent(np.zeros((3, 64)))
         with pytest.raises(RuntimeError):
             ens.hmc_update(0.02, 5)  # nothing set yet
+
+
+def test_paper_protocol_smoke(tmp_path):
+    from paper_1603_08114_b200 import bench_protocol as BP
+    study = BP.run_scaling_study(BP.BenchConfig(b_values=(2, 4), reps=200, repeats=2))
+    pts = study.timings["cuda"]
+    assert [p.b for p in pts] == [2, 4] and all(p.mean_seconds > 0 for p in pts)
+    paths = BP.emit_report(study, tmp_path)
+    assert paths["fits"].read_text().splitlines()[1] == "backend,intercept_a,slope_c,r_squared"

@@ -163,3 +163,15 @@ def test_ensemble_seeding_is_numpy_seedsequence():
     for c in range(3):
         want = np.random.SFC64(np.random.SeedSequence([5, c])).state["state"]["state"]
         assert [int(x) for x in st[c]] == [int(x) for x in want]
+
+
+def test_protocol_fit_matches_reference_formulas():
+    from paper_1603_08114_b200 import bench_protocol as BP
+    pts = [(1, 3.0), (2, 5.0), (4, 9.0)]
+    f = BP.fit_linear(pts)
+    assert abs(f.intercept_a - 1.0) < 1e-12 and abs(f.slope_c - 2.0) < 1e-12 and abs(f.r_squared - 1.0) < 1e-12
+    slow = BP.TimingFit(0.0, 10.0, 1.0)
+    assert abs(BP.compute_gain(slow, f, 4) - 40.0 / 9.0) < 1e-12
+    assert abs(BP.asymptotic_gain(slow, f) - 5.0) < 1e-12
+    with pytest.raises(BP.NumericError):
+        BP.fit_linear([(2, 1.0), (2, 2.0)])
