@@ -25,6 +25,7 @@ extern "C" {
 #define RSV_E_INVALID -1   /* contract violation -> Python ValueError   */
 #define RSV_E_CUDA -2      /* CUDA runtime failure -> RuntimeError      */
 #define RSV_E_STATE -3     /* call order / missing data -> RuntimeError */
+#define RSV_E_STORM -4     /* divergence storm in rsv_run_chain -> DivergenceStormError (sampler.py:39) */
 
 /* Bit generator kinds.  Raw 64-bit words, numpy next_double convention
  * (word >> 11) * 2^-53 for every kind.
@@ -60,6 +61,11 @@ typedef struct {
   uint64_t words_used;   /* raw words consumed: momenta (+1 uniform if drawn)  */
   double u;              /* the Metropolis uniform (NaN if none drawn)         */
 } rsv_result;
+
+/* sampler.py:43-63 PriorSpec */
+typedef struct {
+  double mu_mean, mu_var, xi_mean, xi_var, var_shape, var_scale, phi_a, phi_b;
+} rsv_prior;
 
 typedef struct rsv_ctx rsv_ctx;
 
@@ -148,6 +154,22 @@ int rsv_last_stats(rsv_ctx *ctx, double out[7]);
  * over the last rsv_hmc_update_many call.  Level 0 disables timing. */
 int rsv_set_timing(rsv_ctx *ctx, int level);
 int rsv_get_timing(rsv_ctx *ctx, double *traj_ms, double *momenta_ms, double *total_ms);
+/* sampler.py:291-358 run_chain with the whole sweep on the device: starting
+ * from the context's params, latent path and stream, n_burnin + n_samples *
+ * thin sweeps of [hmc_update_volatility, update_mu, update_phi,
+ * update_sigma_eta_sq, update_xi, update_sigma_u_sq] -- the theta draws by a
+ * device thread on the same raw-word stream (numpy's normal / next_double /
+ * gamma restated), no host round trip per sweep.  Stores every thin-th sweep
+ * after the burn-in: iters[n_samples], params[n_samples x 5] (phi, mu, xi,
+ * sigma_eta_sq, sigma_u_sq), accept[n_samples], delta_h[n_samples] (+inf:
+ * divergent).  On a divergence storm (> 50 of 100 proposals, sampler.py:
+ * 329-337) returns RSV_E_STORM with the sweep in *storm_sweep.  Afterwards the
+ * context holds the final params, path and stream position. */
+int rsv_run_chain(rsv_ctx *ctx, double step_size, int n_steps, int fuse, const rsv_prior *prior, int64_t n_burnin,
+                  int64_t n_samples, int64_t thin, int64_t *iters, double *params, int32_t *accept,
+                  double *delta_h, int64_t *storm_sweep);
+int rsv_get_params(rsv_ctx *ctx, rsv_params *out);
+
 /* ---- ensemble of independent chains (BASELINE config 4) ----
  * n_chains chains of T_chain sites each (chain-major arrays of
  * n_chains * T_chain doubles for rsv_set_data / rsv_set_latent /

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "librsvhmc_b200.so")
 RSV_E_INVALID = -1
 RSV_E_CUDA = -2
 RSV_E_STATE = -3
+RSV_E_STORM = -4
 
 KINDS = {"philox": 0, "minstd": 1, "pcg32": 2, "sfc64": 3}
 KIND_NAMES = {v: k for k, v in KINDS.items()}
@@ -25,6 +26,11 @@ KIND_NAMES = {v: k for k, v in KINDS.items()}
 class PrngState(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("s", ctypes.c_uint64 * 4), ("pos", ctypes.c_uint64)]
+
+
+class Prior(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("mu_mean", "mu_var", "xi_mean", "xi_var", "var_shape", "var_scale",
+                                               "phi_a", "phi_b")]
 
 
 class Params(ctypes.Structure):
@@ -93,6 +99,10 @@ _SIGS = {
     "rsv_get_timing": (ctypes.c_int, [_CTX, _D, _D, _D]),
     "rsv_launch_count": (ctypes.c_int64, [_CTX]),
     "rsv_kernel_stamps": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
+    "rsv_run_chain": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
+    "rsv_get_params": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
     "rsv_ens_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
     "rsv_ens_set_streams": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
     "rsv_ens_get_streams": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
@@ -141,6 +151,10 @@ class NativeError(RuntimeError):
     pass
 
 
+class StormError(NativeError):
+    """RSV_E_STORM from rsv_run_chain (re-raised as DivergenceStormError)."""
+
+
 def check(code: int, ctx=None) -> None:
     if code == 0:
         return
@@ -148,6 +162,8 @@ def check(code: int, ctx=None) -> None:
     msg = msg.decode() if msg else "unknown error"
     if code == RSV_E_INVALID:
         raise ValueError(msg)
+    if code == RSV_E_STORM:
+        raise StormError(msg)
     raise NativeError(msg)
 
 

@@ -76,35 +76,6 @@ __device__ __forceinline__ bool out_of_range(double t, int n_lo, int n_span) {
   return ((unsigned)(n - n_lo) > (unsigned)n_span) | (hw > 1u);
 }
 
-TrajConsts traj_consts(const DevParams &P, double dt) {
-  TrajConsts s;
-  s.mu = P.mu;
-  s.phi = P.phi;
-  s.dt = dt;
-  s.c_half = 0.5 * dt;
-  s.c_full = dt;
-  s.half_dt = 0.5 * dt;
-  s.alpha = dt * P.inv_su2;
-  const double beta = dt * P.inv_se2;
-  s.bphi = beta * P.phi;
-  s.g_int = s.alpha + beta * (2.0 - P.one_m_phi2);
-  s.g_end = s.alpha + beta;
-  s.emu = P.emu;
-  s.xm = P.xi + P.mu;
-  s.inv2su = 0.5 * P.inv_su2;
-  s.inv2se = 0.5 * P.inv_se2;
-  s.one_m_phi2 = P.one_m_phi2;
-  s.hconst = P.hconst;
-  s.e_k = RSV_INV_LN2_N;
-  s.e_hi = RSV_LN2_N_HI;
-  s.e_lo = RSV_LN2_N_LO;
-  s.e_c5 = 0.0;  // unused (degree-3 polynomial)
-  s.e_c4 = 0.0;
-  s.e_c3 = 1.0 / 6.0;
-  s.n_lo = P.n_lo;
-  s.n_span = P.n_span;
-  return s;
-}
 
 // Variable part of H at one site (the theta-only constants are added in
 // the Metropolis step): 0.5 p^2 + 0.5 d + a e^{-mu} e^{-d} + (q-d)^2/2su2 + AR.
@@ -570,7 +541,7 @@ struct PersistSmem {
   int last;
 };
 
-template <int R, int NT, int MINB, bool FUSE, bool STATS, bool ENS = false>
+template <int R, int NT, int MINB, bool FUSE, bool STATS, bool ENS = false, bool DEVK = false>
 __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   using SM = PersistSmem<R, NT>;
   constexpr int NW = SM::NW, W = SM::W;
@@ -578,7 +549,17 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   extern __shared__ __align__(128) unsigned char psmem[];
   SM &S = *reinterpret_cast<SM *>(psmem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const TrajConsts &s = A.k;
+  // DEVK (run_chain on the device): the theta-dependent constants come from
+  // device memory, written by the theta kernel of the previous sweep; the
+  // others stay constant-bank operands of the parameter block
+  TrajConsts sk = A.k;
+  if (DEVK) {
+    const TrajConsts &q = *A.kdev;
+    sk.mu = q.mu; sk.phi = q.phi; sk.alpha = q.alpha; sk.bphi = q.bphi; sk.g_int = q.g_int;
+    sk.g_end = q.g_end; sk.emu = q.emu; sk.xm = q.xm; sk.inv2su = q.inv2su; sk.inv2se = q.inv2se;
+    sk.one_m_phi2 = q.one_m_phi2; sk.hconst = q.hconst; sk.n_lo = q.n_lo; sk.n_span = q.n_span;
+  }
+  const TrajConsts &s = DEVK ? sk : A.k;
   const double *hsrc;
   double *hdst;
   if (A.h_src) {
@@ -854,7 +835,7 @@ static const TrajVariant kVariants[] = {{8, 256, 2}, {4, 256, 3}, {4, 128, 6}, {
                                         // persistent + TMA-staged (9..14); 12..14 are the
                                         // small-window shapes for short series
                                         {8, 256, 2}, {4, 256, 3}, {4, 256, 2}, {4, 128, 3}, {4, 64, 5},
-                                        {4, 32, 8}};
+                                        {4, 32, 8}, {8, 256, 1}, {6, 256, 1}};
 static bool variant_persistent(int v) { return v >= 9; }
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -906,16 +887,46 @@ static void launch_v(const TrajArgs &a, cudaStream_t s) {
   else traj_kernel<R, NT, MINB, false><<<a.g.n_tiles, NT, 0, s>>>(a);
 }
 
-template <int R, int NT, int MINB, bool FUSE, bool STATS, bool ENS = false>
+template <int R, int NT, int MINB, bool FUSE, bool STATS, bool ENS = false, bool DEVK = false>
 static void launch_p2(const TrajArgs &a, cudaStream_t s) {
   const size_t smem = sizeof(PersistSmem<R, NT>);
-  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS>,
+  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // same (maximal) shared-memory carveout as the momenta kernel: no L1/shared
   // reconfiguration of the SMs between the two kernels of a proposal
-  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS>,
+  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS><<<a.g.grid, NT, smem, s>>>(a);
+  traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK><<<a.g.grid, NT, smem, s>>>(a);
+}
+
+// run_chain on the device: the statistics variant with device-resident
+// theta constants (persistent shapes of the automatic geometry only)
+template <int R, int NT, int MINB>
+static void launch_pd(const TrajArgs &a, cudaStream_t s) {
+  if (a.fuse) launch_p2<R, NT, MINB, true, true, false, true>(a, s);
+  else launch_p2<R, NT, MINB, false, true, false, true>(a, s);
+}
+static bool launch_devk(const TrajArgs &a, cudaStream_t s) {
+  switch (a.g.variant) {
+    case 11: launch_pd<4, 256, 2>(a, s); return true;
+    case 12: launch_pd<4, 128, 3>(a, s); return true;
+    case 13: launch_pd<4, 64, 5>(a, s); return true;
+    case 14: launch_pd<4, 32, 8>(a, s); return true;
+    default: return false;
+  }
+}
+const void *traj_kernel_fn_devk(int variant, int fuse) {
+#define RSV_FN(R, NT, MB)                                                                  \
+  (fuse ? (const void *)traj_persistent_kernel<R, NT, MB, true, true, false, true>        \
+        : (const void *)traj_persistent_kernel<R, NT, MB, false, true, false, true>)
+  switch (variant) {
+    case 11: return RSV_FN(4, 256, 2);
+    case 12: return RSV_FN(4, 128, 3);
+    case 13: return RSV_FN(4, 64, 5);
+    case 14: return RSV_FN(4, 32, 8);
+    default: return nullptr;
+  }
+#undef RSV_FN
 }
 template <int R, int NT, int MINB>
 static void launch_p(const TrajArgs &a, cudaStream_t s) {
@@ -951,6 +962,8 @@ const void *traj_kernel_fn(int variant, int fuse, int stats) {
     case 12: return RSV_FN(4, 128, 3);
     case 13: return RSV_FN(4, 64, 5);
     case 14: return RSV_FN(4, 32, 8);
+    case 15: return RSV_FN(8, 256, 1);
+    case 16: return RSV_FN(6, 256, 1);
     default: return RSV_FN(4, 256, 2);
   }
 #undef RSV_FN
@@ -976,6 +989,11 @@ const void *traj_kernel_fn_ens(int fuse) {
 __global__ void ens_decide_kernel(TrajArgs A);
 
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
+  if (a.kdev) {
+    if (!launch_devk(a, s)) return -1;
+    (*launches)++;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   if (a.Tc > 0) {
     if (a.fuse) launch_p2<4, 256, 2, true, false, true>(a, s);
     else launch_p2<4, 256, 2, false, false, true>(a, s);
@@ -998,6 +1016,8 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
     case 12: launch_p<4, 128, 3>(a, s); break;
     case 13: launch_p<4, 64, 5>(a, s); break;
     case 14: launch_p<4, 32, 8>(a, s); break;
+    case 15: launch_p<8, 256, 1>(a, s); break;
+    case 16: launch_p<6, 256, 1>(a, s); break;
     default: launch_p<4, 256, 2>(a, s); break;
   }
   (*launches)++;
@@ -1042,7 +1062,7 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
     for (int k = 0; k < TR_NV; k++) C->shard_parts[k] = tot[k];
     return;
   }
-  const double cst = A.k.hconst;
+  const double cst = A.kdev ? A.kdev->hconst : A.k.hconst;
   DevResult r;
   r.h_old = tot[1] + cst;
   r.h_new = tot[2] + cst;

@@ -143,6 +143,11 @@ struct rsv_ctx {
   EnsPart *ens_parts = nullptr;
   EnsChain *ens = nullptr, *h_ens = nullptr;
   std::map<GraphKey, Cached *> ens_graphs;
+  // run_chain on the device
+  TrajConsts *kdev = nullptr;
+  DevRun *run = nullptr;
+  void *run_store = nullptr;
+  int64_t run_cap = 0;
 };
 
 static std::string g_err;
@@ -187,6 +192,9 @@ int rsv_destroy(rsv_ctx *c) {
       delete kv.second;
     }
   }
+  if (c->kdev) cudaFree(c->kdev);
+  if (c->run) cudaFree(c->run);
+  if (c->run_store) cudaFree(c->run_store);
   if (c->ens_cur) cudaFree(c->ens_cur);
   if (c->ens_parts) cudaFree(c->ens_parts);
   if (c->ens) cudaFree(c->ens);
@@ -330,6 +338,8 @@ static int check_params(rsv_ctx *c, const rsv_params *p) {
   return 0;
 }
 
+static int refresh_graph_params(rsv_ctx *c);
+
 int rsv_set_params(rsv_ctx *c, const rsv_params *p) {
   if (!c) return fail(c, RSV_E_INVALID, "null context");
   int r = check_params(c, p);
@@ -354,15 +364,23 @@ int rsv_set_params(rsv_ctx *c, const rsv_params *p) {
   q.n_span = (int32_t)ceil((q.mu + 50.0) * RSV_INV_LN2_N) - q.n_lo;
   CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(DevParams), cudaMemcpyHostToDevice, c->stream));
   c->has_params = true;
-  // the trajectory reads the derived constants from its parameter block:
-  // update the kernel node of every cached graph
-  for (auto &kv : c->graphs) {
-    auto *g = kv.second;
-    g->args.k = traj_consts(q, g->dt);
-    void *kp[] = {&g->args};
-    cudaKernelNodeParams np = g->traj_params;
-    np.kernelParams = kp;
-    CK(cudaGraphExecKernelNodeSetParams(g->exec, g->traj_node, &np));
+  return refresh_graph_params(c);
+}
+
+// the trajectory reads the derived constants from its parameter block:
+// update the kernel node of every cached graph after a parameter change
+static int refresh_graph_params(rsv_ctx *c) {
+  const DevParams &q = *c->h_prm;
+  for (auto *m : {&c->graphs, &c->ens_graphs}) {
+    for (auto &kv : *m) {
+      auto *g = kv.second;
+      if (!g->traj_node) continue;  // graphs without a trajectory node (paper protocol)
+      g->args.k = traj_consts(q, g->dt);
+      void *kp[] = {&g->args};
+      cudaKernelNodeParams np = g->traj_params;
+      np.kernelParams = kp;
+      CK(cudaGraphExecKernelNodeSetParams(g->exec, g->traj_node, &np));
+    }
   }
   return sync(c);
 }
@@ -1113,6 +1131,108 @@ int rsv_latent_slice(rsv_ctx *c, int64_t offset, int64_t n, double *buf, int to_
     CK(cudaMemcpyAsync(buf, h, sizeof(double) * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                        c->stream));
   }
+  return sync(c);
+}
+
+// ---- run_chain on the device ---------------------------------------------
+int rsv_get_params(rsv_ctx *c, rsv_params *out) {
+  if (!c || !out) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->has_params) return fail(c, RSV_E_STATE, "params not set (rsv_set_params)");
+  const DevParams &q = *c->h_prm;
+  out->phi = q.phi;
+  out->mu = q.mu;
+  out->xi = q.xi;
+  out->sigma_eta_sq = q.se2;
+  out->sigma_u_sq = q.su2;
+  return 0;
+}
+
+int rsv_run_chain(rsv_ctx *c, double dt, int n_steps, int fuse, const rsv_prior *prior, int64_t n_burnin,
+                  int64_t n_samples, int64_t thin, int64_t *iters, double *params, int32_t *accept,
+                  double *delta_h, int64_t *storm_sweep) {
+  if (!c || !prior) return fail(c, RSV_E_INVALID, "null argument");
+  int r;
+  if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
+  if (c->shard || c->ens_C) return fail(c, RSV_E_STATE, "rsv_run_chain needs a single-chain context");
+  if (n_burnin < 0 || n_samples < 1 || thin < 1) return fail(c, RSV_E_INVALID, "bad burn-in / samples / thin");
+  const double pv[] = {prior->mu_var, prior->xi_var, prior->var_shape, prior->var_scale, prior->phi_a, prior->phi_b};
+  for (double v : pv)
+    if (!(v > 0.0)) return fail(c, RSV_E_INVALID, "prior variances, shapes and scales must be positive");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  if (!c->kdev) CK(cudaMalloc(&c->kdev, sizeof(TrajConsts)));
+  if (!c->run) CK(cudaMalloc(&c->run, sizeof(DevRun)));
+  if (n_samples > c->run_cap) {
+    if (c->run_store) cudaFree(c->run_store);
+    CK(cudaMalloc(&c->run_store, (size_t)n_samples * (5 * sizeof(double) + sizeof(double) + sizeof(int64_t) +
+                                                      sizeof(int32_t))));
+    c->run_cap = n_samples;
+  }
+  DevRun hr;
+  memset(&hr, 0, sizeof(hr));
+  hr.n_burnin = n_burnin;
+  hr.thin = thin;
+  hr.n_store = n_samples;
+  char *base = (char *)c->run_store;
+  hr.params = (double *)base;
+  hr.delta_h = hr.params + 5 * n_samples;
+  hr.iters = (int64_t *)(hr.delta_h + n_samples);
+  hr.accept = (int32_t *)(hr.iters + n_samples);
+  hr.storm_sweep = -1;
+  CK(cudaMemcpyAsync(c->run, &hr, sizeof(DevRun), cudaMemcpyHostToDevice, c->stream));
+  const TrajConsts k0 = traj_consts(*c->h_prm, dt);
+  CK(cudaMemcpyAsync(c->kdev, &k0, sizeof(TrajConsts), cudaMemcpyHostToDevice, c->stream));
+  DevPrior pr{prior->mu_mean, prior->mu_var, prior->xi_mean, prior->xi_var,
+              prior->var_shape, prior->var_scale, prior->phi_a, prior->phi_b};
+  // one sweep = one graph: momenta, trajectory (+ statistics, device theta
+  // constants), theta draws.  Not cached (the prior is baked in).
+  const TrajGeom g = traj_geometry(c->T, n_steps, c->sm_count, c->variant < 0 ? -1 : c->variant);
+  if (!g.ok) return fail(c, RSV_E_INVALID, "n_steps=%d too large for one trajectory tile", n_steps);
+  if (g.variant < 11 || g.variant > 14) return fail(c, RSV_E_STATE, "device run_chain needs a persistent shape");
+  TrajArgs ta = traj_args(c, dt, n_steps, fuse, g);
+  ta.stats = 1;
+  ta.kdev = c->kdev;
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  int l = 0;
+  bool ok = launch_momenta(mbufs(c), c->kind, c->Tg, c->stream, &l) == 0;
+  ok &= launch_trajectory(ta, c->stream, &l) == 0;
+  ok &= launch_theta_sweep(c->ctrl, c->prm, c->kdev, c->run, pr, dt, c->T, c->sfc_snaps, c->stream, &l) == 0;
+  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+  if (!ok || e != cudaSuccess) return fail(c, RSV_E_CUDA, "run_chain graph capture failed: %s", cudaGetErrorString(e));
+  CK(cudaGraphInstantiate(&exec, graph, 0));
+  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
+  const int64_t n_sweeps = n_burnin + n_samples * thin;
+  int64_t storm = -1;
+  cudaError_t le = cudaSuccess;
+  for (int64_t i = 0; i < n_sweeps && le == cudaSuccess; i++) {
+    le = cudaGraphLaunch(exec, c->stream);
+    c->launches += l;
+    if ((i & 255) == 255 || i + 1 == n_sweeps) {  // early exit on a storm
+      if ((le = cudaMemcpyAsync(&hr, c->run, sizeof(DevRun), cudaMemcpyDeviceToHost, c->stream)) == cudaSuccess &&
+          (le = cudaStreamSynchronize(c->stream)) == cudaSuccess && hr.storm_sweep >= 0) {
+        storm = hr.storm_sweep;
+        break;
+      }
+    }
+  }
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  if (le != cudaSuccess) return fail(c, RSV_E_CUDA, "run_chain: %s", cudaGetErrorString(le));
+  CK(cudaMemcpyAsync(&hr, c->run, sizeof(DevRun), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_prm, c->prm, sizeof(DevParams), cudaMemcpyDeviceToHost, c->stream));
+  if ((r = pull_ctrl(c)) || (r = check_err_bits(c))) return r;
+  if ((r = refresh_graph_params(c))) return r;
+  if (storm_sweep) *storm_sweep = storm;
+  if (storm >= 0) return fail(c, RSV_E_STORM, "more than %d of the last %d HMC proposals diverged at sweep %lld",
+                              RUN_STORM_LIMIT, RUN_STORM_WINDOW, (long long)storm);
+  if (hr.degenerate) return fail(c, RSV_E_INVALID, "degenerate full-conditional precision");
+  const int64_t n = hr.stored;
+  if (params) CK(cudaMemcpyAsync(params, hr.params, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost, c->stream));
+  if (delta_h) CK(cudaMemcpyAsync(delta_h, hr.delta_h, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  if (iters) CK(cudaMemcpyAsync(iters, hr.iters, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
+  if (accept) CK(cudaMemcpyAsync(accept, hr.accept, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
   return sync(c);
 }
 

@@ -57,6 +57,24 @@ struct EnsChain {  // per chain: sfc64 stream and the last proposal's bookkeepin
   int32_t last_accept, n_accept, n_diverged, overflow;
 };
 
+// ---- run_chain on the device (theta draws by one device thread) --------------
+struct DevPrior {  // mirrors rsv_prior / PriorSpec (sampler.py:43-63)
+  double mu_mean, mu_var, xi_mean, xi_var, var_shape, var_scale, phi_a, phi_b;
+};
+constexpr int RUN_STORM_WINDOW = 100, RUN_STORM_LIMIT = 50;  // sampler.py:36-37
+struct DevRun {
+  int64_t sweep;        // sweeps done
+  int64_t n_burnin, thin, n_store, stored;
+  double *params;       // n_store x 5: phi, mu, xi, sigma_eta_sq, sigma_u_sq
+  int32_t *accept;      // n_store
+  double *delta_h;      // n_store
+  int64_t *iters;       // n_store
+  int64_t storm_sweep;  // first sweep at which the storm guard fired (-1: none)
+  int32_t ring_n, ring_pos, ring_div;  // divergence flags of the last RUN_STORM_WINDOW proposals
+  uint8_t ring[RUN_STORM_WINDOW];
+  int32_t degenerate;   // a full conditional had a non-positive precision (ValueError in the reference)
+};
+
 struct DevResult {  // mirrors rsv_result
   int32_t accept, diverged;
   double delta_h, h_old, h_new;

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "exp_table.h"
 #include "rsv_internal.h"
 
 namespace rsv {
@@ -36,6 +37,7 @@ struct TrajGeom {
 TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant);
 TrajGeom traj_geometry_ens(int64_t T, int64_t Tc, int n_steps, int sm_count);
 const void *traj_kernel_fn_ens(int fuse);
+const void *traj_kernel_fn_devk(int variant, int fuse);
 int traj_num_variants();
 
 // Trajectory constants derived on the host from (params, dt): passed by
@@ -48,7 +50,36 @@ struct TrajConsts {
   double e_k, e_hi, e_lo, e_c5, e_c4, e_c3;
   int32_t n_lo, n_span;
 };
-TrajConsts traj_consts(const DevParams &P, double dt);
+__host__ __device__ inline TrajConsts traj_consts(const DevParams &P, double dt) {
+  TrajConsts s;
+  s.mu = P.mu;
+  s.phi = P.phi;
+  s.dt = dt;
+  s.c_half = 0.5 * dt;
+  s.c_full = dt;
+  s.half_dt = 0.5 * dt;
+  s.alpha = dt * P.inv_su2;
+  const double beta = dt * P.inv_se2;
+  s.bphi = beta * P.phi;
+  s.g_int = s.alpha + beta * (2.0 - P.one_m_phi2);
+  s.g_end = s.alpha + beta;
+  s.emu = P.emu;
+  s.xm = P.xi + P.mu;
+  s.inv2su = 0.5 * P.inv_su2;
+  s.inv2se = 0.5 * P.inv_se2;
+  s.one_m_phi2 = P.one_m_phi2;
+  s.hconst = P.hconst;
+  s.e_k = RSV_INV_LN2_N;
+  s.e_hi = RSV_LN2_N_HI;
+  s.e_lo = RSV_LN2_N_LO;
+  s.e_c5 = 0.0;  // unused (degree-3 polynomial)
+  s.e_c4 = 0.0;
+  s.e_c3 = 1.0 / 6.0;
+  s.n_lo = P.n_lo;
+  s.n_span = P.n_span;
+  return s;
+}
+
 
 struct TrajArgs {
   TrajConsts k;
@@ -83,6 +114,9 @@ struct TrajArgs {
   int8_t *ens_cur;      // per chain: which h buffer holds its current path
   EnsPart *ens_parts;   // per tile: [2] partials
   EnsChain *ens;        // per chain bookkeeping
+  // run_chain on the device: theta-dependent constants read from here (written
+  // by the theta kernel); null: all constants from the parameter block
+  const TrajConsts *kdev;
 };
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches);
 // ensemble: per-chain sfc64 momenta (numpy SFC64 + ziggurat, one thread per chain)
@@ -115,5 +149,10 @@ int launch_energy(const double *h, const double *p, const double *y, const doubl
 int launch_suff_stats(const double *h, const double *lrv, int64_t T, double c_mu, double c_xi, double *partials,
                       double *out, cudaStream_t s, int *launches);
 int reduce_partials_count(int64_t T);
+
+// one Gibbs sweep's theta draws on the device (sampler.py:170-272, run_chain
+// :327-344) after a proposal: updates *prm and *kdev, stores the sample
+int launch_theta_sweep(DevControl *ctrl, DevParams *prm, TrajConsts *kdev, DevRun *run, DevPrior prior,
+                       double dt, int64_t T, const uint64_t *sfc_snaps, cudaStream_t s, int *launches);
 
 }  // namespace rsv

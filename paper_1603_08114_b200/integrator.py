@@ -143,6 +143,33 @@ class DeviceChain:
                                           ctypes.byref(r)))
         return r
 
+    def run_chain_device(self, step_size: float, n_steps: int, fuse: bool, prior, n_burnin: int, n_samples: int,
+                         thin: int):
+        """rsv_run_chain: every sweep on the device.  Returns (iters, params
+        [n x 5], accept, delta_h); raises NativeError subclass StormError on
+        a divergence storm (with .sweep)."""
+        pr = N.Prior(*(float(getattr(prior, f)) for f, _ in N.Prior._fields_))
+        iters = np.empty(n_samples, dtype=np.int64)
+        par = np.empty((n_samples, 5))
+        acc = np.empty(n_samples, dtype=np.int32)
+        dh = np.empty(n_samples)
+        storm = ctypes.c_int64(-1)
+        code = self._lib.rsv_run_chain(self.ctx, float(step_size), int(n_steps), int(bool(fuse)), ctypes.byref(pr),
+                                       int(n_burnin), int(n_samples), int(thin), iters.ctypes.data, par.ctypes.data,
+                                       acc.ctypes.data, dh.ctypes.data, ctypes.byref(storm))
+        self._params_key = None  # the device holds the final parameters now
+        try:
+            self._ck(code)
+        except N.StormError as e:
+            e.sweep = int(storm.value)
+            raise
+        return iters, par, acc.astype(bool), dh
+
+    def get_params(self) -> Params:
+        p = N.Params()
+        self._ck(self._lib.rsv_get_params(self.ctx, ctypes.byref(p)))
+        return N.to_params(p)
+
     def hmc_update_many(self, step_size: float, n_steps: int, n: int, fuse: bool = False,
                         results: bool = True):
         out = (N.Result * n)() if results else None

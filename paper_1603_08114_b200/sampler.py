@@ -297,8 +297,16 @@ def default_init(data: Dataset) -> tuple[Params, np.ndarray]:
 
 def run_chain(data: Dataset, config: SamplerConfig, prior: PriorSpec | None = None,
               init_params: Params | None = None, init_h: np.ndarray | None = None, backend=None,
-              rng: np.random.Generator | None = None) -> Chain:
-    """sampler.py:291-358 with the path resident on the GPU for the whole run."""
+              rng: np.random.Generator | None = None, theta_on: str = "device") -> Chain:
+    """sampler.py:291-358 with the path resident on the GPU for the whole run.
+
+    theta_on="device" (default): every sweep -- proposal and the five theta
+    draws -- runs on the GPU with no host round trip (rsv_run_chain); the
+    draws restate numpy's on the same raw-word stream.  theta_on="host": the
+    proposal on the GPU, the theta draws with numpy on the host from the
+    device's statistics (also used when the latent paths are stored)."""
+    if theta_on not in ("device", "host"):
+        raise ValueError(f"theta_on must be 'device' or 'host', got {theta_on!r}")
     prior = prior or PriorSpec()
     params, h = (init_params, init_h)
     if params is None or h is None:
@@ -322,6 +330,21 @@ def run_chain(data: Dataset, config: SamplerConfig, prior: PriorSpec | None = No
 
     ch = _resolve(backend).chain(data, params)
     ch.set_latent(h)
+    if theta_on == "device" and not config.store_latent:
+        ch.set_params(params)
+        ch.set_stream(stream_state(rng))
+        try:
+            it, par, acc, dh = ch.run_chain_device(config.md.step_size, config.md.n_steps, False, prior,
+                                                   config.n_burnin, n_store, config.thin)
+        except N.StormError as e:
+            raise DivergenceStormError(
+                f"more than {_STORM_LIMIT} of the last {_STORM_WINDOW} HMC proposals diverged at sweep {e.sweep}; "
+                f"reduce the step size (current {config.md.step_size})") from None
+        finally:
+            store_stream_state(rng, ch.get_stream())
+        cols = {name: np.ascontiguousarray(par[:, k]) for k, name in
+                enumerate(("phi", "mu", "xi", "sigma_eta_sq", "sigma_u_sq"))}
+        return Chain(iters=it, accept=acc, delta_h=dh, latent=None, **cols)
     recent: deque[bool] = deque(maxlen=_STORM_WINDOW)
     log_every = max(1, n_sweeps // 10)
     stored = 0

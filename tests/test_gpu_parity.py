@@ -157,16 +157,38 @@ def test_hmc_divergent_sentinel(backend):
 
 # ---------------------------------------------------------------- chains
 @pytest.mark.parametrize("kind,seed", [("pcg32", 3), ("philox", 5)])
-def test_run_chain_vs_reference(backend, kind, seed):
+@pytest.mark.parametrize("theta_on", ["host", "device"])
+def test_run_chain_vs_reference(backend, kind, seed, theta_on):
+    # the reference's own chain (tests/golden/make_golden.py); with theta_on
+    # "device" every sweep, theta draws included, runs on the GPU
     g = golden(f"chain_{kind}.npz")
     data = P.Dataset.from_log_rv(g["y"], g["lrv"])
+    store = theta_on == "host"
     cfg = P.SamplerConfig(seed=seed, md=P.MDConfig(0.05, 10), n_burnin=0, n_samples=len(g["accept"]), thin=1,
-                          store_latent=True, prng=kind)
-    ch = P.run_chain(data, cfg, backend=backend)
+                          store_latent=store, prng=kind)
+    ch = P.run_chain(data, cfg, backend=backend, theta_on=theta_on)
     assert np.array_equal(ch.accept, g["accept"])
     for name in ("phi", "mu", "xi", "sigma_eta_sq", "sigma_u_sq"):
         assert np.allclose(getattr(ch, name), g[name], rtol=1e-9, atol=1e-12), name
-    assert _rel(ch.latent[-1], g["latent_last"]) <= 1e-9
+    if store:
+        assert _rel(ch.latent[-1], g["latent_last"]) <= 1e-9
+    else:
+        assert _rel(backend.chain(data, THETA).get_latent(), g["latent_last"]) <= 1e-9
+
+
+@pytest.mark.parametrize("kind", ["minstd", "sfc64"])
+def test_run_chain_device_theta_equals_host_theta(backend, kind):
+    z = golden("model_T2000.npz")
+    data = P.Dataset.from_log_rv(z["y"], z["lrv"])
+    cfg = P.SamplerConfig(seed=4, md=P.MDConfig(0.02, 20), n_burnin=10, n_samples=40, thin=2, prng=kind)
+    a = P.run_chain(data, cfg, backend=backend, theta_on="host")
+    b = P.run_chain(data, cfg, backend=backend, theta_on="device")
+    assert np.array_equal(a.iters, b.iters) and np.array_equal(a.accept, b.accept)
+    for name in ("phi", "mu", "xi", "sigma_eta_sq", "sigma_u_sq"):
+        assert np.allclose(getattr(a, name), getattr(b, name), rtol=1e-11, atol=1e-13), name
+    fin = np.isfinite(a.delta_h)
+    assert np.array_equal(fin, np.isfinite(b.delta_h))
+    assert np.allclose(a.delta_h[fin], b.delta_h[fin], rtol=1e-8, atol=1e-9)
 
 
 # ---------------------------------------------------------------- large-T properties
