@@ -112,6 +112,28 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def chain_run(P, be, theta):
+    """Config 1 as a full sampler: run_chain (sampler.py:291-358) on T=2000,
+    L=20, dt=0.02, minstd, every sweep (proposal + the five theta draws) on
+    the device; sweeps/s by wall clock around run_chain (host arrays in and
+    out, samples copied back at the end)."""
+    tr = P.simulate_rsv(theta, 2000, seed=0)
+    out = {}
+    for T, tr_ in ((2000, tr), (1 << 20, P.simulate_rsv(theta, 1 << 20, seed=0))):
+        cfg = P.SamplerConfig(seed=1, md=P.MDConfig(0.02, 20), n_burnin=0, n_samples=50, prng="minstd")
+        P.run_chain(tr_.dataset, cfg, backend=be, init_params=theta, init_h=tr_.latent)
+        n = 2000 if T == 2000 else 300
+        cfg = P.SamplerConfig(seed=1, md=P.MDConfig(0.02, 20), n_burnin=0, n_samples=n, prng="minstd")
+        t0 = time.perf_counter()
+        ch = P.run_chain(tr_.dataset, cfg, backend=be, init_params=theta, init_h=tr_.latent)
+        el = time.perf_counter() - t0
+        out[f"T={T}"] = {"sweeps_per_s": n / el, "us_per_sweep": el / n * 1e6, "sweeps": n,
+                         "accept_rate": float(ch.accept.mean()), "theta_on": "device"}
+        be._chains.pop(T, None)
+    out["workload"] = "run_chain, L=20, dt=0.02, minstd, theta draws on the device, init at the true path/params"
+    return out
+
+
 def paper_protocol(no_cpu):
     """Config 2 as the paper measures it (reference bench.py:121-267): the
     elementary step at T = 512*B, B = 2..512, 10^4 reps in segments of 100,
@@ -387,6 +409,7 @@ def main():
             extra["ensemble"] = ensemble_run(P, theta, dt, L, args.ens_chains, args.ens_T, args.steps)
         if not args.no_protocol:
             extra["paper_protocol"] = paper_protocol(args.no_cpu)
+        extra["chain_config1"] = chain_run(P, be, theta)
         if not args.no_cpu:
             extra["cpu_baseline"] = cpu_baseline(T, L, dt, args.prng, args.cpu_seconds, data, truth.latent)
 
