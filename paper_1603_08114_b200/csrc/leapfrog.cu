@@ -582,6 +582,11 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     // the exp table (16 KB) arrives by one bulk copy alongside the first tile
     mbar_expect_tx(&S.bar[2], (uint32_t)sizeof(S.tab));
     tma_load_1d(S.tab, g_exp_tab2, (uint32_t)sizeof(S.tab), &S.bar[2]);
+  }
+  // programmatic dependent launch: everything above overlapped the momenta
+  // kernel's tail; its normals (and stream bookkeeping) are read from here on
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tid == 0) {
     if (tile < n_tiles) {
       if (ENS) stage_tile_ens<W>(A, tile, S.stage[0], &S.bar[0]);
       else stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0]);
@@ -896,7 +901,21 @@ static void launch_p2(const TrajArgs &a, cudaStream_t s) {
   // reconfiguration of the SMs between the two kernels of a proposal
   cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK><<<a.g.grid, NT, smem, s>>>(a);
+  if (a.pdl) {  // overlap this launch with the tail of the momenta kernel
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.g.grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK>, a);
+  } else {
+    traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK><<<a.g.grid, NT, smem, s>>>(a);
+  }
 }
 
 // run_chain on the device: the statistics variant with device-resident

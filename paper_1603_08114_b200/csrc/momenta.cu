@@ -122,6 +122,9 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
 #define ZSTAMP(k) \
   do { if (dbg && threadIdx.x == 0) dbg[(size_t)blockIdx.x * 8 + (k)] = zgt(); } while (0)
   ZSTAMP(0);
+  // the trajectory kernel may launch as soon as every CTA of this grid runs
+  // (it waits for this grid's completion before reading the normals)
+  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ __align__(16) unsigned char zsmem[];
   ZigShared &S = *reinterpret_cast<ZigShared *>(zsmem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

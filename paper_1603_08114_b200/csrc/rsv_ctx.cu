@@ -532,6 +532,8 @@ static int ensure_events(rsv_ctx *c, size_t n) {
 // Capture one proposal into a graph.  With timing, 4 event-record nodes
 // (start, trajectory begin, trajectory end, end) are added; their events are
 // re-pointed per launch with cudaGraphExecEventRecordNodeSetEvent.
+static bool variant_is_persistent(int v) { return v >= 9; }
+
 static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   const TrajGeom g = traj_geometry(c->T, k.n_steps, c->sm_count, c->variant);
   if (!g.ok) return fail(c, RSV_E_INVALID, "n_steps=%d too large for one trajectory tile", k.n_steps);
@@ -542,6 +544,9 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   cg->dt = k.dt;
   cg->args = traj_args(c, k.dt, k.n_steps, k.fuse, g);
   cg->args.stats = k.stats;
+  // programmatic dependent launch of the trajectory after the momenta kernel
+  // (not with timing event nodes between them)
+  cg->args.pdl = (k.timing == 0 && variant_is_persistent(g.variant)) ? 1 : 0;
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   int l = 0;

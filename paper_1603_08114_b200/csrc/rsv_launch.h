@@ -117,6 +117,7 @@ struct TrajArgs {
   // run_chain on the device: theta-dependent constants read from here (written
   // by the theta kernel); null: all constants from the parameter block
   const TrajConsts *kdev;
+  int pdl;  // launched as a programmatic dependent of the momenta kernel
 };
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches);
 // ensemble: per-chain sfc64 momenta (numpy SFC64 + ziggurat, one thread per chain)
