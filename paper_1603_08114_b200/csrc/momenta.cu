@@ -129,7 +129,9 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   ZigShared &S = *reinterpret_cast<ZigShared *>(zsmem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    S.blk = (int)atomicAdd(&ctrl->zig_ticket, 1u);
+    // a co-resident grid needs no scheduling-order ticket (every CTA runs at
+    // once); otherwise the ticket keeps the look-back deadlock-free
+    S.blk = coresident ? (int)blockIdx.x : (int)atomicAdd(&ctrl->zig_ticket, 1u);
     S.epoch = ctrl->zig_epoch & 0xffffffu;
     S.bad = 0;
     S.nq = 0;
