@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-ensemble", action="store_true")
     ap.add_argument("--no-protocol", action="store_true")
+    ap.add_argument("--no-config5", action="store_true")
+    ap.add_argument("--c5-T", type=int, default=1 << 26)
     ap.add_argument("--ens-chains", type=int, default=4096)
     ap.add_argument("--ens-T", type=int, default=4096)
     ap.add_argument("--sharded", action="store_true",
@@ -110,6 +112,32 @@ class ClockSampler:
                           if s[2 + i].strip().lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
+
+
+def config5_run(P, theta, T, block=4096, sweeps=20, dt=0.005):
+    """Config 5 on one GPU: T = 2^26 sites, full theta update every sweep
+    (run_chain with the theta draws on the device), sfc64 in the blocked
+    layout (sites [j*4096, (j+1)*4096) from SFC64(SeedSequence([1, j])),
+    the chain's own SFC64 stream for the uniforms and theta draws).  dt is
+    0.005 here: at T = 2^26 the reference default 0.02 accepts nothing (the
+    energy error grows with T).  The timed region is rsv_run_chain on the
+    device-resident chain (the path was uploaded by the warm-up run);
+    HBM-resident (T >> L2)."""
+    tr = P.simulate_rsv(theta, T, seed=11)
+    be = P.CudaBackend(0)
+    ch = be.chain(tr.dataset, theta)
+    ch.set_blocked_streams(1, block)
+    cfg = P.SamplerConfig(seed=1, md=P.MDConfig(dt, 20), n_burnin=0, n_samples=3, prng="sfc64")
+    P.run_chain(tr.dataset, cfg, backend=be, init_params=theta, init_h=tr.latent)
+    t0 = time.perf_counter()
+    it, par, acc, dh = ch.run_chain_device(dt, 20, False, P.PriorSpec(), 0, sweeps, 1)
+    el = time.perf_counter() - t0
+    be.close()
+    return {"workload": f"config 5 on 1 GPU: T={T}, L=20, dt={dt}, full theta update per sweep (device), sfc64 "
+                        f"blocked momenta ({block}-site blocks, SeedSequence([1, j])), sfc64 main stream",
+            "sweeps": sweeps, "sweeps_per_s": sweeps / el, "ms_per_sweep": el / sweeps * 1e3,
+            "site_updates_per_s": T * 20 * sweeps / el, "accept_rate": float(acc.mean()),
+            "timing": "wall clock around rsv_run_chain (device-resident chain; includes the samples' D2H)"}
 
 
 def chain_run(P, be, theta):
@@ -410,6 +438,8 @@ def main():
         if not args.no_protocol:
             extra["paper_protocol"] = paper_protocol(args.no_cpu)
         extra["chain_config1"] = chain_run(P, be, theta)
+        if not args.no_config5:
+            extra["config5"] = config5_run(P, theta, args.c5_T)
         if not args.no_cpu:
             extra["cpu_baseline"] = cpu_baseline(T, L, dt, args.prng, args.cpu_seconds, data, truth.latent)
 

@@ -154,6 +154,17 @@ int rsv_last_stats(rsv_ctx *ctx, double out[7]);
  * over the last rsv_hmc_update_many call.  Level 0 disables timing. */
 int rsv_set_timing(rsv_ctx *ctx, int level);
 int rsv_get_timing(rsv_ctx *ctx, double *traj_ms, double *momenta_ms, double *total_ms);
+/* Blocked momenta layout (BASELINE config 5; NOT the reference's single-stream
+ * layout): SFC64 has no jump-ahead, so for very long series the
+ * momenta of sites [j*block_len, (j+1)*block_len) come from their own numpy
+ * SFC64 stream j (states: n_blocks x 4 words, the benchmark seeds stream j
+ * with SeedSequence([seed, j])), continued from proposal to proposal; the
+ * context's own stream then supplies only the Metropolis uniforms (and the
+ * theta draws).  n_blocks * block_len must equal T.  states = NULL restores
+ * the single-stream layout. */
+int rsv_set_blocked_streams(rsv_ctx *ctx, int64_t block_len, int64_t n_blocks, const uint64_t *states);
+int rsv_get_blocked_streams(rsv_ctx *ctx, uint64_t *states);
+
 /* sampler.py:291-358 run_chain with the whole sweep on the device: starting
  * from the context's params, latent path and stream, n_burnin + n_samples *
  * thin sweeps of [hmc_update_volatility, update_mu, update_phi,

@@ -103,6 +103,8 @@ _SIGS = {
                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "rsv_get_params": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
+    "rsv_set_blocked_streams": (ctypes.c_int, [_CTX, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]),
+    "rsv_get_blocked_streams": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
     "rsv_ens_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
     "rsv_ens_set_streams": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
     "rsv_ens_get_streams": (ctypes.c_int, [_CTX, ctypes.c_void_p]),

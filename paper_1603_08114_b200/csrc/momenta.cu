@@ -630,7 +630,7 @@ struct ZEnsShared {
 };
 
 __global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *normals, int64_t Tc, int C,
-                                                         unsigned long long *dbg) {
+                                                         unsigned long long *dbg, int advance) {
   extern __shared__ __align__(16) unsigned char zesmem[];
   ZEnsShared &S = *reinterpret_cast<ZEnsShared *>(zesmem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -764,6 +764,8 @@ __global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *nor
             ec.used = (uint64_t)used;
             ec.u_word = sfc64_next(st);
             for (int k = 0; k < 4; k++) ec.st_used1[k] = st[k];
+            if (advance)  // blocked momenta streams: no uniform is ever drawn from them
+              for (int k = 0; k < 4; k++) ec.st[k] = ec.st_used[k];
             ec.overflow = ovf ? 1 : 0;
             S.done[j] = 1;
             atomicAdd(&S.ndone, 1);
@@ -793,10 +795,10 @@ __global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *nor
 }
 
 int launch_momenta_ens(EnsChain *ens, double *normals, int64_t Tc, int n_chains, cudaStream_t s, int *launches,
-                       unsigned long long *dbg) {
+                       unsigned long long *dbg, int advance) {
   const size_t smem = sizeof(ZEnsShared);
   cudaFuncSetAttribute(zig_ens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  zig_ens_kernel<<<(n_chains + ZE_G - 1) / ZE_G, ZE_NT, smem, s>>>(ens, normals, Tc, n_chains, dbg);
+  zig_ens_kernel<<<(n_chains + ZE_G - 1) / ZE_G, ZE_NT, smem, s>>>(ens, normals, Tc, n_chains, dbg, advance);
   (*launches)++;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
@@ -1103,7 +1105,31 @@ static void launch_zig(const MomentaBufs &b, const uint64_t *words, int64_t nbuf
   zig_kernel<KIND><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, coresident, b.dbg);
 }
 
+// Blocked layout (config 5): the momenta come from one SFC64 stream per block
+// of sites; the main stream only supplies the Metropolis uniform (and the
+// theta draws), so the proposal "uses" no main-stream words for momenta.
+__global__ void main_uniform_kernel(DevControl *ctrl, uint64_t *snaps, int64_t T) {
+  if (threadIdx.x || blockIdx.x) return;
+  const StreamState st = ctrl->stream;
+  ctrl->zig_used = 0;
+  ctrl->zig_avail = (uint64_t)T;
+  if (st.kind == PRNG_SFC64) {
+    uint64_t q[4] = {st.s[0], st.s[1], st.s[2], st.s[3]};
+    for (int k = 0; k < 4; k++) snaps[k] = q[k];  // state at the stream position (Metropolis rewinds from here)
+    ctrl->u_word = sfc64_next(q);
+  } else {
+    ctrl->u_word = word_at(st, st.pos);
+    ctrl->seq_next = ctrl->seq_state;
+  }
+}
+
 int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, int *launches) {
+  if (b.blocks) {
+    if (launch_momenta_ens(b.blocks, b.normals, b.block_len, b.n_blocks, s, launches, nullptr, 1)) return -1;
+    main_uniform_kernel<<<1, 32, 0, s>>>(b.ctrl, b.sfc_snaps, T);
+    (*launches)++;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   const int64_t N = momenta_words(T);
   const int nb = (int)(N / ZB);
   uint64_t *status = (uint64_t *)b.scratch;

@@ -143,6 +143,10 @@ struct rsv_ctx {
   EnsPart *ens_parts = nullptr;
   EnsChain *ens = nullptr, *h_ens = nullptr;
   std::map<GraphKey, Cached *> ens_graphs;
+  // blocked momenta streams (config 5): one SFC64 stream per block
+  EnsChain *blocks = nullptr, *h_blocks = nullptr;
+  int64_t block_len = 0;
+  int n_blocks = 0;
   // run_chain on the device
   TrajConsts *kdev = nullptr;
   DevRun *run = nullptr;
@@ -192,6 +196,8 @@ int rsv_destroy(rsv_ctx *c) {
       delete kv.second;
     }
   }
+  if (c->blocks) cudaFree(c->blocks);
+  if (c->h_blocks) cudaFreeHost(c->h_blocks);
   if (c->kdev) cudaFree(c->kdev);
   if (c->run) cudaFree(c->run);
   if (c->run_store) cudaFree(c->run_store);
@@ -462,7 +468,19 @@ static MomentaBufs mbufs(rsv_ctx *c) {
   b.normals = c->normals;
   b.bjump = c->bjump;
   b.dbg = getenv("RSV_ZIG_STAMPS") ? c->dbg : nullptr;
+  b.blocks = c->blocks;
+  b.block_len = c->block_len;
+  b.n_blocks = c->n_blocks;
   return b;
+}
+
+static void drop_graphs(rsv_ctx *c) {  // the momenta layout changed: recapture
+  for (auto &kv : c->graphs) {
+    cudaGraphExecDestroy(kv.second->exec);
+    cudaGraphDestroy(kv.second->graph);
+    delete kv.second;
+  }
+  c->graphs.clear();
 }
 
 static int check_err_bits(rsv_ctx *c) {
@@ -1137,6 +1155,53 @@ int rsv_latent_slice(rsv_ctx *c, int64_t offset, int64_t n, double *buf, int to_
                        c->stream));
   }
   return sync(c);
+}
+
+// ---- blocked momenta streams (config 5) -----------------------------------
+int rsv_set_blocked_streams(rsv_ctx *c, int64_t block_len, int64_t n_blocks, const uint64_t *states) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  if (c->shard || c->ens_C) return fail(c, RSV_E_STATE, "blocked momenta need a single-chain context");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  if (!states || n_blocks == 0) {  // back to the single-stream layout
+    if (c->blocks) cudaFree(c->blocks);
+    if (c->h_blocks) cudaFreeHost(c->h_blocks);
+    c->blocks = c->h_blocks = nullptr;
+    c->block_len = 0;
+    c->n_blocks = 0;
+    drop_graphs(c);
+    return 0;
+  }
+  if (block_len < 64 || block_len % 8 || block_len * n_blocks != c->T || n_blocks > (1 << 24))
+    return fail(c, RSV_E_INVALID, "blocks must tile the series: %lld x %lld != %lld (block length a multiple of 8, >= 64)",
+                (long long)n_blocks, (long long)block_len, (long long)c->T);
+  if (n_blocks != c->n_blocks) {
+    if (c->blocks) cudaFree(c->blocks);
+    if (c->h_blocks) cudaFreeHost(c->h_blocks);
+    c->blocks = c->h_blocks = nullptr;
+    CK(cudaMalloc(&c->blocks, sizeof(EnsChain) * (size_t)n_blocks));
+    CK(cudaMallocHost(&c->h_blocks, sizeof(EnsChain) * (size_t)n_blocks));
+  }
+  memset(c->h_blocks, 0, sizeof(EnsChain) * (size_t)n_blocks);
+  for (int64_t i = 0; i < n_blocks; i++)
+    for (int k = 0; k < 4; k++) c->h_blocks[i].st[k] = states[4 * i + k];
+  CK(cudaMemcpy(c->blocks, c->h_blocks, sizeof(EnsChain) * (size_t)n_blocks, cudaMemcpyHostToDevice));
+  const bool changed = c->block_len != block_len || c->n_blocks != (int)n_blocks;
+  c->block_len = block_len;
+  c->n_blocks = (int)n_blocks;
+  if (changed) drop_graphs(c);
+  return 0;
+}
+
+int rsv_get_blocked_streams(rsv_ctx *c, uint64_t *states) {
+  if (!c || !states) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->blocks) return fail(c, RSV_E_STATE, "no blocked streams set");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(c->h_blocks, c->blocks, sizeof(EnsChain) * (size_t)c->n_blocks, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < c->n_blocks; i++)
+    for (int k = 0; k < 4; k++) states[4 * (size_t)i + k] = c->h_blocks[i].st[k];
+  return 0;
 }
 
 // ---- run_chain on the device ---------------------------------------------

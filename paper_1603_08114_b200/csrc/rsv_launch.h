@@ -16,6 +16,10 @@ struct MomentaBufs {
   double *normals;      // T doubles
   const uint64_t *bjump;  // momenta_jump_bytes(T): per-CTA jump-ahead constants
   unsigned long long *dbg;  // optional per-CTA %globaltimer stamps (development aid)
+  // blocked layout (config 5): one SFC64 stream per block of block_len sites
+  EnsChain *blocks = nullptr;
+  int64_t block_len = 0;
+  int n_blocks = 0;
 };
 
 int64_t momenta_words(int64_t T);
@@ -122,7 +126,7 @@ struct TrajArgs {
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches);
 // ensemble: per-chain sfc64 momenta (numpy SFC64 + ziggurat, one thread per chain)
 int launch_momenta_ens(EnsChain *ens, double *normals, int64_t Tc, int n_chains, cudaStream_t s, int *launches,
-                       unsigned long long *dbg = nullptr);
+                       unsigned long long *dbg = nullptr, int advance = 0);
 const void *traj_kernel_fn(int variant, int fuse, int stats);  // for locating the node in a captured graph
 
 

@@ -165,6 +165,25 @@ class DeviceChain:
             raise
         return iters, par, acc.astype(bool), dh
 
+    def set_blocked_streams(self, seed: int | None, block_len: int = 4096):
+        """Config-5 momenta layout: sites [j*B, (j+1)*B) draw from
+        SFC64(SeedSequence([seed, j])); seed=None restores one stream."""
+        if seed is None:
+            self._ck(self._lib.rsv_set_blocked_streams(self.ctx, 0, 0, None))
+            return
+        if self.T % block_len:
+            raise ValueError(f"block length {block_len} does not divide T={self.T}")
+        from .ensemble import sfc64_states
+        st = sfc64_states(seed, self.T // block_len)
+        self._ck(self._lib.rsv_set_blocked_streams(self.ctx, int(block_len), self.T // block_len, st.ctypes.data))
+        self._block_len = block_len
+
+    def blocked_streams(self) -> np.ndarray:
+        n = self.T // max(1, getattr(self, "_block_len", 1))
+        out = np.empty((n, 4), dtype=np.uint64)
+        self._ck(self._lib.rsv_get_blocked_streams(self.ctx, out.ctypes.data))
+        return out
+
     def get_params(self) -> Params:
         p = N.Params()
         self._ck(self._lib.rsv_get_params(self.ctx, ctypes.byref(p)))
