@@ -816,6 +816,8 @@ struct ThetaGen {
   SeqGen g;
   uint64_t s[4];
   uint64_t used;
+  const uint64_t *ki;  // ziggurat tables (shared-memory copies)
+  const double *wi, *fi;
   __device__ uint64_t next() {
     used++;
     return kind == PRNG_SFC64 ? sfc64_next(s) : g.next();
@@ -828,9 +830,9 @@ struct ThetaGen {
       r >>= 8;
       const int sign = (int)(r & 0x1);
       const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-      double x = __dmul_rn((double)rabs, g_wi[idx]);
+      double x = __dmul_rn((double)rabs, wi[idx]);
       if (sign) x = -x;
-      if (rabs < g_ki[idx]) return x;
+      if (rabs < ki[idx]) return x;
       if (idx == 0) {
         for (;;) {
           const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, glibc_log1p(-next_double()));
@@ -840,7 +842,7 @@ struct ThetaGen {
         }
       }
       const double u = next_double();
-      if (__dadd_rn(__dmul_rn(__dsub_rn(g_fi[idx - 1], g_fi[idx]), u), g_fi[idx]) <
+      if (__dadd_rn(__dmul_rn(__dsub_rn(fi[idx - 1], fi[idx]), u), fi[idx]) <
           exp(__dmul_rn(__dmul_rn(-0.5, x), x)))
         return x;
     }
@@ -892,8 +894,20 @@ __device__ double phi_log_ratio(double prop, double phi, double h1_sq, double se
   return __dadd_rn(__dadd_rn(__dsub_rn(a, b), c), d);
 }
 
-__global__ void theta_sweep_kernel(DevControl *C, DevParams *P, TrajConsts *K, DevRun *R, DevPrior pr, double dt,
-                                   int64_t T, const uint64_t *sfc_snaps) {
+constexpr int TH_NT = 256;
+__global__ void __launch_bounds__(TH_NT) theta_sweep_kernel(DevControl *C, DevParams *P, TrajConsts *K, DevRun *R,
+                                                            DevPrior pr, double dt, int64_t T,
+                                                            const uint64_t *sfc_snaps) {
+  // the draws are one sequential stream (thread 0); the CTA only stages the
+  // ziggurat tables in shared memory so no draw waits on a global load
+  __shared__ uint64_t s_ki[256];
+  __shared__ double s_wi[256], s_fi[256];
+  for (int i = threadIdx.x; i < 256; i += TH_NT) {
+    s_ki[i] = g_ki[i];
+    s_wi[i] = g_wi[i];
+    s_fi[i] = g_fi[i];
+  }
+  __syncthreads();
   if (threadIdx.x || blockIdx.x) return;
   (void)sfc_snaps;
   const DevResult res = C->res;
@@ -911,10 +925,19 @@ __global__ void theta_sweep_kernel(DevControl *C, DevParams *P, TrajConsts *K, D
   ThetaGen G;
   G.kind = C->stream.kind;
   G.used = 0;
-  if (G.kind == PRNG_SFC64)
+  G.ki = s_ki;
+  G.wi = s_wi;
+  G.fi = s_fi;
+  if (G.kind == PRNG_SFC64) {
     for (int k = 0; k < 4; k++) G.s[k] = C->stream.s[k];
-  else
+  } else if (G.kind == PRNG_PHILOX) {
     G.g.init(C->stream, C->stream.pos);
+  } else {  // pcg32 / minstd: the sequential state at the position is kept by the Metropolis step
+    G.g.kind = G.kind;
+    G.g.k = C->stream.pos;
+    G.g.a = C->seq_state;
+    G.g.b = C->stream.s[1];
+  }
   double st[7];
   for (int k = 0; k < 7; k++) st[k] = C->stats[k];
   const double Td = (double)T, Tm1 = Td - 1.0;
@@ -1020,7 +1043,7 @@ __global__ void theta_sweep_kernel(DevControl *C, DevParams *P, TrajConsts *K, D
 
 int launch_theta_sweep(DevControl *ctrl, DevParams *prm, TrajConsts *kdev, DevRun *run, DevPrior prior, double dt,
                        int64_t T, const uint64_t *sfc_snaps, cudaStream_t s, int *launches) {
-  theta_sweep_kernel<<<1, 32, 0, s>>>(ctrl, prm, kdev, run, prior, dt, T, sfc_snaps);
+  theta_sweep_kernel<<<1, TH_NT, 0, s>>>(ctrl, prm, kdev, run, prior, dt, T, sfc_snaps);
   (*launches)++;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

@@ -1262,24 +1262,44 @@ int rsv_run_chain(rsv_ctx *c, double dt, int n_steps, int fuse, const rsv_prior 
   TrajArgs ta = traj_args(c, dt, n_steps, fuse, g);
   ta.stats = 1;
   ta.kdev = c->kdev;
-  cudaGraph_t graph;
-  cudaGraphExec_t exec;
-  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  ta.pdl = 1;
+  // graphs of KS sweeps (fewer graph launches: the gap between two graphs
+  // is ~4 us, between two kernels of one graph ~1 us) and of one sweep
+  constexpr int KS = 8;
+  cudaGraph_t graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};
   int l = 0;
-  bool ok = launch_momenta(mbufs(c), c->kind, c->Tg, c->stream, &l) == 0;
-  ok &= launch_trajectory(ta, c->stream, &l) == 0;
-  ok &= launch_theta_sweep(c->ctrl, c->prm, c->kdev, c->run, pr, dt, c->T, c->sfc_snaps, c->stream, &l) == 0;
-  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
-  if (!ok || e != cudaSuccess) return fail(c, RSV_E_CUDA, "run_chain graph capture failed: %s", cudaGetErrorString(e));
-  CK(cudaGraphInstantiate(&exec, graph, 0));
+  for (int gi = 0; gi < 2; gi++) {
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    bool ok = true;
+    l = 0;
+    for (int k = 0; k < (gi == 0 ? KS : 1); k++) {
+      ok &= launch_momenta(mbufs(c), c->kind, c->Tg, c->stream, &l) == 0;
+      ok &= launch_trajectory(ta, c->stream, &l) == 0;
+      ok &= launch_theta_sweep(c->ctrl, c->prm, c->kdev, c->run, pr, dt, c->T, c->sfc_snaps, c->stream, &l) == 0;
+    }
+    cudaError_t e = cudaStreamEndCapture(c->stream, &graph[gi]);
+    if (!ok || e != cudaSuccess) {
+      for (int q = 0; q < 2; q++) {
+        if (exec[q]) cudaGraphExecDestroy(exec[q]);
+        if (graph[q]) cudaGraphDestroy(graph[q]);
+      }
+      return fail(c, RSV_E_CUDA, "run_chain graph capture failed: %s", cudaGetErrorString(e));
+    }
+    CK(cudaGraphInstantiate(&exec[gi], graph[gi], 0));
+  }
+  const int lps = l;  // kernel launches per sweep
   CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
   const int64_t n_sweeps = n_burnin + n_samples * thin;
   int64_t storm = -1;
   cudaError_t le = cudaSuccess;
-  for (int64_t i = 0; i < n_sweeps && le == cudaSuccess; i++) {
-    le = cudaGraphLaunch(exec, c->stream);
-    c->launches += l;
-    if ((i & 255) == 255 || i + 1 == n_sweeps) {  // early exit on a storm
+  for (int64_t i = 0; i < n_sweeps && le == cudaSuccess;) {
+    const int k = n_sweeps - i >= KS ? KS : 1;
+    le = cudaGraphLaunch(exec[k == KS ? 0 : 1], c->stream);
+    c->launches += (int64_t)lps * k;
+    const int64_t before = i;
+    i += k;
+    if ((before >> 8) != (i >> 8) || i == n_sweeps) {  // every 256 sweeps: early exit on a storm
       if ((le = cudaMemcpyAsync(&hr, c->run, sizeof(DevRun), cudaMemcpyDeviceToHost, c->stream)) == cudaSuccess &&
           (le = cudaStreamSynchronize(c->stream)) == cudaSuccess && hr.storm_sweep >= 0) {
         storm = hr.storm_sweep;
@@ -1287,8 +1307,11 @@ int rsv_run_chain(rsv_ctx *c, double dt, int n_steps, int fuse, const rsv_prior 
       }
     }
   }
-  cudaGraphExecDestroy(exec);
-  cudaGraphDestroy(graph);
+  CK(cudaStreamSynchronize(c->stream));
+  for (int q = 0; q < 2; q++) {
+    cudaGraphExecDestroy(exec[q]);
+    cudaGraphDestroy(graph[q]);
+  }
   if (le != cudaSuccess) return fail(c, RSV_E_CUDA, "run_chain: %s", cudaGetErrorString(le));
   CK(cudaMemcpyAsync(&hr, c->run, sizeof(DevRun), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(c->h_prm, c->prm, sizeof(DevParams), cudaMemcpyDeviceToHost, c->stream));
