@@ -490,18 +490,21 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
 
 // Issue the window [t0 - H, t0 - H + W) of the four arrays into stage[4][W]
 // (clamped to [0, Tpad); arrays are padded to a multiple of 8 doubles).
+// part: 1 = h, (y/2)y, lnRV (+ the whole byte count), 2 = the momenta, 3 = all
 template <int W>
 __device__ __forceinline__ void stage_tile(const TrajArgs &A, const double *hsrc, int tile, double *stage,
-                                           uint64_t *bar) {
+                                           uint64_t *bar, int part = 3) {
   const int64_t g = (int64_t)tile * A.g.core - A.g.halo;
   const int64_t lo = g < 0 ? 0 : g, hi = min(g + W, A.Tpad);
   const uint32_t bytes = (uint32_t)((hi - lo) * 8);
   const int off = (int)(lo - g);
-  mbar_expect_tx(bar, 4 * bytes);
-  tma_load_1d(stage + 0 * W + off, hsrc + lo, bytes, bar);
-  tma_load_1d(stage + 1 * W + off, A.p_in + lo, bytes, bar);
-  tma_load_1d(stage + 2 * W + off, A.a + lo, bytes, bar);
-  tma_load_1d(stage + 3 * W + off, A.lrv + lo, bytes, bar);
+  if (part & 1) {
+    mbar_expect_tx(bar, 4 * bytes);
+    tma_load_1d(stage + 0 * W + off, hsrc + lo, bytes, bar);
+    tma_load_1d(stage + 2 * W + off, A.a + lo, bytes, bar);
+    tma_load_1d(stage + 3 * W + off, A.lrv + lo, bytes, bar);
+  }
+  if (part & 2) tma_load_1d(stage + 1 * W + off, A.p_in + lo, bytes, bar);
 }
 
 // Ensemble: the h window is split at chain boundaries, each piece read from
@@ -582,6 +585,8 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     // the exp table (16 KB) arrives by one bulk copy alongside the first tile
     mbar_expect_tx(&S.bar[2], (uint32_t)sizeof(S.tab));
     tma_load_1d(S.tab, g_exp_tab2, (uint32_t)sizeof(S.tab), &S.bar[2]);
+    // the first tile's h, (y/2)y and lnRV do not depend on the momenta kernel
+    if (!ENS && tile < n_tiles) stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0], 1);
   }
   // programmatic dependent launch: everything above overlapped the momenta
   // kernel's tail; its normals (and stream bookkeeping) are read from here on
@@ -589,7 +594,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   if (tid == 0) {
     if (tile < n_tiles) {
       if (ENS) stage_tile_ens<W>(A, tile, S.stage[0], &S.bar[0]);
-      else stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0]);
+      else stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0], 2);
     }
   }
   __syncthreads();
