@@ -473,38 +473,38 @@ def main():
 
 def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
     """N > 1 (config 3): ONE chain of T sites time-sharded over the N GPUs
-    (strong scaling).  Per proposal: halo exchange of the margins after an
-    accepted move (NCCL send/recv), local momenta + trajectory on each GPU,
-    an all_gather of the shards' totals (NCCL) and the same Metropolis
-    decision on every rank.  Device-timed with CUDA events on the current
-    stream between barrier+synchronize brackets; max over ranks."""
+    (strong scaling), orchestrated on the device: per proposal each GPU
+    draws the (replicated) momenta, runs the trajectory on its sites plus an
+    8(L+1)-site margin, writes its 20 partial totals to device memory; NCCL
+    all-gathers them and every GPU takes the same Metropolis decision on the
+    device; the margins are exchanged (NCCL send/recv) every 7 proposals,
+    which keeps the owned sites exact whatever was accepted in between.  The
+    host only enqueues; timed with CUDA events bracketing the K proposals and
+    the final synchronisation (barrier before and after), max over ranks."""
     T, L, dt = args.T, args.L, args.dt
     dev = f"cuda:{local}"
-    margin = max(64, (L + 1 + 7) // 8 * 8)
+    margin = 8 * (L + 1)
     chain = P.ShardedChain(truth.dataset, theta, rank, ws, margin=margin, device=local)
     chain.set_latent_global(truth.latent)
     chain.set_stream(P.stream_state(P.make_rng(1, args.prng)))
-    for _ in range(max(3, args.warmup)):
-        P.hmc_update_distributed(chain, dt, L, stats=False, device=dev)
+    P.sharded.hmc_update_distributed_device(chain, dt, L, max(3, args.warmup))
     clocks = ClockSampler(local) if rank == 0 else None
     if clocks:
         clocks.start()
     t_load = time.perf_counter()
-    n_load = 0
-    while n_load < 5 or time.perf_counter() - t_load < 0.4:
-        P.hmc_update_distributed(chain, dt, L, stats=False, device=dev)
-        n_load += 1
+    while time.perf_counter() - t_load < 0.4:
+        P.sharded.hmc_update_distributed_device(chain, dt, L, 20)
     dist.barrier()
     torch.cuda.synchronize(local)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = chain.shard.launch_count()
-    e0.record()
-    acc = 0
-    for _ in range(args.steps):
-        d = P.hmc_update_distributed(chain, dt, L, stats=False, device=dev)
-        acc += int(d.accept)
-    e1.record()
+    s = torch.cuda.Stream(torch.device(dev))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    s.synchronize()
+    res = P.sharded.hmc_update_distributed_device(chain, dt, L, args.steps)
     torch.cuda.synchronize(local)
+    e1.record(s)
+    e1.synchronize()
     launches = chain.shard.launch_count() - n0
     dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
@@ -514,18 +514,21 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
     clk = clocks.stop() if clocks else None
     if rank == 0:
         v = T * L / (ms * 1e-3)
+        acc = sum(bool(x.accept) for x in res) / max(1, len(res))
         line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (simulate_rsv, theta of SURVEY §8d, seed 0)",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (simulate_rsv, theta of SURVEY \u00a78d, seed 0)",
                 "config": {"workload": f"config 3: one chain T={T}, L={L}, dt={dt}, {args.prng}, time-sharded over "
                                        f"{ws} GPUs; one step = one full HMC proposal",
                            "T": T, "L": L, "dt": dt, "prng": args.prng,
-                           "parallelism": f"time-sharded x{ws} (margin {margin} sites, NCCL halo send/recv + "
-                                          "all_gather of shard totals)",
+                           "parallelism": f"time-sharded x{ws} (margin {margin} sites, halo every "
+                                          f"{P.sharded.halo_period(margin, L)} proposals, NCCL all_gather of shard "
+                                          "totals, decision on the device)",
                            "l2": "per-GPU working set below L2, not flushed (multi-GPU path)"},
-                "trajectories_per_s": 1e3 / ms, "accept_rate": acc / args.steps, "clocks": clk,
-                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 8 * 14 * ws, "d2h_bytes_per_step": 8 * 14 * ws,
-                        "path": "ShardedChain + hmc_update_distributed: shard totals to host, decision on host"},
+                "trajectories_per_s": 1e3 / ms, "accept_rate": acc, "clocks": clk,
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                        "path": "ShardedChain + sharded.hmc_update_distributed_device (device-resident; results read "
+                                "once at the end)"},
                 "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
 

@@ -154,6 +154,24 @@ int rsv_last_stats(rsv_ctx *ctx, double out[7]);
  * over the last rsv_hmc_update_many call.  Level 0 disables timing. */
 int rsv_set_timing(rsv_ctx *ctx, int level);
 int rsv_get_timing(rsv_ctx *ctx, double *traj_ms, double *momenta_ms, double *total_ms);
+/* Device-side orchestration of a sharded chain (no host synchronisation per
+ * proposal; the host only enqueues): rsv_set_stream puts the context on an
+ * external CUDA stream (e.g. the one NCCL collectives are ordered on; NULL
+ * restores its own).  rsv_shard_propose_async writes this shard's 20 totals
+ * (rsv_shard_totals layout, u_word / words_used as bit patterns) to device
+ * memory; after an all-gather of every rank's totals, rsv_shard_decide_async
+ * takes the Metropolis decision on the device (fixed-order compensated sums:
+ * the same decision on every rank) and advances the stream / flips the path;
+ * rsv_shard_halo_async packs the owned boundary sites of the current path
+ * (unpack = 0: left gets [own_lo, own_lo + nl), right [own_hi - nr, own_hi))
+ * or writes received margins (unpack = 1); rsv_shard_results returns the
+ * decisions recorded since the last call. */
+int rsv_set_stream(rsv_ctx *ctx, void *cuda_stream);
+int rsv_shard_propose_async(rsv_ctx *ctx, double step_size, int n_steps, int fuse, int stats, double *totals_dev);
+int rsv_shard_decide_async(rsv_ctx *ctx, const double *gathered_dev, int world, double h_const);
+int rsv_shard_halo_async(rsv_ctx *ctx, double *left, int64_t n_left, double *right, int64_t n_right, int unpack);
+int rsv_shard_results(rsv_ctx *ctx, rsv_result *out, int max_n, int *n_out);
+
 /* Blocked momenta layout (BASELINE config 5; NOT the reference's single-stream
  * layout): SFC64 has no jump-ahead, so for very long series the
  * momenta of sites [j*block_len, (j+1)*block_len) come from their own numpy

@@ -104,6 +104,13 @@ _SIGS = {
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "rsv_get_params": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
     "rsv_set_blocked_streams": (ctypes.c_int, [_CTX, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]),
+    "rsv_set_stream": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
+    "rsv_shard_propose_async": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_void_p]),
+    "rsv_shard_decide_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int, ctypes.c_double]),
+    "rsv_shard_halo_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                            ctypes.c_int]),
+    "rsv_shard_results": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     "rsv_get_blocked_streams": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
     "rsv_ens_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
     "rsv_ens_set_streams": (ctypes.c_int, [_CTX, ctypes.c_void_p]),

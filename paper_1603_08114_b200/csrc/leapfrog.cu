@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     parity[buf] ^= 1;
     c1 = clock64(); cyc_wait += c1 - c0; c0 = c1;
     double d[R], p[R], Ad[R], Cd[R], av[R], lv[R];
-    uint32_t live = 0, core = 0, endm = 0;
+    uint32_t live = 0, core = 0, wcore = 0, endm = 0;
     unsigned cm[R];
 #pragma unroll
     for (int r = 0; r < R; r += 2) {
@@ -657,9 +657,13 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     for (int r = 0; r < R; r++) {
       const int64_t gi = g0 + r;
       const bool in = gi >= lo_live && gi < hi_live;
-      const bool c = in && own_lane && gi >= t0 && gi < t1 && gi >= A.own_lo && gi < A.own_hi;
+      // wcore: tile-core sites of the local range (written back; a shard keeps
+      // its margins evolving too); core: those this context owns (the sums)
+      const bool wc = in && own_lane && gi >= t0 && gi < t1;
+      const bool c = wc && gi >= A.own_lo && gi < A.own_hi;
       live |= (uint32_t)in << r;
       core |= (uint32_t)c << r;
+      wcore |= (uint32_t)wc << r;
       if (ENS) {
         endm |= (uint32_t)((cf && r == 0) || (cl && r == R - 1)) << r;
         firstm |= (uint32_t)(cf && r == 0) << r;
@@ -742,16 +746,16 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     }
     double *hd = hdst;
     if (ENS && core) hd = A.ens_cur[chain] ? A.hbuf0 : A.hbuf1;
-    if (core == (1u << R) - 1) {
+    if (wcore == (1u << R) - 1) {
 #pragma unroll
       for (int r = 0; r < R; r += 2) {
         *reinterpret_cast<double2 *>(hd + g0 + r) = make_double2(d[r] + s.mu, d[r + 1] + s.mu);
         if (A.p_out) *reinterpret_cast<double2 *>(A.p_out + g0 + r) = make_double2(p[r], p[r + 1]);
       }
-    } else if (core) {
+    } else if (wcore) {
 #pragma unroll
       for (int r = 0; r < R; r++) {
-        if ((core >> r) & 1) {
+        if ((wcore >> r) & 1) {
           hd[g0 + r] = d[r] + s.mu;
           if (A.p_out) A.p_out[g0 + r] = p[r];
         }

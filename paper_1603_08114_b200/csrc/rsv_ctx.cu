@@ -85,6 +85,7 @@ struct rsv_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   int64_t launches = 0;
+  cudaStream_t own_stream = nullptr;  // set when an external stream is in use (rsv_set_stream)
   bool has_data = false, has_params = false, has_latent = false;
   int kind = PRNG_PHILOX;
   // time sharding: this context holds global sites [goff, goff + T) of a
@@ -216,6 +217,7 @@ int rsv_destroy(rsv_ctx *c) {
   void *host[] = {c->h_ctrl, c->h_prm, c->h_out, c->h_flag, c->h_ring};
   for (void *p : host)
     if (p) cudaFreeHost(p);
+  if (c->own_stream) c->stream = c->own_stream;
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return 0;
@@ -265,6 +267,7 @@ static int create_impl(rsv_ctx *c, int device, int64_t T, int64_t Tg) {
   CK(cudaMalloc(&c->rout, sizeof(double) * 8));
   CK(cudaMalloc(&c->dflag, sizeof(int32_t)));
   CK(cudaMalloc(&c->ring_count, sizeof(int32_t)));
+  CK(cudaMemset(c->ring_count, 0, sizeof(int32_t)));
   CK(cudaMalloc(&c->ctrl, sizeof(DevControl)));
   CK(cudaMalloc(&c->prm, sizeof(DevParams)));
   CK(cudaMallocHost(&c->h_ctrl, sizeof(DevControl)));
@@ -1052,10 +1055,16 @@ int rsv_debug_stamps(rsv_ctx *c, unsigned long long *out, int max_tiles) {
 }
 
 // ---- time sharding (one chain split over several contexts / GPUs) ----------
-__global__ void shard_apply_kernel(DevControl *C, int accept, int drew) {
-  if (threadIdx.x || blockIdx.x) return;
+// Advance the context's stream past a proposal (momenta + the uniform if
+// drawn), as the single-chain Metropolis step does.
+__device__ void shard_advance(DevControl *C, int drew, const uint64_t *snaps) {
   const uint64_t consumed = C->zig_used + (drew ? 1 : 0);
-  if (C->stream.kind == PRNG_PCG32) {
+  if (C->stream.kind == PRNG_SFC64) {
+    const uint64_t *q = snaps + 4 * (consumed / SFC_SNAP);
+    uint64_t st[4] = {q[0], q[1], q[2], q[3]};
+    for (uint64_t i = 0; i < consumed % SFC_SNAP; i++) sfc64_next(st);
+    for (int i = 0; i < 4; i++) C->stream.s[i] = st[i];
+  } else if (C->stream.kind == PRNG_PCG32) {
     uint64_t q = C->seq_next;
     if (drew) { q = q * PCG_MULT + C->stream.s[1]; q = q * PCG_MULT + C->stream.s[1]; }
     C->seq_state = q;
@@ -1065,7 +1074,93 @@ __global__ void shard_apply_kernel(DevControl *C, int accept, int drew) {
     C->seq_state = q;
   }
   C->stream.pos += consumed;
+}
+
+__global__ void shard_apply_kernel(DevControl *C, int accept, int drew, const uint64_t *snaps) {
+  if (threadIdx.x || blockIdx.x) return;
+  shard_advance(C, drew, snaps);
   if (accept) C->cur ^= 1;
+}
+
+// ---- device-side orchestration of a sharded chain (no host sync per proposal)
+// pack: this shard's totals into 20 doubles (rsv_shard_totals layout)
+__global__ void shard_pack_kernel(const DevControl *C, int own_first, int own_last, double *out) {
+  if (threadIdx.x || blockIdx.x) return;
+  for (int k = 0; k < TR_NV; k++) out[k] = C->shard_parts[k];
+  out[14] = own_first ? C->ends_old[0] : 0.0;
+  out[15] = own_last ? C->ends_old[1] : 0.0;
+  out[16] = own_first ? C->ends_new[0] : 0.0;
+  out[17] = own_last ? C->ends_new[1] : 0.0;
+  out[18] = __longlong_as_double((long long)C->u_word);
+  out[19] = __longlong_as_double((long long)C->zig_used);
+}
+
+// Metropolis on the all-gathered totals (world x 20, rank order): every rank
+// runs the same fixed-order compensated sums on the same data, so every rank
+// takes the same decision (sampler.py:155-167); then the stream advances and
+// the kept path's statistics and the result are recorded.
+__global__ void shard_decide_kernel(DevControl *C, const double *g, int world, double hconst,
+                                    const uint64_t *snaps, DevResult *ring, int cap, int32_t *count) {
+  if (threadIdx.x || blockIdx.x) return;
+  double S[18];
+  for (int k = 0; k < 18; k++) {
+    double sum = 0.0, comp = 0.0;
+    for (int r = 0; r < world; r++) {  // TwoSum accumulation
+      const double x = g[20 * r + k];
+      const double t = sum + x;
+      const double bp = t - sum;
+      comp += (sum - (t - bp)) + (x - bp);
+      sum = t;
+    }
+    S[k] = sum + comp;
+  }
+  const uint64_t u_word = (uint64_t)__double_as_longlong(g[18]);
+  bool consistent = true;
+  for (int r = 1; r < world; r++) consistent &= (uint64_t)__double_as_longlong(g[20 * r + 18]) == u_word;
+  if (!consistent) atomicOr(&C->err, 8);
+  DevResult res;
+  res.h_old = S[1] + hconst;
+  res.h_new = S[2] + hconst;
+  res.accept = 0;
+  res.u = __longlong_as_double(0x7ff8000000000000LL);
+  const double dh = S[0];
+  bool drew = false;
+  if (S[13] > 0.0 || !isfinite(dh) || fabs(dh) > 1000.0) {
+    res.diverged = 1;
+    res.delta_h = __longlong_as_double(0x7ff0000000000000LL);
+  } else {
+    res.diverged = 0;
+    res.delta_h = dh;
+    res.u = u01(u_word);
+    drew = true;
+    res.accept = (dh <= 0.0) || (res.u < exp(-dh));
+  }
+  res.words_used = C->zig_used + (drew ? 1 : 0);
+  shard_advance(C, drew, snaps);
+  if (res.accept) C->cur ^= 1;
+  C->stats[0] = res.accept ? S[16] : S[14];
+  C->stats[1] = res.accept ? S[17] : S[15];
+  for (int k = 0; k < 5; k++) C->stats[2 + k] = res.accept ? S[8 + k] : S[3 + k];
+  C->res = res;
+  if (ring) {
+    const int i = *count;
+    if (i < cap) ring[i] = res;
+    *count = i + 1;
+  }
+}
+
+// halo: owned boundary sites of the current path out / margins in
+__global__ void shard_halo_kernel(DevControl *C, double *h0, double *h1, int64_t own_lo, int64_t own_hi,
+                                  int64_t T, double *left, int64_t nl, double *right, int64_t nr, int unpack) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double *h = C->cur ? h1 : h0;
+  if (!unpack) {
+    if (i < nl) left[i] = h[own_lo + i];
+    if (i < nr) right[i] = h[own_hi - nr + i];
+  } else {  // left = what the left neighbour sent (my sites [0, nl)), right = [own_hi, own_hi + nr)
+    if (i < nl) h[i] = left[i];
+    if (i < nr && own_hi + i < T) h[own_hi + i] = right[i];
+  }
 }
 
 int rsv_create_shard(rsv_ctx **out, int device, int64_t Tg, int64_t lo, int64_t hi, int64_t margin,
@@ -1132,10 +1227,90 @@ int rsv_shard_propose(rsv_ctx *c, double dt, int n_steps, int fuse, int stats, r
 int rsv_shard_apply(rsv_ctx *c, int accept, int drew) {
   if (!c) return fail(c, RSV_E_INVALID, "null context");
   CK(cudaSetDevice(c->device));
-  shard_apply_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, accept, drew);
+  shard_apply_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, accept, drew, c->sfc_snaps);
   c->launches++;
   CK(cudaGetLastError());
   return sync(c);
+}
+
+int rsv_set_stream(rsv_ctx *c, void *stream) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  if (!c->own_stream) c->own_stream = c->stream;
+  c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+  return 0;
+}
+
+int rsv_shard_propose_async(rsv_ctx *c, double dt, int n_steps, int fuse, int stats, double *totals_dev) {
+  if (!c || !totals_dev) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->shard) return fail(c, RSV_E_STATE, "not a shard context (rsv_create_shard)");
+  int r;
+  if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
+  CK(cudaSetDevice(c->device));
+  rsv_ctx::Cached *cg = nullptr;
+  int kpl = 0;
+  if ((r = get_graph(c, dt, n_steps, fuse, stats, &cg, &kpl))) return r;
+  CK(cudaGraphLaunch(cg->exec, c->stream));
+  const int own_first = c->goff + c->own_lo == 0, own_last = c->goff + c->own_hi == c->Tg;
+  shard_pack_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, own_first, own_last, totals_dev);
+  c->launches += kpl + 1;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int rsv_shard_decide_async(rsv_ctx *c, const double *gathered_dev, int world, double hconst) {
+  if (!c || !gathered_dev || world < 1) return fail(c, RSV_E_INVALID, "bad argument");
+  if (!c->shard) return fail(c, RSV_E_STATE, "not a shard context (rsv_create_shard)");
+  CK(cudaSetDevice(c->device));
+  if (!c->ring || c->ring_cap < 1024) {
+    if (c->ring) cudaFree(c->ring);
+    if (c->h_ring) cudaFreeHost(c->h_ring);
+    c->ring_cap = 1024;
+    CK(cudaMalloc(&c->ring, sizeof(DevResult) * c->ring_cap));
+    CK(cudaMallocHost(&c->h_ring, sizeof(DevResult) * c->ring_cap));
+    CK(cudaMemsetAsync(c->ring_count, 0, sizeof(int32_t), c->stream));
+  }
+  shard_decide_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, gathered_dev, world, hconst, c->sfc_snaps, c->ring,
+                                              c->ring_cap, c->ring_count);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int rsv_shard_halo_async(rsv_ctx *c, double *left, int64_t nl, double *right, int64_t nr, int unpack) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  if (!c->shard) return fail(c, RSV_E_STATE, "not a shard context (rsv_create_shard)");
+  if (nl < 0 || nr < 0 || (nl && !left) || (nr && !right)) return fail(c, RSV_E_INVALID, "bad halo buffers");
+  CK(cudaSetDevice(c->device));
+  const int64_t n = nl > nr ? nl : nr;
+  if (n == 0) return 0;
+  shard_halo_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->ctrl, c->hbuf[0], c->hbuf[1], c->own_lo,
+                                                                      c->own_hi, c->T, left, nl, right, nr, unpack);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// results recorded by rsv_shard_decide_async since the last call (syncs)
+int rsv_shard_results(rsv_ctx *c, rsv_result *out, int max_n, int *n_out) {
+  if (!c || !n_out) return fail(c, RSV_E_INVALID, "null argument");
+  CK(cudaSetDevice(c->device));
+  int32_t n = 0;
+  CK(cudaMemcpyAsync(&n, c->ring_count, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int r;
+  if ((r = pull_ctrl(c))) return r;
+  if (c->h_ctrl->err & 8) return fail(c, RSV_E_CUDA, "shards drew different momenta streams");
+  if ((r = check_err_bits(c))) return r;
+  const int m = n < c->ring_cap ? n : c->ring_cap;
+  if (m > 0 && c->ring) {
+    CK(cudaMemcpy(c->h_ring, c->ring, sizeof(DevResult) * m, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m && i < max_n; i++) to_result(c->h_ring[i], out + i);
+  }
+  *n_out = n;
+  CK(cudaMemset(c->ring_count, 0, sizeof(int32_t)));
+  return 0;
 }
 
 int rsv_latent_slice(rsv_ctx *c, int64_t offset, int64_t n, double *buf, int to_ctx, int on_device) {

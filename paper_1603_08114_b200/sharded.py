@@ -305,3 +305,156 @@ def hmc_update_distributed(chain: ShardedChain, step_size: float, n_steps: int, 
     d = combine([t.cpu().numpy() for t in allt], chain.params, chain.T)
     chain.apply(d)
     return d
+
+
+# ---------------------------------------------------------------------------
+# Device-side orchestration: the host only enqueues work.  Per proposal every
+# shard writes its 20 totals to device memory, the totals are all-gathered
+# (NCCL between GPUs; one buffer for shards sharing a process), and each
+# shard takes the (identical) Metropolis decision on the device.  The margins
+# are refreshed every `halo_every` proposals without knowing the decisions:
+# a margin of M >= (K + 1)(L + 1) sites keeps the owned sites exact for K
+# proposals after an exchange, whatever was accepted in between (each
+# trajectory can corrupt at most L + 1 sites inward from the margin's outer
+# edge).
+
+_RING = 1024  # decisions buffered on the device between two result reads (rsv_shard_decide_async)
+
+
+def halo_period(margin: int, n_steps: int) -> int:
+    """Proposals between two halo exchanges that keep the owned sites exact."""
+    k = margin // (n_steps + 1) - 1
+    if k < 1:
+        raise ValueError(f"margin {margin} too small for n_steps={n_steps}: need >= {2 * (n_steps + 1)}")
+    return k
+
+
+def _cuda_shard_ptrs(chains):
+    for c in chains:
+        if not isinstance(c.shard, CudaShard):
+            raise TypeError("device orchestration needs CUDA shards")
+
+
+def _results(chain, n):
+    if n == 0:
+        return []
+    out = (N.Result * max(1, n))()
+    got = ctypes.c_int(0)
+    chain.shard._ck(chain.shard._lib.rsv_shard_results(chain.shard.ctx, out, int(n), ctypes.byref(got)))
+    return [out[i] for i in range(min(n, got.value))]
+
+
+def hmc_update_local_device(chains: list[ShardedChain], step_size: float, n_steps: int, n: int,
+                            fuse: bool = False, stats: bool = False, halo_every: int | None = None):
+    """n proposals of a chain whose shards live in this process (one GPU or
+    several), orchestrated on the device: no host synchronisation until the
+    results are read back.  Returns the per-proposal rsv_result records."""
+    import torch
+    _cuda_shard_ptrs(chains)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.Stream(dev)  # one ordered stream for every shard and every buffer
+    with torch.cuda.stream(stream):
+        return _local_device(chains, step_size, n_steps, n, fuse, stats, halo_every, dev, stream)
+
+
+def _local_device(chains, step_size, n_steps, n, fuse, stats, halo_every, dev, stream):
+    import torch
+    world = len(chains)
+    for c in chains:
+        c.shard._ck(c.shard._lib.rsv_set_stream(c.shard.ctx, ctypes.c_void_p(stream.cuda_stream)))
+    K = halo_every or halo_period(chains[0].margin, n_steps)
+    hc = h_constant(chains[0].params, chains[0].T)
+    gathered = torch.zeros((world, TOTALS), dtype=torch.float64, device=dev)
+    res = [[] for _ in chains]
+    sends = [(torch.empty(c.halo_sizes(c.rank - 1)[1] if c.rank > 0 else 0, dtype=torch.float64, device=dev),
+              torch.empty(c.halo_sizes(c.rank + 1)[0] if c.rank < world - 1 else 0, dtype=torch.float64, device=dev))
+             for c in chains]
+    lib = chains[0].shard._lib
+    try:
+        for i in range(n):
+            if i % K == 0 or not all(c.halo_valid for c in chains):
+                for c, (sl, sr) in zip(chains, sends):
+                    c.shard._ck(lib.rsv_shard_halo_async(c.shard.ctx, sl.data_ptr(), sl.numel(), sr.data_ptr(),
+                                                         sr.numel(), 0))
+                for r, c in enumerate(chains):  # my left margin <- left neighbour's right send, and vice versa
+                    fl = sends[r - 1][1] if r > 0 else None
+                    fr = sends[r + 1][0] if r < world - 1 else None
+                    c.shard._ck(lib.rsv_shard_halo_async(
+                        c.shard.ctx, fl.data_ptr() if fl is not None else None, fl.numel() if fl is not None else 0,
+                        fr.data_ptr() if fr is not None else None, fr.numel() if fr is not None else 0, 1))
+                    c.halo_valid = True
+            for r, c in enumerate(chains):
+                c.shard._ck(lib.rsv_shard_propose_async(c.shard.ctx, float(step_size), int(n_steps), int(bool(fuse)),
+                                                        int(bool(stats)), gathered[r].data_ptr()))
+            for c in chains:
+                c.shard._ck(lib.rsv_shard_decide_async(c.shard.ctx, gathered.data_ptr(), world, float(hc)))
+            if (i + 1) % _RING == 0:  # the device result ring holds _RING records
+                for c, acc in zip(chains, res):
+                    acc.extend(_results(c, _RING))
+        for c, acc in zip(chains, res):
+            acc.extend(_results(c, n % _RING))
+    finally:
+        for c in chains:
+            c.shard._lib.rsv_set_stream(c.shard.ctx, None)
+    for r in range(1, world):  # every shard recorded the same decisions
+        if [x.accept for x in res[r]] != [x.accept for x in res[0]]:
+            raise RuntimeError("shards took different decisions")
+    return res[0]
+
+
+def hmc_update_distributed_device(chain: ShardedChain, step_size: float, n_steps: int, n: int, fuse: bool = False,
+                                  stats: bool = False, group=None, halo_every: int | None = None):
+    """n proposals of a sharded chain over a torch.distributed (NCCL) group,
+    orchestrated on the device: totals all-gathered on the GPU, decisions on
+    the GPU, periodic halo exchange; the host synchronises once at the end."""
+    import torch
+    _cuda_shard_ptrs([chain])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.Stream(dev)  # the kernels and the NCCL collectives share one ordered stream
+    with torch.cuda.stream(stream):
+        return _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_every, dev, stream)
+
+
+def _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_every, dev, stream):
+    import torch
+    import torch.distributed as dist
+    r, w = chain.rank, chain.world
+    lib = chain.shard._lib
+    chain.shard._ck(lib.rsv_set_stream(chain.shard.ctx, ctypes.c_void_p(stream.cuda_stream)))
+    K = halo_every or halo_period(chain.margin, n_steps)
+    hc = h_constant(chain.params, chain.T)
+    mine = torch.zeros(TOTALS, dtype=torch.float64, device=dev)
+    gathered = torch.zeros((w, TOTALS), dtype=torch.float64, device=dev)
+    nl_send = chain.halo_sizes(r - 1)[1] if r > 0 else 0
+    nr_send = chain.halo_sizes(r + 1)[0] if r < w - 1 else 0
+    nl_recv, nr_recv = chain.halo_sizes(r)
+    send_l = torch.empty(nl_send, dtype=torch.float64, device=dev)
+    send_r = torch.empty(nr_send, dtype=torch.float64, device=dev)
+    recv_l = torch.empty(nl_recv if r > 0 else 0, dtype=torch.float64, device=dev)
+    recv_r = torch.empty(nr_recv if r < w - 1 else 0, dtype=torch.float64, device=dev)
+    out = []
+    try:
+        for i in range(n):
+            if w > 1 and (i % K == 0 or not chain.halo_valid):
+                chain.shard._ck(lib.rsv_shard_halo_async(chain.shard.ctx, send_l.data_ptr(), nl_send,
+                                                         send_r.data_ptr(), nr_send, 0))
+                ops = []
+                if r > 0:
+                    ops += [dist.P2POp(dist.isend, send_l, r - 1, group), dist.P2POp(dist.irecv, recv_l, r - 1, group)]
+                if r < w - 1:
+                    ops += [dist.P2POp(dist.isend, send_r, r + 1, group), dist.P2POp(dist.irecv, recv_r, r + 1, group)]
+                for q in dist.batch_isend_irecv(ops):
+                    q.wait()  # orders the copies on the current stream (no host block)
+                chain.shard._ck(lib.rsv_shard_halo_async(chain.shard.ctx, recv_l.data_ptr(), recv_l.numel(),
+                                                         recv_r.data_ptr(), recv_r.numel(), 1))
+                chain.halo_valid = True
+            chain.shard._ck(lib.rsv_shard_propose_async(chain.shard.ctx, float(step_size), int(n_steps),
+                                                        int(bool(fuse)), int(bool(stats)), mine.data_ptr()))
+            dist.all_gather_into_tensor(gathered, mine, group=group)
+            chain.shard._ck(lib.rsv_shard_decide_async(chain.shard.ctx, gathered.data_ptr(), w, float(hc)))
+            if (i + 1) % _RING == 0:
+                out.extend(_results(chain, _RING))
+        out.extend(_results(chain, n % _RING))
+        return out
+    finally:
+        lib.rsv_set_stream(chain.shard.ctx, None)

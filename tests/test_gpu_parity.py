@@ -291,3 +291,38 @@ def test_sharded_chain_on_one_gpu_matches_single_context(backend, world, T):
     assert all(int(c.get_stream().pos) == int(single.get_stream().pos) for c in shards)
     for c in shards:
         c.shard.close()
+
+
+@pytest.mark.parametrize("world,kind", [(2, "pcg32"), (3, "sfc64"), (4, "philox")])
+def test_sharded_device_orchestration_matches_single_context(backend, world, kind):
+    # the device-side driver: totals gathered in device memory, decisions on
+    # the GPU, margins exchanged only every K proposals (margin >= (K+1)(L+1))
+    T, L, n = 20000, 12, 14
+    truth = P.simulate_rsv(THETA, T, seed=19)
+    data = truth.dataset
+    margin = 3 * (L + 1) + 3
+    assert P.sharded.halo_period(margin, L) == 2
+    shards = [P.ShardedChain(data, THETA, r, world, margin=margin) for r in range(world)]
+    st0 = P.stream_state(P.make_rng(23, kind))
+    for c in shards:
+        c.set_latent_global(truth.latent)
+        c.set_stream(st0)
+    single = backend.chain(data, THETA)
+    single.set_latent(truth.latent)
+    single.set_stream(st0)
+    res = P.sharded.hmc_update_local_device(shards, 0.02, L, n)
+    ref = single.hmc_update_many(0.02, L, n)
+    H = abs(P.hamiltonian(P.PhaseState(truth.latent, np.zeros(T)), THETA, data, backend=backend))
+    assert [bool(x.accept) for x in res] == [bool(x.accept) for x in ref]
+    assert 0 < sum(bool(x.accept) for x in ref) < n  # both outcomes exercised
+    for a, b in zip(res, ref):
+        if b.diverged:
+            assert a.diverged
+        else:
+            assert abs(a.delta_h - b.delta_h) <= 1e-13 * H
+    h = np.concatenate([c.owned_latent() for c in shards])
+    assert _rel(h, single.get_latent()) <= 1e-12
+    for c in shards:
+        s, s1 = c.get_stream(), single.get_stream()
+        assert int(s.pos) == int(s1.pos) and [int(x) for x in s.s] == [int(x) for x in s1.s]
+        c.shard.close()

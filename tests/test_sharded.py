@@ -117,3 +117,11 @@ def test_gloo_two_ranks_match_single_chain():
             assert (math.isinf(dh) and math.isinf(rd)) or abs(dh - rd) <= 1e-12 * H
     h = np.concatenate([out[0][1], out[1][1]])
     assert np.max(np.abs(h - ref_h)) <= 1e-12 * np.max(np.abs(ref_h))
+
+
+def test_halo_period_keeps_owned_sites_exact():
+    from paper_1603_08114_b200.sharded import halo_period
+    assert halo_period(8 * 21, 20) == 7
+    assert halo_period(42, 12) == 2
+    with pytest.raises(ValueError):
+        halo_period(30, 20)
