@@ -38,9 +38,10 @@ UNIT = "site-updates/s"
 THETA = dict(phi=0.97, mu=-9.0, xi=-0.3, sigma_eta_sq=0.05, sigma_u_sq=0.1)
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 # algorithmic FP64 work of one site-update in the trajectory kernel
-# (DESIGN.md "Roofline"): 2 drifts (2 FMA), kick (3 FMA + 2 ADD),
-# exp(-d) (8 FMA + 1 ADD + 1 MUL)  ->  13 FMA + 4 other = 30 flops.
-FLOPS_PER_SITE_UPDATE = 30
+# (DESIGN.md 4.2): 2 drifts (2 FMA), kick (3 FMA + 2 ADD), exp(-d) (6 FMA +
+# 1 ADD + 1 MUL)  ->  11 FMA + 4 other = 26 flops in 15 FP64 instructions.
+FLOPS_PER_SITE_UPDATE = 26
+FP64_INSTR_PER_SITE_UPDATE = 15  # DFMA-pipe instructions (FMA, ADD, MUL each one issue slot)
 HBM_BYTES_PER_SITE = 48  # streamed elementary step: r h,p,(y/2)y,lnRV; w h,p
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
@@ -61,6 +62,7 @@ def parse():
     ap.add_argument("--no-ensemble", action="store_true")
     ap.add_argument("--no-protocol", action="store_true")
     ap.add_argument("--no-config5", action="store_true")
+    ap.add_argument("--no-chain", action="store_true")
     ap.add_argument("--c5-T", type=int, default=1 << 26)
     ap.add_argument("--ens-chains", type=int, default=4096)
     ap.add_argument("--ens-T", type=int, default=4096)
@@ -437,7 +439,8 @@ def main():
             extra["ensemble"] = ensemble_run(P, theta, dt, L, args.ens_chains, args.ens_T, args.steps)
         if not args.no_protocol:
             extra["paper_protocol"] = paper_protocol(args.no_cpu)
-        extra["chain_config1"] = chain_run(P, be, theta)
+        if not args.no_chain:
+            extra["chain_config1"] = chain_run(P, be, theta)
         if not args.no_config5:
             extra["config5"] = config5_run(P, theta, args.c5_T)
         if not args.no_cpu:
@@ -463,7 +466,12 @@ def main():
             "roofline": {"kernel": "traj_kernel (fused L-step trajectory)", "bound": "fp64", "achieved": achieved,
                          "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
                          "flops_per_site_update": FLOPS_PER_SITE_UPDATE,
-                         "peak_source": "measured live: DFMA microbenchmark (rsv_measure_fp64_peak)"},
+                         "peak_source": "measured live: DFMA microbenchmark (rsv_measure_fp64_peak)",
+                         "fp64_pipe": {"instr_per_site_update": FP64_INSTR_PER_SITE_UPDATE,
+                                       "frac": FP64_INSTR_PER_SITE_UPDATE * 2 / FLOPS_PER_SITE_UPDATE * achieved / fp64_peak,
+                                       "note": "issue-slot view: every FP64 instruction occupies the pipe like an FMA"},
+                         "in_kernel": {"trajectory_us": stamps["trajectory_us"],
+                                       "achieved_tflops": FLOPS_PER_SITE_UPDATE * T * L / (stamps["trajectory_us"] * 1e-6) / 1e12}},
             "clocks": clk,
         }
         line.update(extra)
