@@ -653,6 +653,8 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
       chain = g0 >= 0 ? g0 / A.Tc : -1;
     }
     uint32_t firstm = 0;
+    // only a lane whose sites include global site 0 or Tg-1 has end sites
+    const bool near_end = (g0 + goff <= 0 && g0 + goff + R > 0) || (g0 + goff <= Tg - 1 && g0 + goff + R > Tg - 1);
 #pragma unroll
     for (int r = 0; r < R; r++) {
       const int64_t gi = g0 + r;
@@ -667,7 +669,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
       if (ENS) {
         endm |= (uint32_t)((cf && r == 0) || (cl && r == R - 1)) << r;
         firstm |= (uint32_t)(cf && r == 0) << r;
-      } else {
+      } else if (near_end) {
         endm |= (uint32_t)(gi + goff == 0 || gi + goff == Tg - 1) << r;
         firstm |= (uint32_t)(gi + goff == 0) << r;
       }
@@ -819,18 +821,24 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   double w[TR_NV];
 #pragma unroll
   for (int k = 0; k < TR_NV; k++) w[k] = S.acc[k * NT + tid];
-  block_sum<TR_NV, NW>(w, S.red, lane, warp);
-  if (tid == 0) {
-    TilePart *tp = A.parts + blockIdx.x;
-    tp->dh = w[0];
-    tp->hold = w[1];
-    tp->hnew = w[2];
-    for (int k = 0; k < 5; k++) {
-      tp->so[k] = w[3 + k];
-      tp->sn[k] = w[8 + k];
-    }
-    tp->flag = w[13];
+#pragma unroll
+  for (int k = 0; k < TR_NV; k++) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) w[k] += __shfl_xor_sync(0xffffffffu, w[k], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < TR_NV; k++) S.red[warp * TR_NV + k] = w[k];
+  }
+  __syncthreads();
+  if (tid < TR_NV) {  // value k: warp totals in warp order, one thread per value
+    double acc = S.red[tid];
+    for (int q = 1; q < NW; q++) acc += S.red[q * TR_NV + tid];
+    reinterpret_cast<double *>(A.parts + blockIdx.x)[tid] = acc;  // TilePart = TR_NV doubles in w order
     __threadfence();
+  }
+  __syncthreads();
+  if (tid == 0) {
     const unsigned done = atomicAdd(&A.ctrl->tiles_done, 1u);
     S.last = (done == (unsigned)gridDim.x - 1);
   }
@@ -1076,13 +1084,18 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   if (lane == 0)
     for (int k = 0; k < TR_NV; k++) s_v[warp * TR_NV + k] = v[k];
   __syncthreads();
-  if (threadIdx.x) return;
-  double tot[TR_NV];
-  for (int k = 0; k < TR_NV; k++) {
+  // the warp totals of value k are added in warp order by thread k (in
+  // parallel over k), then thread 0 reads the NV results
+  if (threadIdx.x < TR_NV) {
+    const int k = threadIdx.x;
     double acc = s_v[k];
     for (int w = 1; w < NW; w++) acc += s_v[w * TR_NV + k];
-    tot[k] = acc;
+    s_v[NW * TR_NV + k] = acc;
   }
+  __syncthreads();
+  if (threadIdx.x) return;
+  double tot[TR_NV];
+  for (int k = 0; k < TR_NV; k++) tot[k] = s_v[NW * TR_NV + k];
   DevControl *C = A.ctrl;
   C->tiles_done = 0;  // re-arm for the next launch
   C->t_stamp[3] = gtimer();

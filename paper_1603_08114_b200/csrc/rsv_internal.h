@@ -43,6 +43,7 @@ struct TilePart {  // per-tile partial sums over the tile's core sites
   double sn[5];    // proposal: same
   double flag;     // > 0 if any core site left [-50, 50] (or NaN) at a kick
 };
+static_assert(sizeof(TilePart) == TR_NV * sizeof(double), "TilePart is the TR_NV reduced values in order");
 
 // ---- ensemble of independent chains (rsv_ens_*) ------------------------------
 struct EnsPart {  // per trajectory tile: partials of the (<= 2) chains its core touches
