@@ -98,6 +98,13 @@ int rsv_refresh_momenta(rsv_ctx *ctx, double *p_out, int on_device);
  * momenta -> H_old -> L leapfrog steps -> H_new -> Metropolis, all on
  * device.  fuse != 0 selects integrate_trajectory(fuse_half_steps=True). */
 int rsv_hmc_update(rsv_ctx *ctx, double step_size, int n_steps, int fuse, rsv_result *out);
+/* sampler.py:144-167 in one call from host memory (the reference-facing
+ * fast path of hmc_update_volatility): h_in (T doubles) and *stream in; when
+ * the proposal is accepted it is written to h_out (otherwise h_out is left
+ * untouched: the kept path is h_in); *stream advanced; one synchronisation
+ * (two when accepted).  The theta statistics are not evaluated. */
+int rsv_hmc_update_host(rsv_ctx *ctx, const double *h_in, double *h_out, rsv_prng_state *stream, double step_size,
+                        int n_steps, int fuse, rsv_result *out);
 /* n back-to-back proposals with fixed params (one CUDA graph per proposal,
  * no host round trip in between); results (n entries) optional.  Like the
  * reference's hmc_update_volatility these proposals do not evaluate the theta

@@ -733,6 +733,57 @@ int rsv_hmc_update(rsv_ctx *c, double dt, int n_steps, int fuse, rsv_result *out
   return 0;
 }
 
+// sampler.py:144-167 in one call from host memory: the path and the stream
+// state go in with asynchronous copies, the proposal runs as one graph, and
+// one synchronisation returns the result (a second one copies the proposal
+// out when it was accepted).  The theta statistics are not evaluated.
+int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_state *st, double dt, int n_steps,
+                        int fuse, rsv_result *out) {
+  if (!c || !h_in || !h_out || !st || !out) return fail(c, RSV_E_INVALID, "null argument");
+  int r;
+  if ((r = check_md(c, dt, n_steps))) return r;
+  if (!c->has_data) return fail(c, RSV_E_STATE, "data not set (rsv_set_data)");
+  if (!c->has_params) return fail(c, RSV_E_STATE, "params not set (rsv_set_params)");
+  if (c->shard || c->ens_C) return fail(c, RSV_E_STATE, "rsv_hmc_update_host needs a single-chain context");
+  if (st->kind < 0 || st->kind > 3) return fail(c, RSV_E_INVALID, "invalid bit generator state");
+  if (st->kind == PRNG_MINSTD && (st->s[0] == 0 || st->s[0] >= MINSTD_M))
+    return fail(c, RSV_E_INVALID, "minstd state must be in [1, 2^31-2]");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));  // h_ctrl is the staging area below
+  StreamState ss;
+  ss.kind = st->kind;
+  ss.reserved = 0;
+  for (int i = 0; i < 4; i++) ss.s[i] = st->s[i];
+  ss.pos = st->pos;
+  c->h_ctrl->stream = ss;
+  c->h_ctrl->seq_state = ss.kind == PRNG_PCG32    ? pcg_advance(ss.s[0], 2 * ss.pos, ss.s[1])
+                         : ss.kind == PRNG_MINSTD ? mod31(minstd_pow(3 * ss.pos) * ss.s[0])
+                                                  : 0;
+  if (ss.kind != c->kind) c->kind = ss.kind;
+  CK(cudaMemcpyAsync(&c->ctrl->stream, &c->h_ctrl->stream, sizeof(StreamState), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(&c->ctrl->seq_state, &c->h_ctrl->seq_state, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemcpyAsync(c->hbuf[0], h_in, sizeof(double) * c->T, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(&c->ctrl->cur, 0, sizeof(int32_t), c->stream));
+  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
+  c->has_latent = true;
+  rsv_ctx::Cached *cg = nullptr;
+  int kpl = 0;
+  if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl))) return r;
+  CK(cudaGraphLaunch(cg->exec, c->stream));
+  c->launches += kpl;
+  if ((r = pull_ctrl(c)) || (r = check_err_bits(c))) return r;
+  to_result(c->h_ctrl->res, out);
+  st->pos = c->h_ctrl->stream.pos;
+  for (int i = 0; i < 4; i++) st->s[i] = c->h_ctrl->stream.s[i];
+  if (out->accept) {
+    CK(cudaMemcpyAsync(h_out, c->hbuf[c->h_ctrl->cur & 1], sizeof(double) * c->T, cudaMemcpyDeviceToHost,
+                       c->stream));
+    return sync(c);
+  }
+  return 0;  // rejected or divergent: the kept path is h_in, h_out is not written
+}
+
 int rsv_last_stats(rsv_ctx *c, double out[7]) {
   if (!c || !out) return fail(c, RSV_E_INVALID, "null argument");
   for (int i = 0; i < 7; i++) out[i] = c->h_ctrl->stats[i];

@@ -189,6 +189,20 @@ class DeviceChain:
         self._ck(self._lib.rsv_get_params(self.ctx, ctypes.byref(p)))
         return N.to_params(p)
 
+    def hmc_update_host(self, h: np.ndarray, st: N.PrngState, step_size: float, n_steps: int,
+                        fuse: bool = False):
+        """One proposal from a host path (rsv_hmc_update_host): returns
+        (result, path_out) where path_out is a page-locked array holding the
+        proposal when accepted (None otherwise); st is advanced in place."""
+        h = _f64(h)
+        if h.shape != (self.T,):
+            raise ValueError(f"latent path length {h.shape[0]} does not match chain length {self.T}")
+        out = self._pinned_out()
+        r = N.Result()
+        self._ck(self._lib.rsv_hmc_update_host(self.ctx, h.ctypes.data, out.ctypes.data, ctypes.byref(st),
+                                               float(step_size), int(n_steps), int(bool(fuse)), ctypes.byref(r)))
+        return r, (out if r.accept else None)
+
     def hmc_update_many(self, step_size: float, n_steps: int, n: int, fuse: bool = False,
                         results: bool = True):
         out = (N.Result * n)() if results else None

@@ -142,14 +142,13 @@ def hmc_update_volatility(h: np.ndarray, params: Params, data: Dataset, md: MDCo
     out-of-bounds dH rejects with the +inf sentinel and draws no uniform."""
     ch = _resolve(backend).chain(data, params)
     h64 = np.ascontiguousarray(h, dtype=np.float64)
-    ch.set_latent(h64)
-    ch.set_stream(stream_state(rng))
-    r = ch.hmc_update(md.step_size, md.n_steps, fuse_half_steps, stats=False)
-    store_stream_state(rng, ch.get_stream())
+    st = stream_state(rng)
+    r, h_new = ch.hmc_update_host(h64, st, md.step_size, md.n_steps, fuse_half_steps)
+    store_stream_state(rng, st)
     if r.diverged:
         return h, False, DIVERGENT_DELTA_H
     if r.accept:
-        return ch.get_latent(), True, float(r.delta_h)
+        return h_new, True, float(r.delta_h)
     return h, False, float(r.delta_h)
 
 
