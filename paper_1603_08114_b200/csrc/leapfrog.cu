@@ -857,7 +857,7 @@ static const TrajVariant kVariants[] = {{8, 256, 2}, {4, 256, 3}, {4, 128, 6}, {
                                         // persistent + TMA-staged (9..14); 12..14 are the
                                         // small-window shapes for short series
                                         {8, 256, 2}, {4, 256, 3}, {4, 256, 2}, {4, 128, 3}, {4, 64, 5},
-                                        {4, 32, 8}, {8, 256, 1}, {6, 256, 1}};
+                                        {4, 32, 8}, {8, 256, 1}, {6, 256, 1}, {4, 512, 1}};
 static bool variant_persistent(int v) { return v >= 9; }
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -1000,6 +1000,7 @@ const void *traj_kernel_fn(int variant, int fuse, int stats) {
     case 14: return RSV_FN(4, 32, 8);
     case 15: return RSV_FN(8, 256, 1);
     case 16: return RSV_FN(6, 256, 1);
+    case 17: return RSV_FN(4, 512, 1);
     default: return RSV_FN(4, 256, 2);
   }
 #undef RSV_FN
@@ -1054,6 +1055,7 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
     case 14: launch_p<4, 32, 8>(a, s); break;
     case 15: launch_p<8, 256, 1>(a, s); break;
     case 16: launch_p<6, 256, 1>(a, s); break;
+    case 17: launch_p<4, 512, 1>(a, s); break;
     default: launch_p<4, 256, 2>(a, s); break;
   }
   (*launches)++;

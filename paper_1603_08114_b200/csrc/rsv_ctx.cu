@@ -567,7 +567,7 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   cg->args.stats = k.stats;
   // programmatic dependent launch of the trajectory after the momenta kernel
   // (not with timing event nodes between them)
-  cg->args.pdl = (k.timing == 0 && variant_is_persistent(g.variant)) ? 1 : 0;
+  cg->args.pdl = (k.timing == 0 && variant_is_persistent(g.variant) && !getenv("RSV_NO_PDL")) ? 1 : 0;
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   int l = 0;
