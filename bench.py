@@ -142,6 +142,31 @@ def config5_run(P, theta, T, block=4096, sweeps=20, dt=0.005):
             "timing": "wall clock around rsv_run_chain (device-resident chain; includes the samples' D2H)"}
 
 
+def formats_run(P, theta, T=1 << 18, n_lat=8):
+    """The data formats on either side of the sampler (host):
+    dataset CSV save/load at T=2^18 and n_lat latent snapshots in the CSV
+    companion vs the binary .npy sidecar."""
+    import tempfile
+    tr = P.simulate_rsv(theta, T, seed=7)
+    out = {"T": T, "latent_snapshots": n_lat}
+    with tempfile.TemporaryDirectory() as d:
+        f = os.path.join(d, "data.csv")
+        t0 = time.perf_counter(); P.save_dataset(tr.dataset, f); out["dataset_save_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter(); back = P.load_dataset(f); out["dataset_load_s"] = time.perf_counter() - t0
+        out["dataset_round_trip_exact"] = bool(np.array_equal(back.returns, tr.dataset.returns)
+                                               and np.array_equal(back.rv, tr.dataset.rv))
+        lat = tr.latent[None, :] + np.zeros((n_lat, 1))
+        ch = P.Chain(iters=np.arange(n_lat), phi=np.full(n_lat, 0.97), mu=np.full(n_lat, -9.0),
+                     xi=np.full(n_lat, -0.3), sigma_eta_sq=np.full(n_lat, 0.05), sigma_u_sq=np.full(n_lat, 0.1),
+                     accept=np.ones(n_lat, bool), delta_h=np.zeros(n_lat), latent=lat)
+        for kind in ("csv", "npy"):
+            f = os.path.join(d, f"chain_{kind}.csv")
+            t0 = time.perf_counter(); P.save_chain(ch, f, latent=kind); ts = time.perf_counter() - t0
+            t0 = time.perf_counter(); b2 = P.load_chain(f); tl = time.perf_counter() - t0
+            out[f"chain_latent_{kind}"] = {"save_s": ts, "load_s": tl, "exact": bool(np.array_equal(b2.latent, lat))}
+    return out
+
+
 def chain_run(P, be, theta):
     """Config 1 as a full sampler: run_chain (sampler.py:291-358) on T=2000,
     L=20, dt=0.02, minstd, every sweep (proposal + the five theta draws) on
@@ -443,6 +468,7 @@ def main():
             extra["chain_config1"] = chain_run(P, be, theta)
         if not args.no_config5:
             extra["config5"] = config5_run(P, theta, args.c5_T)
+        extra["formats"] = formats_run(P, theta)
         if not args.no_cpu:
             extra["cpu_baseline"] = cpu_baseline(T, L, dt, args.prng, args.cpu_seconds, data, truth.latent)
 

@@ -14,7 +14,11 @@ from .integrator import (DH_DIVERGENCE_THRESHOLD, CudaBackend, DeviceChain, MDCo
                          kernel3_half_position)
 from .model import (PARAM_NAMES, Dataset, Params, PhaseState, grad_neg_log_posterior, hamiltonian,
                     log_posterior, scalar_pack)
+from .bench_protocol import (BenchConfig, NumericError, ScalingStudy, TimingFit, TimingPoint, asymptotic_gain,
+                             compute_gain, emit_report, fit_linear, run_scaling_study, time_elementary_step)
 from .ensemble import Ensemble, sfc64_states
+from .formats import (DataFormatError, IntradayPanel, compute_rv, load_chain, load_dataset, load_intraday,
+                      load_truth, save_chain, save_dataset, save_truth)
 from .sharded import ShardedChain, hmc_update_distributed, hmc_update_local, shard_bounds
 from .rng import RsvBitGenerator, make_rng, seed_material, store_stream_state, stream_state
 from .sampler import (Chain, ChainSample, DivergenceStormError, PriorSpec, SamplerConfig, default_init,
@@ -24,6 +28,10 @@ from .sampler import (Chain, ChainSample, DivergenceStormError, PriorSpec, Sampl
 __version__ = "0.1.0"
 
 __all__ = [
+    "BenchConfig", "DataFormatError", "IntradayPanel", "NumericError", "ScalingStudy", "TimingFit", "TimingPoint",
+    "asymptotic_gain", "compute_gain", "compute_rv", "emit_report", "fit_linear", "load_chain", "load_dataset",
+    "load_intraday", "load_truth", "run_scaling_study", "save_chain", "save_dataset", "save_truth",
+    "time_elementary_step",
     "Chain", "ChainSample", "CudaBackend", "Ensemble", "sfc64_states", "DH_DIVERGENCE_THRESHOLD", "Dataset", "DeviceChain",
     "DivergenceStormError", "MDConfig", "PARAM_NAMES", "Params", "PhaseState", "PriorSpec", "RsvBitGenerator",
     "SamplerConfig", "ShardedChain", "SyntheticTruth", "hmc_update_distributed", "hmc_update_local", "shard_bounds", "ar1_path", "default_backend", "default_init", "elementary_step",

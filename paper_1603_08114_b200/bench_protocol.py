@@ -97,9 +97,15 @@ def _set_state(ch: DeviceChain, h: np.ndarray | None, p: np.ndarray | None):
                                    None if p is None else p.ctypes.data))
 
 
-def time_elementary_step(b: int, reps: int, params: Params, data: Dataset, *, step_size: float = 0.01,
-                         repeats: int = 5, n_warmup: int = 10, seed: int = 0, device: int = 0) -> TimingPoint:
-    """Mean device seconds of one elementary step at T = 512*b (bench.py:121-190)."""
+def time_elementary_step(b: int, backend, reps: int, params: Params, data: Dataset, *, step_size: float = 0.01,
+                         repeats: int = 5, n_warmup: int = 10, precision: str = "double", seed: int = 0,
+                         device: int | None = None) -> TimingPoint:
+    """Mean device seconds of one elementary step at T = 512*b (bench.py:121-190,
+    same signature; `backend` is a CudaBackend or None, only its device is used)."""
+    if precision != "double":
+        raise NotImplementedError("the B200 path computes in float64 only (FP32 bench mode is out of scope)")
+    if device is None:
+        device = getattr(backend, "device", 0) if backend is not None else 0
     t_len = SITES_PER_UNIT * b
     if data.length != t_len:
         raise ValueError(f"dataset length {data.length} does not match 512*B = {t_len}")
@@ -175,7 +181,7 @@ def run_scaling_study(config: BenchConfig = BenchConfig(), params: Params = BENC
     pts = []
     for b in config.b_values:
         data = simulate_rsv(params, SITES_PER_UNIT * b, seed=config.seed + b).dataset
-        pts.append(time_elementary_step(b, config.reps, params, data, step_size=config.step_size,
+        pts.append(time_elementary_step(b, None, config.reps, params, data, step_size=config.step_size,
                                         repeats=config.repeats, seed=config.seed, device=config.device))
     study.timings["cuda"] = pts
     if len(set(config.b_values)) >= 2:

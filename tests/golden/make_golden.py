@@ -141,7 +141,47 @@ def chain(kind="pcg32", seed=3, T=200, n=60):
                         pos=np.uint64(keep["st"].pos))
 
 
+def formats():
+    """Files written by the reference's own data.py writers (data.py:154-327)
+    and what its readers return, for tests/test_formats.py."""
+    import rsvhmc.data as RD
+    out_dir = os.path.join(HERE, "formats")
+    os.makedirs(out_dir, exist_ok=True)
+    truth = RD.simulate_rsv(TRUE, 40, seed=3)
+    ds = truth.dataset
+    RD.save_dataset(ds, os.path.join(out_dir, "dataset.csv"))
+    RD.save_truth(truth, os.path.join(out_dir, "truth.csv"))
+    n, T = 6, 40
+    r = np.random.default_rng(5)
+    ch = RS.Chain(iters=np.arange(100, 100 + 2 * n, 2), phi=r.uniform(0.9, 0.99, n), mu=r.normal(-9, 0.1, n),
+                  xi=r.normal(-0.3, 0.01, n), sigma_eta_sq=r.uniform(0.04, 0.06, n),
+                  sigma_u_sq=r.uniform(0.09, 0.11, n), accept=r.uniform(size=n) < 0.7,
+                  delta_h=np.where(r.uniform(size=n) < 0.2, np.inf, r.normal(0, 1, n)),
+                  latent=truth.latent[None, :] + r.normal(0, 0.01, (n, T)))
+    RD.save_chain(ch, os.path.join(out_dir, "chain.csv"))
+    ch.latent = None
+    RD.save_chain(ch, os.path.join(out_dir, "chain_nolatent.csv"))
+    # an intraday panel (written by hand: the reference only reads these)
+    lines = ["date,time,return"]
+    days = ["2000-01-03", "2000-01-04", "2000-01-05"]
+    for d in days:
+        for k in range(5):
+            v = 0.0 if d == "2000-01-05" else float(r.normal(0, 0.001))
+            lines.append(f"{d},{9 + k:02d}:30,{RD._fmt(v)}")
+    with open(os.path.join(out_dir, "intraday.csv"), "w", newline="\n") as fh:
+        fh.write("\n".join(lines) + "\n")
+    panel = RD.load_intraday(os.path.join(out_dir, "intraday.csv"))
+    rv = RD.compute_rv(panel)
+    back = RD.load_chain(os.path.join(out_dir, "chain.csv"))
+    tp, th = RD.load_truth(os.path.join(out_dir, "truth.csv"))
+    np.savez_compressed(os.path.join(HERE, "formats.npz"), returns=ds.returns, rv=ds.rv, log_rv=ds.log_rv,
+                        latent=truth.latent, intraday_rv=rv, chain_latent=back.latent, chain_mu=back.mu,
+                        chain_dh=back.delta_h, chain_accept=back.accept, truth_h=th,
+                        truth_params=np.array([tp.phi, tp.mu, tp.xi, tp.sigma_eta_sq, tp.sigma_u_sq]))
+
+
 if __name__ == "__main__":
+    formats()
     prng()
     model()
     hmc_sequence("minstd", 1)
