@@ -125,8 +125,8 @@ def config5_run(P, theta, T, block=4096, sweeps=20, dt=0.005):
     energy error grows with T).  The timed region is rsv_run_chain on the
     device-resident chain (the path was uploaded by the warm-up run);
     HBM-resident (T >> L2)."""
-    tr = P.simulate_rsv(theta, T, seed=11)
     be = P.CudaBackend(0)
+    tr = P.simulate_rsv(theta, T, seed=11, backend=be)  # data generation on the device (SURVEY 8f.3)
     ch = be.chain(tr.dataset, theta)
     ch.set_blocked_streams(1, block)
     cfg = P.SamplerConfig(seed=1, md=P.MDConfig(dt, 20), n_burnin=0, n_samples=3, prng="sfc64")

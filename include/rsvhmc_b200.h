@@ -179,6 +179,14 @@ int rsv_shard_decide_async(rsv_ctx *ctx, const double *gathered_dev, int world, 
 int rsv_shard_halo_async(rsv_ctx *ctx, double *left, int64_t n_left, double *right, int64_t n_right, int unpack);
 int rsv_shard_results(rsv_ctx *ctx, rsv_result *out, int max_n, int *n_out);
 
+/* data.py:72-95 simulate_rsv on the device: the reference's 3T normals
+ * (initial deviation, innovations, return shocks, measurement noise) drawn
+ * from *stream bit for bit (the stream is advanced), the AR(1) path by a
+ * parallel affine scan (agrees with the sequential recursion to rounding),
+ * h, returns and log_rv written to host (on_device = 0) or device buffers. */
+int rsv_simulate(int device, const rsv_params *params, int64_t T, rsv_prng_state *stream, double *h, double *returns,
+                 double *log_rv, int on_device);
+
 /* Blocked momenta layout (BASELINE config 5; NOT the reference's single-stream
  * layout): SFC64 has no jump-ahead, so for very long series the
  * momenta of sites [j*block_len, (j+1)*block_len) come from their own numpy

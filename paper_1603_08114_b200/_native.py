@@ -107,6 +107,8 @@ _SIGS = {
     "rsv_get_params": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
     "rsv_set_blocked_streams": (ctypes.c_int, [_CTX, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]),
     "rsv_set_stream": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
+    "rsv_simulate": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "rsv_shard_propose_async": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                ctypes.c_void_p]),
     "rsv_shard_decide_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int, ctypes.c_double]),

@@ -1383,6 +1383,83 @@ int rsv_latent_slice(rsv_ctx *c, int64_t offset, int64_t n, double *buf, int to_
   return sync(c);
 }
 
+// ---- simulate_rsv on the device (data.py:72-95) ----------------------------
+int rsv_simulate(int device, const rsv_params *p, int64_t T, rsv_prng_state *st, double *h, double *y,
+                 double *log_rv, int on_device) {
+  if (!p || !st || !h || !y || !log_rv) return fail(nullptr, RSV_E_INVALID, "null argument");
+  if (T < 2) return fail(nullptr, RSV_E_INVALID, "need t_len >= 2, got %lld", (long long)T);
+  if (st->kind < 0 || st->kind > 3) return fail(nullptr, RSV_E_INVALID, "invalid bit generator state");
+  if (!(p->phi > -1.0 && p->phi < 1.0) || !(p->sigma_eta_sq > 0.0) || !(p->sigma_u_sq > 0.0))
+    return fail(nullptr, RSV_E_INVALID, "params outside the model's domain");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(nullptr, RSV_E_CUDA, "no CUDA device %d", device);
+  // a lean context: only what the momenta draw of 3T normals needs
+  rsv_ctx *c = new rsv_ctx();
+  c->device = device;
+  c->T = c->Tg = 3 * T;
+  int r = 0;
+  double *work = nullptr, *out = nullptr;
+  auto body = [&]() -> int {
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    const int64_t Tn = 3 * T;
+    CK(cudaMalloc(&c->normals, sizeof(double) * (size_t)((Tn + 7) / 8 * 8)));
+    CK(cudaMalloc(&c->zscratch, momenta_scratch_bytes(Tn)));
+    CK(cudaMemset(c->zscratch, 0, momenta_scratch_bytes(Tn)));
+    const int64_t nw = momenta_words(Tn) + 64;
+    CK(cudaMalloc(&c->sfc_words, sizeof(uint64_t) * nw));
+    CK(cudaMalloc(&c->sfc_snaps, sizeof(uint64_t) * 4 * (nw / SFC_SNAP + 2)));
+    CK(cudaMalloc(&c->bjump, momenta_jump_bytes(Tn)));
+    CK(cudaMalloc(&c->ctrl, sizeof(DevControl)));
+    CK(cudaMallocHost(&c->h_ctrl, sizeof(DevControl)));
+    memset(c->h_ctrl, 0, sizeof(DevControl));
+    StreamState ss;
+    ss.kind = st->kind;
+    ss.reserved = 0;
+    for (int i = 0; i < 4; i++) ss.s[i] = st->s[i];
+    ss.pos = st->pos;
+    c->h_ctrl->stream = ss;
+    c->h_ctrl->seq_state = ss.kind == PRNG_PCG32    ? pcg_advance(ss.s[0], 2 * ss.pos, ss.s[1])
+                           : ss.kind == PRNG_MINSTD ? mod31(minstd_pow(3 * ss.pos) * ss.s[0])
+                                                    : 0;
+    c->kind = ss.kind;
+    CK(cudaMemcpy(c->ctrl, c->h_ctrl, sizeof(DevControl), cudaMemcpyHostToDevice));
+    if (momenta_init(c->stream, c->bjump, Tn)) return fail(c, RSV_E_CUDA, "momenta table init failed");
+    int l = 0;
+    if (launch_momenta(mbufs(c), c->kind, Tn, c->stream, &l) || launch_momenta_advance(mbufs(c), c->stream, &l))
+      return fail(c, RSV_E_CUDA, "momenta launch failed");
+    const int64_t n_chunks = (T - 1 + 255) / 256;
+    CK(cudaMalloc(&work, sizeof(double) * (size_t)(T + 2 * n_chunks + 8)));
+    double *dh = h, *dy = y, *dl = log_rv;
+    if (!on_device) {
+      CK(cudaMalloc(&out, sizeof(double) * 3 * (size_t)T));
+      dh = out;
+      dy = out + T;
+      dl = out + 2 * T;
+    }
+    if (launch_simulate(c->normals, T, p->phi, p->mu, p->xi, p->sigma_eta_sq, p->sigma_u_sq, dh, dy, dl, work,
+                        c->stream, &l))
+      return fail(c, RSV_E_CUDA, "simulate launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    if (!on_device) {
+      CK(cudaMemcpyAsync(h, dh, sizeof(double) * T, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(y, dy, sizeof(double) * T, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(log_rv, dl, sizeof(double) * T, cudaMemcpyDeviceToHost, c->stream));
+    }
+    int q;
+    if ((q = pull_ctrl(c)) || (q = check_err_bits(c))) return q;
+    st->pos = c->h_ctrl->stream.pos;
+    for (int i = 0; i < 4; i++) st->s[i] = c->h_ctrl->stream.s[i];
+    return 0;
+  };
+  r = body();
+  if (work) cudaFree(work);
+  if (out) cudaFree(out);
+  if (r) g_err = c->err;
+  rsv_destroy(c);
+  return r;
+}
+
 // ---- blocked momenta streams (config 5) -----------------------------------
 int rsv_set_blocked_streams(rsv_ctx *c, int64_t block_len, int64_t n_blocks, const uint64_t *states) {
   if (!c) return fail(c, RSV_E_INVALID, "null context");

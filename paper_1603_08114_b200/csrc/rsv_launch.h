@@ -160,4 +160,9 @@ int reduce_partials_count(int64_t T);
 int launch_theta_sweep(DevControl *ctrl, DevParams *prm, TrajConsts *kdev, DevRun *run, DevPrior prior,
                        double dt, int64_t T, const uint64_t *sfc_snaps, cudaStream_t s, int *launches);
 
+// data.py:72-95 simulate_rsv from 3T numpy normals already on the device;
+// work: T + 2 * ceil((T-1)/256) doubles
+int launch_simulate(const double *normals, int64_t T, double phi, double mu, double xi, double se2, double su2,
+                    double *h, double *y, double *lrv, double *work, cudaStream_t s, int *launches);
+
 }  // namespace rsv

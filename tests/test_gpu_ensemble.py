@@ -115,3 +115,17 @@ def test_paper_protocol_smoke(tmp_path):
     assert [p.b for p in pts] == [2, 4] and all(p.mean_seconds > 0 for p in pts)
     paths = BP.emit_report(study, tmp_path)
     assert paths["fits"].read_text().splitlines()[1] == "backend,intercept_a,slope_c,r_squared"
+
+
+@pytest.mark.parametrize("T", [2, 1000, 70001])
+def test_simulate_on_device_matches_host(T):
+    # the same normals bit for bit; the AR(1) path by a parallel scan agrees
+    # with the sequential recursion to rounding
+    be = P.CudaBackend(0)
+    a = P.simulate_rsv(THETA, T, seed=17)
+    b = P.simulate_rsv(THETA, T, seed=17, backend=be)
+    rel = lambda x, y: float(np.max(np.abs(x - y)) / max(1.0, float(np.max(np.abs(y)))))
+    assert rel(b.latent, a.latent) <= 1e-12
+    assert rel(b.dataset.log_rv, a.dataset.log_rv) <= 1e-12
+    assert float(np.max(np.abs(b.dataset.returns - a.dataset.returns) / np.abs(a.dataset.returns).clip(1e-300))) <= 1e-12
+    be.close()
