@@ -29,18 +29,26 @@ from .rng import make_rng, store_stream_state, stream_state
 
 logger = logging.getLogger(__name__)
 
-DIVERGENT_DELTA_H = math.inf
-_STORM_WINDOW = 100
-_STORM_LIMIT = 50
+DIVERGENT_DELTA_H = math.inf   # dH sentinel of a divergent proposal (sampler.py:31)
+_STORM_WINDOW, _STORM_LIMIT = 100, 50  # abort when > 50 of the last 100 proposals diverged
 
 
 class DivergenceStormError(RuntimeError):
-    """Raised when the HMC proposals diverge persistently (sampler.py:39)."""
+    """The HMC proposals keep diverging (sampler.py:39)."""
+
+
+def _positive(obj, names):
+    for n in names:
+        v = getattr(obj, n)
+        if not v > 0.0:
+            raise ValueError(f"{n} must be positive, got {v}")
 
 
 @dataclass(frozen=True)
 class PriorSpec:
-    """Priors for the static parameters (sampler.py:43-63)."""
+    """Priors of theta (sampler.py:43-63): normal for mu and xi, one
+    inverse-gamma (shape, scale) for both variances, Beta(phi_a, phi_b) on
+    (phi + 1) / 2."""
 
     mu_mean: float = 0.0
     mu_var: float = 100.0
@@ -52,14 +60,13 @@ class PriorSpec:
     phi_b: float = 1.5
 
     def __post_init__(self):
-        for name in ("mu_var", "xi_var", "var_shape", "var_scale", "phi_a", "phi_b"):
-            if not getattr(self, name) > 0.0:
-                raise ValueError(f"{name} must be positive, got {getattr(self, name)}")
+        _positive(self, ("mu_var", "xi_var", "var_shape", "var_scale", "phi_a", "phi_b"))
 
 
 @dataclass(frozen=True)
 class SamplerConfig:
-    """sampler.py:66-81."""
+    """run_chain settings (sampler.py:66-81), plus the raw-word generator
+    kind (`prng`: philox -- the reference's -- minstd, pcg32 or sfc64)."""
 
     seed: int = 0
     md: MDConfig = field(default_factory=lambda: MDConfig(step_size=0.02, n_steps=50))
@@ -70,16 +77,16 @@ class SamplerConfig:
     prng: str = "philox"
 
     def __post_init__(self):
-        if self.n_burnin < 0:
-            raise ValueError(f"n_burnin must be >= 0, got {self.n_burnin}")
-        if self.n_samples < 1:
-            raise ValueError(f"n_samples must be >= 1, got {self.n_samples}")
-        if self.thin < 1:
-            raise ValueError(f"thin must be >= 1, got {self.thin}")
+        for name, low in (("n_burnin", 0), ("n_samples", 1), ("thin", 1)):
+            v = getattr(self, name)
+            if v < low:
+                raise ValueError(f"{name} must be >= {low}, got {v}")
 
 
 @dataclass
 class ChainSample:
+    """One stored sweep."""
+
     params: Params
     accept: bool
     delta_h: float
@@ -88,7 +95,7 @@ class ChainSample:
 
 @dataclass
 class Chain:
-    """Columnar store of an MCMC run (sampler.py:93-128)."""
+    """The stored sweeps of a run, column by column (sampler.py:93-128)."""
 
     iters: np.ndarray
     phi: np.ndarray
@@ -101,23 +108,21 @@ class Chain:
     latent: np.ndarray | None = None
 
     def __len__(self) -> int:
-        return self.iters.size
+        return int(np.shape(self.iters)[0])
 
     def param_series(self, name: str) -> np.ndarray:
-        if name not in PARAM_NAMES:
-            raise KeyError(f"unknown parameter {name!r}")
-        return getattr(self, name)
+        if name in PARAM_NAMES:
+            return getattr(self, name)
+        raise KeyError(f"unknown parameter {name!r}")
 
     def sample(self, i: int) -> ChainSample:
-        params = Params(phi=float(self.phi[i]), mu=float(self.mu[i]), xi=float(self.xi[i]),
-                        sigma_eta_sq=float(self.sigma_eta_sq[i]), sigma_u_sq=float(self.sigma_u_sq[i]))
-        latent = None if self.latent is None else self.latent[i]
-        return ChainSample(params=params, accept=bool(self.accept[i]), delta_h=float(self.delta_h[i]),
-                           latent=latent)
+        theta = Params(**{n: float(getattr(self, n)[i]) for n in PARAM_NAMES})
+        return ChainSample(params=theta, accept=bool(self.accept[i]), delta_h=float(self.delta_h[i]),
+                           latent=self.latent[i] if self.latent is not None else None)
 
     @property
     def n_divergent(self) -> int:
-        return int(np.sum(np.isinf(self.delta_h)))
+        return int(np.isinf(self.delta_h).sum())
 
 
 def refresh_momenta(rng: np.random.Generator, t_len: int, dtype=np.float64, backend=None) -> np.ndarray:
