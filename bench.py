@@ -305,11 +305,12 @@ def run_reference(args, ws, rank):
     value = args.T * args.L * args.steps / tot
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (simulate_rsv, seed 0)",
-            "impl": "reference",
-            "config": {"workload": f"single chain T={args.T}, L={args.L}, dt={args.dt}, {args.prng}: one full HMC "
-                                   "proposal per step (reference CPU algorithm, oracle port)",
-                       "T": args.T, "L": args.L, "prng": args.prng},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (simulate_rsv, theta of SURVEY \u00a78d, seed 0)", "impl": "reference",
+            "config": {"workload": f"config 3: single chain T={args.T}, L={args.L}, dt={args.dt}, {args.prng}; one "
+                                   "step = one full HMC proposal (reference CPU algorithm: the oracle port, all host "
+                                   "threads for the leapfrog kernels)",
+                       "T": args.T, "L": args.L, "dt": args.dt, "prng": args.prng},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "port",
                              "sample": f"{args.steps} HMC proposals at T={args.T}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
