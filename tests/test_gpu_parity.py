@@ -326,3 +326,37 @@ def test_sharded_device_orchestration_matches_single_context(backend, world, kin
         s, s1 = c.get_stream(), single.get_stream()
         assert int(s.pos) == int(s1.pos) and [int(x) for x in s.s] == [int(x) for x in s1.s]
         c.shard.close()
+
+
+def test_sharded_distributed_device_driver_nccl_world_of_one(backend):
+    # the NCCL path of the device-orchestrated driver (all_gather of totals,
+    # decisions on the GPU) with a process group of one rank
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        T, L, n = 30000, 20, 10
+        truth = P.simulate_rsv(THETA, T, seed=29)
+        data = truth.dataset
+        chain = P.ShardedChain(data, THETA, 0, 1, margin=8 * (L + 1))
+        st0 = P.stream_state(P.make_rng(31, "pcg32"))
+        chain.set_latent_global(truth.latent)
+        chain.set_stream(st0)
+        single = backend.chain(data, THETA)
+        single.set_latent(truth.latent)
+        single.set_stream(st0)
+        res = P.sharded.hmc_update_distributed_device(chain, 0.02, L, n)
+        ref = single.hmc_update_many(0.02, L, n)
+        assert [bool(x.accept) for x in res] == [bool(x.accept) for x in ref]
+        for a, b in zip(res, ref):
+            assert a.diverged == b.diverged and (b.diverged or abs(a.delta_h - b.delta_h) <= 1e-9)
+        assert _rel(chain.owned_latent(), single.get_latent()) <= 1e-12
+        chain.shard.close()
+    finally:
+        if own:
+            dist.destroy_process_group()
