@@ -1361,6 +1361,10 @@ __global__ void __launch_bounds__(RD_NT) reduce1_kernel(const double *h, const d
   __shared__ double s_red[RD_NT / 32][RD_NV];
   DevParams P = {0, 0, 0, 1, 1};
   if (mode == 0) P = *prm;
+  if (mode == 2) {  // statistics shifted by the parameters held on the device
+    c_mu = prm->mu;
+    c_xi = prm->xi;
+  }
   double v[RD_NV] = {0, 0, 0, 0, 0, 0};
   const int64_t i0 = ((int64_t)blockIdx.x * RD_NT + threadIdx.x) * RD_R;
   for (int r = 0; r < RD_R; r++) {
@@ -1419,6 +1423,7 @@ __global__ void __launch_bounds__(RD_NT) reduce2_kernel(const double *partials, 
   }
   if (threadIdx.x) return;
   const double *t = s_v[0];
+  if (mode == 2) c_mu = prm->mu;
   if (mode == 0) {
     const DevParams P = *prm;
     const double Td = (double)T;
@@ -1442,6 +1447,14 @@ int launch_energy(const double *h, const double *p, const double *y, const doubl
   const int nb = reduce_partials_count(T);
   reduce1_kernel<<<nb, RD_NT, 0, s>>>(h, p, y, lrv, prm, T, 0.0, 0.0, 0, partials);
   reduce2_kernel<<<1, RD_NT, 0, s>>>(partials, nb, h, prm, T, 0.0, 0, out);
+  *launches += 2;
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+int launch_suff_stats_dev(const double *h, const double *lrv, int64_t T, const DevParams *prm, double *partials,
+                          double *out, cudaStream_t s, int *launches) {
+  const int nb = reduce_partials_count(T);
+  reduce1_kernel<<<nb, RD_NT, 0, s>>>(h, nullptr, nullptr, lrv, prm, T, 0.0, 0.0, 2, partials);
+  reduce2_kernel<<<1, RD_NT, 0, s>>>(partials, nb, h, prm, T, 0.0, 2, out);
   *launches += 2;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

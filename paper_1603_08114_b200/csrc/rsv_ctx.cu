@@ -104,6 +104,7 @@ struct rsv_ctx {
   int max_tiles = 0;
   double *rpart = nullptr;  // reduction partials
   double *rout = nullptr;   // reduction outputs (8 doubles)
+  double *fb = nullptr;     // long-trajectory fallback: energies and statistics (24 doubles)
   int32_t *dflag = nullptr;
   int32_t *ring_count = nullptr;
   DevResult *ring = nullptr;
@@ -131,6 +132,7 @@ struct rsv_ctx {
     TrajArgs args;
     double dt;
     std::vector<cudaGraphNode_t> ev;  // timing event-record nodes
+    int launches = 0;                 // kernels per launch of the graph
   };
   std::map<GraphKey, Cached *> graphs;
   int timing = 0;  // 0 off, 1 per-proposal total, 2 with momenta / trajectory breakdown
@@ -211,7 +213,7 @@ int rsv_destroy(rsv_ctx *c) {
   for (auto e : c->evpool) cudaEventDestroy(e);
   void *dev[] = {c->hbuf[0], c->hbuf[1], c->y, c->a, c->lrv, c->normals, c->sh, c->sp, c->sh2, c->sp2,
                  c->zscratch, c->sfc_words, c->sfc_snaps, c->parts, c->rpart, c->rout, c->dflag, c->ring_count,
-                 c->ring, c->ctrl, c->prm, c->pl[0], c->pl[1], c->pl[2], c->pl[3], c->bjump};
+                 c->ring, c->ctrl, c->prm, c->pl[0], c->pl[1], c->pl[2], c->pl[3], c->bjump, c->fb};
   for (void *p : dev)
     if (p) cudaFree(p);
   void *host[] = {c->h_ctrl, c->h_prm, c->h_out, c->h_flag, c->h_ring};
@@ -265,6 +267,7 @@ static int create_impl(rsv_ctx *c, int device, int64_t T, int64_t Tg) {
   CK(cudaMalloc(&c->parts, sizeof(TilePart) * c->max_tiles));
   CK(cudaMalloc(&c->rpart, sizeof(double) * 8 * (reduce_partials_count(T) + 1)));
   CK(cudaMalloc(&c->rout, sizeof(double) * 8));
+  CK(cudaMalloc(&c->fb, sizeof(double) * 24));
   CK(cudaMalloc(&c->dflag, sizeof(int32_t)));
   CK(cudaMalloc(&c->ring_count, sizeof(int32_t)));
   CK(cudaMemset(c->ring_count, 0, sizeof(int32_t)));
@@ -550,6 +553,75 @@ static int ensure_events(rsv_ctx *c, size_t n) {
   return 0;
 }
 
+// ---- trajectories longer than a tile's halo allows (L > ~360 at 256
+// threads): the proposal as streamed elementary steps (the reference's
+// K1-K2-K3 grouping, integrator.py:139-146), H by the deterministic
+// reductions, and a one-thread Metropolis step (sampler.py:155-167).  Every
+// parameter is read from device memory, so device-side theta updates work too.
+__global__ void fb_take_current_kernel(const DevControl *C, const double *h0, const double *h1, double *dst,
+                                       int64_t T) {
+  const double *src = C->cur ? h1 : h0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void fb_put_proposal_kernel(const DevControl *C, const double *src, double *h0, double *h1, int64_t T) {
+  double *dst = C->cur ? h0 : h1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__device__ void shard_advance(DevControl *C, int drew, const uint64_t *snaps);
+// e: [0..1] old {kinetic, log f}, [2..3] new, [4..10] old statistics, [11..17] new statistics
+__global__ void fb_metropolis_kernel(DevControl *C, const double *e, const int32_t *flag, const uint64_t *snaps,
+                                     int stats) {
+  if (threadIdx.x || blockIdx.x) return;
+  DevResult r;
+  r.h_old = e[0] - e[1];
+  r.h_new = e[2] - e[3];
+  r.accept = 0;
+  r.u = __longlong_as_double(0x7ff8000000000000LL);
+  const double dh = r.h_new - r.h_old;
+  bool drew = false;
+  if (*flag || !isfinite(dh) || fabs(dh) > 1000.0) {
+    r.diverged = 1;
+    r.delta_h = __longlong_as_double(0x7ff0000000000000LL);
+  } else {
+    r.diverged = 0;
+    r.delta_h = dh;
+    r.u = u01(C->u_word);
+    drew = true;
+    r.accept = (dh <= 0.0) || (r.u < exp(-dh));
+  }
+  r.words_used = C->zig_used + (drew ? 1 : 0);
+  shard_advance(C, drew, snaps);
+  if (r.accept) C->cur ^= 1;
+  if (stats)
+    for (int k = 0; k < 7; k++) C->stats[k] = r.accept ? e[11 + k] : e[4 + k];
+  C->res = r;
+}
+
+static bool enqueue_fallback(rsv_ctx *c, double dt, int n_steps, int stats, int *l) {
+  bool ok = cudaMemsetAsync(c->dflag, 0, sizeof(int32_t), c->stream) == cudaSuccess;
+  const unsigned nb = (unsigned)((c->T + 255) / 256 < 4096 ? (c->T + 255) / 256 : 4096);
+  fb_take_current_kernel<<<nb, 256, 0, c->stream>>>(c->ctrl, c->hbuf[0], c->hbuf[1], c->sh, c->T);
+  ok &= launch_energy(c->sh, c->normals, c->y, c->lrv, c->prm, c->T, c->rpart, c->fb + 0, c->stream, l) == 0;
+  if (stats) ok &= launch_suff_stats_dev(c->sh, c->lrv, c->T, c->prm, c->rpart, c->fb + 4, c->stream, l) == 0;
+  const double *hin = c->sh, *pin = c->normals;
+  double *ho = c->sh2, *po = c->sp2;
+  for (int k = 0; k < n_steps; k++) {
+    ok &= launch_elementary_step(hin, pin, ho, po, c->a, c->lrv, c->prm, dt, c->T, c->dflag, c->stream, l) == 0;
+    hin = ho;
+    pin = po;
+    ho = (ho == c->sh2) ? c->sh : c->sh2;
+    po = (po == c->sp2) ? c->sp : c->sp2;
+  }
+  ok &= launch_energy(hin, pin, c->y, c->lrv, c->prm, c->T, c->rpart, c->fb + 2, c->stream, l) == 0;
+  if (stats) ok &= launch_suff_stats_dev(hin, c->lrv, c->T, c->prm, c->rpart, c->fb + 11, c->stream, l) == 0;
+  fb_put_proposal_kernel<<<nb, 256, 0, c->stream>>>(c->ctrl, hin, c->hbuf[0], c->hbuf[1], c->T);
+  fb_metropolis_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, c->fb, c->dflag, c->sfc_snaps, stats);
+  *l += 3;
+  return ok && cudaGetLastError() == cudaSuccess;
+}
+
 // Capture one proposal into a graph.  With timing, 4 event-record nodes
 // (start, trajectory begin, trajectory end, end) are added; their events are
 // re-pointed per launch with cudaGraphExecEventRecordNodeSetEvent.
@@ -557,8 +629,8 @@ static bool variant_is_persistent(int v) { return v >= 9; }
 
 static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   const TrajGeom g = traj_geometry(c->T, k.n_steps, c->sm_count, c->variant);
-  if (!g.ok) return fail(c, RSV_E_INVALID, "n_steps=%d too large for one trajectory tile", k.n_steps);
-  if (g.n_tiles > c->max_tiles) return fail(c, RSV_E_CUDA, "tile count %d exceeds buffer", g.n_tiles);
+  if (!g.ok && c->shard) return fail(c, RSV_E_INVALID, "n_steps=%d too large for a sharded trajectory", k.n_steps);
+  if (g.ok && g.n_tiles > c->max_tiles) return fail(c, RSV_E_CUDA, "tile count %d exceeds buffer", g.n_tiles);
   int r;
   if ((r = ensure_events(c, 4))) return r;
   auto *cg = new rsv_ctx::Cached();
@@ -575,7 +647,8 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   if (k.timing) cudaEventRecordWithFlags(c->evpool[0], c->stream, cudaEventRecordExternal);
   ok &= launch_momenta(mbufs(c), k.kind, c->Tg, c->stream, &l) == 0;
   if (k.timing) cudaEventRecordWithFlags(c->evpool[1], c->stream, cudaEventRecordExternal);
-  ok &= launch_trajectory(cg->args, c->stream, &l) == 0;
+  if (g.ok) ok &= launch_trajectory(cg->args, c->stream, &l) == 0;
+  else ok &= enqueue_fallback(c, k.dt, k.n_steps, k.stats, &l);
   if (k.timing) cudaEventRecordWithFlags(c->evpool[2], c->stream, cudaEventRecordExternal);
   if (k.timing) cudaEventRecordWithFlags(c->evpool[3], c->stream, cudaEventRecordExternal);
   cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
@@ -588,8 +661,9 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   CK(cudaGraphGetNodes(graph, nullptr, &n));
   std::vector<cudaGraphNode_t> nodes(n);
   CK(cudaGraphGetNodes(graph, nodes.data(), &n));
-  const void *fn = traj_kernel_fn(g.variant, k.fuse, k.stats);
+  const void *fn = g.ok ? traj_kernel_fn(g.variant, k.fuse, k.stats) : nullptr;
   cg->traj_node = nullptr;
+  cg->launches = l;
   cg->ev.assign(4, nullptr);
   for (auto nd : nodes) {
     cudaGraphNodeType t;
@@ -597,7 +671,7 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
     if (t == cudaGraphNodeTypeKernel) {
       cudaKernelNodeParams kp;
       CK(cudaGraphKernelNodeGetParams(nd, &kp));
-      if (kp.func == fn) {
+      if (fn && kp.func == fn) {
         cg->traj_node = nd;
         cg->traj_params = kp;
       }
@@ -608,7 +682,7 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
         if (ev == c->evpool[i]) cg->ev[i] = nd;
     }
   }
-  if (!cg->traj_node) return fail(c, RSV_E_CUDA, "trajectory node not found in the captured graph");
+  if (g.ok && !cg->traj_node) return fail(c, RSV_E_CUDA, "trajectory node not found in the captured graph");
   if (k.timing)
     for (int i = 0; i < 4; i++)
       if (!cg->ev[i]) return fail(c, RSV_E_CUDA, "timing graph: event node %d not found", i);
@@ -628,7 +702,7 @@ static int get_graph(rsv_ctx *c, double dt, int n_steps, int fuse, int stats, rs
     it = c->graphs.emplace(k, cg).first;
   }
   *out = it->second;
-  *kernels = (c->kind == PRNG_SFC64 ? 3 : 2) + 1;
+  *kernels = it->second->launches;
   return 0;
 }
 
@@ -1560,9 +1634,10 @@ int rsv_run_chain(rsv_ctx *c, double dt, int n_steps, int fuse, const rsv_prior 
   // one sweep = one graph: momenta, trajectory (+ statistics, device theta
   // constants), theta draws.  Not cached (the prior is baked in).
   const TrajGeom g = traj_geometry(c->T, n_steps, c->sm_count, c->variant < 0 ? -1 : c->variant);
-  if (!g.ok) return fail(c, RSV_E_INVALID, "n_steps=%d too large for one trajectory tile", n_steps);
-  if (g.variant < 11 || g.variant > 14) return fail(c, RSV_E_STATE, "device run_chain needs a persistent shape");
-  TrajArgs ta = traj_args(c, dt, n_steps, fuse, g);
+  // longer trajectories than a tile holds run as streamed elementary steps
+  if (g.ok && (g.variant < 11 || g.variant > 14))
+    return fail(c, RSV_E_STATE, "device run_chain needs a persistent shape");
+  TrajArgs ta = g.ok ? traj_args(c, dt, n_steps, fuse, g) : TrajArgs{};
   ta.stats = 1;
   ta.kdev = c->kdev;
   ta.pdl = 1;
@@ -1578,7 +1653,8 @@ int rsv_run_chain(rsv_ctx *c, double dt, int n_steps, int fuse, const rsv_prior 
     l = 0;
     for (int k = 0; k < (gi == 0 ? KS : 1); k++) {
       ok &= launch_momenta(mbufs(c), c->kind, c->Tg, c->stream, &l) == 0;
-      ok &= launch_trajectory(ta, c->stream, &l) == 0;
+      if (g.ok) ok &= launch_trajectory(ta, c->stream, &l) == 0;
+      else ok &= enqueue_fallback(c, dt, n_steps, 1, &l);
       ok &= launch_theta_sweep(c->ctrl, c->prm, c->kdev, c->run, pr, dt, c->T, c->sfc_snaps, c->stream, &l) == 0;
     }
     cudaError_t e = cudaStreamEndCapture(c->stream, &graph[gi]);
@@ -1764,7 +1840,7 @@ static int ens_graph(rsv_ctx *c, double dt, int n_steps, int fuse, rsv_ctx::Cach
     if (t == cudaGraphNodeTypeKernel) {
       cudaKernelNodeParams kp;
       CK(cudaGraphKernelNodeGetParams(nd, &kp));
-      if (kp.func == fn) {
+      if (fn && kp.func == fn) {
         cg->traj_node = nd;
         cg->traj_params = kp;
       }

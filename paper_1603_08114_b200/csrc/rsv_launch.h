@@ -154,6 +154,9 @@ int launch_energy(const double *h, const double *p, const double *y, const doubl
 int launch_suff_stats(const double *h, const double *lrv, int64_t T, double c_mu, double c_xi, double *partials,
                       double *out, cudaStream_t s, int *launches);
 int reduce_partials_count(int64_t T);
+// statistics shifted by the device-held parameters (mu, xi)
+int launch_suff_stats_dev(const double *h, const double *lrv, int64_t T, const DevParams *prm, double *partials,
+                          double *out, cudaStream_t s, int *launches);
 
 // one Gibbs sweep's theta draws on the device (sampler.py:170-272, run_chain
 // :327-344) after a proposal: updates *prm and *kdev, stores the sample

@@ -240,6 +240,42 @@ def test_long_trajectory_streamed_fallback(backend):
     assert _rel(fin.h, hh) <= 1e-11
 
 
+@pytest.mark.parametrize("kind,seed", [("pcg32", 2), ("sfc64", 7)])
+def test_long_trajectory_hmc_proposals_vs_oracle(backend, kind, seed):
+    # L beyond a tile's halo budget: the proposal graph streams the steps
+    # (momenta, energies, L step kernels, Metropolis) -- same draws and decisions
+    T = 3000
+    truth = P.simulate_rsv(THETA, T, seed=2)
+    data = truth.dataset
+    md = P.MDConfig(0.003, 500)
+    rng = P.make_rng(seed, kind)
+    st = O.Stream(kind, seed)
+    h_gpu = truth.latent.copy()
+    h_orc = truth.latent.copy()
+    H = abs(O.hamiltonian(h_orc, np.zeros(T), THETA, data.returns, data.log_rv)) + T
+    n_acc = 0
+    for i in range(5):
+        h_gpu, acc, dh = P.hmc_update_volatility(h_gpu, THETA, data, md, rng, backend=backend)
+        h_orc, acc_o, dh_o = O.hmc_update(h_orc, THETA, data.returns, data.log_rv, md.step_size, md.n_steps, st)
+        assert acc == acc_o, i
+        assert abs(dh - dh_o) <= 1e-12 * H, (i, dh, dh_o)
+        assert _rel(h_gpu, h_orc) <= 1e-10, i
+        n_acc += acc
+    assert n_acc >= 1
+    assert int(rng.bit_generator.random_raw()) == int(st.raw(1)[0])   # both streams at the same word
+
+
+def test_long_trajectory_run_chain_device_equals_host(backend):
+    T = 2000
+    truth = P.simulate_rsv(THETA, T, seed=8)
+    cfg = P.SamplerConfig(seed=3, md=P.MDConfig(0.004, 420), n_burnin=2, n_samples=6, thin=1, prng="minstd")
+    a = P.run_chain(truth.dataset, cfg, backend=backend, theta_on="host")
+    b = P.run_chain(truth.dataset, cfg, backend=backend, theta_on="device")
+    assert np.array_equal(a.accept, b.accept) and a.accept.any()
+    for name in ("phi", "mu", "xi", "sigma_eta_sq", "sigma_u_sq"):
+        assert np.allclose(getattr(a, name), getattr(b, name), rtol=1e-11, atol=1e-13), name
+
+
 # ---------------------------------------------------------------- kernel-level plug-in
 def test_backend_run_protocol_matches_reference_kernels(backend):
     z, data = _data_T2000()
