@@ -412,9 +412,11 @@ def main():
         h, acc, _ = P.hmc_update_volatility(h, theta, data, md, rng, backend=be)
         n_acc += int(acc)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
+    zero_copy = be.chain(data, theta).last_update_zero_copy  # h read in place by the trajectory kernel
     state_bytes = 48 + 40  # stream state + params structs
     e2e = {"value": T * L / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * T + state_bytes,
            "d2h_bytes_per_step": int(8 * T * n_acc / e2e_steps) + 48 + 56,
+           "h_in": "read in place over PCIe by the trajectory kernel (zero copy)" if zero_copy else "copied in",
            "path": "paper_1603_08114_b200.hmc_update_volatility(h numpy[pinned], params, data, md, rng) -> C ABI"}
 
     extra = {}

@@ -101,10 +101,14 @@ int rsv_hmc_update(rsv_ctx *ctx, double step_size, int n_steps, int fuse, rsv_re
 /* sampler.py:144-167 in one call from host memory (the reference-facing
  * fast path of hmc_update_volatility): h_in (T doubles) and *stream in; when
  * the proposal is accepted it is written to h_out (otherwise h_out is left
- * untouched: the kept path is h_in); *stream advanced; one synchronisation
- * (two when accepted).  The theta statistics are not evaluated. */
+ * untouched: the kept path is h_in); *stream advanced.  The theta statistics
+ * are not evaluated.  When T >= 2^16, T % 8 == 0 and h_in is page-locked and
+ * 16-byte aligned, the trajectory kernel reads h_in in place over PCIe
+ * (zero copy, overlapped with its tiles) instead of one copy in ahead of the
+ * proposal; rsv_last_update_zero_copy tells which way the last call went. */
 int rsv_hmc_update_host(rsv_ctx *ctx, const double *h_in, double *h_out, rsv_prng_state *stream, double step_size,
                         int n_steps, int fuse, rsv_result *out);
+int rsv_last_update_zero_copy(const rsv_ctx *ctx);
 /* n back-to-back proposals with fixed params (one CUDA graph per proposal,
  * no host round trip in between); results (n entries) optional.  Like the
  * reference's hmc_update_volatility these proposals do not evaluate the theta

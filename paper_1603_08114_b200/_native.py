@@ -99,6 +99,7 @@ _SIGS = {
     "rsv_get_timing": (ctypes.c_int, [_CTX, _D, _D, _D]),
     "rsv_launch_count": (ctypes.c_int64, [_CTX]),
     "rsv_kernel_stamps": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
+    "rsv_last_update_zero_copy": (ctypes.c_int, [_CTX]),
     "rsv_hmc_update_host": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                            ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     "rsv_run_chain": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,

@@ -31,11 +31,16 @@ namespace {
 struct GraphKey {
   int kind, n_steps, fuse, timing, stats;
   double dt;
+  int zc = 0;  // zero-copy input (rsv_hmc_update_host): the trajectory reads h from host memory
   bool operator<(const GraphKey &o) const {
-    return std::tie(kind, n_steps, fuse, timing, stats, dt) <
-           std::tie(o.kind, o.n_steps, o.fuse, o.timing, o.stats, o.dt);
+    return std::tie(kind, n_steps, fuse, timing, stats, dt, zc) <
+           std::tie(o.kind, o.n_steps, o.fuse, o.timing, o.stats, o.dt, o.zc);
   }
 };
+
+// rsv_hmc_update_host reads a page-locked path in place from this length on
+// (below it one copy in is as fast)
+constexpr int64_t ZC_MIN_T = 1 << 16;
 
 __global__ void prep_data_kernel(const double *y, double *a, int64_t T) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -105,6 +110,7 @@ struct rsv_ctx {
   double *rpart = nullptr;  // reduction partials
   double *rout = nullptr;   // reduction outputs (8 doubles)
   double *fb = nullptr;     // long-trajectory fallback: energies and statistics (24 doubles)
+  int zc_last = 0;  // the last rsv_hmc_update_host read h_in in place
   int32_t *dflag = nullptr;
   int32_t *ring_count = nullptr;
   DevResult *ring = nullptr;
@@ -637,6 +643,10 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   cg->dt = k.dt;
   cg->args = traj_args(c, k.dt, k.n_steps, k.fuse, g);
   cg->args.stats = k.stats;
+  if (k.zc && g.ok) {  // h_src is re-pointed at the caller's page-locked path per call
+    cg->args.h_src = c->hbuf[0];
+    cg->args.h_dst = c->hbuf[1];
+  }
   // programmatic dependent launch of the trajectory after the momenta kernel
   // (not with timing event nodes between them)
   cg->args.pdl = (k.timing == 0 && variant_is_persistent(g.variant) && !getenv("RSV_NO_PDL")) ? 1 : 0;
@@ -692,8 +702,8 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
 }
 
 static int get_graph(rsv_ctx *c, double dt, int n_steps, int fuse, int stats, rsv_ctx::Cached **out,
-                     int *kernels) {
-  GraphKey k{c->kind, n_steps, fuse ? 1 : 0, c->timing == 2 ? 1 : 0, stats ? 1 : 0, dt};
+                     int *kernels, int zc = 0) {
+  GraphKey k{c->kind, n_steps, fuse ? 1 : 0, c->timing == 2 ? 1 : 0, stats ? 1 : 0, dt, zc};
   auto it = c->graphs.find(k);
   if (it == c->graphs.end()) {
     rsv_ctx::Cached *cg = nullptr;
@@ -837,16 +847,46 @@ int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_
   CK(cudaMemcpyAsync(&c->ctrl->stream, &c->h_ctrl->stream, sizeof(StreamState), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(&c->ctrl->seq_state, &c->h_ctrl->seq_state, sizeof(uint64_t), cudaMemcpyHostToDevice,
                      c->stream));
-  CK(cudaMemcpyAsync(c->hbuf[0], h_in, sizeof(double) * c->T, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(&c->ctrl->cur, 0, sizeof(int32_t), c->stream));
   CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
   c->has_latent = true;
-  rsv_ctx::Cached *cg = nullptr;
-  int kpl = 0;
-  if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl))) return r;
-  CK(cudaGraphLaunch(cg->exec, c->stream));
-  c->launches += kpl;
-  if ((r = pull_ctrl(c)) || (r = check_err_bits(c))) return r;
+  const TrajGeom g = traj_geometry(c->T, n_steps, c->sm_count, c->variant);
+  // zero copy: the trajectory kernel's tile staging (bulk copies) reads the
+  // caller's page-locked path over PCIe itself, overlapped with the tiles,
+  // instead of one copy in ahead of the proposal; arrays padded to T % 8 == 0
+  // only (the staging reads whole 8-site groups)
+  const void *h_map = nullptr;
+  if (g.ok && c->T >= ZC_MIN_T && c->T % 8 == 0 && ((uintptr_t)h_in & 15) == 0 && c->timing == 0 &&
+      !getenv("RSV_NO_ZERO_COPY")) {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, h_in) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      h_map = pa.devicePointer;
+    cudaGetLastError();
+  }
+  c->zc_last = h_map ? 1 : 0;
+  if (h_map) {
+    rsv_ctx::Cached *cg = nullptr;
+    int kpl = 0;
+    if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl, 2))) return r;
+    cg->args.h_src = (const double *)h_map;
+    void *kp[] = {&cg->args};
+    cudaKernelNodeParams np = cg->traj_params;
+    np.kernelParams = kp;
+    CK(cudaGraphExecKernelNodeSetParams(cg->exec, cg->traj_node, &np));
+    CK(cudaGraphLaunch(cg->exec, c->stream));
+    c->launches += kpl;
+    if ((r = pull_ctrl(c))) return r;
+    c->has_latent = c->h_ctrl->res.accept != 0;  // on a reject the device holds no copy of h_in
+  } else {
+    CK(cudaMemcpyAsync(c->hbuf[0], h_in, sizeof(double) * c->T, cudaMemcpyHostToDevice, c->stream));
+    rsv_ctx::Cached *cg = nullptr;
+    int kpl = 0;
+    if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl))) return r;
+    CK(cudaGraphLaunch(cg->exec, c->stream));
+    c->launches += kpl;
+    if ((r = pull_ctrl(c))) return r;
+  }
+  if ((r = check_err_bits(c))) return r;
   to_result(c->h_ctrl->res, out);
   st->pos = c->h_ctrl->stream.pos;
   for (int i = 0; i < 4; i++) st->s[i] = c->h_ctrl->stream.s[i];
@@ -857,6 +897,8 @@ int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_
   }
   return 0;  // rejected or divergent: the kept path is h_in, h_out is not written
 }
+
+int rsv_last_update_zero_copy(const rsv_ctx *c) { return c ? c->zc_last : 0; }
 
 int rsv_last_stats(rsv_ctx *c, double out[7]) {
   if (!c || !out) return fail(c, RSV_E_INVALID, "null argument");

@@ -203,6 +203,11 @@ class DeviceChain:
                                                float(step_size), int(n_steps), int(bool(fuse)), ctypes.byref(r)))
         return r, (out if r.accept else None)
 
+    @property
+    def last_update_zero_copy(self) -> bool:
+        """The last hmc_update_host read the (page-locked) path in place."""
+        return bool(self._lib.rsv_last_update_zero_copy(self.ctx))
+
     def hmc_update_many(self, step_size: float, n_steps: int, n: int, fuse: bool = False,
                         results: bool = True):
         out = (N.Result * n)() if results else None

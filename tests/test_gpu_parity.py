@@ -145,6 +145,39 @@ def test_hmc_sequence_vs_reference(backend, kind, seed):
     assert _rel(h, g["h_last"]) <= 1e-10
 
 
+@pytest.mark.parametrize("T,kind,pinned", [(300008, "pcg32", True), (1 << 17, "sfc64", True),
+                                           (300007, "philox", True), (1 << 17, "pcg32", False)])
+def test_zero_copy_host_proposals_vs_oracle(backend, T, kind, pinned):
+    # from T = 2^16 a page-locked path (T % 8 == 0) is read in place by the
+    # trajectory kernel: same decisions, stream positions and paths as the
+    # oracle (and as the copy-in path for pageable or ragged inputs)
+    import torch
+    truth = P.simulate_rsv(THETA, T, seed=11)
+    data = truth.dataset
+    md = P.MDConfig(0.02, 20)
+    rng = P.make_rng(4, kind)
+    st = O.Stream(kind, 4)
+    if pinned:
+        h_gpu = torch.empty(T, dtype=torch.float64, pin_memory=True).numpy()
+        h_gpu[:] = truth.latent
+    else:
+        h_gpu = truth.latent.copy()
+    h_orc = truth.latent.copy()
+    H = abs(O.hamiltonian(h_orc, np.zeros(T), THETA, data.returns, data.log_rv)) + T
+    accs = []
+    for i in range(4):
+        was_pinned = pinned or any(accs)   # an accepted path comes back page-locked
+        h_gpu, acc, dh = P.hmc_update_volatility(h_gpu, THETA, data, md, rng, backend=backend)
+        assert backend.chain(data, THETA).last_update_zero_copy == (was_pinned and T % 8 == 0), i
+        h_orc, acc_o, dh_o = O.hmc_update(h_orc, THETA, data.returns, data.log_rv, md.step_size, md.n_steps, st,
+                                          nthreads=O.max_threads())
+        assert acc == acc_o and abs(dh - dh_o) <= 1e-13 * H, (i, dh, dh_o)
+        assert _rel(h_gpu, h_orc) <= 1e-10, i
+        accs.append(acc)
+    assert int(rng.bit_generator.random_raw()) == int(st.raw(1)[0])
+    assert any(accs)
+
+
 def test_hmc_divergent_sentinel(backend):
     g = golden("hmc_divergent.npz")
     data = P.Dataset.from_log_rv(g["y"], g["lrv"])
