@@ -811,6 +811,15 @@ int launch_momenta_ens(EnsChain *ens, double *normals, int64_t Tc, int n_chains,
 // Marsaglia-Tsang gamma), every product / quotient rounded like the host's
 // Python floats (no contraction).  Only exp / log differ from glibc (<= 1 ulp):
 // a draw flips only if a uniform lands within an ulp of its threshold.
+// The theta kernel is one long sequential chain executed by a single
+// thread: its time is instruction-fetch latency, not arithmetic, so the
+// generator, the ziggurat, log1p and the gamma sampler are out-of-line
+// functions (one copy of each stays hot in the instruction cache) instead of
+// being inlined at every call site.
+__device__ __noinline__ double log1p_ool(double x) { return glibc_log1p(x); }
+__device__ __noinline__ double log_ool(double x) { return log(x); }
+__device__ __noinline__ double exp_ool(double x) { return exp(x); }
+
 struct ThetaGen {
   int kind;
   SeqGen g;
@@ -818,12 +827,12 @@ struct ThetaGen {
   uint64_t used;
   const uint64_t *ki;  // ziggurat tables (shared-memory copies)
   const double *wi, *fi;
-  __device__ uint64_t next() {
+  __device__ __noinline__ uint64_t next() {
     used++;
     return kind == PRNG_SFC64 ? sfc64_next(s) : g.next();
   }
   __device__ double next_double() { return u01(next()); }
-  __device__ double normal() {  // numpy random_standard_normal
+  __device__ __noinline__ double normal() {  // numpy random_standard_normal
     for (;;) {
       uint64_t r = next();
       const int idx = (int)(r & 0xff);
@@ -835,19 +844,19 @@ struct ThetaGen {
       if (rabs < ki[idx]) return x;
       if (idx == 0) {
         for (;;) {
-          const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, glibc_log1p(-next_double()));
-          const double yy = -glibc_log1p(-next_double());
+          const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, log1p_ool(-next_double()));
+          const double yy = -log1p_ool(-next_double());
           if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx))
             return ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
         }
       }
       const double u = next_double();
       if (__dadd_rn(__dmul_rn(__dsub_rn(fi[idx - 1], fi[idx]), u), fi[idx]) <
-          exp(__dmul_rn(__dmul_rn(-0.5, x), x)))
+          exp_ool(__dmul_rn(__dmul_rn(-0.5, x), x)))
         return x;
     }
   }
-  __device__ double gamma(double shape) {  // numpy random_standard_gamma, shape > 1
+  __device__ __noinline__ double gamma(double shape) {  // numpy random_standard_gamma, shape > 1
     const double b = __dsub_rn(shape, 1.0 / 3.0);
     const double c = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(9.0, b)));
     for (;;) {
@@ -860,7 +869,7 @@ struct ThetaGen {
       const double U = next_double();
       const double X2 = __dmul_rn(X, X);
       if (U < __dsub_rn(1.0, __dmul_rn(__dmul_rn(0.0331, X2), X2))) return __dmul_rn(b, V);
-      if (log(U) < __dadd_rn(__dmul_rn(0.5, X2), __dmul_rn(b, __dadd_rn(__dsub_rn(1.0, V), log(V)))))
+      if (log_ool(U) < __dadd_rn(__dmul_rn(0.5, X2), __dmul_rn(b, __dadd_rn(__dsub_rn(1.0, V), log_ool(V)))))
         return __dmul_rn(b, V);
     }
   }
@@ -885,12 +894,12 @@ __device__ Recentred recentre(const double *st, double Td, double c, double mu) 
 }
 
 __device__ double phi_log_ratio(double prop, double phi, double h1_sq, double se2, const DevPrior &pr) {
-  const double a = __dmul_rn(0.5, __dsub_rn(glibc_log1p(-__dmul_rn(prop, prop)), glibc_log1p(-__dmul_rn(phi, phi))));
+  const double a = __dmul_rn(0.5, __dsub_rn(log1p_ool(-__dmul_rn(prop, prop)), log1p_ool(-__dmul_rn(phi, phi))));
   const double b = __ddiv_rn(__dmul_rn(h1_sq, __dsub_rn(__dsub_rn(1.0, __dmul_rn(prop, prop)),
                                                         __dsub_rn(1.0, __dmul_rn(phi, phi)))),
                              __dmul_rn(2.0, se2));
-  const double c = __dmul_rn(__dsub_rn(pr.phi_a, 1.0), __dsub_rn(glibc_log1p(prop), glibc_log1p(phi)));
-  const double d = __dmul_rn(__dsub_rn(pr.phi_b, 1.0), __dsub_rn(glibc_log1p(-prop), glibc_log1p(-phi)));
+  const double c = __dmul_rn(__dsub_rn(pr.phi_a, 1.0), __dsub_rn(log1p_ool(prop), log1p_ool(phi)));
+  const double d = __dmul_rn(__dsub_rn(pr.phi_b, 1.0), __dsub_rn(log1p_ool(-prop), log1p_ool(-phi)));
   return __dadd_rn(__dadd_rn(__dsub_rn(a, b), c), d);
 }
 
@@ -974,7 +983,7 @@ __global__ void __launch_bounds__(TH_NT) theta_sweep_kernel(DevControl *C, DevPa
     if (-1.0 < prop && prop < 1.0) {
       const double lr = phi_log_ratio(prop, phi, __dmul_rn(r.d0n, r.d0n), se2, pr);
       const double u = G.next_double();
-      if (lr >= 0.0 || u < exp(lr)) phi = prop;
+      if (lr >= 0.0 || u < exp_ool(lr)) phi = prop;
     }
   }
   // update_sigma_eta_sq (sampler.py:218-230)
@@ -1021,9 +1030,10 @@ __global__ void __launch_bounds__(TH_NT) theta_sweep_kernel(DevControl *C, DevPa
   q.phi = phi; q.mu = mu; q.xi = xi; q.se2 = se2; q.su2 = su2;
   q.inv_su2 = 1.0 / su2;
   q.inv_se2 = 1.0 / se2;
-  q.emu = exp(-mu);
+  q.emu = exp_ool(-mu);
   q.one_m_phi2 = 1.0 - phi * phi;
-  q.hconst = 0.5 * Td * mu + 0.5 * Td * log(su2) + 0.5 * log(se2 / (1.0 - phi * phi)) + 0.5 * Tm1 * log(se2);
+  q.hconst = 0.5 * Td * mu + 0.5 * Td * log_ool(su2) + 0.5 * log_ool(se2 / (1.0 - phi * phi)) +
+             0.5 * Tm1 * log_ool(se2);
   q.n_lo = (int32_t)floor((mu - 50.0) * RSV_INV_LN2_N);
   q.n_span = (int32_t)ceil((mu + 50.0) * RSV_INV_LN2_N) - q.n_lo;
   *P = q;
