@@ -403,33 +403,37 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
     uint64_t accum = 0;
     if (lane == 0) vst[b] = zpack(b == 0 ? 2 : 1, bexit, S.epoch, (uint64_t)btot);
     if (coresident) {
-      // the CTA that publishes last raises the draw's flag; after it, every
-      // count is in place and one round of independent loads sums the
-      // predecessors (no re-polling of hundreds of status words)
-      const unsigned tag = 0x80000000u | S.epoch;
-      unsigned pub = 0;
-      if (lane == 0) {
-        __threadfence();
-        pub = atomicAdd(&ctrl->zig_pub, 1u);
-        if (pub == gridDim.x - 1) {
-          __threadfence();
-          atomicExch(&ctrl->zig_flag, tag);
-        }
-      }
+      // every CTA counts itself into zig_pub with a release reduction after
+      // its status word; once the count reaches the grid size (acquire poll)
+      // every status word is in place and one round of independent loads sums
+      // the predecessors.  The CTA that finishes last resets zig_pub.
+      if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctrl->zig_pub) : "memory");
       bool flag = false;
       for (int it = 0; it < 4096 && !flag; it++) {
-        const unsigned f = lane == 0 ? *(volatile unsigned *)&ctrl->zig_flag : 0u;
-        flag = __shfl_sync(0xffffffffu, f, 0) == tag;
+        unsigned f = 0;
+        if (lane == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(&ctrl->zig_pub) : "memory");
+        flag = __shfl_sync(0xffffffffu, f, 0) == gridDim.x;
         if (!flag) __nanosleep(32);
       }
       if (flag) {
-        __threadfence();
+        __syncwarp();  // the other lanes' loads follow lane 0's acquire
         uint64_t part = 0;
         bool ok = true;
-        for (int j = lane; j < b; j += 32) {
-          const uint64_t v = __ldcg(reinterpret_cast<const unsigned long long *>(status) + j);
-          ok &= zready(v, S.epoch);
-          part += v & ZCNT;
+        // 8 independent loads per lane per round: the L2 latency is paid once
+        // per 256 predecessors, not once per 32
+        for (int base = 0; base < b; base += 256) {
+          uint64_t v[8];
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            const int j = base + lane + 32 * q;
+            v[q] = j < b ? __ldcg(reinterpret_cast<const unsigned long long *>(status) + j)
+                         : (uint64_t)S.epoch << 34 | 2ULL << 62;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            ok &= zready(v[q], S.epoch);
+            part += base + lane + 32 * q < b ? (v[q] & ZCNT) : 0;
+          }
         }
         if (__all_sync(0xffffffffu, ok)) {
 #pragma unroll
@@ -447,10 +451,18 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
         for (;;) {
           uint64_t part = 0;
           bool ok = true;
-          for (int j = lane; j < b; j += 32) {
-            const uint64_t v = vst[j];
-            ok &= zready(v, S.epoch);
-            part += v & ZCNT;
+          for (int base = 0; base < b; base += 256) {
+            uint64_t v[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+              const int j = base + lane + 32 * q;
+              v[q] = j < b ? vst[j] : (uint64_t)S.epoch << 34 | 2ULL << 62;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+              ok &= zready(v[q], S.epoch);
+              part += base + lane + 32 * q < b ? (v[q] & ZCNT) : 0;
+            }
           }
           if (__all_sync(0xffffffffu, ok)) {
 #pragma unroll

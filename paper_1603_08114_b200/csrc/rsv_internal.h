@@ -102,7 +102,7 @@ struct DevControl {
   uint64_t seq_state, seq_next;
   // momenta kernel bookkeeping (reset by its last CTA: no memsets per draw)
   uint32_t zig_ticket, zig_done, zig_epoch, zig_pub;
-  uint32_t zig_flag, pad5;  // epoch of the last draw whose CTA prefixes are published
+  uint32_t pad5[2];
   double shard_parts[TR_NV];  // time-sharded chains: this shard's totals (TilePart order)
   // %globaltimer stamps (ns) of the last proposal: momenta kernel first-CTA
   // entry / last-CTA exit, trajectory kernel CTA-0 entry / last-CTA exit,
