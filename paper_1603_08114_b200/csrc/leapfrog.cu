@@ -171,7 +171,10 @@ __device__ __forceinline__ void kick(double (&d)[R], double (&p)[R], const doubl
     const double dp = r < R - 1 ? d[r + 1] : dr;
     double t;
     const double E = exp_neg_k(d[r], tab, t, s);
-    nmax = max(nmax, ((unsigned)__double2loint(t) - (unsigned)s.n_lo) & cm[r]);
+    // lean warps: each thread's sites are all core or none (the caller keeps
+    // the thread's maximum only in the first case), so no per-site mask
+    if (EDGE) nmax = max(nmax, ((unsigned)__double2loint(t) - (unsigned)s.n_lo) & cm[r]);
+    else nmax = max(nmax, (unsigned)__double2loint(t) - (unsigned)s.n_lo);
     const double G = EDGE && ((endm >> r) & 1) ? s.g_end : s.g_int;
     double pp = p[r] - Cd[r];
     pp = fma(-G, d[r], pp);
@@ -185,6 +188,51 @@ template <int R>
 __device__ __forceinline__ void drift(double (&d)[R], const double (&p)[R], double c) {
 #pragma unroll
   for (int r = 0; r < R; r++) d[r] = fma(c, p[r], d[r]);
+}
+
+template <int R, int NT>
+__device__ __forceinline__ void ghost_refresh(double (&d)[R], double (&p)[R], double *s_gx, int lane, int warp,
+                                              int parity);
+
+// The L leapfrog steps of a tile (integrator.py:149-179), unrolled by the
+// ghost-refresh period R: loop control and the refresh test once per R
+// steps.  EDGE is warp-uniform (masked kick for partially live / end / mixed
+// core threads).  cf / cl: ensemble chain boundaries cut the coupling.
+template <bool EDGE, int R, int NT, bool FUSE, bool ENS>
+__device__ __forceinline__ void run_steps(double (&d)[R], double (&p)[R], const double (&Ad)[R],
+                                          const double (&Cd)[R], const TrajConsts &s,
+                                          const unsigned long long *tab, uint32_t live, uint32_t endm,
+                                          const unsigned (&cm)[R], bool cf, bool cl, int L, double *gx, int lane,
+                                          int warp, unsigned &nmax) {
+  constexpr int NW = NT / 32;
+  int gpar = 0;
+  auto one = [&](int step) {
+    if (!FUSE) drift(d, p, s.c_half);
+    // lanes 0 / 31 get their own value back: those are ghost lanes (or the
+    // CTA window edges, inside the halo) whose stale values never reach a
+    // core site; next to a global end the neighbour lane is non-live (d = 0)
+    double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
+    double dr = __shfl_down_sync(0xffffffffu, d[0], 1);
+    if (ENS) {  // no coupling across chain boundaries
+      dl = cf ? 0.0 : dl;
+      dr = cl ? 0.0 : dr;
+    }
+    kick<EDGE, R>(d, p, Ad, Cd, dl, dr, s, tab, live, endm, cm, nmax);
+    if (FUSE) drift(d, p, step < L - 1 ? s.c_full : s.c_half);
+    else drift(d, p, s.c_half);
+  };
+  if (FUSE) drift(d, p, s.c_half);
+  int step = 0;
+  for (; step + R <= L; step += R) {
+#pragma unroll
+    for (int u = 0; u < R; u++) one(step + u);
+    if (NW > 1 && step + R < L) {
+      ghost_refresh<R, NT>(d, p, gx, lane, warp, gpar);
+      gpar ^= 1;
+    }
+  }
+  for (; step < L; step++) one(step);
+  if (NW > 1) ghost_refresh<R, NT>(d, p, gx, lane, warp, gpar);
 }
 
 // Metropolis step (sampler.py:155-167) on the tile partials, run by the last
@@ -344,6 +392,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_kernel(TrajArgs A) {
 
   // ---- the trajectory: shuffles only, ghost lanes refreshed every R steps ----
   RSV_STAMP(2);
+  const bool masked = edge || (core != 0 && core != (1u << R) - 1);
   unsigned nmax = 0;
   const int L = A.n_steps;
   int parity = 0;
@@ -354,7 +403,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_kernel(TrajArgs A) {
     double dr = __shfl_down_sync(0xffffffffu, d[0], 1);
     if (lane == 0) dl = 0.0;   // window edges: stale ghosts, never read by core results
     if (lane == 31) dr = 0.0;
-    if (edge) kick<true, R>(d, p, Ad, Cd, dl, dr, s, s_tab, live, endm, cm, nmax);
+    if (masked) kick<true, R>(d, p, Ad, Cd, dl, dr, s, s_tab, live, endm, cm, nmax);
     else if (any_live) kick<false, R>(d, p, Ad, Cd, dl, dr, s, s_tab, live, endm, cm, nmax);
     if (FUSE) drift(d, p, step < L - 1 ? s.c_full : s.c_half);
     else drift(d, p, s.c_half);
@@ -364,6 +413,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_kernel(TrajArgs A) {
     }
   }
   if (NW > 1) ghost_refresh<R, NT>(d, p, s_gx, lane, warp, parity);  // exact d_{i-1} for the energies
+  if (!masked && !core) nmax = 0;  // the lean kick does not mask non-core sites
   const bool bad = nmax > (unsigned)s.n_span;
   RSV_STAMP(3);
 
@@ -682,8 +732,10 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     const bool any_live = live != 0;
     const bool edge = (any_live && live != (1u << R) - 1) || endm;
     // warp-uniform kick path: the masked (edge) kick handles partially or
-    // non-live lanes and the global end sites; all other warps run the lean one
-    const bool warp_edge = __any_sync(0xffffffffu, edge || !any_live);
+    // non-live lanes, the global end sites and threads whose sites are only
+    // partly core (shard ownership); all other warps run the lean one
+    const bool mixed_core = core != 0 && core != (1u << R) - 1;
+    const bool warp_edge = __any_sync(0xffffffffu, edge || !any_live || mixed_core);
     // H_old of the owned core sites while a / lnRV are at hand
     double vold[6] = {0, 0, 0, 0, 0, 0};
     {
@@ -707,29 +759,12 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     c1 = clock64(); cyc_pre += c1 - c0; c0 = c1;
     unsigned nmax = 0;
     const int L = A.n_steps;
-    int gpar = 0;
-    if (FUSE) drift(d, p, s.c_half);
-    for (int step = 0; step < L; step++) {
-      if (!FUSE) drift(d, p, s.c_half);
-      // lanes 0 / 31 get their own value back: those are ghost lanes (or the
-      // CTA window edges, inside the halo) whose stale values never reach a
-      // core site; next to a global end the neighbour lane is non-live (d = 0)
-      double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      double dr = __shfl_down_sync(0xffffffffu, d[0], 1);
-      if (ENS) {  // no coupling across chain boundaries
-        dl = cf ? 0.0 : dl;
-        dr = cl ? 0.0 : dr;
-      }
-      if (warp_edge) kick<true, R>(d, p, Ad, Cd, dl, dr, s, S.tab, live, endm, cm, nmax);
-      else kick<false, R>(d, p, Ad, Cd, dl, dr, s, S.tab, live, endm, cm, nmax);
-      if (FUSE) drift(d, p, step < L - 1 ? s.c_full : s.c_half);
-      else drift(d, p, s.c_half);
-      if (NW > 1 && (step + 1) % R == 0 && step + 1 < L) {
-        ghost_refresh<R, NT>(d, p, S.gx, lane, warp, gpar);
-        gpar ^= 1;
-      }
+    if (warp_edge) {
+      run_steps<true, R, NT, FUSE, ENS>(d, p, Ad, Cd, s, S.tab, live, endm, cm, cf, cl, L, S.gx, lane, warp, nmax);
+    } else {
+      run_steps<false, R, NT, FUSE, ENS>(d, p, Ad, Cd, s, S.tab, live, endm, cm, cf, cl, L, S.gx, lane, warp, nmax);
+      nmax = core ? nmax : 0u;
     }
-    if (NW > 1) ghost_refresh<R, NT>(d, p, S.gx, lane, warp, gpar);
     __syncthreads();  // refresh slots reused by the next tile
     c1 = clock64(); cyc_loop += c1 - c0; c0 = c1;
 
