@@ -849,6 +849,10 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     A.dbg[(size_t)blockIdx.x * 8 + 2] = cyc_loop;
     A.dbg[(size_t)blockIdx.x * 8 + 3] = cyc_post;
     A.dbg[(size_t)blockIdx.x * 8 + 4] = clock64();
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    A.dbg[(size_t)blockIdx.x * 8 + 5] = smid;
+    A.dbg[(size_t)blockIdx.x * 8 + 6] = gtimer();
   }
 
   if (ENS) return;  // every chain's decision: ens_decide_kernel

@@ -20,3 +20,19 @@ for T in [int(a) for a in sys.argv[1:]] or [1 << 20, 1 << 22]:
     tot = st[:, :4].sum(axis=1)
     print(f"T={T} CTAs={len(st)} mean cycles: wait {st[:,0].mean():.0f} pre {st[:,1].mean():.0f} loop {st[:,2].mean():.0f} post {st[:,3].mean():.0f}  total {tot.mean():.0f} (max {tot.max()})")
     be.close()
+    # per-CTA totals: spread of the finishing times (tail of the persistent grid)
+    print("  per-CTA total cycles pct 0/10/50/90/100:", np.percentile(tot, [0, 10, 50, 90, 100]).round(0))
+    print("  pre+post share of total: %.3f" % ((st[:, 1] + st[:, 3]).sum() / tot.sum()))
+    sm = st[:, 5]
+    b = np.arange(len(st))
+    print("  total cycles: blockIdx < 148: %.0f, >= 148: %.0f" % (tot[b < 148].mean(), tot[b >= 148].mean()))
+    # pairs on the same SM: faster / slower CTA
+    fast, slow = [], []
+    for s_ in np.unique(sm):
+        idx = np.where(sm == s_)[0]
+        if len(idx) == 2:
+            a_, c_ = sorted(idx, key=lambda i: tot[i])
+            fast.append(tot[a_]); slow.append(tot[c_])
+            if len(fast) <= 4:
+                print("  SM", s_, "blocks", idx.tolist(), "cycles", tot[idx].tolist())
+    print("  SM pairs: fast %.0f slow %.0f" % (np.mean(fast), np.mean(slow)))
