@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     }
     const double hold = vold[0];
 #pragma unroll
-    for (int k = 0; k < 6; k++) S.acc[(k == 0 ? 1 : 2 + k) * NT + tid] += vold[k];  // slots 1, 3..7
+    for (int k = 0; k < (STATS ? 6 : 1); k++) S.acc[(k == 0 ? 1 : 2 + k) * NT + tid] += vold[k];  // slots 1, 3..7
 
     // ---- the trajectory ----
     c1 = clock64(); cyc_pre += c1 - c0; c0 = c1;
@@ -830,7 +830,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
       S.acc[0 * NT + tid] += vnew[0] - hold;
       S.acc[2 * NT + tid] += vnew[0];
 #pragma unroll
-      for (int k = 0; k < 5; k++) S.acc[(8 + k) * NT + tid] += vnew[1 + k];
+      for (int k = 0; k < (STATS ? 5 : 0); k++) S.acc[(8 + k) * NT + tid] += vnew[1 + k];
       if (nmax > (unsigned)s.n_span) S.acc[13 * NT + tid] = 1.0;
     }
     __syncthreads();  // all reads of this tile's buffer done before it is refilled
