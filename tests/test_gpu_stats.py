@@ -131,3 +131,93 @@ def test_run_chain_bitwise_reproducible_and_storm(backend):
     assert list(a.iters[:3]) == [20, 22, 24]
     with pytest.raises(P.DivergenceStormError):
         P.run_chain(data, P.SamplerConfig(seed=1, md=P.MDConfig(50.0, 5), n_burnin=0, n_samples=500), backend=backend)
+
+
+def test_c6_parameter_recovery_coverage(backend):
+    # the reference's c6 (test_acceptance.py:144-169) with every sweep -- HMC
+    # proposal and the five theta draws -- on the device: the 90 % posterior
+    # interval of each parameter covers the truth in >= 4 of 5 replications
+    true_params = P.Params(phi=0.95, mu=-1.0, xi=-0.3, sigma_eta_sq=0.1, sigma_u_sq=0.025)
+    replications = [(100, 1), (101, 2), (105, 6), (108, 9), (109, 10)]
+    names = ("phi", "mu", "xi", "sigma_eta_sq", "sigma_u_sq")
+    hits = {n: 0 for n in names}
+    for data_seed, chain_seed in replications:
+        data = P.simulate_rsv(true_params, 2000, seed=data_seed).dataset
+        cfg = P.SamplerConfig(seed=chain_seed, md=P.MDConfig(step_size=0.02, n_steps=50), n_burnin=5000,
+                              n_samples=15000, thin=1)
+        chain = P.run_chain(data, cfg, backend=backend, theta_on="device")
+        for n in names:
+            lo, hi = np.quantile(chain.param_series(n), [0.05, 0.95])
+            hits[n] += int(lo <= getattr(true_params, n) <= hi)
+    for n, count in hits.items():
+        assert count >= 4, f"{n} covered in only {count}/5 replications ({hits})"
+
+
+def test_tilted_kalman_variance_marginal(backend):
+    # test_sampler.py:284-319: zero returns make the model linear-Gaussian up
+    # to an exp(-h/2) tilt; Gibbs over (path, sigma_eta^2) with the rest fixed
+    # must reproduce the exact marginal posterior mean of sigma_eta^2.  The
+    # path update is the device proposal, the variance draw numpy's gamma.
+    from paper_1603_08114_b200.sampler import update_sigma_eta_sq
+    phi, mu, xi, su2 = 0.95, -1.0, -0.3, 0.025
+    prior = P.PriorSpec()
+    truth = P.simulate_rsv(P.Params(phi, mu, xi, 0.1, su2), 300, seed=33)
+    data = P.Dataset.from_log_rv(np.zeros(300), truth.dataset.log_rv)
+    z = data.log_rv - xi
+    grid = np.linspace(0.03, 0.3, 400)
+    logm = np.array([_tilted_kalman_loglik(z, phi, mu, v, su2) for v in grid])
+    logm += -(prior.var_shape + 1) * np.log(grid) - prior.var_scale / grid
+    w = np.exp(logm - logm.max())
+    w /= w.sum()
+    want = float((grid * w).sum())
+    rng = P.make_rng(34)
+    md = P.MDConfig(0.02, 50)
+    h = (data.log_rv - np.mean(data.log_rv)).copy()
+    params = P.Params(phi, mu, xi, 0.1, su2)
+    n = 12000
+    out = np.empty(n)
+    for i in range(n):
+        h, _, _ = P.hmc_update_volatility(h, params, data, md, rng, backend=backend)
+        se2 = update_sigma_eta_sq(h, params, prior, rng)
+        params = P.Params(phi, mu, xi, se2, su2)
+        out[i] = se2
+    out = out[2000:]
+    tau = _iact(out)
+    se = float(np.std(out)) * math.sqrt(2 * tau / out.size)
+    assert abs(float(np.mean(out)) - want) < max(3 * se, 1e-4)
+
+
+def _tilted_kalman_loglik(z, phi, mu, se2, su2):
+    """Exact log marginal likelihood of sigma_eta^2 when the returns are zero:
+    lnRV - xi = h + u, h a stationary AR(1), and each h_t carries the factor
+    exp(-h_t / 2) from the returns block.  A Gaussian N(m, V) times exp(-h/2)
+    integrates to exp(-m/2 + V/8) and leaves N(m - V/2, V), so the tilt is a
+    mean shift inside an ordinary Kalman filter."""
+    mean, var = mu, se2 / (1.0 - phi * phi)
+    ll = 0.0
+    for zt in z:
+        ll += -0.5 * mean + var / 8.0
+        mean -= 0.5 * var
+        s = var + su2
+        resid = zt - mean
+        ll += -0.5 * math.log(2.0 * math.pi * s) - resid * resid / (2.0 * s)
+        k = var / s
+        mean, var = mean + k * resid, (1.0 - k) * var
+        mean, var = mu + phi * (mean - mu), phi * phi * var + se2
+    return ll
+
+
+def _iact(x):
+    """Integrated autocorrelation time (initial positive sequence)."""
+    x = np.asarray(x, dtype=np.float64) - np.mean(x)
+    n = x.size
+    f = np.fft.rfft(x, 2 * n)
+    ac = np.fft.irfft(f * np.conj(f))[:n]
+    ac /= ac[0]
+    tau = 1.0
+    for k in range(1, n - 1, 2):
+        pair = ac[k] + ac[k + 1]
+        if pair <= 0:
+            break
+        tau += 2 * pair
+    return tau
