@@ -104,6 +104,11 @@ __device__ __forceinline__ bool zready(uint64_t v, uint32_t epoch) {
 
 __device__ void zig_serial(DevControl *ctrl, const uint64_t *words, int64_t nbuf, double *normals, int64_t T);
 
+// glibc log1p as one out-of-line copy: the exponential-tail path of the
+// ziggurat is rare, so its code is cold in the instruction cache (after an L2
+// flush it comes from DRAM); one shared copy halves those fetches.
+__device__ __noinline__ double log1p_ool(double x) { return glibc_log1p(x); }
+
 __device__ __forceinline__ unsigned long long zgt() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -122,6 +127,7 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
 #define ZSTAMP(k) \
   do { if (dbg && threadIdx.x == 0) dbg[(size_t)blockIdx.x * 8 + (k)] = zgt(); } while (0)
   ZSTAMP(0);
+  if (dbg && threadIdx.x == 0) dbg[(size_t)blockIdx.x * 8 + 7] = 0;
   // the trajectory kernel may launch as soon as every CTA of this grid runs
   // (it waits for this grid's completion before reading the normals)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -152,6 +158,14 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   if (KIND == PRNG_PCG32) { jA = g_jump.pcg_a[tid]; jG = g_jump.pcg_g[tid]; }
   if (KIND == PRNG_MINSTD) jA = g_jump.minstd_a[tid];
   const uint64_t seq = ctrl->seq_state;
+  // co-resident grid: the CTA's jump constants are known before the barrier
+  // (one memory round trip fewer on the draw's critical path)
+  uint64_t pbA = 0, pbG = 0;
+  if (coresident && (KIND == PRNG_PCG32 || KIND == PRNG_MINSTD)) {
+    const int bb = (int)blockIdx.x;
+    if (KIND == PRNG_PCG32) { pbA = bjump[2 * bb]; pbG = bjump[2 * bb + 1]; }
+    else pbA = bjump[bb];
+  }
   __syncthreads();
   const int b = S.blk;
   ZSTAMP(1);
@@ -182,7 +196,7 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
     // per-chunk jump: CTA b's base word is max(0, b*ZB - ZG)
     const int cc = b == 0 ? tid - ZG / ZW : tid;
     if (KIND == PRNG_PCG32) {
-      const uint64_t bA = bjump[2 * b], bG = bjump[2 * b + 1];
+      const uint64_t bA = coresident ? pbA : bjump[2 * b], bG = coresident ? pbG : bjump[2 * b + 1];
       const uint64_t cA = b == 0 ? g_jump.pcg_a[cc] : jA, cG = b == 0 ? g_jump.pcg_g[cc] : jG;
       uint64_t s0 = cA * (bA * seq + bG * inc) + cG * inc;
       base = s0;
@@ -194,7 +208,7 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
       }
     } else {  // MINSTD
       const uint64_t cA = b == 0 ? g_jump.minstd_a[cc] : jA;
-      uint64_t x = mod31(cA * mod31(bjump[b] * seq));
+      uint64_t x = mod31(cA * mod31((coresident ? pbA : bjump[b]) * seq));
       base = x;
 #pragma unroll
       for (int i = 0; i < ZW; i++) {
@@ -240,37 +254,76 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   }
   __syncthreads();
   const int nq = S.nq;
-  for (int q = tid; q < nq && q < ZQ; q += ZT) {
-    const int j0 = S.qent[q];
-    uint64_t r = S.w[ZWS(j0)];
-    const int idx = (int)(r & 0xff);
-    r >>= 8;
-    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-    const double fr = __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | rabs)), 4503599627370496.0);
-    double x = __dmul_rn(fr, S.wi[idx]);
-    if (r & 1) x = -x;
-    int len = 2, a = 0;
-    if (idx == 0) {  // exponential tail: pairs of words until accepted
-      len = 0;
-      for (int m = 1; m <= ZMMAX; m++) {
-        const int j = j0 + 2 * m;
-        const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, glibc_log1p(-u01(S.w[ZWS(j - 1)])));
-        const double yy = -glibc_log1p(-u01(S.w[ZWS(j)]));
-        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
-          x = ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
-          len = 1 + 2 * m;
-          a = 1;
-          break;
-        }
-      }
-    } else {  // wedge: one more word
+  const int nqe = nq < ZQ ? nq : ZQ;
+  if (warp < 2) {
+    // wedge entries (one more word and an exp each), one per thread of warps 0-1
+    for (int q = tid; q < nqe; q += 64) {
+      const int j0 = S.qent[q];
+      uint64_t r = S.w[ZWS(j0)];
+      const int idx = (int)(r & 0xff);
+      if (idx == 0) continue;  // exponential tail: evaluated by warps 2.. below
+      r >>= 8;
+      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+      const double fr =
+          __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | rabs)), 4503599627370496.0);
+      double x = __dmul_rn(fr, S.wi[idx]);
+      if (r & 1) x = -x;
       const double u = u01(S.w[ZWS(j0 + 1)]);
       const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(S.fi[idx - 1], S.fi[idx]), u), S.fi[idx]);
-      a = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x)) ? 1 : 0;
+      const int a = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x)) ? 1 : 0;
+      S.qres[q] = (uint8_t)(2 | (a << 4));
+      S.qx[q] = x;
     }
-    S.qres[q] = (uint8_t)(len | (a << 4));
-    S.qx[q] = x;
+  } else {
+    // exponential-tail entries, one warp each: the up to ZMMAX attempts
+    // (pairs of words after the entry) are evaluated at once, one log1p per
+    // lane, and the first accepted pair is kept -- the result of numpy's
+    // sequential loop with one log1p latency instead of 2m
+    constexpr int NTW = ZT / 32 - 2;
+    int rank = 0;
+    for (int base = 0; base < nqe; base += 32) {
+      const int ql = base + lane;
+      const bool tl = ql < nqe && (S.w[ZWS(S.qent[ql])] & 0xff) == 0;
+      uint32_t tm = __ballot_sync(0xffffffffu, tl);
+      while (tm) {
+        const int q = base + __ffs(tm) - 1;
+        tm &= tm - 1;
+        if (rank++ % NTW != warp - 2) continue;
+        const int j0 = S.qent[q];
+        const uint64_t r = S.w[ZWS(j0)] >> 8;
+        const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+        double lg = 0.0;
+        if (lane < 2 * ZMMAX) lg = log1p_ool(-u01(S.w[ZWS(j0 + 1 + lane)]));
+        // pair m = lane + 1: xx from word j0 + 2m - 1 (lane 2m - 2), yy from word j0 + 2m
+        const double lx = __shfl_sync(0xffffffffu, lg, (2 * lane) & 31);
+        const double ly = __shfl_sync(0xffffffffu, lg, (2 * lane + 1) & 31);
+        const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, lx);
+        const double yy = -ly;
+        const bool ok = lane < ZMMAX && __dadd_rn(yy, yy) > __dmul_rn(xx, xx);
+        const uint32_t am = __ballot_sync(0xffffffffu, ok);
+        const int first = am ? __ffs(am) - 1 : 0;
+        const double xs = __shfl_sync(0xffffffffu, xx, first);
+        if (lane == 0) {
+          double x;
+          int len = 0, a = 0;
+          if (am) {
+            x = ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xs) : __dadd_rn(RSV_ZIG_R, xs);
+            len = 1 + 2 * (first + 1);
+            a = 1;
+          } else {  // no accept within ZMMAX loops: the exact serial walk redoes the draw
+            const double fr =
+                __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | rabs)), 4503599627370496.0);
+            x = __dmul_rn(fr, S.wi[0]);
+            if (r & 1) x = -x;
+          }
+          S.qres[q] = (uint8_t)(len | (a << 4));
+          S.qx[q] = x;
+          if (dbg) atomicAdd(&dbg[(size_t)blockIdx.x * 8 + 7], (unsigned long long)(1 + 16 * (len >> 1)));
+        }
+      }
+    }
   }
+  if (dbg && tid == 0) atomicAdd(&dbg[(size_t)blockIdx.x * 8 + 7], (unsigned long long)nq << 32);
   if (tid == 0 && nq > ZQ) atomicOr(&ctrl->zig_overflow, 1);  // never in practice: exact fallback
   __syncthreads();
   // attempt lengths (nibbles), accepts, non-unit-length starts
@@ -828,7 +881,6 @@ int launch_momenta_ens(EnsChain *ens, double *normals, int64_t Tc, int n_chains,
 // generator, the ziggurat, log1p and the gamma sampler are out-of-line
 // functions (one copy of each stays hot in the instruction cache) instead of
 // being inlined at every call site.
-__device__ __noinline__ double log1p_ool(double x) { return glibc_log1p(x); }
 __device__ __noinline__ double log_ool(double x) { return log(x); }
 __device__ __noinline__ double exp_ool(double x) { return exp(x); }
 
