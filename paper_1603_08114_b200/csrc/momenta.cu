@@ -127,7 +127,6 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
 #define ZSTAMP(k) \
   do { if (dbg && threadIdx.x == 0) dbg[(size_t)blockIdx.x * 8 + (k)] = zgt(); } while (0)
   ZSTAMP(0);
-  if (dbg && threadIdx.x == 0) dbg[(size_t)blockIdx.x * 8 + 7] = 0;
   // the trajectory kernel may launch as soon as every CTA of this grid runs
   // (it waits for this grid's completion before reading the normals)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -318,12 +317,10 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
           }
           S.qres[q] = (uint8_t)(len | (a << 4));
           S.qx[q] = x;
-          if (dbg) atomicAdd(&dbg[(size_t)blockIdx.x * 8 + 7], (unsigned long long)(1 + 16 * (len >> 1)));
         }
       }
     }
   }
-  if (dbg && tid == 0) atomicAdd(&dbg[(size_t)blockIdx.x * 8 + 7], (unsigned long long)nq << 32);
   if (tid == 0 && nq > ZQ) atomicOr(&ctrl->zig_overflow, 1);  // never in practice: exact fallback
   __syncthreads();
   // attempt lengths (nibbles), accepts, non-unit-length starts
@@ -460,7 +457,14 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
       // its status word; once the count reaches the grid size (acquire poll)
       // every status word is in place and one round of independent loads sums
       // the predecessors.  The CTA that finishes last resets zig_pub.
-      if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctrl->zig_pub) : "memory");
+      // the count also goes into its 32-CTA group's sum (ordered before the
+      // release), so a CTA later needs <= 31 status words + the group sums
+      unsigned long long *grp = reinterpret_cast<unsigned long long *>(status) + 2 * (gridDim.x + 2);
+      if (lane == 0) {
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(grp + (b >> 5)), "l"((uint64_t)btot)
+                     : "memory");
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctrl->zig_pub) : "memory");
+      }
       bool flag = false;
       for (int it = 0; it < 4096 && !flag; it++) {
         unsigned f = 0;
@@ -469,25 +473,17 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
         if (!flag) __nanosleep(32);
       }
       if (flag) {
+        if (dbg && lane == 0) dbg[(size_t)blockIdx.x * 8 + 7] = zgt();  // publication count complete, seen
         __syncwarp();  // the other lanes' loads follow lane 0's acquire
+        // one round of independent loads: my group's predecessors' status
+        // words (one per lane) and the sums of the groups before mine
+        const int g = b >> 5, j = (g << 5) + lane;
+        const uint64_t v = j < b ? __ldcg(reinterpret_cast<const unsigned long long *>(status) + j)
+                                 : (uint64_t)S.epoch << 34 | 2ULL << 62;
         uint64_t part = 0;
-        bool ok = true;
-        // 8 independent loads per lane per round: the L2 latency is paid once
-        // per 256 predecessors, not once per 32
-        for (int base = 0; base < b; base += 256) {
-          uint64_t v[8];
-#pragma unroll
-          for (int q = 0; q < 8; q++) {
-            const int j = base + lane + 32 * q;
-            v[q] = j < b ? __ldcg(reinterpret_cast<const unsigned long long *>(status) + j)
-                         : (uint64_t)S.epoch << 34 | 2ULL << 62;
-          }
-#pragma unroll
-          for (int q = 0; q < 8; q++) {
-            ok &= zready(v[q], S.epoch);
-            part += base + lane + 32 * q < b ? (v[q] & ZCNT) : 0;
-          }
-        }
+        for (int k = lane; k < g; k += 32) part += __ldcg(grp + k);
+        const bool ok = zready(v, S.epoch);
+        part += j < b ? (v & ZCNT) : 0;
         if (__all_sync(0xffffffffu, ok)) {
 #pragma unroll
           for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -607,15 +603,20 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   // parse could not be trusted (p ~ 1e-12 per word), redoes it serially
   __syncthreads();
   if (tid == 0) {
-    __threadfence();
-    const unsigned done = atomicAdd(&ctrl->zig_done, 1u);
+    // acquire-release count: the CTA's writes (ordered by the barrier) are
+    // released, and the last CTA acquires every other CTA's
+    unsigned done;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(done) : "l"(&ctrl->zig_done) : "memory");
     if (done == gridDim.x - 1) {
-      __threadfence();
       if (ctrl->zig_overflow != 0 || ctrl->zig_avail < (uint64_t)T) zig_serial(ctrl, words, nwords_buf, normals, T);
       ctrl->zig_overflow = 0;
       ctrl->zig_ticket = 0;
       ctrl->zig_done = 0;
       ctrl->zig_pub = 0;
+      if (coresident) {
+        unsigned long long *grp = reinterpret_cast<unsigned long long *>(status) + 2 * (gridDim.x + 2);
+        for (int k = 0; k < (int)(gridDim.x + 31) / 32; k++) grp[k] = 0;
+      }
       ctrl->zig_epoch = ctrl->zig_epoch + 1;
       ctrl->t_stamp[1] = zgt();
     }
@@ -1155,9 +1156,9 @@ int64_t momenta_words(int64_t T) {
   return (n + ZB - 1) / ZB * ZB;
 }
 
-size_t momenta_scratch_bytes(int64_t T) {  // status words + CTA prefixes
+size_t momenta_scratch_bytes(int64_t T) {  // status words + CTA prefixes + 32-CTA group sums
   const int64_t nb = momenta_words(T) / ZB;
-  return (size_t)2 * (nb + 2) * sizeof(uint64_t) + 64;
+  return (size_t)(2 * (nb + 2) + (nb + 31) / 32 + 1) * sizeof(uint64_t) + 64;
 }
 
 // per-CTA jump constants: CTA b's local word 0 is draw word max(0, b*ZB - ZG)

@@ -31,10 +31,5 @@ for T in [int(a) for a in sys.argv[1:]] or [2000, 1 << 20]:
         print("  AGG publish (us) pct 10/50/90/max:", np.percentile(r4, [10, 50, 90, 100]).round(2))
         print("  lookback done    pct 10/50/90/max:", np.percentile(r5, [10, 50, 90, 100]).round(2))
         print("  stage start pct 10/50/90/max:", np.percentile(rel[:, 1], [10, 50, 90, 100]).round(2))
-        q = st[:, 7]
-        ntail = (q & 0xF).astype(int); tl = ((q >> 4) & 0xFFF).astype(int); nq = (q >> 32).astype(int)
-        cl = ph[:, 2]
-        print("  classify us by #tail words:", {k: round(float(cl[ntail == k].mean()), 2) for k in sorted(set(ntail.tolist()))})
-        print("  classify us by queue length (quartiles of nq):", [round(float(cl[(nq >= a) & (nq < b)].mean()), 2) if ((nq >= a) & (nq < b)).any() else None for a, b in [(0, 18), (18, 22), (22, 26), (26, 999)]])
-        top = np.argsort(-cl)[:6]
-        print("  slowest classify CTAs (us, tails, tail-pairs, nq):", [(round(float(cl[i]), 2), int(ntail[i]), int(tl[i]), int(nq[i])) for i in top])
+        seen = (st[:, 7] - t0) / 1e3
+        print("  count seen (us) pct 0/10/50/90/max:", np.percentile(seen, [0, 10, 50, 90, 100]).round(2))
