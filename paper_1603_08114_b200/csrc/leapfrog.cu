@@ -237,11 +237,16 @@ __device__ __forceinline__ void run_steps(double (&d)[R], double (&p)[R], const 
 
 // Metropolis step (sampler.py:155-167) on the tile partials, run by the last
 // tile to finish; deterministic (fixed-order sums).
-template <int NT>
+// TilePart slot of the i-th reduced value (without statistics: 0, 1, 2, 13)
+template <bool STATS>
+__host__ __device__ constexpr int tr_slot(int i) {
+  return STATS ? i : (i < 3 ? i : 13);
+}
+template <int NT, bool STATS = true>
 __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts);
 template <int NT>
 __device__ __forceinline__ void metropolis(const TrajArgs &A, double *s_v) {
-  metropolis_n<NT>(A, s_v, A.g.n_tiles);
+  metropolis_n<NT, true>(A, s_v, A.g.n_tiles);
 }
 
 // Warp windows overlap by one lane on each side ("ghost lanes"): warp w
@@ -856,36 +861,38 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   }
 
   if (ENS) return;  // every chain's decision: ens_decide_kernel
-  // ---- one reduction per CTA ----
-  double w[TR_NV];
+  // ---- one reduction per CTA (without statistics only dh, H_old, H_new
+  // and the flag: TilePart slots 0, 1, 2, 13) ----
+  constexpr int NU = STATS ? TR_NV : 4;
+  double w[NU];
 #pragma unroll
-  for (int k = 0; k < TR_NV; k++) w[k] = S.acc[k * NT + tid];
+  for (int i = 0; i < NU; i++) w[i] = S.acc[tr_slot<STATS>(i) * NT + tid];
 #pragma unroll
-  for (int k = 0; k < TR_NV; k++) {
+  for (int i = 0; i < NU; i++) {
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) w[k] += __shfl_xor_sync(0xffffffffu, w[k], o);
+    for (int o = 16; o >= 1; o >>= 1) w[i] += __shfl_xor_sync(0xffffffffu, w[i], o);
   }
   if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < TR_NV; k++) S.red[warp * TR_NV + k] = w[k];
+    for (int i = 0; i < NU; i++) S.red[warp * TR_NV + tr_slot<STATS>(i)] = w[i];
   }
   __syncthreads();
-  if (tid < TR_NV) {  // value k: warp totals in warp order, one thread per value
-    double acc = S.red[tid];
-    for (int q = 1; q < NW; q++) acc += S.red[q * TR_NV + tid];
-    reinterpret_cast<double *>(A.parts + blockIdx.x)[tid] = acc;  // TilePart = TR_NV doubles in w order
-    __threadfence();
+  if (tid < NU) {  // value k: warp totals in warp order, one thread per value
+    const int k = tr_slot<STATS>(tid);
+    double acc = S.red[k];
+    for (int q = 1; q < NW; q++) acc += S.red[q * TR_NV + k];
+    reinterpret_cast<double *>(A.parts + blockIdx.x)[k] = acc;  // TilePart = TR_NV doubles in w order
   }
   __syncthreads();
   if (tid == 0) {
-    const unsigned done = atomicAdd(&A.ctrl->tiles_done, 1u);
+    // acquire-release count: this CTA's partials (ordered by the barrier)
+    // are released; the last CTA acquires everyone's
+    unsigned done;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(done) : "l"(&A.ctrl->tiles_done) : "memory");
     S.last = (done == (unsigned)gridDim.x - 1);
   }
   __syncthreads();
-  if (S.last) {
-    __threadfence();
-    metropolis_n<NT>(A, S.v, gridDim.x);
-  }
+  if (S.last) metropolis_n<NT, STATS>(A, S.v, gridDim.x);
 }
 
 struct TrajVariant {
@@ -1103,34 +1110,35 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
 
 // ---------------------------------------------------------------------------
 // Metropolis (sampler.py:155-167) on the reduced tile partials.
-template <int NT>
+template <int NT, bool STATS>
 __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   constexpr int NW = NT / 32;
-  double v[TR_NV];
+  constexpr int NU = STATS ? TR_NV : 4;  // reduced values (TilePart slots tr_slot<STATS>(i))
+  double v[NU];
 #pragma unroll
-  for (int k = 0; k < TR_NV; k++) v[k] = 0.0;
-  for (int i = threadIdx.x; i < n_parts; i += NT) {
-    const TilePart &tp = A.parts[i];
-    v[0] += tp.dh; v[1] += tp.hold; v[2] += tp.hnew;
+  for (int i = 0; i < NU; i++) v[i] = 0.0;
+  for (int j = threadIdx.x; j < n_parts; j += NT) {
+    const double *tp = reinterpret_cast<const double *>(A.parts + j);
 #pragma unroll
-    for (int k = 0; k < 5; k++) { v[3 + k] += tp.so[k]; v[8 + k] += tp.sn[k]; }
-    v[13] += tp.flag;
+    for (int i = 0; i < NU; i++) v[i] += tp[tr_slot<STATS>(i)];
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k < TR_NV; k++) {
+  for (int i = 0; i < NU; i++) {
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    for (int o = 16; o >= 1; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
   }
   if (lane == 0)
-    for (int k = 0; k < TR_NV; k++) s_v[warp * TR_NV + k] = v[k];
+    for (int i = 0; i < NU; i++) s_v[warp * TR_NV + tr_slot<STATS>(i)] = v[i];
   __syncthreads();
   // the warp totals of value k are added in warp order by thread k (in
-  // parallel over k), then thread 0 reads the NV results
+  // parallel over k), then thread 0 reads the NV results (0 for the
+  // statistics slots when they are not evaluated)
   if (threadIdx.x < TR_NV) {
     const int k = threadIdx.x;
-    double acc = s_v[k];
-    for (int w = 1; w < NW; w++) acc += s_v[w * TR_NV + k];
+    const bool used = STATS || k < 3 || k == 13;
+    double acc = used ? s_v[k] : 0.0;
+    for (int w = 1; w < NW; w++) acc += used ? s_v[w * TR_NV + k] : 0.0;
     s_v[NW * TR_NV + k] = acc;
   }
   __syncthreads();

@@ -36,3 +36,17 @@ for T in [int(a) for a in sys.argv[1:]] or [1 << 20, 1 << 22]:
             if len(fast) <= 4:
                 print("  SM", s_, "blocks", idx.tolist(), "cycles", tot[idx].tolist())
     print("  SM pairs: fast %.0f slow %.0f" % (np.mean(fast), np.mean(slow)))
+    # the grid's tail: last CTA's loop end -> Metropolis start (t_stamp[3])
+    import ctypes as _c
+    raw = (_c.c_uint64 * 5)()
+    ch2 = P.CudaBackend(0).chain(tr.dataset, theta)
+    ch2.set_latent(tr.latent)
+    ch2.set_stream(P.stream_state(P.make_rng(1, "pcg32")))
+    ch2.hmc_update_many(0.02, 20, 3, results=False)
+    st2 = np.zeros((400, 8), dtype=np.int64)
+    N.check(L.rsv_debug_stamps(ch2.ctx, st2.ctypes.data, 400), ch2.ctx)
+    st2 = st2[st2[:, 2] > 0]
+    N.check(L.rsv_kernel_stamps(ch2.ctx, raw), ch2.ctx)
+    ends = st2[:, 6]
+    print("  traj entry -> CTA loop ends (us) pct 0/50/100:", np.percentile((ends - raw[2]) / 1e3, [0, 50, 100]).round(2),
+          " metropolis start:", round((raw[3] - raw[2]) / 1e3, 2))
