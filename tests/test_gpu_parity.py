@@ -429,3 +429,55 @@ def test_sharded_distributed_device_driver_nccl_world_of_one(backend):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- decomposition independence
+@pytest.mark.parametrize("fuse", [False, True])
+def test_trajectory_bitwise_independent_of_tile_shape(backend, monkeypatch, fuse):
+    # the device analogue of test_integrator.py:55 (worker-count independence):
+    # every site's update uses only its neighbours with the same operations,
+    # so the tile / window shape (RSV_TRAJ_VARIANT, read at context creation)
+    # must not change a single bit of h' or p'
+    from paper_1603_08114_b200.integrator import DeviceChain
+    T = 50021
+    truth = P.simulate_rsv(THETA, T, seed=13)
+    p = O.Stream("pcg32", 17).normals(T)
+    outs = {}
+    for v in (11, 9, 12, 13, 14, 15, 17, 0):
+        monkeypatch.setenv("RSV_TRAJ_VARIANT", str(v))
+        ch = DeviceChain(T, 0)
+        try:
+            ch.set_data(truth.dataset)
+            ch.set_params(THETA)
+            outs[v] = ch.integrate(truth.latent, p, 0.02, 20, fuse)
+        finally:
+            ch.close()
+    h0, p0, d0 = outs[11]
+    for v, (h, pp, d) in outs.items():
+        assert d == d0 and np.array_equal(h, h0) and np.array_equal(pp, p0), v
+
+
+def test_single_site_step_is_the_kernel_matrix_product(backend):
+    # test_integrator.py:229-250: with y = 0 and phi = 0 a site's step is
+    # affine, its linear part k1 k2 k1 (det 1) with w2 = 1/su2 + 1/se2
+    params = P.Params(phi=0.0, mu=-1.0, xi=-0.3, sigma_eta_sq=0.05, sigma_u_sq=0.1)
+    data = P.Dataset.from_log_rv(np.zeros(2), np.array([-1.2, -1.4]))
+    dt = 0.05
+    w2 = 1.0 / params.sigma_u_sq + 1.0 / params.sigma_eta_sq
+    k1 = np.array([[1.0, dt / 2], [0.0, 1.0]])
+    k2 = np.array([[1.0, 0.0], [-dt * w2, 1.0]])
+    m = k1 @ k2 @ k1
+    assert abs(np.linalg.det(m) - 1.0) <= 1e-12
+
+    def step(h0, p0):
+        st = P.PhaseState(np.array([h0, 0.0]), np.array([p0, 0.0]))
+        P.elementary_step(st, P.MDConfig(dt, 1), params, data, backend=backend)
+        return np.array([st.h[0], st.p[0]])
+
+    base = step(0.0, 0.0)
+    cols = np.column_stack([step(1.0, 0.0) - base, step(0.0, 1.0) - base])
+    assert np.allclose(cols, m, rtol=0, atol=1e-12)
+    # the fused trajectory kernel gives the same one-step map
+    st, _ = P.integrate_trajectory(P.PhaseState(np.array([1.0, 0.0]), np.array([0.0, 0.0])), P.MDConfig(dt, 1),
+                                   params, data, backend=backend)
+    assert np.allclose(np.array([st.h[0], st.p[0]]) - base, m[:, 0], rtol=0, atol=1e-12)
