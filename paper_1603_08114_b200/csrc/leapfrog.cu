@@ -629,6 +629,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     hdst = cur ? A.hbuf0 : A.hbuf1;
   }
   if (tid == 0 && blockIdx.x == 0) A.ctrl->t_stamp[2] = gtimer();
+  const unsigned long long t_entry = A.dbg ? gtimer() : 0ull;
   for (int k = 0; k < TR_NV; k++) S.acc[k * NT + tid] = 0.0;
   const int n_tiles = A.g.n_tiles;
   int tile = blockIdx.x;
@@ -853,7 +854,8 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     A.dbg[(size_t)blockIdx.x * 8 + 1] = cyc_pre;
     A.dbg[(size_t)blockIdx.x * 8 + 2] = cyc_loop;
     A.dbg[(size_t)blockIdx.x * 8 + 3] = cyc_post;
-    A.dbg[(size_t)blockIdx.x * 8 + 4] = clock64();
+    A.dbg[(size_t)blockIdx.x * 8 + 4] = (tile - (int)blockIdx.x) / (int)gridDim.x;  // tiles processed
+    A.dbg[(size_t)blockIdx.x * 8 + 7] = t_entry;
     unsigned smid;
     asm("mov.u32 %0, %%smid;" : "=r"(smid));
     A.dbg[(size_t)blockIdx.x * 8 + 5] = smid;

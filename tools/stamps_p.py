@@ -50,3 +50,12 @@ for T in [int(a) for a in sys.argv[1:]] or [1 << 20, 1 << 22]:
     ends = st2[:, 6]
     print("  traj entry -> CTA loop ends (us) pct 0/50/100:", np.percentile((ends - raw[2]) / 1e3, [0, 50, 100]).round(2),
           " metropolis start:", round((raw[3] - raw[2]) / 1e3, 2))
+    # entry / end per CTA (globaltimer) and tiles per CTA
+    ent = (st2[:, 7] - raw[2]) / 1e3
+    endt = (st2[:, 6] - raw[2]) / 1e3
+    nt = st2[:, 4]
+    b2 = np.arange(len(st2))
+    for lo, hi in ((0, 148), (148, 296)):
+        m = (b2 >= lo) & (b2 < hi)
+        print(f"  CTAs {lo}-{hi}: entry us {ent[m].mean():.2f} (max {ent[m].max():.2f}), end us {endt[m].mean():.2f}"
+              f" (max {endt[m].max():.2f}), tiles {np.unique(nt[m]).tolist()}")
