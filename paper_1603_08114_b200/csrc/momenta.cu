@@ -411,6 +411,18 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
     btot += S.warp_tot[q];
   }
   const int toff = woff + incl - cnt;  // exclusive offset of my normals in the CTA
+  // publish the CTA's count now (look-back status word; with a co-resident
+  // grid also the group sum and the release count): the normals below are
+  // staged while the other CTAs publish theirs
+  unsigned long long *grp = reinterpret_cast<unsigned long long *>(status) + 2 * (gridDim.x + 2);
+  if (tid == 0) {
+    volatile uint64_t *vst = status;
+    vst[b] = zpack(b == 0 ? 2 : 1, S.blk_exit, S.epoch, (uint64_t)btot);
+    if (coresident) {
+      asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(grp + (b >> 5)), "l"((uint64_t)btot) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctrl->zig_pub) : "memory");
+    }
+  }
 
   // ---- my normals into the CTA's output staging (block order); the global
   // offset only shifts the coalesced copy-out after the look-back
@@ -451,20 +463,12 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
     volatile uint64_t *vst = status;
     bool have = false;
     uint64_t accum = 0;
-    if (lane == 0) vst[b] = zpack(b == 0 ? 2 : 1, bexit, S.epoch, (uint64_t)btot);
     if (coresident) {
-      // every CTA counts itself into zig_pub with a release reduction after
-      // its status word; once the count reaches the grid size (acquire poll)
-      // every status word is in place and one round of independent loads sums
-      // the predecessors.  The CTA that finishes last resets zig_pub.
-      // the count also goes into its 32-CTA group's sum (ordered before the
-      // release), so a CTA later needs <= 31 status words + the group sums
-      unsigned long long *grp = reinterpret_cast<unsigned long long *>(status) + 2 * (gridDim.x + 2);
-      if (lane == 0) {
-        asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(grp + (b >> 5)), "l"((uint64_t)btot)
-                     : "memory");
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&ctrl->zig_pub) : "memory");
-      }
+      // every CTA counted itself into zig_pub (release reduction after its
+      // status word and its 32-CTA group sum, above); once the count reaches
+      // the grid size (acquire poll) one round of loads -- <= 31 status
+      // words and the group sums -- gives the predecessors' total.  The CTA
+      // that finishes last resets zig_pub and the group sums.
       bool flag = false;
       for (int it = 0; it < 4096 && !flag; it++) {
         unsigned f = 0;
