@@ -461,7 +461,8 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   if (warp == 0) {
     const int bexit = S.blk_exit;
     volatile uint64_t *vst = status;
-    bool have = false;
+    bool have = false, have_prev = false;
+    uint64_t prev_word = 0;
     uint64_t accum = 0;
     if (coresident) {
       // every CTA counted itself into zig_pub (release reduction after its
@@ -481,18 +482,25 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
         __syncwarp();  // the other lanes' loads follow lane 0's acquire
         // one round of independent loads: my group's predecessors' status
         // words (one per lane) and the sums of the groups before mine
+        // (the previous CTA's word, needed by the verification below, is in
+        // the same round: from its lane, or loaded by lane 0 when b opens a group)
         const int g = b >> 5, j = (g << 5) + lane;
-        const uint64_t v = j < b ? __ldcg(reinterpret_cast<const unsigned long long *>(status) + j)
-                                 : (uint64_t)S.epoch << 34 | 2ULL << 62;
+        const bool opens = (b & 31) == 0;
+        const unsigned long long *sw = reinterpret_cast<const unsigned long long *>(status);
+        const uint64_t v = j < b                            ? __ldcg(sw + j)
+                           : (opens && lane == 0 && b > 0) ? __ldcg(sw + b - 1)
+                                                           : (uint64_t)S.epoch << 34 | 2ULL << 62;
         uint64_t part = 0;
         for (int k = lane; k < g; k += 32) part += __ldcg(grp + k);
         const bool ok = zready(v, S.epoch);
         part += j < b ? (v & ZCNT) : 0;
+        prev_word = __shfl_sync(0xffffffffu, v, opens ? 0 : (b - 1) & 31);
         if (__all_sync(0xffffffffu, ok)) {
 #pragma unroll
           for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
           accum = part;
           have = true;
+          have_prev = b > 0;
         }
       }
     }
@@ -572,8 +580,8 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
       if (b == 0) {
         if (S.blk_entry != 0) S.bad = 1;
       } else {  // the previous CTA's exit must equal my block's entry (it has published)
-        uint64_t prev;
-        do { prev = vst[b - 1]; } while (!zready(prev, S.epoch));
+        uint64_t prev = prev_word;
+        if (!have_prev) do { prev = vst[b - 1]; } while (!zready(prev, S.epoch));
         if ((int)((prev >> 58) & 15) != S.blk_entry) S.bad = 1;
       }
       if (S.bad) atomicOr(&ctrl->zig_overflow, 2);

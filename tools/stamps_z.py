@@ -33,3 +33,7 @@ for T in [int(a) for a in sys.argv[1:]] or [2000, 1 << 20]:
         print("  stage start pct 10/50/90/max:", np.percentile(rel[:, 1], [10, 50, 90, 100]).round(2))
         seen = (st[:, 7] - t0) / 1e3
         print("  count seen (us) pct 0/10/50/90/max:", np.percentile(seen, [0, 10, 50, 90, 100]).round(2))
+        ld = rel[:, 5]
+        top = np.argsort(-ld)[:5]
+        print("  slowest look-back CTAs (index, done us, seen us, publish us):",
+              [(int(i), round(float(ld[i]), 2), round(float(seen[i]), 2), round(float(rel[i, 4]), 2)) for i in top])
