@@ -116,7 +116,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def config5_run(P, theta, T, block=4096, sweeps=20, dt=0.005):
+def config5_run(P, theta, T, block=4096, sweeps=60, dt=0.005):
     """Config 5 on one GPU: T = 2^26 sites, full theta update every sweep
     (run_chain with the theta draws on the device), sfc64 in the blocked
     layout (sites [j*4096, (j+1)*4096) from SFC64(SeedSequence([1, j])),
