@@ -105,7 +105,10 @@ int rsv_hmc_update(rsv_ctx *ctx, double step_size, int n_steps, int fuse, rsv_re
  * are not evaluated.  When T >= 2^16, T % 8 == 0 and h_in is page-locked and
  * 16-byte aligned, the trajectory kernel reads h_in in place over PCIe
  * (zero copy, overlapped with its tiles) instead of one copy in ahead of the
- * proposal; rsv_last_update_zero_copy tells which way the last call went. */
+ * proposal; rsv_last_update_zero_copy tells which way the last call went.
+ * The context's own latent path afterwards: h_out when accepted; after a
+ * rejected zero-copy call it holds none (rsv_set_latent before any
+ * device-resident call such as rsv_hmc_update). */
 int rsv_hmc_update_host(rsv_ctx *ctx, const double *h_in, double *h_out, rsv_prng_state *stream, double step_size,
                         int n_steps, int fuse, rsv_result *out);
 int rsv_last_update_zero_copy(const rsv_ctx *ctx);
