@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
+#include <stddef.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -844,11 +845,16 @@ int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_
                          : ss.kind == PRNG_MINSTD ? mod31(minstd_pow(3 * ss.pos) * ss.s[0])
                                                   : 0;
   if (ss.kind != c->kind) c->kind = ss.kind;
-  CK(cudaMemcpyAsync(&c->ctrl->stream, &c->h_ctrl->stream, sizeof(StreamState), cudaMemcpyHostToDevice, c->stream));
+  // stream state, cur = 0 and err = 0 are contiguous: one copy (plus seq_state)
+  c->h_ctrl->cur = 0;
+  c->h_ctrl->err = 0;
+  static_assert(offsetof(DevControl, err) + sizeof(int32_t) - offsetof(DevControl, stream) ==
+                    sizeof(StreamState) + 2 * sizeof(int32_t),
+                "stream, cur, err are contiguous");
+  CK(cudaMemcpyAsync(&c->ctrl->stream, &c->h_ctrl->stream, sizeof(StreamState) + 2 * sizeof(int32_t),
+                     cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(&c->ctrl->seq_state, &c->h_ctrl->seq_state, sizeof(uint64_t), cudaMemcpyHostToDevice,
                      c->stream));
-  CK(cudaMemsetAsync(&c->ctrl->cur, 0, sizeof(int32_t), c->stream));
-  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
   c->has_latent = true;
   const TrajGeom g = traj_geometry(c->T, n_steps, c->sm_count, c->variant);
   // zero copy: the trajectory kernel's tile staging (bulk copies) reads the
