@@ -1288,9 +1288,14 @@ __global__ void __launch_bounds__(ES_NT) estep_kernel(const double *__restrict__
                                                       double *__restrict__ ho, double *__restrict__ po,
                                                       const double *__restrict__ a, const double *__restrict__ lrv,
                                                       const DevParams *prm, double dt, int64_t T, int32_t *flag) {
+  // consecutive steps as programmatic dependents (launch_elementary_step with
+  // pdl): the next step's CTAs launch while this one runs and wait below for
+  // its completion before reading h, p (no-ops for a plain launch)
+  asm volatile("griddepcontrol.launch_dependents;");
   const RefScal s = ref_scal(*prm);
   const double c = __dmul_rn(0.5, dt);
   const int64_t i0 = ((int64_t)blockIdx.x * ES_NT + threadIdx.x) * ES_R;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (i0 >= T) return;
   double hh[ES_R + 2], pv[ES_R + 2], av[ES_R], lv[ES_R];
   const bool full = i0 + ES_R <= T;
@@ -1348,9 +1353,23 @@ __global__ void __launch_bounds__(ES_NT) estep_kernel(const double *__restrict__
 
 int launch_elementary_step(const double *h, const double *p, double *ho, double *po, const double *a,
                            const double *lrv, const DevParams *prm, double dt, int64_t T, int32_t *flag,
-                           cudaStream_t st, int *launches) {
+                           cudaStream_t st, int *launches, int pdl) {
   const int64_t threads = (T + ES_R - 1) / ES_R;
-  estep_kernel<<<(unsigned)((threads + ES_NT - 1) / ES_NT), ES_NT, 0, st>>>(h, p, ho, po, a, lrv, prm, dt, T, flag);
+  const unsigned nb = (unsigned)((threads + ES_NT - 1) / ES_NT);
+  if (pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(ES_NT);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, estep_kernel, h, p, ho, po, a, lrv, prm, dt, T, flag) != cudaSuccess) return -1;
+  } else {
+    estep_kernel<<<nb, ES_NT, 0, st>>>(h, p, ho, po, a, lrv, prm, dt, T, flag);
+  }
   (*launches)++;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

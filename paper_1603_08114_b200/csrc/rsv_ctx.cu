@@ -615,7 +615,7 @@ static bool enqueue_fallback(rsv_ctx *c, double dt, int n_steps, int stats, int 
   const double *hin = c->sh, *pin = c->normals;
   double *ho = c->sh2, *po = c->sp2;
   for (int k = 0; k < n_steps; k++) {
-    ok &= launch_elementary_step(hin, pin, ho, po, c->a, c->lrv, c->prm, dt, c->T, c->dflag, c->stream, l) == 0;
+    ok &= launch_elementary_step(hin, pin, ho, po, c->a, c->lrv, c->prm, dt, c->T, c->dflag, c->stream, l, 1) == 0;
     hin = ho;
     pin = po;
     ho = (ho == c->sh2) ? c->sh : c->sh2;
@@ -1010,8 +1010,10 @@ int rsv_bench_elementary(rsv_ctx *c, double dt, int n_steps, float *ms, int32_t 
     double *h0 = c->sh2, *p0 = c->sp2, *h1 = c->sh, *p1 = c->sp;
     int l = 0;
     bool ok = true;
+    const int pdl_steps = getenv("RSV_NO_PDL") ? 0 : 1;  // step k+1 launched while step k runs
     for (int i = 0; i < n_steps; i++) {
-      ok &= launch_elementary_step(h0, p0, h1, p1, c->a, c->lrv, c->prm, dt, c->T, c->dflag, c->stream, &l) == 0;
+      ok &= launch_elementary_step(h0, p0, h1, p1, c->a, c->lrv, c->prm, dt, c->T, c->dflag, c->stream, &l,
+                                   pdl_steps) == 0;
       std::swap(h0, h1);
       std::swap(p0, p1);
     }

@@ -133,7 +133,7 @@ const void *traj_kernel_fn(int variant, int fuse, int stats);  // for locating t
 // one streamed leapfrog step over all sites (integrator.py:139-146)
 int launch_elementary_step(const double *h, const double *p, double *ho, double *po, const double *a,
                            const double *lrv, const DevParams *prm, double dt, int64_t T, int32_t *flag,
-                           cudaStream_t s, int *launches);
+                           cudaStream_t s, int *launches, int pdl = 0);
 
 // kernel-level plug-in (the reference's backend.run protocol)
 int launch_position_update(double *h, const double *p, double c, int64_t lo, int64_t hi, cudaStream_t s,
