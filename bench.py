@@ -196,14 +196,21 @@ def paper_protocol(no_cpu):
     reference's SerialBackend role) on fewer reps, and the gain curve."""
     from paper_1603_08114_b200 import bench_protocol as BP
     cfg = BP.BenchConfig()
-    study = BP.run_scaling_study(cfg)
+    study = BP.run_scaling_study(cfg, fused=True)
     pts = study.timings["cuda"]
     fit = study.fits["cuda"]
+    fpts = study.timings["cuda_fused"]
+    ffit = study.fits["cuda_fused"]
     out = {"protocol": "reference bench.py:121-267 (device time of the step launches; state device-resident)",
            "params": "BENCH_PARAMS (phi .97, mu -1, xi -.3, se2 .05, su2 .1), dt 0.01, seed 0",
            "points": [{"B": p.b, "T": 512 * p.b, "mean_s": p.mean_seconds, "se_s": p.se_seconds,
                        "site_updates_per_s": 512 * p.b / p.mean_seconds} for p in pts],
-           "fit_cuda": {"A_s": fit.intercept_a, "C_s_per_B": fit.slope_c, "r2": fit.r_squared}}
+           "fit_cuda": {"A_s": fit.intercept_a, "C_s_per_B": fit.slope_c, "r2": fit.r_squared},
+           "fused": {"what": "the same protocol with each 100-step segment one launch of the persistent "
+                             "trajectory kernel (halo tiles, no per-step synchronisation)",
+                     "points": [{"B": p.b, "mean_s": p.mean_seconds, "se_s": p.se_seconds,
+                                 "site_updates_per_s": 512 * p.b / p.mean_seconds} for p in fpts],
+                     "fit": {"A_s": ffit.intercept_a, "C_s_per_B": ffit.slope_c, "r2": ffit.r_squared}}}
     if not no_cpu:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
@@ -225,6 +232,8 @@ def paper_protocol(no_cpu):
         cpu_t = dict(cpu)
         out["gain_measured"] = [{"B": p.b, "gain": cpu_t[p.b] / p.mean_seconds} for p in pts]
         out["asymptotic_gain_fit"] = BP.asymptotic_gain(cfit, fit)
+        out["fused"]["gain_measured"] = [{"B": p.b, "gain": cpu_t[p.b] / p.mean_seconds} for p in fpts]
+        out["fused"]["asymptotic_gain_fit"] = BP.asymptotic_gain(cfit, ffit)
     return out
 
 

@@ -133,6 +133,9 @@ int rsv_elementary_step(rsv_ctx *ctx, double *h, double *p, double step_size, in
  * *diverged = any step flagged |h| > 50 (may be null). */
 int rsv_bench_state(rsv_ctx *ctx, const double *h, const double *p);
 int rsv_bench_elementary(rsv_ctx *ctx, double step_size, int n_steps, float *ms, int32_t *diverged);
+/* The same n steps fused into one launch of the persistent trajectory kernel
+ * (state as for rsv_bench_elementary; device time of the launch in *ms). */
+int rsv_bench_fused(rsv_ctx *ctx, double step_size, int n_steps, float *ms, int32_t *diverged);
 
 /* Kernel-level plug-in (integrator.py:50-65 backend.run protocol):
  * _kernels.py:37-41 position_update, :44-54 momentum_update,

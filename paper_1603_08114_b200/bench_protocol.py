@@ -83,10 +83,11 @@ class ScalingStudy:
     fits: dict[str, TimingFit] = field(default_factory=dict)
 
 
-def _steps(ch: DeviceChain, dt: float, n: int) -> tuple[float, bool]:
+def _steps(ch: DeviceChain, dt: float, n: int, fused: bool = False) -> tuple[float, bool]:
     ms = ctypes.c_float()
     div = ctypes.c_int32(0)
-    ch._ck(ch._lib.rsv_bench_elementary(ch.ctx, float(dt), int(n), ctypes.byref(ms), ctypes.byref(div)))
+    fn = ch._lib.rsv_bench_fused if fused else ch._lib.rsv_bench_elementary
+    ch._ck(fn(ch.ctx, float(dt), int(n), ctypes.byref(ms), ctypes.byref(div)))
     return ms.value * 1e-3, bool(div.value)
 
 
@@ -99,9 +100,11 @@ def _set_state(ch: DeviceChain, h: np.ndarray | None, p: np.ndarray | None):
 
 def time_elementary_step(b: int, backend, reps: int, params: Params, data: Dataset, *, step_size: float = 0.01,
                          repeats: int = 5, n_warmup: int = 10, precision: str = "double", seed: int = 0,
-                         device: int | None = None) -> TimingPoint:
+                         device: int | None = None, fused: bool = False) -> TimingPoint:
     """Mean device seconds of one elementary step at T = 512*b (bench.py:121-190,
-    same signature; `backend` is a CudaBackend or None, only its device is used)."""
+    same signature; `backend` is a CudaBackend or None, only its device is used).
+    fused=True (this package's addition): each 100-step segment is one launch
+    of the persistent trajectory kernel instead of 100 streamed step kernels."""
     if precision != "double":
         raise NotImplementedError("the B200 path computes in float64 only (FP32 bench mode is out of scope)")
     if device is None:
@@ -121,13 +124,13 @@ def time_elementary_step(b: int, backend, reps: int, params: Params, data: Datas
             diverged = False
             for _ in range(repeats):
                 _set_state(ch, h_start, rng.standard_normal(t_len))
-                _, diverged = _steps(ch, dt, n_warmup)
+                _, diverged = _steps(ch, dt, n_warmup, fused)
                 if diverged:
                     break
                 total, done = 0.0, 0
                 while done < reps:
                     seg = min(_REFRESH_EVERY, reps - done)
-                    t, diverged = _steps(ch, dt, seg)
+                    t, diverged = _steps(ch, dt, seg, fused)
                     total += t
                     if diverged:
                         break
@@ -176,16 +179,22 @@ def asymptotic_gain(fit_slow: TimingFit, fit_fast: TimingFit) -> float:
     return fit_slow.slope_c / fit_fast.slope_c
 
 
-def run_scaling_study(config: BenchConfig = BenchConfig(), params: Params = BENCH_PARAMS) -> ScalingStudy:
+def run_scaling_study(config: BenchConfig = BenchConfig(), params: Params = BENCH_PARAMS,
+                      fused: bool = False) -> ScalingStudy:
+    """The reference's study on the GPU ("cuda": one streamed kernel per
+    step); with fused=True also "cuda_fused" (100-step segments in one
+    launch of the persistent trajectory kernel)."""
     study = ScalingStudy(config=config)
-    pts = []
-    for b in config.b_values:
-        data = simulate_rsv(params, SITES_PER_UNIT * b, seed=config.seed + b).dataset
-        pts.append(time_elementary_step(b, None, config.reps, params, data, step_size=config.step_size,
-                                        repeats=config.repeats, seed=config.seed, device=config.device))
-    study.timings["cuda"] = pts
-    if len(set(config.b_values)) >= 2:
-        study.fits["cuda"] = fit_linear([(p.b, p.mean_seconds) for p in pts])
+    for name, fz in (("cuda", False), ("cuda_fused", True)) if fused else (("cuda", False),):
+        pts = []
+        for b in config.b_values:
+            data = simulate_rsv(params, SITES_PER_UNIT * b, seed=config.seed + b).dataset
+            pts.append(time_elementary_step(b, None, config.reps, params, data, step_size=config.step_size,
+                                            repeats=config.repeats, seed=config.seed, device=config.device,
+                                            fused=fz))
+        study.timings[name] = pts
+        if len(set(config.b_values)) >= 2:
+            study.fits[name] = fit_linear([(p.b, p.mean_seconds) for p in pts])
     return study
 
 

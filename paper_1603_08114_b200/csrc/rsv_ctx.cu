@@ -1049,6 +1049,40 @@ int rsv_bench_elementary(rsv_ctx *c, double dt, int n_steps, float *ms, int32_t 
   return 0;
 }
 
+// The same protocol with the n steps fused into one launch of the persistent
+// trajectory kernel (the halo tiles make a segment of n steps exact without
+// per-step synchronisation; energies are evaluated but not used).
+int rsv_bench_fused(rsv_ctx *c, double dt, int n_steps, float *ms, int32_t *diverged) {
+  if (!c || !ms) return fail(c, RSV_E_INVALID, "null argument");
+  int r;
+  if ((r = check_md(c, dt, n_steps))) return r;
+  if (!c->has_data || !c->has_params) return fail(c, RSV_E_STATE, "data/params not set");
+  if (c->shard || c->ens_C) return fail(c, RSV_E_STATE, "rsv_bench_fused needs a single-chain context");
+  CK(cudaSetDevice(c->device));
+  const TrajGeom g = traj_geometry(c->T, n_steps, c->sm_count, c->variant);
+  if (!g.ok) return fail(c, RSV_E_INVALID, "n_steps=%d too large for one fused segment", n_steps);
+  if (g.n_tiles > c->max_tiles) return fail(c, RSV_E_CUDA, "tile count %d exceeds buffer", g.n_tiles);
+  TrajArgs a = traj_args(c, dt, n_steps, 0, g);
+  a.h_src = c->sh2;
+  a.h_dst = c->sh;
+  a.p_in = c->sp2;
+  a.p_out = c->sp;
+  a.integrate_only = 1;
+  a.stats = 0;
+  if ((r = ensure_events(c, 2))) return r;
+  int l = 0;
+  CK(cudaEventRecord(c->evpool[0], c->stream));
+  LK(launch_trajectory(a, c->stream, &l));
+  CK(cudaEventRecord(c->evpool[1], c->stream));
+  c->launches += l;
+  CK(cudaMemcpyAsync(c->sh2, c->sh, sizeof(double) * c->T, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->sp2, c->sp, sizeof(double) * c->T, cudaMemcpyDeviceToDevice, c->stream));
+  if ((r = pull_ctrl(c))) return r;
+  CK(cudaEventElapsedTime(ms, c->evpool[0], c->evpool[1]));
+  if (diverged) *diverged = c->h_ctrl->res.diverged;
+  return 0;
+}
+
 static int ensure_plugin(rsv_ctx *c, int64_t n) {
   if (n <= c->pl_n) return 0;
   for (int i = 0; i < 4; i++) {

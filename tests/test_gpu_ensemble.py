@@ -110,11 +110,15 @@ def test_ensemble_rejects_bad_shapes():
 
 def test_paper_protocol_smoke(tmp_path):
     from paper_1603_08114_b200 import bench_protocol as BP
-    study = BP.run_scaling_study(BP.BenchConfig(b_values=(2, 4), reps=200, repeats=2))
-    pts = study.timings["cuda"]
-    assert [p.b for p in pts] == [2, 4] and all(p.mean_seconds > 0 for p in pts)
+    study = BP.run_scaling_study(BP.BenchConfig(b_values=(2, 4), reps=200, repeats=2), fused=True)
+    for name in ("cuda", "cuda_fused"):
+        pts = study.timings[name]
+        assert [p.b for p in pts] == [2, 4] and all(p.mean_seconds > 0 for p in pts)
+    # a fused 100-step segment is one launch: far below 100 streamed launches
+    assert study.timings["cuda_fused"][0].mean_seconds < study.timings["cuda"][0].mean_seconds
     paths = BP.emit_report(study, tmp_path)
-    assert paths["fits"].read_text().splitlines()[1] == "backend,intercept_a,slope_c,r_squared"
+    lines = paths["fits"].read_text().splitlines()
+    assert lines[1] == "backend,intercept_a,slope_c,r_squared" and lines[3].startswith("cuda_fused,")
 
 
 @pytest.mark.parametrize("T", [2, 1000, 70001])
