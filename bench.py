@@ -540,20 +540,18 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
     t_load = time.perf_counter()
     while time.perf_counter() - t_load < 0.4:
         P.sharded.hmc_update_distributed_device(chain, dt, L, 20)
+    # L2 flushed before every proposal (a 256 MiB write, not timed), one event
+    # pair per proposal around it on the proposal stream (as at N=1)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     dist.barrier()
     torch.cuda.synchronize(local)
     n0 = chain.shard.launch_count()
-    s = torch.cuda.Stream(torch.device(dev))
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
-    s.synchronize()
-    res = P.sharded.hmc_update_distributed_device(chain, dt, L, args.steps)
+    times = []
+    res = P.sharded.hmc_update_distributed_device(chain, dt, L, args.steps, l2_flush=flush, times=times)
     torch.cuda.synchronize(local)
-    e1.record(s)
-    e1.synchronize()
     launches = chain.shard.launch_count() - n0
     dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = sum(a.elapsed_time(b) for a, b in times) / len(times)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
@@ -570,7 +568,7 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
                            "parallelism": f"time-sharded x{ws} (margin {margin} sites, halo every "
                                           f"{P.sharded.halo_period(margin, L)} proposals, NCCL all_gather of shard "
                                           "totals, decision on the device)",
-                           "l2": "per-GPU working set below L2, not flushed (multi-GPU path)"},
+                           "l2": "flushed before every proposal (256 MiB write per GPU, outside the event pairs)"},
                 "trajectories_per_s": 1e3 / ms, "accept_rate": acc, "clocks": clk,
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                         "path": "ShardedChain + sharded.hmc_update_distributed_device (device-resident; results read "

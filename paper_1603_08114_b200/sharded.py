@@ -403,19 +403,25 @@ def _local_device(chains, step_size, n_steps, n, fuse, stats, halo_every, dev, s
 
 
 def hmc_update_distributed_device(chain: ShardedChain, step_size: float, n_steps: int, n: int, fuse: bool = False,
-                                  stats: bool = False, group=None, halo_every: int | None = None):
+                                  stats: bool = False, group=None, halo_every: int | None = None,
+                                  l2_flush=None, times: list | None = None):
     """n proposals of a sharded chain over a torch.distributed (NCCL) group,
     orchestrated on the device: totals all-gathered on the GPU, decisions on
-    the GPU, periodic halo exchange; the host synchronises once at the end."""
+    the GPU, periodic halo exchange; the host synchronises once at the end.
+    Benchmarking: `l2_flush` (a device tensor larger than L2) is overwritten
+    before every proposal, and `times` collects one (start, end) CUDA event
+    pair per proposal, recorded after the flush and after the decision."""
     import torch
     _cuda_shard_ptrs([chain])
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.Stream(dev)  # the kernels and the NCCL collectives share one ordered stream
     with torch.cuda.stream(stream):
-        return _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_every, dev, stream)
+        return _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_every, dev, stream,
+                                   l2_flush, times)
 
 
-def _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_every, dev, stream):
+def _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_every, dev, stream, l2_flush=None,
+                        times=None):
     import torch
     import torch.distributed as dist
     r, w = chain.rank, chain.world
@@ -435,6 +441,11 @@ def _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_e
     out = []
     try:
         for i in range(n):
+            if l2_flush is not None:
+                l2_flush.fill_(i & 0xff)
+            if times is not None:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record(stream)
             if w > 1 and (i % K == 0 or not chain.halo_valid):
                 chain.shard._ck(lib.rsv_shard_halo_async(chain.shard.ctx, send_l.data_ptr(), nl_send,
                                                          send_r.data_ptr(), nr_send, 0))
@@ -452,6 +463,9 @@ def _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_e
                                                         int(bool(fuse)), int(bool(stats)), mine.data_ptr()))
             dist.all_gather_into_tensor(gathered, mine, group=group)
             chain.shard._ck(lib.rsv_shard_decide_async(chain.shard.ctx, gathered.data_ptr(), w, float(hc)))
+            if times is not None:
+                ev[1].record(stream)
+                times.append(ev)
             if (i + 1) % _RING == 0:
                 out.extend(_results(chain, _RING))
         out.extend(_results(chain, n % _RING))
