@@ -70,8 +70,10 @@ def test_momenta_with_tail_draws(backend):
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
 
 
-@pytest.mark.parametrize("T", [2, 3, 7, 2047, 2048, 2049, 100003, 1 << 20])
+@pytest.mark.parametrize("T", [2, 3, 7, 2047, 2048, 2049, 100003, 1 << 20, 3000017])
 def test_momenta_sizes_vs_oracle(backend, T):
+    # 126 K .. 1.16 M normals use the co-resident grid's publication count,
+    # longer draws the decoupled look-back (3000017)
     for kind in ("pcg32", "sfc64"):
         st = O.Stream(kind, T)
         want = st.normals(T)
