@@ -892,6 +892,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     unsigned done;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(done) : "l"(&A.ctrl->tiles_done) : "memory");
     S.last = (done == (unsigned)gridDim.x - 1);
+    if (A.dbg && S.last) A.dbg[(size_t)blockIdx.x * 8 + 5] = gtimer();  // last CTA: count done
   }
   __syncthreads();
   if (S.last) metropolis_n<NT, STATS>(A, S.v, gridDim.x);
@@ -1119,10 +1120,23 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   double v[NU];
 #pragma unroll
   for (int i = 0; i < NU; i++) v[i] = 0.0;
-  for (int j = threadIdx.x; j < n_parts; j += NT) {
-    const double *tp = reinterpret_cast<const double *>(A.parts + j);
+  // two parts per thread per round, loaded together (one memory latency;
+  // the summation order is the plain loop's: part j, then j + NT, ...)
+  for (int j = threadIdx.x; j < n_parts; j += 2 * NT) {
+    const double *t0 = reinterpret_cast<const double *>(A.parts + j);
+    const double *t1 = reinterpret_cast<const double *>(A.parts + j + NT);
+    const bool second = j + NT < n_parts;
+    double a0[NU], a1[NU];
 #pragma unroll
-    for (int i = 0; i < NU; i++) v[i] += tp[tr_slot<STATS>(i)];
+    for (int i = 0; i < NU; i++) {
+      a0[i] = t0[tr_slot<STATS>(i)];
+      a1[i] = second ? t1[tr_slot<STATS>(i)] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < NU; i++) {
+      v[i] += a0[i];
+      if (second) v[i] += a1[i];
+    }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll

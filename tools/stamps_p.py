@@ -59,3 +59,7 @@ for T in [int(a) for a in sys.argv[1:]] or [1 << 20, 1 << 22]:
         m = (b2 >= lo) & (b2 < hi)
         print(f"  CTAs {lo}-{hi}: entry us {ent[m].mean():.2f} (max {ent[m].max():.2f}), end us {endt[m].mean():.2f}"
               f" (max {endt[m].max():.2f}), tiles {np.unique(nt[m]).tolist()}")
+    last = int(np.argmax(st2[:, 5] > 10**12)) if (st2[:, 5] > 10**12).any() else None
+    if last is not None:
+        print("  last CTA", last, ": loop end", round((st2[last, 6] - raw[2]) / 1e3, 2), "count done",
+              round((st2[last, 5] - raw[2]) / 1e3, 2), "metropolis start", round((raw[3] - raw[2]) / 1e3, 2))
