@@ -79,6 +79,7 @@ __device__ __forceinline__ bool out_of_range(double t, int n_lo, int n_span) {
 
 // Variable part of H at one site (the theta-only constants are added in
 // the Metropolis step): 0.5 p^2 + 0.5 d + a e^{-mu} e^{-d} + (q-d)^2/2su2 + AR.
+template <bool KIN = true>
 __device__ __forceinline__ double site_energy(double d, double dprev, double p, double ae, double q, bool first,
                                               const TrajConsts &s, const unsigned long long *tab) {
   double t;
@@ -86,6 +87,7 @@ __device__ __forceinline__ double site_energy(double d, double dprev, double p, 
   const double r = q - d;
   const double tr = d - s.phi * dprev;
   const double ar = first ? s.one_m_phi2 * d * d * s.inv2se : tr * tr * s.inv2se;
+  if (!KIN) return 0.5 * d + ae * E + r * r * s.inv2su + ar;  // potential part (momenta not yet drawn)
   return 0.5 * p * p + 0.5 * d + ae * E + r * r * s.inv2su + ar;
 }
 
@@ -93,7 +95,8 @@ __device__ __forceinline__ double site_energy(double d, double dprev, double p, 
 // the common path; `edge` threads handle the global first site).
 // firstm bit r: site r is the first of its series (stationary AR prior, no
 // predecessor term).
-template <int R, bool STATS = true>
+// KIN = false: the potential part only (the caller adds 0.5 p^2 later).
+template <int R, bool STATS = true, bool KIN = true>
 __device__ __forceinline__ void tile_energy(const double (&d)[R], const double (&p)[R], const double (&av)[R],
                                             const double (&lv)[R], double dl, uint32_t core, uint32_t firstm,
                                             const TrajConsts &s, const unsigned long long *tab, double (&v)[6]) {
@@ -102,7 +105,7 @@ __device__ __forceinline__ void tile_energy(const double (&d)[R], const double (
     const double dprev = r ? d[r - 1] : dl;
     const double q = lv[r] - s.xm;
     const bool first = (firstm >> r) & 1;
-    const double en = site_energy(d[r], dprev, p[r], s.emu * av[r], q, first, s, tab);
+    const double en = site_energy<KIN>(d[r], dprev, p[r], s.emu * av[r], q, first, s, tab);
     const bool c = (core >> r) & 1;
     v[0] += c ? en : 0.0;
     if (STATS) {
@@ -545,7 +548,8 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
 
 // Issue the window [t0 - H, t0 - H + W) of the four arrays into stage[4][W]
 // (clamped to [0, Tpad); arrays are padded to a multiple of 8 doubles).
-// part: 1 = h, (y/2)y, lnRV (+ the whole byte count), 2 = the momenta, 3 = all
+// part: 1 = h, (y/2)y, lnRV, 2 = the momenta, 3 = all, each on `bar` with
+// its own byte count (the first tile stages parts 1 and 2 on two barriers).
 template <int W>
 __device__ __forceinline__ void stage_tile(const TrajArgs &A, const double *hsrc, int tile, double *stage,
                                            uint64_t *bar, int part = 3) {
@@ -553,8 +557,8 @@ __device__ __forceinline__ void stage_tile(const TrajArgs &A, const double *hsrc
   const int64_t lo = g < 0 ? 0 : g, hi = min(g + W, A.Tpad);
   const uint32_t bytes = (uint32_t)((hi - lo) * 8);
   const int off = (int)(lo - g);
+  mbar_expect_tx(bar, (part == 3 ? 4 : part == 1 ? 3 : 1) * bytes);
   if (part & 1) {
-    mbar_expect_tx(bar, 4 * bytes);
     tma_load_1d(stage + 0 * W + off, hsrc + lo, bytes, bar);
     tma_load_1d(stage + 2 * W + off, A.a + lo, bytes, bar);
     tma_load_1d(stage + 3 * W + off, A.lrv + lo, bytes, bar);
@@ -595,7 +599,7 @@ struct PersistSmem {
   double v[NW * TR_NV + TR_NV];
   alignas(16) unsigned long long tab[RSV_EXP_TAB_N];
   double epart[2][NW][8];  // ensemble: per-warp chain partials of a tile (by staging buffer)
-  uint64_t bar[3];  // two staging buffers, the exp table
+  uint64_t bar[4];  // two staging buffers, the exp table, the first tile's momenta
   int last;
 };
 
@@ -637,6 +641,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
     mbar_init(&S.bar[2], 1);
+    mbar_init(&S.bar[3], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // the exp table (16 KB) arrives by one bulk copy alongside the first tile
     mbar_expect_tx(&S.bar[2], (uint32_t)sizeof(S.tab));
@@ -645,13 +650,12 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     if (!ENS && tile < n_tiles) stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0], 1);
   }
   // programmatic dependent launch: everything above overlapped the momenta
-  // kernel's tail; its normals (and stream bookkeeping) are read from here on
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (tid == 0) {
-    if (tile < n_tiles) {
-      if (ENS) stage_tile_ens<W>(A, tile, S.stage[0], &S.bar[0]);
-      else stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0], 2);
-    }
+  // kernel's tail; its normals (and stream bookkeeping) are read only after
+  // griddepcontrol.wait -- here for ensembles, inside the first tile (after
+  // its momentum-free prologue) otherwise
+  if (ENS) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0 && tile < n_tiles) stage_tile_ens<W>(A, tile, S.stage[0], &S.bar[0]);
   }
   __syncthreads();
   mbar_wait(&S.bar[2], 0);
@@ -664,11 +668,12 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   uint32_t parity[2] = {0, 0};
   int buf = 0;
   long long cyc_wait = 0, cyc_pre = 0, cyc_loop = 0, cyc_post = 0, c0, c1;
+  bool first = !ENS;  // first tile of a single chain: momenta not yet readable
   for (; tile < n_tiles; tile += gridDim.x, buf ^= 1) {
     c0 = clock64();
     // the other buffer was released at the end of the previous tile: stream
-    // the next tile into it while this one runs
-    if (tid == 0 && tile + (int)gridDim.x < n_tiles) {
+    // the next tile into it while this one runs (first tile: after the wait)
+    if (tid == 0 && !first && tile + (int)gridDim.x < n_tiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (ENS) stage_tile_ens<W>(A, tile + gridDim.x, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
       else stage_tile<W>(A, hsrc, tile + gridDim.x, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
@@ -689,13 +694,17 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
 #pragma unroll
     for (int r = 0; r < R; r += 2) {
       const double2 h2 = *reinterpret_cast<const double2 *>(stg + 0 * W + lw + r);
-      const double2 p2 = *reinterpret_cast<const double2 *>(stg + 1 * W + lw + r);
       const double2 a2 = *reinterpret_cast<const double2 *>(stg + 2 * W + lw + r);
       const double2 l2 = *reinterpret_cast<const double2 *>(stg + 3 * W + lw + r);
       d[r] = h2.x; d[r + 1] = h2.y;
-      p[r] = p2.x; p[r + 1] = p2.y;
       av[r] = a2.x; av[r + 1] = a2.y;
       lv[r] = l2.x; lv[r + 1] = l2.y;
+      if (!first) {
+        const double2 p2 = *reinterpret_cast<const double2 *>(stg + 1 * W + lw + r);
+        p[r] = p2.x; p[r + 1] = p2.y;
+      } else {
+        p[r] = 0.0; p[r + 1] = 0.0;
+      }
     }
     // ensemble: a thread's R sites never straddle a chain boundary (Tc and
     // the window offsets are multiples of R); cf / cl: my first / last site
@@ -746,7 +755,8 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     double vold[6] = {0, 0, 0, 0, 0, 0};
     {
       const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      tile_energy<R, STATS>(d, p, av, lv, dl, core, firstm, s, S.tab, vold);
+      if (first) tile_energy<R, STATS, false>(d, p, av, lv, dl, core, firstm, s, S.tab, vold);
+      else tile_energy<R, STATS>(d, p, av, lv, dl, core, firstm, s, S.tab, vold);
     }
     if (!ENS && edge && !A.h_src) {
 #pragma unroll
@@ -756,6 +766,29 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
           if (g0 + r + goff == Tg - 1) A.ctrl->ends_old[1] = d[r];
         }
       }
+    }
+    if (!ENS && first) {
+      // the momenta kernel's normals: wait for it (everything above
+      // overlapped its tail), stage this tile's momenta and the next tile
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (tid == 0) {
+        stage_tile<W>(A, hsrc, tile, S.stage[buf], &S.bar[3], 2);
+        if (tile + (int)gridDim.x < n_tiles) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          stage_tile<W>(A, hsrc, tile + gridDim.x, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
+        }
+      }
+      mbar_wait(&S.bar[3], 0);
+#pragma unroll
+      for (int r = 0; r < R; r += 2) {
+        const double2 p2 = *reinterpret_cast<const double2 *>(stg + 1 * W + lw + r);
+        p[r] = ((live >> r) & 1) ? p2.x : 0.0;
+        p[r + 1] = ((live >> (r + 1)) & 1) ? p2.y : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < R; r++)
+        if ((core >> r) & 1) vold[0] += 0.5 * p[r] * p[r];  // kinetic part of H_old
+      first = false;
     }
     const double hold = vold[0];
 #pragma unroll
