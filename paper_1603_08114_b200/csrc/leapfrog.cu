@@ -895,6 +895,10 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     A.dbg[(size_t)blockIdx.x * 8 + 6] = gtimer();
   }
 
+  // a programmatic dependent (the theta kernel of rsv_run_chain) may launch
+  // once every CTA is past its tiles; it waits for this grid's completion
+  // before reading the results
+  asm volatile("griddepcontrol.launch_dependents;");
   if (ENS) return;  // every chain's decision: ens_decide_kernel
   // ---- one reduction per CTA (without statistics only dh, H_old, H_new
   // and the flag: TilePart slots 0, 1, 2, 13) ----

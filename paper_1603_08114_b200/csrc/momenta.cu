@@ -127,12 +127,33 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
 #define ZSTAMP(k) \
   do { if (dbg && threadIdx.x == 0) dbg[(size_t)blockIdx.x * 8 + (k)] = zgt(); } while (0)
   ZSTAMP(0);
-  // the trajectory kernel may launch as soon as every CTA of this grid runs
-  // (it waits for this grid's completion before reading the normals)
-  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ __align__(16) unsigned char zsmem[];
   ZigShared &S = *reinterpret_cast<ZigShared *>(zsmem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // constant data first: tables, per-chunk and (co-resident grid) per-CTA
+  // jump constants -- none of it written by the preceding kernel
+  for (int i = tid; i < 256; i += ZT) {
+    S.ki[i] = g_ki[i];
+    S.wi[i] = g_wi[i];
+    S.fi[i] = g_fi[i];
+  }
+  uint64_t jA = 0, jG = 0;
+  if (KIND == PRNG_PCG32) { jA = g_jump.pcg_a[tid]; jG = g_jump.pcg_g[tid]; }
+  if (KIND == PRNG_MINSTD) jA = g_jump.minstd_a[tid];
+  // (one memory round trip fewer on the draw's critical path)
+  uint64_t pbA = 0, pbG = 0;
+  if (coresident && (KIND == PRNG_PCG32 || KIND == PRNG_MINSTD)) {
+    const int bb = (int)blockIdx.x;
+    if (KIND == PRNG_PCG32) { pbA = bjump[2 * bb]; pbG = bjump[2 * bb + 1]; }
+    else pbA = bjump[bb];
+  }
+  // launched as a programmatic dependent of the theta kernel (rsv_run_chain):
+  // the stream position it advanced is read from here on (no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the trajectory kernel may launch as soon as every CTA of this grid is
+  // past this point (it waits for this grid's completion before reading the
+  // normals; its own start reads what the theta kernel wrote, complete here)
+  asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) {
     // a co-resident grid needs no scheduling-order ticket (every CTA runs at
     // once); otherwise the ticket keeps the look-back deadlock-free
@@ -145,26 +166,9 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
       ctrl->t_stamp[0] = zgt();
     }
   }
-  // tables (independent of the ticket; overlap its latency)
-  for (int i = tid; i < 256; i += ZT) {
-    S.ki[i] = g_ki[i];
-    S.wi[i] = g_wi[i];
-    S.fi[i] = g_fi[i];
-  }
   const StreamState &st = ctrl->stream;
-  uint64_t jA = 0, jG = 0;
   const uint64_t inc = st.s[1];
-  if (KIND == PRNG_PCG32) { jA = g_jump.pcg_a[tid]; jG = g_jump.pcg_g[tid]; }
-  if (KIND == PRNG_MINSTD) jA = g_jump.minstd_a[tid];
   const uint64_t seq = ctrl->seq_state;
-  // co-resident grid: the CTA's jump constants are known before the barrier
-  // (one memory round trip fewer on the draw's critical path)
-  uint64_t pbA = 0, pbG = 0;
-  if (coresident && (KIND == PRNG_PCG32 || KIND == PRNG_MINSTD)) {
-    const int bb = (int)blockIdx.x;
-    if (KIND == PRNG_PCG32) { pbA = bjump[2 * bb]; pbG = bjump[2 * bb + 1]; }
-    else pbA = bjump[bb];
-  }
   __syncthreads();
   const int b = S.blk;
   ZSTAMP(1);
@@ -988,11 +992,16 @@ __global__ void __launch_bounds__(TH_NT) theta_sweep_kernel(DevControl *C, DevPa
   // ziggurat tables in shared memory so no draw waits on a global load
   __shared__ uint64_t s_ki[256];
   __shared__ double s_wi[256], s_fi[256];
+  // programmatic dependent launch (rsv_run_chain): the next sweep's momenta
+  // kernel may launch now; this kernel reads the trajectory's results only
+  // after griddepcontrol.wait (both no-ops for a plain launch)
+  asm volatile("griddepcontrol.launch_dependents;");
   for (int i = threadIdx.x; i < 256; i += TH_NT) {
     s_ki[i] = g_ki[i];
     s_wi[i] = g_wi[i];
     s_fi[i] = g_fi[i];
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   if (threadIdx.x || blockIdx.x) return;
   (void)sfc_snaps;
@@ -1129,7 +1138,22 @@ __global__ void __launch_bounds__(TH_NT) theta_sweep_kernel(DevControl *C, DevPa
 }
 
 int launch_theta_sweep(DevControl *ctrl, DevParams *prm, TrajConsts *kdev, DevRun *run, DevPrior prior, double dt,
-                       int64_t T, const uint64_t *sfc_snaps, cudaStream_t s, int *launches) {
+                       int64_t T, const uint64_t *sfc_snaps, cudaStream_t s, int *launches, int pdl) {
+  if (pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(TH_NT);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, theta_sweep_kernel, ctrl, prm, kdev, run, prior, dt, T, sfc_snaps) != cudaSuccess)
+      return -1;
+    (*launches)++;
+    return 0;
+  }
   theta_sweep_kernel<<<1, TH_NT, 0, s>>>(ctrl, prm, kdev, run, prior, dt, T, sfc_snaps);
   (*launches)++;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
@@ -1212,6 +1236,20 @@ static void launch_zig(const MomentaBufs &b, const uint64_t *words, int64_t nbuf
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, zig_kernel<KIND>, ZT, smem);
   // (small grids poll their few predecessors directly: cheaper than the flag)
   const int coresident = nb >= 64 && nb <= per_sm * sms ? 1 : 0;
+  if (b.pdl) {  // programmatic dependent of the preceding kernel (its griddepcontrol.wait orders the reads)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(ZT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, zig_kernel<KIND>, b.ctrl, words, nbuf, b.normals, T, status, bj, coresident, b.dbg);
+    return;
+  }
   zig_kernel<KIND><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, coresident, b.dbg);
 }
 

@@ -1736,10 +1736,15 @@ int rsv_run_chain(rsv_ctx *c, double dt, int n_steps, int fuse, const rsv_prior 
     bool ok = true;
     l = 0;
     for (int k = 0; k < (gi == 0 ? KS : 1); k++) {
-      ok &= launch_momenta(mbufs(c), c->kind, c->Tg, c->stream, &l) == 0;
+      // programmatic dependent launches: momenta after the previous sweep's
+      // theta kernel, trajectory after the momenta, theta after the trajectory
+      MomentaBufs mb = mbufs(c);
+      mb.pdl = (k > 0 && !getenv("RSV_NO_PDL") && !getenv("RSV_NO_PDL_SWEEP")) ? 1 : 0;
+      ok &= launch_momenta(mb, c->kind, c->Tg, c->stream, &l) == 0;
       if (g.ok) ok &= launch_trajectory(ta, c->stream, &l) == 0;
       else ok &= enqueue_fallback(c, dt, n_steps, 1, &l);
-      ok &= launch_theta_sweep(c->ctrl, c->prm, c->kdev, c->run, pr, dt, c->T, c->sfc_snaps, c->stream, &l) == 0;
+      ok &= launch_theta_sweep(c->ctrl, c->prm, c->kdev, c->run, pr, dt, c->T, c->sfc_snaps, c->stream, &l,
+                               g.ok && !getenv("RSV_NO_PDL") && !getenv("RSV_NO_PDL_SWEEP") ? 1 : 0) == 0;
     }
     cudaError_t e = cudaStreamEndCapture(c->stream, &graph[gi]);
     if (!ok || e != cudaSuccess) {

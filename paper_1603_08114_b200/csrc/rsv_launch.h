@@ -20,6 +20,7 @@ struct MomentaBufs {
   EnsChain *blocks = nullptr;
   int64_t block_len = 0;
   int n_blocks = 0;
+  int pdl = 0;  // launch the draw kernel as a programmatic dependent of the preceding kernel
 };
 
 int64_t momenta_words(int64_t T);
@@ -161,7 +162,7 @@ int launch_suff_stats_dev(const double *h, const double *lrv, int64_t T, const D
 // one Gibbs sweep's theta draws on the device (sampler.py:170-272, run_chain
 // :327-344) after a proposal: updates *prm and *kdev, stores the sample
 int launch_theta_sweep(DevControl *ctrl, DevParams *prm, TrajConsts *kdev, DevRun *run, DevPrior prior,
-                       double dt, int64_t T, const uint64_t *sfc_snaps, cudaStream_t s, int *launches);
+                       double dt, int64_t T, const uint64_t *sfc_snaps, cudaStream_t s, int *launches, int pdl = 0);
 
 // data.py:72-95 simulate_rsv from 3T numpy normals already on the device;
 // work: T + 2 * ceil((T-1)/256) doubles
