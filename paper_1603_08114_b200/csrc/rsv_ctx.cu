@@ -874,11 +874,13 @@ int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_
     rsv_ctx::Cached *cg = nullptr;
     int kpl = 0;
     if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl, 2))) return r;
-    cg->args.h_src = (const double *)h_map;
-    void *kp[] = {&cg->args};
-    cudaKernelNodeParams np = cg->traj_params;
-    np.kernelParams = kp;
-    CK(cudaGraphExecKernelNodeSetParams(cg->exec, cg->traj_node, &np));
+    if (cg->args.h_src != (const double *)h_map) {  // re-point the kernel node (the cached args follow)
+      cg->args.h_src = (const double *)h_map;
+      void *kp[] = {&cg->args};
+      cudaKernelNodeParams np = cg->traj_params;
+      np.kernelParams = kp;
+      CK(cudaGraphExecKernelNodeSetParams(cg->exec, cg->traj_node, &np));
+    }
     CK(cudaGraphLaunch(cg->exec, c->stream));
     c->launches += kpl;
     if ((r = pull_ctrl(c))) return r;
