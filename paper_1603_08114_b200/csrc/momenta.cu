@@ -695,11 +695,17 @@ __device__ void zig_serial(DevControl *ctrl, const uint64_t *words, int64_t nbuf
 // The draw is numpy's random_standard_normal on SFC64(SeedSequence([seed,
 // c])) exactly; the stream states after the draw's words and after the
 // Metropolis uniform are both kept for the trajectory kernel's decision.
-constexpr int ZE_G = 31;      // chains per CTA (one parse warp each)
+// 32 warps: warp 0 generates, warps 4 and 8 (the generator's scheduler, warp
+// id % 4 == 0) stay idle so the generator gets more of its scheduler's issue
+// slots, the other 29 warps parse one chain each
+constexpr int ZE_G = 29;      // chains per CTA (one parse warp each; 4096 chains = 142 CTAs, one wave)
 constexpr int ZE_CH = 64;     // words per chunk
 constexpr int ZE_RING = 256;  // ring words per chain (4 chunks)
 constexpr int ZE_RS = ZE_RING + 1;  // padded row: generator lanes hit distinct banks
-constexpr int ZE_NT = 32 * (ZE_G + 1);
+constexpr int ZE_NT = 1024;
+__device__ __forceinline__ int ze_chain_of_warp(int warp) {  // -1: generator or idle warp
+  return (warp == 0 || warp == 4 || warp == 8) ? -1 : warp - 1 - (warp > 4) - (warp > 8);
+}
 constexpr int ZE_MMAX = 30;   // tail loops resolvable inside the ring window
 
 struct ZEnsShared {
@@ -755,7 +761,7 @@ __global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *nor
     if (warp == 0) {
       if (gen) gen_chunk(r + 2);
     } else {
-      for (int j = warp - 1; j < nch; j += ZE_NT / 32 - 1) {
+      for (int j = ze_chain_of_warp(warp); j >= 0 && j < nch; j += ZE_G) {
         if (S.done[j]) continue;
         const uint64_t *row = S.ring + j * ZE_RS;
         const int64_t base = (int64_t)r * ZE_CH;
