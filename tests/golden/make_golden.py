@@ -180,7 +180,44 @@ def formats():
                         truth_params=np.array([tp.phi, tp.mu, tp.xi, tp.sigma_eta_sq, tp.sigma_u_sq]))
 
 
+def _batch_se(x, n_batches=40):
+    """Monte Carlo standard error of the mean of a correlated series by
+    non-overlapping batch means."""
+    x = np.asarray(x, dtype=np.float64)
+    m = x.size // n_batches
+    b = x[: m * n_batches].reshape(n_batches, m).mean(axis=1)
+    return float(b.std(ddof=1) / np.sqrt(n_batches))
+
+
+H_SITES = (0, 250, 500, 999)
+
+
+def posterior_summary(ch):
+    """Posterior means (theta, time-averaged h, h at H_SITES) and their batch-means errors."""
+    rows = [getattr(ch, n) for n in ("phi", "mu", "xi", "sigma_eta_sq", "sigma_u_sq")]
+    rows.append(ch.latent.mean(axis=1))
+    rows += [ch.latent[:, t] for t in H_SITES]
+    return np.array([r.mean() for r in rows]), np.array([_batch_se(r) for r in rows])
+
+
+def posterior(T=1000, seed=7):
+    """The reference's own chain on simulated data (T=1000, 2000 burn-in
+    sweeps, 2000 samples thinned by 10, latent snapshots kept): posterior
+    means of theta and h with their Monte Carlo errors, for the statistical
+    parity test (tests/test_gpu_stats.py)."""
+    truth = rsvhmc.simulate_rsv(rsvhmc.Params(0.95, -1.0, -0.3, 0.05, 0.1), T, seed=31)
+    cfg = rsvhmc.SamplerConfig(seed=seed, md=rsvhmc.MDConfig(0.02, 30), n_burnin=2000, n_samples=2000, thin=10,
+                               store_latent=True)
+    ch = rsvhmc.run_chain(truth.dataset, cfg)
+    mean, se = posterior_summary(ch)
+    np.savez_compressed(os.path.join(HERE, "posterior_T1000.npz"), y=truth.dataset.returns,
+                        lrv=truth.dataset.log_rv, mean=mean, se=se, accept_rate=float(np.mean(ch.accept)))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "posterior":
+        posterior()
+        sys.exit(0)
     formats()
     prng()
     model()
@@ -189,5 +226,6 @@ if __name__ == "__main__":
     hmc_divergent()
     chain("pcg32", 3)
     chain("philox", 5)
+    posterior()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

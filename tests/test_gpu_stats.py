@@ -221,3 +221,33 @@ def _iact(x):
             break
         tau += 2 * pair
     return tau
+
+
+def _batch_se(x, n_batches=40):
+    x = np.asarray(x, dtype=np.float64)
+    m = x.size // n_batches
+    b = x[: m * n_batches].reshape(n_batches, m).mean(axis=1)
+    return float(b.std(ddof=1) / math.sqrt(n_batches))
+
+
+def test_posterior_means_match_the_reference_chain(backend):
+    # statistical parity with the reference sampler itself: its own chain on
+    # simulated data (tests/golden/make_golden.py posterior(): T=1000, 2000
+    # burn-in sweeps, 2000 samples thinned by 10) against an independent
+    # chain of this package on the same data -- posterior means of theta, of
+    # the time-averaged path and of the path at four sites agree within
+    # 5 combined Monte Carlo standard errors (batch means)
+    from conftest import golden
+    g = golden("posterior_T1000.npz")
+    data = P.Dataset.from_log_rv(g["y"], g["lrv"])
+    cfg = P.SamplerConfig(seed=1234, md=P.MDConfig(0.02, 30), n_burnin=2000, n_samples=2000, thin=10,
+                          store_latent=True)
+    ch = P.run_chain(data, cfg, backend=backend)
+    rows = [ch.param_series(n) for n in ("phi", "mu", "xi", "sigma_eta_sq", "sigma_u_sq")]
+    rows.append(ch.latent.mean(axis=1))
+    rows += [ch.latent[:, t] for t in (0, 250, 500, 999)]
+    mean = np.array([r.mean() for r in rows])
+    se = np.array([_batch_se(r) for r in rows])
+    tol = 5.0 * np.sqrt(se ** 2 + g["se"] ** 2)
+    assert np.all(np.abs(mean - g["mean"]) <= tol), (mean, g["mean"], tol)
+    assert abs(float(np.mean(ch.accept)) - float(g["accept_rate"])) < 0.05
