@@ -266,6 +266,18 @@ def ensemble_run(P, theta, dt, L, C, Tc, steps):
     return out
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (the baseline's hardware)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(T, L, dt, kind, seconds, data, h0):
     """The reference algorithm restated in C (oracle/, kind 'port'), all host
     threads for the leapfrog kernels, on a bounded sample of trajectories."""
@@ -287,7 +299,7 @@ def cpu_baseline(T, L, dt, kind, seconds, data, h0):
     O.lib().orc_pool_shutdown()
     return {"value": T * L * n / el, "unit": UNIT, "cores": nth, "kind": "port",
             "sample": f"{n} HMC proposals (momenta+2H+{L}-step trajectory+Metropolis) at T={T}, {el:.1f} s",
-            "trajectories_per_s": n / el}
+            "trajectories_per_s": n / el, "cpu_model": cpu_model(), "nproc": os.cpu_count()}
 
 
 def run_reference(args, ws, rank):
@@ -321,7 +333,8 @@ def run_reference(args, ws, rank):
                                    "threads for the leapfrog kernels)",
                        "T": args.T, "L": args.L, "dt": args.dt, "prng": args.prng},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "port",
-                             "sample": f"{args.steps} HMC proposals at T={args.T}"},
+                             "sample": f"{args.steps} HMC proposals at T={args.T}", "cpu_model": cpu_model(),
+                             "nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "trajectories_per_s": args.steps / tot}
     print(json.dumps(line), flush=True)
