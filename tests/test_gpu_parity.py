@@ -483,3 +483,49 @@ def test_single_site_step_is_the_kernel_matrix_product(backend):
     st, _ = P.integrate_trajectory(P.PhaseState(np.array([1.0, 0.0]), np.array([0.0, 0.0])), P.MDConfig(dt, 1),
                                    params, data, backend=backend)
     assert np.allclose(np.array([st.h[0], st.p[0]]) - base, m[:, 0], rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------------------------- contract violations (C ABI -> Python errors)
+def test_contract_violations_raise_like_the_reference(backend):
+    # model.py / integrator.py conventions: ValueError for contract
+    # violations (checked again by the C ABI: RSV_E_INVALID), a flag, never an
+    # exception, for divergence
+    import ctypes
+    from paper_1603_08114_b200 import _native as N
+    from paper_1603_08114_b200.integrator import DeviceChain
+    truth = P.simulate_rsv(THETA, 64, seed=2)
+    data = truth.dataset
+    rng = P.make_rng(3, "pcg32")
+    with pytest.raises(ValueError):
+        P.hmc_update_volatility(truth.latent[:-1], THETA, data, P.MDConfig(0.02, 5), rng, backend=backend)
+    with pytest.raises(ValueError):
+        P.MDConfig(0.0, 5)
+    with pytest.raises(ValueError):
+        P.MDConfig(0.02, 0)
+    with pytest.raises(NotImplementedError):
+        P.integrate_trajectory(P.PhaseState(truth.latent.astype(np.float32), np.zeros(64, np.float32)),
+                               P.MDConfig(0.02, 5), THETA, data, backend=backend)
+    ch = DeviceChain(64, 0)
+    try:
+        lib = N.lib()
+        with pytest.raises(ValueError):  # dt <= 0 through the C ABI itself
+            N.check(lib.rsv_hmc_update(ch.ctx, ctypes.c_double(-1.0), 5, 0, ctypes.byref(N.Result())), ch.ctx)
+        with pytest.raises(RuntimeError):  # nothing set on the context yet
+            N.check(lib.rsv_hmc_update(ch.ctx, ctypes.c_double(0.02), 5, 0, ctypes.byref(N.Result())), ch.ctx)
+        ch.set_data(data)
+        ch.set_params(THETA)
+        st = N.PrngState()
+        st.kind = N.KINDS["minstd"]
+        st.s[0] = 0  # not a minstd state
+        with pytest.raises(ValueError):
+            ch.hmc_update_host(truth.latent, st, 0.02, 5)
+        bad = N.to_params(THETA)
+        bad.phi = 1.0  # not stationary
+        with pytest.raises(ValueError):
+            N.check(lib.rsv_set_params(ch.ctx, ctypes.byref(bad)), ch.ctx)
+    finally:
+        ch.close()
+    # divergence is a flag / sentinel, not an exception
+    st, div = P.integrate_trajectory(P.PhaseState(truth.latent, np.full(64, 1e3)), P.MDConfig(0.5, 5), THETA, data,
+                                     backend=backend)
+    assert div
