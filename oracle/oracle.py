@@ -74,7 +74,8 @@ def lib():
         L.orc_elementary_step.restype = ctypes.c_int
         L.orc_integrate.argtypes = [_D, _D, P, _D, _D, i64, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.orc_integrate.restype = ctypes.c_int
-        L.orc_hmc_update.argtypes = [_D, P, _D, _D, i64, ctypes.c_double, ctypes.c_int, S, _D, _D, ctypes.c_int]
+        L.orc_hmc_update.argtypes = [_D, P, _D, _D, i64, ctypes.c_double, ctypes.c_int, S, _D, _D, ctypes.c_int,
+                                     ctypes.c_int]
         L.orc_hmc_update.restype = ctypes.c_int
         L.orc_suff_stats.argtypes = [_D, _D, i64, ctypes.c_double, ctypes.c_double, _D]
         L.orc_max_threads.restype = ctypes.c_int
@@ -196,13 +197,15 @@ def integrate(h, p, params, y, lrv, dt, n_steps, fuse=False, nthreads=1):
     return h, p, bool(f)
 
 
-def hmc_update(h, params, y, lrv, dt, n_steps, stream: Stream, nthreads=1):
-    """sampler.py:144-167.  Returns (h_new, accept, delta_h); advances stream."""
+def hmc_update(h, params, y, lrv, dt, n_steps, stream: Stream, nthreads=1, fuse=False):
+    """sampler.py:144-167 (fuse: integrate_trajectory(fuse_half_steps=True),
+    integrator.py:149).  Returns (h_new, accept, delta_h); advances stream."""
     h = np.array(h, dtype=np.float64)
     work = np.empty(2 * h.size, dtype=np.float64)
     dh = ctypes.c_double(0.0)
     acc = lib().orc_hmc_update(_dp(h), ctypes.byref(_params(params)), _dp(y), _dp(lrv), h.size, float(dt),
-                               int(n_steps), ctypes.byref(stream._st), ctypes.byref(dh), _dp(work), int(nthreads))
+                               int(n_steps), ctypes.byref(stream._st), ctypes.byref(dh), _dp(work), int(nthreads),
+                               int(bool(fuse)))
     return h, bool(acc), float(dh.value)
 
 

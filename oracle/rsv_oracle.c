@@ -428,12 +428,12 @@ int orc_integrate(double *h, double *p, const orc_params *P, const double *y, co
 /* sampler.py:144-167 hmc_update_volatility.  h is updated in place on
  * acceptance; returns accept flag; *delta_h gets dH or +inf (divergence). */
 int orc_hmc_update(double *h, const orc_params *P, const double *y, const double *lrv, int64_t T, double dt,
-                   int n_steps, orc_stream *st, double *delta_h, double *work, int nthreads) {
+                   int n_steps, orc_stream *st, double *delta_h, double *work, int nthreads, int fuse) {
   double *p = work, *hp = work + T;
   orc_fill_normal(st, p, T);                                   /* sampler.py:153 */
   double h_old = orc_hamiltonian(h, p, P, y, lrv, T);           /* :155 */
   memcpy(hp, h, sizeof(double) * (size_t)T);                    /* integrator.py:160 */
-  if (orc_integrate(hp, p, P, y, lrv, T, dt, n_steps, 0, nthreads)) { *delta_h = INFINITY; return 0; }
+  if (orc_integrate(hp, p, P, y, lrv, T, dt, n_steps, fuse, nthreads)) /* integrator.py:149 fuse_half_steps */ { *delta_h = INFINITY; return 0; }
   double h_new = orc_hamiltonian(hp, p, P, y, lrv, T);          /* :159 */
   double dh = h_new - h_old;
   if (!isfinite(dh) || fabs(dh) > 1000.0) { *delta_h = INFINITY; return 0; }

@@ -1201,6 +1201,7 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   DevControl *C = A.ctrl;
   C->tiles_done = 0;  // re-arm for the next launch
   C->t_stamp[3] = gtimer();
+  if (C->halt) return;  // rsv_run_chain stopped at an earlier sweep: stream, path and statistics untouched
   if (A.shard) {  // time-sharded chain: the host combines the shards' totals
     for (int k = 0; k < TR_NV; k++) C->shard_parts[k] = tot[k];
     return;
@@ -1214,7 +1215,9 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   r.words_used = 0;
   const bool flagged = tot[13] > 0.0;
   if (A.integrate_only) {
-    r.diverged = flagged;
+    // a non-finite final state only arises from a kick the reference flags
+    // (NaN / inf are absorbing under the leapfrog map, _kernels.py:50-51)
+    r.diverged = flagged || !isfinite(tot[2]);
     r.delta_h = tot[0];
     C->res = r;
     return;

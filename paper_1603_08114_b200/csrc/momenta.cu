@@ -147,6 +147,15 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
     if (KIND == PRNG_PCG32) { pbA = bjump[2 * bb]; pbG = bjump[2 * bb + 1]; }
     else pbA = bjump[bb];
   }
+  // scheduling-order ticket: the CTA's block of the draw.  The look-back
+  // below only ever waits on smaller tickets, i.e. on CTAs already running,
+  // so the draw makes progress whatever the residency (co-resident grids take
+  // it too: their spin falls back to the look-back when the grid turns out
+  // not to be resident at once, e.g. beside other kernels).  The counter was
+  // re-armed by the previous draw's last CTA, which completed before the
+  // kernels this one depends on started.
+  unsigned ticket = 0;
+  if (tid == 0) ticket = atomicAdd(&ctrl->zig_ticket, 1u);
   // launched as a programmatic dependent of the theta kernel (rsv_run_chain):
   // the stream position it advanced is read from here on (no-op otherwise)
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -154,10 +163,14 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   // past this point (it waits for this grid's completion before reading the
   // normals; its own start reads what the theta kernel wrote, complete here)
   asm volatile("griddepcontrol.launch_dependents;");
+  if (ctrl->halt) {  // rsv_run_chain stopped: no draw; the ticket is given back
+    if (tid == 0) atomicSub(&ctrl->zig_ticket, 1u);
+    return;
+  }
   if (tid == 0) {
     // a co-resident grid needs no scheduling-order ticket (every CTA runs at
     // once); otherwise the ticket keeps the look-back deadlock-free
-    S.blk = coresident ? (int)blockIdx.x : (int)atomicAdd(&ctrl->zig_ticket, 1u);
+    S.blk = (int)ticket;
     S.epoch = ctrl->zig_epoch & 0xffffffu;
     S.bad = 0;
     S.nq = 0;
@@ -171,6 +184,10 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   const uint64_t seq = ctrl->seq_state;
   __syncthreads();
   const int b = S.blk;
+  if (coresident && b != (int)blockIdx.x && (KIND == PRNG_PCG32 || KIND == PRNG_MINSTD)) {
+    if (KIND == PRNG_PCG32) { pbA = bjump[2 * b]; pbG = bjump[2 * b + 1]; }  // prefetched for blockIdx.x
+    else pbA = bjump[b];
+  }
   ZSTAMP(1);
 
   // ---- my 8 raw words, generated into registers
@@ -718,7 +735,8 @@ struct ZEnsShared {
 };
 
 __global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *normals, int64_t Tc, int C,
-                                                         unsigned long long *dbg, int advance) {
+                                                         unsigned long long *dbg, int advance, const int32_t *halt) {
+  if (halt && *halt) return;  // blocked momenta of a stopped rsv_run_chain: streams untouched
   extern __shared__ __align__(16) unsigned char zesmem[];
   ZEnsShared &S = *reinterpret_cast<ZEnsShared *>(zesmem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -883,10 +901,10 @@ __global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *nor
 }
 
 int launch_momenta_ens(EnsChain *ens, double *normals, int64_t Tc, int n_chains, cudaStream_t s, int *launches,
-                       unsigned long long *dbg, int advance) {
+                       unsigned long long *dbg, int advance, const int32_t *halt) {
   const size_t smem = sizeof(ZEnsShared);
   cudaFuncSetAttribute(zig_ens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  zig_ens_kernel<<<(n_chains + ZE_G - 1) / ZE_G, ZE_NT, smem, s>>>(ens, normals, Tc, n_chains, dbg, advance);
+  zig_ens_kernel<<<(n_chains + ZE_G - 1) / ZE_G, ZE_NT, smem, s>>>(ens, normals, Tc, n_chains, dbg, advance, halt);
   (*launches)++;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
@@ -1011,8 +1029,10 @@ __global__ void __launch_bounds__(TH_NT) theta_sweep_kernel(DevControl *C, DevPa
   __syncthreads();
   if (threadIdx.x || blockIdx.x) return;
   (void)sfc_snaps;
+  if (C->halt) return;  // the run stopped at an earlier sweep
   const DevResult res = C->res;
-  // storm guard (sampler.py:329-337), checked on the proposal just made
+  // storm guard (sampler.py:329-337), checked on the proposal just made; the
+  // reference raises before any theta draw, so the run stops right here
   {
     const int div = res.diverged ? 1 : 0;
     if (R->ring_n == RUN_STORM_WINDOW) R->ring_div -= R->ring[R->ring_pos];
@@ -1020,8 +1040,11 @@ __global__ void __launch_bounds__(TH_NT) theta_sweep_kernel(DevControl *C, DevPa
     R->ring[R->ring_pos] = (uint8_t)div;
     R->ring_div += div;
     R->ring_pos = (R->ring_pos + 1) % RUN_STORM_WINDOW;
-    if (R->ring_n == RUN_STORM_WINDOW && R->ring_div > RUN_STORM_LIMIT && R->storm_sweep < 0)
+    if (R->ring_n == RUN_STORM_WINDOW && R->ring_div > RUN_STORM_LIMIT && R->storm_sweep < 0) {
       R->storm_sweep = R->sweep;
+      C->halt = 1;
+      return;
+    }
   }
   ThetaGen G;
   G.kind = C->stream.kind;
@@ -1110,13 +1133,18 @@ __global__ void __launch_bounds__(TH_NT) theta_sweep_kernel(DevControl *C, DevPa
     const double scale = __dadd_rn(pr.var_scale, __dmul_rn(0.5, ss));
     su2 = __ddiv_rn(scale, G.gamma(shape));
   }
-  if (degenerate) R->degenerate = 1;
-  // the stream continues after the draws
+  // the stream continues after the draws (those made before a degenerate
+  // precision included: the reference raises after them, sampler.py:186,200)
   C->stream.pos += G.used;
   if (G.kind == PRNG_SFC64)
     for (int k = 0; k < 4; k++) C->stream.s[k] = G.s[k];
   else if (G.kind == PRNG_PCG32 || G.kind == PRNG_MINSTD)
     C->seq_state = G.g.a;
+  if (degenerate) {  // ValueError in the reference: parameters unchanged, nothing stored
+    R->degenerate = 1;
+    C->halt = 1;
+    return;
+  }
   // new parameters and the constants derived from them (rsv_set_params)
   DevParams q = *P;
   q.phi = phi; q.mu = mu; q.xi = xi; q.se2 = se2; q.su2 = su2;
@@ -1263,7 +1291,7 @@ static void launch_zig(const MomentaBufs &b, const uint64_t *words, int64_t nbuf
 // of sites; the main stream only supplies the Metropolis uniform (and the
 // theta draws), so the proposal "uses" no main-stream words for momenta.
 __global__ void main_uniform_kernel(DevControl *ctrl, uint64_t *snaps, int64_t T) {
-  if (threadIdx.x || blockIdx.x) return;
+  if (threadIdx.x || blockIdx.x || ctrl->halt) return;
   const StreamState st = ctrl->stream;
   ctrl->zig_used = 0;
   ctrl->zig_avail = (uint64_t)T;
@@ -1279,7 +1307,8 @@ __global__ void main_uniform_kernel(DevControl *ctrl, uint64_t *snaps, int64_t T
 
 int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, int *launches) {
   if (b.blocks) {
-    if (launch_momenta_ens(b.blocks, b.normals, b.block_len, b.n_blocks, s, launches, nullptr, 1)) return -1;
+    if (launch_momenta_ens(b.blocks, b.normals, b.block_len, b.n_blocks, s, launches, nullptr, 1, &b.ctrl->halt))
+      return -1;
     main_uniform_kernel<<<1, 32, 0, s>>>(b.ctrl, b.sfc_snaps, T);
     (*launches)++;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;

@@ -1760,6 +1760,7 @@ int rsv_run_chain(rsv_ctx *c, double dt, int n_steps, int fuse, const rsv_prior 
   }
   const int lps = l;  // kernel launches per sweep
   CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
+  CK(cudaMemsetAsync(&c->ctrl->halt, 0, sizeof(int32_t), c->stream));
   const int64_t n_sweeps = n_burnin + n_samples * thin;
   int64_t storm = -1;
   cudaError_t le = cudaSuccess;
@@ -1777,6 +1778,9 @@ int rsv_run_chain(rsv_ctx *c, double dt, int n_steps, int fuse, const rsv_prior 
       }
     }
   }
+  // a stop (storm / degenerate) left every later kernel of the run a no-op;
+  // re-arm the context for ordinary calls
+  if (le == cudaSuccess) le = cudaMemsetAsync(&c->ctrl->halt, 0, sizeof(int32_t), c->stream);
   CK(cudaStreamSynchronize(c->stream));
   for (int q = 0; q < 2; q++) {
     cudaGraphExecDestroy(exec[q]);

@@ -102,7 +102,11 @@ struct DevControl {
   uint64_t seq_state, seq_next;
   // momenta kernel bookkeeping (reset by its last CTA: no memsets per draw)
   uint32_t zig_ticket, zig_done, zig_epoch, zig_pub;
-  uint32_t pad5[2];
+  // rsv_run_chain stopped (divergence storm or degenerate precision): every
+  // later kernel of the run leaves the stream, the path and the parameters
+  // exactly as they were at that sweep (sampler.py:331-337 raises there)
+  int32_t halt;
+  uint32_t pad5;
   double shard_parts[TR_NV];  // time-sharded chains: this shard's totals (TilePart order)
   // %globaltimer stamps (ns) of the last proposal: momenta kernel first-CTA
   // entry / last-CTA exit, trajectory kernel CTA-0 entry / last-CTA exit,

@@ -127,7 +127,7 @@ struct TrajArgs {
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches);
 // ensemble: per-chain sfc64 momenta (numpy SFC64 + ziggurat, one thread per chain)
 int launch_momenta_ens(EnsChain *ens, double *normals, int64_t Tc, int n_chains, cudaStream_t s, int *launches,
-                       unsigned long long *dbg = nullptr, int advance = 0);
+                       unsigned long long *dbg = nullptr, int advance = 0, const int32_t *halt = nullptr);
 const void *traj_kernel_fn(int variant, int fuse, int stats);  // for locating the node in a captured graph
 
 

@@ -17,13 +17,13 @@ kernels per step (``integrator.py:111-146``) run by a pluggable backend
 from __future__ import annotations
 
 import ctypes
-import sys
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _native as N
-from .model import Dataset, Params, PhaseState, _f64, scalar_pack
+from .model import Dataset, Params, PhaseState, _f64, is_frozen, scalar_pack
 
 DEFAULT_CHUNK = 512
 DH_DIVERGENCE_THRESHOLD = 1000.0  # integrator.py:29; applied on device
@@ -45,6 +45,16 @@ class MDConfig:
     @property
     def trajectory_length(self) -> float:
         return self.n_steps * self.step_size
+
+
+class _Lease:
+    """Owner object of one hand-out of a pooled page-locked buffer."""
+
+    __slots__ = ("__array_interface__", "buf", "__weakref__")
+
+    def __init__(self, buf: np.ndarray):
+        self.buf = buf
+        self.__array_interface__ = buf.__array_interface__
 
 
 class DeviceChain:
@@ -77,8 +87,14 @@ class DeviceChain:
 
     # -- state --
     def set_data(self, data: Dataset, force: bool = False):
+        """Upload y and ln RV.  The upload is reused only while both arrays
+        are read-only (``Dataset`` freezes its arrays), so no in-place edit
+        can leave the device on stale data; writable arrays are uploaded on
+        every call."""
         key = (id(data), id(data.returns), id(data.log_rv), data.returns.ctypes.data, data.log_rv.ctypes.data)
-        if force or key != self._data_key:
+        if not (is_frozen(data.returns) and is_frozen(data.log_rv)):
+            key = None
+        if force or key is None or key != self._data_key:
             if data.length != self.T:
                 raise ValueError(f"dataset length {data.length} does not match chain length {self.T}")
             y = np.ascontiguousarray(data.returns, dtype=np.float64)
@@ -100,23 +116,26 @@ class DeviceChain:
         self._ck(self._lib.rsv_set_latent(self.ctx, h.ctypes.data, 0))
 
     def _pinned_out(self) -> np.ndarray:
-        """A page-locked host array for a returned path.  Pool entries are
-        handed out again only once no caller references them any more (the
-        pool's list slot, the loop name and getrefcount's argument are the
-        only references), so a returned path is never overwritten."""
-        pool = self.__dict__.setdefault("_pool", [])
-        for arr in pool:
-            if sys.getrefcount(arr) <= 3:
-                return arr
+        """A page-locked host array for a returned path.  Each hand-out is an
+        array over a fresh ``_Lease`` of a pool buffer, tracked by a weak
+        reference: the lease is the memory owner numpy records for the
+        returned array and for every view derived from it, so a buffer is
+        reused only once all of them are gone -- a returned path is never
+        overwritten."""
+        pool = self.__dict__.setdefault("_pool", [])  # [buffer, weakref to the view handed out]
         if not pool:  # allocate the pool at once (page-locking is slow)
             try:
                 import torch
                 ts = [torch.empty(self.T, dtype=torch.float64, pin_memory=True) for _ in range(3)]
                 self.__dict__["_pool_t"] = ts
-                pool.extend(t.numpy() for t in ts)
-                return pool[0]
+                pool.extend([t.numpy(), None] for t in ts)
             except Exception:
                 pass
+        for ent in pool:
+            if ent[1] is None or ent[1]() is None:
+                lease = _Lease(ent[0])
+                ent[1] = weakref.ref(lease)
+                return np.asarray(lease)
         return np.empty(self.T)
 
     def get_latent(self, out: np.ndarray | None = None) -> np.ndarray:

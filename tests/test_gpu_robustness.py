@@ -1,0 +1,99 @@
+"""GPU tests of the failure paths: non-finite states flag divergence
+(_kernels.py:50-51), a divergence storm in the device run_chain stops exactly
+where the reference raises (sampler.py:329-337), returned paths are never
+recycled while referenced, and data edits reach the device."""
+import gc
+import math
+
+import numpy as np
+import pytest
+
+import paper_1603_08114_b200 as P
+from conftest import TRUE
+
+pytestmark = pytest.mark.gpu
+THETA = P.Params(**TRUE)
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf, 1e200])
+def test_nonfinite_or_huge_momenta_flag_divergence(backend, bad):
+    # the reference flags any kick-time h outside [-50, 50] or NaN; here the
+    # range test on the exp reduction must also catch NaN / inf / huge states
+    tr = P.simulate_rsv(THETA, 3000, seed=4)
+    p = np.zeros(3000)
+    p[1234] = bad
+    for L in (1, 7, 20):
+        _, div = P.integrate_trajectory(P.PhaseState(tr.latent, p), P.MDConfig(0.02, L), THETA, tr.dataset,
+                                        backend=backend)
+        assert div, (bad, L)
+    rng = P.make_rng(3, "pcg32")
+    pos = P.stream_state(rng).pos
+    h = tr.latent.copy()
+    h[10] = bad
+    h2, acc, dh = P.hmc_update_volatility(h, THETA, tr.dataset, P.MDConfig(0.02, 20), rng, backend=backend)
+    assert not acc and math.isinf(dh) and h2 is h
+    assert P.stream_state(rng).pos - pos < 3000 * 1.1  # momenta only: no uniform drawn
+
+
+@pytest.mark.parametrize("kind", ["pcg32", "sfc64"])
+def test_device_run_chain_storm_stops_like_the_reference(backend, kind):
+    # every proposal diverges (huge step): the storm fires at sweep 99; the
+    # device run must raise there with the generator exactly where the
+    # host-driven (reference-ordered) run leaves it -- no theta draws on the
+    # storm sweep, nothing after it
+    tr = P.simulate_rsv(THETA, 256, seed=2)
+    cfg = P.SamplerConfig(seed=7, md=P.MDConfig(2.0, 20), n_burnin=0, n_samples=300, prng=kind)
+    states = {}
+    for theta_on in ("host", "device"):
+        rng = P.make_rng(7, kind)
+        with pytest.raises(P.DivergenceStormError, match="sweep 99"):
+            P.run_chain(tr.dataset, cfg, backend=backend, init_params=THETA, init_h=tr.latent, rng=rng,
+                        theta_on=theta_on)
+        st = P.stream_state(rng)
+        states[theta_on] = (int(st.pos), [int(x) for x in st.s])
+    assert states["host"] == states["device"]
+    # the context works normally afterwards (the stop is re-armed)
+    ch = backend.chain(tr.dataset, THETA)
+    ch.set_latent(tr.latent)
+    r = ch.hmc_update(0.02, 20)
+    assert not r.diverged
+
+
+def test_returned_paths_are_not_recycled_while_referenced(backend):
+    T = 1 << 16
+    tr = P.simulate_rsv(THETA, T, seed=6)
+    ch = backend.chain(tr.dataset, THETA)
+    ch.set_latent(tr.latent)
+    held = [ch.get_latent() for _ in range(5)]   # more than the pool holds
+    addrs = {a.ctypes.data for a in held}
+    assert len(addrs) == 5
+    for a in held:
+        assert np.array_equal(a, tr.latent)
+    sub = held[0][100:200]                        # a derived view keeps its buffer alive
+    base_addr = held[0].ctypes.data
+    del held[0]
+    gc.collect()
+    again = [ch.get_latent() for _ in range(4)]
+    assert base_addr not in {a.ctypes.data for a in again}
+    assert np.array_equal(sub, tr.latent[100:200])
+    del sub, again
+    gc.collect()
+    assert ch.get_latent().ctypes.data in addrs   # buffers come back once nothing refers to them
+
+
+def test_data_edits_reach_the_device(backend):
+    T = 2000
+    tr = P.simulate_rsv(THETA, T, seed=8)
+    data = tr.dataset
+    with pytest.raises(ValueError):
+        data.returns[3] = 1.0                     # frozen: no silent in-place edit
+    lp0 = P.log_posterior(tr.latent, THETA, data, backend=backend)
+    y = np.array(data.returns)
+    y[3] = 0.5
+    data.returns = y                              # writable array: uploaded on every call
+    lp1 = P.log_posterior(tr.latent, THETA, data, backend=backend)
+    y[4] = 0.7                                    # in-place edit of the writable array
+    lp2 = P.log_posterior(tr.latent, THETA, data, backend=backend)
+    assert lp0 != lp1 and lp1 != lp2
+    ref = P.log_posterior(tr.latent, THETA, P.Dataset(returns=y, rv=data.rv), backend=backend)
+    assert lp2 == ref

@@ -175,3 +175,24 @@ def test_protocol_fit_matches_reference_formulas():
     assert abs(BP.asymptotic_gain(slow, f) - 5.0) < 1e-12
     with pytest.raises(BP.NumericError):
         BP.fit_linear([(2, 1.0), (2, 2.0)])
+
+
+def test_dataset_arrays_are_private_and_read_only():
+    # a device context reuses its upload only while the data cannot change
+    # (integrator.DeviceChain.set_data); the caller's arrays stay writable
+    import paper_1603_08114_b200 as P
+    from paper_1603_08114_b200.model import is_frozen
+    y = np.linspace(-0.01, 0.01, 16)
+    rv = np.full(16, 1e-4)
+    d = P.Dataset(returns=y, rv=rv)
+    assert is_frozen(d.returns) and is_frozen(d.rv) and is_frozen(d.log_rv)
+    assert y.flags.writeable and d.returns is not y
+    y[0] = 1.0                       # the caller's array is not aliased
+    assert d.returns[0] == -0.01
+    with pytest.raises(ValueError):
+        d.log_rv[0] = 0.0
+    assert not is_frozen(np.zeros(3)) and not is_frozen(np.zeros(3)[1:])
+    v = np.zeros(3)
+    ro = v[:]
+    ro.setflags(write=False)
+    assert not is_frozen(ro)         # a read-only view of a writable base can still change
