@@ -278,9 +278,83 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline(T, L, dt, kind, seconds, data, h0):
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def config_dict(T, L, dt, prng):
+    """The workload description shared verbatim by both arms (the driver
+    compares the two lines' `config`)."""
+    return {"workload": f"config 3: single chain T={T}, L={L}, dt={dt}, {prng}; one step = one full "
+                        "HMC proposal of hmc_update_volatility (momenta + H_old + trajectory + H_new + Metropolis)",
+            "T": T, "L": L, "dt": dt, "prng": prng}
+
+
+def import_reference():
+    """The unmodified reference package (`rsvhmc`, installed into
+    baseline/_ref by pip --target) -- None when absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "rsvhmc")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "rsvhmc_numba_cache"))
+    try:
+        import rsvhmc
+    except Exception:  # numba or numpy missing on the host
+        return None
+    if not os.path.abspath(rsvhmc.__file__).startswith(REF_DIR):
+        return None
+    return rsvhmc
+
+
+def time_reference(T, L, dt, prng, steps, warmup, seconds=None, parallel_steps=2):
+    """The reference's own CPU path on this host: rsvhmc.hmc_update_volatility
+    (sampler.py:144-167) with its numba kernels, once with SerialBackend (one
+    core; integrator.py:50-65) and once with ParallelBackend(nproc)
+    (integrator.py:68-105, default 512-site chunks) -- the stock code path,
+    nothing of this repository on it except the bit generator object feeding
+    numpy's Generator (oracle Stream: the pcg32 / minstd words of DESIGN 6;
+    the reference itself only ships Philox).  Data: the reference's own
+    simulate_rsv(theta, T, seed=0); the chain starts at the true path.
+    Returns None when the reference cannot be imported here."""
+    ref = import_reference()
+    if ref is None:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from rsvhmc import integrator as RI
+    from rsvhmc import sampler as RS
+    theta = ref.Params(**THETA)
+    truth = ref.simulate_rsv(theta, T, seed=0)
+    md = RI.MDConfig(dt, L)
+    out = {}
+    for name, mk, n_steps in (("serial", lambda: RI.SerialBackend(), steps),
+                              ("parallel", lambda: RI.ParallelBackend(os.cpu_count()), parallel_steps)):
+        if n_steps <= 0:
+            continue
+        gen = O.Stream(prng, 1).generator()
+        h = truth.latent.copy()
+        with mk() as be:
+            for _ in range(max(1, warmup if name == "serial" else 1)):  # numba JIT + caches
+                h, _, _ = RS.hmc_update_volatility(h, theta, truth.dataset, md, gen, backend=be)
+            times = []
+            while len(times) < n_steps:
+                t0 = time.perf_counter()
+                h, _, _ = RS.hmc_update_volatility(h, theta, truth.dataset, md, gen, backend=be)
+                times.append(time.perf_counter() - t0)
+                if seconds is not None and sum(times) >= seconds:
+                    break
+        tot = sum(times)
+        out[name] = {"value": T * L * len(times) / tot, "unit": UNIT, "proposals": len(times),
+                     "seconds": tot, "s_per_proposal": tot / len(times),
+                     "cores": 1 if name == "serial" else os.cpu_count()}
+    best = max(out.values(), key=lambda r: r["value"])
+    out["best"] = "serial" if best is out.get("serial") else "parallel"
+    return out
+
+
+def cpu_port(T, L, dt, kind, seconds, data, h0):
     """The reference algorithm restated in C (oracle/, kind 'port'), all host
-    threads for the leapfrog kernels, on a bounded sample of trajectories."""
+    threads for the leapfrog kernels, on a bounded sample of proposals."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     import paper_1603_08114_b200 as P
@@ -299,44 +373,53 @@ def cpu_baseline(T, L, dt, kind, seconds, data, h0):
     O.lib().orc_pool_shutdown()
     return {"value": T * L * n / el, "unit": UNIT, "cores": nth, "kind": "port",
             "sample": f"{n} HMC proposals (momenta+2H+{L}-step trajectory+Metropolis) at T={T}, {el:.1f} s",
-            "trajectories_per_s": n / el, "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+            "trajectories_per_s": n / el}
+
+
+def cpu_baseline(T, L, dt, kind, seconds, data, h0):
+    """cpu_baseline of the b200 line: the reference itself (rsvhmc + numba,
+    SerialBackend -- the faster of its two backends at this size) on a
+    bounded sample, the C port beside it; the port alone when the reference
+    cannot be imported on this host."""
+    port = cpu_port(T, L, dt, kind, seconds, data, h0)
+    ref = time_reference(T, L, dt, kind, steps=10 ** 6, warmup=1, seconds=seconds, parallel_steps=0)
+    host = {"cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    if ref is None:
+        return dict(port, **host, note="reference (baseline/_ref) not importable on this host: the C port")
+    r = ref["serial"]
+    return {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{r['proposals']} proposals of rsvhmc.hmc_update_volatility (SerialBackend, numba) at T={T}, "
+                      f"{r['seconds']:.1f} s",
+            "trajectories_per_s": 1.0 / r["s_per_proposal"], **host, "port": port}
 
 
 def run_reference(args, ws, rank):
+    """--impl reference: the unmodified reference (baseline/_ref) on this
+    host's cores, same metric / config as the b200 arm; rank 0 only."""
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-    import paper_1603_08114_b200 as P
-    theta = P.Params(**THETA)
-    truth = P.simulate_rsv(theta, args.T, seed=0)
-    data = truth.dataset
-    nth = O.max_threads()
-    st = O.Stream(args.prng, 1)
-    h = truth.latent.copy()
-    for _ in range(args.warmup):
-        h, _, _ = O.hmc_update(h, theta, data.returns, data.log_rv, args.dt, args.L, st, nthreads=nth)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        h, _, _ = O.hmc_update(h, theta, data.returns, data.log_rv, args.dt, args.L, st, nthreads=nth)
-        times.append(time.perf_counter() - t0)
-    O.lib().orc_pool_shutdown()
-    tot = sum(times)
-    value = args.T * args.L * args.steps / tot
+    ref = time_reference(args.T, args.L, args.dt, args.prng, args.steps, args.warmup)
+    host = {"cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    if ref is None:  # fall back to the C restatement, and say so
+        import paper_1603_08114_b200 as P
+        truth = P.simulate_rsv(P.Params(**THETA), args.T, seed=0)
+        port = cpu_port(args.T, args.L, args.dt, args.prng, 1e9, truth.dataset, truth.latent)
+        value, cores, kind = port["value"], port["cores"], "port"
+        sample, extra = port["sample"], {"note": "rsvhmc not importable from baseline/_ref: oracle port timed"}
+    else:
+        best = ref[ref["best"]]
+        value, cores, kind = best["value"], best["cores"], "reference"
+        sample = (f"{best['proposals']} proposals of rsvhmc.hmc_update_volatility at T={args.T} "
+                  f"({ref['best']} backend, numba)")
+        extra = {"backends": {k: ref[k] for k in ("serial", "parallel") if k in ref}}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1e3 * args.T * args.L / value, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (simulate_rsv, theta of SURVEY \u00a78d, seed 0)", "impl": "reference",
-            "config": {"workload": f"config 3: single chain T={args.T}, L={args.L}, dt={args.dt}, {args.prng}; one "
-                                   "step = one full HMC proposal (reference CPU algorithm: the oracle port, all host "
-                                   "threads for the leapfrog kernels)",
-                       "T": args.T, "L": args.L, "dt": args.dt, "prng": args.prng},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "port",
-                             "sample": f"{args.steps} HMC proposals at T={args.T}", "cpu_model": cpu_model(),
-                             "nproc": os.cpu_count()},
+            "config": config_dict(args.T, args.L, args.dt, args.prng),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample, **host},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "trajectories_per_s": args.steps / tot}
+            "trajectories_per_s": value / (args.T * args.L), **extra}
     print(json.dumps(line), flush=True)
 
 
@@ -435,11 +518,26 @@ def main():
         n_acc += int(acc)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     zero_copy = be.chain(data, theta).last_update_zero_copy  # h read in place by the trajectory kernel
+    # the same call with a plain (pageable) numpy path, the reference user's usual case
+    # (every step proposes from the same pageable path, so each call copies it in)
+    hp = np.array(h)
+    for _ in range(2):
+        P.hmc_update_volatility(hp, theta, data, md, rng, backend=be)
+    n_acc_p = 0
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        _, acc, _ = P.hmc_update_volatility(hp, theta, data, md, rng, backend=be)
+        n_acc_p += int(acc)
+    e2e_pg_s = (time.perf_counter() - t0) / e2e_steps
     state_bytes = 48 + 40  # stream state + params structs
     e2e = {"value": T * L / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * T + state_bytes,
            "d2h_bytes_per_step": int(8 * T * n_acc / e2e_steps) + 48 + 56,
            "h_in": "read in place over PCIe by the trajectory kernel (zero copy)" if zero_copy else "copied in",
-           "path": "paper_1603_08114_b200.hmc_update_volatility(h numpy[pinned], params, data, md, rng) -> C ABI"}
+           "path": "paper_1603_08114_b200.hmc_update_volatility(h numpy[pinned], params, data, md, rng) -> C ABI",
+           "pageable": {"value": T * L / e2e_pg_s, "unit": UNIT, "h2d_bytes_per_step": 8 * T + state_bytes,
+                        "d2h_bytes_per_step": int(8 * T * n_acc_p / e2e_steps) + 48 + 56,
+                        "h_in": "pageable numpy array: copied in (cudaMemcpy from pageable memory); every "
+                                "step proposes from the same path"}}
 
     extra = {}
     if rank == 0:
@@ -502,12 +600,9 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (simulate_rsv, theta of SURVEY §8d, seed 0)",
-            "config": {"workload": f"config 3 at N=1 per GPU: single chain T={T}, L={L}, dt={dt}, {args.prng}; "
-                                   "one step = one full HMC proposal (momenta + H_old + trajectory + H_new + "
-                                   "Metropolis), device-resident, CUDA graph",
-                       "T": T, "L": L, "dt": dt, "prng": args.prng,
-                       "parallelism": "single chain, 1 GPU",
-                       "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB memset, not timed)"},
+            "config": config_dict(T, L, dt, args.prng),
+            "parallelism": "single chain, 1 GPU; device-resident, one CUDA graph per proposal",
+            "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB memset, not timed)",
             "trajectories_per_s": 1.0 / step_s, "accept_rate": accept_rate,
             "breakdown_ms": {"momenta": mom_ms, "trajectory": traj_ms, "proposal_with_event_nodes": bd_total_ms},
             "in_kernel_us": stamps,
@@ -575,13 +670,11 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
         line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (simulate_rsv, theta of SURVEY \u00a78d, seed 0)",
-                "config": {"workload": f"config 3: one chain T={T}, L={L}, dt={dt}, {args.prng}, time-sharded over "
-                                       f"{ws} GPUs; one step = one full HMC proposal",
-                           "T": T, "L": L, "dt": dt, "prng": args.prng,
-                           "parallelism": f"time-sharded x{ws} (margin {margin} sites, halo every "
-                                          f"{P.sharded.halo_period(margin, L)} proposals, NCCL all_gather of shard "
-                                          "totals, decision on the device)",
-                           "l2": "flushed before every proposal (256 MiB write per GPU, outside the event pairs)"},
+                "config": config_dict(T, L, dt, args.prng),
+                "parallelism": f"time-sharded x{ws} (margin {margin} sites, halo every "
+                               f"{P.sharded.halo_period(margin, L)} proposals, NCCL all_gather of shard "
+                               "totals, decision on the device)",
+                "l2": "flushed before every proposal (256 MiB write per GPU, outside the event pairs)",
                 "trajectories_per_s": 1e3 / ms, "accept_rate": acc, "clocks": clk,
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                         "path": "ShardedChain + sharded.hmc_update_distributed_device (device-resident; results read "
