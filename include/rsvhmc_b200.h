@@ -174,11 +174,12 @@ int rsv_get_timing(rsv_ctx *ctx, double *traj_ms, double *momenta_ms, double *to
 /* Device-side orchestration of a sharded chain (no host synchronisation per
  * proposal; the host only enqueues): rsv_set_stream puts the context on an
  * external CUDA stream (e.g. the one NCCL collectives are ordered on; NULL
- * restores its own).  rsv_shard_propose_async writes this shard's 20 totals
+ * restores its own).  rsv_shard_propose_async writes this shard's 23-word totals
  * (rsv_shard_totals layout, u_word / words_used as bit patterns) to device
  * memory; after an all-gather of every rank's totals, rsv_shard_decide_async
- * takes the Metropolis decision on the device (fixed-order compensated sums:
- * the same decision on every rank) and advances the stream / flips the path;
+ * takes the Metropolis decision on the device (exact integer sums of the
+ * fixed-point dH / H parts, fixed-order compensated sums of the moments: the
+ * same decision on every rank, and the same dH bits for any world size) and advances the stream / flips the path;
  * rsv_shard_halo_async packs the owned boundary sites of the current path
  * (unpack = 0: left gets [own_lo, own_lo + nl), right [own_hi - nr, own_hi))
  * or writes received margins (unpack = 1); rsv_shard_results returns the
@@ -272,7 +273,13 @@ int64_t rsv_launch_count(const rsv_ctx *ctx);
  * combines the shards' totals in rank order (bitwise independent of the
  * shard count's scheduling), decides (same u on every shard) and applies. */
 typedef struct {
-  double part[14];     /* dH, H_old, H_new (variable parts), 5 old stats, 5 new stats, divergence flag */
+  int64_t dh[2];       /* dH over the owned sites: sum of per-group values (4-aligned groups of 4 global sites)
+                          as 128-bit fixed point, value * 2^64 rounded toward zero, {low, high} words */
+  int64_t h_old[2];    /* the variable part of H_old, same encoding */
+  int64_t h_new[2];    /* the variable part of H_new, same encoding */
+  double stats_old[5]; /* theta moments of the current path (sum d, d^2, d_t d_{t-1}, e, e^2) */
+  double stats_new[5]; /* ... of the proposal */
+  double flag;         /* > 0: a kick flagged |h| > 50 (or an energy beyond the fixed-point range) */
   double ends[4];      /* d_0 old, d_{T-1} old, d_0 new, d_{T-1} new (0 unless owned) */
   uint64_t u_word;     /* raw word after the momenta: the Metropolis uniform */
   uint64_t words_used; /* raw words consumed by the momenta */

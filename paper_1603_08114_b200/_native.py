@@ -44,9 +44,10 @@ class Result(ctypes.Structure):
                 ("u", ctypes.c_double)]
 
 
-class ShardTotals(ctypes.Structure):
-    _fields_ = [("part", ctypes.c_double * 14), ("ends", ctypes.c_double * 4), ("u_word", ctypes.c_uint64),
-                ("words_used", ctypes.c_uint64)]
+class ShardTotals(ctypes.Structure):  # rsv_shard_totals: 23 8-byte words
+    _fields_ = [("dh", ctypes.c_int64 * 2), ("h_old", ctypes.c_int64 * 2), ("h_new", ctypes.c_int64 * 2),
+                ("stats_old", ctypes.c_double * 5), ("stats_new", ctypes.c_double * 5), ("flag", ctypes.c_double),
+                ("ends", ctypes.c_double * 4), ("u_word", ctypes.c_uint64), ("words_used", ctypes.c_uint64)]
 
 
 class Bitgen(ctypes.Structure):  # numpy/random/bitgen.h

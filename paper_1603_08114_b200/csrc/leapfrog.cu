@@ -51,17 +51,20 @@ __device__ __forceinline__ double exp_neg(double d, const unsigned long long *ta
   return fma(S, q, S);
 }
 
-// Same evaluation, constants taken from the kernel's parameter block so the
-// hot loop uses constant-bank operands (no per-iteration immediates).
+// e^{-d} of the step loop, on the scaled state x = K d (K = 2048 / ln 2,
+// DESIGN.md 4.2): n = rint(-x) by the magic-number add, f = -x - n exactly
+// (|f| <= 1/2, no Cody-Waite split), e^{f ln2/2048} - 1 by a degree-3 Horner
+// polynomial in f, and S = 2^(n/2048) from the scale-ready table as above.
+// 7 FP64 instructions (3 DADD, 3 DFMA / DMUL, 1 DFMA), constants from the
+// kernel's parameter block (constant-bank operands).
 template <typename K>
-__device__ __forceinline__ double exp_neg_k(double d, const unsigned long long *tab, double &t, const K &k) {
-  t = fma(-d, k.e_k, MAGIC);
+__device__ __forceinline__ double exp_neg_x(double x, const unsigned long long *tab, double &t, const K &k) {
+  t = MAGIC - x;
   const double nd = t - MAGIC;
-  double r = fma(nd, -k.e_hi, -d);
-  r = fma(nd, -k.e_lo, r);
-  double q = fma(r, k.e_c3, 0.5);
-  q = fma(q, r, 1.0);
-  q = q * r;
+  const double f = -x - nd;
+  double q = fma(f, k.ex3, k.ex2);
+  q = fma(q, f, k.ex1);
+  q = q * f;
   const int n = __double2loint(t);
   const unsigned long long tb = tab[n & (RSV_EXP_TAB_N - 1)];
   const double S = __hiloint2double((int)(tb >> 32) + (n << EXP_HI_SHIFT), (int)(unsigned)tb);
@@ -77,35 +80,33 @@ __device__ __forceinline__ bool out_of_range(double t, int n_lo, int n_span) {
 }
 
 
-// Variable part of H at one site (the theta-only constants are added in
-// the Metropolis step): 0.5 p^2 + 0.5 d + a e^{-mu} e^{-d} + (q-d)^2/2su2 + AR.
-template <bool KIN = true>
-__device__ __forceinline__ double site_energy(double d, double dprev, double p, double ae, double q, bool first,
-                                              const TrajConsts &s, const unsigned long long *tab) {
+// Variable potential part of H at one site (the theta-only constants are
+// added in the Metropolis step): 0.5 d + a e^{-mu} e^{-d} + (q-d)^2/2su2 + AR.
+__device__ __forceinline__ double site_potential(double d, double dprev, double ae, double q, bool first,
+                                                 const TrajConsts &s, const unsigned long long *tab) {
   double t;
   const double E = exp_neg(d, tab, t);
   const double r = q - d;
   const double tr = d - s.phi * dprev;
   const double ar = first ? s.one_m_phi2 * d * d * s.inv2se : tr * tr * s.inv2se;
-  if (!KIN) return 0.5 * d + ae * E + r * r * s.inv2su + ar;  // potential part (momenta not yet drawn)
-  return 0.5 * p * p + 0.5 * d + ae * E + r * r * s.inv2su + ar;
+  return 0.5 * d + ae * E + r * r * s.inv2su + ar;
 }
 
-// Energies and statistics of the thread's owned core sites (branch-free on
-// the common path; `edge` threads handle the global first site).
-// firstm bit r: site r is the first of its series (stationary AR prior, no
-// predecessor term).
-// KIN = false: the potential part only (the caller adds 0.5 p^2 later).
-template <int R, bool STATS = true, bool KIN = true>
-__device__ __forceinline__ void tile_energy(const double (&d)[R], const double (&p)[R], const double (&av)[R],
-                                            const double (&lv)[R], double dl, uint32_t core, uint32_t firstm,
-                                            const TrajConsts &s, const unsigned long long *tab, double (&v)[6]) {
+// Potential energy and statistics of the thread's owned core sites, summed
+// in site order (branch-free on the common path).  firstm bit r: site r is
+// the first of its series (stationary AR prior, no predecessor term).  The
+// kinetic part is added by the caller (kinetic()), in the same order for
+// every tile, so a group's H is the same value whatever tile it falls in.
+template <int R, bool STATS = true>
+__device__ __forceinline__ void tile_energy(const double (&d)[R], const double (&av)[R], const double (&lv)[R],
+                                            double dl, uint32_t core, uint32_t firstm, const TrajConsts &s,
+                                            const unsigned long long *tab, double (&v)[6]) {
 #pragma unroll
   for (int r = 0; r < R; r++) {
     const double dprev = r ? d[r - 1] : dl;
     const double q = lv[r] - s.xm;
     const bool first = (firstm >> r) & 1;
-    const double en = site_energy<KIN>(d[r], dprev, p[r], s.emu * av[r], q, first, s, tab);
+    const double en = site_potential(d[r], dprev, s.emu * av[r], q, first, s, tab);
     const bool c = (core >> r) & 1;
     v[0] += c ? en : 0.0;
     if (STATS) {
@@ -118,46 +119,71 @@ __device__ __forceinline__ void tile_energy(const double (&d)[R], const double (
     }
   }
 }
-
-// Exchange the first / last register site with the neighbouring threads.
-template <int NW>
-__device__ __forceinline__ void exchange(double first, double last, double &left, double &right, double *s_first,
-                                         double *s_last, int lane, int warp) {
-  left = __shfl_up_sync(0xffffffffu, last, 1);
-  right = __shfl_down_sync(0xffffffffu, first, 1);
-  if (lane == 31) s_last[warp] = last;
-  if (lane == 0) s_first[warp] = first;
-  __syncthreads();
-  if (lane == 0) left = warp > 0 ? s_last[warp - 1] : 0.0;
-  if (lane == 31) right = warp < NW - 1 ? s_first[warp + 1] : 0.0;
+template <int R>
+__device__ __forceinline__ double kinetic(const double (&p)[R], uint32_t core) {
+  double k = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; r++) k += ((core >> r) & 1) ? 0.5 * p[r] * p[r] : 0.0;
+  return k;
 }
 
-// Fixed-order block sum (deterministic): warp butterflies, then warp totals
-// in warp order by thread 0.
-template <int NV, int NW>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double *s_red, int lane, int warp) {
-#pragma unroll
-  for (int k = 0; k < NV; k++) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; k++) s_red[warp * NV + k] = v[k];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; k++) {
-      double acc = s_red[k];
-      for (int w = 1; w < NW; w++) acc += s_red[w * NV + k];
-      v[k] = acc;
-    }
-  }
+// Round-toward-zero of v * 2^64 as a 128-bit integer (exact for the 53-bit
+// significand down to 2^-64; the caller keeps |v| < 2^62).  Integer sums of
+// these are associative: the reductions of dH, H_old and H_new give the same
+// bits for any grouping of the partials.
+__device__ __forceinline__ __int128 fix128(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const int ex = (int)((b >> 52) & 0x7ff);
+  const unsigned long long m = (b & 0xFFFFFFFFFFFFFull) | (ex ? 0x10000000000000ull : 0ull);
+  const int sh = ex - 1075 + 64;  // v * 2^64 = m * 2^sh
+  __int128 r;
+  if (sh >= 0) r = (__int128)m << (sh < 74 ? sh : 74);
+  else r = (__int128)(sh > -64 ? m >> (-sh) : 0ull);
+  return (b >> 63) ? -r : r;
+}
+__device__ __forceinline__ double unfix128(__int128 q) {  // nearest double of q * 2^-64
+  const bool neg = q < 0;
+  const unsigned __int128 a = neg ? (unsigned __int128)(-q) : (unsigned __int128)q;
+  const unsigned long long hi = (unsigned long long)(a >> 64), lo = (unsigned long long)a;
+  // hi + lo 2^-64, both exact in two doubles up to rounding of the sum
+  const double r = __ull2double_rn(hi) + __ull2double_rn(lo) * 0x1p-64;
+  return neg ? -r : r;
+}
+__device__ __forceinline__ __int128 shfl_xor_128(__int128 v, int o) {
+  const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+  const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+  return (__int128)(((unsigned __int128)h2 << 64) | l2);
+}
+__device__ __forceinline__ __int128 ld128(const long long (&w)[2]) {
+  return (__int128)(((unsigned __int128)(unsigned long long)w[1] << 64) | (unsigned long long)w[0]);
+}
+__device__ __forceinline__ void st128(long long (&w)[2], __int128 v) {
+  w[0] = (long long)(unsigned long long)v;
+  w[1] = (long long)(v >> 64);
+}
+// 128-bit sums through 64-bit atomics: q = L0 + L1 2^42 + L2 2^84 with
+// L0, L1 in [0, 2^42) and L2 signed; sums of up to 2^22 such limbs fit a
+// 64-bit word, and the total is rebuilt exactly (mod 2^128)
+__device__ __forceinline__ void fx_add(unsigned long long *fx, __int128 q) {
+  const unsigned __int128 u = (unsigned __int128)q;
+  const unsigned long long l0 = (unsigned long long)u & ((1ull << 42) - 1);
+  const unsigned long long l1 = (unsigned long long)(u >> 42) & ((1ull << 42) - 1);
+  const unsigned long long l2 = (unsigned long long)(long long)(q >> 84);
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(fx + 0), "l"(l0) : "memory");
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(fx + 1), "l"(l1) : "memory");
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(fx + 2), "l"(l2) : "memory");
+}
+__device__ __forceinline__ __int128 fx_total(const unsigned long long *fx) {
+  return (__int128)fx[0] + ((__int128)fx[1] << 42) + ((__int128)(long long)fx[2] << 84);
 }
 
-// One kick p -= dt * dU/dh for the thread's R sites (d-space):
-//   p <- p - Cd - G d + beta phi (d_{i-1} + d_{i+1}) + Ad e^{-d}
+// energies beyond 2^62 per group (or non-finite) cannot be represented: they
+// poison the sum to a non-finite dH, which the Metropolis step rejects
+constexpr double FIX_MAX = 0x1p62;
+
+// One kick p -= dt * dU/dh for the thread's R sites, on x = K (h - mu):
+//   p <- p - Cd - (G/K) x + (beta phi/K) (x_{i-1} + x_{i+1}) + Ad e^{-x/K}
+// (d-space form: p - Cd - G d + beta phi (d_{i-1} + d_{i+1}) + Ad e^{-d}).
 // The divergence test (|h| > 50) is accumulated as the largest
 // (unsigned)(n - n_lo) over the thread's core sites and checked once at the
 // end; NaN or astronomically large states (which no longer map to a sane n)
@@ -173,15 +199,15 @@ __device__ __forceinline__ void kick(double (&d)[R], double (&p)[R], const doubl
     const double dm = r ? d[r - 1] : dl;
     const double dp = r < R - 1 ? d[r + 1] : dr;
     double t;
-    const double E = exp_neg_k(d[r], tab, t, s);
+    const double E = exp_neg_x(d[r], tab, t, s);
     // lean warps: each thread's sites are all core or none (the caller keeps
     // the thread's maximum only in the first case), so no per-site mask
     if (EDGE) nmax = max(nmax, ((unsigned)__double2loint(t) - (unsigned)s.n_lo) & cm[r]);
     else nmax = max(nmax, (unsigned)__double2loint(t) - (unsigned)s.n_lo);
-    const double G = EDGE && ((endm >> r) & 1) ? s.g_end : s.g_int;
+    const double G = EDGE && ((endm >> r) & 1) ? s.xg_end : s.xg_int;
     double pp = p[r] - Cd[r];
     pp = fma(-G, d[r], pp);
-    pp = fma(s.bphi, dm + dp, pp);
+    pp = fma(s.xbphi, dm + dp, pp);
     pp = fma(Ad[r], E, pp);
     p[r] = (EDGE && !((live >> r) & 1)) ? 0.0 : pp;
   }
@@ -193,9 +219,16 @@ __device__ __forceinline__ void drift(double (&d)[R], const double (&p)[R], doub
   for (int r = 0; r < R; r++) d[r] = fma(c, p[r], d[r]);
 }
 
+// Ghost-lane refresh slots of one thread (see ghost_lanes below): `w` the
+// slot this lane writes (lanes 1 / 30), `r` the slot it reads (lanes 0 / 31
+// with a neighbour warp), null otherwise; the two parities alternate.
+struct GhostSlots {
+  double *w;
+  const double *r;
+};
+
 template <int R, int NT>
-__device__ __forceinline__ void ghost_refresh(double (&d)[R], double (&p)[R], double *s_gx, int lane, int warp,
-                                              int parity);
+__device__ __forceinline__ void ghost_refresh(double (&d)[R], double (&p)[R], const GhostSlots &g, int parity);
 
 // The L leapfrog steps of a tile (integrator.py:149-179), unrolled by the
 // ghost-refresh period R: loop control and the refresh test once per R
@@ -205,12 +238,12 @@ template <bool EDGE, int R, int NT, bool FUSE, bool ENS>
 __device__ __forceinline__ void run_steps(double (&d)[R], double (&p)[R], const double (&Ad)[R],
                                           const double (&Cd)[R], const TrajConsts &s,
                                           const unsigned long long *tab, uint32_t live, uint32_t endm,
-                                          const unsigned (&cm)[R], bool cf, bool cl, int L, double *gx, int lane,
-                                          int warp, unsigned &nmax) {
+                                          const unsigned (&cm)[R], bool cf, bool cl, int L, const GhostSlots &gs,
+                                          unsigned &nmax) {
   constexpr int NW = NT / 32;
   int gpar = 0;
   auto one = [&](int step) {
-    if (!FUSE) drift(d, p, s.c_half);
+    if (!FUSE) drift(d, p, s.xc_half);
     // lanes 0 / 31 get their own value back: those are ghost lanes (or the
     // CTA window edges, inside the halo) whose stale values never reach a
     // core site; next to a global end the neighbour lane is non-live (d = 0)
@@ -221,21 +254,21 @@ __device__ __forceinline__ void run_steps(double (&d)[R], double (&p)[R], const 
       dr = cl ? 0.0 : dr;
     }
     kick<EDGE, R>(d, p, Ad, Cd, dl, dr, s, tab, live, endm, cm, nmax);
-    if (FUSE) drift(d, p, step < L - 1 ? s.c_full : s.c_half);
-    else drift(d, p, s.c_half);
+    if (FUSE) drift(d, p, step < L - 1 ? s.xc_full : s.xc_half);
+    else drift(d, p, s.xc_half);
   };
-  if (FUSE) drift(d, p, s.c_half);
+  if (FUSE) drift(d, p, s.xc_half);
   int step = 0;
   for (; step + R <= L; step += R) {
 #pragma unroll
     for (int u = 0; u < R; u++) one(step + u);
     if (NW > 1 && step + R < L) {
-      ghost_refresh<R, NT>(d, p, gx, lane, warp, gpar);
+      ghost_refresh<R, NT>(d, p, gs, gpar);
       gpar ^= 1;
     }
   }
   for (; step < L; step++) one(step);
-  if (NW > 1) ghost_refresh<R, NT>(d, p, gx, lane, warp, gpar);
+  if (NW > 1) ghost_refresh<R, NT>(d, p, gs, gpar);
 }
 
 // Metropolis step (sampler.py:155-167) on the tile partials, run by the last
@@ -261,27 +294,38 @@ __device__ __forceinline__ void metropolis(const TrajArgs &A, double *s_v) {
 // R steps).  Core lanes (1..30) are always exact; a site belongs to the one
 // warp whose core lane holds it.
 template <int R, int NT>
-__device__ __forceinline__ void ghost_refresh(double (&d)[R], double (&p)[R], double *s_gx, int lane, int warp,
-                                              int parity) {
+__device__ __forceinline__ GhostSlots ghost_lanes(double *s_gx, int lane, int warp) {
   constexpr int NW = NT / 32;
   // s_gx layout: [parity][warp][side 0: lane 30 -> right neighbour's lane 0,
   //                                side 1: lane 1 -> left neighbour's lane 31][2R]
-  double *slot = s_gx + (size_t)parity * NW * 4 * R;
-  if (lane == 30 || lane == 1) {
-    double *dst = slot + (warp * 2 + (lane == 1)) * 2 * R;
+  GhostSlots g;
+  g.w = (lane == 30 || lane == 1) ? s_gx + (warp * 2 + (lane == 1)) * 2 * R : nullptr;
+  g.r = (lane == 0 && warp > 0)        ? s_gx + ((warp - 1) * 2 + 0) * 2 * R
+        : (lane == 31 && warp < NW - 1) ? s_gx + ((warp + 1) * 2 + 1) * 2 * R
+                                        : nullptr;
+  return g;
+}
+template <int R, int NT>
+__device__ __forceinline__ void ghost_refresh(double (&d)[R], double (&p)[R], const GhostSlots &g, int parity) {
+  constexpr int PO = (NT / 32) * 4 * R;  // doubles per parity
+  static_assert(R % 2 == 0, "16-byte slot accesses");
+  if (g.w) {
+    double2 *dst = reinterpret_cast<double2 *>(g.w + parity * PO);
 #pragma unroll
-    for (int r = 0; r < R; r++) { dst[r] = d[r]; dst[R + r] = p[r]; }
+    for (int r = 0; r < R; r += 2) {
+      dst[r / 2] = make_double2(d[r], d[r + 1]);
+      dst[R / 2 + r / 2] = make_double2(p[r], p[r + 1]);
+    }
   }
   __syncthreads();
-  if (lane == 0 && warp > 0) {
-    const double *src = slot + ((warp - 1) * 2 + 0) * 2 * R;
+  if (g.r) {
+    const double2 *src = reinterpret_cast<const double2 *>(g.r + parity * PO);
 #pragma unroll
-    for (int r = 0; r < R; r++) { d[r] = src[r]; p[r] = src[R + r]; }
-  }
-  if (lane == 31 && warp < NW - 1) {
-    const double *src = slot + ((warp + 1) * 2 + 1) * 2 * R;
-#pragma unroll
-    for (int r = 0; r < R; r++) { d[r] = src[r]; p[r] = src[R + r]; }
+    for (int r = 0; r < R; r += 2) {
+      const double2 a = src[r / 2], b = src[R / 2 + r / 2];
+      d[r] = a.x; d[r + 1] = a.y;
+      p[r] = b.x; p[r + 1] = b.y;
+    }
   }
 }
 
@@ -294,223 +338,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do {                                                                                \
     if (A.dbg && threadIdx.x == 0) A.dbg[(size_t)blockIdx.x * 8 + (k)] = gtimer(); \
   } while (0)
-
-template <int R, int NT, int MINB, bool FUSE>
-__global__ void __launch_bounds__(NT, MINB) traj_kernel(TrajArgs A) {
-  constexpr int NW = NT / 32;
-  constexpr int WSTEP = 30 * R;  // window advance per warp
-  RSV_STAMP(0);
-  __shared__ unsigned long long s_tab[RSV_EXP_TAB_N];
-  __shared__ double s_first[NW], s_last[NW];
-  __shared__ double s_red[NW * TR_NV];
-  __shared__ double s_v[NW * TR_NV + TR_NV];
-  __shared__ double s_gx[2 * NW * 4 * R];
-  __shared__ double s_old[6 * NT];
-  __shared__ int s_last_tile;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < RSV_EXP_TAB_N; i += NT) s_tab[i] = g_exp_tab2[i];
-
-  const TrajConsts &s = A.k;
-  const double *hsrc;
-  double *hdst;
-  if (A.h_src) {
-    hsrc = A.h_src;
-    hdst = A.h_dst;
-  } else {
-    const int cur = A.ctrl->cur;
-    hsrc = cur ? A.hbuf1 : A.hbuf0;
-    hdst = cur ? A.hbuf0 : A.hbuf1;
-  }
-  const int64_t T = A.T;
-  const int H = A.g.halo;                    // multiple of R (>= n_steps + 1)
-  const int64_t t0 = (int64_t)blockIdx.x * A.g.core;  // core is a multiple of R
-  const int64_t t1 = min(t0 + A.g.core, T);
-  // live range [t0 - H, t1 + H): lanes start on multiples of R, so only the
-  // lanes at the global ends of the series hold partially live sites
-  const int64_t lo_live = max((int64_t)0, t0 - H), hi_live = min(T, t1 + H);
-  const int64_t g0 = t0 - H + (int64_t)warp * WSTEP + (int64_t)lane * R;
-  const bool own_lane = (lane >= 1 && lane <= 30) || (lane == 0 && warp == 0) || (lane == 31 && warp == NW - 1);
-
-  // ---- load: vectorised when the lane's R sites are all live ----
-  double d[R], p[R], av[R], lv[R];
-  const bool full = g0 >= lo_live && g0 + R <= hi_live;
-  if (full) {
-#pragma unroll
-    for (int r = 0; r < R; r += 2) {
-      const double2 h2 = __ldg(reinterpret_cast<const double2 *>(hsrc + g0 + r));
-      const double2 p2 = __ldg(reinterpret_cast<const double2 *>(A.p_in + g0 + r));
-      const double2 a2 = __ldg(reinterpret_cast<const double2 *>(A.a + g0 + r));
-      const double2 l2 = __ldg(reinterpret_cast<const double2 *>(A.lrv + g0 + r));
-      d[r] = h2.x; d[r + 1] = h2.y;
-      p[r] = p2.x; p[r + 1] = p2.y;
-      av[r] = a2.x; av[r + 1] = a2.y;
-      lv[r] = l2.x; lv[r + 1] = l2.y;
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      const int64_t gi = g0 + r;
-      const bool in = gi >= lo_live && gi < hi_live;
-      d[r] = in ? hsrc[gi] : s.mu;
-      p[r] = in ? A.p_in[gi] : 0.0;
-      av[r] = in ? A.a[gi] : 0.0;
-      lv[r] = in ? A.lrv[gi] : 0.0;
-    }
-  }
-  uint32_t live = 0, core = 0, endm = 0;
-  double Ad[R], Cd[R];
-  unsigned cm[R];
-#pragma unroll
-  for (int r = 0; r < R; r++) {
-    const int64_t gi = g0 + r;
-    const bool in = gi >= lo_live && gi < hi_live;
-    const bool c = in && own_lane && gi >= t0 && gi < t1;
-    live |= (uint32_t)in << r;
-    core |= (uint32_t)c << r;
-    endm |= (uint32_t)(gi == 0 || gi == T - 1) << r;
-    cm[r] = c ? ~0u : 0u;
-    d[r] = d[r] - s.mu;
-    Ad[r] = s.dt * (s.emu * av[r]);
-    Cd[r] = in ? fma(-s.alpha, lv[r] - s.xm, s.half_dt) : 0.0;
-  }
-  const bool any_live = live != 0;
-  const bool edge = (any_live && live != (1u << R) - 1) || endm;
-  __syncthreads();  // s_tab
-
-  // ---- H_old and statistics of the current path (owned core sites) ----
-  double hold;
-  {
-    double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-    double v[6] = {0, 0, 0, 0, 0, 0};
-    tile_energy<R>(d, p, av, lv, dl, core, (edge && g0 <= 0 && g0 + R > 0) ? 1u << (int)(-g0) : 0u, s, s_tab, v);
-    hold = v[0];
-    asm volatile("" ::: "memory");
-#pragma unroll
-    for (int k = 0; k < 6; k++) s_old[k * NT + tid] = v[k];  // reduced with the new ones at the end
-    if (edge && !A.h_src) {
-#pragma unroll
-      for (int r = 0; r < R; r++) {
-        if ((core >> r) & 1) {
-          if (g0 + r == 0) A.ctrl->ends_old[0] = d[r];
-          if (g0 + r == T - 1) A.ctrl->ends_old[1] = d[r];
-        }
-      }
-    }
-  }
-
-  // ---- the trajectory: shuffles only, ghost lanes refreshed every R steps ----
-  RSV_STAMP(2);
-  const bool masked = edge || (core != 0 && core != (1u << R) - 1);
-  unsigned nmax = 0;
-  const int L = A.n_steps;
-  int parity = 0;
-  if (FUSE) drift(d, p, s.c_half);
-  for (int step = 0; step < L; step++) {
-    if (!FUSE) drift(d, p, s.c_half);
-    double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-    double dr = __shfl_down_sync(0xffffffffu, d[0], 1);
-    if (lane == 0) dl = 0.0;   // window edges: stale ghosts, never read by core results
-    if (lane == 31) dr = 0.0;
-    if (masked) kick<true, R>(d, p, Ad, Cd, dl, dr, s, s_tab, live, endm, cm, nmax);
-    else if (any_live) kick<false, R>(d, p, Ad, Cd, dl, dr, s, s_tab, live, endm, cm, nmax);
-    if (FUSE) drift(d, p, step < L - 1 ? s.c_full : s.c_half);
-    else drift(d, p, s.c_half);
-    if (NW > 1 && (step + 1) % R == 0 && step + 1 < L) {
-      ghost_refresh<R, NT>(d, p, s_gx, lane, warp, parity);
-      parity ^= 1;
-    }
-  }
-  if (NW > 1) ghost_refresh<R, NT>(d, p, s_gx, lane, warp, parity);  // exact d_{i-1} for the energies
-  if (!masked && !core) nmax = 0;  // the lean kick does not mask non-core sites
-  const bool bad = nmax > (unsigned)s.n_span;
-  RSV_STAMP(3);
-
-  // ---- H_new, statistics of the proposal, write-back ----
-  {
-    // reload the static per-site data (L2-resident) rather than holding it
-    // in registers through the trajectory
-    if (full) {
-#pragma unroll
-      for (int r = 0; r < R; r += 2) {
-        const double2 a2 = __ldg(reinterpret_cast<const double2 *>(A.a + g0 + r));
-        const double2 l2 = __ldg(reinterpret_cast<const double2 *>(A.lrv + g0 + r));
-        av[r] = a2.x; av[r + 1] = a2.y;
-        lv[r] = l2.x; lv[r + 1] = l2.y;
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < R; r++) {
-        const int64_t gi = g0 + r;
-        const bool in = gi >= lo_live && gi < hi_live;
-        av[r] = in ? A.a[gi] : 0.0;
-        lv[r] = in ? A.lrv[gi] : 0.0;
-      }
-    }
-    double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-    double v[6] = {0, 0, 0, 0, 0, 0};
-    tile_energy<R>(d, p, av, lv, dl, core, (edge && g0 <= 0 && g0 + R > 0) ? 1u << (int)(-g0) : 0u, s, s_tab, v);
-    const int64_t gi0 = g0;
-    if (full && core == (1u << R) - 1) {
-#pragma unroll
-      for (int r = 0; r < R; r += 2) {
-        *reinterpret_cast<double2 *>(hdst + gi0 + r) = make_double2(d[r] + s.mu, d[r + 1] + s.mu);
-        if (A.p_out) *reinterpret_cast<double2 *>(A.p_out + gi0 + r) = make_double2(p[r], p[r + 1]);
-      }
-    } else if (core) {
-#pragma unroll
-      for (int r = 0; r < R; r++) {
-        if ((core >> r) & 1) {
-          hdst[gi0 + r] = d[r] + s.mu;
-          if (A.p_out) A.p_out[gi0 + r] = p[r];
-        }
-      }
-    }
-    if (edge && !A.h_src) {
-#pragma unroll
-      for (int r = 0; r < R; r++) {
-        if ((core >> r) & 1) {
-          if (g0 + r == 0) A.ctrl->ends_new[0] = d[r];
-          if (g0 + r == T - 1) A.ctrl->ends_new[1] = d[r];
-        }
-      }
-    }
-    double w[TR_NV];
-    w[0] = v[0] - hold;
-    w[1] = s_old[0 * NT + tid];
-    w[2] = v[0];
-#pragma unroll
-    for (int k = 0; k < 5; k++) {
-      w[3 + k] = s_old[(k + 1) * NT + tid];
-      w[8 + k] = v[1 + k];
-    }
-    w[13] = bad ? 1.0 : 0.0;
-    __syncthreads();  // s_red reuse
-    block_sum<TR_NV, NW>(w, s_red, lane, warp);
-    if (tid == 0) {
-      TilePart *tp = A.parts + blockIdx.x;
-      tp->dh = w[0];
-      tp->hold = w[1];
-      tp->hnew = w[2];
-      for (int k = 0; k < 5; k++) {
-        tp->so[k] = w[3 + k];
-        tp->sn[k] = w[8 + k];
-      }
-      tp->flag = w[13];
-      __threadfence();
-      const unsigned done = atomicAdd(&A.ctrl->tiles_done, 1u);
-      s_last_tile = (done == (unsigned)gridDim.x - 1);
-    }
-  }
-  RSV_STAMP(4);
-  __syncthreads();
-  if (s_last_tile) {
-    __threadfence();
-    metropolis<NT>(A, s_v);
-    RSV_STAMP(5);
-  }
-  (void)s_first;
-  (void)s_last;
-}
 
 // ---------------------------------------------------------------------------
 // Persistent, TMA-staged trajectory kernel.  The grid is MINB CTAs per SM;
@@ -588,25 +415,35 @@ __device__ __forceinline__ void stage_tile_ens(const TrajArgs &A, int tile, doub
   tma_load_1d(stage + 3 * W + off, A.lrv + lo, bytes, bar);
 }
 
-template <int R, int NT>
+template <int R, int NT, bool STATS>
 struct PersistSmem {
   static constexpr int NW = NT / 32;
   static constexpr int W = NW > 1 ? NW * 30 * R + 2 * R : 32 * R;
-  double stage[2][4 * W];       // double-buffered tile windows
-  double acc[TR_NV * NT];       // per-thread partials across tiles
+  static constexpr int NM = STATS ? 10 : 1;
+  union {
+    double stage[2][4 * W];     // double-buffered tile windows
+    double red[NW * TR_NV];     // after the last tile: warp totals of the CTA reduction
+  };
+  __int128 acc3[3][NT];         // per-thread fixed-point dh, H_old, H_new across tiles
+  double accm[NM][NT];          // per-thread theta moments across tiles (old 5, new 5)
   double gx[2 * NW * 4 * R];    // ghost-lane refresh slots
-  double red[NW * TR_NV];
   double v[NW * TR_NV + TR_NV];
   alignas(16) unsigned long long tab[RSV_EXP_TAB_N];
   double epart[2][NW][8];  // ensemble: per-warp chain partials of a tile (by staging buffer)
   uint64_t bar[4];  // two staging buffers, the exp table, the first tile's momenta
   int last;
+  int next[2];     // the CTA's next tile (by staging buffer: read after the tile, rewritten two tiles later)
 };
 
 template <int R, int NT, int MINB, bool FUSE, bool STATS, bool ENS = false, bool DEVK = false>
 __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
-  using SM = PersistSmem<R, NT>;
+  using SM = PersistSmem<R, NT, STATS>;
   constexpr int NW = SM::NW, W = SM::W;
+  // Without statistics every reduced value is a fixed-point integer sum, so
+  // tiles can go to whichever CTA is free (dynamic scheduling: the two CTAs
+  // of an SM do not finish a tile apart); the FP64 moments of the statistics
+  // variant keep the static, fixed-order assignment.
+  constexpr bool DYN = !STATS;
   constexpr int WSTEP = 30 * R;
   extern __shared__ __align__(128) unsigned char psmem[];
   SM &S = *reinterpret_cast<SM *>(psmem);
@@ -620,6 +457,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     sk.mu = q.mu; sk.phi = q.phi; sk.alpha = q.alpha; sk.bphi = q.bphi; sk.g_int = q.g_int;
     sk.g_end = q.g_end; sk.emu = q.emu; sk.xm = q.xm; sk.inv2su = q.inv2su; sk.inv2se = q.inv2se;
     sk.one_m_phi2 = q.one_m_phi2; sk.hconst = q.hconst; sk.n_lo = q.n_lo; sk.n_span = q.n_span;
+    sk.xg_int = q.xg_int; sk.xg_end = q.xg_end; sk.xbphi = q.xbphi;
   }
   const TrajConsts &s = DEVK ? sk : A.k;
   const double *hsrc;
@@ -634,7 +472,10 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   }
   if (tid == 0 && blockIdx.x == 0) A.ctrl->t_stamp[2] = gtimer();
   const unsigned long long t_entry = A.dbg ? gtimer() : 0ull;
-  for (int k = 0; k < TR_NV; k++) S.acc[k * NT + tid] = 0.0;
+  for (int k = 0; k < 3; k++) S.acc3[k][tid] = 0;
+  for (int k = 0; k < SM::NM; k++) S.accm[k][tid] = 0.0;
+  bool bad = false;  // a core site flagged at a kick / an energy beyond the fixed-point range
+  int n_done = 0;
   const int n_tiles = A.g.n_tiles;
   int tile = blockIdx.x;
   if (tid == 0) {
@@ -663,33 +504,49 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   const int64_t goff = A.goff; // global index of local site 0
   const int64_t Tg = A.Tg;     // global series length
   const int H = A.g.halo;
+  const int64_t core_len = A.g.core;
   const bool own_lane = (lane >= 1 && lane <= 30) || (lane == 0 && warp == 0) || (lane == 31 && warp == NW - 1);
   const int lw = warp * WSTEP + lane * R;  // my first site inside the window
-  uint32_t parity[2] = {0, 0};
+  const GhostSlots gs = ghost_lanes<R, NT>(S.gx, lane, warp);
+  // Interior tiles (window inside the local range, core fully owned, no
+  // global end site and no chain boundary in the window) need no per-site
+  // masks: every window site is live (sites past the halo only ever feed
+  // sites outside the core) and the thread's core mask is the same for every
+  // such tile (H and the core are multiples of R: all of a thread's sites
+  // are core or none), so it is computed once here.
+  uint32_t core_int = 0;
+#pragma unroll
+  for (int r = 0; r < R; r++) core_int |= (uint32_t)(own_lane && lw + r >= H && lw + r < H + core_len) << r;
+  unsigned parity = 0;  // bit b: mbarrier phase of staging buffer b
   int buf = 0;
-  long long cyc_wait = 0, cyc_pre = 0, cyc_loop = 0, cyc_post = 0, c0, c1;
+  long long cyc_wait = 0, cyc_pre = 0, cyc_loop = 0, cyc_post = 0, c0 = 0, c1 = 0;
+  const bool stamps = A.dbg != nullptr;
   bool first = !ENS;  // first tile of a single chain: momenta not yet readable
-  for (; tile < n_tiles; tile += gridDim.x, buf ^= 1) {
-    c0 = clock64();
-    // the other buffer was released at the end of the previous tile: stream
-    // the next tile into it while this one runs (first tile: after the wait)
-    if (tid == 0 && !first && tile + (int)gridDim.x < n_tiles) {
+  for (; tile < n_tiles; buf ^= 1) {
+    if (stamps) c0 = clock64();
+    // the CTA's next tile (thread 0; everyone reads S.next after the tile's
+    // closing barrier) -- its staging starts now, into the other buffer,
+    // released at the end of the previous tile (first tile: after the wait)
+    if (tid == 0) S.next[buf] = DYN ? (int)gridDim.x + (int)atomicAdd(&A.ctrl->tile_next, 1u) : tile + (int)gridDim.x;
+    const int next = tid == 0 ? S.next[buf] : 0;
+    if (tid == 0 && !first && next < n_tiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (ENS) stage_tile_ens<W>(A, tile + gridDim.x, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
-      else stage_tile<W>(A, hsrc, tile + gridDim.x, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
+      if (ENS) stage_tile_ens<W>(A, next, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
+      else stage_tile<W>(A, hsrc, next, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
     }
     const double *stg = S.stage[buf];
-    const int64_t t0 = (int64_t)tile * A.g.core;
-    const int64_t t1 = min(t0 + A.g.core, T);
-    const int64_t lo_live = max((int64_t)0, t0 - H), hi_live = min(T, t1 + H);
+    const int64_t t0 = (int64_t)tile * core_len;
+    const int64_t t1 = min(t0 + core_len, T);
     const int64_t g0 = t0 - H + lw;
+    const bool interior = !ENS && t0 >= H && t0 + core_len + H <= T && t0 >= A.own_lo && t0 + core_len <= A.own_hi &&
+                          goff + t0 - H > 0 && goff + t0 - H + W < Tg;
 
     // ---- tile data from the staging buffer ----
-    mbar_wait(&S.bar[buf], parity[buf]);
-    parity[buf] ^= 1;
-    c1 = clock64(); cyc_wait += c1 - c0; c0 = c1;
+    mbar_wait(&S.bar[buf], (parity >> buf) & 1);
+    parity ^= 1u << buf;
+    if (stamps) { c1 = clock64(); cyc_wait += c1 - c0; c0 = c1; }
     double d[R], p[R], Ad[R], Cd[R], av[R], lv[R];
-    uint32_t live = 0, core = 0, wcore = 0, endm = 0;
+    uint32_t live, core, wcore, endm = 0, firstm = 0;
     unsigned cm[R];
 #pragma unroll
     for (int r = 0; r < R; r += 2) {
@@ -711,61 +568,75 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     // is the first / last of its chain, so the neighbour across is cut off
     bool cf = false, cl = false;
     int64_t chain = 0;
-    if (ENS) {
-      const int64_t m = ((g0 % A.Tc) + A.Tc) % A.Tc;
-      cf = m == 0;
-      cl = m + R == A.Tc;
-      chain = g0 >= 0 ? g0 / A.Tc : -1;
-    }
-    uint32_t firstm = 0;
-    // only a lane whose sites include global site 0 or Tg-1 has end sites
-    const bool near_end = (g0 + goff <= 0 && g0 + goff + R > 0) || (g0 + goff <= Tg - 1 && g0 + goff + R > Tg - 1);
+    bool warp_edge = false;
+    if (interior) {
+      live = (1u << R) - 1;
+      core = wcore = core_int;
 #pragma unroll
-    for (int r = 0; r < R; r++) {
-      const int64_t gi = g0 + r;
-      const bool in = gi >= lo_live && gi < hi_live;
-      // wcore: tile-core sites of the local range (written back; a shard keeps
-      // its margins evolving too); core: those this context owns (the sums)
-      const bool wc = in && own_lane && gi >= t0 && gi < t1;
-      const bool c = wc && gi >= A.own_lo && gi < A.own_hi;
-      live |= (uint32_t)in << r;
-      core |= (uint32_t)c << r;
-      wcore |= (uint32_t)wc << r;
-      if (ENS) {
-        endm |= (uint32_t)((cf && r == 0) || (cl && r == R - 1)) << r;
-        firstm |= (uint32_t)(cf && r == 0) << r;
-      } else if (near_end) {
-        endm |= (uint32_t)(gi + goff == 0 || gi + goff == Tg - 1) << r;
-        firstm |= (uint32_t)(gi + goff == 0) << r;
+      for (int r = 0; r < R; r++) {
+        cm[r] = ~0u;
+        d[r] = d[r] - s.mu;
+        Ad[r] = s.dt * (s.emu * av[r]);
+        Cd[r] = fma(-s.alpha, lv[r] - s.xm, s.half_dt);
       }
-      cm[r] = c ? ~0u : 0u;
-      d[r] = in ? d[r] - s.mu : 0.0;
-      p[r] = in ? p[r] : 0.0;
-      Ad[r] = in ? s.dt * (s.emu * av[r]) : 0.0;
-      Cd[r] = in ? fma(-s.alpha, lv[r] - s.xm, s.half_dt) : 0.0;
+    } else {
+      if (ENS) {
+        const int64_t m = ((g0 % A.Tc) + A.Tc) % A.Tc;
+        cf = m == 0;
+        cl = m + R == A.Tc;
+        chain = g0 >= 0 ? g0 / A.Tc : -1;
+      }
+      const int64_t lo_live = max((int64_t)0, t0 - H), hi_live = min(T, t1 + H);
+      // only a lane whose sites include global site 0 or Tg-1 has end sites
+      const bool near_end =
+          (g0 + goff <= 0 && g0 + goff + R > 0) || (g0 + goff <= Tg - 1 && g0 + goff + R > Tg - 1);
+      live = core = wcore = 0;
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const int64_t gi = g0 + r;
+        const bool in = gi >= lo_live && gi < hi_live;
+        // wcore: tile-core sites of the local range (written back; a shard
+        // keeps its margins evolving too); core: those this context owns
+        const bool wc = in && own_lane && gi >= t0 && gi < t1;
+        const bool c = wc && gi >= A.own_lo && gi < A.own_hi;
+        live |= (uint32_t)in << r;
+        core |= (uint32_t)c << r;
+        wcore |= (uint32_t)wc << r;
+        if (ENS) {
+          endm |= (uint32_t)((cf && r == 0) || (cl && r == R - 1)) << r;
+          firstm |= (uint32_t)(cf && r == 0) << r;
+        } else if (near_end) {
+          endm |= (uint32_t)(gi + goff == 0 || gi + goff == Tg - 1) << r;
+          firstm |= (uint32_t)(gi + goff == 0) << r;
+        }
+        cm[r] = c ? ~0u : 0u;
+        d[r] = in ? d[r] - s.mu : 0.0;
+        p[r] = in ? p[r] : 0.0;
+        Ad[r] = in ? s.dt * (s.emu * av[r]) : 0.0;
+        Cd[r] = in ? fma(-s.alpha, lv[r] - s.xm, s.half_dt) : 0.0;
+      }
+      const bool any_live = live != 0;
+      const bool edge = (any_live && live != (1u << R) - 1) || endm;
+      // warp-uniform kick path: the masked (edge) kick handles partially or
+      // non-live lanes, the global end sites and threads whose sites are only
+      // partly core (shard ownership); all other warps run the lean one
+      const bool mixed_core = core != 0 && core != (1u << R) - 1;
+      warp_edge = __any_sync(0xffffffffu, edge || !any_live || mixed_core);
+      if (!ENS && edge && !A.h_src) {
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          if ((core >> r) & 1) {
+            if (g0 + r + goff == 0) A.ctrl->ends_old[0] = d[r];
+            if (g0 + r + goff == Tg - 1) A.ctrl->ends_old[1] = d[r];
+          }
+        }
+      }
     }
-    const bool any_live = live != 0;
-    const bool edge = (any_live && live != (1u << R) - 1) || endm;
-    // warp-uniform kick path: the masked (edge) kick handles partially or
-    // non-live lanes, the global end sites and threads whose sites are only
-    // partly core (shard ownership); all other warps run the lean one
-    const bool mixed_core = core != 0 && core != (1u << R) - 1;
-    const bool warp_edge = __any_sync(0xffffffffu, edge || !any_live || mixed_core);
     // H_old of the owned core sites while a / lnRV are at hand
     double vold[6] = {0, 0, 0, 0, 0, 0};
     {
       const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      if (first) tile_energy<R, STATS, false>(d, p, av, lv, dl, core, firstm, s, S.tab, vold);
-      else tile_energy<R, STATS>(d, p, av, lv, dl, core, firstm, s, S.tab, vold);
-    }
-    if (!ENS && edge && !A.h_src) {
-#pragma unroll
-      for (int r = 0; r < R; r++) {
-        if ((core >> r) & 1) {
-          if (g0 + r + goff == 0) A.ctrl->ends_old[0] = d[r];
-          if (g0 + r + goff == Tg - 1) A.ctrl->ends_old[1] = d[r];
-        }
-      }
+      tile_energy<R, STATS>(d, av, lv, dl, core, firstm, s, S.tab, vold);
     }
     if (!ENS && first) {
       // the momenta kernel's normals: wait for it (everything above
@@ -773,9 +644,9 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
       if (tid == 0) {
         stage_tile<W>(A, hsrc, tile, S.stage[buf], &S.bar[3], 2);
-        if (tile + (int)gridDim.x < n_tiles) {
+        if (next < n_tiles) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          stage_tile<W>(A, hsrc, tile + gridDim.x, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
+          stage_tile<W>(A, hsrc, next, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
         }
       }
       mbar_wait(&S.bar[3], 0);
@@ -785,27 +656,30 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
         p[r] = ((live >> r) & 1) ? p2.x : 0.0;
         p[r + 1] = ((live >> (r + 1)) & 1) ? p2.y : 0.0;
       }
-#pragma unroll
-      for (int r = 0; r < R; r++)
-        if ((core >> r) & 1) vold[0] += 0.5 * p[r] * p[r];  // kinetic part of H_old
       first = false;
     }
-    const double hold = vold[0];
+    const double hold = vold[0] + kinetic<R>(p, core);  // the thread's group: H_old of its core sites
+    if (STATS) {
 #pragma unroll
-    for (int k = 0; k < (STATS ? 6 : 1); k++) S.acc[(k == 0 ? 1 : 2 + k) * NT + tid] += vold[k];  // slots 1, 3..7
+      for (int k = 0; k < 5; k++) S.accm[k][tid] += vold[1 + k];
+    }
 
-    // ---- the trajectory ----
-    c1 = clock64(); cyc_pre += c1 - c0; c0 = c1;
+    // ---- the trajectory, on x = K (h - mu) ----
+    if (stamps) { c1 = clock64(); cyc_pre += c1 - c0; c0 = c1; }
+#pragma unroll
+    for (int r = 0; r < R; r++) d[r] *= s.kx;
     unsigned nmax = 0;
     const int L = A.n_steps;
     if (warp_edge) {
-      run_steps<true, R, NT, FUSE, ENS>(d, p, Ad, Cd, s, S.tab, live, endm, cm, cf, cl, L, S.gx, lane, warp, nmax);
+      run_steps<true, R, NT, FUSE, ENS>(d, p, Ad, Cd, s, S.tab, live, endm, cm, cf, cl, L, gs, nmax);
     } else {
-      run_steps<false, R, NT, FUSE, ENS>(d, p, Ad, Cd, s, S.tab, live, endm, cm, cf, cl, L, S.gx, lane, warp, nmax);
+      run_steps<false, R, NT, FUSE, ENS>(d, p, Ad, Cd, s, S.tab, live, endm, cm, cf, cl, L, gs, nmax);
       nmax = core ? nmax : 0u;
     }
+#pragma unroll
+    for (int r = 0; r < R; r++) d[r] *= s.kxinv;
     __syncthreads();  // refresh slots reused by the next tile
-    c1 = clock64(); cyc_loop += c1 - c0; c0 = c1;
+    if (stamps) { c1 = clock64(); cyc_loop += c1 - c0; c0 = c1; }
 
     // ---- H_new, statistics, write-back ----
 #pragma unroll
@@ -818,8 +692,9 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     double vnew[6] = {0, 0, 0, 0, 0, 0};
     {
       const double dl = __shfl_up_sync(0xffffffffu, d[R - 1], 1);
-      tile_energy<R, STATS>(d, p, av, lv, dl, core, firstm, s, S.tab, vnew);
+      tile_energy<R, STATS>(d, av, lv, dl, core, firstm, s, S.tab, vnew);
     }
+    const double hnew = vnew[0] + kinetic<R>(p, core);
     double *hd = hdst;
     if (ENS && core) hd = A.ens_cur[chain] ? A.hbuf0 : A.hbuf1;
     if (wcore == (1u << R) - 1) {
@@ -837,7 +712,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
         }
       }
     }
-    if (!ENS && edge && !A.h_src) {
+    if (!ENS && !interior && !A.h_src) {
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if ((core >> r) & 1) {
@@ -851,9 +726,9 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
       // order: the Metropolis step of each chain sums its tiles in tile order
       const bool right = g0 >= (t0 / A.Tc + 1) * A.Tc;
       const double fl = nmax > (unsigned)s.n_span ? 1.0 : 0.0;
-      const double dhv = vnew[0] - hold;
-      double w8[8] = {right ? 0.0 : dhv, right ? 0.0 : hold, right ? 0.0 : vnew[0], right ? 0.0 : fl,
-                      right ? dhv : 0.0, right ? hold : 0.0, right ? vnew[0] : 0.0, right ? fl : 0.0};
+      const double dhv = hnew - hold;
+      double w8[8] = {right ? 0.0 : dhv, right ? 0.0 : hold, right ? 0.0 : hnew, right ? 0.0 : fl,
+                      right ? dhv : 0.0, right ? hold : 0.0, right ? hnew : 0.0, right ? fl : 0.0};
       // warp butterflies only (no CTA barrier, no serial thread-0 sum): the
       // Metropolis step adds the NW warp partials of each tile in warp order
 #pragma unroll
@@ -865,12 +740,16 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
 #pragma unroll
         for (int k = 0; k < 8; k++) S.epart[buf][warp][k] = w8[k];
       }
-    } else {
-      S.acc[0 * NT + tid] += vnew[0] - hold;
-      S.acc[2 * NT + tid] += vnew[0];
+    } else if (core) {
+      const double dhv = hnew - hold;
+      bad |= nmax > (unsigned)s.n_span || !(fabs(hold) < FIX_MAX) || !(fabs(hnew) < FIX_MAX);
+      S.acc3[0][tid] += fix128(dhv);
+      S.acc3[1][tid] += fix128(hold);
+      S.acc3[2][tid] += fix128(hnew);
+      if (STATS) {
 #pragma unroll
-      for (int k = 0; k < (STATS ? 5 : 0); k++) S.acc[(8 + k) * NT + tid] += vnew[1 + k];
-      if (nmax > (unsigned)s.n_span) S.acc[13 * NT + tid] = 1.0;
+        for (int k = 0; k < 5; k++) S.accm[5 + k][tid] += vnew[1 + k];
+      }
     }
     __syncthreads();  // all reads of this tile's buffer done before it is refilled
     if (ENS && warp == 0 && lane < 8) {  // the tile's two chain records, warps summed in order
@@ -880,14 +759,16 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
       double *q = reinterpret_cast<double *>(A.ens_parts + 2 * (size_t)tile);
       q[lane] = v;  // EnsPart {dh, hold, hnew, flag} x 2
     }
-    c1 = clock64(); cyc_post += c1 - c0;
+    if (stamps) { c1 = clock64(); cyc_post += c1 - c0; }
+    tile = S.next[buf];  // written by thread 0 before this tile's barriers
+    n_done++;
   }
   if (A.dbg && tid == 0) {
     A.dbg[(size_t)blockIdx.x * 8 + 0] = cyc_wait;
     A.dbg[(size_t)blockIdx.x * 8 + 1] = cyc_pre;
     A.dbg[(size_t)blockIdx.x * 8 + 2] = cyc_loop;
     A.dbg[(size_t)blockIdx.x * 8 + 3] = cyc_post;
-    A.dbg[(size_t)blockIdx.x * 8 + 4] = (tile - (int)blockIdx.x) / (int)gridDim.x;  // tiles processed
+    A.dbg[(size_t)blockIdx.x * 8 + 4] = n_done;  // tiles processed
     A.dbg[(size_t)blockIdx.x * 8 + 7] = t_entry;
     unsigned smid;
     asm("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -900,32 +781,58 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   // before reading the results
   asm volatile("griddepcontrol.launch_dependents;");
   if (ENS) return;  // every chain's decision: ens_decide_kernel
-  // ---- one reduction per CTA (without statistics only dh, H_old, H_new
-  // and the flag: TilePart slots 0, 1, 2, 13) ----
-  constexpr int NU = STATS ? TR_NV : 4;
-  double w[NU];
+  // ---- one reduction per CTA: the fixed-point sums in any order (exact),
+  // the moments by warp butterflies and warp totals in warp order ----
+  __int128 q3[3] = {S.acc3[0][tid], S.acc3[1][tid], S.acc3[2][tid]};
+  double m[10];
 #pragma unroll
-  for (int i = 0; i < NU; i++) w[i] = S.acc[tr_slot<STATS>(i) * NT + tid];
+  for (int k = 0; k < 10; k++) m[k] = 0.0;
+  if (STATS) {
 #pragma unroll
-  for (int i = 0; i < NU; i++) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) w[i] += __shfl_xor_sync(0xffffffffu, w[i], o);
+    for (int k = 0; k < 10; k++) m[k] = S.accm[STATS ? k : 0][tid];
   }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 3; k++) q3[k] += shfl_xor_128(q3[k], o);
+    if (STATS) {
+#pragma unroll
+      for (int k = 0; k < 10; k++) m[k] += __shfl_xor_sync(0xffffffffu, m[k], o);
+    }
+  }
+  const bool wbad = __any_sync(0xffffffffu, bad);
+  __syncthreads();  // the stage buffers (aliased by red) are no longer read
   if (lane == 0) {
+    TilePart &w = *reinterpret_cast<TilePart *>(S.red + warp * TR_NV);
+    st128(w.dh, q3[0]);
+    st128(w.hold, q3[1]);
+    st128(w.hnew, q3[2]);
 #pragma unroll
-    for (int i = 0; i < NU; i++) S.red[warp * TR_NV + tr_slot<STATS>(i)] = w[i];
-  }
-  __syncthreads();
-  if (tid < NU) {  // value k: warp totals in warp order, one thread per value
-    const int k = tr_slot<STATS>(tid);
-    double acc = S.red[k];
-    for (int q = 1; q < NW; q++) acc += S.red[q * TR_NV + k];
-    reinterpret_cast<double *>(A.parts + blockIdx.x)[k] = acc;  // TilePart = TR_NV doubles in w order
+    for (int k = 0; k < 5; k++) { w.so[k] = m[k]; w.sn[k] = m[5 + k]; }
+    w.flag = wbad ? 1.0 : 0.0;
   }
   __syncthreads();
   if (tid == 0) {
-    // acquire-release count: this CTA's partials (ordered by the barrier)
-    // are released; the last CTA acquires everyone's
+    const TilePart *w = reinterpret_cast<const TilePart *>(S.red);
+    TilePart o = w[0];
+    __int128 a0 = ld128(o.dh), a1 = ld128(o.hold), a2 = ld128(o.hnew);
+    for (int q = 1; q < NW; q++) {
+      a0 += ld128(w[q].dh);
+      a1 += ld128(w[q].hold);
+      a2 += ld128(w[q].hnew);
+      for (int k = 0; k < 5; k++) { o.so[k] += w[q].so[k]; o.sn[k] += w[q].sn[k]; }
+      o.flag = fmax(o.flag, w[q].flag);
+    }
+    // the fixed-point sums go straight into the grid totals (64-bit atomic
+    // limbs); only the statistics variant leaves a per-CTA record, for the
+    // fixed-order sums of its FP64 moments
+    fx_add(A.ctrl->fx + 0, a0);
+    fx_add(A.ctrl->fx + 3, a1);
+    fx_add(A.ctrl->fx + 6, a2);
+    if (o.flag > 0.0) atomicOr(A.ctrl->fx + 9, 1ull);
+    if (STATS) A.parts[blockIdx.x] = o;
+    // acquire-release count: this CTA's partials are released; the last CTA
+    // acquires everyone's
     unsigned done;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(done) : "l"(&A.ctrl->tiles_done) : "memory");
     S.last = (done == (unsigned)gridDim.x - 1);
@@ -938,20 +845,24 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
 struct TrajVariant {
   int R, NT, MINB;
 };
-static const TrajVariant kVariants[] = {{8, 256, 2}, {4, 256, 3}, {4, 128, 6}, {8, 128, 4}, {16, 128, 2},
-                                        {2, 256, 4}, {8, 64, 8}, {4, 256, 2}, {8, 32, 16},
-                                        // persistent + TMA-staged (9..14); 12..14 are the
-                                        // small-window shapes for short series
-                                        {8, 256, 2}, {4, 256, 3}, {4, 256, 2}, {4, 128, 3}, {4, 64, 5},
-                                        {4, 32, 8}, {8, 256, 1}, {6, 256, 1}, {4, 512, 1}};
-static bool variant_persistent(int v) { return v >= 9; }
+// Persistent, TMA-staged shapes (R sites per thread, threads per CTA, CTAs
+// per SM).  The index is the RSV_TRAJ_VARIANT development switch; 11 is the
+// long-series shape, 12..14 the small windows for short series, 17 one
+// 512-thread CTA per SM.  Retired indices (round-1 experiments: the
+// non-persistent kernel and R = 6 / 8 shapes, all measured slower) fall back
+// to the automatic choice.
+static const TrajVariant kVariants[] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0},
+                                        {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0},
+                                        {4, 256, 2}, {4, 128, 3}, {4, 64, 5}, {4, 32, 8},
+                                        {0, 0, 0}, {0, 0, 0}, {4, 512, 1}};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+static bool variant_available(int v) { return v >= 0 && v < kNumVariants && kVariants[v].R > 0; }
 
 int traj_num_variants() { return kNumVariants; }
 
 static TrajGeom traj_geometry_v(int64_t T, int n_steps, int sm_count, int variant) {
   TrajGeom g;
-  if (variant < 0 || variant >= kNumVariants) variant = 0;
+  if (!variant_available(variant)) variant = 11;
   const TrajVariant v = kVariants[variant];
   const int64_t NWv = v.NT / 32;
   const int64_t W = NWv > 1 ? NWv * 30 * v.R + 2 * v.R : (int64_t)v.R * 32;  // CTA window (ghost lanes overlap)
@@ -965,7 +876,7 @@ static TrajGeom traj_geometry_v(int64_t T, int n_steps, int sm_count, int varian
   if (n > slots / 2) n = (n + slots - 1) / slots * slots;
   g.core = ((T + n - 1) / n + v.R - 1) / v.R * v.R;
   g.n_tiles = (int)((T + g.core - 1) / g.core);
-  g.grid = variant_persistent(variant) ? (int)((int64_t)g.n_tiles < slots ? (int64_t)g.n_tiles : slots) : g.n_tiles;
+  g.grid = (int)((int64_t)g.n_tiles < slots ? (int64_t)g.n_tiles : slots);
   return g;
 }
 
@@ -975,7 +886,7 @@ static TrajGeom traj_geometry_v(int64_t T, int n_steps, int sm_count, int varian
 // T the trajectory is latency-bound per step, and more, smaller tiles
 // shorten it even though the halo share grows.
 TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant) {
-  if (variant >= 0) return traj_geometry_v(T, n_steps, sm_count, variant);
+  if (variant_available(variant)) return traj_geometry_v(T, n_steps, sm_count, variant);
   static const int kAuto[] = {11, 12, 13, 14};
   TrajGeom best{};
   bool have = false;
@@ -989,15 +900,9 @@ TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant) {
   return have ? best : traj_geometry_v(T, n_steps, sm_count, 11);
 }
 
-template <int R, int NT, int MINB>
-static void launch_v(const TrajArgs &a, cudaStream_t s) {
-  if (a.fuse) traj_kernel<R, NT, MINB, true><<<a.g.n_tiles, NT, 0, s>>>(a);
-  else traj_kernel<R, NT, MINB, false><<<a.g.n_tiles, NT, 0, s>>>(a);
-}
-
 template <int R, int NT, int MINB, bool FUSE, bool STATS, bool ENS = false, bool DEVK = false>
 static void launch_p2(const TrajArgs &a, cudaStream_t s) {
-  const size_t smem = sizeof(PersistSmem<R, NT>);
+  const size_t smem = sizeof(PersistSmem<R, NT, STATS>);
   cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // same (maximal) shared-memory carveout as the momenta kernel: no L1/shared
@@ -1062,30 +967,15 @@ static void launch_p(const TrajArgs &a, cudaStream_t s) {
 }
 
 const void *traj_kernel_fn(int variant, int fuse, int stats) {
-#define RSV_FN(R, NT, MB) (fuse ? (const void *)traj_kernel<R, NT, MB, true> : (const void *)traj_kernel<R, NT, MB, false>)
-  switch (variant) {
-    case 0: return RSV_FN(8, 256, 2);
-    case 1: return RSV_FN(4, 256, 3);
-    case 2: return RSV_FN(4, 128, 6);
-    case 3: return RSV_FN(8, 128, 4);
-    case 4: return RSV_FN(16, 128, 2);
-    case 5: return RSV_FN(2, 256, 4);
-    case 6: return RSV_FN(8, 64, 8);
-    case 7: return RSV_FN(4, 256, 2);
-    case 8: return RSV_FN(8, 32, 16);
-#undef RSV_FN
 #define RSV_FN(R, NT, MB)                                                                                   \
   (fuse ? (stats ? (const void *)traj_persistent_kernel<R, NT, MB, true, true>                             \
                  : (const void *)traj_persistent_kernel<R, NT, MB, true, false>)                           \
         : (stats ? (const void *)traj_persistent_kernel<R, NT, MB, false, true>                            \
                  : (const void *)traj_persistent_kernel<R, NT, MB, false, false>))
-    case 9: return RSV_FN(8, 256, 2);
-    case 10: return RSV_FN(4, 256, 3);
+  switch (variant) {
     case 12: return RSV_FN(4, 128, 3);
     case 13: return RSV_FN(4, 64, 5);
     case 14: return RSV_FN(4, 32, 8);
-    case 15: return RSV_FN(8, 256, 1);
-    case 16: return RSV_FN(6, 256, 1);
     case 17: return RSV_FN(4, 512, 1);
     default: return RSV_FN(4, 256, 2);
   }
@@ -1125,22 +1015,9 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
   switch (a.g.variant) {
-    case 0: launch_v<8, 256, 2>(a, s); break;
-    case 1: launch_v<4, 256, 3>(a, s); break;
-    case 2: launch_v<4, 128, 6>(a, s); break;
-    case 3: launch_v<8, 128, 4>(a, s); break;
-    case 4: launch_v<16, 128, 2>(a, s); break;
-    case 5: launch_v<2, 256, 4>(a, s); break;
-    case 6: launch_v<8, 64, 8>(a, s); break;
-    case 7: launch_v<4, 256, 2>(a, s); break;
-    case 8: launch_v<8, 32, 16>(a, s); break;
-    case 9: launch_p<8, 256, 2>(a, s); break;
-    case 10: launch_p<4, 256, 3>(a, s); break;
     case 12: launch_p<4, 128, 3>(a, s); break;
     case 13: launch_p<4, 64, 5>(a, s); break;
     case 14: launch_p<4, 32, 8>(a, s); break;
-    case 15: launch_p<8, 256, 1>(a, s); break;
-    case 16: launch_p<6, 256, 1>(a, s); break;
     case 17: launch_p<4, 512, 1>(a, s); break;
     default: launch_p<4, 256, 2>(a, s); break;
   }
@@ -1153,57 +1030,58 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
 template <int NT, bool STATS>
 __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   constexpr int NW = NT / 32;
-  constexpr int NU = STATS ? TR_NV : 4;  // reduced values (TilePart slots tr_slot<STATS>(i))
-  double v[NU];
+  TilePart tp;
+  if (STATS) {
+    // the moments: CTA records in the plain loop's order (part j, then
+    // j + NT, ...), then warp butterflies and warp totals in warp order
+    double mm[10];
 #pragma unroll
-  for (int i = 0; i < NU; i++) v[i] = 0.0;
-  // two parts per thread per round, loaded together (one memory latency;
-  // the summation order is the plain loop's: part j, then j + NT, ...)
-  for (int j = threadIdx.x; j < n_parts; j += 2 * NT) {
-    const double *t0 = reinterpret_cast<const double *>(A.parts + j);
-    const double *t1 = reinterpret_cast<const double *>(A.parts + j + NT);
-    const bool second = j + NT < n_parts;
-    double a0[NU], a1[NU];
+    for (int k = 0; k < 10; k++) mm[k] = 0.0;
+    for (int j = threadIdx.x; j < n_parts; j += NT) {
+      const TilePart &t = A.parts[j];
 #pragma unroll
-    for (int i = 0; i < NU; i++) {
-      a0[i] = t0[tr_slot<STATS>(i)];
-      a1[i] = second ? t1[tr_slot<STATS>(i)] : 0.0;
+      for (int k = 0; k < 5; k++) { mm[k] += t.so[k]; mm[5 + k] += t.sn[k]; }
     }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int i = 0; i < NU; i++) {
-      v[i] += a0[i];
-      if (second) v[i] += a1[i];
+    for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+      for (int k = 0; k < 10; k++) mm[k] += __shfl_xor_sync(0xffffffffu, mm[k], o);
     }
+    if (lane == 0)
+      for (int k = 0; k < 10; k++) s_v[warp * TR_NV + k] = mm[k];
+    __syncthreads();
+    if (threadIdx.x) return;
+    for (int k = 0; k < 5; k++) { tp.so[k] = s_v[k]; tp.sn[k] = s_v[5 + k]; }
+    for (int q = 1; q < NW; q++)
+      for (int k = 0; k < 5; k++) { tp.so[k] += s_v[q * TR_NV + k]; tp.sn[k] += s_v[q * TR_NV + 5 + k]; }
+  } else {
+    if (threadIdx.x) return;
+    for (int k = 0; k < 5; k++) tp.so[k] = tp.sn[k] = 0.0;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int i = 0; i < NU; i++) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-  }
-  if (lane == 0)
-    for (int i = 0; i < NU; i++) s_v[warp * TR_NV + tr_slot<STATS>(i)] = v[i];
-  __syncthreads();
-  // the warp totals of value k are added in warp order by thread k (in
-  // parallel over k), then thread 0 reads the NV results (0 for the
-  // statistics slots when they are not evaluated)
-  if (threadIdx.x < TR_NV) {
-    const int k = threadIdx.x;
-    const bool used = STATS || k < 3 || k == 13;
-    double acc = used ? s_v[k] : 0.0;
-    for (int w = 1; w < NW; w++) acc += used ? s_v[w * TR_NV + k] : 0.0;
-    s_v[NW * TR_NV + k] = acc;
-  }
-  __syncthreads();
-  if (threadIdx.x) return;
-  double tot[TR_NV];
-  for (int k = 0; k < TR_NV; k++) tot[k] = s_v[NW * TR_NV + k];
+  // the fixed-point totals (acquired with the CTA count), then cleared for
+  // the next launch
+  unsigned long long *fx = A.ctrl->fx;
+  const __int128 a0 = fx_total(fx + 0), a1 = fx_total(fx + 3), a2 = fx_total(fx + 6);
+  tp.flag = fx[9] ? 1.0 : 0.0;
+  for (int k = 0; k < 10; k++) fx[k] = 0;
+  st128(tp.dh, a0);
+  st128(tp.hold, a1);
+  st128(tp.hnew, a2);
+  // tot: dH, H_old, H_new (variable parts), the moments (old 3..7, new 8..12), the flag (13)
+  double tot[14];
+  tot[0] = unfix128(a0);
+  tot[1] = unfix128(a1);
+  tot[2] = unfix128(a2);
+  for (int k = 0; k < 5; k++) { tot[3 + k] = tp.so[k]; tot[8 + k] = tp.sn[k]; }
+  tot[13] = tp.flag;
   DevControl *C = A.ctrl;
   C->tiles_done = 0;  // re-arm for the next launch
+  C->tile_next = 0;
   C->t_stamp[3] = gtimer();
   if (C->halt) return;  // rsv_run_chain stopped at an earlier sweep: stream, path and statistics untouched
-  if (A.shard) {  // time-sharded chain: the host combines the shards' totals
-    for (int k = 0; k < TR_NV; k++) C->shard_parts[k] = tot[k];
+  if (A.shard) {  // time-sharded chain: the shards' records are combined by the decision
+    *reinterpret_cast<TilePart *>(C->shard_parts) = tp;
     return;
   }
   const double cst = A.kdev ? A.kdev->hconst : A.k.hconst;
@@ -1216,8 +1094,9 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   const bool flagged = tot[13] > 0.0;
   if (A.integrate_only) {
     // a non-finite final state only arises from a kick the reference flags
-    // (NaN / inf are absorbing under the leapfrog map, _kernels.py:50-51)
-    r.diverged = flagged || !isfinite(tot[2]);
+    // (NaN / inf are absorbing under the leapfrog map, _kernels.py:50-51);
+    // the flag also covers energies beyond the fixed-point range
+    r.diverged = flagged;
     r.delta_h = tot[0];
     C->res = r;
     return;
@@ -1267,7 +1146,10 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
 // its buffer.
 __global__ void ens_decide_kernel(TrajArgs A) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c == 0) A.ctrl->t_stamp[3] = gtimer();
+  if (c == 0) {
+    A.ctrl->t_stamp[3] = gtimer();
+    A.ctrl->tile_next = 0;  // re-arm the trajectory kernel's dynamic tile counter
+  }
   if (c >= A.n_chains) return;
   const int64_t Tc = A.Tc, core = A.g.core;
   const int64_t s0 = (int64_t)c * Tc, s1 = s0 + Tc - 1;

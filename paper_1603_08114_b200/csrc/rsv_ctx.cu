@@ -1294,30 +1294,47 @@ __global__ void shard_apply_kernel(DevControl *C, int accept, int drew, const ui
 }
 
 // ---- device-side orchestration of a sharded chain (no host sync per proposal)
-// pack: this shard's totals into 20 doubles (rsv_shard_totals layout)
-__global__ void shard_pack_kernel(const DevControl *C, int own_first, int own_last, double *out) {
+// pack: this shard's record (ShardRec = rsv_shard_totals layout)
+__global__ void shard_pack_kernel(const DevControl *C, int own_first, int own_last, ShardRec *out) {
   if (threadIdx.x || blockIdx.x) return;
-  for (int k = 0; k < TR_NV; k++) out[k] = C->shard_parts[k];
-  out[14] = own_first ? C->ends_old[0] : 0.0;
-  out[15] = own_last ? C->ends_old[1] : 0.0;
-  out[16] = own_first ? C->ends_new[0] : 0.0;
-  out[17] = own_last ? C->ends_new[1] : 0.0;
-  out[18] = __longlong_as_double((long long)C->u_word);
-  out[19] = __longlong_as_double((long long)C->zig_used);
+  ShardRec r;
+  r.part = *reinterpret_cast<const TilePart *>(C->shard_parts);
+  r.ends[0] = own_first ? C->ends_old[0] : 0.0;
+  r.ends[1] = own_last ? C->ends_old[1] : 0.0;
+  r.ends[2] = own_first ? C->ends_new[0] : 0.0;
+  r.ends[3] = own_last ? C->ends_new[1] : 0.0;
+  r.u_word = C->u_word;
+  r.words_used = C->zig_used;
+  *out = r;
 }
 
-// Metropolis on the all-gathered totals (world x 20, rank order): every rank
-// runs the same fixed-order compensated sums on the same data, so every rank
-// takes the same decision (sampler.py:155-167); then the stream advances and
-// the kept path's statistics and the result are recorded.
-__global__ void shard_decide_kernel(DevControl *C, const double *g, int world, double hconst,
+__device__ __forceinline__ __int128 rec128(const long long (&w)[2]) {
+  return (__int128)(((unsigned __int128)(unsigned long long)w[1] << 64) | (unsigned long long)w[0]);
+}
+__device__ __forceinline__ double rec_unfix(__int128 q) {  // as unfix128 in leapfrog.cu
+  const bool neg = q < 0;
+  const unsigned __int128 a = neg ? (unsigned __int128)(-q) : (unsigned __int128)q;
+  const double r = __ull2double_rn((unsigned long long)(a >> 64)) + __ull2double_rn((unsigned long long)a) * 0x1p-64;
+  return neg ? -r : r;
+}
+
+// Metropolis on the all-gathered records (world ShardRecs, rank order):
+// dH, H_old and H_new are exact integer sums of the fixed-point parts (the
+// same bits as a single context over the whole series, for any world size);
+// the moments use fixed-order compensated sums.  Every rank runs this on the
+// same data, so every rank takes the same decision (sampler.py:155-167);
+// then the stream advances and the kept path's statistics and the result
+// are recorded.
+__global__ void shard_decide_kernel(DevControl *C, const ShardRec *g, int world, double hconst,
                                     const uint64_t *snaps, DevResult *ring, int cap, int32_t *count) {
   if (threadIdx.x || blockIdx.x) return;
-  double S[18];
-  for (int k = 0; k < 18; k++) {
+  __int128 q0 = 0, q1 = 0, q2 = 0;
+  double fl = 0.0;
+  double S[14];  // moments old 0..4, new 5..9, ends 10..13
+  for (int k = 0; k < 14; k++) {
     double sum = 0.0, comp = 0.0;
     for (int r = 0; r < world; r++) {  // TwoSum accumulation
-      const double x = g[20 * r + k];
+      const double x = k < 5 ? g[r].part.so[k] : k < 10 ? g[r].part.sn[k - 5] : g[r].ends[k - 10];
       const double t = sum + x;
       const double bp = t - sum;
       comp += (sum - (t - bp)) + (x - bp);
@@ -1325,18 +1342,24 @@ __global__ void shard_decide_kernel(DevControl *C, const double *g, int world, d
     }
     S[k] = sum + comp;
   }
-  const uint64_t u_word = (uint64_t)__double_as_longlong(g[18]);
+  for (int r = 0; r < world; r++) {
+    q0 += rec128(g[r].part.dh);
+    q1 += rec128(g[r].part.hold);
+    q2 += rec128(g[r].part.hnew);
+    fl = fmax(fl, g[r].part.flag);
+  }
+  const uint64_t u_word = g[0].u_word;
   bool consistent = true;
-  for (int r = 1; r < world; r++) consistent &= (uint64_t)__double_as_longlong(g[20 * r + 18]) == u_word;
+  for (int r = 1; r < world; r++) consistent &= g[r].u_word == u_word;
   if (!consistent) atomicOr(&C->err, 8);
   DevResult res;
-  res.h_old = S[1] + hconst;
-  res.h_new = S[2] + hconst;
+  res.h_old = rec_unfix(q1) + hconst;
+  res.h_new = rec_unfix(q2) + hconst;
   res.accept = 0;
   res.u = __longlong_as_double(0x7ff8000000000000LL);
-  const double dh = S[0];
+  const double dh = rec_unfix(q0);
   bool drew = false;
-  if (S[13] > 0.0 || !isfinite(dh) || fabs(dh) > 1000.0) {
+  if (fl > 0.0 || !isfinite(dh) || fabs(dh) > 1000.0) {
     res.diverged = 1;
     res.delta_h = __longlong_as_double(0x7ff0000000000000LL);
   } else {
@@ -1349,9 +1372,9 @@ __global__ void shard_decide_kernel(DevControl *C, const double *g, int world, d
   res.words_used = C->zig_used + (drew ? 1 : 0);
   shard_advance(C, drew, snaps);
   if (res.accept) C->cur ^= 1;
-  C->stats[0] = res.accept ? S[16] : S[14];
-  C->stats[1] = res.accept ? S[17] : S[15];
-  for (int k = 0; k < 5; k++) C->stats[2 + k] = res.accept ? S[8 + k] : S[3 + k];
+  C->stats[0] = res.accept ? S[12] : S[10];
+  C->stats[1] = res.accept ? S[13] : S[11];
+  for (int k = 0; k < 5; k++) C->stats[2 + k] = res.accept ? S[5 + k] : S[k];
   C->res = res;
   if (ring) {
     const int i = *count;
@@ -1424,14 +1447,17 @@ int rsv_shard_propose(rsv_ctx *c, double dt, int n_steps, int fuse, int stats, r
   if ((r = pull_ctrl(c))) return r;
   if ((r = check_err_bits(c))) return r;
   const DevControl &C = *c->h_ctrl;
-  for (int k = 0; k < TR_NV; k++) out->part[k] = C.shard_parts[k];
+  static_assert(sizeof(rsv_shard_totals) == sizeof(ShardRec), "rsv_shard_totals mirrors ShardRec");
+  ShardRec rec;
+  rec.part = *reinterpret_cast<const TilePart *>(C.shard_parts);
   const bool own_first = c->goff + c->own_lo == 0, own_last = c->goff + c->own_hi == c->Tg;
-  out->ends[0] = own_first ? C.ends_old[0] : 0.0;
-  out->ends[1] = own_last ? C.ends_old[1] : 0.0;
-  out->ends[2] = own_first ? C.ends_new[0] : 0.0;
-  out->ends[3] = own_last ? C.ends_new[1] : 0.0;
-  out->u_word = C.u_word;
-  out->words_used = C.zig_used;
+  rec.ends[0] = own_first ? C.ends_old[0] : 0.0;
+  rec.ends[1] = own_last ? C.ends_old[1] : 0.0;
+  rec.ends[2] = own_first ? C.ends_new[0] : 0.0;
+  rec.ends[3] = own_last ? C.ends_new[1] : 0.0;
+  rec.u_word = C.u_word;
+  rec.words_used = C.zig_used;
+  memcpy(out, &rec, sizeof(rec));
   return 0;
 }
 
@@ -1464,7 +1490,7 @@ int rsv_shard_propose_async(rsv_ctx *c, double dt, int n_steps, int fuse, int st
   if ((r = get_graph(c, dt, n_steps, fuse, stats, &cg, &kpl))) return r;
   CK(cudaGraphLaunch(cg->exec, c->stream));
   const int own_first = c->goff + c->own_lo == 0, own_last = c->goff + c->own_hi == c->Tg;
-  shard_pack_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, own_first, own_last, totals_dev);
+  shard_pack_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, own_first, own_last, reinterpret_cast<ShardRec *>(totals_dev));
   c->launches += kpl + 1;
   CK(cudaGetLastError());
   return 0;
@@ -1482,7 +1508,8 @@ int rsv_shard_decide_async(rsv_ctx *c, const double *gathered_dev, int world, do
     CK(cudaMallocHost(&c->h_ring, sizeof(DevResult) * c->ring_cap));
     CK(cudaMemsetAsync(c->ring_count, 0, sizeof(int32_t), c->stream));
   }
-  shard_decide_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, gathered_dev, world, hconst, c->sfc_snaps, c->ring,
+  shard_decide_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, reinterpret_cast<const ShardRec *>(gathered_dev), world,
+                                              hconst, c->sfc_snaps, c->ring,
                                               c->ring_cap, c->ring_count);
   c->launches++;
   CK(cudaGetLastError());

@@ -22,7 +22,7 @@ constexpr int TR_R = 4;          // consecutive sites per thread (registers)
 constexpr int TR_MINB = 3;       // resident CTAs per SM (register budget 85/thread)
 constexpr int TR_W = TR_NT * TR_R;
 constexpr int TR_NW = TR_NT / 32;
-constexpr int TR_NV = 14;        // reduced values per tile (see TilePart)
+constexpr int TR_NV = 17;        // 8-byte words of a tile / CTA partial record (see TilePart)
 
 // ---- streamed (one step per pass) kernel ------------------------------------
 constexpr int ES_NT = 256;
@@ -36,14 +36,31 @@ struct DevParams {
   int32_t n_lo, n_span;  // |h| <= 50  <=>  rint(-2048 (h - mu)/ln2) - n_lo in [0, n_span]
 };
 
-struct TilePart {  // per-tile partial sums over the tile's core sites
-  double dh;       // sum of per-thread (H_new - H_old) variable parts
-  double hold, hnew;
+// Per-CTA partial record of the trajectory kernel.  dh, H_old and H_new are
+// exact sums of per-group values (a group = 4 consecutive sites 4-aligned in
+// the global series, summed in site order) rounded to 128-bit fixed point
+// (value * 2^64, fix128 in leapfrog.cu): integer addition is associative, so
+// the totals do not depend on the tile shape, the tile -> CTA assignment or
+// how the series is split across GPUs (bitwise the same dH for any world
+// size).  The theta moments stay fixed-order FP64 sums.
+struct TilePart {
+  long long dh[2], hold[2], hnew[2];  // int128 as {low word, high word}
   double so[5];    // old path: sum d, sum d^2, sum d_t d_{t-1}, sum e, sum e^2
   double sn[5];    // proposal: same
   double flag;     // > 0 if any core site left [-50, 50] (or NaN) at a kick
 };
-static_assert(sizeof(TilePart) == TR_NV * sizeof(double), "TilePart is the TR_NV reduced values in order");
+static_assert(sizeof(TilePart) == TR_NV * 8, "TilePart is TR_NV 8-byte words");
+
+// ---- time-sharded chains: one shard's record, all-gathered per proposal
+// (mirrors rsv_shard_totals of the C ABI: 23 8-byte words)
+struct ShardRec {
+  TilePart part;       // over the shard's owned sites
+  double ends[4];      // d_0 old, d_{T-1} old, d_0 new, d_{T-1} new (0 unless this shard owns the end)
+  uint64_t u_word;     // raw word after the momenta (the Metropolis uniform)
+  uint64_t words_used; // raw words the momenta consumed
+};
+constexpr int SHARD_W = (int)(sizeof(ShardRec) / 8);
+static_assert(SHARD_W == 23, "rsv_shard_totals layout");
 
 // ---- ensemble of independent chains (rsv_ens_*) ------------------------------
 struct EnsPart {  // per trajectory tile: partials of the (<= 2) chains its core touches
@@ -95,8 +112,8 @@ struct DevControl {
   double stats[7];      // statistics of the kept path (shift mu, xi of the params used)
   DevResult res;
   uint64_t u_word;      // raw word right after the momenta (the Metropolis uniform)
-  uint32_t tiles_done;  // trajectory tiles finished (last one runs the Metropolis step)
-  uint32_t pad3;
+  uint32_t tiles_done;  // trajectory CTAs finished (last one runs the Metropolis step)
+  uint32_t tile_next;   // dynamic tile scheduling: tiles handed out beyond the first wave
   // sequential state of jump-ahead generators at the stream position (pcg32:
   // LCG state before output 2*pos; minstd: x_{3*pos}); seq_next = at pos + used
   uint64_t seq_state, seq_next;
@@ -108,6 +125,10 @@ struct DevControl {
   int32_t halt;
   uint32_t pad5;
   double shard_parts[TR_NV];  // time-sharded chains: this shard's totals (TilePart order)
+  // trajectory kernel: every CTA adds its fixed-point dH, H_old, H_new as
+  // three 42-bit limbs each (fx[3 v + l]; <= 2^22 CTAs cannot carry out of a
+  // 64-bit word) and ORs its flag into fx[9]; the last CTA reads and clears
+  unsigned long long fx[10];
   // %globaltimer stamps (ns) of the last proposal: momenta kernel first-CTA
   // entry / last-CTA exit, trajectory kernel CTA-0 entry / last-CTA exit,
   // and the previous proposal's trajectory exit

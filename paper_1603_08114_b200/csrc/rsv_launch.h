@@ -51,8 +51,11 @@ int traj_num_variants();
 struct TrajConsts {
   double mu, phi, dt, c_half, c_full, half_dt, alpha, bphi, g_int, g_end, emu, xm, inv2su, inv2se, one_m_phi2;
   double hconst;
-  // exp(-d) constants: constant-bank operands of the FP64 instructions
-  double e_k, e_hi, e_lo, e_c5, e_c4, e_c3;
+  // The step loop runs on x = K (h - mu), K = 2048 / ln 2: the
+  // drift and the kick's linear terms take their constants pre-scaled, and
+  // e^{-d} = 2^{-x/2048} needs no Cody-Waite split (f = -x - rint(-x) is exact)
+  double xc_half, xc_full, xg_int, xg_end, xbphi, kx, kxinv;
+  double ex1, ex2, ex3;  // e^{f ln2/2048} - 1 = f (ex1 + f (ex2 + f ex3))
   int32_t n_lo, n_span;
 };
 __host__ __device__ inline TrajConsts traj_consts(const DevParams &P, double dt) {
@@ -74,12 +77,16 @@ __host__ __device__ inline TrajConsts traj_consts(const DevParams &P, double dt)
   s.inv2se = 0.5 * P.inv_se2;
   s.one_m_phi2 = P.one_m_phi2;
   s.hconst = P.hconst;
-  s.e_k = RSV_INV_LN2_N;
-  s.e_hi = RSV_LN2_N_HI;
-  s.e_lo = RSV_LN2_N_LO;
-  s.e_c5 = 0.0;  // unused (degree-3 polynomial)
-  s.e_c4 = 0.0;
-  s.e_c3 = 1.0 / 6.0;
+  s.kx = RSV_INV_LN2_N;
+  s.kxinv = RSV_LN2_N_HI + RSV_LN2_N_LO;
+  s.xc_half = s.c_half * s.kx;
+  s.xc_full = s.c_full * s.kx;
+  s.xg_int = s.g_int * s.kxinv;
+  s.xg_end = s.g_end * s.kxinv;
+  s.xbphi = s.bphi * s.kxinv;
+  s.ex1 = s.kxinv;
+  s.ex2 = 0.5 * s.kxinv * s.kxinv;
+  s.ex3 = s.kxinv * s.kxinv * s.kxinv / 6.0;
   s.n_lo = P.n_lo;
   s.n_span = P.n_span;
   return s;

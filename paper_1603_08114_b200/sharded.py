@@ -35,7 +35,38 @@ from . import _native as N
 from .integrator import DH_DIVERGENCE_THRESHOLD
 from .model import Dataset, Params
 
-TOTALS = 14 + 4 + 2  # part[14], ends[4], u_word, words_used (as float64 bit patterns)
+# one shard's record (rsv_shard_totals, 23 8-byte words, viewed as float64):
+# dh, H_old, H_new as 128-bit fixed point (2 words each), 5 + 5 moments, the
+# flag, 4 end values, u_word, words_used (bit patterns)
+TOTALS = 23
+W_DH, W_HOLD, W_HNEW, W_SO, W_SN, W_FLAG, W_ENDS, W_U, W_USED = 0, 2, 4, 6, 11, 16, 17, 21, 22
+FIX_SCALE = 2.0 ** 64
+
+
+def fix128(v: float) -> int:
+    """v * 2^64 rounded toward zero (exactly the device's fix128): per-group
+    values become integers whose sums are independent of the grouping."""
+    return int(float(v) * FIX_SCALE)
+
+
+def unfix128(q: int) -> float:
+    """The device's conversion back (unfix128 in leapfrog.cu): nearest doubles
+    of the high and low 64-bit halves, combined in one rounded addition."""
+    a = -q if q < 0 else q
+    r = float(a >> 64) + float(a & 0xFFFFFFFFFFFFFFFF) * 2.0 ** -64
+    return -r if q < 0 else r
+
+
+def rec128(words: np.ndarray, at: int) -> int:
+    """The int128 stored as {low, high} 64-bit words at `at` of a record."""
+    lo = int(words[at:at + 1].view(np.uint64)[0])
+    hi = int(words[at + 1:at + 2].view(np.int64)[0])
+    return (hi << 64) | lo
+
+
+def put128(words: np.ndarray, at: int, q: int):
+    words[at:at + 1] = np.array([q & 0xFFFFFFFFFFFFFFFF], dtype=np.uint64).view(np.float64)
+    words[at + 1:at + 2] = np.array([q >> 64], dtype=np.int64).view(np.float64)
 
 
 def shard_bounds(T: int, world: int, align: int = 8) -> list[tuple[int, int]]:
@@ -127,11 +158,7 @@ class CudaShard:
         t = N.ShardTotals()
         self._ck(self._lib.rsv_shard_propose(self.ctx, float(step_size), int(n_steps), int(bool(fuse)),
                                              int(bool(stats)), ctypes.byref(t)))
-        v = np.empty(TOTALS)
-        v[:14] = list(t.part)
-        v[14:18] = list(t.ends)
-        v[18:20] = np.array([t.u_word, t.words_used], dtype=np.uint64).view(np.float64)
-        return v
+        return np.frombuffer(bytes(t), dtype=np.float64).copy()
 
     def apply(self, accept: bool, drew: bool):
         self._ck(self._lib.rsv_shard_apply(self.ctx, int(bool(accept)), int(bool(drew))))
@@ -157,30 +184,33 @@ def h_constant(params: Params, T: int) -> float:
 
 
 def combine(totals: list[np.ndarray], params: Params, T: int) -> Decision:
-    """Metropolis step of sampler.py:155-167 on the shards' partial sums.
-    math.fsum is exactly rounded, so the result is independent of the order
-    and grouping of the shards."""
-    tot = np.array(totals)
-    s = [math.fsum(tot[:, k]) for k in range(18)]
-    u_word = int(tot[0, 18:19].view(np.uint64)[0])
-    if any(int(t[18:19].view(np.uint64)[0]) != u_word for t in tot):
+    """Metropolis step of sampler.py:155-167 on the shards' records.  dH,
+    H_old and H_new are exact integer sums of the fixed-point parts (the same
+    bits for any number or order of shards, and as a single context); the
+    moments and end values use math.fsum (exactly rounded, order-free)."""
+    tot = [np.asarray(t, dtype=np.float64) for t in totals]
+    q = [sum(rec128(t, at) for t in tot) for at in (W_DH, W_HOLD, W_HNEW)]
+    fl = max(float(t[W_FLAG]) for t in tot)
+    mom = [math.fsum(float(t[W_SO + k]) for t in tot) for k in range(10)]
+    ends = [math.fsum(float(t[W_ENDS + k]) for t in tot) for k in range(4)]
+    u_word = int(tot[0][W_U:W_U + 1].view(np.uint64)[0])
+    if any(int(t[W_U:W_U + 1].view(np.uint64)[0]) != u_word for t in tot):
         raise RuntimeError("shards drew different momenta streams")
     c = h_constant(params, T)
-    dh = s[0]
-    flagged = s[13] > 0.0
+    dh = unfix128(q[0])
     drew = False
     u = float("nan")
     accept = False
-    if flagged or not math.isfinite(dh) or abs(dh) > DH_DIVERGENCE_THRESHOLD:
+    if fl > 0.0 or not math.isfinite(dh) or abs(dh) > DH_DIVERGENCE_THRESHOLD:
         diverged, delta_h = True, math.inf
     else:
         diverged, delta_h = False, dh
         u = float(u_word >> 11) * (1.0 / 9007199254740992.0)
         drew = True
         accept = dh <= 0.0 or u < math.exp(-dh)
-    ends_old, ends_new = (s[14], s[15]), (s[16], s[17])
-    kept = np.array([*(ends_new if accept else ends_old), *(s[8:13] if accept else s[3:8])])
-    return Decision(accept, diverged, delta_h, s[1] + c, s[2] + c, drew, u, kept)
+    ends_old, ends_new = ends[0:2], ends[2:4]
+    kept = np.array([*(ends_new if accept else ends_old), *(mom[5:10] if accept else mom[0:5])])
+    return Decision(accept, diverged, delta_h, unfix128(q[1]) + c, unfix128(q[2]) + c, drew, u, kept)
 
 
 class ShardedChain:

@@ -8,7 +8,7 @@ import ctypes
 import numpy as np
 
 import oracle as O
-from paper_1603_08114_b200.sharded import TOTALS, local_range
+from paper_1603_08114_b200.sharded import TOTALS, W_ENDS, W_FLAG, W_SN, W_SO, W_U, fix128, local_range, put128
 
 
 class OracleShard:
@@ -61,7 +61,8 @@ class OracleShard:
         self.h[offset:offset + len(buf)] = buf
 
     def _site_terms(self, h, p):
-        """per-site K + V (variable parts, d-space) and statistics, owned sites only"""
+        """per-site potential and kinetic energy (variable parts, d-space) and
+        statistics; the owned slice"""
         P = self.params
         ls = self.local_start
         d = h - P.mu
@@ -73,13 +74,30 @@ class OracleShard:
         ar[first] = (1 - P.phi ** 2) * d[first] ** 2 / (2 * P.sigma_eta_sq)
         e = self.lrv - P.xi - h
         V = 0.5 * d + 0.5 * self.y * self.y * np.exp(-h) + e * e / (2 * P.sigma_u_sq) + ar
-        en = 0.5 * p * p + V
+        K = 0.5 * p * p
         own = slice(self.lo - ls, self.hi - ls)
         dprev = np.concatenate([[0.0], d[:-1]])
         cross = d * dprev
         cross[first] = 0.0
         stats = [d[own].sum(), (d * d)[own].sum(), cross[own].sum(), e[own].sum(), (e * e)[own].sum()]
-        return en, own, d, stats
+        return V, K, own, d, stats
+
+    def _groups(self, V, K):
+        """per-group H (4-aligned groups of global sites, owned part): the sum
+        of the group's potentials then of its kinetic terms, as the device
+        forms it, one fixed-point integer per group"""
+        ls = self.local_start
+        out = []
+        for g0 in range(self.lo, self.hi, 4):
+            sl = slice(g0 - ls, min(g0 + 4, self.hi) - ls)
+            pot = 0.0
+            for x in V[sl]:
+                pot += float(x)
+            kin = 0.0
+            for x in K[sl]:
+                kin += float(x)
+            out.append(pot + kin)
+        return out
 
     def propose(self, dt, n_steps, fuse, stats):
         s = self._copy_stream()
@@ -90,20 +108,21 @@ class OracleShard:
         p = normals[ls:ls + self.local_len]
         hn, pn, div = O.integrate(self.h, p, self.params, self.y, self.lrv, dt, n_steps, fuse=fuse)
         self._prop = hn
-        e_old, own, d_old, s_old = self._site_terms(self.h, p)
-        e_new, _, d_new, s_new = self._site_terms(hn, pn)
+        V0, K0, own, d_old, s_old = self._site_terms(self.h, p)
+        V1, K1, _, d_new, s_new = self._site_terms(hn, pn)
+        g_old, g_new = self._groups(V0, K0), self._groups(V1, K1)
         v = np.zeros(TOTALS)
-        v[0] = float(np.sum((e_new - e_old)[own]))
-        v[1] = float(np.sum(e_old[own]))
-        v[2] = float(np.sum(e_new[own]))
-        v[3:8] = s_old
-        v[8:13] = s_new
-        v[13] = 1.0 if div else 0.0
+        put128(v, 0, sum(fix128(b - a) for a, b in zip(g_old, g_new)))
+        put128(v, 2, sum(fix128(a) for a in g_old))
+        put128(v, 4, sum(fix128(b) for b in g_new))
+        v[W_SO:W_SO + 5] = s_old
+        v[W_SN:W_SN + 5] = s_new
+        v[W_FLAG] = 1.0 if div else 0.0
         if self.lo == 0:
-            v[14], v[16] = d_old[0 - ls], d_new[0 - ls]
+            v[W_ENDS + 0], v[W_ENDS + 2] = d_old[0 - ls], d_new[0 - ls]
         if self.hi == self.T:
-            v[15], v[17] = d_old[self.T - 1 - ls], d_new[self.T - 1 - ls]
-        v[18:20] = np.array([u_word, used], dtype=np.uint64).view(np.float64)
+            v[W_ENDS + 1], v[W_ENDS + 3] = d_old[self.T - 1 - ls], d_new[self.T - 1 - ls]
+        v[W_U:W_U + 2] = np.array([u_word, used], dtype=np.uint64).view(np.float64)
         self._used = used
         return v
 

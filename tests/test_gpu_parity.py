@@ -356,9 +356,10 @@ def test_sharded_chain_on_one_gpu_matches_single_context(backend, world, T):
         if r.diverged:
             assert math.isinf(d.delta_h)
         else:
-            assert abs(d.delta_h - r.delta_h) <= 1e-13 * H, (i, d.delta_h, r.delta_h)
+            # fixed-point group sums: the same dH bits for any world size
+            assert d.delta_h == r.delta_h, (i, d.delta_h, r.delta_h)
     h = np.concatenate([c.owned_latent() for c in shards])
-    assert _rel(h, single.get_latent()) <= 1e-12
+    assert np.array_equal(h, single.get_latent())
     assert all(int(c.get_stream().pos) == int(single.get_stream().pos) for c in shards)
     for c in shards:
         c.shard.close()
@@ -390,9 +391,9 @@ def test_sharded_device_orchestration_matches_single_context(backend, world, kin
         if b.diverged:
             assert a.diverged
         else:
-            assert abs(a.delta_h - b.delta_h) <= 1e-13 * H
+            assert a.delta_h == b.delta_h and a.h_old == b.h_old and a.h_new == b.h_new
     h = np.concatenate([c.owned_latent() for c in shards])
-    assert _rel(h, single.get_latent()) <= 1e-12
+    assert np.array_equal(h, single.get_latent())
     for c in shards:
         s, s1 = c.get_stream(), single.get_stream()
         assert int(s.pos) == int(s1.pos) and [int(x) for x in s.s] == [int(x) for x in s1.s]
@@ -445,7 +446,7 @@ def test_trajectory_bitwise_independent_of_tile_shape(backend, monkeypatch, fuse
     truth = P.simulate_rsv(THETA, T, seed=13)
     p = O.Stream("pcg32", 17).normals(T)
     outs = {}
-    for v in (11, 9, 12, 13, 14, 15, 17, 0):
+    for v in (11, 12, 13, 14, 17):
         monkeypatch.setenv("RSV_TRAJ_VARIANT", str(v))
         ch = DeviceChain(T, 0)
         try:

@@ -35,14 +35,54 @@ def test_shard_bounds():
 
 
 def test_combine_is_order_independent():
+    from paper_1603_08114_b200.sharded import TOTALS, W_FLAG, W_U, fix128, put128
     rng = np.random.default_rng(0)
-    parts = [np.concatenate([rng.normal(size=18) * 1e6, np.array([7, 3], dtype=np.uint64).view(np.float64)])
-             for _ in range(5)]
-    for p in parts:
-        p[13] = 0.0
+    parts = []
+    for _ in range(5):
+        p = np.zeros(TOTALS)
+        p[6:21] = rng.normal(size=15) * 1e6
+        p[W_FLAG] = 0.0
+        for at in (0, 2, 4):
+            put128(p, at, sum(fix128(x) for x in rng.normal(size=50) * 10.0))
+        p[W_U:W_U + 2] = np.array([7, 3], dtype=np.uint64).view(np.float64)
+        parts.append(p)
     a = combine(parts, THETA, 1000)
     b = combine(parts[::-1], THETA, 1000)
     assert a.delta_h == b.delta_h and a.accept == b.accept and a.h_old == b.h_old
+
+
+def test_fixed_point_roundtrip_and_exactness():
+    from paper_1603_08114_b200.sharded import fix128, unfix128
+    for v in (0.0, 1.0, -1.0, 0.1, -3.25e-7, 1234.5678, 2.0 ** 61, -(2.0 ** -64)):
+        q = fix128(v)
+        assert q == int(v * 2.0 ** 64)
+        assert abs(unfix128(q) - v) <= abs(v) * 2 ** -52 + 2.0 ** -64
+    # sums are associative: any grouping gives the same integer
+    xs = np.random.default_rng(1).normal(size=1000) * 50
+    qs = [fix128(x) for x in xs]
+    assert sum(qs) == sum(qs[::-1]) == sum(sum(qs[i:i + 7]) for i in range(0, 1000, 7))
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_sharded_dh_bitwise_independent_of_world(world):
+    """SURVEY 8e / the reference's worker-count independence
+    (test_acceptance.py:269-309): the per-group fixed-point dH makes the
+    combined dH the same bits for 1..4 shards."""
+    T, n, dt, L = 640, 6, 0.02, 10
+    truth = P.simulate_rsv(THETA, T, seed=4)
+    runs = {}
+    for w in (1, world):
+        chains = [P.ShardedChain(truth.dataset, THETA, r, w, margin=24,
+                                 shard_factory=lambda T_, lo, hi, m: OracleShard(T_, lo, hi, m)) for r in range(w)]
+        st0 = P.stream_state(P.make_rng(9, "philox"))
+        for c in chains:
+            c.set_latent_global(truth.latent)
+            c.set_stream(st0)
+        runs[w] = [hmc_update_local(chains, dt, L) for _ in range(n)]
+        runs[w] = ([d.delta_h for d in runs[w]], [d.accept for d in runs[w]],
+                   np.concatenate([c.owned_latent() for c in chains]))
+    assert runs[1][0] == runs[world][0] and runs[1][1] == runs[world][1]
+    assert np.array_equal(runs[1][2], runs[world][2])
 
 
 @pytest.mark.parametrize("world", [2, 3])
