@@ -186,9 +186,41 @@ int rsv_get_timing(rsv_ctx *ctx, double *traj_ms, double *momenta_ms, double *to
  * decisions recorded since the last call. */
 int rsv_set_stream(rsv_ctx *ctx, void *cuda_stream);
 int rsv_shard_propose_async(rsv_ctx *ctx, double step_size, int n_steps, int fuse, int stats, double *totals_dev);
-int rsv_shard_decide_async(rsv_ctx *ctx, const double *gathered_dev, int world, double h_const);
+int rsv_shard_decide_async(rsv_ctx *ctx, const double *gathered_dev, int world);
 int rsv_shard_halo_async(rsv_ctx *ctx, double *left, int64_t n_left, double *right, int64_t n_right, int unpack);
 int rsv_shard_results(rsv_ctx *ctx, rsv_result *out, int max_n, int *n_out);
+
+/* Time-sharded momenta (replaces sampler.py:136-141
+ * refresh_momenta for one shard).  rsv_shard_set_momenta(ctx, 1) switches a
+ * shard from drawing the whole series to parsing only a window of the
+ * raw-word stream around its own sites (jump-ahead generators: philox,
+ * pcg32, minstd; sfc64 uses rsv_shard_set_blocked_streams).  Per proposal:
+ * rsv_shard_momenta_async writes this shard's 8-word window record to
+ * device memory; after an all-gather of the records (rank order),
+ * rsv_shard_place_async gives the window its global normal indices (the
+ * exclusive prefix of the counts between anchor words), checks that
+ * neighbouring windows agree on the attempt boundary at each anchor, and
+ * places the shard's normals; then rsv_shard_propose_async runs the
+ * trajectory only.  The normals are bit for bit those of the whole-series
+ * draw. */
+int rsv_shard_set_momenta(rsv_ctx *ctx, int windowed);
+int rsv_shard_momenta_async(rsv_ctx *ctx, double *window_record_dev);
+int rsv_shard_place_async(rsv_ctx *ctx, const double *gathered_records_dev, int world, int rank);
+/* Blocked layout of a shard (config 5): the streams of the blocks
+ * [first_block, first_block + n_blocks) its local range touches. */
+int rsv_shard_set_blocked_streams(rsv_ctx *ctx, int64_t block_len, int64_t first_block, int64_t n_blocks,
+                                  const uint64_t *states);
+/* run_chain of a time-sharded chain (sampler.py:291-358): begin (prior,
+ * schedule; theta constants move to device memory), then per sweep the
+ * proposal protocol above with stats = 1, rsv_shard_decide_async, and
+ * rsv_shard_theta_async (the theta draws of sampler.py:339-344 from the
+ * all-gathered statistics of the kept path -- identical on every shard);
+ * end copies the stored samples out (storm -> RSV_E_STORM as rsv_run_chain). */
+int rsv_shard_run_begin(rsv_ctx *ctx, double step_size, const rsv_prior *prior, int64_t n_burnin, int64_t n_samples,
+                        int64_t thin);
+int rsv_shard_theta_async(rsv_ctx *ctx);
+int rsv_shard_run_end(rsv_ctx *ctx, int64_t *iters, double *params, int32_t *accept, double *delta_h,
+                      int64_t *n_stored, int64_t *storm_sweep);
 
 /* data.py:72-95 simulate_rsv on the device: the reference's 3T normals
  * (initial deviation, innovations, return shocks, measurement noise) drawn

@@ -115,7 +115,17 @@ _SIGS = {
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "rsv_shard_propose_async": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                ctypes.c_void_p]),
-    "rsv_shard_decide_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int, ctypes.c_double]),
+    "rsv_shard_decide_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int]),
+    "rsv_shard_set_momenta": (ctypes.c_int, [_CTX, ctypes.c_int]),
+    "rsv_shard_momenta_async": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
+    "rsv_shard_place_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+    "rsv_shard_set_blocked_streams": (ctypes.c_int, [_CTX, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                                     ctypes.c_void_p]),
+    "rsv_shard_run_begin": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                           ctypes.c_int64]),
+    "rsv_shard_theta_async": (ctypes.c_int, [_CTX]),
+    "rsv_shard_run_end": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "rsv_shard_halo_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                             ctypes.c_int]),
     "rsv_shard_results": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),

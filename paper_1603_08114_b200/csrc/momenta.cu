@@ -103,6 +103,7 @@ __device__ __forceinline__ bool zready(uint64_t v, uint32_t epoch) {
 }
 
 __device__ void zig_serial(DevControl *ctrl, const uint64_t *words, int64_t nbuf, double *normals, int64_t T);
+__device__ void zig_serial_window(DevControl *ctrl, const ZigWin &win, int64_t nwords);
 
 // glibc log1p as one out-of-line copy: the exponential-tail path of the
 // ziggurat is rare, so its code is cold in the instruction cache (after an L2
@@ -123,7 +124,12 @@ __device__ __forceinline__ unsigned long long zgt() {
 template <int KIND>
 __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint64_t *words, int64_t nwords_buf,
                                                  double *normals, int64_t T, uint64_t *status, const uint64_t *bjump,
-                                                 int coresident, unsigned long long *dbg) {
+                                                 int coresident, unsigned long long *dbg, ZigWin win) {
+  // window mode (time-sharded momenta, win.out != null): CTA b parses block
+  // wb0 + b of the full stream; the first CTA's entry is speculative (no
+  // predecessor in this window), the normals go to win.out in stream order
+  // and the anchors' counts to win.info (see WinInfo)
+  const bool wmode = win.out != nullptr;
 #define ZSTAMP(k) \
   do { if (dbg && threadIdx.x == 0) dbg[(size_t)blockIdx.x * 8 + (k)] = zgt(); } while (0)
   ZSTAMP(0);
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   // (one memory round trip fewer on the draw's critical path)
   uint64_t pbA = 0, pbG = 0;
   if (coresident && (KIND == PRNG_PCG32 || KIND == PRNG_MINSTD)) {
-    const int bb = (int)blockIdx.x;
+    const int bb = (int)blockIdx.x + (int)win.wb0;
     if (KIND == PRNG_PCG32) { pbA = bjump[2 * bb]; pbG = bjump[2 * bb + 1]; }
     else pbA = bjump[bb];
   }
@@ -183,15 +189,16 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   const uint64_t inc = st.s[1];
   const uint64_t seq = ctrl->seq_state;
   __syncthreads();
-  const int b = S.blk;
+  const int b = S.blk;            // ticket: this CTA's block within the draw (or window)
+  const int B = b + (int)win.wb0;  // ... within the full stream
   if (coresident && b != (int)blockIdx.x && (KIND == PRNG_PCG32 || KIND == PRNG_MINSTD)) {
-    if (KIND == PRNG_PCG32) { pbA = bjump[2 * b]; pbG = bjump[2 * b + 1]; }  // prefetched for blockIdx.x
-    else pbA = bjump[b];
+    if (KIND == PRNG_PCG32) { pbA = bjump[2 * B]; pbG = bjump[2 * B + 1]; }  // prefetched for blockIdx.x
+    else pbA = bjump[B];
   }
   ZSTAMP(1);
 
   // ---- my 8 raw words, generated into registers
-  const int64_t k_t = (int64_t)b * ZB - ZG + (int64_t)tid * ZW;  // draw word of my chunk's first word
+  const int64_t k_t = (int64_t)B * ZB - ZG + (int64_t)tid * ZW;  // draw word of my chunk's first word
   const bool valid = k_t >= 0;                                    // CTA 0 has no guard words
   uint64_t w[ZW];
   uint64_t base = 0;  // pcg: LCG state before output 2*k_t; minstd: x_{3 k_t}
@@ -214,10 +221,10 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   } else {
     // per-CTA jump (bjump, built once per context) composed with the
     // per-chunk jump: CTA b's base word is max(0, b*ZB - ZG)
-    const int cc = b == 0 ? tid - ZG / ZW : tid;
+    const int cc = B == 0 ? tid - ZG / ZW : tid;
     if (KIND == PRNG_PCG32) {
-      const uint64_t bA = coresident ? pbA : bjump[2 * b], bG = coresident ? pbG : bjump[2 * b + 1];
-      const uint64_t cA = b == 0 ? g_jump.pcg_a[cc] : jA, cG = b == 0 ? g_jump.pcg_g[cc] : jG;
+      const uint64_t bA = coresident ? pbA : bjump[2 * B], bG = coresident ? pbG : bjump[2 * B + 1];
+      const uint64_t cA = B == 0 ? g_jump.pcg_a[cc] : jA, cG = B == 0 ? g_jump.pcg_g[cc] : jG;
       uint64_t s0 = cA * (bA * seq + bG * inc) + cG * inc;
       base = s0;
 #pragma unroll
@@ -227,8 +234,8 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
         s0 = s1 * PCG_MULT + inc;
       }
     } else {  // MINSTD
-      const uint64_t cA = b == 0 ? g_jump.minstd_a[cc] : jA;
-      uint64_t x = mod31(cA * mod31((coresident ? pbA : bjump[b]) * seq));
+      const uint64_t cA = B == 0 ? g_jump.minstd_a[cc] : jA;
+      uint64_t x = mod31(cA * mod31((coresident ? pbA : bjump[B]) * seq));
       base = x;
 #pragma unroll
       for (int i = 0; i < ZW; i++) {
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   }
   const bool counting = tid >= 2 && tid < ZT - 2;
   int entry = 0, exitst = 0, cnt = 0;
-  uint32_t vis = 0;
+  uint32_t vis = 0, starts = 0;
   int ovf = 0;
   if (counting) {
     uint64_t cov = 0;  // window words inside an attempt that started earlier
@@ -403,6 +410,7 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
     const uint32_t free_mine = ~(uint32_t)(cov >> 16);
     entry = __ffs(free_mine) - 1;  // <= 14 (an attempt covers at most 14 more words)
     vis = free_mine & 0xffu & (0xffu << entry);
+    starts = vis;  // attempt starts in my chunk (accepted or not)
     cnt = __popc(vis & acc);
     vis &= acc;
     exitst = __ffs(~(uint32_t)(cov >> 24)) - 1;
@@ -599,7 +607,9 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
     if (lane == 0) {
       S.blk_off = accum;
       if (b == 0) {
-        if (S.blk_entry != 0) S.bad = 1;
+        // the draw's first block starts exactly at the stream position; a
+        // window's first block is speculative (checked across shards)
+        if (B == 0 && S.blk_entry != 0) S.bad = 1;
       } else {  // the previous CTA's exit must equal my block's entry (it has published)
         uint64_t prev = prev_word;
         if (!have_prev) do { prev = vst[b - 1]; } while (!zready(prev, S.epoch));
@@ -614,10 +624,47 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   // ---- coalesced copy-out of the CTA's normals; the thread whose normal is
   // the draw's last (index T-1) records where the draw ended in the stream
   const uint64_t boff = S.blk_off;
-  for (int j = tid; j < btot; j += ZT) {
-    if (boff + (uint64_t)j < (uint64_t)T) normals[boff + j] = S.xout[ZXS(j)];
+  if (wmode) {
+    for (int j = tid; j < btot; j += ZT) {
+      if (boff + (uint64_t)j < (uint64_t)win.cap) win.out[boff + j] = S.xout[ZXS(j)];
+    }
+    if (win.nend && vis) {  // where each of my normals' attempts ended
+      int o = toff;
+      for (int i = 0; i < ZW; i++) {
+        if ((vis >> i) & 1) {
+          const int L = (int)((lens >> (4 * i)) & 15u);
+          if (boff + (uint64_t)o < (uint64_t)win.cap) win.nend[boff + o] = (uint32_t)(k_t - win.w0 + i + L);
+          o++;
+        }
+      }
+    }
+    // anchors: the thread whose chunk holds the anchor word counts the
+    // window's normals before it and finds the first attempt at or after it
+    if (counting) {
+      const int64_t an[2] = {win.a_lo, win.a_hi};
+      for (int q = 0; q < 2; q++) {
+        const int64_t a = an[q];
+        if (a < k_t || a >= k_t + ZW) continue;
+        const int off = (int)(a - k_t);
+        const uint32_t before = (1u << off) - 1u;
+        const int64_t c = (int64_t)boff + toff + __popc(vis & before);
+        const uint32_t m = starts & ~before;
+        const int64_t s = m ? k_t + __ffs(m) - 1 : k_t + ZW + exitst;
+        if (q == 0) { win.info->cnt_lo = c; win.info->s_lo = s; }
+        else { win.info->cnt_hi = c; win.info->s_hi = s; }
+      }
+    }
+    if (tid == ZT - 1 && b == (int)gridDim.x - 1) {
+      win.info->n_win = (int64_t)(S.blk_off + (uint64_t)btot);
+      win.info->w0 = win.w0;
+      if (win.a_hi < 0) { win.info->cnt_hi = (int64_t)(S.blk_off + (uint64_t)btot); win.info->s_hi = -1; }
+    }
+  } else {
+    for (int j = tid; j < btot; j += ZT) {
+      if (boff + (uint64_t)j < (uint64_t)T) normals[boff + j] = S.xout[ZXS(j)];
+    }
   }
-  if (vis && boff + (uint64_t)toff <= (uint64_t)T - 1 && (uint64_t)T - 1 < boff + (uint64_t)toff + (uint64_t)cnt) {
+  if (!wmode && vis && boff + (uint64_t)toff <= (uint64_t)T - 1 && (uint64_t)T - 1 < boff + (uint64_t)toff + (uint64_t)cnt) {
     const int rank = (int)((uint64_t)T - 1 - boff - (uint64_t)toff);  // which of my normals
     uint32_t m = vis;
     for (int k = 0; k < rank; k++) m &= m - 1;
@@ -630,7 +677,7 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
     else if (KIND == PRNG_MINSTD) ctrl->seq_next = mod31(minstd_pow(3 * (uint64_t)(i + L)) * base);
   }
   // the last CTA publishes how many normals the parse produced
-  if (tid == ZT - 1 && b == (int)gridDim.x - 1) ctrl->zig_avail = S.blk_off + (uint64_t)btot;
+  if (!wmode && tid == ZT - 1 && b == (int)gridDim.x - 1) ctrl->zig_avail = S.blk_off + (uint64_t)btot;
   ZSTAMP(6);
   // the CTA that finishes last re-arms the bookkeeping and, if the parallel
   // parse could not be trusted (p ~ 1e-12 per word), redoes it serially
@@ -641,7 +688,12 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
     unsigned done;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(done) : "l"(&ctrl->zig_done) : "memory");
     if (done == gridDim.x - 1) {
-      if (ctrl->zig_overflow != 0 || ctrl->zig_avail < (uint64_t)T) zig_serial(ctrl, words, nwords_buf, normals, T);
+      if (wmode) {
+        win.info->err = 0;
+        if (ctrl->zig_overflow != 0) zig_serial_window(ctrl, win, (int64_t)gridDim.x * ZB);
+      } else if (ctrl->zig_overflow != 0 || ctrl->zig_avail < (uint64_t)T) {
+        zig_serial(ctrl, words, nwords_buf, normals, T);
+      }
       ctrl->zig_overflow = 0;
       ctrl->zig_ticket = 0;
       ctrl->zig_done = 0;
@@ -699,6 +751,62 @@ __device__ void zig_serial(DevControl *ctrl, const uint64_t *words, int64_t nbuf
   ctrl->zig_avail = (uint64_t)T;
   ctrl->err |= 2;
   if (st.kind == PRNG_SFC64 && j + 1 > (uint64_t)nbuf) ctrl->err |= 1;  // ran past the generated words
+}
+
+// Exact serial walk of a momenta window (fallback of the window mode).  The
+// walk assumes an attempt starts at the window's first word: exact for the
+// draw's first window (word 0), and -- like the parallel parse's
+// speculation -- in step with the true attempt chain within a few words
+// elsewhere, long before the first anchor (checked across shards).
+__device__ void zig_serial_window(DevControl *ctrl, const ZigWin &win, int64_t nwords) {
+  const StreamState st = ctrl->stream;
+  const int64_t w_end = win.w0 + nwords;
+  uint64_t j = (uint64_t)win.w0;
+  int64_t i = 0;
+  bool lo_done = false, hi_done = win.a_hi < 0;
+  while ((int64_t)j < w_end) {
+    const uint64_t j0 = j;  // this attempt's start
+    if (!lo_done && (int64_t)j0 >= win.a_lo) { win.info->cnt_lo = i; win.info->s_lo = (int64_t)j0; lo_done = true; }
+    if (!hi_done && (int64_t)j0 >= win.a_hi) { win.info->cnt_hi = i; win.info->s_hi = (int64_t)j0; hi_done = true; }
+    uint64_t r = word_at(st, st.pos + j);
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 0x1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double x = __dmul_rn((double)rabs, g_wi[idx]);
+    if (sign) x = -x;
+    j++;
+    bool acc = rabs < g_ki[idx];
+    if (!acc && idx == 0) {
+      for (;;) {
+        const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, glibc_log1p(-u01(word_at(st, st.pos + j))));
+        const double yy = -glibc_log1p(-u01(word_at(st, st.pos + j + 1)));
+        j += 2;
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+          x = ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
+          acc = true;
+          break;
+        }
+      }
+    } else if (!acc) {
+      const double u = u01(word_at(st, st.pos + j));
+      j++;
+      const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(g_fi[idx - 1], g_fi[idx]), u), g_fi[idx]);
+      acc = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x));
+    }
+    if (acc) {
+      if (i < win.cap) {
+        win.out[i] = x;
+        if (win.nend) win.nend[i] = (uint32_t)(j - (uint64_t)win.w0);
+      }
+      i++;
+    }
+  }
+  win.info->n_win = i;
+  win.info->w0 = win.w0;
+  if (win.a_hi < 0) { win.info->cnt_hi = i; win.info->s_hi = -1; }
+  win.info->err = 2;
+  ctrl->err |= 2;
 }
 
 // ---- ensemble: one numpy SFC64 stream per chain ------------------------------
@@ -1257,6 +1365,7 @@ int momenta_init(cudaStream_t s, uint64_t *bjump, int64_t T) {
 }
 
 size_t momenta_jump_bytes(int64_t T) { return (size_t)3 * (momenta_words(T) / ZB) * sizeof(uint64_t); }
+int64_t momenta_blocks(int64_t T) { return momenta_words(T) / ZB; }
 
 template <int KIND>
 static void launch_zig(const MomentaBufs &b, const uint64_t *words, int64_t nbuf, int64_t T, uint64_t *status,
@@ -1281,10 +1390,10 @@ static void launch_zig(const MomentaBufs &b, const uint64_t *words, int64_t nbuf
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, zig_kernel<KIND>, b.ctrl, words, nbuf, b.normals, T, status, bj, coresident, b.dbg);
+    cudaLaunchKernelEx(&cfg, zig_kernel<KIND>, b.ctrl, words, nbuf, b.normals, T, status, bj, coresident, b.dbg, ZigWin{});
     return;
   }
-  zig_kernel<KIND><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, coresident, b.dbg);
+  zig_kernel<KIND><<<nb, ZT, smem, s>>>(b.ctrl, words, nbuf, b.normals, T, status, bj, coresident, b.dbg, ZigWin{});
 }
 
 // Blocked layout (config 5): the momenta come from one SFC64 stream per block
@@ -1323,13 +1432,40 @@ int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, in
     words = b.sfc_words;
     (*launches)++;
   }
-  const uint64_t *bj = kind == PRNG_MINSTD ? b.bjump + 2 * nb : b.bjump;
+  // (the jump tables may cover more blocks than this draw: time-sharded contexts build them for windows)
+  const uint64_t *bj = kind == PRNG_MINSTD ? b.bjump + 2 * (b.bjump_blocks ? b.bjump_blocks : nb) : b.bjump;
   const size_t smem = sizeof(ZigShared);
   switch (kind) {
     case PRNG_PHILOX: launch_zig<PRNG_PHILOX>(b, words, nbuf, T, status, bj, nb, smem, s); break;
     case PRNG_MINSTD: launch_zig<PRNG_MINSTD>(b, words, nbuf, T, status, bj, nb, smem, s); break;
     case PRNG_PCG32: launch_zig<PRNG_PCG32>(b, words, nbuf, T, status, bj, nb, smem, s); break;
     default: launch_zig<PRNG_SFC64>(b, words, nbuf, T, status, bj, nb, smem, s); break;
+  }
+  (*launches)++;
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// Window mode (time-sharded momenta): parse blocks [w.wb0, w.wb0 + nb) of the
+// stream at the context's position into w.out, anchors into w.info.
+int launch_momenta_window(const MomentaBufs &b, int kind, const ZigWin &w, int nb, cudaStream_t s, int *launches) {
+  if (kind == PRNG_SFC64 || nb < 1) return -1;  // sequential generator: no window without the prefix
+  uint64_t *status = (uint64_t *)b.scratch;
+  const uint64_t *bj = kind == PRNG_MINSTD ? b.bjump + 2 * b.bjump_blocks : b.bjump;
+  const size_t smem = sizeof(ZigShared);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ZT, smem);
+    const int coresident = nb >= 64 && nb <= per_sm * sms ? 1 : 0;
+    kern<<<nb, ZT, smem, s>>>(b.ctrl, nullptr, 0, nullptr, 0, status, bj, coresident, b.dbg, w);
+  };
+  switch (kind) {
+    case PRNG_PHILOX: go(zig_kernel<PRNG_PHILOX>); break;
+    case PRNG_MINSTD: go(zig_kernel<PRNG_MINSTD>); break;
+    default: go(zig_kernel<PRNG_PCG32>); break;
   }
   (*launches)++;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;

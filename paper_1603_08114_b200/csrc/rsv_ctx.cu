@@ -32,10 +32,12 @@ namespace {
 struct GraphKey {
   int kind, n_steps, fuse, timing, stats;
   double dt;
-  int zc = 0;  // zero-copy input (rsv_hmc_update_host): the trajectory reads h from host memory
+  int zc = 0;     // zero-copy input (rsv_hmc_update_host): the trajectory reads h from host memory
+  int nomom = 0;  // time-sharded windowed momenta: the normals are placed before the graph runs
+  int devk = 0;   // theta constants from device memory (sharded run_chain)
   bool operator<(const GraphKey &o) const {
-    return std::tie(kind, n_steps, fuse, timing, stats, dt, zc) <
-           std::tie(o.kind, o.n_steps, o.fuse, o.timing, o.stats, o.dt, o.zc);
+    return std::tie(kind, n_steps, fuse, timing, stats, dt, zc, nomom, devk) <
+           std::tie(o.kind, o.n_steps, o.fuse, o.timing, o.stats, o.dt, o.zc, o.nomom, o.devk);
   }
 };
 
@@ -98,6 +100,17 @@ struct rsv_ctx {
   // series of Tg sites and owns [goff + own_lo, goff + own_hi)
   int64_t Tg = 0, goff = 0, own_lo = 0, own_hi = 0;
   bool shard = false;
+  int64_t jump_T = 0;  // length the momenta jump tables cover (time-sharded: the windows' reach)
+  // time-sharded windowed momenta (rsv_shard_set_momenta): this shard's window
+  // of the raw-word stream, its anchors, and the parse outputs
+  int win_mode = 0;
+  int64_t win_wb0 = 0, win_nb = 0, win_cap = 0, win_a_lo = 0, win_a_hi = -1;
+  double *win_out = nullptr;
+  uint32_t *win_nend = nullptr;
+  // sharded run_chain (rsv_shard_run_begin / _theta_async / _run_end)
+  DevPrior run_prior{};
+  double run_dt = 0.0;
+  int run_active = 0;
   int variant = -1;  // automatic: persistent, TMA-staged, window size by T (traj_geometry in leapfrog.cu)
   unsigned long long *dbg = nullptr;  // RSV_TRAJ_STAMPS=1: per-tile timestamps
 
@@ -157,6 +170,7 @@ struct rsv_ctx {
   EnsChain *blocks = nullptr, *h_blocks = nullptr;
   int64_t block_len = 0;
   int n_blocks = 0;
+  int64_t block_first = 0;  // time-sharded: the series block of this context's first block
   // run_chain on the device
   TrajConsts *kdev = nullptr;
   DevRun *run = nullptr;
@@ -208,6 +222,8 @@ int rsv_destroy(rsv_ctx *c) {
   }
   if (c->blocks) cudaFree(c->blocks);
   if (c->h_blocks) cudaFreeHost(c->h_blocks);
+  if (c->win_out) cudaFree(c->win_out);
+  if (c->win_nend) cudaFree(c->win_nend);
   if (c->kdev) cudaFree(c->kdev);
   if (c->run) cudaFree(c->run);
   if (c->run_store) cudaFree(c->run_store);
@@ -231,6 +247,14 @@ int rsv_destroy(rsv_ctx *c) {
   delete c;
   return 0;
 }
+
+// Time-sharded windowed momenta: raw words per normal of numpy's ziggurat
+// (1.0225 on average) and the slack around a shard's expected word range --
+// the position of normal i wanders ~0.11 sqrt(i) words from i * rho, so the
+// slack covers > 30 standard deviations at any length.
+constexpr double WIN_RHO = 1.0225;
+static int64_t shard_slack(int64_t Tg) { return 8192 + (int64_t)(4.0 * sqrt((double)Tg)); }
+static int64_t shard_anchor(int64_t site) { return (int64_t)llround((double)site * WIN_RHO); }
 
 // T: local series length; Tg: global length (== T unless time-sharded: the
 // momenta are drawn for the whole series so every shard sees the same stream)
@@ -287,8 +311,11 @@ static int create_impl(rsv_ctx *c, int device, int64_t T, int64_t Tg) {
   memset(c->h_ctrl, 0, sizeof(DevControl));
   c->h_ctrl->stream.kind = PRNG_PHILOX;
   CK(cudaMemcpy(c->ctrl, c->h_ctrl, sizeof(DevControl), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&c->bjump, momenta_jump_bytes(Tg)));
-  if (momenta_init(c->stream, c->bjump, Tg)) return fail(c, RSV_E_CUDA, "momenta table init failed");
+  // time-sharded contexts parse windows that reach a little past the
+  // expected end of the draw (shard_window): their jump tables cover it
+  c->jump_T = c->shard ? Tg + 2 * shard_slack(Tg) + 4 * (int64_t)ZB : Tg;
+  CK(cudaMalloc(&c->bjump, momenta_jump_bytes(c->jump_T)));
+  if (momenta_init(c->stream, c->bjump, c->jump_T)) return fail(c, RSV_E_CUDA, "momenta table init failed");
   c->launches += 2;
   CK(cudaStreamSynchronize(c->stream));
   return 0;
@@ -376,7 +403,7 @@ int rsv_set_params(rsv_ctx *c, const rsv_params *p) {
   q.inv_se2 = 1.0 / q.se2;
   q.emu = exp(-q.mu);
   q.one_m_phi2 = 1.0 - q.phi * q.phi;
-  const double Td = (double)c->T;
+  const double Td = (double)(c->shard ? c->Tg : c->T);  // a shard's H constant is the whole series'
   q.hconst = 0.5 * Td * q.mu + 0.5 * Td * log(q.su2) + 0.5 * log(q.se2 / (1.0 - q.phi * q.phi)) +
              0.5 * (Td - 1.0) * log(q.se2);
   q.n_lo = (int32_t)floor((q.mu - 50.0) * RSV_INV_LN2_N);
@@ -480,8 +507,10 @@ static MomentaBufs mbufs(rsv_ctx *c) {
   b.sfc_snaps = c->sfc_snaps;
   b.normals = c->normals;
   b.bjump = c->bjump;
+  b.bjump_blocks = momenta_blocks(c->jump_T ? c->jump_T : c->Tg);
   b.dbg = getenv("RSV_ZIG_STAMPS") ? c->dbg : nullptr;
   b.blocks = c->blocks;
+  if (c->blocks) b.normals = c->normals + c->block_first * c->block_len;  // a shard's first block
   b.block_len = c->block_len;
   b.n_blocks = c->n_blocks;
   return b;
@@ -498,6 +527,9 @@ static void drop_graphs(rsv_ctx *c) {  // the momenta layout changed: recapture
 
 static int check_err_bits(rsv_ctx *c) {
   if (c->h_ctrl->err & 1) return fail(c, RSV_E_CUDA, "momenta word budget exhausted (ziggurat shortfall)");
+  if (c->h_ctrl->err & 16)
+    return fail(c, RSV_E_CUDA, "sharded momenta: neighbouring windows disagree on an attempt boundary");
+  if (c->h_ctrl->err & 32) return fail(c, RSV_E_CUDA, "sharded momenta: a window does not cover its shard");
   if (c->h_ctrl->err & 4) return fail(c, RSV_E_CUDA, "ensemble momenta: a tail draw needed > 30 loops");
   return 0;
 }
@@ -644,19 +676,24 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   cg->dt = k.dt;
   cg->args = traj_args(c, k.dt, k.n_steps, k.fuse, g);
   cg->args.stats = k.stats;
+  if (k.devk) {
+    if (!g.ok || g.variant < 11 || g.variant > 14 || !c->kdev)
+      return fail(c, RSV_E_STATE, "sharded run_chain needs a persistent trajectory shape");
+    cg->args.kdev = c->kdev;
+  }
   if (k.zc && g.ok) {  // h_src is re-pointed at the caller's page-locked path per call
     cg->args.h_src = c->hbuf[0];
     cg->args.h_dst = c->hbuf[1];
   }
   // programmatic dependent launch of the trajectory after the momenta kernel
   // (not with timing event nodes between them)
-  cg->args.pdl = (k.timing == 0 && variant_is_persistent(g.variant) && !getenv("RSV_NO_PDL")) ? 1 : 0;
+  cg->args.pdl = (k.timing == 0 && !k.nomom && variant_is_persistent(g.variant) && !getenv("RSV_NO_PDL")) ? 1 : 0;
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   int l = 0;
   bool ok = true;
   if (k.timing) cudaEventRecordWithFlags(c->evpool[0], c->stream, cudaEventRecordExternal);
-  ok &= launch_momenta(mbufs(c), k.kind, c->Tg, c->stream, &l) == 0;
+  if (!k.nomom) ok &= launch_momenta(mbufs(c), k.kind, c->Tg, c->stream, &l) == 0;
   if (k.timing) cudaEventRecordWithFlags(c->evpool[1], c->stream, cudaEventRecordExternal);
   if (g.ok) ok &= launch_trajectory(cg->args, c->stream, &l) == 0;
   else ok &= enqueue_fallback(c, k.dt, k.n_steps, k.stats, &l);
@@ -672,7 +709,7 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   CK(cudaGraphGetNodes(graph, nullptr, &n));
   std::vector<cudaGraphNode_t> nodes(n);
   CK(cudaGraphGetNodes(graph, nodes.data(), &n));
-  const void *fn = g.ok ? traj_kernel_fn(g.variant, k.fuse, k.stats) : nullptr;
+  const void *fn = !g.ok ? nullptr : k.devk ? traj_kernel_fn_devk(g.variant, k.fuse) : traj_kernel_fn(g.variant, k.fuse, k.stats);
   cg->traj_node = nullptr;
   cg->launches = l;
   cg->ev.assign(4, nullptr);
@@ -705,6 +742,8 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
 static int get_graph(rsv_ctx *c, double dt, int n_steps, int fuse, int stats, rsv_ctx::Cached **out,
                      int *kernels, int zc = 0) {
   GraphKey k{c->kind, n_steps, fuse ? 1 : 0, c->timing == 2 ? 1 : 0, stats ? 1 : 0, dt, zc};
+  k.nomom = c->shard && c->win_mode && !c->blocks ? 1 : 0;
+  k.devk = c->shard && c->run_active && stats ? 1 : 0;
   auto it = c->graphs.find(k);
   if (it == c->graphs.end()) {
     rsv_ctx::Cached *cg = nullptr;
@@ -1325,9 +1364,10 @@ __device__ __forceinline__ double rec_unfix(__int128 q) {  // as unfix128 in lea
 // same data, so every rank takes the same decision (sampler.py:155-167);
 // then the stream advances and the kept path's statistics and the result
 // are recorded.
-__global__ void shard_decide_kernel(DevControl *C, const ShardRec *g, int world, double hconst,
-                                    const uint64_t *snaps, DevResult *ring, int cap, int32_t *count) {
+__global__ void shard_decide_kernel(DevControl *C, const ShardRec *g, int world, const DevParams *prm,
+                                    const uint64_t *snaps, DevResult *ring, int cap, int32_t *count, int windowed) {
   if (threadIdx.x || blockIdx.x) return;
+  if (C->halt) return;  // sharded run_chain stopped at an earlier sweep
   __int128 q0 = 0, q1 = 0, q2 = 0;
   double fl = 0.0;
   double S[14];  // moments old 0..4, new 5..9, ends 10..13
@@ -1348,13 +1388,24 @@ __global__ void shard_decide_kernel(DevControl *C, const ShardRec *g, int world,
     q2 += rec128(g[r].part.hnew);
     fl = fmax(fl, g[r].part.flag);
   }
-  const uint64_t u_word = g[0].u_word;
-  bool consistent = true;
-  for (int r = 1; r < world; r++) consistent &= g[r].u_word == u_word;
-  if (!consistent) atomicOr(&C->err, 8);
+  // the momenta's end in the stream: every shard drew the whole series
+  // (replicated) -- then all records must agree -- or the last shard's
+  // window holds the draw's end (windowed); either way the last record
+  const uint64_t u_word = g[world - 1].u_word;
+  if (!windowed) {
+    bool consistent = true;
+    for (int r = 0; r < world - 1; r++) consistent &= g[r].u_word == u_word && g[r].words_used == g[world - 1].words_used;
+    if (!consistent) atomicOr(&C->err, 8);
+  }
+  C->zig_used = g[world - 1].words_used;
+  {
+    const StreamState &st = C->stream;
+    if (st.kind == PRNG_PCG32) C->seq_next = pcg_advance(st.s[0], 2 * (st.pos + C->zig_used), st.s[1]);
+    else if (st.kind == PRNG_MINSTD) C->seq_next = mod31(minstd_pow(3 * (st.pos + C->zig_used)) * st.s[0]);
+  }
   DevResult res;
-  res.h_old = rec_unfix(q1) + hconst;
-  res.h_new = rec_unfix(q2) + hconst;
+  res.h_old = rec_unfix(q1) + prm->hconst;
+  res.h_new = rec_unfix(q2) + prm->hconst;
   res.accept = 0;
   res.u = __longlong_as_double(0x7ff8000000000000LL);
   const double dh = rec_unfix(q0);
@@ -1496,7 +1547,7 @@ int rsv_shard_propose_async(rsv_ctx *c, double dt, int n_steps, int fuse, int st
   return 0;
 }
 
-int rsv_shard_decide_async(rsv_ctx *c, const double *gathered_dev, int world, double hconst) {
+int rsv_shard_decide_async(rsv_ctx *c, const double *gathered_dev, int world) {
   if (!c || !gathered_dev || world < 1) return fail(c, RSV_E_INVALID, "bad argument");
   if (!c->shard) return fail(c, RSV_E_STATE, "not a shard context (rsv_create_shard)");
   CK(cudaSetDevice(c->device));
@@ -1509,8 +1560,8 @@ int rsv_shard_decide_async(rsv_ctx *c, const double *gathered_dev, int world, do
     CK(cudaMemsetAsync(c->ring_count, 0, sizeof(int32_t), c->stream));
   }
   shard_decide_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, reinterpret_cast<const ShardRec *>(gathered_dev), world,
-                                              hconst, c->sfc_snaps, c->ring,
-                                              c->ring_cap, c->ring_count);
+                                              c->prm, c->sfc_snaps, c->ring, c->ring_cap, c->ring_count,
+                                              c->win_mode && !c->blocks ? 1 : 0);
   c->launches++;
   CK(cudaGetLastError());
   return 0;
@@ -1528,6 +1579,228 @@ int rsv_shard_halo_async(rsv_ctx *c, double *left, int64_t nl, double *right, in
   c->launches++;
   CK(cudaGetLastError());
   return 0;
+}
+
+// ---- windowed momenta of a time-sharded chain ----------------------------
+// Placement: the all-gathered windows give every shard the global index of
+// its window's normals (exclusive prefix of the counts between anchors);
+// the neighbours' views of each anchor must agree, and the window must
+// cover the shard's sites.  The shard's normals are copied to where the
+// trajectory reads them; the last shard also finds the draw's end (the word
+// after normal Tg - 1) and the Metropolis uniform right after it.
+__global__ void shard_place_kernel(DevControl *C, const WinInfo *g, int world, int rank, const double *win,
+                                   const uint32_t *nend, double *dst, int64_t n_local, int64_t ls, int64_t Tg) {
+  __shared__ int64_t s_k0;
+  if (C->halt) return;
+  if (threadIdx.x == 0) {
+    int64_t off = 0;
+    bool ok = true;
+    for (int q = 0; q < world; q++) {
+      if (g[q].cnt_lo < 0 || g[q].cnt_hi < g[q].cnt_lo || g[q].n_win < g[q].cnt_hi) ok = false;
+      if (q < rank) off += g[q].cnt_hi - g[q].cnt_lo;
+      if (q + 1 < world && g[q].s_hi != g[q + 1].s_lo) ok = false;
+    }
+    const WinInfo &m = g[rank];
+    const int64_t k0 = ls - off + m.cnt_lo;  // window index of global normal ls
+    int err = ok ? 0 : 16;
+    if (k0 < 0 || k0 + n_local > m.n_win) err |= 32;
+    if (blockIdx.x == 0 && rank == world - 1 && !err) {
+      const int64_t kT = Tg - 1 - off + m.cnt_lo;
+      if (kT < 0 || kT >= m.n_win) {
+        err |= 32;
+      } else {
+        const uint64_t used = (uint64_t)(m.w0 + nend[kT]);
+        const StreamState &st = C->stream;
+        C->zig_used = used;
+        C->u_word = word_at(st, st.pos + used);
+        if (st.kind == PRNG_PCG32) C->seq_next = pcg_advance(st.s[0], 2 * (st.pos + used), st.s[1]);
+        else if (st.kind == PRNG_MINSTD) C->seq_next = mod31(minstd_pow(3 * (st.pos + used)) * st.s[0]);
+      }
+    }
+    if (err && blockIdx.x == 0) atomicOr(&C->err, err);
+    s_k0 = err ? -1 : k0;
+  }
+  __syncthreads();
+  const int64_t k0 = s_k0;
+  if (k0 < 0) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = win[k0 + i];
+}
+
+int rsv_shard_set_momenta(rsv_ctx *c, int windowed) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  if (!c->shard) return fail(c, RSV_E_STATE, "not a shard context (rsv_create_shard)");
+  if (!windowed) {
+    c->win_mode = 0;
+    return 0;
+  }
+  if (c->kind == PRNG_SFC64)
+    return fail(c, RSV_E_INVALID, "sfc64 has no jump-ahead: its single stream cannot be drawn in windows "
+                                "(use the blocked layout, rsv_set_blocked_streams)");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  // the shard's sites [goff, goff + T) are normals [goff, goff + T) of the
+  // draw; its window covers their expected words with the slack on both sides
+  const int64_t slack = shard_slack(c->Tg);
+  int64_t w_lo = shard_anchor(c->goff) - slack;
+  w_lo = w_lo < 0 ? 0 : w_lo;
+  if (c->goff == 0) w_lo = 0;
+  const int64_t w_hi = shard_anchor(c->goff + c->T) + slack;
+  c->win_wb0 = w_lo / ZB;
+  c->win_nb = (w_hi + ZB - 1) / ZB - c->win_wb0;
+  if (c->win_wb0 + c->win_nb > momenta_blocks(c->jump_T))
+    return fail(c, RSV_E_STATE, "momenta window beyond the jump tables");
+  // anchors: the expected first word of the owned range; the first shard's is
+  // word 0 (exact), the last shard has none above
+  const int64_t lo_g = c->goff + c->own_lo, hi_g = c->goff + c->own_hi;
+  c->win_a_lo = lo_g == 0 ? 0 : shard_anchor(lo_g);
+  c->win_a_hi = hi_g == c->Tg ? -1 : shard_anchor(hi_g);
+  const int64_t w0 = c->win_wb0 * ZB;
+  if (c->win_a_lo < w0 + 64 && lo_g != 0)
+    return fail(c, RSV_E_STATE, "momenta window starts too close to its anchor (margin too small)");
+  const int64_t cap = c->win_nb * ZB;
+  if (cap > c->win_cap) {
+    if (c->win_out) cudaFree(c->win_out);
+    if (c->win_nend) cudaFree(c->win_nend);
+    c->win_out = nullptr;
+    c->win_nend = nullptr;
+    CK(cudaMalloc(&c->win_out, sizeof(double) * (size_t)cap));
+    CK(cudaMalloc(&c->win_nend, sizeof(uint32_t) * (size_t)cap));
+    c->win_cap = cap;
+  }
+  c->win_mode = 1;
+  return 0;
+}
+
+__global__ void winfo_reset_kernel(WinInfo *w) {
+  if (threadIdx.x || blockIdx.x) return;
+  w->cnt_lo = w->cnt_hi = w->s_lo = w->s_hi = w->n_win = -1;
+  w->w0 = 0;
+  w->err = 0;
+  w->pad = 0;
+}
+
+int rsv_shard_momenta_async(rsv_ctx *c, double *winfo_dev) {
+  if (!c || !winfo_dev) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->shard || !c->win_mode) return fail(c, RSV_E_STATE, "windowed momenta not enabled (rsv_shard_set_momenta)");
+  int r;
+  if ((r = ready(c))) return r;
+  CK(cudaSetDevice(c->device));
+  WinInfo *wi = reinterpret_cast<WinInfo *>(winfo_dev);
+  winfo_reset_kernel<<<1, 1, 0, c->stream>>>(wi);
+  ZigWin w;
+  w.wb0 = c->win_wb0;
+  w.w0 = c->win_wb0 * ZB;
+  w.cap = c->win_cap;
+  w.a_lo = c->win_a_lo;
+  w.a_hi = c->win_a_hi;
+  w.out = c->win_out;
+  w.nend = c->win_a_hi < 0 ? c->win_nend : nullptr;  // only the last shard finds the draw's end
+  w.info = wi;
+  int l = 1;
+  if (launch_momenta_window(mbufs(c), c->kind, w, (int)c->win_nb, c->stream, &l))
+    return fail(c, RSV_E_CUDA, "windowed momenta launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  c->launches += l;
+  return 0;
+}
+
+int rsv_shard_place_async(rsv_ctx *c, const double *winfo_all, int world, int rank) {
+  if (!c || !winfo_all || world < 1 || rank < 0 || rank >= world) return fail(c, RSV_E_INVALID, "bad argument");
+  if (!c->shard || !c->win_mode) return fail(c, RSV_E_STATE, "windowed momenta not enabled (rsv_shard_set_momenta)");
+  if ((rank == world - 1) != (c->win_a_hi < 0) || (rank == 0) != (c->goff + c->own_lo == 0))
+    return fail(c, RSV_E_INVALID, "rank %d of %d does not match this shard's position", rank, world);
+  CK(cudaSetDevice(c->device));
+  const int nb = (int)((c->T + 255) / 256 < 2 * c->sm_count ? (c->T + 255) / 256 : 2 * c->sm_count);
+  shard_place_kernel<<<nb, 256, 0, c->stream>>>(c->ctrl, reinterpret_cast<const WinInfo *>(winfo_all), world, rank,
+                                                c->win_out, c->win_nend, c->normals + c->goff, c->T, c->goff, c->Tg);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// ---- run_chain of a time-sharded chain (sampler.py:291-358): every shard
+// runs the same theta kernel on the all-gathered statistics, so the
+// parameters stay identical across shards -----------------------------------
+int rsv_shard_run_begin(rsv_ctx *c, double dt, const rsv_prior *prior, int64_t n_burnin, int64_t n_samples,
+                        int64_t thin) {
+  if (!c || !prior) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->shard) return fail(c, RSV_E_STATE, "not a shard context (rsv_create_shard)");
+  int r;
+  if ((r = ready(c))) return r;
+  if (n_burnin < 0 || n_samples < 1 || thin < 1) return fail(c, RSV_E_INVALID, "bad burn-in / samples / thin");
+  const double pv[] = {prior->mu_var, prior->xi_var, prior->var_shape, prior->var_scale, prior->phi_a, prior->phi_b};
+  for (double v : pv)
+    if (!(v > 0.0)) return fail(c, RSV_E_INVALID, "prior variances, shapes and scales must be positive");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  if (!c->kdev) CK(cudaMalloc(&c->kdev, sizeof(TrajConsts)));
+  if (!c->run) CK(cudaMalloc(&c->run, sizeof(DevRun)));
+  if (n_samples > c->run_cap) {
+    if (c->run_store) cudaFree(c->run_store);
+    CK(cudaMalloc(&c->run_store, (size_t)n_samples * (5 * sizeof(double) + sizeof(double) + sizeof(int64_t) +
+                                                      sizeof(int32_t))));
+    c->run_cap = n_samples;
+  }
+  DevRun hr;
+  memset(&hr, 0, sizeof(hr));
+  hr.n_burnin = n_burnin;
+  hr.thin = thin;
+  hr.n_store = n_samples;
+  char *base = (char *)c->run_store;
+  hr.params = (double *)base;
+  hr.delta_h = hr.params + 5 * n_samples;
+  hr.iters = (int64_t *)(hr.delta_h + n_samples);
+  hr.accept = (int32_t *)(hr.iters + n_samples);
+  hr.storm_sweep = -1;
+  CK(cudaMemcpyAsync(c->run, &hr, sizeof(DevRun), cudaMemcpyHostToDevice, c->stream));
+  const TrajConsts k0 = traj_consts(*c->h_prm, dt);
+  CK(cudaMemcpyAsync(c->kdev, &k0, sizeof(TrajConsts), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
+  CK(cudaMemsetAsync(&c->ctrl->halt, 0, sizeof(int32_t), c->stream));
+  c->run_prior = DevPrior{prior->mu_mean, prior->mu_var, prior->xi_mean, prior->xi_var,
+                          prior->var_shape, prior->var_scale, prior->phi_a, prior->phi_b};
+  c->run_dt = dt;
+  c->run_active = 1;
+  return sync(c);
+}
+
+// the theta draws of one sweep, after rsv_shard_decide_async (statistics of
+// the kept path over the whole series, combined from every shard)
+int rsv_shard_theta_async(rsv_ctx *c) {
+  if (!c || !c->shard || !c->run_active) return fail(c, RSV_E_STATE, "no sharded run (rsv_shard_run_begin)");
+  CK(cudaSetDevice(c->device));
+  int l = 0;
+  if (launch_theta_sweep(c->ctrl, c->prm, c->kdev, c->run, c->run_prior, c->run_dt, c->Tg, c->sfc_snaps, c->stream, &l,
+                         0))
+    return fail(c, RSV_E_CUDA, "theta kernel launch failed");
+  c->launches += l;
+  return 0;
+}
+
+int rsv_shard_run_end(rsv_ctx *c, int64_t *iters, double *params, int32_t *accept, double *delta_h,
+                      int64_t *n_stored, int64_t *storm_sweep) {
+  if (!c || !c->shard || !c->run_active) return fail(c, RSV_E_STATE, "no sharded run (rsv_shard_run_begin)");
+  CK(cudaSetDevice(c->device));
+  c->run_active = 0;
+  DevRun hr;
+  CK(cudaMemcpyAsync(&hr, c->run, sizeof(DevRun), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_prm, c->prm, sizeof(DevParams), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemsetAsync(&c->ctrl->halt, 0, sizeof(int32_t), c->stream));
+  int r;
+  if ((r = pull_ctrl(c)) || (r = check_err_bits(c))) return r;
+  if ((r = refresh_graph_params(c))) return r;
+  if (storm_sweep) *storm_sweep = hr.storm_sweep;
+  if (n_stored) *n_stored = hr.stored;
+  if (hr.storm_sweep >= 0)
+    return fail(c, RSV_E_STORM, "more than %d of the last %d HMC proposals diverged at sweep %lld", RUN_STORM_LIMIT,
+                RUN_STORM_WINDOW, (long long)hr.storm_sweep);
+  if (hr.degenerate) return fail(c, RSV_E_INVALID, "degenerate full-conditional precision");
+  const int64_t n = hr.stored;
+  if (params) CK(cudaMemcpyAsync(params, hr.params, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost, c->stream));
+  if (delta_h) CK(cudaMemcpyAsync(delta_h, hr.delta_h, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  if (iters) CK(cudaMemcpyAsync(iters, hr.iters, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
+  if (accept) CK(cudaMemcpyAsync(accept, hr.accept, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+  return sync(c);
 }
 
 // results recorded by rsv_shard_decide_async since the last call (syncs)
@@ -1648,9 +1921,34 @@ int rsv_simulate(int device, const rsv_params *p, int64_t T, rsv_prng_state *st,
 }
 
 // ---- blocked momenta streams (config 5) -----------------------------------
+static int set_blocks(rsv_ctx *c, int64_t block_len, int64_t first_block, int64_t n_blocks, const uint64_t *states);
+
 int rsv_set_blocked_streams(rsv_ctx *c, int64_t block_len, int64_t n_blocks, const uint64_t *states) {
   if (!c) return fail(c, RSV_E_INVALID, "null context");
   if (c->shard || c->ens_C) return fail(c, RSV_E_STATE, "blocked momenta need a single-chain context");
+  return set_blocks(c, block_len, 0, n_blocks, states);
+}
+
+// a time-sharded chain: the shard holds the streams of the blocks its local
+// range (owned sites and margins) touches, [first_block, first_block +
+// n_blocks) of the series' Tg / block_len blocks; a block in two shards'
+// ranges is drawn by both, from identical states
+int rsv_shard_set_blocked_streams(rsv_ctx *c, int64_t block_len, int64_t first_block, int64_t n_blocks,
+                                  const uint64_t *states) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  if (!c->shard) return fail(c, RSV_E_STATE, "not a shard context (rsv_create_shard)");
+  if (states && n_blocks) {
+    if (block_len < 64 || block_len % 8 || c->Tg % block_len)
+      return fail(c, RSV_E_INVALID, "blocks must tile the series (block length a multiple of 8, >= 64)");
+    const int64_t j0 = c->goff / block_len, j1 = (c->goff + c->T + block_len - 1) / block_len;
+    if (first_block != j0 || n_blocks != j1 - j0)
+      return fail(c, RSV_E_INVALID, "shard [%lld, %lld) needs blocks [%lld, %lld)", (long long)c->goff,
+                  (long long)(c->goff + c->T), (long long)j0, (long long)j1);
+  }
+  return set_blocks(c, block_len, first_block, n_blocks, states);
+}
+
+static int set_blocks(rsv_ctx *c, int64_t block_len, int64_t first_block, int64_t n_blocks, const uint64_t *states) {
   CK(cudaSetDevice(c->device));
   CK(cudaStreamSynchronize(c->stream));
   if (!states || n_blocks == 0) {  // back to the single-stream layout
@@ -1659,10 +1957,11 @@ int rsv_set_blocked_streams(rsv_ctx *c, int64_t block_len, int64_t n_blocks, con
     c->blocks = c->h_blocks = nullptr;
     c->block_len = 0;
     c->n_blocks = 0;
+    c->block_first = 0;
     drop_graphs(c);
     return 0;
   }
-  if (block_len < 64 || block_len % 8 || block_len * n_blocks != c->T || n_blocks > (1 << 24))
+  if (!c->shard && (block_len < 64 || block_len % 8 || block_len * n_blocks != c->T || n_blocks > (1 << 24)))
     return fail(c, RSV_E_INVALID, "blocks must tile the series: %lld x %lld != %lld (block length a multiple of 8, >= 64)",
                 (long long)n_blocks, (long long)block_len, (long long)c->T);
   if (n_blocks != c->n_blocks) {
@@ -1676,9 +1975,10 @@ int rsv_set_blocked_streams(rsv_ctx *c, int64_t block_len, int64_t n_blocks, con
   for (int64_t i = 0; i < n_blocks; i++)
     for (int k = 0; k < 4; k++) c->h_blocks[i].st[k] = states[4 * i + k];
   CK(cudaMemcpy(c->blocks, c->h_blocks, sizeof(EnsChain) * (size_t)n_blocks, cudaMemcpyHostToDevice));
-  const bool changed = c->block_len != block_len || c->n_blocks != (int)n_blocks;
+  const bool changed = c->block_len != block_len || c->n_blocks != (int)n_blocks || c->block_first != first_block;
   c->block_len = block_len;
   c->n_blocks = (int)n_blocks;
+  c->block_first = first_block;
   if (changed) drop_graphs(c);
   return 0;
 }

@@ -62,6 +62,32 @@ struct ShardRec {
 constexpr int SHARD_W = (int)(sizeof(ShardRec) / 8);
 static_assert(SHARD_W == 23, "rsv_shard_totals layout");
 
+// ---- time-sharded momenta: each shard parses only a window of the raw-word
+// stream around its sites.  Anchor words a_r (the expected
+// start of shard r's first owned normal) split the stream; a shard counts
+// the normals whose attempts start in [a_r, a_{r+1}), the counts are
+// all-gathered and their exclusive prefix gives every window its global
+// normal index.  Neighbouring windows overlap around each anchor: both
+// shards report the first attempt start at or after it, which must agree
+// (the check that the speculative start of a window has synchronised).
+struct WinInfo {           // one shard's window, all-gathered (8 words)
+  int64_t cnt_lo, cnt_hi;  // window normals whose attempts start before a_lo / a_hi
+  int64_t s_lo, s_hi;      // first attempt start at or after a_lo / a_hi (words past the stream position)
+  int64_t n_win;           // normals the window produced
+  int64_t w0;              // first word of the window
+  int64_t err;             // bit 1: the exact serial walk redid the window
+  int64_t pad;
+};
+struct ZigWin {            // window mode of the momenta kernel
+  int64_t wb0;             // first block: CTA b of the window parses block wb0 + b of the full stream
+  int64_t w0;              // wb0 * ZB
+  int64_t cap;             // capacity of out / nend (normals)
+  int64_t a_lo, a_hi;      // anchors (words past the stream position); a_hi < 0: the last shard
+  double *out;             // the window's normals, in stream order
+  uint32_t *nend;          // optional: per normal, the word after its attempt (relative to w0)
+  WinInfo *info;
+};
+
 // ---- ensemble of independent chains (rsv_ens_*) ------------------------------
 struct EnsPart {  // per trajectory tile: partials of the (<= 2) chains its core touches
   double dh, hold, hnew, flag;

@@ -15,6 +15,7 @@ struct MomentaBufs {
   uint64_t *sfc_snaps;  // SFC64 only: 4 * ((momenta_words(T) + 64) / SFC_SNAP + 1) words
   double *normals;      // T doubles
   const uint64_t *bjump;  // momenta_jump_bytes(T): per-CTA jump-ahead constants
+  int64_t bjump_blocks = 0;  // blocks of the full draw the tables were built for (minstd's half follows pcg's)
   unsigned long long *dbg;  // optional per-CTA %globaltimer stamps (development aid)
   // blocked layout (config 5): one SFC64 stream per block of block_len sites
   EnsChain *blocks = nullptr;
@@ -29,6 +30,8 @@ size_t momenta_jump_bytes(int64_t T);
 size_t momenta_scratch_bytes(int64_t T);
 int launch_momenta(const MomentaBufs &b, int kind, int64_t T, cudaStream_t s, int *launches);
 int launch_momenta_advance(const MomentaBufs &b, cudaStream_t s, int *launches);
+int launch_momenta_window(const MomentaBufs &b, int kind, const ZigWin &w, int nb, cudaStream_t s, int *launches);
+int64_t momenta_blocks(int64_t T);  // CTAs (blocks of ZB words) of a full draw of T normals
 
 // Tile geometry of the fused trajectory kernel for (T, n_steps).
 struct TrajGeom {

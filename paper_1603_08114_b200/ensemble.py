@@ -22,12 +22,12 @@ from . import _native as N
 from .model import Params
 
 
-def sfc64_states(seed: int, n_chains: int) -> np.ndarray:
+def sfc64_states(seed: int, n_chains: int, start: int = 0) -> np.ndarray:
     """State words (a, b, c, counter) of ``SFC64(SeedSequence([seed, c]))``
-    for c = 0 .. n_chains-1 (the config-4 seeding)."""
+    for c = start .. start+n_chains-1 (the config-4 seeding)."""
     out = np.empty((n_chains, 4), dtype=np.uint64)
-    for c in range(n_chains):
-        out[c] = np.random.SFC64(np.random.SeedSequence([seed, c])).state["state"]["state"]
+    for i in range(n_chains):
+        out[i] = np.random.SFC64(np.random.SeedSequence([seed, start + i])).state["state"]["state"]
     return out
 
 

@@ -163,6 +163,22 @@ class CudaShard:
     def apply(self, accept: bool, drew: bool):
         self._ck(self._lib.rsv_shard_apply(self.ctx, int(bool(accept)), int(bool(drew))))
 
+    def set_momenta(self, windowed: bool):
+        self._ck(self._lib.rsv_shard_set_momenta(self.ctx, int(bool(windowed))))
+
+    def set_blocked_streams(self, block_len: int, first_block: int, states):
+        if states is None:
+            self._ck(self._lib.rsv_shard_set_blocked_streams(self.ctx, 0, 0, 0, None))
+            return
+        states = np.ascontiguousarray(states, dtype=np.uint64)
+        self._ck(self._lib.rsv_shard_set_blocked_streams(self.ctx, int(block_len), int(first_block),
+                                                         int(states.shape[0]), states.ctypes.data))
+
+    def get_params(self) -> Params:
+        out = N.Params()
+        self._ck(self._lib.rsv_get_params(self.ctx, ctypes.byref(out)))
+        return Params(phi=out.phi, mu=out.mu, xi=out.xi, sigma_eta_sq=out.sigma_eta_sq, sigma_u_sq=out.sigma_u_sq)
+
 
 @dataclass
 class Decision:
@@ -231,6 +247,29 @@ class ShardedChain:
         self.params = params
         self.shard.set_params(params)
         self.halo_valid = False
+        self.windowed = False
+
+    # -- momenta layout --
+    def set_windowed_momenta(self, on: bool = True):
+        """Draw only this shard's window of the momenta stream (jump-ahead
+        generators; device-orchestrated drivers): the normals are the
+        whole-series draw's, bit for bit (rsv_shard_set_momenta)."""
+        self.shard.set_momenta(on)
+        self.windowed = bool(on)
+
+    def set_blocked_streams(self, seed: int | None, block_len: int = 4096):
+        """Config-5 layout on a shard: the streams SFC64(SeedSequence([seed,
+        j])) of the blocks j its local range touches (DeviceChain's layout,
+        per shard)."""
+        if seed is None:
+            self.shard.set_blocked_streams(0, 0, None)
+            return
+        if self.T % block_len:
+            raise ValueError(f"block length {block_len} does not divide T={self.T}")
+        from .ensemble import sfc64_states
+        j0, j1 = self.ls // block_len, -(-self.le // block_len)
+        states = sfc64_states(seed, j1 - j0, j0)
+        self.shard.set_blocked_streams(block_len, j0, states)
 
     # -- state --
     def set_params(self, params: Params):
@@ -374,101 +413,81 @@ def _results(chain, n):
     return [out[i] for i in range(min(n, got.value))]
 
 
-def hmc_update_local_device(chains: list[ShardedChain], step_size: float, n_steps: int, n: int,
-                            fuse: bool = False, stats: bool = False, halo_every: int | None = None):
-    """n proposals of a chain whose shards live in this process (one GPU or
-    several), orchestrated on the device: no host synchronisation until the
-    results are read back.  Returns the per-proposal rsv_result records."""
-    import torch
-    _cuda_shard_ptrs(chains)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    stream = torch.cuda.Stream(dev)  # one ordered stream for every shard and every buffer
-    with torch.cuda.stream(stream):
-        return _local_device(chains, step_size, n_steps, n, fuse, stats, halo_every, dev, stream)
+WIN_W = 8  # 8-byte words of a momenta window record (WinInfo)
 
 
-def _local_device(chains, step_size, n_steps, n, fuse, stats, halo_every, dev, stream):
+class _LocalComm:
+    """All shards of the chain in this process (one GPU, one stream): the
+    records are gathered by device copies, the halos by direct slices."""
+
+    def __init__(self, chains):
+        self.chains = chains
+        self.world = len(chains)
+
+    def gather(self, out, mine):
+        for r, m in enumerate(mine):
+            out[r].copy_(m)
+
+    def halo(self, chains, sends, recvs):
+        for r, c in enumerate(chains):  # my left margin <- left neighbour's right send, and vice versa
+            recvs[r][0].copy_(sends[r - 1][1]) if r > 0 else None
+            recvs[r][1].copy_(sends[r + 1][0]) if r < len(chains) - 1 else None
+
+
+class _NcclComm:
+    """One shard per rank of a torch.distributed (NCCL) group: records by
+    all_gather_into_tensor, halos by batched send/recv with the neighbours."""
+
+    def __init__(self, chain, group):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank, self.world = chain.rank, chain.world
+
+    def gather(self, out, mine):
+        self.dist.all_gather_into_tensor(out, mine[0], group=self.group)
+
+    def halo(self, chains, sends, recvs):
+        dist, r, w = self.dist, self.rank, self.world
+        (send_l, send_r), (recv_l, recv_r) = sends[0], recvs[0]
+        ops = []
+        if r > 0:
+            ops += [dist.P2POp(dist.isend, send_l, r - 1, self.group), dist.P2POp(dist.irecv, recv_l, r - 1, self.group)]
+        if r < w - 1:
+            ops += [dist.P2POp(dist.isend, send_r, r + 1, self.group), dist.P2POp(dist.irecv, recv_r, r + 1, self.group)]
+        for q in dist.batch_isend_irecv(ops) if ops else []:
+            q.wait()  # orders the copies on the current stream (no host block)
+
+
+def _drive(chains, comm, step_size, n_steps, n, fuse, stats, halo_every, dev, stream, l2_flush=None, times=None,
+           theta=False):
+    """n proposals (or sweeps with theta=True) of the chain whose shards
+    `chains` live in this process, every step enqueued on `stream`:
+    [margins every K proposals] -> [windowed momenta: window parse,
+    all-gather of the window records, placement] -> trajectory + this
+    shard's record -> all-gather of the records -> the same decision on
+    every shard -> [theta draws].  The host synchronises only to read the
+    result ring."""
     import torch
-    world = len(chains)
+    world = comm.world
+    c0 = chains[0]
+    lib = c0.shard._lib
     for c in chains:
-        c.shard._ck(c.shard._lib.rsv_set_stream(c.shard.ctx, ctypes.c_void_p(stream.cuda_stream)))
-    K = halo_every or halo_period(chains[0].margin, n_steps)
-    hc = h_constant(chains[0].params, chains[0].T)
-    gathered = torch.zeros((world, TOTALS), dtype=torch.float64, device=dev)
-    res = [[] for _ in chains]
-    sends = [(torch.empty(c.halo_sizes(c.rank - 1)[1] if c.rank > 0 else 0, dtype=torch.float64, device=dev),
-              torch.empty(c.halo_sizes(c.rank + 1)[0] if c.rank < world - 1 else 0, dtype=torch.float64, device=dev))
-             for c in chains]
-    lib = chains[0].shard._lib
-    try:
-        for i in range(n):
-            if i % K == 0 or not all(c.halo_valid for c in chains):
-                for c, (sl, sr) in zip(chains, sends):
-                    c.shard._ck(lib.rsv_shard_halo_async(c.shard.ctx, sl.data_ptr(), sl.numel(), sr.data_ptr(),
-                                                         sr.numel(), 0))
-                for r, c in enumerate(chains):  # my left margin <- left neighbour's right send, and vice versa
-                    fl = sends[r - 1][1] if r > 0 else None
-                    fr = sends[r + 1][0] if r < world - 1 else None
-                    c.shard._ck(lib.rsv_shard_halo_async(
-                        c.shard.ctx, fl.data_ptr() if fl is not None else None, fl.numel() if fl is not None else 0,
-                        fr.data_ptr() if fr is not None else None, fr.numel() if fr is not None else 0, 1))
-                    c.halo_valid = True
-            for r, c in enumerate(chains):
-                c.shard._ck(lib.rsv_shard_propose_async(c.shard.ctx, float(step_size), int(n_steps), int(bool(fuse)),
-                                                        int(bool(stats)), gathered[r].data_ptr()))
-            for c in chains:
-                c.shard._ck(lib.rsv_shard_decide_async(c.shard.ctx, gathered.data_ptr(), world, float(hc)))
-            if (i + 1) % _RING == 0:  # the device result ring holds _RING records
-                for c, acc in zip(chains, res):
-                    acc.extend(_results(c, _RING))
-        for c, acc in zip(chains, res):
-            acc.extend(_results(c, n % _RING))
-    finally:
-        for c in chains:
-            c.shard._lib.rsv_set_stream(c.shard.ctx, None)
-    for r in range(1, world):  # every shard recorded the same decisions
-        if [x.accept for x in res[r]] != [x.accept for x in res[0]]:
-            raise RuntimeError("shards took different decisions")
-    return res[0]
-
-
-def hmc_update_distributed_device(chain: ShardedChain, step_size: float, n_steps: int, n: int, fuse: bool = False,
-                                  stats: bool = False, group=None, halo_every: int | None = None,
-                                  l2_flush=None, times: list | None = None):
-    """n proposals of a sharded chain over a torch.distributed (NCCL) group,
-    orchestrated on the device: totals all-gathered on the GPU, decisions on
-    the GPU, periodic halo exchange; the host synchronises once at the end.
-    Benchmarking: `l2_flush` (a device tensor larger than L2) is overwritten
-    before every proposal, and `times` collects one (start, end) CUDA event
-    pair per proposal, recorded after the flush and after the decision."""
-    import torch
-    _cuda_shard_ptrs([chain])
-    dev = torch.device("cuda", torch.cuda.current_device())
-    stream = torch.cuda.Stream(dev)  # the kernels and the NCCL collectives share one ordered stream
-    with torch.cuda.stream(stream):
-        return _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_every, dev, stream,
-                                   l2_flush, times)
-
-
-def _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_every, dev, stream, l2_flush=None,
-                        times=None):
-    import torch
-    import torch.distributed as dist
-    r, w = chain.rank, chain.world
-    lib = chain.shard._lib
-    chain.shard._ck(lib.rsv_set_stream(chain.shard.ctx, ctypes.c_void_p(stream.cuda_stream)))
-    K = halo_every or halo_period(chain.margin, n_steps)
-    hc = h_constant(chain.params, chain.T)
-    mine = torch.zeros(TOTALS, dtype=torch.float64, device=dev)
-    gathered = torch.zeros((w, TOTALS), dtype=torch.float64, device=dev)
-    nl_send = chain.halo_sizes(r - 1)[1] if r > 0 else 0
-    nr_send = chain.halo_sizes(r + 1)[0] if r < w - 1 else 0
-    nl_recv, nr_recv = chain.halo_sizes(r)
-    send_l = torch.empty(nl_send, dtype=torch.float64, device=dev)
-    send_r = torch.empty(nr_send, dtype=torch.float64, device=dev)
-    recv_l = torch.empty(nl_recv if r > 0 else 0, dtype=torch.float64, device=dev)
-    recv_r = torch.empty(nr_recv if r < w - 1 else 0, dtype=torch.float64, device=dev)
-    out = []
+        c.shard._ck(lib.rsv_set_stream(c.shard.ctx, ctypes.c_void_p(stream.cuda_stream)))
+    K = halo_every or halo_period(c0.margin, n_steps)
+    f64 = dict(dtype=torch.float64, device=dev)
+    rec_mine = [torch.zeros(TOTALS, **f64) for _ in chains]
+    rec_all = torch.zeros((world, TOTALS), **f64)
+    windowed = c0.windowed
+    win_mine = [torch.zeros(WIN_W, **f64) for _ in chains] if windowed else None
+    win_all = torch.zeros((world, WIN_W), **f64) if windowed else None
+    sends, recvs = [], []
+    for c in chains:
+        r = c.rank
+        nl_recv, nr_recv = c.halo_sizes(r)
+        sends.append((torch.empty(c.halo_sizes(r - 1)[1] if r > 0 else 0, **f64),
+                      torch.empty(c.halo_sizes(r + 1)[0] if r < world - 1 else 0, **f64)))
+        recvs.append((torch.empty(nl_recv if r > 0 else 0, **f64), torch.empty(nr_recv if r < world - 1 else 0, **f64)))
+    out = [[] for _ in chains]
     try:
         for i in range(n):
             if l2_flush is not None:
@@ -476,29 +495,122 @@ def _distributed_device(chain, step_size, n_steps, n, fuse, stats, group, halo_e
             if times is not None:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record(stream)
-            if w > 1 and (i % K == 0 or not chain.halo_valid):
-                chain.shard._ck(lib.rsv_shard_halo_async(chain.shard.ctx, send_l.data_ptr(), nl_send,
-                                                         send_r.data_ptr(), nr_send, 0))
-                ops = []
-                if r > 0:
-                    ops += [dist.P2POp(dist.isend, send_l, r - 1, group), dist.P2POp(dist.irecv, recv_l, r - 1, group)]
-                if r < w - 1:
-                    ops += [dist.P2POp(dist.isend, send_r, r + 1, group), dist.P2POp(dist.irecv, recv_r, r + 1, group)]
-                for q in dist.batch_isend_irecv(ops):
-                    q.wait()  # orders the copies on the current stream (no host block)
-                chain.shard._ck(lib.rsv_shard_halo_async(chain.shard.ctx, recv_l.data_ptr(), recv_l.numel(),
-                                                         recv_r.data_ptr(), recv_r.numel(), 1))
-                chain.halo_valid = True
-            chain.shard._ck(lib.rsv_shard_propose_async(chain.shard.ctx, float(step_size), int(n_steps),
-                                                        int(bool(fuse)), int(bool(stats)), mine.data_ptr()))
-            dist.all_gather_into_tensor(gathered, mine, group=group)
-            chain.shard._ck(lib.rsv_shard_decide_async(chain.shard.ctx, gathered.data_ptr(), w, float(hc)))
+            if world > 1 and (i % K == 0 or not all(c.halo_valid for c in chains)):
+                for c, (sl, sr) in zip(chains, sends):
+                    c.shard._ck(lib.rsv_shard_halo_async(c.shard.ctx, sl.data_ptr(), sl.numel(), sr.data_ptr(),
+                                                         sr.numel(), 0))
+                comm.halo(chains, sends, recvs)
+                for c, (fl, fr) in zip(chains, recvs):
+                    c.shard._ck(lib.rsv_shard_halo_async(c.shard.ctx, fl.data_ptr(), fl.numel(), fr.data_ptr(),
+                                                         fr.numel(), 1))
+                    c.halo_valid = True
+            if windowed:
+                for c, w in zip(chains, win_mine):
+                    c.shard._ck(lib.rsv_shard_momenta_async(c.shard.ctx, w.data_ptr()))
+                comm.gather(win_all, win_mine)
+                for c in chains:
+                    c.shard._ck(lib.rsv_shard_place_async(c.shard.ctx, win_all.data_ptr(), world, c.rank))
+            for c, m in zip(chains, rec_mine):
+                c.shard._ck(lib.rsv_shard_propose_async(c.shard.ctx, float(step_size), int(n_steps), int(bool(fuse)),
+                                                        int(bool(stats or theta)), m.data_ptr()))
+            comm.gather(rec_all, rec_mine)
+            for c in chains:
+                c.shard._ck(lib.rsv_shard_decide_async(c.shard.ctx, rec_all.data_ptr(), world))
+                if theta:
+                    c.shard._ck(lib.rsv_shard_theta_async(c.shard.ctx))
             if times is not None:
                 ev[1].record(stream)
                 times.append(ev)
-            if (i + 1) % _RING == 0:
-                out.extend(_results(chain, _RING))
-        out.extend(_results(chain, n % _RING))
-        return out
+            if (i + 1) % _RING == 0:  # the device result ring holds _RING records
+                for c, acc in zip(chains, out):
+                    acc.extend(_results(c, _RING))
+        for c, acc in zip(chains, out):
+            acc.extend(_results(c, n % _RING))
     finally:
-        lib.rsv_set_stream(chain.shard.ctx, None)
+        for c in chains:
+            lib.rsv_set_stream(c.shard.ctx, None)
+    for r in range(1, len(chains)):  # every shard recorded the same decisions
+        if [x.accept for x in out[r]] != [x.accept for x in out[0]]:
+            raise RuntimeError("shards took different decisions")
+    return out[0]
+
+
+def hmc_update_local_device(chains: list[ShardedChain], step_size: float, n_steps: int, n: int,
+                            fuse: bool = False, stats: bool = False, halo_every: int | None = None):
+    """n proposals of a chain whose shards all live in this process (one
+    GPU), orchestrated on the device: no host synchronisation until the
+    results are read back.  Returns the per-proposal rsv_result records."""
+    import torch
+    _cuda_shard_ptrs(chains)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.Stream(dev)  # one ordered stream for every shard and every buffer
+    with torch.cuda.stream(stream):
+        return _drive(chains, _LocalComm(chains), step_size, n_steps, n, fuse, stats, halo_every, dev, stream)
+
+
+def hmc_update_distributed_device(chain: ShardedChain, step_size: float, n_steps: int, n: int, fuse: bool = False,
+                                  stats: bool = False, group=None, halo_every: int | None = None,
+                                  l2_flush=None, times: list | None = None):
+    """n proposals of a sharded chain over a torch.distributed (NCCL) group,
+    orchestrated on the device: window records and shard records
+    all-gathered on the GPU, decisions on the GPU, periodic halo exchange;
+    the host synchronises once at the end.  Benchmarking: `l2_flush` (a
+    device tensor larger than L2) is overwritten before every proposal, and
+    `times` collects one (start, end) CUDA event pair per proposal, recorded
+    after the flush and after the decision."""
+    import torch
+    _cuda_shard_ptrs([chain])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.Stream(dev)  # the kernels and the NCCL collectives share one ordered stream
+    with torch.cuda.stream(stream):
+        return _drive([chain], _NcclComm(chain, group), step_size, n_steps, n, fuse, stats, halo_every, dev, stream,
+                      l2_flush, times)
+
+
+def run_chain_sharded(chains: list[ShardedChain], step_size: float, n_steps: int, prior, n_burnin: int,
+                      n_samples: int, thin: int = 1, group=None, halo_every: int | None = None):
+    """run_chain (sampler.py:291-358) of a time-sharded chain, every sweep on
+    the devices: the proposal protocol of _drive with the statistics of the
+    kept path, then the theta draws (sampler.py:339-344) on every shard from
+    the all-gathered statistics -- the same parameters on every shard.
+    `chains` are this process's shards (all of them, or one per rank with
+    `group`).  Returns (iters, params [n x 5], accept, delta_h) as
+    DeviceChain.run_chain_device; raises NativeError subclass StormError on a
+    divergence storm (with .sweep)."""
+    import torch
+    _cuda_shard_ptrs(chains)
+    pr = N.Prior(*(float(getattr(prior, f)) for f, _ in N.Prior._fields_))
+    for c in chains:
+        c.shard._ck(c.shard._lib.rsv_shard_run_begin(c.shard.ctx, float(step_size), ctypes.byref(pr), int(n_burnin),
+                                                       int(n_samples), int(thin)))
+    n_sweeps = n_burnin + n_samples * thin
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.Stream(dev)
+    comm = _LocalComm(chains) if group is None and len(chains) == chains[0].world else _NcclComm(chains[0], group)
+    err = None
+    with torch.cuda.stream(stream):
+        try:
+            _drive(chains, comm, step_size, n_steps, n_sweeps, False, True, halo_every, dev, stream, theta=True)
+        except N.NativeError as e:  # a storm stops the device loop; the run's end reports it
+            err = e
+    outs = []
+    for c in chains:
+        iters = np.empty(n_samples, dtype=np.int64)
+        par = np.empty((n_samples, 5))
+        acc = np.empty(n_samples, dtype=np.int32)
+        dh = np.empty(n_samples)
+        stored, storm = ctypes.c_int64(0), ctypes.c_int64(-1)
+        code = c.shard._lib.rsv_shard_run_end(c.shard.ctx, iters.ctypes.data, par.ctypes.data, acc.ctypes.data,
+                                              dh.ctypes.data, ctypes.byref(stored), ctypes.byref(storm))
+        try:
+            c.shard._ck(code)
+        except N.StormError as e:
+            e.sweep = int(storm.value)
+            raise
+        outs.append((iters, par, acc.astype(bool), dh))
+    if err is not None:
+        raise err
+    for o in outs[1:]:
+        if not (np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])):
+            raise RuntimeError("shards drew different parameters")
+    return outs[0]
