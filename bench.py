@@ -628,19 +628,25 @@ def main():
 def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
     """N > 1 (config 3): ONE chain of T sites time-sharded over the N GPUs
     (strong scaling), orchestrated on the device: per proposal each GPU
-    draws the (replicated) momenta, runs the trajectory on its sites plus an
-    8(L+1)-site margin, writes its 20 partial totals to device memory; NCCL
-    all-gathers them and every GPU takes the same Metropolis decision on the
-    device; the margins are exchanged (NCCL send/recv) every 7 proposals,
-    which keeps the owned sites exact whatever was accepted in between.  The
-    host only enqueues; timed with CUDA events bracketing the K proposals and
-    the final synchronisation (barrier before and after), max over ranks."""
+    parses only its window of the momenta stream (window records
+    all-gathered, normals placed bit for bit as the whole-series draw), runs
+    the trajectory on its sites plus an 8(L+1)-site margin, writes its
+    23-word record (fixed-point dH / H parts: the same dH bits as one GPU);
+    NCCL all-gathers the records and every GPU takes the same Metropolis
+    decision on the device; the margins are exchanged (NCCL send/recv) every
+    7 proposals, which keeps the owned sites exact whatever was accepted in
+    between.  The host only enqueues; timed with CUDA events per proposal
+    (max over ranks).  Beside it: e2e with host buffers, and config 5
+    (T=2^26, run_chain) sharded the same way."""
     T, L, dt = args.T, args.L, args.dt
     dev = f"cuda:{local}"
     margin = 8 * (L + 1)
     chain = P.ShardedChain(truth.dataset, theta, rank, ws, margin=margin, device=local)
     chain.set_latent_global(truth.latent)
     chain.set_stream(P.stream_state(P.make_rng(1, args.prng)))
+    windowed = args.prng != "sfc64"
+    if windowed:
+        chain.set_windowed_momenta(True)
     P.sharded.hmc_update_distributed_device(chain, dt, L, max(3, args.warmup))
     clocks = ClockSampler(local) if rank == 0 else None
     if clocks:
@@ -664,6 +670,38 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
     clk = clocks.stop() if clocks else None
+
+    # ---- e2e with host buffers: each step the rank's local slice of the path
+    # goes in from page-locked host memory, one proposal runs, the decision
+    # and the owned slice come back (wall clock, max over ranks)
+    ls, le, lo, hi = chain.ls, chain.le, chain.lo, chain.hi
+    h_host = torch.empty(T, dtype=torch.float64, pin_memory=True).numpy()
+    h_host[:] = truth.latent
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        chain.shard.set_latent(h_host[ls:le])
+        chain.halo_valid = True
+        P.sharded.hmc_update_distributed_device(chain, dt, L, 1)
+    dist.barrier()
+    n_acc = 0
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        chain.shard.set_latent(h_host[ls:le])
+        chain.halo_valid = True
+        r = P.sharded.hmc_update_distributed_device(chain, dt, L, 1)
+        if r[0].accept:
+            h_host[lo:hi] = chain.owned_latent()
+            n_acc += 1
+    dist.barrier()
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_s[0])
+
+    # ---- config 5 sharded: T = 2^26, full theta update per sweep, blocked sfc64
+    c5 = None
+    if not args.no_config5:
+        c5 = config5_sharded(args, P, theta, rank, ws, local, dist, torch)
+
     if rank == 0:
         v = T * L / (ms * 1e-3)
         acc = sum(bool(x.accept) for x in res) / max(1, len(res))
@@ -672,15 +710,53 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (simulate_rsv, theta of SURVEY \u00a78d, seed 0)",
                 "config": config_dict(T, L, dt, args.prng),
                 "parallelism": f"time-sharded x{ws} (margin {margin} sites, halo every "
-                               f"{P.sharded.halo_period(margin, L)} proposals, NCCL all_gather of shard "
-                               "totals, decision on the device)",
+                               f"{P.sharded.halo_period(margin, L)} proposals, "
+                               + ("windowed momenta (each GPU parses its window of the stream), " if windowed else
+                                  "replicated momenta (sfc64: no jump-ahead), ")
+                               + "NCCL all_gather of the shard records, decision on the device)",
                 "l2": "flushed before every proposal (256 MiB write per GPU, outside the event pairs)",
                 "trajectories_per_s": 1e3 / ms, "accept_rate": acc, "clocks": clk,
-                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                        "path": "ShardedChain + sharded.hmc_update_distributed_device (device-resident; results read "
-                                "once at the end)"},
+                "e2e": {"value": T * L / e2e_s, "unit": UNIT,
+                        "h2d_bytes_per_step": 8 * (le - ls),
+                        "d2h_bytes_per_step": int(8 * (hi - lo) * n_acc / e2e_steps) + 48,
+                        "path": "per rank: local path slice from pinned host memory -> ShardedChain -> "
+                                "sharded.hmc_update_distributed_device (one proposal) -> decision + owned slice "
+                                "back to host; wall clock, max over ranks; bytes are rank 0's"},
                 "gpu_launches": int(launches)}
+        if c5 is not None:
+            line["config5"] = c5
         print(json.dumps(line), flush=True)
+
+
+def config5_sharded(args, P, theta, rank, ws, local, dist, torch, block=4096, sweeps=30, dt=0.005):
+    """Config 5 across the N GPUs: T = 2^26, run_chain with the theta draws
+    on every GPU from the all-gathered statistics, sfc64 blocked momenta
+    (each GPU draws the blocks its sites touch).  Wall clock around the
+    sweeps (device-orchestrated; includes the samples' D2H), max over ranks."""
+    T = args.c5_T
+    truth = P.simulate_rsv(theta, T, seed=11, backend=P.CudaBackend(local))
+    margin = 8 * 21
+    ch = P.ShardedChain(truth.dataset, theta, rank, ws, margin=margin, device=local)
+    ch.set_latent_global(truth.latent)
+    ch.set_stream(P.stream_state(P.make_rng(1, "sfc64")))
+    ch.set_blocked_streams(1, block)
+    prior = P.PriorSpec()
+    P.sharded.run_chain_sharded([ch], dt, 20, prior, 0, 2, 1)
+    ch.set_params(theta)
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    t0 = time.perf_counter()
+    it, par, acc, dh = P.sharded.run_chain_sharded([ch], dt, 20, prior, 0, sweeps, 1)
+    torch.cuda.synchronize(local)
+    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    el = float(el[0])
+    ch.shard.close()
+    return {"workload": f"config 5 on {ws} GPUs: T={T}, L=20, dt={dt}, full theta update per sweep (on every GPU "
+                        f"from all-gathered statistics), sfc64 blocked momenta ({block}-site blocks), time-sharded",
+            "sweeps": sweeps, "sweeps_per_s": sweeps / el, "ms_per_sweep": el / sweeps * 1e3,
+            "site_updates_per_s": T * 20 * sweeps / el, "accept_rate": float(np.mean(acc)),
+            "timing": "wall clock around run_chain_sharded (device-orchestrated; samples' D2H), max over ranks"}
 
 
 if __name__ == "__main__":

@@ -369,6 +369,21 @@ class CudaBackend:
             return int(flag.value)
         raise NotImplementedError(f"CudaBackend cannot run kernel {name!r}")
 
+    # -- the proposal-level hook of INTEGRATION.md (level 2): a reference
+    # function that finds these methods on its backend forwards to them --
+    def hmc_update_volatility(self, h, params, data, md, rng):
+        """sampler.py:144-167 for the reference's own objects (duck-typed
+        Dataset / Params / MDConfig, a numpy Generator): one fused proposal."""
+        from .sampler import hmc_update_volatility
+        return hmc_update_volatility(h, params, data, md, rng, backend=self)
+
+    def integrate_trajectory(self, state, config, params, data, fuse_half_steps: bool = False):
+        """integrator.py:149-179 for the reference's objects; returns the
+        caller's PhaseState type."""
+        ps, diverged = integrate_trajectory(state, config, params, data, backend=self,
+                                            fuse_half_steps=fuse_half_steps)
+        return type(state)(ps.h, ps.p), diverged
+
     @staticmethod
     def _f64_arrays(*arrs):
         for a in arrs:
