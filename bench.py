@@ -37,11 +37,13 @@ METRIC = "HMC site-updates/sec (T x leapfrog steps/s)"
 UNIT = "site-updates/s"
 THETA = dict(phi=0.97, mu=-9.0, xi=-0.3, sigma_eta_sq=0.05, sigma_u_sq=0.1)
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
-# algorithmic FP64 work of one site-update in the trajectory kernel
-# (DESIGN.md 4.2): 2 drifts (2 FMA), kick (3 FMA + 2 ADD), exp(-d) (6 FMA +
-# 1 ADD + 1 MUL)  ->  11 FMA + 4 other = 26 flops in 15 FP64 instructions.
+# algorithmic FP64 work of one site-update of the leapfrog (DESIGN.md 4.2,
+# SURVEY 8d): 2 half drifts (2 FMA), the kick (3 FMA + 2 ADD) and e^{-d}
+# (a degree-3 polynomial after range reduction: 4 FMA-class + 3 ADD +
+# rounding) -- counted as 26 flops.  The kernel issues 14 FP64 instructions
+# per site-update for them (scaled-state exp: 3 DADD + 3 DFMA/DMUL + 1 DFMA).
 FLOPS_PER_SITE_UPDATE = 26
-FP64_INSTR_PER_SITE_UPDATE = 15  # DFMA-pipe instructions (FMA, ADD, MUL each one issue slot)
+FP64_INSTR_PER_SITE_UPDATE = 14  # DFMA-pipe instructions (FMA, ADD, MUL each one issue slot)
 HBM_BYTES_PER_SITE = 48  # streamed elementary step: r h,p,(y/2)y,lnRV; w h,p
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
@@ -491,9 +493,12 @@ def main():
     step_s = step_ms * 1e-3
     value = T * L / step_s
 
-    # ---------------- roofline of the dominant kernel (trajectory, FP64-bound)
+    # ---------------- roofline of the dominant kernel (trajectory, FP64-bound):
+    # its launch duration = CUDA events around 20 back-to-back launches of the
+    # proposal's trajectory kernel on the context's stream (bench_trajectory)
     fp64_peak = ch.fp64_peak_tflops()
-    achieved = FLOPS_PER_SITE_UPDATE * T * L / (traj_ms * 1e-3) / 1e12
+    traj_launch_ms = ch.bench_trajectory(dt, L, 20)
+    achieved = FLOPS_PER_SITE_UPDATE * T * L / (traj_launch_ms * 1e-3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traj_dram_bytes.json")
     if os.path.exists(tp):
@@ -609,7 +614,10 @@ def main():
             "bracket_ms_per_step_incl_flush": bracket_s * 1e3 / args.steps,
             "e2e": e2e,
             "gpu_launches": int(launches),
-            "roofline": {"kernel": "traj_kernel (fused L-step trajectory)", "bound": "fp64", "achieved": achieved,
+            "roofline": {"kernel": "traj_persistent_kernel (fused L-step trajectory)", "bound": "fp64",
+                         "achieved": achieved, "launch_ms": traj_launch_ms,
+                         "launch_timing": "CUDA events around 20 back-to-back launches on the context's stream "
+                                          "(integrate-only, the proposal's geometry; L2 warm as inside a proposal)",
                          "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
                          "flops_per_site_update": FLOPS_PER_SITE_UPDATE,
                          "peak_source": "measured live: DFMA microbenchmark (rsv_measure_fp64_peak)",

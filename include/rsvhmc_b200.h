@@ -136,6 +136,10 @@ int rsv_bench_elementary(rsv_ctx *ctx, double step_size, int n_steps, float *ms,
 /* The same n steps fused into one launch of the persistent trajectory kernel
  * (state as for rsv_bench_elementary; device time of the launch in *ms). */
 int rsv_bench_fused(rsv_ctx *ctx, double step_size, int n_steps, float *ms, int32_t *diverged);
+/* The proposal's trajectory kernel alone, n launches back to back between
+ * one CUDA event pair (integrate-only on the current path and momenta):
+ * the per-launch duration bench.py's roofline divides by. */
+int rsv_bench_trajectory(rsv_ctx *ctx, double step_size, int n_steps, int n, float *ms_per_launch);
 
 /* Kernel-level plug-in (integrator.py:50-65 backend.run protocol):
  * _kernels.py:37-41 position_update, :44-54 momentum_update,

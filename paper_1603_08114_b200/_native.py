@@ -86,6 +86,8 @@ _SIGS = {
     "rsv_bench_fused": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_float),
                                        ctypes.c_void_p]),
     "rsv_bench_state": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p]),
+    "rsv_bench_trajectory": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                            ctypes.POINTER(ctypes.c_float)]),
     "rsv_position_update": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_int64,
                                            ctypes.c_int64, ctypes.c_int64, ctypes.c_int]),
     "rsv_momentum_update": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,

@@ -1124,6 +1124,39 @@ int rsv_bench_fused(rsv_ctx *c, double dt, int n_steps, float *ms, int32_t *dive
   return 0;
 }
 
+// The trajectory kernel alone, n launches back to back on the context's
+// stream bracketed by one CUDA event pair (the roofline's launch duration,
+// bench.py): the proposal's own kernel configuration on the current path and
+// the last momenta, integrate-only (no Metropolis bookkeeping, no state
+// change; the proposal goes to scratch).  L2 as inside a proposal (warm).
+int rsv_bench_trajectory(rsv_ctx *c, double dt, int n_steps, int n, float *ms_per_launch) {
+  if (!c || !ms_per_launch || n < 1) return fail(c, RSV_E_INVALID, "bad argument");
+  int r;
+  if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
+  if (c->shard || c->ens_C) return fail(c, RSV_E_STATE, "rsv_bench_trajectory needs a single-chain context");
+  CK(cudaSetDevice(c->device));
+  const TrajGeom g = traj_geometry(c->T, n_steps, c->sm_count, c->variant);
+  if (!g.ok) return fail(c, RSV_E_INVALID, "n_steps=%d too large for one fused trajectory", n_steps);
+  TrajArgs a = traj_args(c, dt, n_steps, 0, g);
+  CK(cudaMemcpy(c->h_ctrl, c->ctrl, sizeof(DevControl), cudaMemcpyDeviceToHost));
+  a.h_src = c->hbuf[c->h_ctrl->cur];
+  a.h_dst = c->sh;
+  a.integrate_only = 1;
+  a.stats = 0;
+  if ((r = ensure_events(c, 2))) return r;
+  int l = 0;
+  LK(launch_trajectory(a, c->stream, &l));  // warm
+  CK(cudaEventRecord(c->evpool[0], c->stream));
+  for (int i = 0; i < n; i++) LK(launch_trajectory(a, c->stream, &l));
+  CK(cudaEventRecord(c->evpool[1], c->stream));
+  c->launches += l;
+  CK(cudaEventSynchronize(c->evpool[1]));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->evpool[0], c->evpool[1]));
+  *ms_per_launch = ms / n;
+  return sync(c);
+}
+
 static int ensure_plugin(rsv_ctx *c, int64_t n) {
   if (n <= c->pl_n) return 0;
   for (int i = 0; i < 4; i++) {

@@ -306,6 +306,12 @@ class DeviceChain:
     def launch_count(self) -> int:
         return int(self._lib.rsv_launch_count(self.ctx))
 
+    def bench_trajectory(self, step_size: float, n_steps: int, n: int = 20) -> float:
+        """Per-launch ms of the trajectory kernel alone (rsv_bench_trajectory)."""
+        ms = ctypes.c_float()
+        self._ck(self._lib.rsv_bench_trajectory(self.ctx, float(step_size), int(n_steps), int(n), ctypes.byref(ms)))
+        return float(ms.value)
+
 
 class CudaBackend:
     """Drop-in ``backend=`` for the reference API (integrator.py:50-105).
