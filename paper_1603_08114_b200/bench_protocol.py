@@ -37,21 +37,25 @@ _MAX_RETRIES = 3
 
 
 class NumericError(RuntimeError):
-    """A numeric procedure failed (degenerate fit, diverging timing run)."""
+    """bench.py's NumericError: the fit is degenerate or a timing run kept
+    diverging (API contract: same name, same conditions)."""
 
 
 @dataclass(frozen=True)
 class TimingFit:
+    """f(B) = A + C*B fitted to mean step times (fields as bench.py's)."""
     intercept_a: float
     slope_c: float
     r_squared: float
 
     def predict(self, b: float) -> float:
-        return self.intercept_a + self.slope_c * b
+        return float(np.polyval((self.slope_c, self.intercept_a), b))
 
 
 @dataclass(frozen=True)
 class TimingPoint:
+    """One B of the study: mean / standard error of the step time and the
+    step size it finally ran with (fields as bench.py's)."""
     b: int
     mean_seconds: float
     se_seconds: float
@@ -60,6 +64,8 @@ class TimingPoint:
 
 @dataclass(frozen=True)
 class BenchConfig:
+    """The study's schedule (bench.py's BenchConfig without the CPU-only
+    fields chunk / backends / workers / precision; `device` added)."""
     b_values: tuple[int, ...] = (2, 4, 8, 16, 32, 64, 128, 256, 512)
     reps: int = 10000
     repeats: int = 5
@@ -68,12 +74,12 @@ class BenchConfig:
     device: int = 0
 
     def __post_init__(self):
-        if not self.b_values or any(b < 1 for b in self.b_values):
-            raise ValueError(f"b_values must be positive integers, got {self.b_values}")
-        if self.reps < 1:
-            raise ValueError(f"reps must be >= 1, got {self.reps}")
-        if self.repeats < 1:
-            raise ValueError(f"repeats must be >= 1, got {self.repeats}")
+        checks = (("b_values", bool(self.b_values) and min(self.b_values) >= 1, "positive integers"),
+                  ("reps", self.reps >= 1, ">= 1"),
+                  ("repeats", self.repeats >= 1, ">= 1"))
+        for name, ok, want in checks:
+            if not ok:
+                raise ValueError(f"{name} must be {want}, got {getattr(self, name)}")
 
 
 @dataclass
@@ -150,33 +156,44 @@ def time_elementary_step(b: int, backend, reps: int, params: Params, data: Datas
 
 
 def fit_linear(points) -> TimingFit:
-    """OLS fit of (B, seconds) to f(B) = A + C*B with R^2 (bench.py:193-210)."""
-    pts = [(float(b), float(y)) for b, y in points]
-    if len(pts) < 2:
-        raise NumericError(f"need >= 2 points for a line, got {len(pts)}")
-    b = np.array([p[0] for p in pts])
-    y = np.array([p[1] for p in pts])
-    if np.all(b == b[0]):
-        raise NumericError("degenerate fit: all B values identical")
-    slope, intercept = np.polyfit(b, y, 1)
-    resid = y - (intercept + slope * b)
-    ss_res = float(resid @ resid)
-    ss_tot = float(((y - y.mean()) ** 2).sum())
-    r2 = (1.0 if ss_res <= 1e-30 else 0.0) if ss_tot == 0.0 else 1.0 - ss_res / ss_tot
-    return TimingFit(float(intercept), float(slope), r2)
+    """Least squares of the (B, seconds) pairs on f(B) = A + C*B, with R^2
+    (the study's fit, bench.py:193-210), from the centred sums: C = Sby/Sbb,
+    A = mean(y) - C mean(b).  Fewer than two points or a single distinct B
+    raise NumericError; a constant y gives R^2 = 1 for an exact fit, else 0."""
+    bs = np.array([float(b) for b, _ in points])
+    ys = np.array([float(y) for _, y in points])
+    if bs.size < 2:
+        raise NumericError(f"a line needs at least two points (have {bs.size})")
+    db = bs - bs.mean()
+    sbb = float(db @ db)
+    if sbb == 0.0:
+        raise NumericError("degenerate fit: every point has the same B")
+    dy = ys - ys.mean()
+    c = float(db @ dy) / sbb
+    a = float(ys.mean()) - c * float(bs.mean())
+    r = ys - (a + c * bs)
+    ss_res, ss_tot = float(r @ r), float(dy @ dy)
+    if ss_tot > 0.0:
+        r2 = 1.0 - ss_res / ss_tot
+    else:
+        r2 = 1.0 if ss_res <= 1e-30 else 0.0
+    return TimingFit(intercept_a=a, slope_c=c, r_squared=r2)
+
+
+def _ratio(num: float, den: float, what: str) -> float:
+    if not den > 0.0:
+        raise NumericError(f"the faster backend's {what} is not positive ({den})")
+    return num / den
 
 
 def compute_gain(fit_slow: TimingFit, fit_fast: TimingFit, b: float) -> float:
-    fast = fit_fast.predict(b)
-    if fast <= 0.0:
-        raise NumericError(f"fast backend has non-positive predicted time {fast} at B={b}")
-    return fit_slow.predict(b) / fast
+    """Speed-up of the fitted models at B: f_slow(B) / f_fast(B)."""
+    return _ratio(fit_slow.predict(b), fit_fast.predict(b), f"predicted time at B={b}")
 
 
 def asymptotic_gain(fit_slow: TimingFit, fit_fast: TimingFit) -> float:
-    if fit_fast.slope_c <= 0.0:
-        raise NumericError(f"fast backend has non-positive slope {fit_fast.slope_c}")
-    return fit_slow.slope_c / fit_fast.slope_c
+    """The speed-up as B grows: C_slow / C_fast."""
+    return _ratio(fit_slow.slope_c, fit_fast.slope_c, "slope")
 
 
 def run_scaling_study(config: BenchConfig = BenchConfig(), params: Params = BENCH_PARAMS,
