@@ -7,16 +7,17 @@
 //   sampler.py:155-167 (dH, divergence sentinel, Metropolis),
 //   the sums inside sampler.py:170-272 (theta sufficient statistics).
 //
-// traj_kernel: one CTA owns a tile of `core` consecutive sites plus a halo
-// of n_steps + 1 sites on each side; each thread keeps 8 consecutive sites
-// (d = h - mu, p, and the per-site force constants) in registers for the
-// whole trajectory.  Neighbour values move by warp shuffles and, across
-// warps, through shared memory with one barrier per step.  Because the
+// traj_persistent_kernel: a persistent grid (2 CTAs per SM) walks tiles of
+// `core` consecutive sites, each with a halo of n_steps + 1 sites on either
+// side; each thread keeps R = 4 consecutive sites (x = K (h - mu), p, and
+// the per-site force constants) in registers for the whole trajectory.
+// Neighbour values move by warp shuffles and, across warps, through
+// ghost lanes refreshed via shared memory every R steps.  Because the
 // stencil is nearest-neighbour, L steps on a tile with an L-site halo give
 // the core sites exactly the values a global step-by-step sweep gives, so
 // the whole trajectory is one launch with no grid-wide synchronisation.
-// HBM traffic per trajectory is ~40 B/site, the FP64 pipe is the bound
-// ("Roofline").
+// HBM traffic per trajectory is 32 B/site (h, p, (y/2)y, lnRV in; h' out);
+// the FP64 pipe is the bound.
 #include <math.h>
 
 #include "exp_table.h"
