@@ -12,7 +12,10 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librsvhmc_b200.so")
+# RSV_LIB=checked selects the build with device-side invariant checks
+# (make -C paper_1603_08114_b200/csrc checked; tools/checked_run.sh)
+LIB_PATH = os.path.join(_HERE, "librsvhmc_b200_checked.so" if os.environ.get("RSV_LIB") == "checked"
+                        else "librsvhmc_b200.so")
 
 RSV_E_INVALID = -1
 RSV_E_CUDA = -2

@@ -21,6 +21,7 @@
 #include <math.h>
 
 #include "exp_table.h"
+#include "rsv_check.h"
 #include "rsv_internal.h"
 #include "rsv_launch.h"
 
@@ -385,6 +386,9 @@ __device__ __forceinline__ void stage_tile(const TrajArgs &A, const double *hsrc
   const int64_t lo = g < 0 ? 0 : g, hi = min(g + W, A.Tpad);
   const uint32_t bytes = (uint32_t)((hi - lo) * 8);
   const int off = (int)(lo - g);
+  RSV_CHECK(tile >= 0 && tile < A.g.n_tiles && lo < hi && off >= 0 && off + (hi - lo) <= W);
+  RSV_CHECK(bytes % 16 == 0 && off % 2 == 0 && lo % 2 == 0);
+  RSV_CHECK((((uintptr_t)(hsrc + lo)) & 15) == 0 && (((uintptr_t)(A.p_in + lo)) & 15) == 0);
   mbar_expect_tx(bar, (part == 3 ? 4 : part == 1 ? 3 : 1) * bytes);
   if (part & 1) {
     tma_load_1d(stage + 0 * W + off, hsrc + lo, bytes, bar);
@@ -403,6 +407,7 @@ __device__ __forceinline__ void stage_tile_ens(const TrajArgs &A, int tile, doub
   const int64_t lo = g < 0 ? 0 : g, hi = min(g + W, A.Tpad);
   const uint32_t bytes = (uint32_t)((hi - lo) * 8);
   const int off = (int)(lo - g);
+  RSV_CHECK(tile >= 0 && tile < A.g.n_tiles && lo < hi && off >= 0 && off + (hi - lo) <= W && bytes % 16 == 0);
   mbar_expect_tx(bar, 4 * bytes);
   for (int64_t x = lo; x < hi;) {
     const int64_t c = x / A.Tc;
@@ -509,6 +514,9 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   const bool own_lane = (lane >= 1 && lane <= 30) || (lane == 0 && warp == 0) || (lane == 31 && warp == NW - 1);
   const int lw = warp * WSTEP + lane * R;  // my first site inside the window
   const GhostSlots gs = ghost_lanes<R, NT>(S.gx, lane, warp);
+  RSV_CHECK(lw >= 0 && lw + R <= W && lw % 2 == 0);
+  RSV_CHECK((!gs.w || (gs.w >= S.gx && gs.w + 2 * R <= S.gx + NW * 4 * R)) &&
+            (!gs.r || (gs.r >= S.gx && gs.r + 2 * R <= S.gx + NW * 4 * R)));
   // Interior tiles (window inside the local range, core fully owned, no
   // global end site and no chain boundary in the window) need no per-site
   // masks: every window site is live (sites past the halo only ever feed
@@ -697,7 +705,11 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     }
     const double hnew = vnew[0] + kinetic<R>(p, core);
     double *hd = hdst;
-    if (ENS && core) hd = A.ens_cur[chain] ? A.hbuf0 : A.hbuf1;
+    if (ENS && core) {
+      RSV_CHECK(chain >= 0 && chain < A.n_chains);
+      hd = A.ens_cur[chain] ? A.hbuf0 : A.hbuf1;
+    }
+    RSV_CHECK(!wcore || (g0 >= 0 && g0 + R <= A.Tpad));
     if (wcore == (1u << R) - 1) {
 #pragma unroll
       for (int r = 0; r < R; r += 2) {

@@ -28,6 +28,7 @@
 
 #include "rsv_internal.h"
 #include "rsv_launch.h"
+#include "rsv_check.h"
 
 namespace rsv {
 
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
 
   // ---- my 8 raw words, generated into registers
   const int64_t k_t = (int64_t)B * ZB - ZG + (int64_t)tid * ZW;  // draw word of my chunk's first word
+  RSV_CHECK(b >= 0 && b < (int)gridDim.x && B >= 0);
   const bool valid = k_t >= 0;                                    // CTA 0 has no guard words
   uint64_t w[ZW];
   uint64_t base = 0;  // pcg: LCG state before output 2*k_t; minstd: x_{3 k_t}
@@ -474,6 +476,7 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
           x = __dmul_rn(fr, S.wi[idx]);
           if (r & 1) x = -x;
         }
+        RSV_CHECK(o >= 0 && o < ZB);
         S.xout[ZXS(o)] = x;
         o++;
       }
@@ -625,6 +628,7 @@ __global__ void __launch_bounds__(ZT, 4) zig_kernel(DevControl *ctrl, const uint
   // the draw's last (index T-1) records where the draw ended in the stream
   const uint64_t boff = S.blk_off;
   if (wmode) {
+    RSV_CHECK(boff + (uint64_t)btot <= (uint64_t)win.cap);
     for (int j = tid; j < btot; j += ZT) {
       if (boff + (uint64_t)j < (uint64_t)win.cap) win.out[boff + j] = S.xout[ZXS(j)];
     }

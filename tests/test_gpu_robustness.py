@@ -8,6 +8,7 @@ import math
 import numpy as np
 import pytest
 
+import oracle as O
 import paper_1603_08114_b200 as P
 from conftest import TRUE
 
@@ -97,3 +98,52 @@ def test_data_edits_reach_the_device(backend):
     assert lp0 != lp1 and lp1 != lp2
     ref = P.log_posterior(tr.latent, THETA, P.Dataset(returns=y, rv=data.rv), backend=backend)
     assert lp2 == ref
+
+
+# ---------------------------------------------------------------- inter-CTA protocols under contention
+@pytest.mark.parametrize("T", [300007, 1 << 20, 3000017])
+def test_momenta_exact_while_other_kernels_hold_the_sms(backend, T):
+    """The momenta draw's look-back (decoupled, by scheduling ticket) must
+    make progress and stay bit-exact when its grid cannot be co-resident
+    because other kernels occupy the SMs (long matmuls on another stream are
+    launched right before every draw).  compute-sanitizer is closed on this
+    pool; this and the checked build (tools/checked_run.sh) exercise the
+    protocols instead."""
+    import torch
+    side = torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.float64)
+    for kind in ("pcg32", "philox"):
+        st = O.Stream(kind, T + 1)
+        want = st.normals(T)
+        rng = P.make_rng(T + 1, kind)
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                a = (a @ a) * 1e-3
+        got = P.refresh_momenta(rng, T, backend=backend)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), kind
+
+
+def test_trajectory_tiles_exact_while_other_kernels_hold_the_sms(backend):
+    """Dynamic tile scheduling and the fixed-point totals under contention:
+    proposals with a concurrent FP64 matmul equal the oracle's."""
+    import torch
+    T, L, n = 1 << 18, 20, 4
+    truth = P.simulate_rsv(THETA, T, seed=21)
+    y, lrv = truth.dataset.returns, truth.dataset.log_rv
+    ch = backend.chain(truth.dataset, THETA)
+    ch.set_latent(truth.latent)
+    ch.set_stream(P.stream_state(P.make_rng(3, "pcg32")))
+    side = torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.float64)
+    st = O.Stream("pcg32", 3)
+    h = truth.latent.copy()
+    H = abs(O.hamiltonian(h, np.zeros(T), THETA, y, lrv)) + T
+    for i in range(n):
+        with torch.cuda.stream(side):
+            a = (a @ a) * 1e-3
+        r = ch.hmc_update(0.02, L)
+        h, acc, dh = O.hmc_update(h, THETA, y, lrv, 0.02, L, st, nthreads=O.max_threads())
+        assert bool(r.accept) == acc and abs(r.delta_h - dh) <= 1e-13 * H, i
+    torch.cuda.synchronize()
+    assert np.max(np.abs(ch.get_latent() - h)) <= 1e-12 * np.max(np.abs(h))
