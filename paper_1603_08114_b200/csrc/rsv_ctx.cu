@@ -779,11 +779,6 @@ int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv
   if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
   if (n < 1) return fail(c, RSV_E_INVALID, "n must be >= 1");
   CK(cudaSetDevice(c->device));
-  rsv_ctx::Cached *cg = nullptr;
-  int kpl = 0;
-  // HMC-only proposals (the reference's hmc_update_volatility): no theta statistics
-  if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl))) return r;
-  cudaGraphExec_t exec = cg->exec;
   if (out && n > c->ring_cap) {
     if (c->ring) cudaFree(c->ring);
     if (c->h_ring) cudaFreeHost(c->h_ring);
@@ -793,6 +788,11 @@ int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv
   }
   CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
   CK(cudaMemsetAsync(c->ring_count, 0, sizeof(int32_t), c->stream));
+  rsv_ctx::Cached *cg = nullptr;
+  int kpl = 0;
+  // HMC-only proposals (the reference's hmc_update_volatility): no theta statistics
+  if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl))) return r;
+  cudaGraphExec_t exec = cg->exec;
   // timing 1: one event pair per proposal on the stream around the graph
   // launch (the L2 flush stays outside); timing 2: the graph's own four
   // event-record nodes give the momenta / trajectory breakdown as well
@@ -845,10 +845,10 @@ int rsv_hmc_update(rsv_ctx *c, double dt, int n_steps, int fuse, rsv_result *out
   int r;
   if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
   CK(cudaSetDevice(c->device));
+  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
   rsv_ctx::Cached *cg = nullptr;
   int kpl = 0;
   if ((r = get_graph(c, dt, n_steps, fuse, 1, &cg, &kpl))) return r;
-  CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
   CK(cudaGraphLaunch(cg->exec, c->stream));
   c->launches += kpl;
   if ((r = pull_ctrl(c))) return r;

@@ -1,0 +1,262 @@
+// theta_dev.cuh -- numpy's ziggurat tables and the theta draws of one Gibbs
+// sweep (sampler.py:170-272, run_chain :339-344) as device code of the theta
+// kernel (momenta.cu), callable by any one-thread consumer:
+// numpy's normal / uniform / Marsaglia-Tsang gamma restated on the raw-word
+// stream (ThetaGen), the five full conditionals from the 7 moments of the
+// kept path, the storm guard and the sample store.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#include "prng.cuh"
+#include "rsv_internal.h"
+#include "rsv_launch.h"
+
+namespace rsv {
+
+static __device__ const uint64_t g_ki[256] = RSV_KI_DOUBLE_INIT;
+static __device__ const double g_wi[256] = RSV_WI_DOUBLE_INIT;
+static __device__ const double g_fi[256] = RSV_FI_DOUBLE_INIT;
+
+// glibc log1p as one out-of-line copy: the exponential-tail path of the
+// ziggurat is rare, so its code is cold in the instruction cache (after an L2
+// flush it comes from DRAM); one shared copy halves those fetches.
+static __device__ __noinline__ double log1p_ool(double x) { return glibc_log1p(x); }
+static __device__ __noinline__ double log_ool(double x) { return log(x); }
+static __device__ __noinline__ double exp_ool(double x) { return exp(x); }
+
+struct ThetaGen {
+  int kind;
+  SeqGen g;
+  uint64_t s[4];
+  uint64_t used;
+  const uint64_t *ki;  // ziggurat tables (shared-memory copies)
+  const double *wi, *fi;
+  __device__ __noinline__ uint64_t next() {
+    used++;
+    return kind == PRNG_SFC64 ? sfc64_next(s) : g.next();
+  }
+  __device__ double next_double() { return u01(next()); }
+  __device__ __noinline__ double normal() {  // numpy random_standard_normal
+    for (;;) {
+      uint64_t r = next();
+      const int idx = (int)(r & 0xff);
+      r >>= 8;
+      const int sign = (int)(r & 0x1);
+      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+      double x = __dmul_rn((double)rabs, wi[idx]);
+      if (sign) x = -x;
+      if (rabs < ki[idx]) return x;
+      if (idx == 0) {
+        for (;;) {
+          const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R, log1p_ool(-next_double()));
+          const double yy = -log1p_ool(-next_double());
+          if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx))
+            return ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
+        }
+      }
+      const double u = next_double();
+      if (__dadd_rn(__dmul_rn(__dsub_rn(fi[idx - 1], fi[idx]), u), fi[idx]) <
+          exp_ool(__dmul_rn(__dmul_rn(-0.5, x), x)))
+        return x;
+    }
+  }
+  __device__ __noinline__ double gamma(double shape) {  // numpy random_standard_gamma, shape > 1
+    const double b = __dsub_rn(shape, 1.0 / 3.0);
+    const double c = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(9.0, b)));
+    for (;;) {
+      double X, V;
+      do {
+        X = normal();
+        V = __dadd_rn(1.0, __dmul_rn(c, X));
+      } while (V <= 0.0);
+      V = __dmul_rn(__dmul_rn(V, V), V);
+      const double U = next_double();
+      const double X2 = __dmul_rn(X, X);
+      if (U < __dsub_rn(1.0, __dmul_rn(__dmul_rn(0.0331, X2), X2))) return __dmul_rn(b, V);
+      if (log_ool(U) < __dadd_rn(__dmul_rn(0.5, X2), __dmul_rn(b, __dadd_rn(__dsub_rn(1.0, V), log_ool(V)))))
+        return __dmul_rn(b, V);
+    }
+  }
+};
+
+// _recentre (sampler.py mirror): moments of d' = h - mu from d = h - c
+struct Recentred {
+  double d0n, sxx, sall, sxz;
+};
+static __device__ Recentred recentre(const double *st, double Td, double c, double mu) {
+  const double delta = __dsub_rn(mu, c);
+  const double d0 = st[0], dl = st[1], s1 = st[2], s2 = st[3], sx = st[4];
+  const double Tm1 = Td - 1.0;
+  Recentred r;
+  r.d0n = __dsub_rn(d0, delta);
+  r.sxx = __dadd_rn(__dsub_rn(__dsub_rn(s2, __dmul_rn(dl, dl)), __dmul_rn(__dmul_rn(2.0, delta), __dsub_rn(s1, dl))),
+                    __dmul_rn(__dmul_rn(Tm1, delta), delta));
+  r.sall = __dadd_rn(__dsub_rn(s2, __dmul_rn(__dmul_rn(2.0, delta), s1)), __dmul_rn(__dmul_rn(Td, delta), delta));
+  r.sxz = __dadd_rn(__dsub_rn(sx, __dmul_rn(delta, __dadd_rn(__dsub_rn(s1, d0), __dsub_rn(s1, dl)))),
+                    __dmul_rn(__dmul_rn(Tm1, delta), delta));
+  return r;
+}
+
+static __device__ double phi_log_ratio(double prop, double phi, double h1_sq, double se2, const DevPrior &pr) {
+  const double a = __dmul_rn(0.5, __dsub_rn(log1p_ool(-__dmul_rn(prop, prop)), log1p_ool(-__dmul_rn(phi, phi))));
+  const double b = __ddiv_rn(__dmul_rn(h1_sq, __dsub_rn(__dsub_rn(1.0, __dmul_rn(prop, prop)),
+                                                        __dsub_rn(1.0, __dmul_rn(phi, phi)))),
+                             __dmul_rn(2.0, se2));
+  const double c = __dmul_rn(__dsub_rn(pr.phi_a, 1.0), __dsub_rn(log1p_ool(prop), log1p_ool(phi)));
+  const double d = __dmul_rn(__dsub_rn(pr.phi_b, 1.0), __dsub_rn(log1p_ool(-prop), log1p_ool(-phi)));
+  return __dadd_rn(__dadd_rn(__dsub_rn(a, b), c), d);
+}
+
+
+// One sweep's theta draws, run by one thread after the proposal (C->res,
+// C->stats hold its result and the kept path's statistics): storm guard,
+// mu, phi, sigma_eta^2, xi, sigma_u^2 in the reference's order on the same
+// raw words, new DevParams / TrajConsts, and the sample store.  ki / wi / fi:
+// the ziggurat tables (shared-memory copies).
+static __device__ __noinline__ void theta_sweep_body(DevControl *C, DevParams *P, TrajConsts *K, DevRun *R,
+                                                     const DevPrior &pr, double dt, int64_t T, const uint64_t *ki,
+                                                     const double *wi, const double *fi) {
+  if (C->halt) return;  // the run stopped at an earlier sweep
+  const DevResult res = C->res;
+  // storm guard (sampler.py:329-337), checked on the proposal just made; the
+  // reference raises before any theta draw, so the run stops right here
+  {
+    const int div = res.diverged ? 1 : 0;
+    if (R->ring_n == RUN_STORM_WINDOW) R->ring_div -= R->ring[R->ring_pos];
+    else R->ring_n++;
+    R->ring[R->ring_pos] = (uint8_t)div;
+    R->ring_div += div;
+    R->ring_pos = (R->ring_pos + 1) % RUN_STORM_WINDOW;
+    if (R->ring_n == RUN_STORM_WINDOW && R->ring_div > RUN_STORM_LIMIT && R->storm_sweep < 0) {
+      R->storm_sweep = R->sweep;
+      C->halt = 1;
+      return;
+    }
+  }
+  ThetaGen G;
+  G.kind = C->stream.kind;
+  G.used = 0;
+  G.ki = ki;
+  G.wi = wi;
+  G.fi = fi;
+  if (G.kind == PRNG_SFC64) {
+    for (int k = 0; k < 4; k++) G.s[k] = C->stream.s[k];
+  } else if (G.kind == PRNG_PHILOX) {
+    G.g.init(C->stream, C->stream.pos);
+  } else {  // pcg32 / minstd: the sequential state at the position is kept by the Metropolis step
+    G.g.kind = G.kind;
+    G.g.k = C->stream.pos;
+    G.g.a = C->seq_state;
+    G.g.b = C->stream.s[1];
+  }
+  double st[7];
+  for (int k = 0; k < 7; k++) st[k] = C->stats[k];
+  const double Td = (double)T, Tm1 = Td - 1.0;
+  double phi = P->phi, mu = P->mu, xi = P->xi, se2 = P->se2, su2 = P->su2;
+  const double c_mu = mu, c_xi = xi;
+  bool degenerate = false;
+  // update_mu (sampler.py:170-188)
+  {
+    const double omp = __dsub_rn(1.0, phi);
+    const double prec = __dadd_rn(
+        __ddiv_rn(__dadd_rn(__dsub_rn(1.0, __dmul_rn(phi, phi)), __dmul_rn(Tm1, __dmul_rn(omp, omp))), se2),
+        __ddiv_rn(1.0, pr.mu_var));
+    const double d0 = st[0], dl = st[1], s1 = st[2];
+    const double h0 = __dadd_rn(d0, c_mu);
+    const double trans = __dadd_rn(__dsub_rn(__dsub_rn(s1, d0), __dmul_rn(phi, __dsub_rn(s1, dl))),
+                                   __dmul_rn(__dmul_rn(Tm1, omp), c_mu));
+    const double num = __dadd_rn(__dadd_rn(__ddiv_rn(__dmul_rn(__dsub_rn(1.0, __dmul_rn(phi, phi)), h0), se2),
+                                           __ddiv_rn(__dmul_rn(omp, trans), se2)),
+                                 __ddiv_rn(pr.mu_mean, pr.mu_var));
+    if (!(isfinite(prec) && prec > 0.0)) {
+      degenerate = true;
+    } else {
+      const double sd = __dsqrt_rn(__ddiv_rn(1.0, prec));
+      mu = __dadd_rn(__ddiv_rn(num, prec), __dmul_rn(sd, G.normal()));
+    }
+  }
+  // update_phi (sampler.py:249-272)
+  if (!degenerate) {
+    const Recentred r = recentre(st, Td, c_mu, mu);
+    const double sxx = r.sxx > 1e-300 ? r.sxx : 1e-300;
+    const double phi_hat = __ddiv_rn(r.sxz, sxx);
+    const double sd = __dsqrt_rn(__ddiv_rn(se2, sxx));
+    const double prop = __dadd_rn(phi_hat, __dmul_rn(sd, G.normal()));
+    if (-1.0 < prop && prop < 1.0) {
+      const double lr = phi_log_ratio(prop, phi, __dmul_rn(r.d0n, r.d0n), se2, pr);
+      const double u = G.next_double();
+      if (lr >= 0.0 || u < exp_ool(lr)) phi = prop;
+    }
+  }
+  // update_sigma_eta_sq (sampler.py:218-230)
+  if (!degenerate) {
+    const Recentred r = recentre(st, Td, c_mu, mu);
+    const double tail_sq = __dsub_rn(r.sall, __dmul_rn(r.d0n, r.d0n));
+    const double q = __dadd_rn(
+        __dmul_rn(__dmul_rn(__dsub_rn(1.0, __dmul_rn(phi, phi)), r.d0n), r.d0n),
+        __dadd_rn(__dsub_rn(tail_sq, __dmul_rn(__dmul_rn(2.0, phi), r.sxz)), __dmul_rn(__dmul_rn(phi, phi), r.sxx)));
+    const double shape = __dadd_rn(pr.var_shape, __dmul_rn(0.5, Td));
+    const double scale = __dadd_rn(pr.var_scale, __dmul_rn(0.5, q));
+    se2 = __ddiv_rn(scale, G.gamma(shape));
+  }
+  // update_xi (sampler.py:191-202)
+  if (!degenerate) {
+    const double sum_r = __dadd_rn(st[5], __dmul_rn(Td, c_xi));
+    const double prec = __dadd_rn(__ddiv_rn(Td, su2), __ddiv_rn(1.0, pr.xi_var));
+    const double num = __dadd_rn(__ddiv_rn(sum_r, su2), __ddiv_rn(pr.xi_mean, pr.xi_var));
+    if (!(isfinite(prec) && prec > 0.0)) {
+      degenerate = true;
+    } else {
+      const double sd = __dsqrt_rn(__ddiv_rn(1.0, prec));
+      xi = __dadd_rn(__ddiv_rn(num, prec), __dmul_rn(sd, G.normal()));
+    }
+  }
+  // update_sigma_u_sq (sampler.py:209-215)
+  if (!degenerate) {
+    const double delta = __dsub_rn(xi, c_xi);
+    const double ss = __dadd_rn(__dsub_rn(st[6], __dmul_rn(__dmul_rn(2.0, delta), st[5])),
+                                __dmul_rn(__dmul_rn(Td, delta), delta));
+    const double shape = __dadd_rn(pr.var_shape, __dmul_rn(0.5, Td));
+    const double scale = __dadd_rn(pr.var_scale, __dmul_rn(0.5, ss));
+    su2 = __ddiv_rn(scale, G.gamma(shape));
+  }
+  // the stream continues after the draws (those made before a degenerate
+  // precision included: the reference raises after them, sampler.py:186,200)
+  C->stream.pos += G.used;
+  if (G.kind == PRNG_SFC64)
+    for (int k = 0; k < 4; k++) C->stream.s[k] = G.s[k];
+  else if (G.kind == PRNG_PCG32 || G.kind == PRNG_MINSTD)
+    C->seq_state = G.g.a;
+  if (degenerate) {  // ValueError in the reference: parameters unchanged, nothing stored
+    R->degenerate = 1;
+    C->halt = 1;
+    return;
+  }
+  // new parameters and the constants derived from them (rsv_set_params)
+  DevParams q = *P;
+  q.phi = phi; q.mu = mu; q.xi = xi; q.se2 = se2; q.su2 = su2;
+  q.inv_su2 = 1.0 / su2;
+  q.inv_se2 = 1.0 / se2;
+  q.emu = exp_ool(-mu);
+  q.one_m_phi2 = 1.0 - phi * phi;
+  q.hconst = 0.5 * Td * mu + 0.5 * Td * log_ool(su2) + 0.5 * log_ool(se2 / (1.0 - phi * phi)) +
+             0.5 * Tm1 * log_ool(se2);
+  q.n_lo = (int32_t)floor((mu - 50.0) * RSV_INV_LN2_N);
+  q.n_span = (int32_t)ceil((mu + 50.0) * RSV_INV_LN2_N) - q.n_lo;
+  *P = q;
+  *K = traj_consts(q, dt);
+  // store (sampler.py:346-354)
+  const int64_t sw = R->sweep;
+  if (sw >= R->n_burnin && (sw - R->n_burnin) % R->thin == 0 && R->stored < R->n_store) {
+    const int64_t i = R->stored++;
+    double *o = R->params + 5 * i;
+    o[0] = phi; o[1] = mu; o[2] = xi; o[3] = se2; o[4] = su2;
+    R->accept[i] = res.accept;
+    R->delta_h[i] = res.diverged ? __longlong_as_double(0x7ff0000000000000LL) : res.delta_h;
+    R->iters[i] = sw;
+  }
+  R->sweep = sw + 1;
+}
+
+}  // namespace rsv
