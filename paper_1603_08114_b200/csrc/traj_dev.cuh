@@ -73,9 +73,9 @@ __device__ __forceinline__ bool out_of_range(double t, int n_lo, int n_span) {
 // Variable potential part of H at one site (the theta-only constants are
 // added in the Metropolis step): 0.5 d + a e^{-mu} e^{-d} + (q-d)^2/2su2 + AR.
 // Every operation is an explicit round-to-nearest intrinsic: the compiler's
-// FMA contraction would otherwise depend on the surrounding code, and the
-// tiled and the resident kernels must form the same per-group energies bit
-// for bit (their fixed-point sums are compared exactly).
+// FMA contraction would otherwise depend on the surrounding code, and every
+// kernel variant (shapes, statistics, shards) must form the same per-group
+// energies bit for bit (their fixed-point sums are compared exactly).
 __device__ __forceinline__ double site_potential(double d, double dprev, double ae, double q, bool first,
                                                  const TrajConsts &s, const unsigned long long *tab) {
   double t;
