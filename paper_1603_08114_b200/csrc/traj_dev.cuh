@@ -105,14 +105,14 @@ __device__ __forceinline__ void tile_energy(const double (&d)[R], const double (
     const bool first = (firstm >> r) & 1;
     const double en = site_potential(d[r], dprev, __dmul_rn(s.emu, av[r]), q, first, s, tab);
     const bool c = (core >> r) & 1;
-    v[0] = c ? __dadd_rn(v[0], en) : v[0];
+    v[0] = __dadd_rn(v[0], c ? en : 0.0);
     if (STATS) {
       const double e = __dsub_rn(q, d[r]);
-      v[1] = c ? __dadd_rn(v[1], d[r]) : v[1];
-      v[2] = c ? __fma_rn(d[r], d[r], v[2]) : v[2];
-      v[3] = (c && !first) ? __fma_rn(d[r], dprev, v[3]) : v[3];
-      v[4] = c ? __dadd_rn(v[4], e) : v[4];
-      v[5] = c ? __fma_rn(e, e, v[5]) : v[5];
+      v[1] = __dadd_rn(v[1], c ? d[r] : 0.0);
+      v[2] = __dadd_rn(v[2], c ? __dmul_rn(d[r], d[r]) : 0.0);
+      v[3] = __dadd_rn(v[3], (c && !first) ? __dmul_rn(d[r], dprev) : 0.0);
+      v[4] = __dadd_rn(v[4], c ? e : 0.0);
+      v[5] = __dadd_rn(v[5], c ? __dmul_rn(e, e) : 0.0);
     }
   }
 }
@@ -120,7 +120,7 @@ template <int R>
 __device__ __forceinline__ double kinetic(const double (&p)[R], uint32_t core) {
   double k = 0.0;
 #pragma unroll
-  for (int r = 0; r < R; r++) k = ((core >> r) & 1) ? __fma_rn(__dmul_rn(0.5, p[r]), p[r], k) : k;
+  for (int r = 0; r < R; r++) k = __dadd_rn(k, ((core >> r) & 1) ? __dmul_rn(__dmul_rn(0.5, p[r]), p[r]) : 0.0);
   return k;
 }
 
