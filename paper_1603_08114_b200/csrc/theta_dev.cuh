@@ -117,43 +117,60 @@ static __device__ double phi_log_ratio(double prop, double phi, double h1_sq, do
 static __device__ __noinline__ void theta_sweep_body(DevControl *C, DevParams *P, TrajConsts *K, DevRun *R,
                                                      const DevPrior &pr, double dt, int64_t T, const uint64_t *ki,
                                                      const double *wi, const double *fi) {
-  if (C->halt) return;  // the run stopped at an earlier sweep
+  // every input in one round of independent loads (one thread: each load
+  // issued on its own would cost a full memory latency on the critical path)
+  const int halt = C->halt;
   const DevResult res = C->res;
+  const StreamState ss = C->stream;
+  const uint64_t seq0 = C->seq_state;
+  double st[7];
+#pragma unroll
+  for (int k = 0; k < 7; k++) st[k] = C->stats[k];
+  const DevParams P0 = *P;
+  const int32_t ring_n = R->ring_n, ring_pos = R->ring_pos, ring_div0 = R->ring_div;
+  const int64_t storm0 = R->storm_sweep, sweep0 = R->sweep;
+  const int64_t n_burnin = R->n_burnin, thin = R->thin, n_store = R->n_store, stored0 = R->stored;
+  double *const r_params = R->params, *const r_dh = R->delta_h;
+  int32_t *const r_acc = R->accept;
+  int64_t *const r_it = R->iters;
+  const uint8_t ring_old = R->ring[ring_pos];
+  if (halt) return;  // the run stopped at an earlier sweep
   // storm guard (sampler.py:329-337), checked on the proposal just made; the
   // reference raises before any theta draw, so the run stops right here
   {
     const int div = res.diverged ? 1 : 0;
-    if (R->ring_n == RUN_STORM_WINDOW) R->ring_div -= R->ring[R->ring_pos];
-    else R->ring_n++;
-    R->ring[R->ring_pos] = (uint8_t)div;
-    R->ring_div += div;
-    R->ring_pos = (R->ring_pos + 1) % RUN_STORM_WINDOW;
-    if (R->ring_n == RUN_STORM_WINDOW && R->ring_div > RUN_STORM_LIMIT && R->storm_sweep < 0) {
-      R->storm_sweep = R->sweep;
+    int rn = ring_n, rd = ring_div0;
+    if (rn == RUN_STORM_WINDOW) rd -= ring_old;
+    else rn++;
+    rd += div;
+    R->ring[ring_pos] = (uint8_t)div;
+    R->ring_n = rn;
+    R->ring_div = rd;
+    R->ring_pos = (ring_pos + 1) % RUN_STORM_WINDOW;
+    if (rn == RUN_STORM_WINDOW && rd > RUN_STORM_LIMIT && storm0 < 0) {
+      R->storm_sweep = sweep0;
       C->halt = 1;
       return;
     }
   }
   ThetaGen G;
-  G.kind = C->stream.kind;
+  G.kind = ss.kind;
   G.used = 0;
   G.ki = ki;
   G.wi = wi;
   G.fi = fi;
   if (G.kind == PRNG_SFC64) {
-    for (int k = 0; k < 4; k++) G.s[k] = C->stream.s[k];
+    for (int k = 0; k < 4; k++) G.s[k] = ss.s[k];
   } else if (G.kind == PRNG_PHILOX) {
-    G.g.init(C->stream, C->stream.pos);
+    G.g.init(ss, ss.pos);
   } else {  // pcg32 / minstd: the sequential state at the position is kept by the Metropolis step
     G.g.kind = G.kind;
-    G.g.k = C->stream.pos;
-    G.g.a = C->seq_state;
-    G.g.b = C->stream.s[1];
+    G.g.k = ss.pos;
+    G.g.a = seq0;
+    G.g.b = ss.s[1];
   }
-  double st[7];
-  for (int k = 0; k < 7; k++) st[k] = C->stats[k];
   const double Td = (double)T, Tm1 = Td - 1.0;
-  double phi = P->phi, mu = P->mu, xi = P->xi, se2 = P->se2, su2 = P->su2;
+  double phi = P0.phi, mu = P0.mu, xi = P0.xi, se2 = P0.se2, su2 = P0.su2;
   const double c_mu = mu, c_xi = xi;
   bool degenerate = false;
   // update_mu (sampler.py:170-188)
@@ -223,7 +240,7 @@ static __device__ __noinline__ void theta_sweep_body(DevControl *C, DevParams *P
   }
   // the stream continues after the draws (those made before a degenerate
   // precision included: the reference raises after them, sampler.py:186,200)
-  C->stream.pos += G.used;
+  C->stream.pos = ss.pos + G.used;
   if (G.kind == PRNG_SFC64)
     for (int k = 0; k < 4; k++) C->stream.s[k] = G.s[k];
   else if (G.kind == PRNG_PCG32 || G.kind == PRNG_MINSTD)
@@ -234,7 +251,7 @@ static __device__ __noinline__ void theta_sweep_body(DevControl *C, DevParams *P
     return;
   }
   // new parameters and the constants derived from them (rsv_set_params)
-  DevParams q = *P;
+  DevParams q = P0;
   q.phi = phi; q.mu = mu; q.xi = xi; q.se2 = se2; q.su2 = su2;
   q.inv_su2 = 1.0 / su2;
   q.inv_se2 = 1.0 / se2;
@@ -247,14 +264,15 @@ static __device__ __noinline__ void theta_sweep_body(DevControl *C, DevParams *P
   *P = q;
   *K = traj_consts(q, dt);
   // store (sampler.py:346-354)
-  const int64_t sw = R->sweep;
-  if (sw >= R->n_burnin && (sw - R->n_burnin) % R->thin == 0 && R->stored < R->n_store) {
-    const int64_t i = R->stored++;
-    double *o = R->params + 5 * i;
+  const int64_t sw = sweep0;
+  if (sw >= n_burnin && (sw - n_burnin) % thin == 0 && stored0 < n_store) {
+    const int64_t i = stored0;
+    R->stored = stored0 + 1;
+    double *o = r_params + 5 * i;
     o[0] = phi; o[1] = mu; o[2] = xi; o[3] = se2; o[4] = su2;
-    R->accept[i] = res.accept;
-    R->delta_h[i] = res.diverged ? __longlong_as_double(0x7ff0000000000000LL) : res.delta_h;
-    R->iters[i] = sw;
+    r_acc[i] = res.accept;
+    r_dh[i] = res.diverged ? __longlong_as_double(0x7ff0000000000000LL) : res.delta_h;
+    r_it[i] = sw;
   }
   R->sweep = sw + 1;
 }
