@@ -661,7 +661,7 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
         clocks.start()
     t_load = time.perf_counter()
     while time.perf_counter() - t_load < 0.4:
-        P.sharded.hmc_update_distributed_device(chain, dt, L, 20)
+        P.sharded.hmc_update_distributed_device(chain, dt, L, 21, graph=True)
     # L2 flushed before every proposal (a 256 MiB write, not timed), one event
     # pair per proposal around it on the proposal stream (as at N=1)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -669,11 +669,11 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
     torch.cuda.synchronize(local)
     n0 = chain.shard.launch_count()
     times = []
-    res = P.sharded.hmc_update_distributed_device(chain, dt, L, args.steps, l2_flush=flush, times=times)
+    res = P.sharded.hmc_update_distributed_device(chain, dt, L, args.steps, l2_flush=flush, times=times, graph=True)
     torch.cuda.synchronize(local)
     launches = chain.shard.launch_count() - n0
     dist.barrier()
-    ms = sum(a.elapsed_time(b) for a, b in times) / len(times)
+    ms = sum(times) / len(times)
     t = torch.tensor([ms], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])

@@ -191,6 +191,10 @@ int rsv_get_timing(rsv_ctx *ctx, double *traj_ms, double *momenta_ms, double *to
 int rsv_set_stream(rsv_ctx *ctx, void *cuda_stream);
 int rsv_shard_propose_async(rsv_ctx *ctx, double step_size, int n_steps, int fuse, int stats, double *totals_dev);
 int rsv_shard_decide_async(rsv_ctx *ctx, const double *gathered_dev, int world);
+/* builds the cached proposal graph ahead (before a caller-side stream capture
+ * of the per-proposal sequence; inside a capture rsv_shard_propose_async
+ * enqueues that graph's kernels directly) */
+int rsv_shard_prepare(rsv_ctx *ctx, double step_size, int n_steps, int fuse, int stats);
 int rsv_shard_halo_async(rsv_ctx *ctx, double *left, int64_t n_left, double *right, int64_t n_right, int unpack);
 int rsv_shard_results(rsv_ctx *ctx, rsv_result *out, int max_n, int *n_out);
 

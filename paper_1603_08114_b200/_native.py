@@ -122,6 +122,7 @@ _SIGS = {
                                                ctypes.c_void_p]),
     "rsv_shard_decide_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int]),
     "rsv_shard_set_momenta": (ctypes.c_int, [_CTX, ctypes.c_int]),
+    "rsv_shard_prepare": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "rsv_shard_momenta_async": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
     "rsv_shard_place_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
     "rsv_shard_set_blocked_streams": (ctypes.c_int, [_CTX, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,

@@ -1572,12 +1572,47 @@ int rsv_shard_propose_async(rsv_ctx *c, double dt, int n_steps, int fuse, int st
   rsv_ctx::Cached *cg = nullptr;
   int kpl = 0;
   if ((r = get_graph(c, dt, n_steps, fuse, stats, &cg, &kpl))) return r;
-  CK(cudaGraphLaunch(cg->exec, c->stream));
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(c->stream, &cs));
+  if (cs == cudaStreamCaptureStatusActive) {
+    // inside the caller's stream capture (the sharded driver records whole
+    // halo periods as one CUDA graph): the cached graph's kernels directly
+    int l = 0;
+    bool ok = true;
+    if (!(c->win_mode && !c->blocks)) ok &= launch_momenta(mbufs(c), c->kind, c->Tg, c->stream, &l) == 0;
+    if (cg->args.g.ok) ok &= launch_trajectory(cg->args, c->stream, &l) == 0;
+    else return fail(c, RSV_E_STATE, "n_steps=%d too large for a sharded trajectory", n_steps);
+    if (!ok) return fail(c, RSV_E_CUDA, "captured proposal launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  } else {
+    CK(cudaGraphLaunch(cg->exec, c->stream));
+  }
   const int own_first = c->goff + c->own_lo == 0, own_last = c->goff + c->own_hi == c->Tg;
   shard_pack_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, own_first, own_last, reinterpret_cast<ShardRec *>(totals_dev));
   c->launches += kpl + 1;
   CK(cudaGetLastError());
   return 0;
+}
+
+// Build (and cache) the proposal graph of rsv_shard_propose_async ahead of
+// time, e.g. before the caller records its own stream capture.
+int rsv_shard_prepare(rsv_ctx *c, double dt, int n_steps, int fuse, int stats) {
+  if (!c) return fail(c, RSV_E_INVALID, "null context");
+  if (!c->shard) return fail(c, RSV_E_STATE, "not a shard context (rsv_create_shard)");
+  int r;
+  if ((r = check_md(c, dt, n_steps)) || (r = ready(c))) return r;
+  CK(cudaSetDevice(c->device));
+  rsv_ctx::Cached *cg = nullptr;
+  int kpl = 0;
+  if ((r = get_graph(c, dt, n_steps, fuse, stats, &cg, &kpl))) return r;
+  if (!c->ring || c->ring_cap < 1024) {  // the decision ring (rsv_shard_decide_async), outside any capture
+    if (c->ring) cudaFree(c->ring);
+    if (c->h_ring) cudaFreeHost(c->h_ring);
+    c->ring_cap = 1024;
+    CK(cudaMalloc(&c->ring, sizeof(DevResult) * c->ring_cap));
+    CK(cudaMallocHost(&c->h_ring, sizeof(DevResult) * c->ring_cap));
+    CK(cudaMemsetAsync(c->ring_count, 0, sizeof(int32_t), c->stream));
+  }
+  return sync(c);
 }
 
 int rsv_shard_decide_async(rsv_ctx *c, const double *gathered_dev, int world) {

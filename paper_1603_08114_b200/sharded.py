@@ -459,14 +459,16 @@ class _NcclComm:
 
 
 def _drive(chains, comm, step_size, n_steps, n, fuse, stats, halo_every, dev, stream, l2_flush=None, times=None,
-           theta=False):
+           theta=False, graph=False):
     """n proposals (or sweeps with theta=True) of the chain whose shards
     `chains` live in this process, every step enqueued on `stream`:
     [margins every K proposals] -> [windowed momenta: window parse,
     all-gather of the window records, placement] -> trajectory + this
     shard's record -> all-gather of the records -> the same decision on
     every shard -> [theta draws].  The host synchronises only to read the
-    result ring."""
+    result ring.  graph=True records one halo period (K proposals, with the
+    collectives) as a CUDA graph and replays it: one host launch per K
+    proposals instead of ~15 library calls per proposal."""
     import torch
     world = comm.world
     c0 = chains[0]
@@ -487,45 +489,96 @@ def _drive(chains, comm, step_size, n_steps, n, fuse, stats, halo_every, dev, st
         sends.append((torch.empty(c.halo_sizes(r - 1)[1] if r > 0 else 0, **f64),
                       torch.empty(c.halo_sizes(r + 1)[0] if r < world - 1 else 0, **f64)))
         recvs.append((torch.empty(nl_recv if r > 0 else 0, **f64), torch.empty(nr_recv if r < world - 1 else 0, **f64)))
-    out = [[] for _ in chains]
-    try:
-        for i in range(n):
-            if l2_flush is not None:
-                l2_flush.fill_(i & 0xff)
-            if times is not None:
-                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                ev[0].record(stream)
-            if world > 1 and (i % K == 0 or not all(c.halo_valid for c in chains)):
-                for c, (sl, sr) in zip(chains, sends):
-                    c.shard._ck(lib.rsv_shard_halo_async(c.shard.ctx, sl.data_ptr(), sl.numel(), sr.data_ptr(),
-                                                         sr.numel(), 0))
-                comm.halo(chains, sends, recvs)
-                for c, (fl, fr) in zip(chains, recvs):
-                    c.shard._ck(lib.rsv_shard_halo_async(c.shard.ctx, fl.data_ptr(), fl.numel(), fr.data_ptr(),
-                                                         fr.numel(), 1))
-                    c.halo_valid = True
-            if windowed:
-                for c, w in zip(chains, win_mine):
-                    c.shard._ck(lib.rsv_shard_momenta_async(c.shard.ctx, w.data_ptr()))
-                comm.gather(win_all, win_mine)
-                for c in chains:
-                    c.shard._ck(lib.rsv_shard_place_async(c.shard.ctx, win_all.data_ptr(), world, c.rank))
-            for c, m in zip(chains, rec_mine):
-                c.shard._ck(lib.rsv_shard_propose_async(c.shard.ctx, float(step_size), int(n_steps), int(bool(fuse)),
-                                                        int(bool(stats or theta)), m.data_ptr()))
-            comm.gather(rec_all, rec_mine)
+
+    def halo():
+        for c, (sl, sr) in zip(chains, sends):
+            c.shard._ck(lib.rsv_shard_halo_async(c.shard.ctx, sl.data_ptr(), sl.numel(), sr.data_ptr(), sr.numel(), 0))
+        comm.halo(chains, sends, recvs)
+        for c, (fl, fr) in zip(chains, recvs):
+            c.shard._ck(lib.rsv_shard_halo_async(c.shard.ctx, fl.data_ptr(), fl.numel(), fr.data_ptr(),
+                                                 fr.numel(), 1))
+            c.halo_valid = True
+
+    def proposal(i, ev=None):
+        if l2_flush is not None:
+            l2_flush.fill_(i & 0xff)
+        if ev is not None:
+            ev[0].record(stream)
+        if world > 1 and (i % K == 0 or not all(c.halo_valid for c in chains)):
+            halo()
+        if windowed:
+            for c, w in zip(chains, win_mine):
+                c.shard._ck(lib.rsv_shard_momenta_async(c.shard.ctx, w.data_ptr()))
+            comm.gather(win_all, win_mine)
             for c in chains:
-                c.shard._ck(lib.rsv_shard_decide_async(c.shard.ctx, rec_all.data_ptr(), world))
-                if theta:
-                    c.shard._ck(lib.rsv_shard_theta_async(c.shard.ctx))
-            if times is not None:
-                ev[1].record(stream)
-                times.append(ev)
-            if (i + 1) % _RING == 0:  # the device result ring holds _RING records
-                for c, acc in zip(chains, out):
-                    acc.extend(_results(c, _RING))
+                c.shard._ck(lib.rsv_shard_place_async(c.shard.ctx, win_all.data_ptr(), world, c.rank))
+        for c, m in zip(chains, rec_mine):
+            c.shard._ck(lib.rsv_shard_propose_async(c.shard.ctx, float(step_size), int(n_steps), int(bool(fuse)),
+                                                    int(bool(stats or theta)), m.data_ptr()))
+        comm.gather(rec_all, rec_mine)
+        for c in chains:
+            c.shard._ck(lib.rsv_shard_decide_async(c.shard.ctx, rec_all.data_ptr(), world))
+            if theta:
+                c.shard._ck(lib.rsv_shard_theta_async(c.shard.ctx))
+        if ev is not None:
+            ev[1].record(stream)
+
+    def events(external=False):  # external: recorded as event nodes when captured in a graph
+        return (torch.cuda.Event(enable_timing=True, external=external),
+                torch.cuda.Event(enable_timing=True, external=external))
+
+    out = [[] for _ in chains]
+
+    def drain(k):
         for c, acc in zip(chains, out):
-            acc.extend(_results(c, n % _RING))
+            acc.extend(_results(c, k))
+
+    direct = []  # event pairs of the proposals enqueued one by one
+    try:
+        i = 0
+        pending = 0
+        if graph and n >= 2 * K:
+            # align to a halo period, then replay captured periods
+            while i % K:
+                ev = events() if times is not None else None
+                proposal(i, ev)
+                if ev is not None:
+                    direct.append(ev)
+                i += 1
+                pending += 1
+            for c in chains:
+                c.halo_valid = False  # the captured period starts with an exchange
+                c.shard._ck(lib.rsv_shard_prepare(c.shard.ctx, float(step_size), int(n_steps), int(bool(fuse)),
+                                                  int(bool(stats or theta))))
+            g = torch.cuda.CUDAGraph()
+            evs = [events(True) for _ in range(K)] if times is not None else [None] * K
+            with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+                for j in range(K):
+                    proposal(j, evs[j])
+            while n - i >= K:
+                if pending + K > _RING:
+                    drain(pending)
+                    pending = 0
+                g.replay()
+                i += K
+                pending += K
+                if times is not None:  # the captured events are re-recorded by the next replay
+                    stream.synchronize()
+                    times.extend(a.elapsed_time(b) for a, b in evs)
+        while i < n:
+            ev = events() if times is not None else None
+            proposal(i, ev)
+            if ev is not None:
+                direct.append(ev)
+            i += 1
+            pending += 1
+            if pending == _RING:
+                drain(pending)
+                pending = 0
+        drain(pending)
+        if times is not None:
+            stream.synchronize()
+            times.extend(a.elapsed_time(b) for a, b in direct)
     finally:
         for c in chains:
             lib.rsv_set_stream(c.shard.ctx, None)
@@ -536,7 +589,8 @@ def _drive(chains, comm, step_size, n_steps, n, fuse, stats, halo_every, dev, st
 
 
 def hmc_update_local_device(chains: list[ShardedChain], step_size: float, n_steps: int, n: int,
-                            fuse: bool = False, stats: bool = False, halo_every: int | None = None):
+                            fuse: bool = False, stats: bool = False, halo_every: int | None = None,
+                            graph: bool = False):
     """n proposals of a chain whose shards all live in this process (one
     GPU), orchestrated on the device: no host synchronisation until the
     results are read back.  Returns the per-proposal rsv_result records."""
@@ -545,26 +599,28 @@ def hmc_update_local_device(chains: list[ShardedChain], step_size: float, n_step
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.Stream(dev)  # one ordered stream for every shard and every buffer
     with torch.cuda.stream(stream):
-        return _drive(chains, _LocalComm(chains), step_size, n_steps, n, fuse, stats, halo_every, dev, stream)
+        return _drive(chains, _LocalComm(chains), step_size, n_steps, n, fuse, stats, halo_every, dev, stream,
+                      graph=graph)
 
 
 def hmc_update_distributed_device(chain: ShardedChain, step_size: float, n_steps: int, n: int, fuse: bool = False,
                                   stats: bool = False, group=None, halo_every: int | None = None,
-                                  l2_flush=None, times: list | None = None):
+                                  l2_flush=None, times: list | None = None, graph: bool = False):
     """n proposals of a sharded chain over a torch.distributed (NCCL) group,
     orchestrated on the device: window records and shard records
     all-gathered on the GPU, decisions on the GPU, periodic halo exchange;
     the host synchronises once at the end.  Benchmarking: `l2_flush` (a
     device tensor larger than L2) is overwritten before every proposal, and
-    `times` collects one (start, end) CUDA event pair per proposal, recorded
-    after the flush and after the decision."""
+    `times` collects each proposal's milliseconds between a CUDA event
+    pair recorded after the flush and after the decision.  graph=True
+    replays captured halo periods (see _drive)."""
     import torch
     _cuda_shard_ptrs([chain])
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.Stream(dev)  # the kernels and the NCCL collectives share one ordered stream
     with torch.cuda.stream(stream):
         return _drive([chain], _NcclComm(chain, group), step_size, n_steps, n, fuse, stats, halo_every, dev, stream,
-                      l2_flush, times)
+                      l2_flush, times, graph=graph)
 
 
 def run_chain_sharded(chains: list[ShardedChain], step_size: float, n_steps: int, prior, n_burnin: int,

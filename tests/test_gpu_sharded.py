@@ -133,3 +133,30 @@ def test_sharded_run_chain_matches_single_context(backend, world, kind, windowed
         assert all(int(c.get_stream().pos) == int(single.get_stream().pos) for c in shards)
     finally:
         _close(shards)
+
+
+@pytest.mark.parametrize("windowed", [True, False])
+def test_captured_halo_periods_equal_single_context(backend, windowed):
+    """graph=True: whole halo periods (halo exchange, windowed momenta,
+    trajectories, records, gathers, decisions) recorded as one CUDA graph and
+    replayed -- the same bits as the single context."""
+    T, L, n, world = 40000, 12, 23, 3
+    truth = P.simulate_rsv(THETA, T, seed=37)
+    data = truth.dataset
+    margin = 4 * (L + 1)  # halo period 3
+    st0 = P.stream_state(P.make_rng(17, "pcg32"))
+    shards = _shards(data, world, margin, st0, truth.latent, windowed=windowed)
+    single = backend.chain(data, THETA)
+    single.set_latent(truth.latent)
+    single.set_stream(st0)
+    try:
+        res = S.hmc_update_local_device(shards, 0.02, L, n, graph=True)
+        ref = single.hmc_update_many(0.02, L, n)
+        assert len(res) == n
+        assert [bool(x.accept) for x in res] == [bool(x.accept) for x in ref]
+        assert [x.delta_h for x in res] == [x.delta_h for x in ref]
+        h = np.concatenate([c.owned_latent() for c in shards])
+        assert np.array_equal(h, single.get_latent())
+        assert all(int(c.get_stream().pos) == int(single.get_stream().pos) for c in shards)
+    finally:
+        _close(shards)
