@@ -809,38 +809,75 @@ __device__ void zig_serial_window(DevControl *ctrl, const ZigWin &win, int64_t n
 
 // ---- ensemble: one numpy SFC64 stream per chain ------------------------------
 // SFC64 has no jump-ahead, so a chain's raw words are inherently sequential.
-// A CTA serves 31 chains: warp 0 generates (lane j runs chain j's SFC64 two
-// 64-word chunks ahead into a shared-memory ring), warp j+1 parses chain j's
-// chunks (lanes = words: one table compare per word, a ballot walk over the
-// few multi-word attempts, coalesced stores of the normals).  A round costs
-// one chunk's generation (~15 cycles per word, the sequential floor) since
-// every parse warp has a single chain.
+// A CTA (16 warps) serves 29 chains with a pipeline over 64-word chunks, one
+// CTA barrier per round.  The stages are placed so that the generator does
+// not share its scheduler's issue slots (scheduler = warp id % 4).  In round r:
+//   * warp 0 generates chunk r+2: lane j runs chain j's SFC64 into a 4-chunk
+//     shared-memory ring and snapshots the state before each chunk.  The
+//     generator is the critical path (64 sequential steps of 64-bit integer
+//     work per lane and round), so it has scheduler 0 to itself;
+//   * warps 1, 2, 9, 10 classify chunk r+1 (lane = chain; a quarter each):
+//     one table compare per word gives the chunk's fast-path mask, the value
+//     the word's attempt yields on the fast path (or the wedge) is staged, and
+//     the few non-fast words (~1 %) go to the chunk's queue;
+//   * warp 6 evaluates chunk r's queue (lane = queued word): the attempt a
+//     non-fast word would start -- wedge: one more word and exp; exponential
+//     tail: pairs of words and glibc log1p, up to ZE_MMAX loops into the next
+//     chunk -- its length, whether it yields a normal, and a tail's value;
+//   * warp 5 walks chunk r-1 (lane = chain): the attempts between two
+//     non-fast starts are single-word normals, so the walk only stops at the
+//     evaluated non-fast starts; it marks the attempts that yield normals and
+//     finds where the chain's draw ends;
+//   * warps 3, 7, 11, 13, 14, 15 emit chunk r-2 (lanes = words, two chains at
+//     a time): each marked attempt's staged value goes to its place, coalesced.
+// (Round 1 had one parse warp per chain with lanes = words; the generator
+// shared its scheduler with five of them and every word was classified by a
+// whole-warp pass: ~190 us for 4096 x 4096 against ~125 us now.)
 // The draw is numpy's random_standard_normal on SFC64(SeedSequence([seed,
 // c])) exactly; the stream states after the draw's words and after the
 // Metropolis uniform are both kept for the trajectory kernel's decision.
-// 32 warps: warp 0 generates, warps 4 and 8 (the generator's scheduler, warp
-// id % 4 == 0) stay idle so the generator gets more of its scheduler's issue
-// slots, the other 29 warps parse one chain each
-constexpr int ZE_G = 29;      // chains per CTA (one parse warp each; 4096 chains = 142 CTAs, one wave)
+constexpr int ZE_G = 29;      // chains per CTA (4096 chains = 142 CTAs, one wave)
 constexpr int ZE_CH = 64;     // words per chunk
 constexpr int ZE_RING = 256;  // ring words per chain (4 chunks)
-constexpr int ZE_RS = ZE_RING + 1;  // padded row: generator lanes hit distinct banks
-constexpr int ZE_NT = 1024;
-__device__ __forceinline__ int ze_chain_of_warp(int warp) {  // -1: generator or idle warp
-  return (warp == 0 || warp == 4 || warp == 8) ? -1 : warp - 1 - (warp > 4) - (warp > 8);
-}
+constexpr int ZE_RS = ZE_RING + 1;  // padded rows: lanes of a chain-parallel access hit distinct banks
+constexpr int ZE_XS = ZE_CH + 1;
+constexpr int ZE_NT = 512;
+constexpr int ZE_NE = 6;      // emitting warps
+constexpr int ZE_QMAX = 512;  // queued non-fast words per chunk (expected ~20)
 constexpr int ZE_MMAX = 30;   // tail loops resolvable inside the ring window
+__device__ __forceinline__ int ze_emitter(int warp) {  // emitter index, -1: another role
+  return (warp & 3) == 3 ? warp >> 2 : warp == 13 ? 4 : warp == 14 ? 5 : -1;
+}
+__device__ __forceinline__ int ze_classifier(int warp) {  // quarter of a chunk, -1: another role
+  return warp == 1 ? 0 : warp == 2 ? 1 : warp == 9 ? 2 : warp == 10 ? 3 : -1;
+}
+__device__ __forceinline__ uint64_t ze_low(int n) { return n >= 64 ? ~0ull : ((1ull << n) - 1); }
+
+// cycle counter that memory operations are not moved across (stamps only)
+__device__ __forceinline__ long long ze_clk() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+  return t;
+}
 
 struct ZEnsShared {
   uint64_t ring[ZE_G * ZE_RS];
-  uint64_t snap[ZE_G][4][4];   // generator state before each chunk (by chunk & 3)
-  uint64_t ki[256];
+  uint64_t snap[ZE_G][4][4];     // generator state before each chunk (by chunk & 3)
+  ulonglong2 kw[256];            // (ki, wi bits): one 16-byte lookup per classified word
   double wi[256], fi[256];
-  int32_t n0[ZE_G], carry[ZE_G], done[ZE_G];
-  int32_t ndone;
+  double xs[4][ZE_G][ZE_XS];     // by chunk & 3: the value an attempt at each word yields
+  uint64_t vis[2][ZE_G];         // by chunk & 1: attempt starts that yield a normal
+  uint16_t fast[4][ZE_G][4];     // fast-path words
+  uint32_t eacc[4][ZE_G][2];     // non-fast words whose attempt yields a normal
+  int8_t elen[4][ZE_G][ZE_CH];   // ... their attempt's length in words (0: beyond the window)
+  uint16_t qe[4][ZE_QMAX];       // queued non-fast words: chain << 6 | word
+  int32_t qn[4];
+  int32_t n0e[2][ZE_G], wr[2][ZE_G];  // by chunk & 1: normals before the chunk, the chunk walked
+  int32_t n0[ZE_G], carry[ZE_G], done[ZE_G], ovf[ZE_G];
+  int32_t ndone, last_round;
 };
 
-__global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *normals, int64_t Tc, int C,
+__global__ void __launch_bounds__(ZE_NT, 1) zig_ens_kernel(EnsChain *E, double *normals, int64_t Tc, int C,
                                                          unsigned long long *dbg, int advance, const int32_t *halt) {
   if (halt && *halt) return;  // blocked momenta of a stopped rsv_run_chain: streams untouched
   extern __shared__ __align__(16) unsigned char zesmem[];
@@ -849,7 +886,7 @@ __global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *nor
   const int c0 = blockIdx.x * ZE_G;
   const int nch = min(ZE_G, C - c0);
   for (int i = tid; i < 256; i += ZE_NT) {
-    S.ki[i] = g_ki[i];
+    S.kw[i] = make_ulonglong2(g_ki[i], (unsigned long long)__double_as_longlong(g_wi[i]));
     S.wi[i] = g_wi[i];
     S.fi[i] = g_fi[i];
   }
@@ -857,8 +894,14 @@ __global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *nor
     S.n0[tid] = 0;
     S.carry[tid] = 0;
     S.done[tid] = tid >= nch;
+    S.ovf[tid] = 0;
+    S.wr[0][tid] = S.wr[1][tid] = -1;
   }
-  if (tid == 0) S.ndone = ZE_G - nch;
+  if (tid < 4) S.qn[tid] = 0;
+  if (tid == 0) {
+    S.ndone = ZE_G - nch;
+    S.last_round = -2;
+  }
   // generator state (warp 0, lane j = chain c0 + j)
   uint64_t g[4] = {0, 0, 0, 0};
   const bool gen = warp == 0 && lane < nch;
@@ -871,139 +914,225 @@ __global__ void __launch_bounds__(ZE_NT) zig_ens_kernel(EnsChain *E, double *nor
 #pragma unroll 8
     for (int k = 0; k < ZE_CH; k++) row[o + k] = sfc64_next(g);
   };
+  // quarter h of chunk m (lane = chain): fast-path mask and values, the other words queued
+  auto classify = [&](int m, int h) {
+    if (lane >= nch || S.done[lane]) return;
+    // words in, values computed, values out: no staging store between two
+    // words' loads (the compiler cannot tell the ring, the tables and the
+    // staging area apart, and would serialise every word)
+    const uint64_t *row = S.ring + lane * ZE_RS + ((m * ZE_CH + h * 16) & (ZE_RING - 1));
+    uint64_t wv[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) wv[k] = row[k];
+    double xv[16];
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      uint64_t w = wv[k];
+      const int idx = (int)(w & 0xff);
+      w >>= 8;
+      const uint64_t rabs = (w >> 1) & 0x000fffffffffffffULL;
+      const double fr =
+          __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | rabs)), 4503599627370496.0);
+      const ulonglong2 kw = S.kw[idx];
+      const double x = __dmul_rn(fr, __longlong_as_double((long long)kw.y));
+      xv[k] = (w & 1) ? -x : x;
+      bits |= (uint32_t)(rabs < kw.x) << k;
+    }
+    double *xr = S.xs[m & 3][lane] + h * 16;
+#pragma unroll
+    for (int k = 0; k < 16; k++) xr[k] = xv[k];
+    S.fast[m & 3][lane][h] = (uint16_t)bits;
+    if (h < 2) S.eacc[m & 3][lane][h] = 0;
+    for (uint32_t sl = ~bits & 0xffffu; sl; sl &= sl - 1) {
+      const int e = atomicAdd(&S.qn[m & 3], 1);
+      if (e < ZE_QMAX) S.qe[m & 3][e] = (uint16_t)((lane << 6) | (h * 16 + __ffs(sl) - 1));
+      else S.ovf[lane] = 1;  // never in practice: the draw is flagged (the proposal is rejected)
+    }
+  };
+  // the attempts the queued words of chunk m would start (lane = queued word)
+  auto evaluate = [&](int m) {
+    const int n = min(S.qn[m & 3], ZE_QMAX);
+    const int64_t base = (int64_t)m * ZE_CH;
+    for (int e = lane; e < n; e += 32) {
+      const int jq = S.qe[m & 3][e], j = jq >> 6, q = jq & 63;
+      const uint64_t *row = S.ring + j * ZE_RS;
+      uint64_t w = row[(base + q) & (ZE_RING - 1)];
+      const int idx = (int)(w & 0xff);
+      w >>= 8;
+      const uint64_t rabs = (w >> 1) & 0x000fffffffffffffULL;
+      int L = 0;
+      bool acc = false;
+      if (idx == 0) {  // exponential tail
+        for (int mm = 1; mm <= ZE_MMAX; mm++) {
+          const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R,
+                                      glibc_log1p(-u01(row[(base + q + 2 * mm - 1) & (ZE_RING - 1)])));
+          const double yy = -glibc_log1p(-u01(row[(base + q + 2 * mm) & (ZE_RING - 1)]));
+          if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+            S.xs[m & 3][j][q] = ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
+            L = 1 + 2 * mm;
+            acc = true;
+            break;
+          }
+        }
+      } else {  // wedge (the staged value stands)
+        const double fr =
+            __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | rabs)), 4503599627370496.0);
+        const double x = __dmul_rn(fr, S.wi[idx]);
+        const double u = u01(row[(base + q + 1) & (ZE_RING - 1)]);
+        const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(S.fi[idx - 1], S.fi[idx]), u), S.fi[idx]);
+        acc = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x));
+        L = 2;
+      }
+      S.elen[m & 3][j][q] = (int8_t)L;
+      if (acc) atomicOr(&S.eacc[m & 3][j][q >> 5], 1u << (q & 31));
+    }
+  };
+  // the attempt chain through chunk m (lane = chain)
+  auto walk = [&](int m, int r) {
+    const int j = lane;
+    if (j >= nch || S.done[j]) return;
+    const uint64_t fm = *reinterpret_cast<const uint64_t *>(S.fast[m & 3][j]);
+    const uint64_t ea = (uint64_t)S.eacc[m & 3][j][0] | ((uint64_t)S.eacc[m & 3][j][1] << 32);
+    const int64_t base = (int64_t)m * ZE_CH;
+    const int64_t n0 = S.n0[j], need = Tc - n0;  // >= 1 normals still to draw
+    int pos = S.carry[j];
+    uint64_t vis = 0;
+    int64_t used = -1;  // the draw's words, once it ends in this chunk
+    bool ovf = false;
+    while (pos < ZE_CH) {
+      const uint64_t from = ~0ull << pos;
+      const uint64_t slow = ~fm & from;
+      const int q = slow ? __ffsll((long long)slow) - 1 : ZE_CH;
+      const int have = __popcll(vis);
+      if (have + (q - pos) >= need) {  // the draw ends at a single-word attempt in [pos, q)
+        const int qe = pos + (int)(need - have) - 1;
+        vis |= from & ze_low(qe + 1);
+        used = base + qe + 1;
+        break;
+      }
+      vis |= from & ze_low(q);
+      if (q >= ZE_CH) {
+        pos = ZE_CH;
+        break;
+      }
+      int L = S.elen[m & 3][j][q];
+      if (L <= 0) {  // a tail beyond the ring window (never in practice): flagged
+        L = 1 + 2 * ZE_MMAX;
+        ovf = true;
+      }
+      if ((ea >> q) & 1) {
+        vis |= 1ull << q;
+        if (have + (q - pos) + 1 >= need) {
+          used = base + q + L;
+          break;
+        }
+      }
+      pos = q + L;
+    }
+    S.vis[m & 1][j] = vis;
+    S.n0e[m & 1][j] = (int32_t)n0;
+    S.wr[m & 1][j] = m;
+    if (used >= 0) {
+      EnsChain &ec = E[c0 + j];
+      const int mc = (int)(used / ZE_CH);
+      uint64_t st[4];
+      for (int k = 0; k < 4; k++) st[k] = S.snap[j][mc & 3][k];
+      for (int64_t t = (int64_t)mc * ZE_CH; t < used; t++) sfc64_next(st);
+      for (int k = 0; k < 4; k++) ec.st_used[k] = st[k];
+      ec.used = (uint64_t)used;
+      ec.u_word = sfc64_next(st);
+      for (int k = 0; k < 4; k++) ec.st_used1[k] = st[k];
+      if (advance)  // blocked momenta streams: no uniform is ever drawn from them
+        for (int k = 0; k < 4; k++) ec.st[k] = ec.st_used[k];
+      ec.overflow = (S.ovf[j] | (int)ovf) ? 1 : 0;
+      S.done[j] = 1;
+      atomicAdd(&S.ndone, 1);
+      atomicMax(&S.last_round, r);
+    } else {
+      S.n0[j] = (int32_t)(n0 + __popcll(vis));
+      S.carry[j] = pos - ZE_CH;
+      S.ovf[j] |= (int)ovf;
+    }
+  };
+  // the normals of chunk m (lanes = words; two chains at a time, all loads
+  // before the stores)
+  const int em = ze_emitter(warp);
+  auto emit = [&](int m) {
+    for (int j0 = em; j0 < nch; j0 += 2 * ZE_NE) {
+      uint64_t vis[2];
+      int64_t n0[2];
+      double xv[2][2];
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        const int j = min(j0 + t * ZE_NE, nch - 1);
+        const bool ok = j0 + t * ZE_NE < nch && S.wr[m & 1][j] == m;
+        vis[t] = ok ? S.vis[m & 1][j] : 0ull;
+        n0[t] = S.n0e[m & 1][j];
+#pragma unroll
+        for (int h = 0; h < 2; h++) xv[t][h] = S.xs[m & 3][j][h * 32 + lane];
+      }
+#pragma unroll
+      for (int t = 0; t < 2; t++) {
+        double *out = normals + (int64_t)(c0 + j0 + t * ZE_NE) * Tc + n0[t];
+        const int64_t lim = Tc - n0[t];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int q = h * 32 + lane;
+          const int o = __popcll(vis[t] & ze_low(q));
+          if (((vis[t] >> q) & 1) && o < lim) out[o] = xv[t][h];
+        }
+      }
+    }
+  };
   if (gen) {
     gen_chunk(0);
     gen_chunk(1);
   }
   __syncthreads();
+  const int cq = ze_classifier(warp);
+  if (cq >= 0) classify(0, cq);
+  __syncthreads();
   long long cy_work = 0, cy_wait = 0, t_a = 0;
   int rounds = 0;
+  const unsigned long long t_loop = dbg ? zgt() : 0ull;
   for (int r = 0;; r++) {
-    if (S.ndone >= ZE_G) break;
+    // chains still drawing, or the last chunk walked still to be emitted
+    if (S.ndone >= ZE_G && S.last_round + 1 < r) break;
     rounds++;
-    if (dbg) t_a = clock64();
+    if (dbg) t_a = ze_clk();
     if (warp == 0) {
+      if (lane == 0) S.qn[(r + 2) & 3] = 0;  // chunk r+2's queue (its previous user, chunk r-2, is done)
       if (gen) gen_chunk(r + 2);
-    } else {
-      for (int j = ze_chain_of_warp(warp); j >= 0 && j < nch; j += ZE_G) {
-        if (S.done[j]) continue;
-        const uint64_t *row = S.ring + j * ZE_RS;
-        const int64_t base = (int64_t)r * ZE_CH;
-        int len[2], acc[2];
-        double x[2];
-#pragma unroll
-        for (int hf = 0; hf < 2; hf++) {
-          const int q = hf * 32 + lane;
-          const int k = (int)((base + q) & (ZE_RING - 1));
-          uint64_t w = row[k];
-          const int idx = (int)(w & 0xff);
-          w >>= 8;
-          const uint64_t rabs = (w >> 1) & 0x000fffffffffffffULL;
-          const double fr =
-              __dsub_rn(__longlong_as_double((long long)(0x4330000000000000ULL | rabs)), 4503599627370496.0);
-          x[hf] = __dmul_rn(fr, S.wi[idx]);
-          if (w & 1) x[hf] = -x[hf];
-          len[hf] = 1;
-          acc[hf] = 1;
-          if (!(rabs < S.ki[idx])) {
-            if (idx == 0) {  // exponential tail
-              len[hf] = 0;
-              acc[hf] = 0;
-              for (int m = 1; m <= ZE_MMAX; m++) {
-                const double xx = __dmul_rn(RSV_ZIG_NEG_INV_R,
-                                            glibc_log1p(-u01(row[(k + 2 * m - 1) & (ZE_RING - 1)])));
-                const double yy = -glibc_log1p(-u01(row[(k + 2 * m) & (ZE_RING - 1)]));
-                if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
-                  x[hf] = ((rabs >> 8) & 0x1) ? -__dadd_rn(RSV_ZIG_R, xx) : __dadd_rn(RSV_ZIG_R, xx);
-                  len[hf] = 1 + 2 * m;
-                  acc[hf] = 1;
-                  break;
-                }
-              }
-            } else {  // wedge
-              const double u = u01(row[(k + 1) & (ZE_RING - 1)]);
-              const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(S.fi[idx - 1], S.fi[idx]), u), S.fi[idx]);
-              acc[hf] = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x[hf]), x[hf])) ? 1 : 0;
-              len[hf] = 2;
-            }
-          }
-        }
-        const uint64_t nu = (uint64_t)__ballot_sync(0xffffffffu, len[0] != 1) |
-                            ((uint64_t)__ballot_sync(0xffffffffu, len[1] != 1) << 32);
-        const uint64_t am = (uint64_t)__ballot_sync(0xffffffffu, acc[0]) |
-                            ((uint64_t)__ballot_sync(0xffffffffu, acc[1]) << 32);
-        // walk: positions covered by attempts that started earlier
-        const int e = S.carry[j];
-        uint64_t cov_lo = e ? ((1ull << e) - 1) : 0, cov_hi = 0;
-        bool ovf = false;
-        uint64_t m = nu;
-        while (m) {
-          const int q = __ffsll((long long)m) - 1;
-          m &= m - 1;
-          if ((cov_lo >> q) & 1) continue;
-          const int L = __shfl_sync(0xffffffffu, q < 32 ? len[0] : len[1], q & 31);
-          if (L == 0) { ovf = true; continue; }
-          for (int t = q + 1; t < q + L; t++) {  // at most 60 positions
-            if (t < 64) cov_lo |= 1ull << t;
-            else cov_hi |= 1ull << (t - 64);
-          }
-        }
-        const uint64_t vis = ~cov_lo & am;
-        const int cnt = __popcll(vis);
-        const int64_t n0 = S.n0[j];
-        double *out = normals + (int64_t)(c0 + j) * Tc;
-#pragma unroll
-        for (int hf = 0; hf < 2; hf++) {
-          const int q = hf * 32 + lane;
-          if ((vis >> q) & 1) {
-            const int64_t o = n0 + __popcll(vis & ((1ull << q) - 1));
-            if (o < Tc) out[o] = x[hf];
-          }
-        }
-        if (n0 + cnt >= Tc) {  // the draw ends in this chunk
-          uint64_t v = vis;
-          for (int64_t t = n0; t < Tc - 1; t++) v &= v - 1;
-          const int q = __ffsll((long long)v) - 1;
-          const int L = __shfl_sync(0xffffffffu, q < 32 ? len[0] : len[1], q & 31);
-          if (lane == 0) {
-            EnsChain &ec = E[c0 + j];
-            const int64_t used = base + q + L;
-            const int mc = (int)(used / ZE_CH);
-            uint64_t st[4];
-            for (int k = 0; k < 4; k++) st[k] = S.snap[j][mc & 3][k];
-            for (int64_t t = (int64_t)mc * ZE_CH; t < used; t++) sfc64_next(st);
-            for (int k = 0; k < 4; k++) ec.st_used[k] = st[k];
-            ec.used = (uint64_t)used;
-            ec.u_word = sfc64_next(st);
-            for (int k = 0; k < 4; k++) ec.st_used1[k] = st[k];
-            if (advance)  // blocked momenta streams: no uniform is ever drawn from them
-              for (int k = 0; k < 4; k++) ec.st[k] = ec.st_used[k];
-            ec.overflow = ovf ? 1 : 0;
-            S.done[j] = 1;
-            atomicAdd(&S.ndone, 1);
-          }
-        } else if (lane == 0) {
-          S.n0[j] = (int32_t)(n0 + cnt);
-          S.carry[j] = __ffsll((long long)~cov_hi) - 1;
-          if (ovf) E[c0 + j].overflow = 1;
-        }
-        __syncwarp();
-      }
+    } else if (cq >= 0) {
+      classify(r + 1, cq);
+    } else if (warp == 6) {
+      evaluate(r);
+    } else if (warp == 5) {
+      if (r >= 1) walk(r - 1, r);
+    } else if (em >= 0 && r >= 2) {
+      emit(r - 2);
     }
     if (dbg) {
-      const long long t_b = clock64();
+      const long long t_b = ze_clk();
       cy_work += t_b - t_a;
       __syncthreads();
-      cy_wait += clock64() - t_b;
+      cy_wait += ze_clk() - t_b;
     } else {
       __syncthreads();
     }
   }
-  if (dbg && lane == 0 && warp < 2) {
-    dbg[(size_t)blockIdx.x * 8 + warp * 2] = cy_work;
-    dbg[(size_t)blockIdx.x * 8 + warp * 2 + 1] = cy_wait;
-    if (warp == 0) dbg[(size_t)blockIdx.x * 8 + 4] = rounds;
+  // stamps: generator work / wait cycles, rounds, walk work / wait cycles,
+  // and %globaltimer at entry, loop start, exit
+  if (dbg && lane == 0 && warp == 0) {
+    unsigned long long *d = dbg + (size_t)blockIdx.x * 8;
+    d[0] = cy_work;
+    d[4] = rounds;
+    d[3] = t_loop;
+    d[7] = zgt();
   }
+  if (dbg && lane == 0 && (warp == 1 || warp == 3 || warp == 5 || warp == 6))  // classify, emit, walk, evaluate
+    dbg[(size_t)blockIdx.x * 8 + (warp == 1 ? 1 : warp == 3 ? 2 : warp)] = cy_work;
 }
 
 int launch_momenta_ens(EnsChain *ens, double *normals, int64_t Tc, int n_chains, cudaStream_t s, int *launches,
