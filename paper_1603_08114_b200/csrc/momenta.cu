@@ -1176,7 +1176,9 @@ __global__ void __launch_bounds__(TH_NT) theta_sweep_kernel(DevControl *C, DevPa
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
-  if (threadIdx.x || blockIdx.x) return;
+  // warp 0 runs the draws, every lane on the same values (theta_dev.cuh:
+  // lane-parallel transcendentals); the identical stores of its lanes merge
+  if (threadIdx.x >= 32 || blockIdx.x) return;
   (void)sfc_snaps;
   theta_sweep_body(C, P, K, R, pr, dt, T, s_ki, s_wi, s_fi);
 }

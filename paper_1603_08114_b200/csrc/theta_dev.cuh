@@ -98,13 +98,23 @@ static __device__ Recentred recentre(const double *st, double Td, double c, doub
   return r;
 }
 
+// The theta body runs on all 32 lanes of one warp with identical values (the
+// same sequential draws in every lane); where it needs several independent
+// logarithms, each lane evaluates one and the results are gathered by
+// shuffles -- one glibc log1p latency instead of six on the chain of the phi
+// update.  (Spreading the quotients of the mu / xi updates the same way was
+// measured slower: the divisions already overlap within one thread.)
+__device__ __forceinline__ double lane_pick(double v, int k) { return __shfl_sync(0xffffffffu, v, k); }
+
 static __device__ double phi_log_ratio(double prop, double phi, double h1_sq, double se2, const DevPrior &pr) {
-  const double a = __dmul_rn(0.5, __dsub_rn(log1p_ool(-__dmul_rn(prop, prop)), log1p_ool(-__dmul_rn(phi, phi))));
-  const double b = __ddiv_rn(__dmul_rn(h1_sq, __dsub_rn(__dsub_rn(1.0, __dmul_rn(prop, prop)),
-                                                        __dsub_rn(1.0, __dmul_rn(phi, phi)))),
-                             __dmul_rn(2.0, se2));
-  const double c = __dmul_rn(__dsub_rn(pr.phi_a, 1.0), __dsub_rn(log1p_ool(prop), log1p_ool(phi)));
-  const double d = __dmul_rn(__dsub_rn(pr.phi_b, 1.0), __dsub_rn(log1p_ool(-prop), log1p_ool(-phi)));
+  const int lane = threadIdx.x & 31;
+  const double pp = __dmul_rn(prop, prop), ff = __dmul_rn(phi, phi);
+  const double arg = lane == 0 ? -pp : lane == 1 ? -ff : lane == 2 ? prop : lane == 3 ? phi : lane == 4 ? -prop : -phi;
+  const double lg = log1p_ool(arg);
+  const double a = __dmul_rn(0.5, __dsub_rn(lane_pick(lg, 0), lane_pick(lg, 1)));
+  const double b = __ddiv_rn(__dmul_rn(h1_sq, __dsub_rn(__dsub_rn(1.0, pp), __dsub_rn(1.0, ff))), __dmul_rn(2.0, se2));
+  const double c = __dmul_rn(__dsub_rn(pr.phi_a, 1.0), __dsub_rn(lane_pick(lg, 2), lane_pick(lg, 3)));
+  const double d = __dmul_rn(__dsub_rn(pr.phi_b, 1.0), __dsub_rn(lane_pick(lg, 4), lane_pick(lg, 5)));
   return __dadd_rn(__dadd_rn(__dsub_rn(a, b), c), d);
 }
 
@@ -255,10 +265,14 @@ static __device__ __noinline__ void theta_sweep_body(DevControl *C, DevParams *P
   q.phi = phi; q.mu = mu; q.xi = xi; q.se2 = se2; q.su2 = su2;
   q.inv_su2 = 1.0 / su2;
   q.inv_se2 = 1.0 / se2;
-  q.emu = exp_ool(-mu);
   q.one_m_phi2 = 1.0 - phi * phi;
-  q.hconst = 0.5 * Td * mu + 0.5 * Td * log_ool(su2) + 0.5 * log_ool(se2 / (1.0 - phi * phi)) +
-             0.5 * Tm1 * log_ool(se2);
+  {
+    const int lane = threadIdx.x & 31;
+    const double lg = log_ool(lane == 0 ? su2 : lane == 1 ? se2 / (1.0 - phi * phi) : se2);
+    const double l_su2 = lane_pick(lg, 0), l_st = lane_pick(lg, 1), l_se2 = lane_pick(lg, 2);
+    q.emu = exp_ool(-mu);
+    q.hconst = 0.5 * Td * mu + 0.5 * Td * l_su2 + 0.5 * l_st + 0.5 * Tm1 * l_se2;
+  }
   q.n_lo = (int32_t)floor((mu - 50.0) * RSV_INV_LN2_N);
   q.n_span = (int32_t)ceil((mu + 50.0) * RSV_INV_LN2_N) - q.n_lo;
   *P = q;
