@@ -433,6 +433,9 @@ class _LocalComm:
             recvs[r][0].copy_(sends[r - 1][1]) if r > 0 else None
             recvs[r][1].copy_(sends[r + 1][0]) if r < len(chains) - 1 else None
 
+    def agree(self, ok: bool) -> bool:
+        return ok
+
 
 class _NcclComm:
     """One shard per rank of a torch.distributed (NCCL) group: records by
@@ -456,6 +459,13 @@ class _NcclComm:
             ops += [dist.P2POp(dist.isend, send_r, r + 1, self.group), dist.P2POp(dist.irecv, recv_r, r + 1, self.group)]
         for q in dist.batch_isend_irecv(ops) if ops else []:
             q.wait()  # orders the copies on the current stream (no host block)
+
+    def agree(self, ok: bool) -> bool:
+        """True on every rank iff true on every rank (eager, outside any capture)."""
+        import torch
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.cuda.current_device())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return bool(t.item())
 
 
 def _drive(chains, comm, step_size, n_steps, n, fuse, stats, halo_every, dev, stream, l2_flush=None, times=None,
@@ -499,12 +509,12 @@ def _drive(chains, comm, step_size, n_steps, n, fuse, stats, halo_every, dev, st
                                                  fr.numel(), 1))
             c.halo_valid = True
 
-    def proposal(i, ev=None):
+    def proposal(i, ev=None, halo_here=True):
         if l2_flush is not None:
             l2_flush.fill_(i & 0xff)
         if ev is not None:
             ev[0].record(stream)
-        if world > 1 and (i % K == 0 or not all(c.halo_valid for c in chains)):
+        if halo_here and world > 1 and (i % K == 0 or not all(c.halo_valid for c in chains)):
             halo()
         if windowed:
             for c, w in zip(chains, win_mine):
@@ -547,24 +557,43 @@ def _drive(chains, comm, step_size, n_steps, n, fuse, stats, halo_every, dev, st
                 i += 1
                 pending += 1
             for c in chains:
-                c.halo_valid = False  # the captured period starts with an exchange
                 c.shard._ck(lib.rsv_shard_prepare(c.shard.ctx, float(step_size), int(n_steps), int(bool(fuse)),
                                                   int(bool(stats or theta))))
-            g = torch.cuda.CUDAGraph()
+            # the captured period: K proposals with their collectives; the
+            # margin exchange that opens each period (NCCL send/recv between
+            # neighbours) stays eager, before every replay.  If any rank cannot
+            # capture, every rank stays on the eager path.
             evs = [events(True) for _ in range(K)] if times is not None else [None] * K
-            with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
-                for j in range(K):
-                    proposal(j, evs[j])
-            while n - i >= K:
+            g = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+                    for j in range(K):
+                        proposal(j, evs[j], halo_here=False)
+                captured = True
+            except Exception:  # noqa: BLE001 -- any capture failure means the eager path
+                captured = False
+            if not comm.agree(captured):
+                g = None
+            hev = events() if times is not None and world > 1 else None
+            while g is not None and n - i >= K:
                 if pending + K > _RING:
                     drain(pending)
                     pending = 0
+                if world > 1:
+                    if hev is not None:
+                        hev[0].record(stream)
+                    halo()
+                    if hev is not None:
+                        hev[1].record(stream)
                 g.replay()
                 i += K
                 pending += K
                 if times is not None:  # the captured events are re-recorded by the next replay
                     stream.synchronize()
-                    times.extend(a.elapsed_time(b) for a, b in evs)
+                    t = [a.elapsed_time(b) for a, b in evs]
+                    if hev is not None:  # the period's margin exchange belongs to its first proposal
+                        t[0] += hev[0].elapsed_time(hev[1])
+                    times.extend(t)
         while i < n:
             ev = events() if times is not None else None
             proposal(i, ev)
