@@ -38,6 +38,25 @@ def test_ensemble_momenta_bit_exact_per_chain():
                 assert [int(x) for x in st[c]] == [int(x) for x in gens[c].bit_generator.state["state"]["state"]]
 
 
+@pytest.mark.parametrize("C,Tc", [(1, 64), (29, 64), (30, 1032), (61, 200), (59, 4096)])
+def test_ensemble_momenta_pipeline_shapes(C, Tc):
+    """The ensemble momenta kernel's chunk pipeline (29 chains per CTA,
+    64-word chunks): partial CTAs, chains shorter than a chunk, chains ending
+    mid-chunk, three consecutive draws -- every chain bit-exact against
+    numpy's own SFC64 stream, and the streams continue exactly."""
+    seed = 3
+    gens = [np.random.Generator(np.random.SFC64(np.random.SeedSequence([seed, c]))) for c in range(C)]
+    with P.Ensemble(C, Tc) as ens:
+        ens.seed(seed)
+        for _ in range(3):
+            got = ens.refresh_momenta()
+            st = ens.streams()
+            for c in range(C):
+                want = gens[c].standard_normal(Tc)
+                assert np.array_equal(got[c].view(np.uint64), want.view(np.uint64)), c
+                assert [int(x) for x in st[c]] == [int(x) for x in gens[c].bit_generator.state["state"]["state"]]
+
+
 @pytest.mark.parametrize("fuse", [False, True])
 def test_ensemble_matches_single_chain_oracle(fuse):
     C, Tc, L, dt, seed = 6, 256, 12, 0.03, 11
