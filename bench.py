@@ -649,19 +649,41 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
     T, L, dt = args.T, args.L, args.dt
     dev = f"cuda:{local}"
     margin = 8 * (L + 1)
-    chain = P.ShardedChain(truth.dataset, theta, rank, ws, margin=margin, device=local)
-    chain.set_latent_global(truth.latent)
-    chain.set_stream(P.stream_state(P.make_rng(1, args.prng)))
     windowed = args.prng != "sfc64"
-    if windowed:
-        chain.set_windowed_momenta(True)
-    P.sharded.hmc_update_distributed_device(chain, dt, L, max(3, args.warmup))
+
+    def make_chain():
+        ch = P.ShardedChain(truth.dataset, theta, rank, ws, margin=margin, device=local)
+        ch.set_latent_global(truth.latent)
+        ch.set_stream(P.stream_state(P.make_rng(1, args.prng)))
+        if windowed:
+            ch.set_windowed_momenta(True)
+        return ch
+
+    # the per-proposal records go through the peer-memory boxes (NVLink
+    # stores) unless RSV_P2P=0 or any rank cannot map its peers' boxes; a run
+    # in which some rank's records never arrive (the collect kernel's 5 s
+    # timeout) falls back to the NCCL exchange on every rank
+    p2p = P.sharded._p2p_default(ws)
+    chain = make_chain()
+    ok = True
+    try:
+        P.sharded.hmc_update_distributed_device(chain, dt, L, max(3, args.warmup), p2p=p2p)
+    except P._native.NativeError:
+        ok = False
+    agreed = torch.tensor([1 if ok else 0], dtype=torch.int32, device=f"cuda:{local}")
+    dist.all_reduce(agreed, op=dist.ReduceOp.MIN)
+    if not int(agreed.item()):
+        chain.shard.close()
+        p2p = False
+        chain = make_chain()
+        P.sharded.hmc_update_distributed_device(chain, dt, L, max(3, args.warmup), p2p=False)
+    exchange = P.sharded.exchange_kind(chain)
     clocks = ClockSampler(local) if rank == 0 else None
     if clocks:
         clocks.start()
     t_load = time.perf_counter()
     while time.perf_counter() - t_load < 0.4:
-        P.sharded.hmc_update_distributed_device(chain, dt, L, 21, graph=True)
+        P.sharded.hmc_update_distributed_device(chain, dt, L, 21, graph=True, p2p=p2p)
     # L2 flushed before every proposal (a 256 MiB write, not timed), one event
     # pair per proposal around it on the proposal stream (as at N=1)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -669,7 +691,8 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
     torch.cuda.synchronize(local)
     n0 = chain.shard.launch_count()
     times = []
-    res = P.sharded.hmc_update_distributed_device(chain, dt, L, args.steps, l2_flush=flush, times=times, graph=True)
+    res = P.sharded.hmc_update_distributed_device(chain, dt, L, args.steps, l2_flush=flush, times=times, graph=True,
+                                                  p2p=p2p)
     torch.cuda.synchronize(local)
     launches = chain.shard.launch_count() - n0
     dist.barrier()
@@ -689,14 +712,14 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
     for _ in range(2):
         chain.shard.set_latent(h_host[ls:le])
         chain.halo_valid = True
-        P.sharded.hmc_update_distributed_device(chain, dt, L, 1)
+        P.sharded.hmc_update_distributed_device(chain, dt, L, 1, p2p=p2p)
     dist.barrier()
     n_acc = 0
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         chain.shard.set_latent(h_host[ls:le])
         chain.halo_valid = True
-        r = P.sharded.hmc_update_distributed_device(chain, dt, L, 1)
+        r = P.sharded.hmc_update_distributed_device(chain, dt, L, 1, p2p=p2p)
         if r[0].accept:
             h_host[lo:hi] = chain.owned_latent()
             n_acc += 1
@@ -708,7 +731,7 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
     # ---- config 5 sharded: T = 2^26, full theta update per sweep, blocked sfc64
     c5 = None
     if not args.no_config5:
-        c5 = config5_sharded(args, P, theta, rank, ws, local, dist, torch)
+        c5 = config5_sharded(args, P, theta, rank, ws, local, dist, torch, p2p=p2p)
 
     if rank == 0:
         v = T * L / (ms * 1e-3)
@@ -721,7 +744,10 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
                                f"{P.sharded.halo_period(margin, L)} proposals, "
                                + ("windowed momenta (each GPU parses its window of the stream), " if windowed else
                                   "replicated momenta (sfc64: no jump-ahead), ")
-                               + "NCCL all_gather of the shard records, decision on the device)",
+                               + ("shard records exchanged by NVLink stores into every GPU's box (peer memory), "
+                                  if exchange == "p2p" else "NCCL all_gather of the shard records, ")
+                               + "decision on the device)",
+                "exchange": exchange,
                 "l2": "flushed before every proposal (256 MiB write per GPU, outside the event pairs)",
                 "trajectories_per_s": 1e3 / ms, "accept_rate": acc, "clocks": clk,
                 "e2e": {"value": T * L / e2e_s, "unit": UNIT,
@@ -736,7 +762,7 @@ def sharded_run(args, P, theta, truth, rank, ws, local, dist, torch):
         print(json.dumps(line), flush=True)
 
 
-def config5_sharded(args, P, theta, rank, ws, local, dist, torch, block=4096, sweeps=30, dt=0.005):
+def config5_sharded(args, P, theta, rank, ws, local, dist, torch, block=4096, sweeps=30, dt=0.005, p2p=None):
     """Config 5 across the N GPUs: T = 2^26, run_chain with the theta draws
     on every GPU from the all-gathered statistics, sfc64 blocked momenta
     (each GPU draws the blocks its sites touch).  Wall clock around the
@@ -749,12 +775,12 @@ def config5_sharded(args, P, theta, rank, ws, local, dist, torch, block=4096, sw
     ch.set_stream(P.stream_state(P.make_rng(1, "sfc64")))
     ch.set_blocked_streams(1, block)
     prior = P.PriorSpec()
-    P.sharded.run_chain_sharded([ch], dt, 20, prior, 0, 2, 1)
+    P.sharded.run_chain_sharded([ch], dt, 20, prior, 0, 2, 1, p2p=p2p)
     ch.set_params(theta)
     dist.barrier()
     torch.cuda.synchronize(local)
     t0 = time.perf_counter()
-    it, par, acc, dh = P.sharded.run_chain_sharded([ch], dt, 20, prior, 0, sweeps, 1)
+    it, par, acc, dh = P.sharded.run_chain_sharded([ch], dt, 20, prior, 0, sweeps, 1, p2p=p2p)
     torch.cuda.synchronize(local)
     el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
     dist.all_reduce(el, op=dist.ReduceOp.MAX)

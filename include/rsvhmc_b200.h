@@ -214,6 +214,26 @@ int rsv_shard_results(rsv_ctx *ctx, rsv_result *out, int max_n, int *n_out);
 int rsv_shard_set_momenta(rsv_ctx *ctx, int windowed);
 int rsv_shard_momenta_async(rsv_ctx *ctx, double *window_record_dev);
 int rsv_shard_place_async(rsv_ctx *ctx, const double *gathered_records_dev, int world, int rank);
+/* Peer-memory exchange of the per-proposal records (replaces the two NCCL
+ * all-gathers of the protocol above by NVLink stores between the GPUs; the
+ * reference's ΔH / statistics reduction, sampler.py:155-167 over the whole
+ * series): every shard owns a small receive box.  rsv_shard_p2p_init
+ * allocates it and returns its 64-byte CUDA IPC handle (and its device
+ * address, for shards of the same process); rsv_shard_p2p_connect maps
+ * every shard's box (boxes[q] != 0: that address, same device; otherwise
+ * handles[64 q..] is opened over NVLink).  Per exchange (words = 23: shard
+ * totals, 8: window records) every shard calls rsv_shard_p2p_push_async
+ * with its own record, then rsv_shard_p2p_collect_async, which waits for
+ * every shard's record of this exchange (flags written with release
+ * semantics after the record; a missing peer raises an error after 5 s
+ * instead of hanging) and copies the records out in rank order -- the
+ * layout the all-gather produced, so rsv_shard_decide_async /
+ * rsv_shard_place_async read it unchanged.  Shards of one process push all
+ * before any of them collects. */
+int rsv_shard_p2p_init(rsv_ctx *ctx, int world, int rank, unsigned char handle[64], uint64_t *box_dev);
+int rsv_shard_p2p_connect(rsv_ctx *ctx, const unsigned char *handles, const uint64_t *boxes);
+int rsv_shard_p2p_push_async(rsv_ctx *ctx, const double *record_dev, int words);
+int rsv_shard_p2p_collect_async(rsv_ctx *ctx, double *records_out_dev, int words);
 /* Blocked layout of a shard (config 5): the streams of the blocks
  * [first_block, first_block + n_blocks) its local range touches. */
 int rsv_shard_set_blocked_streams(rsv_ctx *ctx, int64_t block_len, int64_t first_block, int64_t n_blocks,

@@ -125,6 +125,11 @@ _SIGS = {
     "rsv_shard_prepare": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "rsv_shard_momenta_async": (ctypes.c_int, [_CTX, ctypes.c_void_p]),
     "rsv_shard_place_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+    "rsv_shard_p2p_init": (ctypes.c_int, [_CTX, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                          ctypes.POINTER(ctypes.c_uint64)]),
+    "rsv_shard_p2p_connect": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_void_p]),
+    "rsv_shard_p2p_push_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int]),
+    "rsv_shard_p2p_collect_async": (ctypes.c_int, [_CTX, ctypes.c_void_p, ctypes.c_int]),
     "rsv_shard_set_blocked_streams": (ctypes.c_int, [_CTX, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                                      ctypes.c_void_p]),
     "rsv_shard_run_begin": (ctypes.c_int, [_CTX, ctypes.c_double, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,

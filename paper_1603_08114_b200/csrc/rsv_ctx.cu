@@ -104,6 +104,11 @@ struct rsv_ctx {
   // time-sharded windowed momenta (rsv_shard_set_momenta): this shard's window
   // of the raw-word stream, its anchors, and the parse outputs
   int win_mode = 0;
+  // peer-memory record exchange (rsv_shard_p2p_*)
+  P2PBox *p2p_box = nullptr;         // mine (receives every shard's records)
+  P2PBox **p2p_peers = nullptr;      // device array: every shard's box, as this device sees it
+  std::vector<void *> p2p_opened;    // boxes opened from IPC handles (closed on destroy)
+  int p2p_world = 0, p2p_rank = 0;
   int64_t win_wb0 = 0, win_nb = 0, win_cap = 0, win_a_lo = 0, win_a_hi = -1;
   double *win_out = nullptr;
   uint32_t *win_nend = nullptr;
@@ -224,6 +229,9 @@ int rsv_destroy(rsv_ctx *c) {
   if (c->h_blocks) cudaFreeHost(c->h_blocks);
   if (c->win_out) cudaFree(c->win_out);
   if (c->win_nend) cudaFree(c->win_nend);
+  for (void *q : c->p2p_opened) cudaIpcCloseMemHandle(q);
+  if (c->p2p_peers) cudaFree(c->p2p_peers);
+  if (c->p2p_box) cudaFree(c->p2p_box);
   if (c->kdev) cudaFree(c->kdev);
   if (c->run) cudaFree(c->run);
   if (c->run_store) cudaFree(c->run_store);
@@ -531,6 +539,8 @@ static int check_err_bits(rsv_ctx *c) {
     return fail(c, RSV_E_CUDA, "sharded momenta: neighbouring windows disagree on an attempt boundary");
   if (c->h_ctrl->err & 32) return fail(c, RSV_E_CUDA, "sharded momenta: a window does not cover its shard");
   if (c->h_ctrl->err & 4) return fail(c, RSV_E_CUDA, "ensemble momenta: a tail draw needed > 30 loops");
+  if (c->h_ctrl->err & 64)
+    return fail(c, RSV_E_CUDA, "sharded chain: a peer's record did not arrive within the timeout (peer exchange)");
   return 0;
 }
 
@@ -1781,6 +1791,130 @@ int rsv_shard_place_async(rsv_ctx *c, const double *winfo_all, int world, int ra
   const int nb = (int)((c->T + 255) / 256 < 2 * c->sm_count ? (c->T + 255) / 256 : 2 * c->sm_count);
   shard_place_kernel<<<nb, 256, 0, c->stream>>>(c->ctrl, reinterpret_cast<const WinInfo *>(winfo_all), world, rank,
                                                 c->win_out, c->win_nend, c->normals + c->goff, c->T, c->goff, c->Tg);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// ---- peer-memory exchange of the per-proposal records (instead of an NCCL
+// all-gather): push = this shard's record into every shard's box over
+// NVLink, collect = wait for every flag of my box, copy the records out.
+// One thread per destination / source rank; the records are 8-23 words.
+__global__ void p2p_push_kernel(DevControl *C, P2PBox *const *peers, int world, int rank, const double *src, int kind,
+                                int words) {
+  __shared__ unsigned long long s_e;
+  if (threadIdx.x == 0) {
+    const unsigned long long e = C->p2p_seq[kind] + 1;
+    C->p2p_seq[kind] = e;
+    s_e = e;
+  }
+  __syncthreads();
+  const unsigned long long e = s_e;
+  const int q = threadIdx.x;
+  if (q >= world) return;
+  P2PBox *box = peers[q];
+  double *dst = box->rec[kind][e & 1][rank];
+  for (int k = 0; k < words; k++) dst[k] = src[k];
+  // the record before its flag, for any observer in the system
+  asm volatile("fence.sc.sys;" ::: "memory");
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&box->flag[kind][e & 1][rank]), "l"(e) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long p2p_ld_acquire(const unsigned long long *f) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+  return v;
+}
+
+__global__ void p2p_collect_kernel(DevControl *C, const P2PBox *box, int world, int kind, int words, double *out) {
+  const int q = threadIdx.x;
+  const unsigned long long e = C->p2p_seq[kind];  // my own push of this exchange came first on the stream
+  if (q < world) {
+    const unsigned long long *f = &box->flag[kind][e & 1][q];
+    const unsigned long long t0 = gtimer_ns();
+    bool ok = true;
+    while (p2p_ld_acquire(f) != e) {
+      if (gtimer_ns() - t0 > 5000000000ull) {  // 5 s: a peer is gone; flagged, never a hang
+        ok = false;
+        break;
+      }
+      __nanosleep(100);
+    }
+    if (!ok) atomicOr(&C->err, 64);
+    const double *r = box->rec[kind][e & 1][q];
+    for (int k = 0; k < words; k++) out[(size_t)q * words + k] = __ldcv(r + k);  // not from a stale L1 line
+  }
+}
+
+int rsv_shard_p2p_init(rsv_ctx *c, int world, int rank, unsigned char *handle, uint64_t *box_dev) {
+  if (!c || !handle) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->shard) return fail(c, RSV_E_STATE, "not a shard context (rsv_create_shard)");
+  if (world < 1 || world > P2P_MAXW || rank < 0 || rank >= world)
+    return fail(c, RSV_E_INVALID, "peer exchange supports 1..%d shards (rank %d of %d)", P2P_MAXW, rank, world);
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  if (!c->p2p_box) CK(cudaMalloc(&c->p2p_box, sizeof(P2PBox)));
+  CK(cudaMemset(c->p2p_box, 0, sizeof(P2PBox)));
+  CK(cudaMemset(c->ctrl->p2p_seq, 0, sizeof(c->ctrl->p2p_seq)));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->p2p_box));
+  memcpy(handle, &h, sizeof(h));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "rsv_shard_p2p_init: 64-byte handles");
+  if (box_dev) *box_dev = (uint64_t)(uintptr_t)c->p2p_box;
+  c->p2p_world = world;
+  c->p2p_rank = rank;
+  return 0;
+}
+
+int rsv_shard_p2p_connect(rsv_ctx *c, const unsigned char *handles, const uint64_t *boxes) {
+  if (!c || (!handles && !boxes)) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->p2p_box) return fail(c, RSV_E_STATE, "rsv_shard_p2p_init first");
+  CK(cudaSetDevice(c->device));
+  const int w = c->p2p_world;
+  std::vector<P2PBox *> ptr(w, nullptr);
+  for (int q = 0; q < w; q++) {
+    if (q == c->p2p_rank) {
+      ptr[q] = c->p2p_box;
+    } else if (boxes && boxes[q]) {  // a shard of this process (same device)
+      ptr[q] = reinterpret_cast<P2PBox *>((uintptr_t)boxes[q]);
+    } else {  // another process's box: mapped over NVLink
+      cudaIpcMemHandle_t h;
+      memcpy(&h, handles + 64 * (size_t)q, sizeof(h));
+      void *d = nullptr;
+      CK(cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess));
+      c->p2p_opened.push_back(d);
+      ptr[q] = reinterpret_cast<P2PBox *>(d);
+    }
+  }
+  if (!c->p2p_peers) CK(cudaMalloc(&c->p2p_peers, sizeof(P2PBox *) * P2P_MAXW));
+  CK(cudaMemcpy(c->p2p_peers, ptr.data(), sizeof(P2PBox *) * w, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int rsv_shard_p2p_push_async(rsv_ctx *c, const double *mine_dev, int words) {
+  if (!c || !mine_dev) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->p2p_peers) return fail(c, RSV_E_STATE, "peer exchange not connected (rsv_shard_p2p_connect)");
+  if (words != SHARD_W && words != (int)(sizeof(WinInfo) / 8)) return fail(c, RSV_E_INVALID, "bad record size");
+  CK(cudaSetDevice(c->device));
+  p2p_push_kernel<<<1, 32, 0, c->stream>>>(c->ctrl, c->p2p_peers, c->p2p_world, c->p2p_rank, mine_dev,
+                                          words == SHARD_W ? 0 : 1, words);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int rsv_shard_p2p_collect_async(rsv_ctx *c, double *out_dev, int words) {
+  if (!c || !out_dev) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c->p2p_peers) return fail(c, RSV_E_STATE, "peer exchange not connected (rsv_shard_p2p_connect)");
+  if (words != SHARD_W && words != (int)(sizeof(WinInfo) / 8)) return fail(c, RSV_E_INVALID, "bad record size");
+  CK(cudaSetDevice(c->device));
+  p2p_collect_kernel<<<1, 32, 0, c->stream>>>(c->ctrl, c->p2p_box, c->p2p_world, words == SHARD_W ? 0 : 1, words,
+                                             out_dev);
   c->launches++;
   CK(cudaGetLastError());
   return 0;

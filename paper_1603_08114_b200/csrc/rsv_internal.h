@@ -78,6 +78,20 @@ struct WinInfo {           // one shard's window, all-gathered (8 words)
   int64_t err;             // bit 1: the exact serial walk redid the window
   int64_t pad;
 };
+// Peer-memory exchange of the sharded chain's per-proposal records: every
+// shard context owns one box; each shard writes its record into slot
+// [epoch & 1][rank] of every shard's box over NVLink (P2P stores) and then
+// the slot's flag (the epoch, release at system scope); a shard reads the
+// records once all flags of its box carry its own epoch.  Two slots: a rank
+// can run at most one exchange ahead of the slowest (its next record needs
+// everyone's current one).
+constexpr int P2P_MAXW = 16;
+constexpr int P2P_KINDS = 2;  // 0: shard records (ShardRec, 23 words), 1: window records (WinInfo, 8 words)
+constexpr int P2P_WORDS = 24;
+struct P2PBox {
+  unsigned long long flag[P2P_KINDS][2][P2P_MAXW];
+  double rec[P2P_KINDS][2][P2P_MAXW][P2P_WORDS];
+};
 struct ZigWin {            // window mode of the momenta kernel
   int64_t wb0;             // first block: CTA b of the window parses block wb0 + b of the full stream
   int64_t w0;              // wb0 * ZB
@@ -155,6 +169,9 @@ struct DevControl {
   // three 42-bit limbs each (fx[3 v + l]; <= 2^22 CTAs cannot carry out of a
   // 64-bit word) and ORs its flag into fx[9]; the last CTA reads and clears
   unsigned long long fx[10];
+  // peer-memory record exchange of a time-sharded chain (rsv_shard_p2p_*):
+  // epochs of this shard's pushes (shard records, window records)
+  unsigned long long p2p_seq[2];
   // %globaltimer stamps (ns) of the last proposal: momenta kernel first-CTA
   // entry / last-CTA exit, trajectory kernel CTA-0 entry / last-CTA exit,
   // and the previous proposal's trajectory exit

@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -468,6 +469,106 @@ class _NcclComm:
         return bool(t.item())
 
 
+def _p2p_push_collect(chains, out, mine):
+    """The records of one exchange through the peer-memory boxes: every
+    shard of this process pushes its record into every shard's box, then
+    every shard waits for and collects its own box (into `out`, rank order:
+    the layout of the all-gather)."""
+    words = out.shape[1]
+    for c, m in zip(chains, mine):
+        c.shard._ck(c.shard._lib.rsv_shard_p2p_push_async(c.shard.ctx, m.data_ptr(), words))
+    for c in chains:
+        c.shard._ck(c.shard._lib.rsv_shard_p2p_collect_async(c.shard.ctx, out.data_ptr(), words))
+
+
+class _LocalP2PComm(_LocalComm):
+    """In-process shards (one GPU) exchanging their records through the
+    peer-memory boxes -- the multi-GPU protocol with same-device addresses."""
+
+    def __init__(self, chains):
+        super().__init__(chains)
+        boxes = (ctypes.c_uint64 * len(chains))()
+        handle = (ctypes.c_ubyte * 64)()
+        for r, c in enumerate(chains):
+            v = ctypes.c_uint64()
+            c.shard._ck(c.shard._lib.rsv_shard_p2p_init(c.shard.ctx, len(chains), r, handle, ctypes.byref(v)))
+            boxes[r] = v.value
+        for c in chains:
+            c.shard._ck(c.shard._lib.rsv_shard_p2p_connect(c.shard.ctx, None, boxes))
+
+    def gather(self, out, mine):
+        _p2p_push_collect(self.chains, out, mine)
+
+
+class P2PUnavailable(RuntimeError):
+    """Some rank could not set up the peer-memory exchange (every rank gets it)."""
+
+
+class _P2PComm(_NcclComm):
+    """One shard per rank, the per-proposal records exchanged by NVLink
+    stores into every rank's box (CUDA IPC mappings, set up once over the
+    NCCL group); the margins still go by NCCL send/recv (every K proposals).
+    The set-up is collective and agreed: if any rank fails (allocation, IPC
+    mapping), every rank raises P2PUnavailable and none is left waiting."""
+
+    def __init__(self, chain, group):
+        import torch
+        super().__init__(chain, group)
+        self.chain = chain
+        lib, ctx = chain.shard._lib, chain.shard.ctx
+        handle = (ctypes.c_ubyte * 64)()
+        box = ctypes.c_uint64()
+        ok = lib.rsv_shard_p2p_init(ctx, self.world, self.rank, handle, ctypes.byref(box)) == 0
+        dev = torch.device("cuda", torch.cuda.current_device())
+        mine = torch.tensor([1 if ok else 0] + list(bytes(handle)), dtype=torch.uint8, device=dev)
+        every = torch.empty(self.world * 65, dtype=torch.uint8, device=dev)
+        self.dist.all_gather_into_tensor(every, mine, group=group)
+        rows = every.cpu().numpy().reshape(self.world, 65)
+        ok = bool(rows[:, 0].all())
+        if ok:
+            hb = rows[:, 1:].tobytes()
+            ok = lib.rsv_shard_p2p_connect(ctx, hb, None) == 0
+        if not self.agree(ok):
+            raise P2PUnavailable("peer-memory exchange unavailable on some rank; use NCCL")
+
+    def gather(self, out, mine):
+        _p2p_push_collect([self.chain], out, mine)
+
+
+def _comm_for(chains, group, p2p):
+    """The exchange for this process's shards: in-process (all shards here)
+    or one shard per rank; by peer memory (p2p) or NCCL / device copies.
+    The connection is made once per chain and group."""
+    local = group is None and len(chains) == chains[0].world
+    key = ("local" if local else id(group), bool(p2p))
+    c0 = chains[0]
+    cache = c0.__dict__.setdefault("_comms", {})
+    if key not in cache:
+        if local:
+            cache[key] = _LocalP2PComm(chains) if p2p else _LocalComm(chains)
+        elif p2p:
+            try:
+                cache[key] = _P2PComm(c0, group)
+            except P2PUnavailable:  # agreed by every rank: all of them take the NCCL exchange
+                cache[key] = _NcclComm(c0, group)
+        else:
+            cache[key] = _NcclComm(c0, group)
+    return cache[key]
+
+
+def exchange_kind(chain, group=None) -> str:
+    """'p2p' or 'nccl': the record exchange the last distributed call used."""
+    comms = chain.__dict__.get("_comms", {})
+    for (k, _), comm in comms.items():
+        if k != "local" and k == id(group):
+            return "p2p" if isinstance(comm, _P2PComm) else "nccl"
+    return "nccl"
+
+
+def _p2p_default(world):
+    return world > 1 and os.environ.get("RSV_P2P", "1") != "0"
+
+
 def _drive(chains, comm, step_size, n_steps, n, fuse, stats, halo_every, dev, stream, l2_flush=None, times=None,
            theta=False, graph=False):
     """n proposals (or sweeps with theta=True) of the chain whose shards
@@ -619,7 +720,7 @@ def _drive(chains, comm, step_size, n_steps, n, fuse, stats, halo_every, dev, st
 
 def hmc_update_local_device(chains: list[ShardedChain], step_size: float, n_steps: int, n: int,
                             fuse: bool = False, stats: bool = False, halo_every: int | None = None,
-                            graph: bool = False):
+                            graph: bool = False, p2p: bool = False):
     """n proposals of a chain whose shards all live in this process (one
     GPU), orchestrated on the device: no host synchronisation until the
     results are read back.  Returns the per-proposal rsv_result records."""
@@ -628,13 +729,14 @@ def hmc_update_local_device(chains: list[ShardedChain], step_size: float, n_step
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.Stream(dev)  # one ordered stream for every shard and every buffer
     with torch.cuda.stream(stream):
-        return _drive(chains, _LocalComm(chains), step_size, n_steps, n, fuse, stats, halo_every, dev, stream,
-                      graph=graph)
+        return _drive(chains, _comm_for(chains, None, p2p), step_size, n_steps, n, fuse, stats, halo_every, dev,
+                      stream, graph=graph)
 
 
 def hmc_update_distributed_device(chain: ShardedChain, step_size: float, n_steps: int, n: int, fuse: bool = False,
                                   stats: bool = False, group=None, halo_every: int | None = None,
-                                  l2_flush=None, times: list | None = None, graph: bool = False):
+                                  l2_flush=None, times: list | None = None, graph: bool = False,
+                                  p2p: bool | None = None):
     """n proposals of a sharded chain over a torch.distributed (NCCL) group,
     orchestrated on the device: window records and shard records
     all-gathered on the GPU, decisions on the GPU, periodic halo exchange;
@@ -648,12 +750,14 @@ def hmc_update_distributed_device(chain: ShardedChain, step_size: float, n_steps
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.Stream(dev)  # the kernels and the NCCL collectives share one ordered stream
     with torch.cuda.stream(stream):
-        return _drive([chain], _NcclComm(chain, group), step_size, n_steps, n, fuse, stats, halo_every, dev, stream,
-                      l2_flush, times, graph=graph)
+        comm = _comm_for([chain], group, _p2p_default(chain.world) if p2p is None else p2p)
+        return _drive([chain], comm, step_size, n_steps, n, fuse, stats, halo_every, dev, stream, l2_flush, times,
+                      graph=graph)
 
 
 def run_chain_sharded(chains: list[ShardedChain], step_size: float, n_steps: int, prior, n_burnin: int,
-                      n_samples: int, thin: int = 1, group=None, halo_every: int | None = None):
+                      n_samples: int, thin: int = 1, group=None, halo_every: int | None = None,
+                      p2p: bool | None = None):
     """run_chain (sampler.py:291-358) of a time-sharded chain, every sweep on
     the devices: the proposal protocol of _drive with the statistics of the
     kept path, then the theta draws (sampler.py:339-344) on every shard from
@@ -671,7 +775,8 @@ def run_chain_sharded(chains: list[ShardedChain], step_size: float, n_steps: int
     n_sweeps = n_burnin + n_samples * thin
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.Stream(dev)
-    comm = _LocalComm(chains) if group is None and len(chains) == chains[0].world else _NcclComm(chains[0], group)
+    local = group is None and len(chains) == chains[0].world
+    comm = _comm_for(chains, group, (not local and _p2p_default(chains[0].world)) if p2p is None else p2p)
     err = None
     with torch.cuda.stream(stream):
         try:

@@ -160,3 +160,52 @@ def test_captured_halo_periods_equal_single_context(backend, windowed):
         assert all(int(c.get_stream().pos) == int(single.get_stream().pos) for c in shards)
     finally:
         _close(shards)
+
+
+@pytest.mark.parametrize("world,windowed,graph", [(2, True, False), (3, True, True), (4, False, True),
+                                                  (3, False, False)])
+def test_peer_memory_exchange_equals_single_context(backend, world, windowed, graph):
+    """The records exchanged through the peer-memory boxes (each shard's
+    record stored into every shard's box, flags released after the records,
+    each shard collecting its own box) instead of the all-gather: the same
+    bits as the single context, eager and in captured halo periods."""
+    T, L, n = 50000, 12, 23
+    truth = P.simulate_rsv(THETA, T, seed=43)
+    data = truth.dataset
+    st0 = P.stream_state(P.make_rng(19, "pcg32"))
+    shards = _shards(data, world, 4 * (L + 1), st0, truth.latent, windowed=windowed)
+    single = backend.chain(data, THETA)
+    single.set_latent(truth.latent)
+    single.set_stream(st0)
+    try:
+        res = S.hmc_update_local_device(shards, 0.02, L, n, graph=graph, p2p=True)
+        res += S.hmc_update_local_device(shards, 0.02, L, 5, p2p=True)  # the boxes' epochs carry over calls
+        ref = single.hmc_update_many(0.02, L, n + 5)
+        assert [bool(x.accept) for x in res] == [bool(x.accept) for x in ref]
+        assert [x.delta_h for x in res] == [x.delta_h for x in ref]
+        h = np.concatenate([c.owned_latent() for c in shards])
+        assert np.array_equal(h, single.get_latent())
+        assert all(int(c.get_stream().pos) == int(single.get_stream().pos) for c in shards)
+    finally:
+        _close(shards)
+
+
+def test_peer_memory_run_chain_matches_single_context(backend):
+    T, L, dt, world = 6000, 20, 0.02, 3
+    truth = P.simulate_rsv(THETA, T, seed=35)
+    data = truth.dataset
+    prior = P.PriorSpec()
+    st0 = P.stream_state(P.make_rng(13, "pcg32"))
+    shards = _shards(data, world, 3 * (L + 1), st0, truth.latent, windowed=True)
+    single = backend.chain(data, THETA)
+    single.set_latent(truth.latent)
+    single.set_params(THETA)
+    single.set_stream(st0)
+    try:
+        it, par, acc, dh = S.run_chain_sharded(shards, dt, L, prior, n_burnin=3, n_samples=12, thin=1, p2p=True)
+        it1, par1, acc1, dh1 = single.run_chain_device(dt, L, False, prior, 3, 12, 1)
+        assert np.array_equal(it, it1)
+        assert np.array_equal(acc, acc1)
+        assert np.allclose(par, par1, rtol=1e-12, atol=0)
+    finally:
+        _close(shards)
