@@ -956,6 +956,7 @@ __global__ void __launch_bounds__(ZE_NT, 1) zig_ens_kernel(EnsChain *E, double *
     const int64_t base = (int64_t)m * ZE_CH;
     for (int e = lane; e < n; e += 32) {
       const int jq = S.qe[m & 3][e], j = jq >> 6, q = jq & 63;
+      RSV_CHECK(j < nch);
       const uint64_t *row = S.ring + j * ZE_RS;
       uint64_t w = row[(base + q) & (ZE_RING - 1)];
       const int idx = (int)(w & 0xff);
@@ -1033,6 +1034,7 @@ __global__ void __launch_bounds__(ZE_NT, 1) zig_ens_kernel(EnsChain *E, double *
     S.vis[m & 1][j] = vis;
     S.n0e[m & 1][j] = (int32_t)n0;
     S.wr[m & 1][j] = m;
+    RSV_CHECK(pos <= 2 * ZE_CH && (used < 0 || (used > base && used <= base + 2 * ZE_CH)));
     if (used >= 0) {
       EnsChain &ec = E[c0 + j];
       const int mc = (int)(used / ZE_CH);
