@@ -583,8 +583,19 @@ def main():
                 cq.hmc_update_many(dt, L, 50, results=False)
                 tq, mq, _ = cq.timing()
                 cq.set_timing(0)
+                # throughput of back-to-back proposals: hmc_update_many without
+                # per-proposal events runs them in graphs of 8 with programmatic
+                # dependent launches (the per-graph gap dominates at small T)
+                nb_ = 400
+                cq.hmc_update_many(dt, L, 16)
+                t0 = time.perf_counter()
+                cq.hmc_update_many(dt, L, nb_)
+                bq = (time.perf_counter() - t0) / nb_ * 1e3
                 sweep.append({"T": Tq, "ms_per_proposal": sq, "traj_kernel_ms": tq, "momenta_ms": mq,
-                              "trajectories_per_s": 1e3 / sq, "site_updates_per_s": Tq * L / (sq * 1e-3)})
+                              "trajectories_per_s": 1e3 / sq, "site_updates_per_s": Tq * L / (sq * 1e-3),
+                              "batched": {"ms_per_proposal": bq, "trajectories_per_s": 1e3 / bq,
+                                          "how": f"one hmc_update_many({nb_}) call, wall clock incl. the result "
+                                                 "copy; proposals in graphs of 8, L2 not flushed"}})
                 be._chains.pop(Tq, None)
                 cq.close()
             extra["sweep"] = sweep

@@ -958,6 +958,11 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   C->stats[1] = r.accept ? C->ends_new[1] : C->ends_old[1];
   for (int k = 0; k < 5; k++) C->stats[2 + k] = sm[k];
   C->res = r;
+  if (A.ring) {  // batched proposals: the result ring (as ring_store_kernel)
+    const int i = *A.ring_count;
+    if (i < A.ring_cap) A.ring[i] = r;
+    *A.ring_count = i + 1;
+  }
 }
 
 // Metropolis step of every chain of an ensemble (sampler.py:155-167 per

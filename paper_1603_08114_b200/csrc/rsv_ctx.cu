@@ -160,6 +160,11 @@ struct rsv_ctx {
     int launches = 0;                 // kernels per launch of the graph
   };
   std::map<GraphKey, Cached *> graphs;
+  // rsv_hmc_update_many without per-proposal timing or L2 flush: one graph of
+  // UPDATE_BATCH proposals (rebuilt when its key, its ring or the parameters change)
+  Cached *batched = nullptr;
+  GraphKey batched_key{};
+  const DevResult *batched_ring = nullptr;
   int timing = 0;  // 0 off, 1 per-proposal total, 2 with momenta / trajectory breakdown
   std::vector<cudaEvent_t> evpool;
   std::vector<double> last_traj_ms, last_mom_ms, last_total_ms;
@@ -224,6 +229,11 @@ int rsv_destroy(rsv_ctx *c) {
       cudaGraphDestroy(kv.second->graph);
       delete kv.second;
     }
+  }
+  if (c->batched) {
+    cudaGraphExecDestroy(c->batched->exec);
+    cudaGraphDestroy(c->batched->graph);
+    delete c->batched;
   }
   if (c->blocks) cudaFree(c->blocks);
   if (c->h_blocks) cudaFreeHost(c->h_blocks);
@@ -423,7 +433,16 @@ int rsv_set_params(rsv_ctx *c, const rsv_params *p) {
 
 // the trajectory reads the derived constants from its parameter block:
 // update the kernel node of every cached graph after a parameter change
+static void drop_batched(rsv_ctx *c) {
+  if (!c->batched) return;
+  cudaGraphExecDestroy(c->batched->exec);
+  cudaGraphDestroy(c->batched->graph);
+  delete c->batched;
+  c->batched = nullptr;
+}
+
 static int refresh_graph_params(rsv_ctx *c) {
+  drop_batched(c);  // its trajectory nodes carry the old constants: rebuilt on demand
   const DevParams &q = *c->h_prm;
   for (auto *m : {&c->graphs, &c->ens_graphs}) {
     for (auto &kv : *m) {
@@ -525,6 +544,7 @@ static MomentaBufs mbufs(rsv_ctx *c) {
 }
 
 static void drop_graphs(rsv_ctx *c) {  // the momenta layout changed: recapture
+  drop_batched(c);
   for (auto &kv : c->graphs) {
     cudaGraphExecDestroy(kv.second->exec);
     cudaGraphDestroy(kv.second->graph);
@@ -783,6 +803,56 @@ static void to_result(const DevResult &d, rsv_result *o) {
   o->u = d.u;
 }
 
+// UPDATE_BATCH proposals as one graph: momenta (a programmatic dependent of
+// the previous trajectory from the second proposal on) and trajectory, the
+// result ring written by the Metropolis step -- no graph-to-graph gap and no
+// ring-store kernel between proposals.
+constexpr int UPDATE_BATCH = 8;
+static int get_batched(rsv_ctx *c, double dt, int n_steps, int fuse, bool results, rsv_ctx::Cached **out) {
+  *out = nullptr;
+  GraphKey k{c->kind, n_steps, fuse ? 1 : 0, 0, 0, dt};
+  const DevResult *ring = results ? c->ring : nullptr;
+  if (c->batched && !(c->batched_key < k) && !(k < c->batched_key) && c->batched_ring == ring) {
+    *out = c->batched;
+    return 0;
+  }
+  drop_batched(c);
+  const TrajGeom g = traj_geometry(c->T, n_steps, c->sm_count, c->variant);
+  if (!g.ok || !variant_is_persistent(g.variant) || getenv("RSV_NO_PDL")) return 0;  // per-proposal graphs
+  if (g.n_tiles > c->max_tiles) return fail(c, RSV_E_CUDA, "tile count %d exceeds buffer", g.n_tiles);
+  auto *cg = new rsv_ctx::Cached();
+  cg->dt = dt;
+  cg->args = traj_args(c, dt, n_steps, fuse, g);
+  cg->args.pdl = 1;
+  cg->args.ring = const_cast<DevResult *>(ring);
+  cg->args.ring_count = ring ? c->ring_count : nullptr;
+  cg->args.ring_cap = ring ? c->ring_cap : 0;
+  cg->traj_node = nullptr;
+  cudaGraph_t graph;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  int l = 0;
+  bool ok = true;
+  for (int j = 0; j < UPDATE_BATCH; j++) {
+    MomentaBufs mb = mbufs(c);
+    mb.pdl = j > 0 ? 1 : 0;
+    ok &= launch_momenta(mb, k.kind, c->Tg, c->stream, &l) == 0;
+    ok &= launch_trajectory(cg->args, c->stream, &l) == 0;
+  }
+  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+  if (!ok || e != cudaSuccess) {
+    delete cg;
+    return fail(c, RSV_E_CUDA, "batched graph capture failed: %s", cudaGetErrorString(e));
+  }
+  cg->graph = graph;
+  cg->launches = l;
+  CK(cudaGraphInstantiate(&cg->exec, graph, 0));
+  c->batched = cg;
+  c->batched_key = k;
+  c->batched_ring = ring;
+  *out = cg;
+  return 0;
+}
+
 int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv_result *out) {
   if (!c) return fail(c, RSV_E_INVALID, "null context");
   int r;
@@ -811,7 +881,16 @@ int rsv_hmc_update_many(rsv_ctx *c, double dt, int n_steps, int fuse, int n, rsv
     if (c->timing == 2) evn = &cg->ev;
     if ((r = ensure_events(c, 4 * (size_t)n + 4))) return r;
   }
+  rsv_ctx::Cached *bg = nullptr;  // batches of UPDATE_BATCH proposals (no per-proposal timing / flush)
+  if (!c->timing && c->flush_bytes == 0 && !c->shard && !c->ens_C && n >= UPDATE_BATCH && !getenv("RSV_NO_BATCH"))
+    if ((r = get_batched(c, dt, n_steps, fuse, out != nullptr, &bg))) return r;
   for (int i = 0; i < n; i++) {
+    if (bg && n - i >= UPDATE_BATCH) {
+      CK(cudaGraphLaunch(bg->exec, c->stream));
+      c->launches += bg->launches;
+      i += UPDATE_BATCH - 1;
+      continue;
+    }
     if (evn) {
       for (int j = 0; j < 4; j++) CK(cudaGraphExecEventRecordNodeSetEvent(exec, (*evn)[j], c->evpool[4 + 4 * i + j]));
     }

@@ -133,6 +133,11 @@ struct TrajArgs {
   // by the theta kernel); null: all constants from the parameter block
   const TrajConsts *kdev;
   int pdl;  // launched as a programmatic dependent of the momenta kernel
+  // batched proposals (rsv_hmc_update_many): the Metropolis step appends its
+  // result to this ring (null: the caller stores it)
+  DevResult *ring;
+  int32_t *ring_count;
+  int ring_cap;
 };
 int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches);
 // ensemble: per-chain sfc64 momenta (numpy SFC64 + ziggurat, one thread per chain)

@@ -530,3 +530,30 @@ def test_contract_violations_raise_like_the_reference(backend):
     st, div = P.integrate_trajectory(P.PhaseState(truth.latent, np.full(64, 1e3)), P.MDConfig(0.5, 5), THETA, data,
                                      backend=backend)
     assert div
+
+
+@pytest.mark.parametrize("T,kind", [(1024, "pcg32"), (70001, "minstd"), (1 << 18, "philox")])
+def test_batched_proposals_equal_one_by_one(backend, T, kind):
+    """rsv_hmc_update_many without per-proposal timing or L2 flush runs the
+    proposals in graphs of 8 (programmatic dependent launches, the result
+    ring written by the Metropolis step): the same bits as proposals
+    launched one by one."""
+    truth = P.simulate_rsv(P.Params(**TRUE), T, seed=5)
+    theta = P.Params(**TRUE)
+    st0 = P.stream_state(P.make_rng(23, kind))
+    other = P.CudaBackend(0)  # a second context (a backend keeps one chain per length)
+    a, b = backend.chain(truth.dataset, theta), other.chain(truth.dataset, theta)
+    assert a is not b
+    for ch in (a, b):
+        ch.set_latent(truth.latent)
+        ch.set_stream(st0)
+    ra = list(a.hmc_update_many(0.02, 20, 20)) + list(a.hmc_update_many(0.02, 20, 9))
+    rb = []
+    for _ in range(29):
+        rb += list(b.hmc_update_many(0.02, 20, 1))
+    assert [bool(x.accept) for x in ra] == [bool(x.accept) for x in rb]
+    assert [x.delta_h for x in ra] == [x.delta_h for x in rb]
+    assert [x.words_used for x in ra] == [x.words_used for x in rb]
+    assert np.array_equal(a.get_latent(), b.get_latent())
+    assert int(a.get_stream().pos) == int(b.get_stream().pos)
+    other.close()
