@@ -165,6 +165,7 @@ struct rsv_ctx {
   Cached *batched = nullptr;
   GraphKey batched_key{};
   const DevResult *batched_ring = nullptr;
+  int batched_ring_cap = 0;
   int timing = 0;  // 0 off, 1 per-proposal total, 2 with momenta / trajectory breakdown
   std::vector<cudaEvent_t> evpool;
   std::vector<double> last_traj_ms, last_mom_ms, last_total_ms;
@@ -812,7 +813,9 @@ static int get_batched(rsv_ctx *c, double dt, int n_steps, int fuse, bool result
   *out = nullptr;
   GraphKey k{c->kind, n_steps, fuse ? 1 : 0, 0, 0, dt};
   const DevResult *ring = results ? c->ring : nullptr;
-  if (c->batched && !(c->batched_key < k) && !(k < c->batched_key) && c->batched_ring == ring) {
+  // (the ring's capacity too: a reallocated ring can come back at the same address)
+  if (c->batched && !(c->batched_key < k) && !(k < c->batched_key) && c->batched_ring == ring &&
+      c->batched_ring_cap == (ring ? c->ring_cap : 0)) {
     *out = c->batched;
     return 0;
   }
@@ -849,6 +852,7 @@ static int get_batched(rsv_ctx *c, double dt, int n_steps, int fuse, bool result
   c->batched = cg;
   c->batched_key = k;
   c->batched_ring = ring;
+  c->batched_ring_cap = ring ? c->ring_cap : 0;
   *out = cg;
   return 0;
 }

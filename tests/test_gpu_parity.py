@@ -547,9 +547,11 @@ def test_batched_proposals_equal_one_by_one(backend, T, kind):
     for ch in (a, b):
         ch.set_latent(truth.latent)
         ch.set_stream(st0)
-    ra = list(a.hmc_update_many(0.02, 20, 20)) + list(a.hmc_update_many(0.02, 20, 9))
+    # the third call grows the result ring (the batched graph must follow it)
+    ra = (list(a.hmc_update_many(0.02, 20, 20)) + list(a.hmc_update_many(0.02, 20, 9))
+          + list(a.hmc_update_many(0.02, 20, 40)))
     rb = []
-    for _ in range(29):
+    for _ in range(69):
         rb += list(b.hmc_update_many(0.02, 20, 1))
     assert [bool(x.accept) for x in ra] == [bool(x.accept) for x in rb]
     assert [x.delta_h for x in ra] == [x.delta_h for x in rb]
