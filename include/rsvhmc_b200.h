@@ -225,8 +225,8 @@ int rsv_shard_place_async(rsv_ctx *ctx, const double *gathered_records_dev, int 
  * totals, 8: window records) every shard calls rsv_shard_p2p_push_async
  * with its own record, then rsv_shard_p2p_collect_async, which waits for
  * every shard's record of this exchange (flags written with release
- * semantics after the record; a missing peer raises an error after 5 s
- * instead of hanging) and copies the records out in rank order -- the
+ * semantics after the record; a missing peer raises an error after 5 s,
+ * RSV_P2P_TIMEOUT_MS, instead of hanging) and copies the records out in rank order -- the
  * layout the all-gather produced, so rsv_shard_decide_async /
  * rsv_shard_place_async read it unchanged.  Shards of one process push all
  * before any of them collects. */

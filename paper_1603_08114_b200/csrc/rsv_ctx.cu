@@ -109,6 +109,7 @@ struct rsv_ctx {
   P2PBox **p2p_peers = nullptr;      // device array: every shard's box, as this device sees it
   std::vector<void *> p2p_opened;    // boxes opened from IPC handles (closed on destroy)
   int p2p_world = 0, p2p_rank = 0;
+  unsigned long long p2p_timeout_ns = 5000000000ull;  // RSV_P2P_TIMEOUT_MS (read at rsv_shard_p2p_init)
   int64_t win_wb0 = 0, win_nb = 0, win_cap = 0, win_a_lo = 0, win_a_hi = -1;
   double *win_out = nullptr;
   uint32_t *win_nend = nullptr;
@@ -1914,7 +1915,8 @@ __device__ __forceinline__ unsigned long long p2p_ld_acquire(const unsigned long
   return v;
 }
 
-__global__ void p2p_collect_kernel(DevControl *C, const P2PBox *box, int world, int kind, int words, double *out) {
+__global__ void p2p_collect_kernel(DevControl *C, const P2PBox *box, int world, int kind, int words, double *out,
+                                   unsigned long long timeout_ns) {
   const int q = threadIdx.x;
   const unsigned long long e = C->p2p_seq[kind];  // my own push of this exchange came first on the stream
   if (q < world) {
@@ -1922,7 +1924,7 @@ __global__ void p2p_collect_kernel(DevControl *C, const P2PBox *box, int world, 
     const unsigned long long t0 = gtimer_ns();
     bool ok = true;
     while (p2p_ld_acquire(f) != e) {
-      if (gtimer_ns() - t0 > 5000000000ull) {  // 5 s: a peer is gone; flagged, never a hang
+      if (gtimer_ns() - t0 > timeout_ns) {  // (5 s) a peer is gone: flagged, never a hang
         ok = false;
         break;
       }
@@ -1951,6 +1953,8 @@ int rsv_shard_p2p_init(rsv_ctx *c, int world, int rank, unsigned char *handle, u
   if (box_dev) *box_dev = (uint64_t)(uintptr_t)c->p2p_box;
   c->p2p_world = world;
   c->p2p_rank = rank;
+  const char *to = getenv("RSV_P2P_TIMEOUT_MS");
+  c->p2p_timeout_ns = (to && atoll(to) > 0 ? (unsigned long long)atoll(to) : 5000ull) * 1000000ull;
   return 0;
 }
 
@@ -1997,7 +2001,7 @@ int rsv_shard_p2p_collect_async(rsv_ctx *c, double *out_dev, int words) {
   if (words != SHARD_W && words != (int)(sizeof(WinInfo) / 8)) return fail(c, RSV_E_INVALID, "bad record size");
   CK(cudaSetDevice(c->device));
   p2p_collect_kernel<<<1, 32, 0, c->stream>>>(c->ctrl, c->p2p_box, c->p2p_world, words == SHARD_W ? 0 : 1, words,
-                                             out_dev);
+                                             out_dev, c->p2p_timeout_ns);
   c->launches++;
   CK(cudaGetLastError());
   return 0;

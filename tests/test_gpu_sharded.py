@@ -209,3 +209,26 @@ def test_peer_memory_run_chain_matches_single_context(backend):
         assert np.allclose(par, par1, rtol=1e-12, atol=0)
     finally:
         _close(shards)
+
+
+def test_peer_memory_missing_peer_is_an_error_not_a_hang(backend, monkeypatch):
+    """A shard whose peer never publishes its record: the collect kernel
+    gives up after RSV_P2P_TIMEOUT_MS and the next result read raises
+    (bench.py then falls back to NCCL on every rank)."""
+    monkeypatch.setenv("RSV_P2P_TIMEOUT_MS", "50")
+    truth = P.simulate_rsv(THETA, 4000, seed=3)
+    st0 = P.stream_state(P.make_rng(1, "pcg32"))
+    shards = _shards(truth.dataset, 2, 63, st0, truth.latent)
+    try:
+        comm = S._LocalP2PComm(shards)
+        import torch
+        rec = torch.zeros(S.TOTALS, dtype=torch.float64, device="cuda")
+        out = torch.zeros((2, S.TOTALS), dtype=torch.float64, device="cuda")
+        c0 = shards[0].shard
+        c0._ck(c0._lib.rsv_shard_p2p_push_async(c0.ctx, rec.data_ptr(), S.TOTALS))  # shard 1 never pushes
+        c0._ck(c0._lib.rsv_shard_p2p_collect_async(c0.ctx, out.data_ptr(), S.TOTALS))
+        with pytest.raises(P._native.NativeError, match="peer"):
+            S._results(shards[0], 1)
+        assert comm.world == 2
+    finally:
+        _close(shards)
