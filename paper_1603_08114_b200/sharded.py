@@ -461,10 +461,17 @@ class _NcclComm:
         for q in dist.batch_isend_irecv(ops) if ops else []:
             q.wait()  # orders the copies on the current stream (no host block)
 
+    def _device(self):
+        """Where the group's collectives take their tensors (NCCL: the GPU; gloo: the host)."""
+        import torch
+        if self.dist.get_backend(self.group) == "nccl":
+            return torch.device("cuda", torch.cuda.current_device())
+        return torch.device("cpu")
+
     def agree(self, ok: bool) -> bool:
         """True on every rank iff true on every rank (eager, outside any capture)."""
         import torch
-        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=torch.cuda.current_device())
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=self._device())
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
         return bool(t.item())
 
@@ -519,7 +526,7 @@ class _P2PComm(_NcclComm):
         handle = (ctypes.c_ubyte * 64)()
         box = ctypes.c_uint64()
         ok = lib.rsv_shard_p2p_init(ctx, self.world, self.rank, handle, ctypes.byref(box)) == 0
-        dev = torch.device("cuda", torch.cuda.current_device())
+        dev = self._device()
         mine = torch.tensor([1 if ok else 0] + list(bytes(handle)), dtype=torch.uint8, device=dev)
         every = torch.empty(self.world * 65, dtype=torch.uint8, device=dev)
         self.dist.all_gather_into_tensor(every, mine, group=group)

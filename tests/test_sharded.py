@@ -165,3 +165,67 @@ def test_halo_period_keeps_owned_sites_exact():
     assert halo_period(42, 12) == 2
     with pytest.raises(ValueError):
         halo_period(30, 20)
+
+
+class _FakeP2PLib:
+    """Stand-in for the peer-memory entry points (rank `fail_rank` cannot
+    allocate / map): exercises the collective, agreed set-up of
+    sharded._P2PComm on CPU ranks."""
+
+    def __init__(self, rank, fail_rank, fail_at):
+        self.rank, self.fail_rank, self.fail_at = rank, fail_rank, fail_at
+        self.connected_with = None
+
+    def rsv_shard_p2p_init(self, ctx, world, rank, handle, box):
+        if self.rank == self.fail_rank and self.fail_at == "init":
+            return -2
+        for i in range(64):
+            handle[i] = (rank * 64 + i) % 256
+        return 0
+
+    def rsv_shard_p2p_connect(self, ctx, handles, boxes):
+        if self.rank == self.fail_rank and self.fail_at == "connect":
+            return -2
+        self.connected_with = bytes(handles)
+        return 0
+
+
+def _p2p_worker(rank, world, port, fail_rank, fail_at, q):
+    import types
+    import torch.distributed as dist
+    from paper_1603_08114_b200 import sharded as S
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lib = _FakeP2PLib(rank, fail_rank, fail_at)
+    chain = types.SimpleNamespace(rank=rank, world=world, shard=types.SimpleNamespace(_lib=lib, ctx=None))
+    comm = S._comm_for([chain], dist.group.WORLD, True)
+    q.put((rank, type(comm).__name__, lib.connected_with))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank,fail_at", [(-1, None), (1, "init"), (0, "connect")])
+def test_gloo_peer_memory_setup_is_agreed(fail_rank, fail_at):
+    """Every rank takes the peer-memory exchange only if every rank could
+    allocate its box and map every peer's; otherwise every rank falls back
+    to the NCCL exchange (none is left waiting in a collective)."""
+    import torch.multiprocessing as mp
+    world = 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, fail_rank, fail_at, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict((r, (kind, hb)) for r, kind, hb in (q.get(timeout=300) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = "_P2PComm" if fail_rank < 0 else "_NcclComm"
+    assert [out[r][0] for r in range(world)] == [want] * world
+    if fail_rank < 0:  # every rank received every rank's handle, in rank order
+        every = bytes((r * 64 + i) % 256 for r in range(world) for i in range(64))
+        assert all(out[r][1] == every for r in range(world))
