@@ -40,10 +40,11 @@ L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 # algorithmic FP64 work of one site-update of the leapfrog (DESIGN.md 4.2,
 # SURVEY 8d): 2 half drifts (2 FMA), the kick (3 FMA + 2 ADD) and e^{-d}
 # (a degree-3 polynomial after range reduction: 4 FMA-class + 3 ADD +
-# rounding) -- counted as 26 flops.  The kernel issues 14 FP64 instructions
-# per site-update for them (scaled-state exp: 3 DADD + 3 DFMA/DMUL + 1 DFMA).
+# rounding) -- counted as 26 flops.  The kernel issues 13 FP64 instructions
+# per site-update for them (one full drift between kicks, the kick, and the
+# scaled-state exp: 3 DADD + 3 DFMA/DMUL + 1 DFMA).
 FLOPS_PER_SITE_UPDATE = 26
-FP64_INSTR_PER_SITE_UPDATE = 14  # DFMA-pipe instructions (FMA, ADD, MUL each one issue slot)
+FP64_INSTR_PER_SITE_UPDATE = 13  # DFMA-pipe instructions (FMA, ADD, MUL each one issue slot)
 HBM_BYTES_PER_SITE = 48  # streamed elementary step: r h,p,(y/2)y,lnRV; w h,p
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
