@@ -532,7 +532,7 @@ def test_contract_violations_raise_like_the_reference(backend):
     assert div
 
 
-@pytest.mark.parametrize("T,kind", [(1024, "pcg32"), (70001, "minstd"), (1 << 18, "philox")])
+@pytest.mark.parametrize("T,kind", [(1024, "pcg32"), (70001, "minstd"), (1 << 18, "philox"), (3001, "sfc64")])
 def test_batched_proposals_equal_one_by_one(backend, T, kind):
     """rsv_hmc_update_many without per-proposal timing or L2 flush runs the
     proposals in graphs of 8 (programmatic dependent launches, the result
@@ -554,6 +554,33 @@ def test_batched_proposals_equal_one_by_one(backend, T, kind):
     for _ in range(69):
         rb += list(b.hmc_update_many(0.02, 20, 1))
     assert [bool(x.accept) for x in ra] == [bool(x.accept) for x in rb]
+    assert [x.delta_h for x in ra] == [x.delta_h for x in rb]
+    assert [x.words_used for x in ra] == [x.words_used for x in rb]
+    assert np.array_equal(a.get_latent(), b.get_latent())
+    assert int(a.get_stream().pos) == int(b.get_stream().pos)
+    other.close()
+
+
+def test_batched_divergent_proposals_equal_one_by_one(backend):
+    """Batches whose proposals all diverge (no uniform drawn, sampler.py:157-158)
+    between batches that accept: stream positions and paths stay those of
+    proposals launched one by one."""
+    truth = P.simulate_rsv(P.Params(**TRUE), 2048, seed=5)
+    theta = P.Params(**TRUE)
+    st0 = P.stream_state(P.make_rng(23, "pcg32"))
+    other = P.CudaBackend(0)
+    a, b = backend.chain(truth.dataset, theta), other.chain(truth.dataset, theta)
+    for ch in (a, b):
+        ch.set_latent(truth.latent)
+        ch.set_stream(st0)
+    plan = [(0.02, 16), (0.3, 9), (0.02, 8), (0.6, 8), (0.02, 11)]
+    ra, rb = [], []
+    for dt, n in plan:
+        ra += list(a.hmc_update_many(dt, 20, n))
+        for _ in range(n):
+            rb += list(b.hmc_update_many(dt, 20, 1))
+    assert sum(bool(x.diverged) for x in ra) >= 17 and sum(bool(x.accept) for x in ra) > 0
+    assert [(bool(x.accept), bool(x.diverged)) for x in ra] == [(bool(x.accept), bool(x.diverged)) for x in rb]
     assert [x.delta_h for x in ra] == [x.delta_h for x in rb]
     assert [x.words_used for x in ra] == [x.words_used for x in rb]
     assert np.array_equal(a.get_latent(), b.get_latent())
