@@ -1493,22 +1493,34 @@ __device__ __forceinline__ double rec_unfix(__int128 q) {  // as unfix128 in lea
 // are recorded.
 __global__ void shard_decide_kernel(DevControl *C, const ShardRec *g, int world, const DevParams *prm,
                                     const uint64_t *snaps, DevResult *ring, int cap, int32_t *count, int windowed) {
-  if (threadIdx.x || blockIdx.x) return;
-  if (C->halt) return;  // sharded run_chain stopped at an earlier sweep
-  __int128 q0 = 0, q1 = 0, q2 = 0;
-  double fl = 0.0;
-  double S[14];  // moments old 0..4, new 5..9, ends 10..13
-  for (int k = 0; k < 14; k++) {
+  if (threadIdx.x >= 32 || blockIdx.x) return;
+  const int lane = threadIdx.x;
+  // every control word of the step is loaded up front: a value written and
+  // read back through device memory would cost an L2 round trip each time
+  const int halt = C->halt;
+  const StreamState st = C->stream;
+  const uint64_t seq = C->seq_state;
+  const int cur = C->cur;
+  const double hconst = prm->hconst;
+  const int i_ring = ring ? *count : 0;
+  if (halt) return;  // sharded run_chain stopped at an earlier sweep
+  // lane k < 14: moment / end sum k over the ranks in rank order (TwoSum):
+  // old moments 0..4, new 5..9, ends 10..13
+  double Sk = 0.0;
+  if (lane < 14) {
     double sum = 0.0, comp = 0.0;
-    for (int r = 0; r < world; r++) {  // TwoSum accumulation
-      const double x = k < 5 ? g[r].part.so[k] : k < 10 ? g[r].part.sn[k - 5] : g[r].ends[k - 10];
+    for (int r = 0; r < world; r++) {
+      const double x = lane < 5 ? g[r].part.so[lane] : lane < 10 ? g[r].part.sn[lane - 5] : g[r].ends[lane - 10];
       const double t = sum + x;
       const double bp = t - sum;
       comp += (sum - (t - bp)) + (x - bp);
       sum = t;
     }
-    S[k] = sum + comp;
+    Sk = sum + comp;
   }
+  // every lane: the exact fixed-point totals and the decision (same values)
+  __int128 q0 = 0, q1 = 0, q2 = 0;
+  double fl = 0.0;
   for (int r = 0; r < world; r++) {
     q0 += rec128(g[r].part.dh);
     q1 += rec128(g[r].part.hold);
@@ -1519,20 +1531,15 @@ __global__ void shard_decide_kernel(DevControl *C, const ShardRec *g, int world,
   // (replicated) -- then all records must agree -- or the last shard's
   // window holds the draw's end (windowed); either way the last record
   const uint64_t u_word = g[world - 1].u_word;
-  if (!windowed) {
+  const uint64_t used = g[world - 1].words_used;
+  if (!windowed && lane == 0) {
     bool consistent = true;
-    for (int r = 0; r < world - 1; r++) consistent &= g[r].u_word == u_word && g[r].words_used == g[world - 1].words_used;
+    for (int r = 0; r < world - 1; r++) consistent &= g[r].u_word == u_word && g[r].words_used == used;
     if (!consistent) atomicOr(&C->err, 8);
   }
-  C->zig_used = g[world - 1].words_used;
-  {
-    const StreamState &st = C->stream;
-    if (st.kind == PRNG_PCG32) C->seq_next = pcg_advance(st.s[0], 2 * (st.pos + C->zig_used), st.s[1]);
-    else if (st.kind == PRNG_MINSTD) C->seq_next = mod31(minstd_pow(3 * (st.pos + C->zig_used)) * st.s[0]);
-  }
   DevResult res;
-  res.h_old = rec_unfix(q1) + prm->hconst;
-  res.h_new = rec_unfix(q2) + prm->hconst;
+  res.h_old = rec_unfix(q1) + hconst;
+  res.h_new = rec_unfix(q2) + hconst;
   res.accept = 0;
   res.u = __longlong_as_double(0x7ff8000000000000LL);
   const double dh = rec_unfix(q0);
@@ -1547,17 +1554,40 @@ __global__ void shard_decide_kernel(DevControl *C, const ShardRec *g, int world,
     drew = true;
     res.accept = (dh <= 0.0) || (res.u < exp(-dh));
   }
-  res.words_used = C->zig_used + (drew ? 1 : 0);
-  shard_advance(C, drew, snaps);
-  if (res.accept) C->cur ^= 1;
-  C->stats[0] = res.accept ? S[12] : S[10];
-  C->stats[1] = res.accept ? S[13] : S[11];
-  for (int k = 0; k < 5; k++) C->stats[2 + k] = res.accept ? S[5 + k] : S[k];
+  res.words_used = used + (drew ? 1 : 0);
+  // statistics of the kept path (lane k holds sum k)
+  if (res.accept) {
+    if (lane == 12 || lane == 13) C->stats[lane - 12] = Sk;
+    if (lane >= 5 && lane < 10) C->stats[2 + lane - 5] = Sk;
+  } else {
+    if (lane == 10 || lane == 11) C->stats[lane - 10] = Sk;
+    if (lane < 5) C->stats[2 + lane] = Sk;
+  }
+  if (lane) return;
+  // the stream after the momenta (and the uniform, if drawn): from the state
+  // at the proposal's stream position, advanced by the words used
+  C->zig_used = used;
+  if (st.kind == PRNG_SFC64) {
+    shard_advance(C, drew, snaps);
+  } else {
+    uint64_t q = seq;
+    if (st.kind == PRNG_PCG32) {
+      q = pcg_advance(seq, 2 * used, st.s[1]);
+      C->seq_next = q;
+      if (drew) { q = q * PCG_MULT + st.s[1]; q = q * PCG_MULT + st.s[1]; }
+    } else if (st.kind == PRNG_MINSTD) {
+      q = mod31(minstd_pow(3 * used) * seq);
+      C->seq_next = q;
+      if (drew) q = mod31(mod31(mod31(q * MINSTD_A) * MINSTD_A) * MINSTD_A);
+    }
+    C->seq_state = q;
+    C->stream.pos = st.pos + used + (drew ? 1 : 0);
+  }
+  if (res.accept) C->cur = cur ^ 1;
   C->res = res;
   if (ring) {
-    const int i = *count;
-    if (i < cap) ring[i] = res;
-    *count = i + 1;
+    if (i_ring < cap) ring[i_ring] = res;
+    *count = i_ring + 1;
   }
 }
 
@@ -1721,7 +1751,7 @@ int rsv_shard_decide_async(rsv_ctx *c, const double *gathered_dev, int world) {
     CK(cudaMallocHost(&c->h_ring, sizeof(DevResult) * c->ring_cap));
     CK(cudaMemsetAsync(c->ring_count, 0, sizeof(int32_t), c->stream));
   }
-  shard_decide_kernel<<<1, 1, 0, c->stream>>>(c->ctrl, reinterpret_cast<const ShardRec *>(gathered_dev), world,
+  shard_decide_kernel<<<1, 32, 0, c->stream>>>(c->ctrl, reinterpret_cast<const ShardRec *>(gathered_dev), world,
                                               c->prm, c->sfc_snaps, c->ring, c->ring_cap, c->ring_count,
                                               c->win_mode && !c->blocks ? 1 : 0);
   c->launches++;
