@@ -872,8 +872,17 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
     if (threadIdx.x) return;
     for (int k = 0; k < 5; k++) tp.so[k] = tp.sn[k] = 0.0;
   }
-  // the fixed-point totals (acquired with the CTA count), then cleared for
-  // the next launch
+  // every control word the decision needs, loaded in one round with the
+  // fixed-point totals (acquired with the CTA count; a value first read after
+  // the branches below would cost an L2 round trip each)
+  DevControl *C = A.ctrl;
+  const int halt = C->halt, cur = C->cur, kind = C->stream.kind;
+  const uint64_t used = C->zig_used, u_word = C->u_word, seq_next = C->seq_next;
+  const uint64_t pos = C->stream.pos, inc = C->stream.s[1];
+  const double e_old0 = C->ends_old[0], e_old1 = C->ends_old[1], e_new0 = C->ends_new[0], e_new1 = C->ends_new[1];
+  const int ring_i = A.ring ? *A.ring_count : 0;
+  const double cst = A.kdev ? A.kdev->hconst : A.k.hconst;
+  // the fixed-point totals, then cleared for the next launch
   unsigned long long *fx = A.ctrl->fx;
   const __int128 a0 = fx_total(fx + 0), a1 = fx_total(fx + 3), a2 = fx_total(fx + 6);
   tp.flag = fx[9] ? 1.0 : 0.0;
@@ -888,16 +897,14 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   tot[2] = unfix128(a2);
   for (int k = 0; k < 5; k++) { tot[3 + k] = tp.so[k]; tot[8 + k] = tp.sn[k]; }
   tot[13] = tp.flag;
-  DevControl *C = A.ctrl;
   C->tiles_done = 0;  // re-arm for the next launch
   C->tile_next = 0;
   C->t_stamp[3] = gtimer();
-  if (C->halt) return;  // rsv_run_chain stopped at an earlier sweep: stream, path and statistics untouched
+  if (halt) return;  // rsv_run_chain stopped at an earlier sweep: stream, path and statistics untouched
   if (A.shard) {  // time-sharded chain: the shards' records are combined by the decision
     *reinterpret_cast<TilePart *>(C->shard_parts) = tp;
     return;
   }
-  const double cst = A.kdev ? A.kdev->hconst : A.k.hconst;
   DevResult r;
   r.h_old = tot[1] + cst;
   r.h_new = tot[2] + cst;
@@ -914,7 +921,6 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
     C->res = r;
     return;
   }
-  const uint64_t used = C->zig_used;
   bool drew = false;
   const double dh = tot[0];
   if (flagged || !isfinite(dh) || fabs(dh) > 1000.0) {
@@ -923,38 +929,37 @@ __device__ void metropolis_n(const TrajArgs &A, double *s_v, int n_parts) {
   } else {
     r.diverged = 0;
     r.delta_h = dh;
-    r.u = u01(C->u_word);  // raw word at stream position pos0 + used (momenta kernel)
+    r.u = u01(u_word);  // raw word at stream position pos0 + used (momenta kernel)
     drew = true;
     r.accept = (dh <= 0.0) || (r.u < exp(-dh));
   }
   const uint64_t consumed = used + (drew ? 1 : 0);
   r.words_used = consumed;
-  if (C->stream.kind == PRNG_SFC64) {
+  if (kind == PRNG_SFC64) {
     const uint64_t *q = A.sfc_snaps + 4 * (consumed / SFC_SNAP);
     uint64_t st[4] = {q[0], q[1], q[2], q[3]};
     for (uint64_t i = 0; i < consumed % SFC_SNAP; i++) sfc64_next(st);
     for (int i = 0; i < 4; i++) C->stream.s[i] = st[i];
   }
-  C->stream.pos += consumed;
-  if (C->stream.kind == PRNG_PCG32) {
-    uint64_t q = C->seq_next;
-    if (drew) { q = q * PCG_MULT + C->stream.s[1]; q = q * PCG_MULT + C->stream.s[1]; }
+  C->stream.pos = pos + consumed;
+  if (kind == PRNG_PCG32) {
+    uint64_t q = seq_next;
+    if (drew) { q = q * PCG_MULT + inc; q = q * PCG_MULT + inc; }
     C->seq_state = q;
-  } else if (C->stream.kind == PRNG_MINSTD) {
-    uint64_t q = C->seq_next;
+  } else if (kind == PRNG_MINSTD) {
+    uint64_t q = seq_next;
     if (drew) q = mod31(mod31(mod31(q * MINSTD_A) * MINSTD_A) * MINSTD_A);
     C->seq_state = q;
   }
-  if (r.accept) C->cur ^= 1;
+  if (r.accept) C->cur = cur ^ 1;
   const double *sm = r.accept ? tot + 8 : tot + 3;
-  C->stats[0] = r.accept ? C->ends_new[0] : C->ends_old[0];
-  C->stats[1] = r.accept ? C->ends_new[1] : C->ends_old[1];
+  C->stats[0] = r.accept ? e_new0 : e_old0;
+  C->stats[1] = r.accept ? e_new1 : e_old1;
   for (int k = 0; k < 5; k++) C->stats[2 + k] = sm[k];
   C->res = r;
   if (A.ring) {  // batched proposals: the result ring (as ring_store_kernel)
-    const int i = *A.ring_count;
-    if (i < A.ring_cap) A.ring[i] = r;
-    *A.ring_count = i + 1;
+    if (ring_i < A.ring_cap) A.ring[ring_i] = r;
+    *A.ring_count = ring_i + 1;
   }
 }
 
