@@ -1176,13 +1176,27 @@ __global__ void __launch_bounds__(TH_NT) theta_sweep_kernel(DevControl *C, DevPa
     s_wi[i] = g_wi[i];
     s_fi[i] = g_fi[i];
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   // warp 0 runs the draws, every lane on the same values (theta_dev.cuh:
   // lane-parallel transcendentals); the identical stores of its lanes merge
   if (threadIdx.x >= 32 || blockIdx.x) return;
   (void)sfc_snaps;
-  theta_sweep_body(C, P, K, R, pr, dt, T, s_ki, s_wi, s_fi);
+  // while the trajectory kernel finishes: the draws at the position the
+  // proposal will most likely leave the stream at -- after the momenta's
+  // words (seq_next, written by the momenta kernel) and the uniform; the
+  // chain checks the actual state before it uses any of them
+  ThetaSpec sp;
+  const int kind = C->stream.kind;
+  const bool speculate = kind == PRNG_PCG32 || kind == PRNG_MINSTD;
+  if (speculate) {
+    const uint64_t inc = C->stream.s[1];
+    uint64_t q = C->seq_next;
+    if (kind == PRNG_PCG32) { q = q * PCG_MULT + inc; q = q * PCG_MULT + inc; }
+    else q = mod31(mod31(mod31(q * MINSTD_A) * MINSTD_A) * MINSTD_A);
+    theta_spec_fill(sp, kind, q, inc, __dadd_rn(pr.var_shape, __dmul_rn(0.5, (double)T)), s_ki, s_wi, s_fi);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  theta_sweep_body(C, P, K, R, pr, dt, T, s_ki, s_wi, s_fi, speculate ? &sp : nullptr);
 }
 
 int launch_theta_sweep(DevControl *ctrl, DevParams *prm, TrajConsts *kdev, DevRun *run, DevPrior prior, double dt,

@@ -25,6 +25,20 @@ static __device__ __noinline__ double log1p_ool(double x) { return glibc_log1p(x
 static __device__ __noinline__ double log_ool(double x) { return log(x); }
 static __device__ __noinline__ double exp_ool(double x) { return exp(x); }
 
+// Speculative draws of a sweep's theta chain (pcg32 / minstd): lane j holds
+// the normal, the gamma(shape) draw and the raw word that start at word j
+// after the position the proposal is predicted to leave the stream at (its
+// uniform drawn).  Filled while the trajectory kernel finishes; used only if
+// the generator state there is the predicted one, so the draws are the same
+// numbers on the same words -- the chain only looks them up.
+struct ThetaSpec {
+  uint64_t state;  // predicted generator state at window word 0
+  double shape;
+  double nval, gval;
+  int nlen, glen;
+  uint64_t word;
+};
+
 struct ThetaGen {
   int kind;
   SeqGen g;
@@ -32,12 +46,34 @@ struct ThetaGen {
   uint64_t used;
   const uint64_t *ki;  // ziggurat tables (shared-memory copies)
   const double *wi, *fi;
+  bool spec;             // draws served from *sp while `used` stays inside its window
+  const ThetaSpec *sp;
+  uint64_t seq0, inc;    // pcg32 / minstd: state at word 0 (for leaving the window)
+  __device__ __noinline__ void unspec() {  // the sequential generator at word `used`
+    spec = false;
+    g.a = kind == PRNG_PCG32 ? pcg_advance(seq0, 2 * used, inc) : mod31(minstd_pow(3 * used) * seq0);
+    g.b = inc;
+  }
   __device__ __noinline__ uint64_t next() {
+    if (spec) unspec();
     used++;
     return kind == PRNG_SFC64 ? sfc64_next(s) : g.next();
   }
-  __device__ double next_double() { return u01(next()); }
+  __device__ double next_double() {
+    if (spec && used < 32) {
+      const uint64_t w = __shfl_sync(0xffffffffu, sp->word, (int)used);
+      used++;
+      return u01(w);
+    }
+    return u01(next());
+  }
   __device__ __noinline__ double normal() {  // numpy random_standard_normal
+    if (spec && used < 32) {
+      const int len = __shfl_sync(0xffffffffu, sp->nlen, (int)used);
+      const double v = __shfl_sync(0xffffffffu, sp->nval, (int)used);
+      used += (uint64_t)len;
+      return v;
+    }
     for (;;) {
       uint64_t r = next();
       const int idx = (int)(r & 0xff);
@@ -62,6 +98,12 @@ struct ThetaGen {
     }
   }
   __device__ __noinline__ double gamma(double shape) {  // numpy random_standard_gamma, shape > 1
+    if (spec && used < 32 && shape == sp->shape) {
+      const int len = __shfl_sync(0xffffffffu, sp->glen, (int)used);
+      const double v = __shfl_sync(0xffffffffu, sp->gval, (int)used);
+      used += (uint64_t)len;
+      return v;
+    }
     const double b = __dsub_rn(shape, 1.0 / 3.0);
     const double c = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(9.0, b)));
     for (;;) {
@@ -79,6 +121,40 @@ struct ThetaGen {
     }
   }
 };
+
+// Every lane: the draws that would start at word `lane` after `state`
+// (computed with the same functions the chain uses, so the same bits).
+static __device__ __noinline__ void theta_spec_fill(ThetaSpec &sp, int kind, uint64_t state, uint64_t inc,
+                                                    double shape, const uint64_t *ki, const double *wi,
+                                                    const double *fi) {
+  const uint64_t lane = threadIdx.x & 31;
+  sp.state = state;
+  sp.shape = shape;
+  const uint64_t st_l =
+      kind == PRNG_PCG32 ? pcg_advance(state, 2 * lane, inc) : mod31(minstd_pow(3 * lane) * state);
+  ThetaGen g;
+  g.kind = kind;
+  g.ki = ki;
+  g.wi = wi;
+  g.fi = fi;
+  g.spec = false;
+  g.sp = nullptr;
+  g.seq0 = st_l;
+  g.inc = inc;
+  g.g.kind = kind;
+  g.g.k = 0;
+  g.g.a = st_l;
+  g.g.b = inc;
+  SeqGen w = g.g;
+  sp.word = w.next();
+  g.used = 0;
+  sp.nval = g.normal();
+  sp.nlen = (int)g.used;
+  g.g.a = st_l;
+  g.used = 0;
+  sp.gval = g.gamma(shape);
+  sp.glen = (int)g.used;
+}
 
 // _recentre (sampler.py mirror): moments of d' = h - mu from d = h - c
 struct Recentred {
@@ -126,7 +202,7 @@ static __device__ double phi_log_ratio(double prop, double phi, double h1_sq, do
 // the ziggurat tables (shared-memory copies).
 static __device__ __noinline__ void theta_sweep_body(DevControl *C, DevParams *P, TrajConsts *K, DevRun *R,
                                                      const DevPrior &pr, double dt, int64_t T, const uint64_t *ki,
-                                                     const double *wi, const double *fi) {
+                                                     const double *wi, const double *fi, const ThetaSpec *sp) {
   // every input in one round of independent loads (one thread: each load
   // issued on its own would cost a full memory latency on the critical path)
   const int halt = C->halt;
@@ -169,6 +245,10 @@ static __device__ __noinline__ void theta_sweep_body(DevControl *C, DevParams *P
   G.ki = ki;
   G.wi = wi;
   G.fi = fi;
+  G.spec = false;
+  G.sp = sp;
+  G.seq0 = seq0;
+  G.inc = ss.s[1];
   if (G.kind == PRNG_SFC64) {
     for (int k = 0; k < 4; k++) G.s[k] = ss.s[k];
   } else if (G.kind == PRNG_PHILOX) {
@@ -178,6 +258,7 @@ static __device__ __noinline__ void theta_sweep_body(DevControl *C, DevParams *P
     G.g.k = ss.pos;
     G.g.a = seq0;
     G.g.b = ss.s[1];
+    G.spec = sp != nullptr && sp->state == seq0;  // the position the speculation assumed
   }
   const double Td = (double)T, Tm1 = Td - 1.0;
   double phi = P0.phi, mu = P0.mu, xi = P0.xi, se2 = P0.se2, su2 = P0.su2;
@@ -250,6 +331,7 @@ static __device__ __noinline__ void theta_sweep_body(DevControl *C, DevParams *P
   }
   // the stream continues after the draws (those made before a degenerate
   // precision included: the reference raises after them, sampler.py:186,200)
+  if (G.spec) G.unspec();  // the generator state after the last draw
   C->stream.pos = ss.pos + G.used;
   if (G.kind == PRNG_SFC64)
     for (int k = 0; k < 4; k++) C->stream.s[k] = G.s[k];
