@@ -515,15 +515,36 @@ def main():
     h_host[:] = truth.latent
     h = h_host
     for _ in range(max(3, args.warmup)):  # warm: graph, pinned result buffers
-        h, _, _ = P.hmc_update_volatility(h, theta, data, md, rng, backend=be)
+        h, _, _ = P.hmc_update_volatility(h.view(), theta, data, md, rng, backend=be)
     e2e_steps = max(3, min(args.steps, 20))
     n_acc = 0
+    # the path crosses the link every step: a view of the returned array is
+    # not the chain's own returned path, so it is read from host memory again
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        h, acc, _ = P.hmc_update_volatility(h, theta, data, md, rng, backend=be)
+        h, acc, _ = P.hmc_update_volatility(h.view(), theta, data, md, rng, backend=be)
         n_acc += int(acc)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    zero_copy = be.chain(data, theta).last_update_zero_copy  # h read in place by the trajectory kernel
+    ch_e2e = be.chain(data, theta)
+    zero_copy = ch_e2e.last_update_zero_copy  # h read in place by the trajectory kernel
+    assert not ch_e2e.last_update_resident
+    # a chain loop passing the returned path straight back (the reference's
+    # run_chain does): the device keeps the path, only the stream state goes
+    # in and an accepted proposal comes out
+    hr = h
+    for _ in range(400):  # until a returned path is in hand (an accepted proposal)
+        if not hr.flags.writeable:
+            break
+        hr, _, _ = P.hmc_update_volatility(hr, theta, data, md, rng, backend=be)
+    for _ in range(3):
+        hr, _, _ = P.hmc_update_volatility(hr, theta, data, md, rng, backend=be)
+    n_acc_r = 0
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        hr, acc, _ = P.hmc_update_volatility(hr, theta, data, md, rng, backend=be)
+        n_acc_r += int(acc)
+    e2e_res_s = (time.perf_counter() - t0) / e2e_steps
+    resident = ch_e2e.last_update_resident
     # the same call with a plain (pageable) numpy path, the reference user's usual case
     # (every step proposes from the same pageable path, so each call copies it in)
     hp = np.array(h)
@@ -540,6 +561,11 @@ def main():
            "d2h_bytes_per_step": int(8 * T * n_acc / e2e_steps) + 48 + 56,
            "h_in": "read in place over PCIe by the trajectory kernel (zero copy)" if zero_copy else "copied in",
            "path": "paper_1603_08114_b200.hmc_update_volatility(h numpy[pinned], params, data, md, rng) -> C ABI",
+           "resident_chain": {"value": T * L / e2e_res_s, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
+                              "d2h_bytes_per_step": int(8 * T * n_acc_r / e2e_steps) + 48 + 56,
+                              "resident": resident,
+                              "h_in": "the returned (read-only) path passed back: proposed from the device's "
+                                      "copy, only the stream state crosses the link"},
            "pageable": {"value": T * L / e2e_pg_s, "unit": UNIT, "h2d_bytes_per_step": 8 * T + state_bytes,
                         "d2h_bytes_per_step": int(8 * T * n_acc_p / e2e_steps) + 48 + 56,
                         "h_in": "pageable numpy array: copied in (cudaMemcpy from pageable memory); every "

@@ -108,7 +108,10 @@ int rsv_hmc_update(rsv_ctx *ctx, double step_size, int n_steps, int fuse, rsv_re
  * proposal; rsv_last_update_zero_copy tells which way the last call went.
  * The context's own latent path afterwards: h_out when accepted; after a
  * rejected zero-copy call it holds none (rsv_set_latent before any
- * device-resident call such as rsv_hmc_update). */
+ * device-resident call such as rsv_hmc_update).  h_in == NULL proposes from
+ * the path the context holds (RSV_E_STATE when it holds none): a chain driven
+ * through this call then moves only its stream state in and, when accepted,
+ * the proposal out. */
 int rsv_hmc_update_host(rsv_ctx *ctx, const double *h_in, double *h_out, rsv_prng_state *stream, double step_size,
                         int n_steps, int fuse, rsv_result *out);
 int rsv_last_update_zero_copy(const rsv_ctx *ctx);

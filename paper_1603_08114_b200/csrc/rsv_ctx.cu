@@ -955,11 +955,14 @@ int rsv_hmc_update(rsv_ctx *c, double dt, int n_steps, int fuse, rsv_result *out
 // state go in with asynchronous copies, the proposal runs as one graph, and
 // one synchronisation returns the result (a second one copies the proposal
 // out when it was accepted).  The theta statistics are not evaluated.
+// h_in == NULL: propose from the path the context holds (a chain driven
+// through this call keeps its path resident: only the stream state goes in).
 int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_state *st, double dt, int n_steps,
                         int fuse, rsv_result *out) {
-  if (!c || !h_in || !h_out || !st || !out) return fail(c, RSV_E_INVALID, "null argument");
+  if (!c || !h_out || !st || !out) return fail(c, RSV_E_INVALID, "null argument");
   int r;
   if ((r = check_md(c, dt, n_steps))) return r;
+  if (!h_in && !c->has_latent) return fail(c, RSV_E_STATE, "no resident latent path (h_in is NULL)");
   if (!c->has_data) return fail(c, RSV_E_STATE, "data not set (rsv_set_data)");
   if (!c->has_params) return fail(c, RSV_E_STATE, "params not set (rsv_set_params)");
   if (c->shard || c->ens_C) return fail(c, RSV_E_STATE, "rsv_hmc_update_host needs a single-chain context");
@@ -984,8 +987,14 @@ int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_
   static_assert(offsetof(DevControl, err) + sizeof(int32_t) - offsetof(DevControl, stream) ==
                     sizeof(StreamState) + 2 * sizeof(int32_t),
                 "stream, cur, err are contiguous");
-  CK(cudaMemcpyAsync(&c->ctrl->stream, &c->h_ctrl->stream, sizeof(StreamState) + 2 * sizeof(int32_t),
-                     cudaMemcpyHostToDevice, c->stream));
+  if (h_in) {
+    CK(cudaMemcpyAsync(&c->ctrl->stream, &c->h_ctrl->stream, sizeof(StreamState) + 2 * sizeof(int32_t),
+                       cudaMemcpyHostToDevice, c->stream));
+  } else {  // the resident path stays where it is: cur untouched
+    CK(cudaMemcpyAsync(&c->ctrl->stream, &c->h_ctrl->stream, sizeof(StreamState), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemsetAsync(&c->ctrl->err, 0, sizeof(int32_t), c->stream));
+  }
   CK(cudaMemcpyAsync(&c->ctrl->seq_state, &c->h_ctrl->seq_state, sizeof(uint64_t), cudaMemcpyHostToDevice,
                      c->stream));
   c->has_latent = true;
@@ -995,7 +1004,7 @@ int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_
   // instead of one copy in ahead of the proposal; arrays padded to T % 8 == 0
   // only (the staging reads whole 8-site groups)
   const void *h_map = nullptr;
-  if (g.ok && c->T >= ZC_MIN_T && c->T % 8 == 0 && ((uintptr_t)h_in & 15) == 0 && c->timing == 0 &&
+  if (h_in && g.ok && c->T >= ZC_MIN_T && c->T % 8 == 0 && ((uintptr_t)h_in & 15) == 0 && c->timing == 0 &&
       !getenv("RSV_NO_ZERO_COPY")) {
     cudaPointerAttributes pa;
     if (cudaPointerGetAttributes(&pa, h_in) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
@@ -1019,7 +1028,7 @@ int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_
     if ((r = pull_ctrl(c))) return r;
     c->has_latent = c->h_ctrl->res.accept != 0;  // on a reject the device holds no copy of h_in
   } else {
-    CK(cudaMemcpyAsync(c->hbuf[0], h_in, sizeof(double) * c->T, cudaMemcpyHostToDevice, c->stream));
+    if (h_in) CK(cudaMemcpyAsync(c->hbuf[0], h_in, sizeof(double) * c->T, cudaMemcpyHostToDevice, c->stream));
     rsv_ctx::Cached *cg = nullptr;
     int kpl = 0;
     if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl))) return r;

@@ -48,13 +48,17 @@ class MDConfig:
 
 
 class _Lease:
-    """Owner object of one hand-out of a pooled page-locked buffer."""
+    """Owner object of one hand-out of a pooled page-locked buffer.  A
+    read-only lease exposes no writable buffer, so neither the array over it
+    nor any view of it can be made writable again."""
 
     __slots__ = ("__array_interface__", "buf", "__weakref__")
 
-    def __init__(self, buf: np.ndarray):
+    def __init__(self, buf: np.ndarray, readonly: bool = False):
         self.buf = buf
-        self.__array_interface__ = buf.__array_interface__
+        ai = dict(buf.__array_interface__)
+        ai["data"] = (ai["data"][0], bool(readonly))
+        self.__array_interface__ = ai
 
 
 class DeviceChain:
@@ -69,6 +73,7 @@ class DeviceChain:
         self.ctx = h.value
         self._data_key = None
         self._params_key = None
+        self._resident = None  # weakref to the lease of the returned path the device holds
 
     # -- lifecycle --
     def close(self):
@@ -82,7 +87,12 @@ class DeviceChain:
         except Exception:
             pass
 
-    def _ck(self, code):
+    def _ck(self, code, keeps_path: bool = False):
+        """Check a C-ABI return code.  Every call that may move the device's
+        path (or its cur index) drops the resident-path link of
+        hmc_update_host; calls that leave it alone say keeps_path."""
+        if not keeps_path:
+            self._resident = None
         N.check(code, self.ctx)
 
     # -- state --
@@ -99,14 +109,14 @@ class DeviceChain:
                 raise ValueError(f"dataset length {data.length} does not match chain length {self.T}")
             y = np.ascontiguousarray(data.returns, dtype=np.float64)
             lrv = np.ascontiguousarray(data.log_rv, dtype=np.float64)
-            self._ck(self._lib.rsv_set_data(self.ctx, y.ctypes.data, lrv.ctypes.data, 0))
+            self._ck(self._lib.rsv_set_data(self.ctx, y.ctypes.data, lrv.ctypes.data, 0), keeps_path=True)
             self._data_key = key
             self._data_ref = data  # keep ids alive
 
     def set_params(self, params: Params):
         key = (params.phi, params.mu, params.xi, params.sigma_eta_sq, params.sigma_u_sq)
         if key != self._params_key:
-            self._ck(self._lib.rsv_set_params(self.ctx, ctypes.byref(N.to_params(params))))
+            self._ck(self._lib.rsv_set_params(self.ctx, ctypes.byref(N.to_params(params))), keeps_path=True)
             self._params_key = key
 
     def set_latent(self, h: np.ndarray):
@@ -115,7 +125,7 @@ class DeviceChain:
             raise ValueError(f"latent path length {h.shape[0]} does not match chain length {self.T}")
         self._ck(self._lib.rsv_set_latent(self.ctx, h.ctypes.data, 0))
 
-    def _pinned_out(self) -> np.ndarray:
+    def _pinned_out(self, readonly: bool = False) -> np.ndarray:
         """A page-locked host array for a returned path.  Each hand-out is an
         array over a fresh ``_Lease`` of a pool buffer, tracked by a weak
         reference: the lease is the memory owner numpy records for the
@@ -133,22 +143,25 @@ class DeviceChain:
                 pass
         for ent in pool:
             if ent[1] is None or ent[1]() is None:
-                lease = _Lease(ent[0])
+                lease = _Lease(ent[0], readonly)
                 ent[1] = weakref.ref(lease)
                 return np.asarray(lease)
-        return np.empty(self.T)
+        out = np.empty(self.T)
+        if readonly:
+            out.flags.writeable = False
+        return out
 
     def get_latent(self, out: np.ndarray | None = None) -> np.ndarray:
         out = self._pinned_out() if out is None else out
-        self._ck(self._lib.rsv_get_latent(self.ctx, N.ptr(out), 0))
+        self._ck(self._lib.rsv_get_latent(self.ctx, N.ptr(out), 0), keeps_path=True)
         return out
 
     def set_stream(self, st: N.PrngState):
-        self._ck(self._lib.rsv_set_prng_state(self.ctx, ctypes.byref(st)))
+        self._ck(self._lib.rsv_set_prng_state(self.ctx, ctypes.byref(st)), keeps_path=True)
 
     def get_stream(self) -> N.PrngState:
         st = N.PrngState()
-        self._ck(self._lib.rsv_get_prng_state(self.ctx, ctypes.byref(st)))
+        self._ck(self._lib.rsv_get_prng_state(self.ctx, ctypes.byref(st)), keeps_path=True)
         return st
 
     # -- hot path --
@@ -205,22 +218,45 @@ class DeviceChain:
 
     def get_params(self) -> Params:
         p = N.Params()
-        self._ck(self._lib.rsv_get_params(self.ctx, ctypes.byref(p)))
+        self._ck(self._lib.rsv_get_params(self.ctx, ctypes.byref(p)), keeps_path=True)
         return N.to_params(p)
+
+    def _holds(self, h) -> bool:
+        """h is the read-only path this chain returned last and the device
+        still holds it (no call since has moved the device's path)."""
+        lease = self._resident() if self._resident is not None else None
+        return (lease is not None and isinstance(h, np.ndarray) and h.base is lease and not h.flags.writeable
+                and h.dtype == np.float64 and h.shape == (self.T,) and h.strides == (8,)
+                and h.ctypes.data == lease.__array_interface__["data"][0])
 
     def hmc_update_host(self, h: np.ndarray, st: N.PrngState, step_size: float, n_steps: int,
                         fuse: bool = False):
         """One proposal from a host path (rsv_hmc_update_host): returns
-        (result, path_out) where path_out is a page-locked array holding the
-        proposal when accepted (None otherwise); st is advanced in place."""
-        h = _f64(h)
-        if h.shape != (self.T,):
-            raise ValueError(f"latent path length {h.shape[0]} does not match chain length {self.T}")
-        out = self._pinned_out()
+        (result, path_out) where path_out is a read-only page-locked array
+        holding the proposal when accepted (None otherwise); st is advanced in
+        place.  A path this chain returned (read-only, so unchanged since) and
+        still holds on the device is not sent again: the proposal runs from
+        the device's copy and only the stream state crosses the link."""
+        resident = self._holds(h)
+        if not resident:
+            h = _f64(h)
+            if h.shape != (self.T,):
+                raise ValueError(f"latent path length {h.shape[0]} does not match chain length {self.T}")
+        out = self._pinned_out(readonly=True)
         r = N.Result()
-        self._ck(self._lib.rsv_hmc_update_host(self.ctx, h.ctypes.data, out.ctypes.data, ctypes.byref(st),
-                                               float(step_size), int(n_steps), int(bool(fuse)), ctypes.byref(r)))
+        code = self._lib.rsv_hmc_update_host(self.ctx, None if resident else h.ctypes.data, out.ctypes.data,
+                                             ctypes.byref(st), float(step_size), int(n_steps), int(bool(fuse)),
+                                             ctypes.byref(r))
+        self._ck(code, keeps_path=resident and code == 0)
+        self._last_resident = resident
+        if r.accept and isinstance(out.base, _Lease):
+            self._resident = weakref.ref(out.base)  # the device's path is now the returned one
         return r, (out if r.accept else None)
+
+    @property
+    def last_update_resident(self) -> bool:
+        """The last hmc_update_host proposed from the device's resident path."""
+        return bool(getattr(self, "_last_resident", False))
 
     @property
     def last_update_zero_copy(self) -> bool:

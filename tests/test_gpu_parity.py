@@ -168,9 +168,14 @@ def test_zero_copy_host_proposals_vs_oracle(backend, T, kind, pinned):
     H = abs(O.hamiltonian(h_orc, np.zeros(T), THETA, data.returns, data.log_rv)) + T
     accs = []
     for i in range(4):
-        was_pinned = pinned or any(accs)   # an accepted path comes back page-locked
+        # an accepted path comes back read-only and stays on the device: passed
+        # back, it is proposed from the device's copy; before that the path is
+        # read in place (page-locked) or copied in
+        resident = any(accs)
         h_gpu, acc, dh = P.hmc_update_volatility(h_gpu, THETA, data, md, rng, backend=backend)
-        assert backend.chain(data, THETA).last_update_zero_copy == (was_pinned and T % 8 == 0), i
+        ch = backend.chain(data, THETA)
+        assert ch.last_update_resident == resident, i
+        assert ch.last_update_zero_copy == (not resident and pinned and T % 8 == 0), i
         h_orc, acc_o, dh_o = O.hmc_update(h_orc, THETA, data.returns, data.log_rv, md.step_size, md.n_steps, st,
                                           nthreads=O.max_threads())
         assert acc == acc_o and abs(dh - dh_o) <= 1e-13 * H, (i, dh, dh_o)

@@ -147,3 +147,46 @@ def test_trajectory_tiles_exact_while_other_kernels_hold_the_sms(backend):
         assert bool(r.accept) == acc and abs(r.delta_h - dh) <= 1e-13 * H, i
     torch.cuda.synchronize()
     assert np.max(np.abs(ch.get_latent() - h)) <= 1e-12 * np.max(np.abs(h))
+
+
+@pytest.mark.parametrize("T", [4096, 1 << 16])
+def test_returned_path_stays_resident_and_matches_the_oracle(backend, T):
+    # a chain loop passing the returned path back (sampler.py:327-344 does):
+    # after the first accept the proposal runs from the device's copy (only
+    # the stream state crosses the link); every step equals the oracle's, the
+    # returned path cannot be made writable, and any other call that moves
+    # the device's path (here set_latent) makes the next call read the host
+    # path again
+    truth = P.simulate_rsv(THETA, T, seed=21)
+    data = truth.dataset
+    md = P.MDConfig(0.02, 20)
+    rng = P.make_rng(6, "pcg32")
+    st = O.Stream("pcg32", 6)
+    h_gpu, h_orc = truth.latent.copy(), truth.latent.copy()
+    H = abs(O.hamiltonian(h_orc, np.zeros(T), THETA, data.returns, data.log_rv)) + T
+    ch = backend.chain(data, THETA)
+    seen_resident = link = False  # link: the device holds the path last returned
+    for i in range(16):
+        if i == 10:
+            ch.set_latent(np.zeros(T))  # the device's path moves: the link is dropped
+            link = False
+        h_gpu, acc, dh = P.hmc_update_volatility(h_gpu, THETA, data, md, rng, backend=backend)
+        assert ch.last_update_resident == link, i
+        seen_resident |= link
+        link = bool(acc) or link
+        h_orc, acc_o, dh_o = O.hmc_update(h_orc, THETA, data.returns, data.log_rv, md.step_size, md.n_steps, st,
+                                          nthreads=O.max_threads())
+        assert acc == acc_o and abs(dh - dh_o) <= 1e-13 * H, (i, dh, dh_o)
+        assert np.max(np.abs(h_gpu - h_orc)) <= 1e-10 * max(1.0, np.max(np.abs(h_orc))), i
+        if acc:
+            assert not h_gpu.flags.writeable
+            with pytest.raises(ValueError):
+                h_gpu.flags.writeable = True
+            with pytest.raises(ValueError):
+                h_gpu[:1].flags.writeable = True
+    assert seen_resident
+    assert int(rng.bit_generator.random_raw()) == int(st.raw(1)[0])
+    # a writable copy of a returned path is the caller's own: read from the host
+    hc = np.array(h_gpu)
+    P.hmc_update_volatility(hc, THETA, data, md, rng, backend=backend)
+    assert not ch.last_update_resident
