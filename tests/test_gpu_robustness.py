@@ -150,7 +150,8 @@ def test_trajectory_tiles_exact_while_other_kernels_hold_the_sms(backend):
 
 
 @pytest.mark.parametrize("T", [4096, 1 << 16])
-def test_returned_path_stays_resident_and_matches_the_oracle(backend, T):
+@pytest.mark.parametrize("kind", ["pcg32", "philox", "sfc64", "minstd"])
+def test_returned_path_stays_resident_and_matches_the_oracle(backend, T, kind):
     # a chain loop passing the returned path back (sampler.py:327-344 does):
     # after the first accept the proposal runs from the device's copy (only
     # the stream state crosses the link); every step equals the oracle's, the
@@ -160,8 +161,8 @@ def test_returned_path_stays_resident_and_matches_the_oracle(backend, T):
     truth = P.simulate_rsv(THETA, T, seed=21)
     data = truth.dataset
     md = P.MDConfig(0.02, 20)
-    rng = P.make_rng(6, "pcg32")
-    st = O.Stream("pcg32", 6)
+    rng = P.make_rng(6, kind)
+    st = O.Stream(kind, 6)
     h_gpu, h_orc = truth.latent.copy(), truth.latent.copy()
     H = abs(O.hamiltonian(h_orc, np.zeros(T), THETA, data.returns, data.log_rv)) + T
     ch = backend.chain(data, THETA)
