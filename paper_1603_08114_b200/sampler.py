@@ -144,7 +144,10 @@ def hmc_update_volatility(h: np.ndarray, params: Params, data: Dataset, md: MDCo
     """sampler.py:144-167: one HMC proposal for the whole path, on the GPU.
 
     Returns (path, accept, delta_h); a divergent trajectory or an
-    out-of-bounds dH rejects with the +inf sentinel and draws no uniform."""
+    out-of-bounds dH rejects with the +inf sentinel and draws no uniform.
+    An accepted path comes back read-only: it mirrors the device's copy, and
+    passed back unchanged it is not sent over the link again (np.array(path)
+    for a writable copy)."""
     ch = _resolve(backend).chain(data, params)
     h64 = np.ascontiguousarray(h, dtype=np.float64)
     st = stream_state(rng)
