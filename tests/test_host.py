@@ -196,3 +196,33 @@ def test_dataset_arrays_are_private_and_read_only():
     ro = v[:]
     ro.setflags(write=False)
     assert not is_frozen(ro)         # a read-only view of a writable base can still change
+
+
+def test_read_only_lease_cannot_be_made_writable():
+    # a returned path is an array over a read-only lease of a pooled buffer:
+    # neither it nor any view of it can be made writable, which is what lets
+    # hmc_update_host trust that a path passed back is the one the device holds
+    import gc
+    import weakref
+    from paper_1603_08114_b200.integrator import _Lease
+    buf = np.arange(16, dtype=np.float64)
+    lease = _Lease(buf, readonly=True)
+    a = np.asarray(lease)
+    assert a.base is lease and not a.flags.writeable and a.ctypes.data == buf.ctypes.data
+    for v in (a, a[:4], a.view(), a.reshape(4, 4)):
+        with pytest.raises(ValueError):
+            v.flags.writeable = True
+        with pytest.raises(ValueError):
+            v[0] = 1.0
+    assert a.view().base is a  # a view is not the returned array itself
+    w = np.asarray(_Lease(buf))  # the writable hand-out (get_latent)
+    assert w.flags.writeable
+    # the lease lives as long as any array over it
+    ref = weakref.ref(lease)
+    v = a[2:]
+    del a, lease
+    gc.collect()
+    assert ref() is not None and v[0] == 2.0
+    del v
+    gc.collect()
+    assert ref() is None
