@@ -203,7 +203,8 @@ __device__ __forceinline__ void stage_tile(const TrajArgs &A, const double *hsrc
   RSV_CHECK((((uintptr_t)(hsrc + lo)) & 15) == 0 && (((uintptr_t)(A.p_in + lo)) & 15) == 0);
   mbar_expect_tx(bar, (part == 3 ? 4 : part == 1 ? 3 : 1) * bytes);
   if (part & 1) {
-    tma_load_1d(stage + 0 * W + off, hsrc + lo, bytes, bar);
+    const double *hs = (A.h_head && hi <= A.head_end) ? A.h_head : hsrc;
+    tma_load_1d(stage + 0 * W + off, hs + lo, bytes, bar);
     tma_load_1d(stage + 2 * W + off, A.a + lo, bytes, bar);
     tma_load_1d(stage + 3 * W + off, A.lrv + lo, bytes, bar);
   }

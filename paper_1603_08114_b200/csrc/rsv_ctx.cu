@@ -44,6 +44,13 @@ struct GraphKey {
 // rsv_hmc_update_host reads a page-locked path in place from this length on
 // (below it one copy in is as fast)
 constexpr int64_t ZC_MIN_T = 1 << 16;
+// share (in eighths) of a zero-copy path copied in by the copy engine, beside
+// the momenta kernel, ahead of the trajectory (which reads the rest in place):
+// the copy engine moves bytes faster than the kernel's in-place reads and
+// the link is otherwise idle under the momenta kernel.  Measured at 2^20
+// (tools/e2e_head_ab.py): 257 us per call without, 252 / 248 / 241 / 242 us
+// with 1/16, 1/4, 3/8, 1/2 of the path.
+constexpr int64_t ZC_HEAD_EIGHTHS = 3;
 
 __global__ void prep_data_kernel(const double *y, double *a, int64_t T) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -155,6 +162,9 @@ struct rsv_ctx {
     cudaGraphExec_t exec;
     cudaGraphNode_t traj_node;
     cudaKernelNodeParams traj_params;
+    cudaGraphNode_t head_node = nullptr;  // zero-copy graphs: the path's head, copied in beside the momenta
+    const void *head_src = nullptr;
+    size_t head_bytes = 0;
     TrajArgs args;
     double dt;
     std::vector<cudaGraphNode_t> ev;  // timing event-record nodes
@@ -698,7 +708,7 @@ static bool enqueue_fallback(rsv_ctx *c, double dt, int n_steps, int stats, int 
 // re-pointed per launch with cudaGraphExecEventRecordNodeSetEvent.
 static bool variant_is_persistent(int v) { return v >= 9; }
 
-static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
+static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out, const void *head_src = nullptr) {
   const TrajGeom g = traj_geometry(c->T, k.n_steps, c->sm_count, c->variant);
   if (!g.ok && c->shard) return fail(c, RSV_E_INVALID, "n_steps=%d too large for a sharded trajectory", k.n_steps);
   if (g.ok && g.n_tiles > c->max_tiles) return fail(c, RSV_E_CUDA, "tile count %d exceeds buffer", g.n_tiles);
@@ -716,6 +726,12 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
   if (k.zc && g.ok) {  // h_src is re-pointed at the caller's page-locked path per call
     cg->args.h_src = c->hbuf[0];
     cg->args.h_dst = c->hbuf[1];
+    if (head_src) {
+      const int64_t head = getenv("RSV_ZC_HEAD") ? atoll(getenv("RSV_ZC_HEAD")) : c->T * ZC_HEAD_EIGHTHS / 8;
+      const int64_t he = std::min<int64_t>(head, c->T) / 8 * 8;
+      cg->args.h_head = he > 0 ? c->hbuf[0] : nullptr;
+      cg->args.head_end = he > 0 ? he : 0;
+    }
   }
   // programmatic dependent launch of the trajectory after the momenta kernel
   // (not with timing event nodes between them)
@@ -763,6 +779,16 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
     }
   }
   if (g.ok && !cg->traj_node) return fail(c, RSV_E_CUDA, "trajectory node not found in the captured graph");
+  if (k.zc && g.ok && head_src && cg->args.head_end > 0) {
+    // the copy engine brings the path's first sites in while the momenta
+    // kernel runs (the link is otherwise idle then); the trajectory kernel
+    // (a full dependent of the copy) stages windows inside it from device memory
+    cg->head_bytes = sizeof(double) * (size_t)cg->args.head_end;
+    cg->head_src = head_src;
+    CK(cudaGraphAddMemcpyNode1D(&cg->head_node, graph, nullptr, 0, c->hbuf[0], head_src, cg->head_bytes,
+                                cudaMemcpyHostToDevice));
+    CK(cudaGraphAddDependencies(graph, &cg->head_node, &cg->traj_node, 1));
+  }
   if (k.timing)
     for (int i = 0; i < 4; i++)
       if (!cg->ev[i]) return fail(c, RSV_E_CUDA, "timing graph: event node %d not found", i);
@@ -772,14 +798,14 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out) {
 }
 
 static int get_graph(rsv_ctx *c, double dt, int n_steps, int fuse, int stats, rsv_ctx::Cached **out,
-                     int *kernels, int zc = 0) {
+                     int *kernels, int zc = 0, const void *head_src = nullptr) {
   GraphKey k{c->kind, n_steps, fuse ? 1 : 0, c->timing == 2 ? 1 : 0, stats ? 1 : 0, dt, zc};
   k.nomom = c->shard && c->win_mode && !c->blocks ? 1 : 0;
   k.devk = c->shard && c->run_active && stats ? 1 : 0;
   auto it = c->graphs.find(k);
   if (it == c->graphs.end()) {
     rsv_ctx::Cached *cg = nullptr;
-    int r = build_graph(c, k, &cg);
+    int r = build_graph(c, k, &cg, head_src);
     if (r) return r;
     it = c->graphs.emplace(k, cg).first;
   }
@@ -1015,7 +1041,12 @@ int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_
   if (h_map) {
     rsv_ctx::Cached *cg = nullptr;
     int kpl = 0;
-    if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl, 2))) return r;
+    if ((r = get_graph(c, dt, n_steps, fuse, 0, &cg, &kpl, 2, h_in))) return r;
+    if (cg->head_node && cg->head_src != (const void *)h_in) {
+      CK(cudaGraphExecMemcpyNodeSetParams1D(cg->exec, cg->head_node, c->hbuf[0], h_in, cg->head_bytes,
+                                            cudaMemcpyHostToDevice));
+      cg->head_src = h_in;
+    }
     if (cg->args.h_src != (const double *)h_map) {  // re-point the kernel node (the cached args follow)
       cg->args.h_src = (const double *)h_map;
       void *kp[] = {&cg->args};

@@ -109,6 +109,11 @@ struct TrajArgs {
   TrajGeom g;
   const double *h_src;  // if null: h buffers selected by ctrl->cur
   double *h_dst;
+  // zero-copy input: sites [0, head_end) of h_src were copied to h_head by a
+  // copy-engine node that ran beside the momenta kernel; windows inside it
+  // are staged from there instead of over the link
+  const double *h_head;
+  int64_t head_end;
   double *hbuf0, *hbuf1;
   const double *p_in;
   double *p_out;        // optional

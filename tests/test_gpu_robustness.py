@@ -191,3 +191,39 @@ def test_returned_path_stays_resident_and_matches_the_oracle(backend, T, kind):
     hc = np.array(h_gpu)
     P.hmc_update_volatility(hc, THETA, data, md, rng, backend=backend)
     assert not ch.last_update_resident
+
+
+@pytest.mark.parametrize("head", [None, "8", "40000", str(1 << 17)])
+def test_zero_copy_with_copied_head_matches_the_oracle(monkeypatch, head):
+    # a page-locked path sent every step (a view of the returned array is not
+    # the chain's own): the copy engine brings the path's head in beside the
+    # momenta kernel and the trajectory kernel reads the rest in place; any
+    # head size (none, one group, mid-tile, the whole path) gives the oracle's
+    # decisions and paths
+    import torch
+    if head is None:
+        monkeypatch.delenv("RSV_ZC_HEAD", raising=False)
+    else:
+        monkeypatch.setenv("RSV_ZC_HEAD", head)
+    T = 1 << 17
+    truth = P.simulate_rsv(THETA, T, seed=8)
+    data = truth.dataset
+    md = P.MDConfig(0.02, 20)
+    rng = P.make_rng(9, "pcg32")
+    st = O.Stream("pcg32", 9)
+    h_gpu = torch.empty(T, dtype=torch.float64, pin_memory=True).numpy()
+    h_gpu[:] = truth.latent
+    h_orc = truth.latent.copy()
+    H = abs(O.hamiltonian(h_orc, np.zeros(T), THETA, data.returns, data.log_rv)) + T
+    with P.CudaBackend(0) as be:
+        n_acc = 0
+        for i in range(6):
+            h_gpu, acc, dh = P.hmc_update_volatility(h_gpu.view(), THETA, data, md, rng, backend=be)
+            ch = be.chain(data, THETA)
+            assert ch.last_update_zero_copy and not ch.last_update_resident, i
+            h_orc, acc_o, dh_o = O.hmc_update(h_orc, THETA, data.returns, data.log_rv, md.step_size, md.n_steps,
+                                              st, nthreads=O.max_threads())
+            assert acc == acc_o and abs(dh - dh_o) <= 1e-13 * H, (i, dh, dh_o)
+            assert np.max(np.abs(h_gpu - h_orc)) <= 1e-10 * max(1.0, np.max(np.abs(h_orc))), i
+            n_acc += acc
+    assert int(rng.bit_generator.random_raw()) == int(st.raw(1)[0])
