@@ -51,6 +51,8 @@ constexpr int64_t ZC_MIN_T = 1 << 16;
 // (tools/e2e_head_ab.py): 257 us per call without, 252 / 248 / 241 / 242 us
 // with 1/16, 1/4, 3/8, 1/2 of the path.
 constexpr int64_t ZC_HEAD_EIGHTHS = 3;
+// host threads copying a pageable path into the page-locked staging buffer
+constexpr int HOST_STAGE_THREADS = 8;
 
 __global__ void prep_data_kernel(const double *y, double *a, int64_t T) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -138,6 +140,7 @@ struct rsv_ctx {
   double *rout = nullptr;   // reduction outputs (8 doubles)
   double *fb = nullptr;     // long-trajectory fallback: energies and statistics (24 doubles)
   int zc_last = 0;  // the last rsv_hmc_update_host read h_in in place
+  double *h_stage = nullptr;  // page-locked staging of a pageable path (rsv_hmc_update_host)
   int32_t *dflag = nullptr;
   int32_t *ring_count = nullptr;
   DevResult *ring = nullptr;
@@ -264,6 +267,7 @@ int rsv_destroy(rsv_ctx *c) {
   if (c->flush_buf) cudaFree(c->flush_buf);
   if (c->dbg) cudaFree(c->dbg);
   for (auto e : c->evpool) cudaEventDestroy(e);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   void *dev[] = {c->hbuf[0], c->hbuf[1], c->y, c->a, c->lrv, c->normals, c->sh, c->sp, c->sh2, c->sp2,
                  c->zscratch, c->sfc_words, c->sfc_snaps, c->parts, c->rpart, c->rout, c->dflag, c->ring_count,
                  c->ring, c->ctrl, c->prm, c->pl[0], c->pl[1], c->pl[2], c->pl[3], c->bjump, c->fb};
@@ -1036,6 +1040,30 @@ int rsv_hmc_update_host(rsv_ctx *c, const double *h_in, double *h_out, rsv_prng_
     if (cudaPointerGetAttributes(&pa, h_in) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
       h_map = pa.devicePointer;
     cudaGetLastError();
+  }
+  // a pageable path (T large enough for the in-place route): copied into a
+  // page-locked staging buffer by host threads, then read like a page-locked
+  // one -- the driver's own pageable copy is a single staged stream
+  if (!h_map && h_in && g.ok && c->T >= ZC_MIN_T && c->T % 8 == 0 && c->timing == 0 && !getenv("RSV_NO_ZERO_COPY") &&
+      !getenv("RSV_NO_HOST_STAGE")) {
+    cudaPointerAttributes pa;
+    const bool pageable = cudaPointerGetAttributes(&pa, h_in) == cudaSuccess && pa.type == cudaMemoryTypeUnregistered;
+    cudaGetLastError();
+    if (pageable) {
+      if (!c->h_stage) {
+        CK(cudaHostAlloc((void **)&c->h_stage, sizeof(double) * (size_t)c->T, cudaHostAllocMapped));
+      }
+      const int64_t T = c->T, nchunk = 64;
+#pragma omp parallel for num_threads(HOST_STAGE_THREADS) schedule(static)
+      for (int64_t k = 0; k < nchunk; k++) {
+        const int64_t lo = T * k / nchunk / 8 * 8, hi = k + 1 == nchunk ? T : T * (k + 1) / nchunk / 8 * 8;
+        memcpy(c->h_stage + lo, h_in + lo, sizeof(double) * (size_t)(hi - lo));
+      }
+      h_in = c->h_stage;
+      void *dp = nullptr;
+      CK(cudaHostGetDevicePointer(&dp, (void *)c->h_stage, 0));
+      h_map = dp;
+    }
   }
   c->zc_last = h_map ? 1 : 0;
   if (h_map) {

@@ -175,7 +175,8 @@ def test_zero_copy_host_proposals_vs_oracle(backend, T, kind, pinned):
         h_gpu, acc, dh = P.hmc_update_volatility(h_gpu, THETA, data, md, rng, backend=backend)
         ch = backend.chain(data, THETA)
         assert ch.last_update_resident == resident, i
-        assert ch.last_update_zero_copy == (not resident and pinned and T % 8 == 0), i
+        # (a pageable path is staged into page-locked memory by host threads first)
+        assert ch.last_update_zero_copy == (not resident and T % 8 == 0), i
         h_orc, acc_o, dh_o = O.hmc_update(h_orc, THETA, data.returns, data.log_rv, md.step_size, md.n_steps, st,
                                           nthreads=O.max_threads())
         assert acc == acc_o and abs(dh - dh_o) <= 1e-13 * H, (i, dh, dh_o)

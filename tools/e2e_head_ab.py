@@ -23,13 +23,19 @@ h = torch.empty(T, dtype=torch.float64, pin_memory=True).numpy()
 h[:] = truth.latent
 for _ in range(10):
     h, _, _ = P.hmc_update_volatility(h.view(), theta, data, md, rng, backend=be)
+pageable = os.environ.get("E2E_PAGEABLE") == "1"  # the same plain numpy path every step
+hp = truth.latent.copy()
 blocks, acc = [], 0
 for _ in range(5):
     t0 = time.perf_counter()
     for _ in range(40):
-        h, a, _ = P.hmc_update_volatility(h.view(), theta, data, md, rng, backend=be)
+        if pageable:
+            _, a, _ = P.hmc_update_volatility(hp, theta, data, md, rng, backend=be)
+        else:
+            h, a, _ = P.hmc_update_volatility(h.view(), theta, data, md, rng, backend=be)
         acc += a
     blocks.append((time.perf_counter() - t0) / 40 * 1e6)
 ch = be.chain(data, theta)
-print(f"RSV_ZC_HEAD={os.environ.get('RSV_ZC_HEAD', 'default')}: {statistics.median(blocks):.1f} us/call "
+print(f"pageable={pageable} RSV_NO_HOST_STAGE={os.environ.get('RSV_NO_HOST_STAGE', '-')} "
+      f"RSV_ZC_HEAD={os.environ.get('RSV_ZC_HEAD', 'default')}: {statistics.median(blocks):.1f} us/call "
       f"(blocks {', '.join(f'{b:.1f}' for b in blocks)}), accepts {acc}/200, zero_copy={ch.last_update_zero_copy}")
