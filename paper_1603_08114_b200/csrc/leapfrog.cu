@@ -191,7 +191,7 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
 // (clamped to [0, Tpad); arrays are padded to a multiple of 8 doubles).
 // part: 1 = h, (y/2)y, lnRV, 2 = the momenta, 3 = all, each on `bar` with
 // its own byte count (the first tile stages parts 1 and 2 on two barriers).
-template <int W>
+template <int W, bool HEADK = false>
 __device__ __forceinline__ void stage_tile(const TrajArgs &A, const double *hsrc, int tile, double *stage,
                                            uint64_t *bar, int part = 3) {
   const int64_t g = (int64_t)tile * A.g.core - A.g.halo;
@@ -203,7 +203,9 @@ __device__ __forceinline__ void stage_tile(const TrajArgs &A, const double *hsrc
   RSV_CHECK((((uintptr_t)(hsrc + lo)) & 15) == 0 && (((uintptr_t)(A.p_in + lo)) & 15) == 0);
   mbar_expect_tx(bar, (part == 3 ? 4 : part == 1 ? 3 : 1) * bytes);
   if (part & 1) {
-    const double *hs = (A.h_head && hi <= A.head_end) ? A.h_head : hsrc;
+    // (a separate instantiation: the branch alone costs the device-resident
+    // kernel ~1 us at 2^20 through the step loop's schedule, measured)
+    const double *hs = (HEADK && hi <= A.head_end) ? A.h_head : hsrc;
     tma_load_1d(stage + 0 * W + off, hs + lo, bytes, bar);
     tma_load_1d(stage + 2 * W + off, A.a + lo, bytes, bar);
     tma_load_1d(stage + 3 * W + off, A.lrv + lo, bytes, bar);
@@ -254,7 +256,7 @@ struct PersistSmem {
   int next[2];     // the CTA's next tile (by staging buffer: read after the tile, rewritten two tiles later)
 };
 
-template <int R, int NT, int MINB, bool STATS, bool ENS = false, bool DEVK = false>
+template <int R, int NT, int MINB, bool STATS, bool ENS = false, bool DEVK = false, bool HEADK = false>
 __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
   using SM = PersistSmem<R, NT, STATS>;
   constexpr int NW = SM::NW, W = SM::W;
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     mbar_expect_tx(&S.bar[2], (uint32_t)sizeof(S.tab));
     tma_load_1d(S.tab, g_exp_tab2, (uint32_t)sizeof(S.tab), &S.bar[2]);
     // the first tile's h, (y/2)y and lnRV do not depend on the momenta kernel
-    if (!ENS && tile < n_tiles) stage_tile<W>(A, hsrc, tile, S.stage[0], &S.bar[0], 1);
+    if (!ENS && tile < n_tiles) stage_tile<W, HEADK>(A, hsrc, tile, S.stage[0], &S.bar[0], 1);
   }
   // programmatic dependent launch: everything above overlapped the momenta
   // kernel's tail; its normals (and stream bookkeeping) are read only after
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
     if (tid == 0 && !first && next < n_tiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (ENS) stage_tile_ens<W>(A, next, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
-      else stage_tile<W>(A, hsrc, next, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
+      else stage_tile<W, HEADK>(A, hsrc, next, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
     }
     const double *stg = S.stage[buf];
     const int64_t t0 = (int64_t)tile * core_len;
@@ -465,10 +467,10 @@ __global__ void __launch_bounds__(NT, MINB) traj_persistent_kernel(TrajArgs A) {
       // overlapped its tail), stage this tile's momenta and the next tile
       asm volatile("griddepcontrol.wait;" ::: "memory");
       if (tid == 0) {
-        stage_tile<W>(A, hsrc, tile, S.stage[buf], &S.bar[3], 2);
+        stage_tile<W, HEADK>(A, hsrc, tile, S.stage[buf], &S.bar[3], 2);
         if (next < n_tiles) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          stage_tile<W>(A, hsrc, next, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
+          stage_tile<W, HEADK>(A, hsrc, next, S.stage[buf ^ 1], &S.bar[buf ^ 1]);
         }
       }
       mbar_wait(&S.bar[3], 0);
@@ -726,14 +728,14 @@ TrajGeom traj_geometry(int64_t T, int n_steps, int sm_count, int variant) {
   return have ? best : traj_geometry_v(T, n_steps, sm_count, 11);
 }
 
-template <int R, int NT, int MINB, bool STATS, bool ENS = false, bool DEVK = false>
+template <int R, int NT, int MINB, bool STATS, bool ENS = false, bool DEVK = false, bool HEADK = false>
 static void launch_p2(const TrajArgs &a, cudaStream_t s) {
   const size_t smem = sizeof(PersistSmem<R, NT, STATS>);
-  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK>,
+  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK, HEADK>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // same (maximal) shared-memory carveout as the momenta kernel: no L1/shared
   // reconfiguration of the SMs between the two kernels of a proposal
-  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK>,
+  cudaFuncSetAttribute(traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK, HEADK>,
                        cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (a.pdl) {  // overlap this launch with the tail of the momenta kernel
     cudaLaunchConfig_t cfg = {};
@@ -746,9 +748,9 @@ static void launch_p2(const TrajArgs &a, cudaStream_t s) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK>, a);
+    cudaLaunchKernelEx(&cfg, traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK, HEADK>, a);
   } else {
-    traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK><<<a.g.grid, NT, smem, s>>>(a);
+    traj_persistent_kernel<R, NT, MINB, STATS, ENS, DEVK, HEADK><<<a.g.grid, NT, smem, s>>>(a);
   }
 }
 
@@ -783,6 +785,8 @@ static void launch_p(const TrajArgs &a, cudaStream_t s) {
   if (a.stats) launch_p2<R, NT, MINB, true>(a, s);
   else launch_p2<R, NT, MINB, false>(a, s);
 }
+
+const void *traj_kernel_fn_head() { return (const void *)traj_persistent_kernel<4, 256, 2, false, false, false, true>; }
 
 const void *traj_kernel_fn(int variant, int, int stats) {
 #define RSV_FN(R, NT, MB)                                                     \
@@ -826,6 +830,11 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches) {
     launch_p2<4, 256, 2, false, true>(a, s);
     ens_decide_kernel<<<(a.n_chains + 127) / 128, 128, 0, s>>>(a);
     (*launches) += 2;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
+  if (a.h_head && a.g.variant == 11 && !a.stats) {  // zero-copy input with a copied head
+    launch_p2<4, 256, 2, false, false, false, true>(a, s);
+    (*launches)++;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
   switch (a.g.variant) {

@@ -733,8 +733,9 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out, con
     if (head_src) {
       const int64_t head = getenv("RSV_ZC_HEAD") ? atoll(getenv("RSV_ZC_HEAD")) : c->T * ZC_HEAD_EIGHTHS / 8;
       const int64_t he = std::min<int64_t>(head, c->T) / 8 * 8;
-      cg->args.h_head = he > 0 ? c->hbuf[0] : nullptr;
-      cg->args.head_end = he > 0 ? he : 0;
+      const bool use = he > 0 && g.variant == 11 && !k.stats;  // the instantiation that has the head
+      cg->args.h_head = use ? c->hbuf[0] : nullptr;
+      cg->args.head_end = use ? he : 0;
     }
   }
   // programmatic dependent launch of the trajectory after the momenta kernel
@@ -761,7 +762,10 @@ static int build_graph(rsv_ctx *c, const GraphKey &k, rsv_ctx::Cached **out, con
   CK(cudaGraphGetNodes(graph, nullptr, &n));
   std::vector<cudaGraphNode_t> nodes(n);
   CK(cudaGraphGetNodes(graph, nodes.data(), &n));
-  const void *fn = !g.ok ? nullptr : k.devk ? traj_kernel_fn_devk(g.variant, k.fuse) : traj_kernel_fn(g.variant, k.fuse, k.stats);
+  const void *fn = !g.ok                ? nullptr
+                   : k.devk             ? traj_kernel_fn_devk(g.variant, k.fuse)
+                   : cg->args.h_head    ? traj_kernel_fn_head()
+                                        : traj_kernel_fn(g.variant, k.fuse, k.stats);
   cg->traj_node = nullptr;
   cg->launches = l;
   cg->ev.assign(4, nullptr);

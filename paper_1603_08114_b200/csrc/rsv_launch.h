@@ -149,6 +149,7 @@ int launch_trajectory(const TrajArgs &a, cudaStream_t s, int *launches);
 int launch_momenta_ens(EnsChain *ens, double *normals, int64_t Tc, int n_chains, cudaStream_t s, int *launches,
                        unsigned long long *dbg = nullptr, int advance = 0, const int32_t *halt = nullptr);
 const void *traj_kernel_fn(int variant, int fuse, int stats);  // for locating the node in a captured graph
+const void *traj_kernel_fn_head();  // the zero-copy instantiation that stages a copied head
 
 
 // one streamed leapfrog step over all sites (integrator.py:139-146)
